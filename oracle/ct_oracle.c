@@ -1,0 +1,137 @@
+/*
+ * ct_oracle.c -- plain, slow, obviously-correct CPU oracle for Compact-Table
+ * propagation (arXiv 2507.18413).  TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs may load this file's library.  The product path
+ * (paper_2507_18413_b200/, include/) never includes, links or calls it, and it
+ * shares no code, header, table or helper with the CUDA path.
+ *
+ * What it computes (section 2):
+ *   - L52-55  : c is GAC iff every value a of every x_i has a tuple of rel(c)
+ *               with a in position i ("a is supported"); unsupported values are
+ *               removed; if no solution exists, unsatisfiability is reported.
+ *   - L189-193: tuple tau_j is *valid* iff tau_j[i] in dom(x_i) for every i;
+ *               currTable bit j = 1 iff tau_j is valid.
+ *   - L144-146: Alg. 1 fails iff currTable = 0 (no valid tuple).
+ *   - L226-238: Alg. 3 keeps a in dom(x_i) iff currTable & supports[x_i,a] != 0,
+ *               i.e. iff some valid tuple has value a in position i.
+ * So, given the domains D_in (the domains after the caller's removals), the
+ * result is:  V = { j : all i, tau_j[i] in D_in(x_i) };  FAIL iff V is empty;
+ * else D_out(x_i) = { tau_j[i] : j in V }.  This is the definition written out
+ * as one tuple scan (no supports matrix, no bitsets, no residues, no index).
+ *
+ * Readings:
+ *   - a tuple value outside [lo_i, lo_i + d_i) is never in any domain, so such
+ *     a tuple is never valid;
+ *   - D_out is not written on FAIL.
+ *
+ * Encoding (the oracle's own): domains are one byte per (variable, value);
+ * variable i's d_i bytes start at rowbase_i = d_0 + ... + d_{i-1}; byte
+ * rowbase_i + (v - lo_i) is 1 iff v is in the domain.  tuples is int32
+ * [t][n] row-major.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Returns 1 (OK, GAC domains written to dom_out), 0 (FAIL), -1 (bad args).
+ * valid_out (may be NULL): t bytes, valid_out[j] = 1 iff tau_j is valid. */
+int oracle_gac(int32_t n, const int32_t *lo, const int32_t *d, int64_t t,
+               const int32_t *tuples, const uint8_t *dom_in, uint8_t *dom_out,
+               uint8_t *valid_out)
+{
+    if (n < 1) return -1;
+    int64_t *rowbase = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    if (!rowbase) return -1;
+    int64_t R = 0;
+    for (int32_t i = 0; i < n; ++i) { rowbase[i] = R; R += d[i]; }
+
+    uint8_t *acc = (uint8_t *)calloc((size_t)(R > 0 ? R : 1), 1);
+    if (!acc) { free(rowbase); return -1; }
+    int any_valid = 0;
+
+    for (int64_t j = 0; j < t; ++j) {
+        const int32_t *tau = tuples + j * (int64_t)n;
+        int valid = 1;
+        for (int32_t i = 0; i < n; ++i) {
+            int64_t v = (int64_t)tau[i] - lo[i];
+            if (v < 0 || v >= d[i] || !dom_in[rowbase[i] + v]) { valid = 0; break; }
+        }
+        if (valid_out) valid_out[j] = (uint8_t)valid;
+        if (valid) {
+            any_valid = 1;
+            for (int32_t i = 0; i < n; ++i)
+                acc[rowbase[i] + ((int64_t)tau[i] - lo[i])] = 1;
+        }
+    }
+    if (any_valid) memcpy(dom_out, acc, (size_t)R);
+    free(acc);
+    free(rowbase);
+    return any_valid;
+}
+
+/* One row of the static supports matrix, by its definition:
+ * out[j] = 1 iff tau_j[i] = value.  (Used to pin the CUDA supports builder.) */
+void oracle_supports_row(int32_t n, int64_t t, const int32_t *tuples,
+                         int32_t i, int32_t value, uint8_t *out)
+{
+    for (int64_t j = 0; j < t; ++j)
+        out[j] = (uint8_t)(tuples[j * (int64_t)n + i] == value);
+}
+
+/*
+ * Fixpoint of several table constraints sharing variables (SURVEY §8(f) f1,
+ * the engine alternates propagation until nothing changes).
+ * Tables are revisited in a fixed round-robin order until a full round changes
+ * no domain (the greatest fixpoint is unique) or one fails.
+ *
+ * Model: nv variables with global domains dom[] (byte per value, variable v at
+ * vbase_v = dv_0+...+dv_{v-1}, values lo_v..lo_v+dv_v-1).  Table k has arity
+ * ar[k], scope scope[k][0..ar-1] (global var ids), t[k] tuples at tuples[k].
+ * Returns 1 OK (dom updated in place), 0 FAIL, -1 bad args.
+ */
+int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t ntab,
+                    const int32_t *ar, const int32_t *const *scope, const int64_t *t,
+                    const int32_t *const *tuples, uint8_t *dom)
+{
+    int64_t *vbase = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nv + 1));
+    if (!vbase) return -1;
+    vbase[0] = 0;
+    for (int32_t v = 0; v < nv; ++v) vbase[v + 1] = vbase[v] + vd[v];
+    int result = 1;
+    int changed = 1;
+    while (changed && result == 1) {
+        changed = 0;
+        for (int32_t k = 0; k < ntab && result == 1; ++k) {
+            int32_t n = ar[k];
+            int32_t *lo = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+            int32_t *d = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+            int64_t R = 0;
+            for (int32_t i = 0; i < n; ++i) { lo[i] = vlo[scope[k][i]]; d[i] = vd[scope[k][i]]; R += d[i]; }
+            uint8_t *din = (uint8_t *)malloc((size_t)R);
+            uint8_t *dout = (uint8_t *)malloc((size_t)R);
+            int64_t off = 0;
+            for (int32_t i = 0; i < n; ++i) {
+                memcpy(din + off, dom + vbase[scope[k][i]], (size_t)d[i]);
+                off += d[i];
+            }
+            int r = oracle_gac(n, lo, d, t[k], tuples[k], din, dout, NULL);
+            if (r != 1) {
+                result = r;
+            } else {
+                off = 0;
+                for (int32_t i = 0; i < n; ++i) {
+                    uint8_t *g = dom + vbase[scope[k][i]];
+                    for (int32_t a = 0; a < d[i]; ++a) {
+                        if (g[a] != dout[off + a]) { g[a] = dout[off + a]; changed = 1; }
+                    }
+                    off += d[i];
+                }
+            }
+            free(lo); free(d); free(din); free(dout);
+        }
+    }
+    free(vbase);
+    return result;
+}
