@@ -1,0 +1,249 @@
+/*
+ * ct.h -- C ABI of the B200-native Compact-Table (CT) propagation library
+ * (paper_2507_18413_b200/libct_b200.so).
+ *
+ * What it computes: GAC propagation of ONE positive table constraint
+ * (PAPER.md L46-55 problem statement; Algorithms 1-3, L131-244):
+ *   given the current domains D of x_1..x_n and the values the caller removes,
+ *   V = { tuples tau_j : tau_j[i] in D'(x_i) for all i }  (currTable, L189-193)
+ *   where D' = D minus the removed values;  FAIL iff V is empty (Alg. 1 L5);
+ *   else every value with no valid tuple is pruned (Alg. 3): the new domain of
+ *   x_i is { tau_j[i] : j in V }.
+ * It gets there the CT way, on the device: static per-(x,a) support bitsets
+ * (L188), an RSparseBitSet-style currTable with a compacted index of non-zero
+ * words, updateTable with the Delta- or dom-branch (Alg. 2), and filterDomains
+ * with residues (L220).  Everything is integer/bitwise; results are exact.
+ *
+ * Conventions used by every entry point:
+ *   - Domains of a table with n variables are "domain bitmaps": uint64 words,
+ *     variable i owns ceil(d_i/64) consecutive words starting at word
+ *     ct_dom_word_offset(t, i); value v of x_i is bit (v - lo_i) % 64 of word
+ *     offset_i + (v - lo_i) / 64 (LSB-first).  Total words: ct_dom_words(t)
+ *     ("Wd").  Bits >= d_i in a variable's last word are ignored on input and
+ *     written as 0 on output.
+ *   - The initial domain of x_i is the interval [lo_i, lo_i + d_i) minus the
+ *     holes given by `init_dom` (_variablesOffsets = lo_i).
+ *   - currTable is a bitset over tuples: tuple j -> word j/64, bit j%64.
+ *   - Status: CT_OK (=0) GAC fixpoint reached; CT_FAIL (=1) no valid tuple
+ *     (a normal result that drives backtracking);
+ *     negative values are errors; ct_last_error() describes the last one
+ *     raised on the calling thread.
+ *   - Ownership: the caller owns every buffer it passes; the library copies
+ *     what it keeps.  The library owns handles and the device memory behind
+ *     them until the matching *_destroy.  Host pointers are plain pageable
+ *     memory unless stated; "device pointer" means memory on cfg.device.
+ *   - Streams: all device work of a table and its states is ordered on one
+ *     CUDA stream (cfg.stream, or a library stream if NULL).  *_async calls
+ *     only enqueue work; synchronous calls return after it completed.
+ *   - Thread safety: distinct states/batches may be driven from distinct host
+ *     threads only if they use distinct streams (ct_state_set_stream); one
+ *     state must not be used concurrently.
+ *   - A state that returned CT_FAIL is dead: later propagations return
+ *     CT_ESTATE without touching the outputs until ct_state_copy() restores it
+ *     (SURVEY Q19).
+ */
+#ifndef CT_B200_H
+#define CT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum ct_status {
+  CT_OK = 0,        /* GAC fixpoint reached; outputs written                        */
+  CT_FAIL = 1,      /* no valid tuple (currTable = 0); outputs not written          */
+  CT_EINVAL = -1,   /* invalid argument (message in ct_last_error)                   */
+  CT_ENOMEM = -2,   /* device or pinned-host allocation failed                      */
+  CT_ECUDA = -3,    /* a CUDA runtime call failed                                   */
+  CT_ENCCL = -4,    /* an NCCL call failed                                          */
+  CT_ESTATE = -5    /* state is dead (after CT_FAIL) or belongs to another table    */
+} ct_status;
+
+typedef struct ct_table ct_table;   /* immutable: geometry + device supports (this shard) */
+typedef struct ct_state ct_state;   /* mutable: domains, currTable, index, residues      */
+typedef struct ct_batch ct_batch;   /* S independent states of one table, one device pool */
+
+/* Device-memory provider.  alloc returns a device pointer (NULL on failure);
+ * `stream` is the cudaStream_t the memory will be used on.  The Python binding
+ * passes PyTorch's caching allocator here. */
+typedef struct ct_allocator {
+  void *(*alloc)(size_t bytes, void *stream, void *ctx);
+  void (*free)(void *ptr, size_t bytes, void *stream, void *ctx);
+  void *ctx;
+} ct_allocator;
+
+/* update_policy: which branch of Alg. 2 each changed
+ * variable uses.  Results are identical for all three. */
+enum { CT_POLICY_AUTO = 0,   /* Delta-branch iff |Delta_x| < |dom(x)| (L163), else dom   */
+       CT_POLICY_DOM = 1,    /* dom-branch only: the paper's implementations (L269-271)  */
+       CT_POLICY_DELTA = 2 };/* Delta-branch only                                        */
+
+typedef struct ct_config {
+  int32_t device;             /* CUDA device ordinal                                     */
+  void *stream;               /* cudaStream_t; NULL -> a library-owned stream           */
+  const ct_allocator *alloc;  /* NULL -> cudaMalloc/cudaFree                             */
+  int32_t n_shards;           /* tuple-range sharding: 1 = off                           */
+  int32_t shard_rank;         /* this process's shard in [0, n_shards)                  */
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId shared by all shards, or NULL:   */
+                              /*  NULL with n_shards > 1 -> caller combines the flags    */
+                              /*  (ct_propagate_local_async / ct_propagate_apply_async)  */
+  int32_t update_policy;      /* CT_POLICY_*                                             */
+  int32_t use_residues;       /* 1: probe residue word first in filter (L220)            */
+  int32_t use_index;          /* 1: keep the compacted non-zero-word index (RSparseBitSet)*/
+  int32_t use_graph;          /* 1: synchronous calls replay a captured CUDA graph      */
+} ct_config;
+
+/* Fill *cfg with defaults: device 0, NULL stream, default allocator, 1 shard,
+ * CT_POLICY_AUTO, residues, index and graphs on. */
+void ct_config_init(ct_config *cfg);
+
+/* ---------------------------------------------------------------- creation */
+/* Build the table (supports bitsets) and its root state, and run
+ * the root propagation ("checks if each variable ... is supported by at least
+ * one tuple, otherwise unsatisfiability is reported", L305-306).
+ *   n_vars      >= 1
+ *   scope       n_vars distinct variable ids (only checked for duplicates and
+ *               kept for the caller; PAPER.md L48 var(c) is a set); may be NULL
+ *   dom_lo      int32[n_vars]  lo_i
+ *   dom_size    int32[n_vars]  d_i >= 1
+ *   init_dom    uint64[Wd] domain bitmap of the initial domains, or NULL = the
+ *               full intervals
+ *   n_tuples    t >= 0 (t = 0 gives a root CT_FAIL)
+ *   tuples      int32[t][n_vars] row-major host array; values outside
+ *               [lo_i, lo_i + d_i) are legal and make the tuple never valid.
+ *               With n_shards > 1 every rank passes the FULL array and keeps
+ *               its own range of 64-tuple words.
+ *   cfg         may be NULL (defaults)
+ *   out_table, out_root   receive the handles (also on CT_FAIL)
+ *   out_dom     host uint64[Wd]: root domains on CT_OK; may be NULL
+ * Returns CT_OK, CT_FAIL (root wipe-out; the root state is dead) or an error
+ * (no handles are returned on error). */
+ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
+                    const int32_t *dom_size, const uint64_t *init_dom, int64_t n_tuples,
+                    const int32_t *tuples, const ct_config *cfg, ct_table **out_table,
+                    ct_state **out_root, uint64_t *out_dom);
+
+typedef struct ct_table_info {
+  int32_t n_vars, n_rows;       /* n, R = sum d_i (support rows)          */
+  int32_t dom_words;            /* Wd                                                    */
+  int32_t n_shards, shard_rank;
+  int64_t n_tuples;             /* t (whole table)                                       */
+  int64_t words_total;          /* ceil(t / 64)                                          */
+  int64_t word_begin, words;    /* this shard's currTable words [begin, begin + words)   */
+  int64_t row_stride_words;     /* padded words per support row on the device            */
+  int64_t device_bytes;         /* supports + table metadata on the device               */
+  int64_t state_bytes;          /* device bytes of one state                             */
+} ct_table_info;
+
+ct_status ct_table_info_get(const ct_table *t, ct_table_info *out);
+int32_t ct_dom_words(const ct_table *t);                    /* Wd                         */
+int32_t ct_dom_word_offset(const ct_table *t, int32_t i);   /* first word of var i; -1 if bad */
+
+/* ---------------------------------------------------------------- propagation */
+/* Synchronous, host buffers (the user-facing call; Alg. 1).
+ *   removed     host uint64[Wd]: values to remove (bit set = remove); values
+ *               already absent and bits >= d_i are ignored.  May
+ *               be NULL = remove nothing.
+ *   out_dom     host uint64[Wd]: domains after GAC (written on CT_OK only)
+ *   out_pruned  host uint64[Wd] or NULL: values pruned by this call's
+ *               filtering, i.e. (domain after the removal) AND NOT out_dom.
+ * Copies removed in, runs the whole path on the device (one CUDA graph when
+ * cfg.use_graph), copies the result out, and waits for it. */
+ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
+                       uint64_t *out_pruned);
+
+/* Asynchronous, device buffers, enqueued on the state's stream; nothing is
+ * copied to or from the host and the call does not wait.
+ *   removed     device uint64[Wd] (NULL = nothing removed)
+ *   out_dom     device uint64[Wd] or NULL
+ *   out_pruned  device uint64[Wd] or NULL
+ *   out_status  device int32[1] or NULL: CT_OK / CT_FAIL / CT_ESTATE
+ * Returns CT_OK if the work was enqueued (the propagation's own status lands
+ * in *out_status), or an error. */
+ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
+                             uint64_t *out_pruned, int32_t *out_status);
+
+/* Tuple-range sharding with a caller-side combine (n_shards > 1 and no NCCL id,
+ * or for testing several shards on one device).  local: phases a2-a6 on this
+ * shard's words, leaving R+1 flag bytes (per support row: "supported by a valid
+ * tuple of my slice"; last byte: "my slice has a valid tuple") at the device
+ * pointer returned by ct_state_flags.  The caller ORs the flag arrays of all
+ * shards element-wise (e.g. an all-reduce with MAX over uint8) into every
+ * shard's flags, then calls apply, which finishes the call exactly as the
+ * unsharded path would. */
+ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed);
+ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes);
+ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned,
+                                   int32_t *out_status);
+
+/* ---------------------------------------------------------------- states */
+ct_status ct_state_clone(const ct_state *src, ct_state **out);       /* new state = src      */
+ct_status ct_state_copy(ct_state *dst, const ct_state *src);         /* dst := src (async,   */
+                                                                    /* device to device)    */
+ct_status ct_state_set_stream(ct_state *s, void *stream);            /* cudaStream_t          */
+void *ct_state_stream(const ct_state *s);
+ct_status ct_synchronize(ct_state *s);                               /* wait for its stream   */
+void ct_state_destroy(ct_state *s);
+void ct_table_destroy(ct_table *t);   /* destroy all states and batches of t first */
+
+/* ---------------------------------------------------------------- batches */
+/* S independent states of one table in one device pool (BASELINE config 4:
+ * independent search states).  Each slot starts as a copy of `init`. */
+ct_status ct_batch_create(ct_table *t, int32_t n_states, const ct_state *init, ct_batch **out);
+int32_t ct_batch_size(const ct_batch *b);
+ct_status ct_batch_copy(ct_batch *b, int32_t dst_index, const ct_state *src);   /* async */
+ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src);                  /* async */
+/* Synchronous, host buffers: removed/out_dom are [S][Wd] row-major (removed may
+ * be NULL); out_status int32[S] receives CT_OK / CT_FAIL / CT_ESTATE per state.
+ * Returns CT_OK unless an error occurred. */
+ct_status ct_propagate_many(ct_batch *b, const uint64_t *removed, uint64_t *out_dom,
+                            int32_t *out_status);
+/* Asynchronous, device buffers of the same shapes (out_dom, out_status nullable). */
+ct_status ct_propagate_many_async(ct_batch *b, const uint64_t *removed, uint64_t *out_dom,
+                                  int32_t *out_status);
+void ct_batch_destroy(ct_batch *b);
+
+/* ---------------------------------------------------------------- introspection */
+/* Test/measurement only.  currTable of this shard: host uint64[words]. */
+ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits);
+/* One support row (row = rowbase_i + v - lo_i) of this shard: host uint64[words]. */
+ct_status ct_table_read_supports(const ct_table *t, int32_t row, uint64_t *out_bits);
+/* Current domains of a state (its last fixpoint): host uint64[Wd]. */
+ct_status ct_state_read_dom(const ct_state *s, uint64_t *out_dom);
+
+typedef struct ct_stats {
+  int64_t calls;            /* propagations run on this state (copies carry it over)  */
+  int32_t last_status;      /* CT_OK / CT_FAIL / CT_ESTATE of the last call            */
+  int32_t noop;             /* last call had no changed variable                       */
+  int32_t n_changed;        /* |s_val|                                 */
+  int32_t n_update_rows;    /* support rows OR-ed by updateTable                       */
+  int32_t n_filter_items;   /* (x,a) checked by filterDomains (x in s_sup, L201)       */
+  int32_t n_residue_miss;   /* of those, residue probe misses -> index scans           */
+  int64_t words_in;         /* active currTable words before the update (L_in)         */
+  int64_t words_out;        /* active words after the update (L_out)                   */
+} ct_stats;
+ct_status ct_state_stats(const ct_state *s, ct_stats *out);
+
+/* Tuple-range partition used by sharded tables (host-only, no device needed):
+ * shard `rank` of `n_shards` owns currTable words [*word_begin, *word_begin +
+ * *words) of the ceil(n_tuples/64) words, i.e. tuples [64*begin, min(64*(begin
+ * + words), n_tuples)).  Boundaries are floor(g * words_total / n_shards)
+ * rounded down to a multiple of 16 words (128-byte rows); the shards tile the
+ * table exactly.  Returns CT_EINVAL on bad arguments. */
+ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin,
+                         int64_t *words);
+
+/* NCCL bootstrap helper: writes a fresh 128-byte ncclUniqueId (rank 0 calls it
+ * and broadcasts the bytes, e.g. with torch.distributed). */
+ct_status ct_nccl_unique_id(void *out128);
+
+const char *ct_last_error(void);
+const char *ct_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CT_B200_H */

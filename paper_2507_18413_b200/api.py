@@ -1,0 +1,143 @@
+"""Object wrappers over the C names in ct.py (lifetime management only).
+
+    tab = Table(lo, d, tuples)                  # ct_create: supports + root GAC on cuda:device
+    st = tab.root.clone()                       # ct_state_clone
+    status, dom, pruned = st.propagate(removed) # ct_propagate (host numpy uint64[Wd])
+    st.copy_from(tab.root)                      # ct_state_copy (backtrack / restore)
+    b = tab.batch(4096)                         # ct_batch_create
+    status, doms = b.propagate(removed_SxWd)    # ct_propagate_many
+
+Device memory comes from PyTorch's caching allocator and work is ordered on a
+torch.cuda.Stream owned by the table (pass `stream=` to share one).
+"""
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import ct as C
+
+
+class Table:
+    def __init__(self, lo, d, tuples, init_dom=None, scope=None, device: int = 0, stream=None,
+                 torch_alloc: bool = True, n_shards: int = 1, shard_rank: int = 0, nccl_unique_id=None,
+                 update_policy: int = C.CT_POLICY_AUTO, use_residues: bool = True, use_index: bool = True,
+                 use_graph: bool = True):
+        import torch
+        self.device = int(device)
+        if stream is None:
+            self.torch_stream = torch.cuda.Stream(device=self.device)
+            stream_ptr = self.torch_stream.cuda_stream
+        else:
+            self.torch_stream = stream if hasattr(stream, "cuda_stream") else None
+            stream_ptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self.allocator = C.TorchAllocator(self.device) if torch_alloc else None
+        cfg, self._keep = C.make_config(self.device, stream_ptr, self.allocator, n_shards, shard_rank,
+                                        nccl_unique_id, update_policy, use_residues, use_index, use_graph)
+        self.lo = np.ascontiguousarray(lo, np.int32)
+        self.d = np.ascontiguousarray(d, np.int32)
+        status, handle, root, dom = C.ct_create(self.lo, self.d, tuples, init_dom, scope, cfg)
+        self.handle = handle
+        self._states = weakref.WeakSet()
+        self._batches = weakref.WeakSet()
+        self.info = C.ct_table_info_get(handle)
+        self.Wd = int(self.info.dom_words)
+        self.root_status = status
+        self.root_dom = dom
+        self.root = State(self, root)
+
+    @property
+    def stream_ptr(self) -> int:
+        return C.ct_state_stream(self.root.handle)
+
+    def batch(self, n_states: int, init: "State | None" = None) -> "Batch":
+        return Batch(self, n_states, init or self.root)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            for b in list(self._batches):
+                b.close()
+            for s in list(self._states):
+                s.close()
+            C.ct_table_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class State:
+    def __init__(self, table: Table, handle):
+        self.table = table
+        self.handle = handle
+        table._states.add(self)
+
+    def clone(self) -> "State":
+        return State(self.table, C.ct_state_clone(self.handle))
+
+    def copy_from(self, src: "State") -> None:
+        C.ct_state_copy(self.handle, src.handle)
+
+    def propagate(self, removed=None):
+        """Synchronous host call.  Returns (status, dom, pruned); dom/pruned are
+        None unless status == CT_OK."""
+        wd = self.table.Wd
+        out = np.zeros(max(wd, 1), np.uint64)
+        pr = np.zeros(max(wd, 1), np.uint64)
+        rem = None if removed is None else np.ascontiguousarray(removed, np.uint64)
+        st = C.ct_propagate(self.handle, rem, out, pr)
+        return (st, out[:wd], pr[:wd]) if st == C.CT_OK else (st, None, None)
+
+    def propagate_async(self, removed, out_dom=None, out_pruned=None, out_status=None):
+        C.ct_propagate_async(self.handle, removed, out_dom, out_pruned, out_status)
+
+    def read_table(self) -> np.ndarray:
+        return C.ct_state_read_table(self.handle, int(self.table.info.words))
+
+    def read_dom(self) -> np.ndarray:
+        return C.ct_state_read_dom(self.handle, self.table.Wd)
+
+    def stats(self):
+        return C.ct_state_stats(self.handle)
+
+    def synchronize(self):
+        C.ct_synchronize(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None) and self.table.handle:
+            C.ct_state_destroy(self.handle)
+        self.handle = None
+
+
+class Batch:
+    def __init__(self, table: Table, n_states: int, init: State):
+        self.table = table
+        self.S = int(n_states)
+        self.handle = C.ct_batch_create(table.handle, self.S, init.handle)
+        table._batches.add(self)
+
+    def copy(self, index: int, src: State):
+        C.ct_batch_copy(self.handle, index, src.handle)
+
+    def copy_all(self, src: State):
+        C.ct_batch_copy_all(self.handle, src.handle)
+
+    def propagate(self, removed=None):
+        wd = self.table.Wd
+        out = np.zeros((self.S, max(wd, 1)), np.uint64)
+        status = np.zeros(self.S, np.int32)
+        rem = None if removed is None else np.ascontiguousarray(removed, np.uint64).reshape(self.S, wd)
+        C.ct_propagate_many(self.handle, rem, out, status)
+        return status, out[:, :wd]
+
+    def propagate_async(self, removed, out_dom=None, out_status=None):
+        C.ct_propagate_many_async(self.handle, removed, out_dom, out_status)
+
+    def close(self):
+        if getattr(self, "handle", None) and self.table.handle:
+            C.ct_batch_destroy(self.handle)
+        self.handle = None

@@ -1,0 +1,586 @@
+// ct_kernels.cuh -- sm_100a device code of the Compact-Table propagation path.
+//
+// One propagation of a state (Alg. 1) is five launches on
+// one stream, every size fixed at create time so the sequence can be captured
+// in a CUDA graph:
+//
+//   k_ingest   (a2)  removed ∧ dom -> Δ_x, D_x = dom ∧ ¬removed, |Δ_x|, |D_x|,
+//                    s_val, s_sup (Alg. 1 L1-3), the Δ/dom branch of each changed
+//                    var (Alg. 2), the update row list and the filter items.
+//   k_update   (a3-a5) for every active currTable word w:
+//                    T[w] &= AND_{x in s_val} (Δ ? ¬OR_{a∈Δx} S[x,a][w] : OR_{a∈Dx} S[x,a][w])
+//                    (Alg. 2; the per-variable ANDs commute, so all s_val vars
+//                    are folded in one pass), then order-preserving compaction
+//                    of the non-zero words (RSparseBitSet index) with a
+//                    single-pass chained scan; L_out = 0 <=> FAIL (Alg. 1 L5).
+//   k_probe    (a6a) residue probe for each (x,a), x in s_sup (Alg. 3 L3, L220).
+//   k_scan     (a6b) probe misses: warp-parallel intersect of S[x,a] with
+//                    currTable over the compacted index (__ballot_sync any).
+//   k_finalize (a6c-a8) prune unsupported values, lastDom <- dom, outputs.
+//
+// Tuple-range sharding (a10) splits k_finalize's input: the per-row flags sup[]
+// written by k_probe/k_scan are OR-combined across shards before it runs.
+//
+// All kernels take the table by value (TableDev) and an array of per-state
+// descriptors (StateDev), indexed by blockIdx.y, so the same code serves one
+// state (gridDim.y = 1) and a batch of independent states (a9).
+#pragma once
+#include <cstdint>
+
+namespace ctk {
+
+constexpr int kUpdTPB = 256;      // k_update threads per block = words per tile
+constexpr int kIngestTPB = 512;
+constexpr int kProbeTPB = 256;
+constexpr int kScanTPB = 256;
+constexpr int kFinTPB = 256;
+constexpr int kScanUnroll = 8;    // words per lane per scan round
+constexpr int kScanRounds = 4;    // rounds per work unit: unit = 32*8*4 = 1024 index entries
+constexpr int kScanChunk = 32 * kScanUnroll * kScanRounds;
+
+constexpr uint32_t kRowMask = 0x3FFFFFFFu;   // update-list entry: row id
+constexpr uint32_t kEndBit = 1u << 30;        //   last row of its variable's group
+constexpr uint32_t kInvBit = 1u << 31;        //   group uses the Δ-branch (complemented)
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;   // chained-scan tile status
+constexpr unsigned long long kFlagPre = 2ull << 62;
+
+// Device view of an immutable table (one shard).
+struct TableDev {
+  const uint64_t *S;        // supports [R][Wp], row = rowBase[x] + (a - lo[x])
+  const int32_t *rowBase;   // [n+1]   first support row of each var (_supportJmp, L286)
+  const int32_t *domOff;    // [n+1]   first domain word of each var
+  const int32_t *wordVar;   // [Wd]    var owning each domain word
+  const int32_t *rowVar;    // [R]     var owning each support row
+  int32_t n, R, Wd;
+  int32_t W;                // currTable words of this shard
+  int64_t Wp;               // padded row stride in words (multiple of 16)
+  int32_t policy;           // CT_POLICY_*
+  int32_t use_res, use_index;
+  int32_t ntiles_max;       // ceil(W / kUpdTPB)
+};
+
+// Per-state control block (device).  The first four fields persist across
+// calls (they are part of the state); the rest is per-call scratch.
+struct Ctl {
+  int32_t dead;        // 1 after CT_FAIL until restored by a copy
+  int32_t parity;      // which index buffer holds the active index
+  int32_t identity;    // 1: active index is implicitly 0..L-1 (root, or use_index=0)
+  int32_t L;           // active words
+  long long calls;
+  int32_t last_status;
+  // ---- per call
+  int32_t skip;        // dead at entry
+  int32_t noop;        // no changed variable: state already at fixpoint
+  int32_t fail_fast;   // some D_x empty
+  int32_t nrows;       // update-list length
+  int32_t ngroups;     // |s_val|
+  int32_t nitems;      // filter items
+  int32_t L_in;
+  int32_t L_out;       // active words after the update (this shard)
+  int32_t tile_ctr;
+  int32_t nscan;       // residue misses queued for scanning
+  int32_t pad[15];
+};
+static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
+
+struct StateDev {
+  Ctl *ctl;
+  uint64_t *T;              // currTable [Wp]
+  int32_t *idx0, *idx1;     // compacted index double buffer [Wp]
+  int32_t *res;             // residues [R] (word ids of this shard)
+  uint64_t *dom;            // current domains [Wd] (lastDom between calls)
+  uint64_t *din;            // dom after the caller's removals [Wd]
+  int32_t *ulist;           // update row list [R]
+  int32_t *items;           // filter items (support rows) [R]
+  int32_t *scanlist;        // residue misses [R]
+  uint8_t *sup;             // [R+1]: per-row "supported", [R] = "currTable non-empty"
+  int32_t *varcnt;          // [2n]: |Δ_x|, |D_x|
+  unsigned long long *tilestat;  // [ntiles_max] chained-scan tile status
+  uint64_t *out;            // [1 + 2 Wd]: status word, dom, pruned (sync path)
+  uint64_t *slot;           // [Wd] removed (sync path, filled by an H2D copy)
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// Streaming read of a support word: read-only path, no L1 allocation.
+__device__ __forceinline__ uint64_t ld_sup(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Exclusive block scan of a 64-bit value (two packed 32-bit counters never
+// overflow into each other here: each half sums to <= R < 2^30).
+template <int NT>
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *s_warp, uint64_t &total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = lane < NT / 32 ? s_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NT / 32) s_warp[lane] = w;
+  }
+  __syncthreads();
+  const uint64_t base = warp > 0 ? s_warp[warp - 1] : 0;
+  total = s_warp[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+// ------------------------------------------------------------------ a1: supports builder
+// One thread per tuple of this shard: sets bit j of row (x_i, tau_j[i]) for
+// every in-range value (cell ([x_i,v], j) = 1 iff tau_j[i] = v),
+// and the in-range validity of tau_j into the initial currTable (one ballot
+// per 32 tuples -> one 32-bit half-word).  Out-of-range values create no row
+// bit and make the tuple invalid forever.
+__global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int n,
+                        const int32_t *__restrict__ lo, const int32_t *__restrict__ d,
+                        const int32_t *__restrict__ rowBase, uint64_t *__restrict__ S, int64_t Wp,
+                        uint32_t *__restrict__ T32, int64_t n_half_words) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = j < t_local;
+  if (valid) {
+    const int32_t *tau = tuples + j * n;
+    const uint64_t bit = 1ull << (j & 63);
+    const int64_t word = j >> 6;
+    for (int i = 0; i < n; ++i) {
+      const int64_t v = (int64_t)tau[i] - lo[i];
+      if (v >= 0 && v < d[i]) {
+        atomicOr(reinterpret_cast<unsigned long long *>(S + (int64_t)(rowBase[i] + v) * Wp + word),
+                 (unsigned long long)bit);
+      } else {
+        valid = false;
+      }
+    }
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, valid);
+  const int64_t hw = j >> 5;
+  if ((threadIdx.x & 31) == 0 && hw < n_half_words) T32[hw] = bal;
+}
+
+// ------------------------------------------------------------------ a2: ingest
+// grid (1, S), kIngestTPB threads.
+__global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateDev *__restrict__ states,
+                                                       const uint64_t *__restrict__ removed,
+                                                       int64_t removed_stride, int root_mode) {
+  const StateDev st = states[blockIdx.y];
+  Ctl *c = st.ctl;
+  const uint64_t *rem = removed ? removed + (int64_t)blockIdx.y * removed_stride : nullptr;
+  const int tid = threadIdx.x;
+  __shared__ int s_dead, s_fail, s_ngroups;
+  __shared__ uint64_t s_warp[kIngestTPB / 32];
+
+  if (tid == 0) {
+    s_dead = c->dead;
+    s_fail = 0;
+    s_ngroups = 0;
+  }
+  __syncthreads();
+  if (s_dead) {
+    if (tid == 0) {
+      c->skip = 1;
+      c->noop = 0;
+      c->fail_fast = 0;
+    }
+    return;
+  }
+  // reset per-call scratch
+  for (int v = tid; v < 2 * tb.n; v += kIngestTPB) st.varcnt[v] = 0;
+  for (int r = tid; r <= tb.R; r += kIngestTPB) st.sup[r] = 0;
+  for (int k = tid; k < tb.ntiles_max; k += kIngestTPB) st.tilestat[k] = 0;
+  __syncthreads();
+
+  // phase 1: Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, and their sizes
+  for (int k = tid; k < tb.Wd; k += kIngestTPB) {
+    const uint64_t dm = st.dom[k];
+    const uint64_t rm = rem ? rem[k] : 0ull;
+    const uint64_t delta = rm & dm, di = dm & ~rm;
+    st.din[k] = di;
+    const int x = tb.wordVar[k];
+    if (delta) atomicAdd(&st.varcnt[2 * x], __popcll(delta));
+    if (di) atomicAdd(&st.varcnt[2 * x + 1], __popcll(di));
+  }
+  __syncthreads();
+  for (int x = tid; x < tb.n; x += kIngestTPB) {
+    if (st.varcnt[2 * x] > 0) atomicAdd(&s_ngroups, 1);
+    if (st.varcnt[2 * x + 1] == 0) s_fail = 1;     // D_x empty -> no valid tuple
+  }
+  __syncthreads();
+  const bool noop = (s_ngroups == 0) && !root_mode;
+  if (s_fail || noop) {
+    if (tid == 0) {
+      c->skip = 0;
+      c->noop = noop && !s_fail;
+      c->fail_fast = s_fail;
+      c->ngroups = s_ngroups;
+      c->nrows = 0;
+      c->nitems = 0;
+      c->L_in = c->L;
+      c->L_out = 0;
+      c->tile_ctr = 0;
+      c->nscan = 0;
+    }
+    return;
+  }
+
+  // phase 2: update row list (s_val vars, branch rows) + filter items (s_sup)
+  uint64_t carry = 0;
+  for (int base = 0; base < tb.Wd; base += kIngestTPB) {
+    const int k = base + tid;
+    uint64_t ub = 0, fb = 0;
+    bool useDelta = false;
+    int x = 0;
+    if (k < tb.Wd) {
+      x = tb.wordVar[k];
+      const int cd = st.varcnt[2 * x], cs = st.varcnt[2 * x + 1];
+      const uint64_t di = st.din[k];
+      const uint64_t delta = st.dom[k] & ~di;
+      useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);   // Alg. 2
+      if (cd > 0) ub = useDelta ? delta : di;
+      if (cs > 1) fb = di;                                          // Alg. 1 L3: s_sup
+    }
+    const uint64_t packed = ((uint64_t)__popcll(ub) << 32) | (uint64_t)__popcll(fb);
+    uint64_t total;
+    const uint64_t excl = block_excl_scan<kIngestTPB>(packed, s_warp, total) + carry;
+    if (k < tb.Wd) {
+      int up = (int)(excl >> 32), fp = (int)(excl & 0xffffffffu);
+      const int rb = tb.rowBase[x] + (k - tb.domOff[x]) * 64;
+      const uint32_t inv = useDelta ? kInvBit : 0u;
+      while (ub) {
+        const int b = __ffsll(ub) - 1;
+        ub &= ub - 1;
+        st.ulist[up++] = (int32_t)((uint32_t)(rb + b) | inv);
+      }
+      while (fb) {
+        const int b = __ffsll(fb) - 1;
+        fb &= fb - 1;
+        st.items[fp++] = rb + b;
+      }
+    }
+    carry += total;
+  }
+  const int nrows = (int)(carry >> 32), nitems = (int)(carry & 0xffffffffu);
+  __syncthreads();
+  // phase 3: mark the last row of each variable's group
+  for (int base = 0; base < nrows; base += kIngestTPB) {
+    const int p = base + tid;
+    bool last = false;
+    if (p < nrows) {
+      const int r = (int)((uint32_t)st.ulist[p] & kRowMask);
+      last = (p + 1 == nrows) || tb.rowVar[(uint32_t)st.ulist[p + 1] & kRowMask] != tb.rowVar[r];
+    }
+    __syncthreads();
+    if (last) st.ulist[p] = (int32_t)((uint32_t)st.ulist[p] | kEndBit);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    c->skip = 0;
+    c->noop = 0;
+    c->fail_fast = 0;
+    c->ngroups = s_ngroups;
+    c->nrows = nrows;
+    c->nitems = nitems;
+    c->L_in = c->L;
+    c->L_out = 0;
+    c->tile_ctr = 0;
+    c->nscan = 0;
+  }
+}
+
+// ------------------------------------------------------------------ a3-a5: update + compaction
+// Chained-scan look-back (warp 0 of the block); returns the exclusive prefix.
+__device__ __forceinline__ uint32_t tile_lookback(unsigned long long *ts, int tile, uint32_t agg, int lane) {
+  if (tile == 0) {
+    if (lane == 0) st_release(ts, kFlagPre | agg);
+    return 0;
+  }
+  if (lane == 0) st_release(ts + tile, kFlagAgg | agg);
+  uint32_t excl = 0;
+  int base = tile - 1;
+  while (true) {
+    const int p = base - lane;
+    unsigned long long s = kFlagPre;   // before tile 0: prefix 0
+    if (p >= 0) {
+      do {
+        s = ld_acquire(ts + p);
+      } while ((s >> 62) == 0);
+    }
+    const unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+    uint32_t v = (uint32_t)s;
+    if (pre) {
+      const int f = __ffs(pre) - 1;
+      if (lane > f) v = 0;
+    }
+    excl += warp_sum_u32(v);
+    if (pre) break;
+    base -= 32;
+  }
+  if (lane == 0) st_release(ts + tile, kFlagPre | (excl + agg));
+  return excl;
+}
+
+// grid (blocks, S), kUpdTPB threads; persistent over tiles of kUpdTPB active words.
+__global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev *__restrict__ states) {
+  const StateDev st = states[blockIdx.y];
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_go, s_tile, s_nrows, s_L, s_ident, s_par;
+  __shared__ uint32_t s_woff[kUpdTPB / 32];
+  __shared__ uint32_t s_excl;
+  if (tid == 0) {
+    s_go = !(c->skip | c->noop | c->fail_fast);
+    s_nrows = c->nrows;
+    s_L = c->L;
+    s_ident = c->identity;
+    s_par = c->parity;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const int nrows = s_nrows, L = s_L;
+  const int32_t *__restrict__ idx_in = s_par ? st.idx1 : st.idx0;
+  int32_t *__restrict__ idx_out = s_par ? st.idx0 : st.idx1;
+  const bool compact = tb.use_index != 0;
+  const int ntiles = (L + kUpdTPB - 1) / kUpdTPB;
+  const int32_t *__restrict__ ulist = st.ulist;
+  const int64_t Wp = tb.Wp;
+
+  while (true) {
+    if (tid == 0) s_tile = atomicAdd(&c->tile_ctr, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= ntiles) break;
+    const int k = tile * kUpdTPB + tid;
+    const bool valid = k < L;
+    int w = 0;
+    uint64_t nt = 0;
+    if (valid) {
+      w = s_ident ? k : idx_in[k];
+      const uint64_t tw = st.T[w];
+      const uint64_t *__restrict__ col = tb.S + w;
+      uint64_t m = ~0ull, acc = 0;
+      for (int p = 0; p < nrows; p += 8) {
+        if ((tw & m) == 0) break;                      // Alg. 2, per word
+        uint32_t e[8];
+        uint64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) e[u] = (p + u < nrows) ? (uint32_t)__ldg(ulist + p + u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = (p + u < nrows) ? ld_sup(col + (int64_t)(e[u] & kRowMask) * Wp) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (p + u < nrows) {
+            acc |= v[u];
+            if (e[u] & kEndBit) {
+              m &= (e[u] & kInvBit) ? ~acc : acc;
+              acc = 0;
+            }
+          }
+        }
+      }
+      nt = tw & m;
+      if (nt != tw) st.T[w] = nt;
+    }
+    const bool keep = valid && nt != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_woff[warp] = __popc(bal);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t cnt = lane < kUpdTPB / 32 ? s_woff[lane] : 0u;
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const uint32_t agg = __shfl_sync(0xffffffffu, x, kUpdTPB / 32 - 1);
+      if (lane < kUpdTPB / 32) s_woff[lane] = x - cnt;
+      uint32_t excl = 0;
+      if (compact) {
+        excl = tile_lookback(st.tilestat, tile, agg, lane);
+        if (lane == 0 && tile == ntiles - 1) c->L_out = (int32_t)(excl + agg);
+      } else if (lane == 0 && agg) {
+        atomicAdd(&c->L_out, (int32_t)agg);
+      }
+      if (lane == 0) s_excl = excl;
+    }
+    __syncthreads();
+    if (compact && keep) idx_out[s_excl + s_woff[warp] + __popc(bal & lanemask_lt())] = w;
+  }
+}
+
+// ------------------------------------------------------------------ a6: filter
+// grid (ceil(R / kProbeTPB), S): residue probe, one thread per (x,a) item.
+__global__ void __launch_bounds__(kProbeTPB) k_probe(TableDev tb, const StateDev *__restrict__ states) {
+  const StateDev st = states[blockIdx.y];
+  const Ctl *c = st.ctl;
+  if (c->skip | c->noop | c->fail_fast) return;
+  const int Lout = c->L_out;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st.sup[tb.R] = Lout > 0;
+  if (Lout == 0) return;
+  const int i = blockIdx.x * kProbeTPB + threadIdx.x;
+  if (i >= c->nitems) return;
+  const int row = st.items[i];
+  if (tb.use_res) {
+    const int r = st.res[row];
+    if (st.T[r] & tb.S[(int64_t)row * tb.Wp + r]) {
+      st.sup[row] = 1;
+      return;
+    }
+  }
+  const int pos = atomicAdd(&st.ctl->nscan, 1);
+  st.scanlist[pos] = row;
+}
+
+// grid (blocks, S), kScanTPB threads: one warp per (miss, chunk) unit, chunk-major.
+__global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *__restrict__ states) {
+  const StateDev st = states[blockIdx.y];
+  const Ctl *c = st.ctl;
+  if (c->skip | c->noop | c->fail_fast) return;
+  const int nscan = c->nscan;
+  const int Lout = c->L_out;
+  if (nscan == 0 || Lout == 0) return;
+  const bool compact = tb.use_index != 0;
+  // the index written by this call's update lives in the other buffer
+  const int32_t *__restrict__ idx = compact ? (c->parity ? st.idx0 : st.idx1) : nullptr;
+  const int L = compact ? Lout : tb.W;
+  const int lane = threadIdx.x & 31;
+  const int64_t nch = (L + kScanChunk - 1) / kScanChunk;
+  const int64_t total = nch * nscan;
+  const int64_t nw = (int64_t)gridDim.x * (kScanTPB / 32);
+  const uint64_t *__restrict__ T = st.T;
+  for (int64_t u = (int64_t)blockIdx.x * (kScanTPB / 32) + (threadIdx.x >> 5); u < total; u += nw) {
+    const int chunk = (int)(u / nscan);
+    const int item = (int)(u - (int64_t)chunk * nscan);
+    const int row = st.scanlist[item];
+    if (*(volatile const uint8_t *)(st.sup + row)) continue;
+    const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+    const int k0 = chunk * kScanChunk;
+    const int k1 = min(k0 + kScanChunk, L);
+    for (int kb = k0; kb < k1; kb += 32 * kScanUnroll) {
+      int w[kScanUnroll];
+      uint64_t v[kScanUnroll];
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const int k = kb + q * 32 + lane;
+        w[q] = k < k1 ? (compact ? __ldg(idx + k) : k) : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) v[q] = w[q] >= 0 ? (T[w[q]] & ld_sup(srow + w[q])) : 0ull;
+      int hitw = -1;
+#pragma unroll
+      for (int q = kScanUnroll - 1; q >= 0; --q) {
+        const unsigned b = __ballot_sync(0xffffffffu, v[q] != 0);
+        if (b) hitw = __shfl_sync(0xffffffffu, w[q], __ffs(b) - 1);
+      }
+      if (hitw >= 0) {
+        if (lane == 0) {
+          st.sup[row] = 1;
+          st.res[row] = hitw;
+        }
+        break;
+      }
+    }
+  }
+}
+
+// grid (1, S), kFinTPB threads.  Writes the per-state status and outputs.
+__global__ void __launch_bounds__(kFinTPB) k_finalize(TableDev tb, const StateDev *__restrict__ states,
+                                                      uint64_t *__restrict__ out_dom, int64_t dom_stride,
+                                                      uint64_t *__restrict__ out_pruned,
+                                                      int32_t *__restrict__ out_status, int use_state_out) {
+  const StateDev st = states[blockIdx.y];
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x;
+  __shared__ int s_status, s_noop;
+  if (use_state_out) {
+    out_dom = st.out + 1;
+    out_pruned = st.out + 1 + tb.Wd;
+    out_status = reinterpret_cast<int32_t *>(st.out);
+  } else {
+    if (out_dom) out_dom += (int64_t)blockIdx.y * dom_stride;
+    if (out_pruned) out_pruned += (int64_t)blockIdx.y * dom_stride;
+    if (out_status) out_status += blockIdx.y;
+  }
+  if (tid == 0) {
+    int s;
+    if (c->skip) s = -5;                         // CT_ESTATE
+    else if (c->fail_fast) s = 1;                // CT_FAIL
+    else if (c->noop) s = 0;
+    else s = st.sup[tb.R] ? 0 : 1;               // global "currTable non-empty"
+    s_status = s;
+    s_noop = c->noop;
+  }
+  __syncthreads();
+  const int status = s_status;
+  if (status != 0) {
+    if (tid == 0) {
+      if (status == 1) c->dead = 1;
+      c->last_status = status;
+      if (status == 1) c->calls += 1;
+      if (out_status) *out_status = status;
+    }
+    return;
+  }
+  const bool noop = s_noop != 0;
+  for (int k = tid; k < tb.Wd; k += kFinTPB) {
+    const uint64_t di = st.din[k];
+    uint64_t nd = di;
+    if (!noop) {
+      const int x = tb.wordVar[k];
+      if (st.varcnt[2 * x + 1] > 1) {               // x in s_sup (Alg. 3 L1)
+        const int rb = tb.rowBase[x] + (k - tb.domOff[x]) * 64;
+        uint64_t bits = di;
+        while (bits) {
+          const int b = __ffsll(bits) - 1;
+          bits &= bits - 1;
+          if (!st.sup[rb + b]) nd &= ~(1ull << b);  // Alg. 3 L3-4
+        }
+      }
+    }
+    st.dom[k] = nd;
+    if (out_dom) out_dom[k] = nd;
+    if (out_pruned) out_pruned[k] = di & ~nd;
+  }
+  if (tid == 0) {
+    if (!noop && tb.use_index) {
+      c->parity ^= 1;
+      c->L = c->L_out;
+      c->identity = 0;
+    }
+    c->calls += 1;
+    c->last_status = 0;
+    if (out_status) *out_status = 0;
+  }
+}
+
+}  // namespace ctk

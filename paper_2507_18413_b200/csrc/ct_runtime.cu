@@ -1,0 +1,873 @@
+// ct_runtime.cu -- host runtime and C ABI (include/ct.h) of the B200 Compact-Table
+// propagation library.  Owns device memory (through the caller's allocator hook),
+// streams, per-state CUDA graphs and the optional NCCL communicator for
+// tuple-range sharding.  All propagation arithmetic is in ct_kernels.cuh.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "ct.h"
+#include "ct_kernels.cuh"
+
+using namespace ctk;
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[1024] = "";
+
+static ct_status fail(ct_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof g_err, fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(CT_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, \
+                                       cudaGetErrorString(e_));                              \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                       \
+  do {                                                                                       \
+    ncclResult_t r_ = (expr);                                                                \
+    if (r_ != ncclSuccess) return fail(CT_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #expr, \
+                                       ncclGetErrorString(r_));                              \
+  } while (0)
+
+#define CT_TRY(expr)              \
+  do {                            \
+    ct_status s_ = (expr);        \
+    if (s_ < 0) return s_;        \
+  } while (0)
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Byte layout of one state's device block.  The persistent prefix [0, persist)
+// is what ct_state_copy moves; the rest is per-call scratch.
+struct StateLayout {
+  size_t ctl, T, idx0, idx1, res, dom, persist;
+  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, desc, total;
+};
+
+}  // namespace
+
+struct ct_table {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  ct_allocator alloc{};
+  bool has_alloc = false;
+  int n = 0, R = 0, Wd = 0;
+  int64_t t = 0, Wtot = 0, wbeg = 0, W = 0, Wp = 0, t_local = 0;
+  int policy = 0, use_res = 1, use_index = 1, use_graph = 1;
+  int n_shards = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  std::vector<int32_t> lo, d, rowBase, domOff, scope;
+  std::vector<uint64_t> full_dom;    // full-interval domain bitmap
+  void *meta = nullptr;
+  size_t meta_bytes = 0;
+  uint64_t *S = nullptr;
+  size_t S_bytes = 0;
+  TableDev dev{};
+  StateLayout lay{};
+  int sm_count = 148;
+  int upd_occ = 1, scan_occ = 1;
+  int live = 0;   // states + batches alive
+
+  void *dalloc(size_t bytes) {
+    if (bytes == 0) bytes = 256;
+    if (has_alloc) return alloc.alloc(bytes, (void *)stream, alloc.ctx);
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    return p;
+  }
+  void dfree(void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes == 0) bytes = 256;
+    if (has_alloc) alloc.free(p, bytes, (void *)stream, alloc.ctx);
+    else cudaFree(p);
+  }
+};
+
+struct ct_state {
+  ct_table *tb = nullptr;
+  cudaStream_t stream = nullptr;
+  char *mem = nullptr;
+  StateDev h{};              // host copy of the descriptor
+  StateDev *d_desc = nullptr;
+  uint64_t *h_in = nullptr;  // pinned [Wd]
+  uint64_t *h_out = nullptr; // pinned [1 + 2 Wd]
+  cudaGraphExec_t gexec = nullptr;
+};
+
+struct ct_batch {
+  ct_table *tb = nullptr;
+  int S = 0;
+  char *mem = nullptr;
+  size_t bytes = 0;
+  StateDev *d_desc = nullptr;
+  std::vector<StateDev> h;
+  size_t desc_bytes = 0;
+  uint64_t *h_in = nullptr, *h_dom = nullptr;   // pinned [S][Wd]
+  int32_t *h_status = nullptr;                  // pinned [S]
+  uint64_t *d_in = nullptr, *d_dom = nullptr;   // device [S][Wd]
+  int32_t *d_status = nullptr;
+};
+
+// ------------------------------------------------------------------ layout / descriptors
+static StateLayout make_layout(const ct_table *tb) {
+  StateLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = (size_t)round_up((int64_t)(o + bytes), 256);
+    return at;
+  };
+  const int ntiles = tb->dev.ntiles_max;
+  L.ctl = take(256);
+  L.T = take(tb->Wp * 8);
+  L.idx0 = take(tb->Wp * 4);
+  L.idx1 = take(tb->Wp * 4);
+  L.res = take((size_t)tb->R * 4);
+  L.dom = take((size_t)tb->Wd * 8);
+  L.persist = o;
+  L.din = take((size_t)tb->Wd * 8);
+  L.ulist = take((size_t)tb->R * 4);
+  L.items = take((size_t)tb->R * 4);
+  L.scanlist = take((size_t)tb->R * 4);
+  L.sup = take((size_t)tb->R + 1);
+  L.varcnt = take((size_t)tb->n * 8);
+  L.tilestat = take((size_t)std::max(ntiles, 1) * 8);
+  L.out = take((size_t)(1 + 2 * tb->Wd) * 8);
+  L.slot = take((size_t)tb->Wd * 8);
+  L.desc = take(sizeof(StateDev));
+  L.total = o;
+  return L;
+}
+
+static StateDev make_desc(const ct_table *tb, char *mem) {
+  const StateLayout &L = tb->lay;
+  StateDev s{};
+  s.ctl = reinterpret_cast<Ctl *>(mem + L.ctl);
+  s.T = reinterpret_cast<uint64_t *>(mem + L.T);
+  s.idx0 = reinterpret_cast<int32_t *>(mem + L.idx0);
+  s.idx1 = reinterpret_cast<int32_t *>(mem + L.idx1);
+  s.res = reinterpret_cast<int32_t *>(mem + L.res);
+  s.dom = reinterpret_cast<uint64_t *>(mem + L.dom);
+  s.din = reinterpret_cast<uint64_t *>(mem + L.din);
+  s.ulist = reinterpret_cast<int32_t *>(mem + L.ulist);
+  s.items = reinterpret_cast<int32_t *>(mem + L.items);
+  s.scanlist = reinterpret_cast<int32_t *>(mem + L.scanlist);
+  s.sup = reinterpret_cast<uint8_t *>(mem + L.sup);
+  s.varcnt = reinterpret_cast<int32_t *>(mem + L.varcnt);
+  s.tilestat = reinterpret_cast<unsigned long long *>(mem + L.tilestat);
+  s.out = reinterpret_cast<uint64_t *>(mem + L.out);
+  s.slot = reinterpret_cast<uint64_t *>(mem + L.slot);
+  return s;
+}
+
+// ------------------------------------------------------------------ launch helpers
+static int update_blocks(const ct_table *tb, int S) {
+  const int resident = tb->sm_count * tb->upd_occ;
+  const int ntiles = std::max(tb->dev.ntiles_max, 1);
+  int per_state = (resident + S - 1) / S;
+  return std::max(1, std::min(per_state, ntiles));
+}
+static int scan_blocks(const ct_table *tb, int S) {
+  const int resident = tb->sm_count * tb->scan_occ;
+  return std::max(1, (resident + S - 1) / S);
+}
+
+// a2-a6 on S states (everything before the cross-shard combine).
+static ct_status enqueue_local(ct_table *tb, const StateDev *d_desc, int S, const uint64_t *removed,
+                               int root_mode, cudaStream_t st) {
+  k_ingest<<<dim3(1, S), kIngestTPB, 0, st>>>(tb->dev, d_desc, removed, tb->Wd, root_mode);
+  k_update<<<dim3(update_blocks(tb, S), S), kUpdTPB, 0, st>>>(tb->dev, d_desc);
+  k_probe<<<dim3((unsigned)std::max(1, (tb->R + kProbeTPB - 1) / kProbeTPB), S), kProbeTPB, 0, st>>>(
+      tb->dev, d_desc);
+  k_scan<<<dim3(scan_blocks(tb, S), S), kScanTPB, 0, st>>>(tb->dev, d_desc);
+  CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
+static ct_status enqueue_combine(ct_table *tb, const StateDev &h, cudaStream_t st) {
+  if (tb->comm) NCCL_TRY(ncclAllReduce(h.sup, h.sup, (size_t)tb->R + 1, ncclUint8, ncclMax, tb->comm, st));
+  return CT_OK;
+}
+
+static ct_status enqueue_finalize(ct_table *tb, const StateDev *d_desc, int S, uint64_t *out_dom,
+                                  uint64_t *out_pruned, int32_t *out_status, int use_state_out,
+                                  cudaStream_t st) {
+  k_finalize<<<dim3(1, S), kFinTPB, 0, st>>>(tb->dev, d_desc, out_dom, tb->Wd, out_pruned, out_status,
+                                             use_state_out);
+  CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
+// Whole single-state call into the state's own out buffer, with host copies.
+static ct_status enqueue_sync_call(ct_state *s, int root_mode) {
+  ct_table *tb = s->tb;
+  const size_t in_b = (size_t)tb->Wd * 8, out_b = (size_t)(1 + 2 * tb->Wd) * 8;
+  if (in_b) CUDA_TRY(cudaMemcpyAsync(s->h.slot, s->h_in, in_b, cudaMemcpyHostToDevice, s->stream));
+  CT_TRY(enqueue_local(tb, s->d_desc, 1, s->h.slot, root_mode, s->stream));
+  CT_TRY(enqueue_combine(tb, s->h, s->stream));
+  CT_TRY(enqueue_finalize(tb, s->d_desc, 1, nullptr, nullptr, nullptr, 1, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(s->h_out, s->h.out, out_b, cudaMemcpyDeviceToHost, s->stream));
+  return CT_OK;
+}
+
+// ------------------------------------------------------------------ state lifetime
+static void free_state_mem(ct_state *s) {
+  if (!s) return;
+  ct_table *tb = s->tb;
+  DeviceGuard g(tb->device);
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  if (s->h_in) cudaFreeHost(s->h_in);
+  if (s->h_out) cudaFreeHost(s->h_out);
+  if (s->mem) tb->dfree(s->mem, tb->lay.total);
+  tb->live--;
+  delete s;
+}
+
+static ct_status new_state(ct_table *tb, ct_state **out) {
+  ct_state *s = new (std::nothrow) ct_state();
+  if (!s) return fail(CT_ENOMEM, "host allocation failed");
+  s->tb = tb;
+  s->stream = tb->stream;
+  tb->live++;
+  s->mem = (char *)tb->dalloc(tb->lay.total);
+  if (!s->mem) {
+    free_state_mem(s);
+    return fail(CT_ENOMEM, "device allocation of %zu bytes for a state failed", tb->lay.total);
+  }
+  if (cudaHostAlloc((void **)&s->h_in, std::max<size_t>(8, (size_t)tb->Wd * 8), cudaHostAllocDefault) !=
+          cudaSuccess ||
+      cudaHostAlloc((void **)&s->h_out, (size_t)(1 + 2 * tb->Wd) * 8, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    free_state_mem(s);
+    return fail(CT_ENOMEM, "pinned host allocation failed");
+  }
+  s->h = make_desc(tb, s->mem);
+  s->d_desc = reinterpret_cast<StateDev *>(s->mem + tb->lay.desc);
+  ct_status st = CT_OK;
+  // synchronous: the descriptor must be in place whichever stream uses the state first
+  if (cudaMemcpy(s->d_desc, &s->h, sizeof(StateDev), cudaMemcpyHostToDevice) != cudaSuccess) {
+    st = fail(CT_ECUDA, "descriptor upload failed: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  if (st != CT_OK) {
+    free_state_mem(s);
+    return st;
+  }
+  *out = s;
+  return CT_OK;
+}
+
+// ------------------------------------------------------------------ table lifetime
+static void free_table(ct_table *tb) {
+  if (!tb) return;
+  DeviceGuard g(tb->device);
+  if (tb->stream) cudaStreamSynchronize(tb->stream);
+  if (tb->comm) ncclCommDestroy(tb->comm);
+  if (tb->S) tb->dfree(tb->S, tb->S_bytes);
+  if (tb->meta) tb->dfree(tb->meta, tb->meta_bytes);
+  if (tb->own_stream && tb->stream) cudaStreamDestroy(tb->stream);
+  delete tb;
+}
+
+extern "C" {
+
+void ct_config_init(ct_config *cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof *cfg);
+  cfg->device = 0;
+  cfg->n_shards = 1;
+  cfg->shard_rank = 0;
+  cfg->update_policy = CT_POLICY_AUTO;
+  cfg->use_residues = 1;
+  cfg->use_index = 1;
+  cfg->use_graph = 1;
+}
+
+ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin, int64_t *words) {
+  if (n_tuples < 0 || n_shards < 1 || rank < 0 || rank >= n_shards || !word_begin || !words)
+    return fail(CT_EINVAL, "ct_shard_range: bad arguments");
+  const int64_t wtot = (n_tuples + 63) / 64;
+  // shard g owns words [b_g, b_{g+1}), b_g = floor(g*Wtot/G) rounded down to 16 words, b_G = Wtot
+  auto bound = [&](int64_t g) -> int64_t {
+    if (g >= n_shards) return wtot;
+    return (int64_t)((__int128)wtot * g / n_shards) / 16 * 16;
+  };
+  *word_begin = bound(rank);
+  *words = bound(rank + 1) - *word_begin;
+  return CT_OK;
+}
+
+const char *ct_last_error(void) { return g_err; }
+const char *ct_version(void) { return "ct_b200 0.1 (sm_100a)"; }
+
+ct_status ct_nccl_unique_id(void *out128) {
+  if (!out128) return fail(CT_EINVAL, "ct_nccl_unique_id: NULL output");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(out128, &id, 128);
+  return CT_OK;
+}
+
+static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom_lo, const int32_t *dom_size,
+                             const uint64_t *init_dom, int64_t n_tuples, const int32_t *tuples,
+                             const ct_config *cfg_in, ct_table **out_table, ct_state **out_root,
+                             uint64_t *out_dom, ct_table *tb) {
+  ct_config cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else ct_config_init(&cfg);
+
+  // ---------------- validation (include/ct.h)
+  if (n < 1) return fail(CT_EINVAL, "n_vars must be >= 1 (got %d)", n);
+  if (!dom_lo || !dom_size) return fail(CT_EINVAL, "dom_lo and dom_size are required");
+  if (n_tuples < 0) return fail(CT_EINVAL, "n_tuples must be >= 0");
+  if (n_tuples > 0 && !tuples) return fail(CT_EINVAL, "tuples is NULL");
+  if (!out_table || !out_root) return fail(CT_EINVAL, "out_table and out_root are required");
+  if (cfg.n_shards < 1 || cfg.shard_rank < 0 || cfg.shard_rank >= cfg.n_shards)
+    return fail(CT_EINVAL, "bad shard config (n_shards=%d, shard_rank=%d)", cfg.n_shards, cfg.shard_rank);
+  if (cfg.update_policy < 0 || cfg.update_policy > 2) return fail(CT_EINVAL, "bad update_policy");
+  if (cfg.alloc && (!cfg.alloc->alloc || !cfg.alloc->free)) return fail(CT_EINVAL, "allocator hooks missing");
+  int64_t R = 0;
+  for (int i = 0; i < n; ++i) {
+    if (dom_size[i] < 1) return fail(CT_EINVAL, "dom_size[%d] must be >= 1", i);
+    if ((int64_t)dom_lo[i] + dom_size[i] - 1 > INT32_MAX) return fail(CT_EINVAL, "domain %d overflows int32", i);
+    R += dom_size[i];
+  }
+  if (R >= (int64_t)kRowMask) return fail(CT_EINVAL, "too many support rows (%lld)", (long long)R);
+  if (scope) {
+    std::vector<int32_t> sc(scope, scope + n);
+    std::sort(sc.begin(), sc.end());
+    if (std::adjacent_find(sc.begin(), sc.end()) != sc.end())
+      return fail(CT_EINVAL, "duplicate variable in scope (var(c) is a set, PAPER.md L48)");
+  }
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cfg.device < 0 || cfg.device >= ndev) return fail(CT_EINVAL, "device %d not present (%d devices)", cfg.device, ndev);
+
+  // ---------------- geometry
+  tb->device = cfg.device;
+  tb->n = n;
+  tb->R = (int)R;
+  tb->t = n_tuples;
+  tb->policy = cfg.update_policy;
+  tb->use_res = cfg.use_residues ? 1 : 0;
+  tb->use_index = cfg.use_index ? 1 : 0;
+  tb->use_graph = cfg.use_graph ? 1 : 0;
+  tb->n_shards = cfg.n_shards;
+  tb->rank = cfg.shard_rank;
+  if (cfg.alloc) {
+    tb->alloc = *cfg.alloc;
+    tb->has_alloc = true;
+  }
+  tb->lo.assign(dom_lo, dom_lo + n);
+  tb->d.assign(dom_size, dom_size + n);
+  if (scope) tb->scope.assign(scope, scope + n);
+  tb->rowBase.assign(n + 1, 0);
+  tb->domOff.assign(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    tb->rowBase[i + 1] = tb->rowBase[i] + dom_size[i];
+    tb->domOff[i + 1] = tb->domOff[i] + (dom_size[i] + 63) / 64;
+  }
+  tb->Wd = tb->domOff[n];
+  tb->Wtot = (n_tuples + 63) / 64;
+  CT_TRY(ct_shard_range(n_tuples, tb->n_shards, tb->rank, &tb->wbeg, &tb->W));
+  if (tb->W > INT32_MAX - 1024) return fail(CT_EINVAL, "table shard too large (%lld words)", (long long)tb->W);
+  tb->Wp = round_up(std::max<int64_t>(tb->W, 1), 16);
+  const int64_t j0 = std::min(tb->wbeg * 64, n_tuples), j1 = std::min((tb->wbeg + tb->W) * 64, n_tuples);
+  tb->t_local = j1 - j0;
+  tb->full_dom.assign(tb->Wd, 0ull);
+  for (int i = 0; i < n; ++i)
+    for (int a = 0; a < dom_size[i]; ++a) tb->full_dom[tb->domOff[i] + a / 64] |= 1ull << (a % 64);
+
+  DeviceGuard guard(tb->device);
+  if (cfg.stream) {
+    tb->stream = (cudaStream_t)cfg.stream;
+  } else {
+    CUDA_TRY(cudaStreamCreateWithFlags(&tb->stream, cudaStreamNonBlocking));
+    tb->own_stream = true;
+  }
+  CUDA_TRY(cudaDeviceGetAttribute(&tb->sm_count, cudaDevAttrMultiProcessorCount, tb->device));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb->upd_occ, k_update, kUpdTPB, 0));
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb->scan_occ, k_scan, kScanTPB, 0));
+  tb->upd_occ = std::max(1, tb->upd_occ);
+  tb->scan_occ = std::max(1, tb->scan_occ);
+
+  // ---------------- NCCL (tuple-range sharding)
+  if (cfg.nccl_unique_id) {
+    ncclUniqueId id;
+    memcpy(&id, cfg.nccl_unique_id, sizeof id);
+    NCCL_TRY(ncclCommInitRank(&tb->comm, tb->n_shards, id, tb->rank));
+  }
+
+  // ---------------- table metadata on the device
+  std::vector<int32_t> wordVar(std::max(tb->Wd, 1)), rowVar(std::max(tb->R, 1));
+  for (int i = 0; i < n; ++i) {
+    for (int k = tb->domOff[i]; k < tb->domOff[i + 1]; ++k) wordVar[k] = i;
+    for (int r = tb->rowBase[i]; r < tb->rowBase[i + 1]; ++r) rowVar[r] = i;
+  }
+  std::vector<int32_t> meta;
+  meta.insert(meta.end(), tb->rowBase.begin(), tb->rowBase.end());   // [0, n+1)
+  meta.insert(meta.end(), tb->domOff.begin(), tb->domOff.end());     // [n+1, 2n+2)
+  meta.insert(meta.end(), wordVar.begin(), wordVar.end());           // [2n+2, +Wd)
+  meta.insert(meta.end(), rowVar.begin(), rowVar.end());             // [.., +R)
+  meta.insert(meta.end(), tb->lo.begin(), tb->lo.end());
+  meta.insert(meta.end(), tb->d.begin(), tb->d.end());
+  tb->meta_bytes = meta.size() * 4;
+  tb->meta = tb->dalloc(tb->meta_bytes);
+  if (!tb->meta) return fail(CT_ENOMEM, "device allocation of table metadata failed");
+  CUDA_TRY(cudaMemcpyAsync(tb->meta, meta.data(), tb->meta_bytes, cudaMemcpyHostToDevice, tb->stream));
+  const int32_t *m = (const int32_t *)tb->meta;
+  const int32_t *d_rowBase = m, *d_domOff = m + n + 1, *d_wordVar = m + 2 * n + 2;
+  const int32_t *d_rowVar = d_wordVar + std::max(tb->Wd, 1);
+  const int32_t *d_lo = d_rowVar + std::max(tb->R, 1), *d_d = d_lo + n;
+
+  tb->S_bytes = (size_t)tb->R * (size_t)tb->Wp * 8;
+  tb->S = (uint64_t *)tb->dalloc(tb->S_bytes);
+  if (!tb->S) return fail(CT_ENOMEM, "device allocation of %zu bytes of supports failed", tb->S_bytes);
+  CUDA_TRY(cudaMemsetAsync(tb->S, 0, tb->S_bytes, tb->stream));
+
+  TableDev &dv = tb->dev;
+  dv.S = tb->S;
+  dv.rowBase = d_rowBase;
+  dv.domOff = d_domOff;
+  dv.wordVar = d_wordVar;
+  dv.rowVar = d_rowVar;
+  dv.n = n;
+  dv.R = tb->R;
+  dv.Wd = tb->Wd;
+  dv.W = (int32_t)tb->W;
+  dv.Wp = tb->Wp;
+  dv.policy = tb->policy;
+  dv.use_res = tb->use_res;
+  dv.use_index = tb->use_index;
+  dv.ntiles_max = (int32_t)((tb->W + kUpdTPB - 1) / kUpdTPB);
+  tb->lay = make_layout(tb);
+
+  // ---------------- root state + supports (a1)
+  ct_state *root = nullptr;
+  CT_TRY(new_state(tb, &root));
+  *out_root = root;   // owned by the caller's cleanup path from here on
+  CUDA_TRY(cudaMemsetAsync(root->mem, 0, tb->lay.persist, tb->stream));
+  if (tb->t_local > 0) {
+    const size_t tb_bytes = (size_t)tb->t_local * n * 4;
+    void *d_tup = tb->dalloc(tb_bytes);
+    if (!d_tup) return fail(CT_ENOMEM, "device allocation of %zu bytes of tuples failed", tb_bytes);
+    cudaError_t e = cudaMemcpyAsync(d_tup, tuples + j0 * n, tb_bytes, cudaMemcpyHostToDevice, tb->stream);
+    if (e == cudaSuccess) {
+      const int threads = 256;
+      const int64_t blocks = (tb->t_local + threads - 1) / threads;
+      k_build<<<(unsigned)blocks, threads, 0, tb->stream>>>((const int32_t *)d_tup, tb->t_local, n, d_lo, d_d,
+                                                            d_rowBase, tb->S, tb->Wp, (uint32_t *)root->h.T,
+                                                            2 * tb->Wp);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(tb->stream);   // tuples freed below
+    tb->dfree(d_tup, tb_bytes);
+    if (e != cudaSuccess) return fail(CT_ECUDA, "supports build failed: %s", cudaGetErrorString(e));
+  }
+  Ctl c0{};
+  c0.L = (int32_t)tb->W;
+  c0.identity = 1;
+  CUDA_TRY(cudaMemcpyAsync(root->h.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice, tb->stream));
+  if (tb->Wd)
+    CUDA_TRY(cudaMemcpyAsync(root->h.dom, tb->full_dom.data(), (size_t)tb->Wd * 8, cudaMemcpyHostToDevice,
+                             tb->stream));
+  // root propagation: remove the holes of init_dom
+  for (int k = 0; k < tb->Wd; ++k) root->h_in[k] = init_dom ? (tb->full_dom[k] & ~init_dom[k]) : 0ull;
+  CT_TRY(enqueue_sync_call(root, /*root_mode=*/1));
+  CUDA_TRY(cudaStreamSynchronize(tb->stream));
+  const int32_t status = *(const int32_t *)root->h_out;
+  if (status == CT_OK && out_dom && tb->Wd) memcpy(out_dom, root->h_out + 1, (size_t)tb->Wd * 8);
+  *out_table = tb;
+  return status == CT_OK ? CT_OK : CT_FAIL;
+}
+
+ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo, const int32_t *dom_size,
+                    const uint64_t *init_dom, int64_t n_tuples, const int32_t *tuples, const ct_config *cfg,
+                    ct_table **out_table, ct_state **out_root, uint64_t *out_dom) {
+  if (out_table) *out_table = nullptr;
+  if (out_root) *out_root = nullptr;
+  ct_table *tb = new (std::nothrow) ct_table();
+  if (!tb) return fail(CT_ENOMEM, "host allocation failed");
+  ct_state *root = nullptr;
+  ct_table *tab = nullptr;
+  ct_status s = create_impl(n_vars, scope, dom_lo, dom_size, init_dom, n_tuples, tuples, cfg, &tab, &root,
+                            out_dom, tb);
+  if (s < 0) {
+    if (root) free_state_mem(root);
+    free_table(tb);
+    return s;
+  }
+  *out_table = tab;
+  *out_root = root;
+  return s;
+}
+
+ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
+  if (!t || !o) return fail(CT_EINVAL, "NULL argument");
+  o->n_vars = t->n;
+  o->n_rows = t->R;
+  o->dom_words = t->Wd;
+  o->n_shards = t->n_shards;
+  o->shard_rank = t->rank;
+  o->n_tuples = t->t;
+  o->words_total = t->Wtot;
+  o->word_begin = t->wbeg;
+  o->words = t->W;
+  o->row_stride_words = t->Wp;
+  o->device_bytes = (int64_t)(t->S_bytes + t->meta_bytes);
+  o->state_bytes = (int64_t)t->lay.total;
+  return CT_OK;
+}
+
+int32_t ct_dom_words(const ct_table *t) { return t ? t->Wd : -1; }
+int32_t ct_dom_word_offset(const ct_table *t, int32_t i) {
+  if (!t || i < 0 || i >= t->n) return -1;
+  return t->domOff[i];
+}
+
+// ------------------------------------------------------------------ propagation
+ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  ct_table *tb = s->tb;
+  if (tb->n_shards > 1 && !tb->comm)
+    return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
+  DeviceGuard g(tb->device);
+  if (tb->Wd) {
+    if (removed) memcpy(s->h_in, removed, (size_t)tb->Wd * 8);
+    else memset(s->h_in, 0, (size_t)tb->Wd * 8);
+  }
+  if (tb->use_graph) {
+    if (!s->gexec) {
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+      ct_status st = enqueue_sync_call(s, 0);
+      cudaError_t e = cudaStreamEndCapture(s->stream, &graph);
+      if (st < 0) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (e != cudaSuccess) return fail(CT_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&s->gexec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        s->gexec = nullptr;
+        return fail(CT_ECUDA, "graph instantiate failed: %s", cudaGetErrorString(e));
+      }
+    }
+    CUDA_TRY(cudaGraphLaunch(s->gexec, s->stream));
+  } else {
+    CT_TRY(enqueue_sync_call(s, 0));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const int32_t status = *(const int32_t *)s->h_out;
+  if (status == CT_OK) {
+    if (out_dom && tb->Wd) memcpy(out_dom, s->h_out + 1, (size_t)tb->Wd * 8);
+    if (out_pruned && tb->Wd) memcpy(out_pruned, s->h_out + 1 + tb->Wd, (size_t)tb->Wd * 8);
+  }
+  if (status == CT_ESTATE) return fail(CT_ESTATE, "state is dead (returned CT_FAIL); restore it with ct_state_copy");
+  return (ct_status)status;
+}
+
+ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned,
+                             int32_t *out_status) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  ct_table *tb = s->tb;
+  if (tb->n_shards > 1 && !tb->comm)
+    return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
+  DeviceGuard g(tb->device);
+  CT_TRY(enqueue_local(tb, s->d_desc, 1, removed, 0, s->stream));
+  CT_TRY(enqueue_combine(tb, s->h, s->stream));
+  return enqueue_finalize(tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream);
+}
+
+ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  DeviceGuard g(s->tb->device);
+  return enqueue_local(s->tb, s->d_desc, 1, removed, 0, s->stream);
+}
+
+ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes) {
+  if (!s || !flags_dev || !n_bytes) return fail(CT_EINVAL, "NULL argument");
+  *flags_dev = s->h.sup;
+  *n_bytes = s->tb->R + 1;
+  return CT_OK;
+}
+
+ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  DeviceGuard g(s->tb->device);
+  return enqueue_finalize(s->tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream);
+}
+
+// ------------------------------------------------------------------ states
+ct_status ct_state_clone(const ct_state *src, ct_state **out) {
+  if (!src || !out) return fail(CT_EINVAL, "NULL argument");
+  ct_table *tb = src->tb;
+  DeviceGuard g(tb->device);
+  ct_state *s = nullptr;
+  CT_TRY(new_state(tb, &s));
+  s->stream = src->stream;
+  cudaError_t e = cudaMemcpyAsync(s->mem, src->mem, tb->lay.persist, cudaMemcpyDeviceToDevice, s->stream);
+  if (e != cudaSuccess) {
+    free_state_mem(s);
+    return fail(CT_ECUDA, "state clone copy failed: %s", cudaGetErrorString(e));
+  }
+  *out = s;
+  return CT_OK;
+}
+
+ct_status ct_state_copy(ct_state *dst, const ct_state *src) {
+  if (!dst || !src) return fail(CT_EINVAL, "NULL argument");
+  if (dst->tb != src->tb) return fail(CT_ESTATE, "states belong to different tables");
+  if (dst == src) return CT_OK;
+  DeviceGuard g(dst->tb->device);
+  if (src->stream != dst->stream) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEventRecord(ev, src->stream);
+    cudaStreamWaitEvent(dst->stream, ev, 0);
+    cudaEventDestroy(ev);
+  }
+  CUDA_TRY(cudaMemcpyAsync(dst->mem, src->mem, dst->tb->lay.persist, cudaMemcpyDeviceToDevice, dst->stream));
+  return CT_OK;
+}
+
+ct_status ct_state_set_stream(ct_state *s, void *stream) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  if (!stream) return fail(CT_EINVAL, "stream must be a non-legacy cudaStream_t");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->stream = (cudaStream_t)stream;
+  if (s->gexec) {
+    cudaGraphExecDestroy(s->gexec);
+    s->gexec = nullptr;
+  }
+  return CT_OK;
+}
+
+void *ct_state_stream(const ct_state *s) { return s ? (void *)s->stream : nullptr; }
+
+ct_status ct_synchronize(ct_state *s) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return CT_OK;
+}
+
+void ct_state_destroy(ct_state *s) {
+  if (!s) return;
+  {
+    DeviceGuard g(s->tb->device);
+    cudaStreamSynchronize(s->stream);
+  }
+  free_state_mem(s);
+}
+
+void ct_table_destroy(ct_table *t) { free_table(t); }
+
+// ------------------------------------------------------------------ batches
+ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, ct_batch **out) {
+  if (!tb || !init || !out) return fail(CT_EINVAL, "NULL argument");
+  if (init->tb != tb) return fail(CT_ESTATE, "init state belongs to another table");
+  if (n_states < 1 || n_states > 65535) return fail(CT_EINVAL, "n_states must be in [1, 65535]");
+  if (tb->n_shards > 1) return fail(CT_EINVAL, "batches of sharded tables are not supported");
+  DeviceGuard g(tb->device);
+  ct_batch *b = new (std::nothrow) ct_batch();
+  if (!b) return fail(CT_ENOMEM, "host allocation failed");
+  b->tb = tb;
+  b->S = n_states;
+  b->bytes = tb->lay.total * (size_t)n_states;
+  b->desc_bytes = sizeof(StateDev) * (size_t)n_states;
+  const size_t io = (size_t)n_states * tb->Wd * 8;
+  auto cleanup = [&](ct_status s) {
+    if (b->mem) tb->dfree(b->mem, b->bytes);
+    if (b->d_desc) tb->dfree(b->d_desc, b->desc_bytes);
+    if (b->d_in) tb->dfree(b->d_in, io);
+    if (b->d_dom) tb->dfree(b->d_dom, io);
+    if (b->d_status) tb->dfree(b->d_status, (size_t)n_states * 4);
+    if (b->h_in) cudaFreeHost(b->h_in);
+    if (b->h_dom) cudaFreeHost(b->h_dom);
+    if (b->h_status) cudaFreeHost(b->h_status);
+    delete b;
+    return s;
+  };
+  b->mem = (char *)tb->dalloc(b->bytes);
+  b->d_desc = (StateDev *)tb->dalloc(b->desc_bytes);
+  b->d_in = (uint64_t *)tb->dalloc(io);
+  b->d_dom = (uint64_t *)tb->dalloc(io);
+  b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
+  if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status)
+    return cleanup(fail(CT_ENOMEM, "device allocation of a %d-state batch (%zu bytes) failed", n_states, b->bytes));
+  if (cudaHostAlloc((void **)&b->h_in, std::max<size_t>(io, 8), 0) != cudaSuccess ||
+      cudaHostAlloc((void **)&b->h_dom, std::max<size_t>(io, 8), 0) != cudaSuccess ||
+      cudaHostAlloc((void **)&b->h_status, (size_t)n_states * 4, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return cleanup(fail(CT_ENOMEM, "pinned host allocation failed"));
+  }
+  b->h.resize(n_states);
+  for (int i = 0; i < n_states; ++i) b->h[i] = make_desc(tb, b->mem + (size_t)i * tb->lay.total);
+  if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
+    return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
+  if (init->stream != tb->stream) cudaStreamSynchronize(init->stream);
+  for (int i = 0; i < n_states; ++i)
+    if (cudaMemcpyAsync(b->mem + (size_t)i * tb->lay.total, init->mem, tb->lay.persist, cudaMemcpyDeviceToDevice,
+                        tb->stream) != cudaSuccess)
+      return cleanup(fail(CT_ECUDA, "batch init copy failed"));
+  tb->live++;
+  *out = b;
+  return CT_OK;
+}
+
+int32_t ct_batch_size(const ct_batch *b) { return b ? b->S : -1; }
+
+ct_status ct_batch_copy(ct_batch *b, int32_t i, const ct_state *src) {
+  if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
+  if (i < 0 || i >= b->S) return fail(CT_EINVAL, "batch index %d out of range", i);
+  DeviceGuard g(b->tb->device);
+  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  CUDA_TRY(cudaMemcpyAsync(b->mem + (size_t)i * b->tb->lay.total, src->mem, b->tb->lay.persist,
+                           cudaMemcpyDeviceToDevice, b->tb->stream));
+  return CT_OK;
+}
+
+ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src) {
+  if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
+  DeviceGuard g(b->tb->device);
+  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  const size_t pitch = b->tb->lay.total;
+  CUDA_TRY(cudaMemcpy2DAsync(b->mem, pitch, src->mem, 0, b->tb->lay.persist, (size_t)b->S,
+                             cudaMemcpyDeviceToDevice, b->tb->stream));
+  return CT_OK;
+}
+
+ct_status ct_propagate_many_async(ct_batch *b, const uint64_t *removed, uint64_t *out_dom, int32_t *out_status) {
+  if (!b) return fail(CT_EINVAL, "NULL batch");
+  ct_table *tb = b->tb;
+  DeviceGuard g(tb->device);
+  CT_TRY(enqueue_local(tb, b->d_desc, b->S, removed, 0, tb->stream));
+  return enqueue_finalize(tb, b->d_desc, b->S, out_dom, nullptr, out_status, 0, tb->stream);
+}
+
+ct_status ct_propagate_many(ct_batch *b, const uint64_t *removed, uint64_t *out_dom, int32_t *out_status) {
+  if (!b || !out_status) return fail(CT_EINVAL, "NULL argument");
+  ct_table *tb = b->tb;
+  DeviceGuard g(tb->device);
+  const size_t io = (size_t)b->S * tb->Wd * 8;
+  if (io) {
+    if (removed) memcpy(b->h_in, removed, io);
+    else memset(b->h_in, 0, io);
+    CUDA_TRY(cudaMemcpyAsync(b->d_in, b->h_in, io, cudaMemcpyHostToDevice, tb->stream));
+  }
+  CT_TRY(ct_propagate_many_async(b, b->d_in, b->d_dom, b->d_status));
+  if (io) CUDA_TRY(cudaMemcpyAsync(b->h_dom, b->d_dom, io, cudaMemcpyDeviceToHost, tb->stream));
+  CUDA_TRY(cudaMemcpyAsync(b->h_status, b->d_status, (size_t)b->S * 4, cudaMemcpyDeviceToHost, tb->stream));
+  CUDA_TRY(cudaStreamSynchronize(tb->stream));
+  memcpy(out_status, b->h_status, (size_t)b->S * 4);
+  if (out_dom && io) {
+    // outputs are written for CT_OK states only (include/ct.h)
+    for (int i = 0; i < b->S; ++i)
+      if (b->h_status[i] == CT_OK)
+        memcpy(out_dom + (size_t)i * tb->Wd, b->h_dom + (size_t)i * tb->Wd, (size_t)tb->Wd * 8);
+  }
+  return CT_OK;
+}
+
+void ct_batch_destroy(ct_batch *b) {
+  if (!b) return;
+  ct_table *tb = b->tb;
+  DeviceGuard g(tb->device);
+  cudaStreamSynchronize(tb->stream);
+  const size_t io = (size_t)b->S * tb->Wd * 8;
+  tb->dfree(b->mem, b->bytes);
+  tb->dfree(b->d_desc, b->desc_bytes);
+  tb->dfree(b->d_in, io);
+  tb->dfree(b->d_dom, io);
+  tb->dfree(b->d_status, (size_t)b->S * 4);
+  cudaFreeHost(b->h_in);
+  cudaFreeHost(b->h_dom);
+  cudaFreeHost(b->h_status);
+  tb->live--;
+  delete b;
+}
+
+// ------------------------------------------------------------------ introspection
+ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
+  if (!s || !out_bits) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->tb->W) CUDA_TRY(cudaMemcpy(out_bits, s->h.T, (size_t)s->tb->W * 8, cudaMemcpyDeviceToHost));
+  return CT_OK;
+}
+
+ct_status ct_table_read_supports(const ct_table *t, int32_t row, uint64_t *out_bits) {
+  if (!t || !out_bits) return fail(CT_EINVAL, "NULL argument");
+  if (row < 0 || row >= t->R) return fail(CT_EINVAL, "row %d out of range", row);
+  DeviceGuard g(t->device);
+  CUDA_TRY(cudaStreamSynchronize(t->stream));
+  if (t->W) CUDA_TRY(cudaMemcpy(out_bits, t->S + (size_t)row * t->Wp, (size_t)t->W * 8, cudaMemcpyDeviceToHost));
+  return CT_OK;
+}
+
+ct_status ct_state_read_dom(const ct_state *s, uint64_t *out_dom) {
+  if (!s || !out_dom) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->tb->Wd) CUDA_TRY(cudaMemcpy(out_dom, s->h.dom, (size_t)s->tb->Wd * 8, cudaMemcpyDeviceToHost));
+  return CT_OK;
+}
+
+ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
+  if (!s || !o) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  Ctl c;
+  CUDA_TRY(cudaMemcpy(&c, s->h.ctl, sizeof c, cudaMemcpyDeviceToHost));
+  memset(o, 0, sizeof *o);
+  o->calls = c.calls;
+  o->last_status = c.last_status;
+  o->noop = c.noop;
+  o->n_changed = c.ngroups;
+  o->n_update_rows = c.nrows;
+  o->n_filter_items = c.nitems;
+  o->n_residue_miss = c.nscan;
+  o->words_in = c.L_in;
+  o->words_out = c.L_out;
+  return CT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,362 @@
+"""Thin ctypes binding of include/ct.h (libct_b200.so).
+
+Same names as the C ABI; argument marshalling only -- every step of the
+propagation runs in the library's CUDA kernels.  Host buffers are numpy arrays,
+device buffers are torch CUDA tensors (their data_ptr()).  PyTorch supplies the
+device memory (caching-allocator hooks passed as ct_allocator), the CUDA
+stream, and -- for tuple-range sharding -- torch.distributed for broadcasting
+the NCCL unique id.
+
+There is no fallback: if the CUDA library is missing or fails to load, every
+entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libct_b200.so")
+
+CT_OK, CT_FAIL, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE = 0, 1, -1, -2, -3, -4, -5
+CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA = 0, 1, 2
+STATUS_NAMES = {0: "OK", 1: "FAIL", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE"}
+
+
+class CTError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class ct_allocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", ctypes.c_void_p)]
+
+
+class ct_config(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
+                ("alloc", ctypes.POINTER(ct_allocator)),
+                ("n_shards", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p),
+                ("update_policy", ctypes.c_int32), ("use_residues", ctypes.c_int32),
+                ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+
+
+class ct_table_info(ctypes.Structure):
+    _fields_ = [("n_vars", ctypes.c_int32), ("n_rows", ctypes.c_int32), ("dom_words", ctypes.c_int32),
+                ("n_shards", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
+                ("n_tuples", ctypes.c_int64), ("words_total", ctypes.c_int64),
+                ("word_begin", ctypes.c_int64), ("words", ctypes.c_int64),
+                ("row_stride_words", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
+                ("state_bytes", ctypes.c_int64)]
+
+
+class ct_stats(ctypes.Structure):
+    _fields_ = [("calls", ctypes.c_int64), ("last_status", ctypes.c_int32), ("noop", ctypes.c_int32),
+                ("n_changed", ctypes.c_int32), ("n_update_rows", ctypes.c_int32),
+                ("n_filter_items", ctypes.c_int32), ("n_residue_miss", ctypes.c_int32),
+                ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64)]
+
+
+# exported symbol -> (restype, argtypes); the CPU test checks the .so exports all of them
+P = ctypes.c_void_p
+I32, I64 = ctypes.c_int32, ctypes.c_int64
+SIGNATURES = {
+    "ct_config_init": (None, [P]),
+    "ct_create": (I32, [I32, P, P, P, P, I64, P, P, P, P, P]),
+    "ct_table_info_get": (I32, [P, P]),
+    "ct_dom_words": (I32, [P]),
+    "ct_dom_word_offset": (I32, [P, I32]),
+    "ct_propagate": (I32, [P, P, P, P]),
+    "ct_propagate_async": (I32, [P, P, P, P, P]),
+    "ct_propagate_local_async": (I32, [P, P]),
+    "ct_state_flags": (I32, [P, P, P]),
+    "ct_propagate_apply_async": (I32, [P, P, P, P]),
+    "ct_state_clone": (I32, [P, P]),
+    "ct_state_copy": (I32, [P, P]),
+    "ct_state_set_stream": (I32, [P, P]),
+    "ct_state_stream": (P, [P]),
+    "ct_synchronize": (I32, [P]),
+    "ct_state_destroy": (None, [P]),
+    "ct_table_destroy": (None, [P]),
+    "ct_batch_create": (I32, [P, I32, P, P]),
+    "ct_batch_size": (I32, [P]),
+    "ct_batch_copy": (I32, [P, I32, P]),
+    "ct_batch_copy_all": (I32, [P, P]),
+    "ct_propagate_many": (I32, [P, P, P, P]),
+    "ct_propagate_many_async": (I32, [P, P, P, P]),
+    "ct_batch_destroy": (None, [P]),
+    "ct_state_read_table": (I32, [P, P]),
+    "ct_table_read_supports": (I32, [P, I32, P]),
+    "ct_state_read_dom": (I32, [P, P]),
+    "ct_state_stats": (I32, [P, P]),
+    "ct_nccl_unique_id": (I32, [P]),
+    "ct_shard_range": (I32, [I64, I32, I32, P, P]),
+    "ct_last_error": (ctypes.c_char_p, []),
+    "ct_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libct_b200.so (raises if it is missing -- build it with
+    `python -m paper_2507_18413_b200.build` or __graft_entry__.build())."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(f"CUDA library {LIB_PATH} not built; run `python -m paper_2507_18413_b200.build`")
+            L = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                f = getattr(L, name)
+                f.restype = res
+                f.argtypes = args
+            _lib = L
+    return _lib
+
+
+def ct_last_error() -> str:
+    return lib().ct_last_error().decode(errors="replace")
+
+
+def ct_version() -> str:
+    return lib().ct_version().decode()
+
+
+def _check(status: int, allow_fail: bool = True) -> int:
+    if status < 0 or (status == CT_FAIL and not allow_fail):
+        raise CTError(status, ct_last_error())
+    return status
+
+
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dev_ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("device buffers must be contiguous CUDA tensors")
+        return ctypes.c_void_p(t.data_ptr())
+    return ctypes.c_void_p(int(t))
+
+
+# ---------------------------------------------------------------- torch plumbing
+class TorchAllocator:
+    """ct_allocator backed by PyTorch's CUDA caching allocator."""
+
+    def __init__(self, device: int):
+        import torch
+        self.device = device
+        self._live = {}
+
+        def _alloc(nbytes, stream, ctx):
+            try:
+                p = torch.cuda.caching_allocator_alloc(int(nbytes), device=self.device, stream=int(stream or 0))
+                self._live[p] = nbytes
+                return p
+            except Exception:
+                return None
+
+        def _free(ptr, nbytes, stream, ctx):
+            if ptr in self._live:
+                del self._live[ptr]
+                torch.cuda.caching_allocator_delete(ptr)
+
+        self._alloc_fn = _ALLOC_FN(_alloc)
+        self._free_fn = _FREE_FN(_free)
+        self.struct = ct_allocator(self._alloc_fn, self._free_fn, None)
+
+
+def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1, shard_rank: int = 0,
+                nccl_unique_id: bytes | None = None, update_policy: int = CT_POLICY_AUTO,
+                use_residues: bool = True, use_index: bool = True, use_graph: bool = True):
+    cfg = ct_config()
+    lib().ct_config_init(ctypes.byref(cfg))
+    cfg.device = device
+    cfg.stream = stream
+    cfg.alloc = ctypes.pointer(allocator.struct) if allocator is not None else None
+    cfg.n_shards = n_shards
+    cfg.shard_rank = shard_rank
+    keep = None
+    if nccl_unique_id is not None:
+        keep = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
+        cfg.nccl_unique_id = ctypes.cast(keep, ctypes.c_void_p)
+    cfg.update_policy = update_policy
+    cfg.use_residues = int(bool(use_residues))
+    cfg.use_index = int(bool(use_index))
+    cfg.use_graph = int(bool(use_graph))
+    return cfg, keep
+
+
+# ---------------------------------------------------------------- C names
+def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None):
+    """Returns (status, table, root, root_dom).  root_dom: uint64[Wd] or None on FAIL."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.int32)
+    tuples = np.ascontiguousarray(tuples, dtype=np.int32)
+    n = int(d.size)
+    t = int(tuples.shape[0]) if tuples.ndim == 2 else 0
+    wd = int(((d.astype(np.int64) + 63) // 64).sum())
+    out_dom = np.zeros(max(wd, 1), dtype=np.uint64)
+    sc = None if scope is None else np.ascontiguousarray(scope, dtype=np.int32)
+    idom = None if init_dom is None else np.ascontiguousarray(init_dom, dtype=np.uint64)
+    tab, root = ctypes.c_void_p(), ctypes.c_void_p()
+    st = lib().ct_create(n, _np_ptr(sc), _np_ptr(lo), _np_ptr(d), _np_ptr(idom), t,
+                         _np_ptr(tuples) if t else None, ctypes.byref(cfg) if cfg is not None else None,
+                         ctypes.byref(tab), ctypes.byref(root), _np_ptr(out_dom))
+    _check(st)
+    return st, tab, root, (out_dom[:wd] if st == CT_OK else None)
+
+
+def ct_table_info_get(table) -> ct_table_info:
+    info = ct_table_info()
+    _check(lib().ct_table_info_get(table, ctypes.byref(info)))
+    return info
+
+
+def ct_dom_words(table) -> int:
+    return int(lib().ct_dom_words(table))
+
+
+def ct_dom_word_offset(table, i: int) -> int:
+    return int(lib().ct_dom_word_offset(table, i))
+
+
+def ct_propagate(state, removed, out_dom, out_pruned=None) -> int:
+    """Host numpy buffers (uint64[Wd]); returns CT_OK / CT_FAIL (raises on errors,
+    including CT_ESTATE)."""
+    return _check(lib().ct_propagate(state, _np_ptr(removed), _np_ptr(out_dom), _np_ptr(out_pruned)))
+
+
+def ct_propagate_async(state, removed, out_dom=None, out_pruned=None, out_status=None) -> int:
+    """Device tensors; enqueue only."""
+    return _check(lib().ct_propagate_async(state, _dev_ptr(removed), _dev_ptr(out_dom), _dev_ptr(out_pruned),
+                                           _dev_ptr(out_status)), allow_fail=False)
+
+
+def ct_propagate_local_async(state, removed) -> int:
+    return _check(lib().ct_propagate_local_async(state, _dev_ptr(removed)), allow_fail=False)
+
+
+def ct_state_flags(state):
+    """Returns (device pointer int, n_bytes) of the state's R+1 shard flag bytes."""
+    p = ctypes.c_void_p()
+    n = ctypes.c_int32()
+    _check(lib().ct_state_flags(state, ctypes.byref(p), ctypes.byref(n)), allow_fail=False)
+    return int(p.value or 0), int(n.value)
+
+
+def ct_propagate_apply_async(state, out_dom=None, out_pruned=None, out_status=None) -> int:
+    return _check(lib().ct_propagate_apply_async(state, _dev_ptr(out_dom), _dev_ptr(out_pruned),
+                                                 _dev_ptr(out_status)), allow_fail=False)
+
+
+def ct_state_clone(state):
+    out = ctypes.c_void_p()
+    _check(lib().ct_state_clone(state, ctypes.byref(out)), allow_fail=False)
+    return out
+
+
+def ct_state_copy(dst, src) -> None:
+    _check(lib().ct_state_copy(dst, src), allow_fail=False)
+
+
+def ct_state_set_stream(state, stream) -> None:
+    _check(lib().ct_state_set_stream(state, ctypes.c_void_p(int(stream))), allow_fail=False)
+
+
+def ct_state_stream(state) -> int:
+    return int(lib().ct_state_stream(state) or 0)
+
+
+def ct_synchronize(state) -> None:
+    _check(lib().ct_synchronize(state), allow_fail=False)
+
+
+def ct_state_destroy(state) -> None:
+    lib().ct_state_destroy(state)
+
+
+def ct_table_destroy(table) -> None:
+    lib().ct_table_destroy(table)
+
+
+def ct_batch_create(table, n_states: int, init_state):
+    out = ctypes.c_void_p()
+    _check(lib().ct_batch_create(table, n_states, init_state, ctypes.byref(out)), allow_fail=False)
+    return out
+
+
+def ct_batch_size(batch) -> int:
+    return int(lib().ct_batch_size(batch))
+
+
+def ct_batch_copy(batch, index: int, state) -> None:
+    _check(lib().ct_batch_copy(batch, index, state), allow_fail=False)
+
+
+def ct_batch_copy_all(batch, state) -> None:
+    _check(lib().ct_batch_copy_all(batch, state), allow_fail=False)
+
+
+def ct_propagate_many(batch, removed, out_dom, out_status) -> None:
+    _check(lib().ct_propagate_many(batch, _np_ptr(removed), _np_ptr(out_dom), _np_ptr(out_status)),
+           allow_fail=False)
+
+
+def ct_propagate_many_async(batch, removed, out_dom=None, out_status=None) -> None:
+    _check(lib().ct_propagate_many_async(batch, _dev_ptr(removed), _dev_ptr(out_dom), _dev_ptr(out_status)),
+           allow_fail=False)
+
+
+def ct_batch_destroy(batch) -> None:
+    lib().ct_batch_destroy(batch)
+
+
+def ct_state_read_table(state, n_words: int) -> np.ndarray:
+    out = np.zeros(max(n_words, 1), dtype=np.uint64)
+    _check(lib().ct_state_read_table(state, _np_ptr(out)), allow_fail=False)
+    return out[:n_words]
+
+
+def ct_table_read_supports(table, row: int, n_words: int) -> np.ndarray:
+    out = np.zeros(max(n_words, 1), dtype=np.uint64)
+    _check(lib().ct_table_read_supports(table, row, _np_ptr(out)), allow_fail=False)
+    return out[:n_words]
+
+
+def ct_state_read_dom(state, wd: int) -> np.ndarray:
+    out = np.zeros(max(wd, 1), dtype=np.uint64)
+    _check(lib().ct_state_read_dom(state, _np_ptr(out)), allow_fail=False)
+    return out[:wd]
+
+
+def ct_state_stats(state) -> ct_stats:
+    s = ct_stats()
+    _check(lib().ct_state_stats(state, ctypes.byref(s)), allow_fail=False)
+    return s
+
+
+def ct_shard_range(n_tuples: int, n_shards: int, rank: int):
+    """(word_begin, words) of shard `rank` (host-only; include/ct.h)."""
+    b, w = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().ct_shard_range(n_tuples, n_shards, rank, ctypes.byref(b), ctypes.byref(w)), allow_fail=False)
+    return int(b.value), int(w.value)
+
+
+def ct_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().ct_nccl_unique_id(buf), allow_fail=False)
+    return buf.raw

@@ -1,0 +1,407 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact.
+
+Run on a B200 with `python -m pytest tests -m gpu`.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+from ctharness import check_root, oracle_call, run_walk
+from golden_io import load_table1, member_from_lists
+from paper_2507_18413_b200 import (CT_OK, CT_FAIL, CT_ESTATE, CT_POLICY_AUTO, CT_POLICY_DOM,
+                                   CT_POLICY_DELTA, CTError, Table)
+from paper_2507_18413_b200 import ct as C
+from workloads import (Rng, random_table, banded_table, table1, member_to_bitmap, bitmap_to_member,
+                       bulk_removal, fix_one_value_removal)
+from workloads.layout import bits_to_bool, dom_word_offsets
+
+pytestmark = pytest.mark.gpu
+
+KNOBS = [
+    dict(),
+    dict(update_policy=CT_POLICY_DOM),
+    dict(update_policy=CT_POLICY_DELTA),
+    dict(use_residues=False),
+    dict(use_index=False),
+    dict(use_graph=False),
+]
+KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2507_18413_b200 import build
+    build.build()
+    import torch
+    assert torch.cuda.is_available()
+
+
+def make(p, **kw):
+    return Table(p.lo, p.d, p.tuples, **kw)
+
+
+# --------------------------------------------------------------------------- a1 supports builder
+def test_supports_table1_printed_rows():
+    T1 = load_table1()
+    p = table1()
+    tab = make(p)
+    rb = np.concatenate([[0], np.cumsum(p.d)])
+    for (i, v), bits in T1["supports"].items():
+        row = rb[i] + v - p.lo[i]
+        got = bits_to_bool(C.ct_table_read_supports(tab.handle, int(row), 1), p.t)
+        assert np.array_equal(got, bits), (i, v)
+    tab.close()
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 1, 200), (4, 70, -3, 1000), (2, 130, 7, 4097), (6, 1, 0, 64)])
+def test_supports_random_vs_definition(shape):
+    n, d, lo, t = shape
+    p = random_table(n, d + 2, t, seed=11, lo=lo - 1)        # values in [lo-1, lo+d]: some out of range
+    p.lo[:] = lo
+    p.d[:] = d
+    tab = make(p)
+    W = (t + 63) // 64
+    for i in range(n):
+        for a in range(d):
+            row = i * d + a
+            got = C.ct_table_read_supports(tab.handle, row, W)
+            exp = oracle.supports_row(p.tuples, i, lo + a)
+            assert np.array_equal(bits_to_bool(got, t), exp)
+            if t % 64:
+                assert int(got[-1]) >> (t % 64) == 0          # padding bits stay 0
+    tab.close()
+
+
+# --------------------------------------------------------------------------- Table 1
+def test_table1_root_and_currtable():
+    T1 = load_table1()
+    p = table1()
+    tab = make(p)
+    check_root(tab, p)
+    assert bitmap_to_member(tab.root_dom, p.d).tolist() == [1, 1, 1, 0, 1, 1, 1, 1, 1, 0, 1, 0]
+    st = tab.root.clone()
+    rem = member_from_lists(p.lo, p.d, [[2, 3], [], []])     # dom(x1) -> {1}
+    status, dom, pr = st.propagate(member_to_bitmap(rem, p.d))
+    assert status == CT_OK
+    assert np.array_equal(bits_to_bool(st.read_table(), 5), T1["currtable"])
+    assert bitmap_to_member(dom, p.d).tolist() == [1, 0, 0, 0, 0, 1, 0, 1, 1, 0, 1, 0]
+    tab.close()
+
+
+@pytest.mark.parametrize("knobs", KNOBS, ids=KNOB_IDS)
+def test_table1_exhaustive_4096(knobs):
+    """Every domain state of Table 1 (16^3), from the root, vs the oracle."""
+    p = table1()
+    tab = make(p, **knobs)
+    st = tab.root.clone()
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    for bits in itertools.product(range(16), repeat=3):
+        D = np.array([(b >> k) & 1 for b in bits for k in range(4)], np.uint8)
+        ok, dout, valid = oracle_call(p, D, want_valid=True)
+        rem = (1 - D).astype(np.uint8)
+        status, dom, pr = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL), bits
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout), bits
+            assert np.array_equal(bitmap_to_member(pr, p.d), (D & root_m) & (1 - dout)), bits
+            assert np.array_equal(bits_to_bool(st.read_table(), 5), valid), bits
+        st.copy_from(tab.root)
+    tab.close()
+
+
+# --------------------------------------------------------------------------- random walks
+@pytest.mark.parametrize("knobs", KNOBS, ids=KNOB_IDS)
+def test_walk_small_random(knobs):
+    p = random_table(5, 12, 3000, seed=21, lo=-4)
+    tab = make(p, **knobs)
+    nfail, nsolved = run_walk(tab, p, calls=250, seed=5, check_table_every=7)
+    assert nfail + nsolved > 0
+    tab.close()
+
+
+@pytest.mark.parametrize("shape", [(1, 9, 40), (2, 70, 700), (3, 130, 5000), (8, 3, 64), (4, 20, 4096 * 5 + 17)])
+def test_walk_shapes(shape):
+    """Edge shapes: arity 1 and 2, domains > 64 values (multi-word), t = 64, ragged t."""
+    n, d, t = shape
+    p = random_table(n, d, t, seed=n * 1000 + d)
+    tab = make(p)
+    run_walk(tab, p, calls=120, seed=3, check_table_every=5)
+    tab.close()
+
+
+def test_walk_config2_full():
+    """BASELINE config 2: arity 5, domain 20, 1e5 tuples, 1000 random-removal calls."""
+    p = random_table(5, 20, 100_000, seed=1)
+    tab = make(p)
+    nfail, nsolved = run_walk(tab, p, calls=1000, seed=2, check_table_every=50)
+    assert nfail > 0 and nsolved > 0
+    tab.close()
+
+
+def test_banded_walk():
+    p = banded_table(5, 30, 20000, seed=4)
+    tab = make(p)
+    run_walk(tab, p, calls=200, seed=8, check_table_every=10, m=1, q=0.8)
+    tab.close()
+
+
+# --------------------------------------------------------------------------- C3 at full size (sampled)
+@pytest.fixture(scope="module")
+def c3():
+    return random_table(8, 100, 10_000_000, seed=3)
+
+
+def test_config3_bulk_full_size(c3):
+    """BASELINE config 3 (1e7 tuples, ~1 GB supports) in the bench's launch
+    configuration: root, then bulk calls from the root, each vs the oracle
+    (domains, pruned set and the full currTable)."""
+    p = c3
+    tab = make(p)
+    check_root(tab, p)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rng = Rng(11)
+    st = tab.root.clone()
+    out_dev_checked = False
+    for k in range(3):
+        rem = bulk_removal(rng, root_m, p.d, q=0.5)
+        din = root_m & (1 - rem)
+        ok, dout, valid = oracle_call(p, din, want_valid=True)
+        st.copy_from(tab.root)
+        status, dom, pr = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL)
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout)
+            assert np.array_equal(bits_to_bool(st.read_table(), p.t), valid)
+        if not out_dev_checked:
+            # the device-buffer entry point gives the same answer
+            import torch
+            wd = tab.Wd
+            st.copy_from(tab.root)
+            remd = torch.from_numpy(member_to_bitmap(rem, p.d).view(np.int64)).cuda()
+            outd = torch.zeros(wd, dtype=torch.int64, device="cuda")
+            sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+            st.propagate_async(remd, outd, None, sd)
+            st.synchronize()
+            assert int(sd.item()) == (CT_OK if ok else CT_FAIL)
+            if ok:
+                assert np.array_equal(bitmap_to_member(outd.cpu().numpy().view(np.uint64), p.d), dout)
+            out_dev_checked = True
+    # a few walk calls continuing from the last bulk state
+    st.close()
+    tab.close()
+
+
+def test_config3b_banded_filter_heavy():
+    p = banded_table(8, 100, 2_000_000, seed=4)
+    tab = make(p)
+    check_root(tab, p)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rng = Rng(12)
+    st = tab.root.clone()
+    for k in range(3):
+        rem = fix_one_value_removal(rng, root_m, p.d, var=0)
+        ok, dout, _ = oracle_call(p, root_m & (1 - rem))
+        st.copy_from(tab.root)
+        status, dom, _ = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL)
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout)
+        s = st.stats()
+        assert s.n_residue_miss > 0          # this workload exercises the full scans
+    st.close()
+    tab.close()
+
+
+# --------------------------------------------------------------------------- edge cases
+def test_empty_table_root_fail():
+    tab = Table([0, 0], [3, 3], np.zeros((0, 2), np.int32))
+    assert tab.root_status == CT_FAIL and tab.root_dom is None
+    with pytest.raises(CTError) as e:
+        tab.root.propagate(None)
+    assert e.value.status == CT_ESTATE
+    tab.close()
+
+
+def test_all_tuples_out_of_range_root_fail():
+    tab = Table([0], [4], np.array([[7], [-1], [4]], np.int32))
+    assert tab.root_status == CT_FAIL
+    tab.close()
+
+
+def test_init_dom_holes_and_single_tuple():
+    p = random_table(3, 10, 500, seed=9, lo=100)
+    D = (Rng(4).uniform(p.R, 3) > 0).astype(np.uint8)
+    tab = Table(p.lo, p.d, p.tuples, init_dom=member_to_bitmap(D, p.d))
+    ok, dout, _ = oracle_call(p, D)
+    assert (tab.root_status == CT_OK) == ok
+    if ok:
+        assert np.array_equal(bitmap_to_member(tab.root_dom, p.d), dout)
+    tab.close()
+    one = np.array([[5, 6]], np.int32)
+    tab = Table([5, 5], [3, 3], one)
+    assert bitmap_to_member(tab.root_dom, [3, 3]).tolist() == [1, 0, 0, 0, 1, 0]
+    tab.close()
+
+
+def test_noop_idempotence_absent_values_and_garbage_bits():
+    p = random_table(4, 70, 5000, seed=13)
+    tab = make(p)
+    st = tab.root.clone()
+    root = tab.root_dom.copy()
+    status, dom, pr = st.propagate(None)                  # nothing removed -> unchanged
+    assert status == CT_OK and np.array_equal(dom, root) and not pr.any()
+    assert st.stats().noop == 1
+    # bits >= d and already-absent values are ignored (include/ct.h)
+    garbage = np.zeros(tab.Wd, np.uint64)
+    offs = dom_word_offsets(p.d)
+    for i in range(p.n):
+        garbage[offs[i + 1] - 1] = np.uint64(0xFFFFFFFFFFFFFFFF) << np.uint64(70 - 64)
+    status, dom, _ = st.propagate(garbage)
+    assert status == CT_OK and np.array_equal(dom, root)
+    # idempotence after a real removal
+    rem = np.zeros(p.R, np.uint8)
+    rem[3:40] = 1
+    status, d1, _ = st.propagate(member_to_bitmap(rem, p.d))
+    status2, d2, pr2 = st.propagate(member_to_bitmap(rem, p.d))
+    assert status == status2 == CT_OK and np.array_equal(d1, d2) and not pr2.any()
+    tab.close()
+
+
+def test_dead_state_and_restore():
+    p = table1()
+    tab = make(p)
+    st = tab.root.clone()
+    rem = member_from_lists(p.lo, p.d, [[2, 3], [2, 3, 4], []])   # x1={1}, x2={1} -> FAIL
+    status, _, _ = st.propagate(member_to_bitmap(rem, p.d))
+    assert status == CT_FAIL
+    with pytest.raises(CTError) as e:
+        st.propagate(None)
+    assert e.value.status == CT_ESTATE
+    st.copy_from(tab.root)
+    status, dom, _ = st.propagate(None)
+    assert status == CT_OK and np.array_equal(dom, tab.root_dom)
+    tab.close()
+
+
+def test_confluence_two_calls_vs_one():
+    p = random_table(5, 20, 20000, seed=17)
+    tab = make(p)
+    rng = Rng(9)
+    a, b = tab.root.clone(), tab.root.clone()
+    for trial in range(30):
+        r1 = (rng.uniform(p.R, 6) == 0).astype(np.uint8)
+        r2 = (rng.uniform(p.R, 6) == 0).astype(np.uint8)
+        a.copy_from(tab.root)
+        b.copy_from(tab.root)
+        s1, _, _ = a.propagate(member_to_bitmap(r1, p.d))
+        if s1 == CT_OK:
+            s1, da, _ = a.propagate(member_to_bitmap(r2, p.d))
+        s2, db, _ = b.propagate(member_to_bitmap(r1 | r2, p.d))
+        assert s1 == s2
+        if s1 == CT_OK:
+            assert np.array_equal(da, db)
+    tab.close()
+
+
+# --------------------------------------------------------------------------- batched (a9)
+def test_batch_matches_oracle_and_single_state():
+    p = random_table(6, 50, 200_000, seed=5)
+    tab = make(p)
+    S = 96
+    b = tab.batch(S)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    cur = [root_m.copy() for _ in range(S)]
+    rngs = [Rng(1000 + s, lanes=1) for s in range(S)]
+    from workloads.policies import walk_removal
+    for step in range(12):
+        rem = np.zeros((S, tab.Wd), np.uint64)
+        exp = []
+        for s in range(S):
+            r = walk_removal(rngs[s], cur[s], p.d)
+            if r is None:
+                r = np.zeros(p.R, np.uint8)
+            rem[s] = member_to_bitmap(r, p.d)
+            exp.append(oracle_call(p, cur[s] & (1 - r)))
+        status, doms = b.propagate(rem)
+        for s in range(S):
+            ok, dout, _ = exp[s]
+            assert status[s] == (CT_OK if ok else CT_FAIL), (step, s)
+            if ok:
+                assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), (step, s)
+                cur[s] = dout
+            else:
+                b.copy(s, tab.root)
+                cur[s] = root_m.copy()
+    b.close()
+    tab.close()
+
+
+# --------------------------------------------------------------------------- sharded (a10)
+@pytest.mark.parametrize("G", [2, 3, 5])
+def test_virtual_shards_one_gpu(G):
+    """G tuple-range shards on one device, flags OR-combined by the caller."""
+    import torch
+    from paper_2507_18413_b200.sharded import flags_tensor
+    p = random_table(5, 20, 50_000 + 33, seed=23)
+    full = make(p)
+    shards = [make(p, n_shards=G, shard_rank=g) for g in range(G)]
+    root_m = bitmap_to_member(full.root_dom, p.d)
+    for s in shards:
+        assert s.root_status == full.root_status and np.array_equal(s.root_dom, full.root_dom)
+    # the shards tile the table
+    rngs = [C.ct_shard_range(p.t, G, g) for g in range(G)]
+    assert rngs[0][0] == 0 and sum(w for _, w in rngs) == (p.t + 63) // 64
+    states = [s.root.clone() for s in shards]
+    rng = Rng(77)
+    wd = full.Wd
+    cur = root_m.copy()
+    from workloads.policies import walk_removal
+    for k in range(60):
+        r = walk_removal(rng, cur, p.d)
+        if r is None:
+            for st, s in zip(states, shards):
+                st.copy_from(s.root)
+            cur = root_m.copy()
+            continue
+        ok, dout, _ = oracle_call(p, cur & (1 - r))
+        remd = torch.from_numpy(member_to_bitmap(r, p.d).view(np.int64)).cuda()
+        for st in states:
+            C.ct_propagate_local_async(st.handle, remd)
+        for st in states:
+            st.synchronize()
+        fl = [flags_tensor(st.handle) for st in states]
+        comb = torch.stack(fl).amax(dim=0)
+        for f in fl:
+            f.copy_(comb)
+        torch.cuda.synchronize()
+        outs = []
+        for st in states:
+            od = torch.zeros(wd, dtype=torch.int64, device="cuda")
+            sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+            C.ct_propagate_apply_async(st.handle, od, None, sd)
+            st.synchronize()
+            outs.append((int(sd.item()), od.cpu().numpy().view(np.uint64)))
+        for sd, od in outs:
+            assert sd == (CT_OK if ok else CT_FAIL), k
+            if ok:
+                assert np.array_equal(bitmap_to_member(od, p.d), dout), k
+        if ok:
+            cur = dout
+        else:
+            for st, s in zip(states, shards):
+                st.copy_from(s.root)
+            cur = root_m.copy()
+    for s in shards:
+        s.close()
+    full.close()
+
+
+def test_nccl_single_rank_path():
+    """The in-library NCCL combine (all-reduce inside the call) on a 1-rank communicator."""
+    p = random_table(5, 20, 30_000, seed=29)
+    nid = C.ct_nccl_unique_id()
+    tab = make(p, n_shards=1, shard_rank=0, nccl_unique_id=nid)
+    run_walk(tab, p, calls=150, seed=4, check_table_every=10)
+    tab.close()
