@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""Benchmark of the Compact-Table propagation hot path on B200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c3bulk|c4]
+
+Default workload (BASELINE config 3, "c3bulk"): random positive table, arity 8,
+domain 100, 1e7 tuples (1.0 GB of support bitsets); one step = restore the
+root state (device copy) + one ct_propagate of a seeded bulk removal (a random
+50 % of every variable's values), i.e. one pass of every §8(a) row: ingest,
+updateTable (dense, HBM-bound), index compaction, emptiness check, residue
+filter, finalize.  At N > 1 (torchrun) the table is tuple-range sharded over
+the N GPUs and the per-row support flags are OR-combined with an in-library
+NCCL all-reduce inside every step (strong scaling: the table is fixed).
+
+`value` = propagations/s with inputs resident in HBM (device-buffer entry
+point, CUDA events on the library stream, max over ranks).  `e2e` = the same
+metric through the synchronous host-buffer C call ct_propagate (H2D of the
+removal set and D2H of status+domains inside every step).  `roofline` = the
+dominant kernel (k_update): bytes it loads/stores per launch (counted by the
+kernel itself) / its CUDA-event duration, against MEASURED_PEAKS.json's HBM
+copy bandwidth.  `cpu_baseline` = the CPU oracle (oracle/, plain C brute
+force) on the host cores, rank 0 at N = 1 only.  `latency` = p50/p90/p99 of
+ct_propagate on BASELINE config 2 (arity 5, domain 20, 1e5 tuples, 1000
+random-removal calls, policy P(2, 0.5)).
+
+--impl reference times the oracle (the reference arm of this tier) on the same
+workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0   # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: copy_ of 1 Gi bf16)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.2)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workloads
+def c3_problem():
+    from workloads import random_table
+    return random_table(8, 100, 10_000_000, seed=3, name="C3 random n=8 d=100 t=1e7 seed=3")
+
+
+def c2_problem():
+    from workloads import random_table
+    return random_table(5, 20, 100_000, seed=1, name="C2 random n=5 d=20 t=1e5 seed=1")
+
+
+def c4_problem():
+    from workloads import random_table
+    return random_table(6, 50, 1_000_000, seed=5, name="C4 random n=6 d=50 t=1e6 seed=5")
+
+
+def bulk_patterns(root_member, d, count: int, seed: int = 11):
+    from workloads import Rng, bulk_removal
+    rng = Rng(seed)
+    return [bulk_removal(rng, root_member, d, q=0.5) for _ in range(count)]
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    from paper_2507_18413_b200 import CT_OK, Table
+    from paper_2507_18413_b200 import ct as C
+    from paper_2507_18413_b200.sharded import broadcast_nccl_id
+    from workloads import member_to_bitmap, bitmap_to_member
+
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    p = c3_problem()
+    nid = broadcast_nccl_id() if world > 1 else None
+    t0 = time.perf_counter()
+    tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=world, shard_rank=rank, nccl_unique_id=nid)
+    build_s = time.perf_counter() - t0
+    assert tab.root_status == CT_OK
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    P = 16
+    pats = bulk_patterns(root_m, p.d, P)
+    wd = tab.Wd
+    rem_host = np.stack([member_to_bitmap(m, p.d) for m in pats])                 # [P][Wd] uint64
+    rem_dev = torch.from_numpy(rem_host.view(np.int64)).to(f"cuda:{dev}")
+    out_dom = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    out_pr = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+    work = tab.root.clone()
+    stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+
+    def step(k):
+        work.copy_from(tab.root)
+        work.propagate_async(rem_dev[k % P], out_dom, out_pr, status)
+
+    # per-pattern work counters (deterministic; untimed): bytes k_update moves
+    per_pat = []
+    for k in range(P):
+        step(k)
+        s = work.stats()
+        assert s.last_status == CT_OK
+        per_pat.append(dict(L_in=s.words_in, L_out=s.words_out, rows=s.n_update_rows,
+                            loads=s.update_support_words, writes=s.update_table_writes,
+                            scan=s.filter_support_words, miss=s.n_residue_miss))
+    for k in range(args.warmup):
+        step(k)
+    work.synchronize()
+
+    clocks = Clocks(dev)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    C.ct_table_profile(tab.handle, False)
+    clk = clocks.stop()
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
+    value = args.steps / (ms_max / 1e3)
+
+    # roofline of k_update (bytes counted by the kernel: support loads, T read, T writes, index r/w)
+    upd_n, upd_ms = prof["update"]
+    byts = 0
+    for k in range(args.steps):
+        c = per_pat[k % P]
+        byts += 8 * c["loads"] + 16 * c["L_in"] + 16 * c["writes"] + 4 * (c["L_in"] + c["L_out"])
+    upd_bytes_per_launch = byts / max(upd_n, 1)
+    upd_ms_per_launch = upd_ms / max(upd_n, 1)
+    achieved = upd_bytes_per_launch / (upd_ms_per_launch / 1e3) / 1e9
+    peak, peak_src = peaks()
+    model = [16 * c["L_in"] * (c["rows"] + 2) for c in per_pat]                # SURVEY §8(d) B_upd (16-B blocks)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_update_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("workload") == "c3bulk" and tj.get("n_gpus", 1) == world:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    kernel_ms = {k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()}
+    step_ms = ms_max / args.steps
+    launches = sum(v[0] for k, v in prof.items() if k != "combine")
+
+    # ---- e2e: the synchronous host-buffer C call (H2D + D2H inside every step)
+    e2e_steps = max(50, min(args.steps, 400))
+    host_rems = [rem_host[k % P].copy() for k in range(e2e_steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    for k in range(5):
+        work.copy_from(tab.root)
+        work.propagate(host_rems[k])
+    barrier(world)
+    t1 = time.perf_counter()
+    for k in range(e2e_steps):
+        work.copy_from(tab.root)
+        st_, dom_, pr_ = work.propagate(host_rems[k])
+    t2 = time.perf_counter()
+    e2e_s = max_over_ranks(t2 - t1, world)
+    e2e = {"value": e2e_steps / e2e_s, "unit": "propagations/s", "h2d_bytes_per_step": 8 * wd,
+           "d2h_bytes_per_step": 8 * (1 + 2 * wd), "steps": e2e_steps,
+           "api": "ct_propagate (host buffers, pinned staging, CUDA graph, sync)"}
+
+    # ---- p50 latency on config 2 (rank 0, N=1 only; latency-bound, not sharded)
+    latency = None
+    if world == 1 and not args.skip_latency:
+        latency = c2_latency(dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        cpu = cpu_baseline(p, root_m, pats, budget_s=args.cpu_budget)
+
+    tab.close()
+    if rank == 0:
+        line = {
+            "metric": "propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
+            "value": value, "unit": "propagations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded i.i.d. table, workloads/)",
+            "config": {"workload": "c3bulk", "table": "arity 8, domain 100, 1e7 tuples, seed 3",
+                       "step": "state restore (D2D) + ct_propagate_async of a bulk removal (50% of every var)",
+                       "patterns": P, "parallelism": f"tuple-range shards x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (1.0 GB supports streamed each step)",
+                       "build_s": round(build_s, 3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "ctk::k_update",
+                         "bytes_per_launch": upd_bytes_per_launch, "ms_per_launch": upd_ms_per_launch,
+                         "model_bytes_per_launch_full_rows": float(np.mean(model)),
+                         "peak_source": peak_src},
+            "kernel_ms_per_launch": kernel_ms,
+            "update_share_of_step": (upd_ms / max(upd_n, 1)) / step_ms,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "latency": latency,
+            "cpu_baseline": cpu, "workload_counters": per_pat[0],
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def c2_latency(dev):
+    """p50/p90/p99 of ct_propagate (sync, host buffers) on config 2, 1000 calls of P(2,0.5)."""
+    from paper_2507_18413_b200 import CT_OK, Table
+    from workloads import Rng, member_to_bitmap, bitmap_to_member
+    from workloads.policies import walk_removal
+    p = c2_problem()
+    tab = Table(p.lo, p.d, p.tuples, device=dev)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    st = tab.root.clone()
+    rng = Rng(2, lanes=1)
+    cur = root_m.copy()
+    lat = []
+    fails = solved = 0
+    for k in range(1100):
+        rem = walk_removal(rng, cur, p.d)
+        if rem is None:
+            st.copy_from(tab.root)
+            cur = root_m.copy()
+            solved += 1
+            continue
+        bm = member_to_bitmap(rem, p.d)
+        t0 = time.perf_counter()
+        s, dom, _ = st.propagate(bm)
+        t1 = time.perf_counter()
+        if k >= 100:
+            lat.append((t1 - t0) * 1e6)
+        if s == CT_OK:
+            cur = bitmap_to_member(dom, p.d)
+        else:
+            fails += 1
+            st.copy_from(tab.root)
+            cur = root_m.copy()
+    tab.close()
+    lat.sort()
+    q = lambda f: lat[min(len(lat) - 1, int(f * len(lat)))]
+    return {"config": "C2 arity 5, domain 20, 1e5 tuples; policy P(2,0.5)", "calls": len(lat),
+            "p50_us": q(0.5), "p90_us": q(0.9), "p99_us": q(0.99), "fails": fails, "restores_solved": solved,
+            "api": "ct_propagate (host buffers, CUDA graph)"}
+
+
+def cpu_baseline(p, root_m, pats, budget_s=12.0):
+    import oracle
+    oracle.lib()
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s or n == 0:
+        rem = pats[n % len(pats)]
+        oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - rem))
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "propagations/s", "cores": 1, "kind": "oracle",
+            "sample": f"{n} full C3 bulk propagations (oracle/ct_oracle.c brute-force scan of all 1e7 tuples, "
+                      f"single thread) in {dt:.1f} s", "host_nproc": os.cpu_count()}
+
+
+# ---------------------------------------------------------------- reference arm (the oracle)
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    from workloads import bitmap_to_member, full_member
+    oracle.lib()
+    p = c3_problem()
+    ok, root_m, _ = oracle.gac(p.lo, p.d, p.tuples, full_member(p.d))
+    pats = bulk_patterns(root_m, p.d, 16)
+    # one full oracle call costs ~0.1-0.3 s; if K+W of them would exceed ~120 s,
+    # each step runs on a contiguous tuple slice and the rate is scaled by t/slice.
+    t0 = time.perf_counter()
+    oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - pats[0]))
+    est = time.perf_counter() - t0
+    frac = min(1.0, 120.0 / max(1e-9, est * (args.steps + args.warmup)))
+    ts = max(1, int(p.t * frac))
+    tup = p.tuples[:ts]
+    for k in range(args.warmup):
+        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]))
+    t1 = time.perf_counter()
+    for k in range(args.steps):
+        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]))
+    dt = time.perf_counter() - t1
+    value = args.steps / (dt * (p.t / ts))
+    sample = (f"{args.steps} C3 bulk propagations by the CPU oracle over "
+              + ("all 1e7 tuples" if ts == p.t else f"the first {ts} of 1e7 tuples, time scaled by t/{ts} (linear scan)"))
+    line = {"impl": "reference", "metric": "propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
+            "value": value, "unit": "propagations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3 * (p.t / ts), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded i.i.d. table, workloads/)",
+            "config": {"workload": "c3bulk", "table": "arity 8, domain 100, 1e7 tuples, seed 3"},
+            "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "propagations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-latency", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

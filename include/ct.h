@@ -222,10 +222,27 @@ typedef struct ct_stats {
   int32_t n_update_rows;    /* support rows OR-ed by updateTable                       */
   int32_t n_filter_items;   /* (x,a) checked by filterDomains (x in s_sup, L201)       */
   int32_t n_residue_miss;   /* of those, residue probe misses -> index scans           */
-  int64_t words_in;         /* active currTable words before the update (L_in)         */
-  int64_t words_out;        /* active words after the update (L_out)                   */
+  int64_t words_in;         /* index entries before the update (L_in); an entry is a   */
+                            /* 16-byte block (2 currTable words) with a valid tuple    */
+  int64_t words_out;        /* index entries after the update (L_out)                  */
+  int64_t update_support_words;  /* 64-bit support words loaded by updateTable          */
+  int64_t update_table_writes;   /* 16-byte currTable blocks rewritten by updateTable   */
+  int64_t filter_support_words;  /* support words loaded by the filter's index scans    */
 } ct_stats;
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
+
+/* Per-kernel device timing (measurement only).  While enabled, every
+ * *_async / ct_propagate_many call on this table's states and batches records a
+ * CUDA event pair around each of its kernels on the launching stream (not inside
+ * captured graphs).  read() waits for the stream, returns the summed durations
+ * and launch counts since the last reset, and resets them if `reset`.
+ * Kernel slots: 0 ingest, 1 update, 2 probe, 3 scan, 4 combine (NCCL), 5 finalize. */
+typedef struct ct_kernel_times {
+  int64_t launches[6];
+  double ms[6];
+} ct_kernel_times;
+ct_status ct_table_profile(ct_table *t, int32_t enable);
+ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset);
 
 /* Tuple-range partition used by sharded tables (host-only, no device needed):
  * shard `rank` of `n_shards` owns currTable words [*word_begin, *word_begin +

@@ -34,9 +34,10 @@ constexpr int kIngestTPB = 512;
 constexpr int kProbeTPB = 256;
 constexpr int kScanTPB = 256;
 constexpr int kFinTPB = 256;
-constexpr int kScanUnroll = 8;    // words per lane per scan round
-constexpr int kScanRounds = 4;    // rounds per work unit: unit = 32*8*4 = 1024 index entries
-constexpr int kScanChunk = 32 * kScanUnroll * kScanRounds;
+constexpr int kUpdUnroll = 8;     // support rows in flight per thread in k_update
+constexpr int kScanUnroll = 4;    // index entries (16-byte blocks) per lane per scan round
+constexpr int kFirstScan = 32 * kScanUnroll * 2;     // entries k_probe scans itself (2 rounds)
+constexpr int kScanChunk = 32 * kScanUnroll * 8;     // entries per k_scan work unit (8 rounds)
 
 constexpr uint32_t kRowMask = 0x3FFFFFFFu;   // update-list entry: row id
 constexpr uint32_t kEndBit = 1u << 30;        //   last row of its variable's group
@@ -54,10 +55,11 @@ struct TableDev {
   const int32_t *rowVar;    // [R]     var owning each support row
   int32_t n, R, Wd;
   int32_t W;                // currTable words of this shard
+  int32_t W2;               // 16-byte blocks of this shard = ceil(W/2) (index granularity)
   int64_t Wp;               // padded row stride in words (multiple of 16)
   int32_t policy;           // CT_POLICY_*
   int32_t use_res, use_index;
-  int32_t ntiles_max;       // ceil(W / kUpdTPB)
+  int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
 };
 
 // Per-state control block (device).  The first four fields persist across
@@ -66,7 +68,7 @@ struct Ctl {
   int32_t dead;        // 1 after CT_FAIL until restored by a copy
   int32_t parity;      // which index buffer holds the active index
   int32_t identity;    // 1: active index is implicitly 0..L-1 (root, or use_index=0)
-  int32_t L;           // active words
+  int32_t L;           // active 16-byte blocks (index entries)
   long long calls;
   int32_t last_status;
   // ---- per call
@@ -80,7 +82,10 @@ struct Ctl {
   int32_t L_out;       // active words after the update (this shard)
   int32_t tile_ctr;
   int32_t nscan;       // residue misses queued for scanning
-  int32_t pad[15];
+  unsigned long long upd_loads;    // support words loaded by k_update (this call)
+  unsigned long long upd_writes;   // currTable words rewritten by k_update
+  unsigned long long scan_loads;   // support words loaded by k_scan
+  int32_t pad[9];
 };
 static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
 
@@ -114,6 +119,11 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
 __device__ __forceinline__ uint64_t ld_sup(const uint64_t *p) {
   uint64_t v;
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ ulonglong2 ld_sup2(const uint64_t *p) {
+  ulonglong2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -248,6 +258,9 @@ __global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateD
       c->L_out = 0;
       c->tile_ctr = 0;
       c->nscan = 0;
+      c->upd_loads = 0;
+      c->upd_writes = 0;
+      c->scan_loads = 0;
     }
     return;
   }
@@ -313,6 +326,9 @@ __global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateD
     c->L_out = 0;
     c->tile_ctr = 0;
     c->nscan = 0;
+    c->upd_loads = 0;
+    c->upd_writes = 0;
+    c->scan_loads = 0;
   }
 }
 
@@ -348,7 +364,9 @@ __device__ __forceinline__ uint32_t tile_lookback(unsigned long long *ts, int ti
   return excl;
 }
 
-// grid (blocks, S), kUpdTPB threads; persistent over tiles of kUpdTPB active words.
+// grid (blocks, S), kUpdTPB threads; persistent over tiles of kUpdTPB active
+// 16-byte blocks ("pairs" of currTable words; the index is over pairs so every
+// support/currTable access is an aligned 128-bit vector load).
 __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev *__restrict__ states) {
   const StateDev st = states[blockIdx.y];
   Ctl *c = st.ctl;
@@ -372,6 +390,8 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
   const int ntiles = (L + kUpdTPB - 1) / kUpdTPB;
   const int32_t *__restrict__ ulist = st.ulist;
   const int64_t Wp = tb.Wp;
+  ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+  uint32_t n_loads = 0, n_writes = 0;
 
   while (true) {
     if (tid == 0) s_tile = atomicAdd(&c->tile_ctr, 1);
@@ -380,37 +400,54 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
     if (tile >= ntiles) break;
     const int k = tile * kUpdTPB + tid;
     const bool valid = k < L;
-    int w = 0;
-    uint64_t nt = 0;
+    int pid = 0;
+    ulonglong2 nt = make_ulonglong2(0ull, 0ull);
     if (valid) {
-      w = s_ident ? k : idx_in[k];
-      const uint64_t tw = st.T[w];
-      const uint64_t *__restrict__ col = tb.S + w;
-      uint64_t m = ~0ull, acc = 0;
-      for (int p = 0; p < nrows; p += 8) {
-        if ((tw & m) == 0) break;                      // Alg. 2, per word
-        uint32_t e[8];
-        uint64_t v[8];
+      pid = s_ident ? k : idx_in[k];
+      const ulonglong2 tw = T2[pid];
+      const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+      uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+      uint32_t e[kUpdUnroll];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) e[u] = (p + u < nrows) ? (uint32_t)__ldg(ulist + p + u) : 0u;
+      for (int u = 0; u < kUpdUnroll; ++u) e[u] = (u < nrows) ? (uint32_t)__ldg(ulist + u) : 0u;
+      for (int p = 0; p < nrows; p += kUpdUnroll) {
+        if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 128-bit block
+        ulonglong2 v[kUpdUnroll];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          v[u] = (p + u < nrows) ? ld_sup(col + (int64_t)(e[u] & kRowMask) * Wp) : 0ull;
+        for (int u = 0; u < kUpdUnroll; ++u)
+          v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
+        n_loads += 2 * min(kUpdUnroll, nrows - p);
+        uint32_t en[kUpdUnroll];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kUpdUnroll; ++u)
+          en[u] = (p + kUpdUnroll + u < nrows) ? (uint32_t)__ldg(ulist + p + kUpdUnroll + u) : 0u;
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u) {
           if (p + u < nrows) {
-            acc |= v[u];
+            ax |= v[u].x;
+            ay |= v[u].y;
             if (e[u] & kEndBit) {
-              m &= (e[u] & kInvBit) ? ~acc : acc;
-              acc = 0;
+              if (e[u] & kInvBit) {
+                mx &= ~ax;
+                my &= ~ay;
+              } else {
+                mx &= ax;
+                my &= ay;
+              }
+              ax = ay = 0;
             }
           }
         }
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u) e[u] = en[u];
       }
-      nt = tw & m;
-      if (nt != tw) st.T[w] = nt;
+      nt = make_ulonglong2(tw.x & mx, tw.y & my);
+      if (nt.x != tw.x || nt.y != tw.y) {
+        T2[pid] = nt;
+        ++n_writes;
+      }
     }
-    const bool keep = valid && nt != 0;
+    const bool keep = valid && (nt.x | nt.y) != 0;
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) s_woff[warp] = __popc(bal);
     __syncthreads();
@@ -434,34 +471,108 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
       if (lane == 0) s_excl = excl;
     }
     __syncthreads();
-    if (compact && keep) idx_out[s_excl + s_woff[warp] + __popc(bal & lanemask_lt())] = w;
+    if (compact && keep) idx_out[s_excl + s_woff[warp] + __popc(bal & lanemask_lt())] = pid;
+  }
+  n_loads = warp_sum_u32(n_loads);
+  n_writes = warp_sum_u32(n_writes);
+  if (lane == 0 && (n_loads | n_writes)) {
+    atomicAdd(&c->upd_loads, (unsigned long long)n_loads);
+    atomicAdd(&c->upd_writes, (unsigned long long)n_writes);
   }
 }
 
 // ------------------------------------------------------------------ a6: filter
-// grid (ceil(R / kProbeTPB), S): residue probe, one thread per (x,a) item.
+// Warp-cooperative intersect of support row `srow` with currTable over index
+// entries [k0, k1) (Alg. 3 L3 "currTable & supports[x,a] != 0", residue-style
+// intersectIndex of CT): kScanUnroll pairs per lane per round, one
+// __ballot_sync "any" per pair.  Returns the first (lowest-entry) pair with a
+// common valid tuple, -1 if none, -2 if `supflag` was set by another warp.
+__device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const ulonglong2 *__restrict__ T2,
+                                          const uint64_t *__restrict__ srow, int k0, int k1,
+                                          const uint8_t *supflag, int lane, uint32_t &n_loads) {
+  for (int kb = k0; kb < k1; kb += 32 * kScanUnroll) {
+    if (supflag && kb != k0) {
+      const int f = lane == 0 ? *(volatile const uint8_t *)supflag : 0;
+      if (__shfl_sync(0xffffffffu, f, 0)) return -2;
+    }
+    int pid[kScanUnroll];
+    uint64_t v[kScanUnroll];
+#pragma unroll
+    for (int q = 0; q < kScanUnroll; ++q) {
+      const int k = kb + q * 32 + lane;
+      pid[q] = k < k1 ? (idx ? __ldg(idx + k) : k) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < kScanUnroll; ++q) {
+      if (pid[q] >= 0) {
+        const ulonglong2 t = T2[pid[q]];
+        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)pid[q]);
+        v[q] = (t.x & s.x) | (t.y & s.y);
+      } else {
+        v[q] = 0;
+      }
+    }
+    n_loads += 2 * min(32 * kScanUnroll, k1 - kb);
+    int hit = -1;
+#pragma unroll
+    for (int q = kScanUnroll - 1; q >= 0; --q) {
+      const unsigned b = __ballot_sync(0xffffffffu, v[q] != 0);
+      if (b) hit = __shfl_sync(0xffffffffu, pid[q], __ffs(b) - 1);
+    }
+    if (hit >= 0) return hit;
+  }
+  return -1;
+}
+
+// grid (ceil(R / warps per block), S): one warp per (x,a) item, x in s_sup:
+// residue probe, then the first kFirstScan index entries; the
+// items still unsupported go to the scan list for k_scan.
 __global__ void __launch_bounds__(kProbeTPB) k_probe(TableDev tb, const StateDev *__restrict__ states) {
   const StateDev st = states[blockIdx.y];
-  const Ctl *c = st.ctl;
+  Ctl *c = st.ctl;
   if (c->skip | c->noop | c->fail_fast) return;
   const int Lout = c->L_out;
   if (blockIdx.x == 0 && threadIdx.x == 0) st.sup[tb.R] = Lout > 0;
   if (Lout == 0) return;
-  const int i = blockIdx.x * kProbeTPB + threadIdx.x;
-  if (i >= c->nitems) return;
-  const int row = st.items[i];
+  const int lane = threadIdx.x & 31;
+  const int item = blockIdx.x * (kProbeTPB / 32) + (threadIdx.x >> 5);
+  if (item >= c->nitems) return;
+  const int row = st.items[item];
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
   if (tb.use_res) {
-    const int r = st.res[row];
-    if (st.T[r] & tb.S[(int64_t)row * tb.Wp + r]) {
-      st.sup[row] = 1;
+    int hit = 0;
+    if (lane == 0) {
+      const int r = st.res[row];
+      const ulonglong2 t = T2[r];
+      const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
+      hit = ((t.x & s.x) | (t.y & s.y)) != 0;
+    }
+    if (__shfl_sync(0xffffffffu, hit, 0)) {
+      if (lane == 0) st.sup[row] = 1;
       return;
     }
   }
-  const int pos = atomicAdd(&st.ctl->nscan, 1);
-  st.scanlist[pos] = row;
+  const bool compact = tb.use_index != 0;
+  const int32_t *__restrict__ idx = compact ? (c->parity ? st.idx0 : st.idx1) : nullptr;
+  const int L = compact ? Lout : tb.W2;
+  uint32_t n_loads = 0;
+  const int hit = scan_pairs(idx, T2, srow, 0, min(L, kFirstScan), nullptr, lane, n_loads);
+  if (lane == 0) {
+    if (hit >= 0) {
+      st.sup[row] = 1;
+      st.res[row] = hit;
+    } else if (L > kFirstScan) {
+      st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+    }
+    atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
+  }
 }
 
-// grid (blocks, S), kScanTPB threads: one warp per (miss, chunk) unit, chunk-major.
+// grid (blocks, S), kScanTPB threads: the items k_probe left unresolved, over
+// index entries [kFirstScan, L) in chunks of kScanChunk; one warp per
+// (item, chunk) unit, chunk-major so early chunks of every item go first, and
+// every round re-checks the item's flag so late chunks stop once any chunk hit.
 __global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *__restrict__ states) {
   const StateDev st = states[blockIdx.y];
   const Ctl *c = st.ctl;
@@ -470,47 +581,30 @@ __global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *
   const int Lout = c->L_out;
   if (nscan == 0 || Lout == 0) return;
   const bool compact = tb.use_index != 0;
-  // the index written by this call's update lives in the other buffer
   const int32_t *__restrict__ idx = compact ? (c->parity ? st.idx0 : st.idx1) : nullptr;
-  const int L = compact ? Lout : tb.W;
+  const int L = compact ? Lout : tb.W2;
+  if (L <= kFirstScan) return;
   const int lane = threadIdx.x & 31;
-  const int64_t nch = (L + kScanChunk - 1) / kScanChunk;
+  const int64_t nch = (L - kFirstScan + kScanChunk - 1) / kScanChunk;
   const int64_t total = nch * nscan;
   const int64_t nw = (int64_t)gridDim.x * (kScanTPB / 32);
-  const uint64_t *__restrict__ T = st.T;
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  uint32_t n_loads = 0;
   for (int64_t u = (int64_t)blockIdx.x * (kScanTPB / 32) + (threadIdx.x >> 5); u < total; u += nw) {
     const int chunk = (int)(u / nscan);
     const int item = (int)(u - (int64_t)chunk * nscan);
     const int row = st.scanlist[item];
-    if (*(volatile const uint8_t *)(st.sup + row)) continue;
-    const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
-    const int k0 = chunk * kScanChunk;
+    int f = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
+    if (__shfl_sync(0xffffffffu, f, 0)) continue;
+    const int k0 = kFirstScan + chunk * kScanChunk;
     const int k1 = min(k0 + kScanChunk, L);
-    for (int kb = k0; kb < k1; kb += 32 * kScanUnroll) {
-      int w[kScanUnroll];
-      uint64_t v[kScanUnroll];
-#pragma unroll
-      for (int q = 0; q < kScanUnroll; ++q) {
-        const int k = kb + q * 32 + lane;
-        w[q] = k < k1 ? (compact ? __ldg(idx + k) : k) : -1;
-      }
-#pragma unroll
-      for (int q = 0; q < kScanUnroll; ++q) v[q] = w[q] >= 0 ? (T[w[q]] & ld_sup(srow + w[q])) : 0ull;
-      int hitw = -1;
-#pragma unroll
-      for (int q = kScanUnroll - 1; q >= 0; --q) {
-        const unsigned b = __ballot_sync(0xffffffffu, v[q] != 0);
-        if (b) hitw = __shfl_sync(0xffffffffu, w[q], __ffs(b) - 1);
-      }
-      if (hitw >= 0) {
-        if (lane == 0) {
-          st.sup[row] = 1;
-          st.res[row] = hitw;
-        }
-        break;
-      }
+    const int hit = scan_pairs(idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, st.sup + row, lane, n_loads);
+    if (hit >= 0 && lane == 0) {
+      st.sup[row] = 1;
+      st.res[row] = hit;
     }
   }
+  if (lane == 0 && n_loads) atomicAdd(&st.ctl->scan_loads, (unsigned long long)n_loads);
 }
 
 // grid (1, S), kFinTPB threads.  Writes the per-state status and outputs.

@@ -95,6 +95,12 @@ struct ct_table {
   TableDev dev{};
   StateLayout lay{};
   int sm_count = 148;
+  // per-kernel event timing (ct_table_profile)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  struct Mark { int kid, e0, e1; };
+  std::vector<Mark> marks;
   int upd_occ = 1, scan_occ = 1;
   int live = 0;   // states + batches alive
 
@@ -153,8 +159,8 @@ static StateLayout make_layout(const ct_table *tb) {
   const int ntiles = tb->dev.ntiles_max;
   L.ctl = take(256);
   L.T = take(tb->Wp * 8);
-  L.idx0 = take(tb->Wp * 4);
-  L.idx1 = take(tb->Wp * 4);
+  L.idx0 = take(tb->Wp / 2 * 4);   // index over 16-byte blocks
+  L.idx1 = take(tb->Wp / 2 * 4);
   L.res = take((size_t)tb->R * 4);
   L.dom = take((size_t)tb->Wd * 8);
   L.persist = o;
@@ -193,6 +199,26 @@ static StateDev make_desc(const ct_table *tb, char *mem) {
   return s;
 }
 
+// ------------------------------------------------------------------ profiling
+static int prof_event(ct_table *tb, cudaStream_t st) {
+  if (!tb->prof_on) return -1;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return -1;
+  if (tb->ev_used == tb->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return -1;
+    tb->ev_pool.push_back(e);
+  }
+  const int i = (int)tb->ev_used++;
+  cudaEventRecord(tb->ev_pool[i], st);
+  return i;
+}
+static void prof_mark(ct_table *tb, int kid, int e0, cudaStream_t st) {
+  if (e0 < 0) return;
+  const int e1 = prof_event(tb, st);
+  if (e1 >= 0) tb->marks.push_back({kid, e0, e1});
+}
+
 // ------------------------------------------------------------------ launch helpers
 static int update_blocks(const ct_table *tb, int S) {
   const int resident = tb->sm_count * tb->upd_occ;
@@ -208,25 +234,40 @@ static int scan_blocks(const ct_table *tb, int S) {
 // a2-a6 on S states (everything before the cross-shard combine).
 static ct_status enqueue_local(ct_table *tb, const StateDev *d_desc, int S, const uint64_t *removed,
                                int root_mode, cudaStream_t st) {
+  int e = prof_event(tb, st);
   k_ingest<<<dim3(1, S), kIngestTPB, 0, st>>>(tb->dev, d_desc, removed, tb->Wd, root_mode);
+  prof_mark(tb, 0, e, st);
+  e = prof_event(tb, st);
   k_update<<<dim3(update_blocks(tb, S), S), kUpdTPB, 0, st>>>(tb->dev, d_desc);
-  k_probe<<<dim3((unsigned)std::max(1, (tb->R + kProbeTPB - 1) / kProbeTPB), S), kProbeTPB, 0, st>>>(
+  prof_mark(tb, 1, e, st);
+  e = prof_event(tb, st);
+  constexpr int kProbeWarps = kProbeTPB / 32;
+  k_probe<<<dim3((unsigned)std::max(1, (tb->R + kProbeWarps - 1) / kProbeWarps), S), kProbeTPB, 0, st>>>(
       tb->dev, d_desc);
+  prof_mark(tb, 2, e, st);
+  e = prof_event(tb, st);
   k_scan<<<dim3(scan_blocks(tb, S), S), kScanTPB, 0, st>>>(tb->dev, d_desc);
+  prof_mark(tb, 3, e, st);
   CUDA_TRY(cudaGetLastError());
   return CT_OK;
 }
 
 static ct_status enqueue_combine(ct_table *tb, const StateDev &h, cudaStream_t st) {
-  if (tb->comm) NCCL_TRY(ncclAllReduce(h.sup, h.sup, (size_t)tb->R + 1, ncclUint8, ncclMax, tb->comm, st));
+  if (tb->comm) {
+    const int e = prof_event(tb, st);
+    NCCL_TRY(ncclAllReduce(h.sup, h.sup, (size_t)tb->R + 1, ncclUint8, ncclMax, tb->comm, st));
+    prof_mark(tb, 4, e, st);
+  }
   return CT_OK;
 }
 
 static ct_status enqueue_finalize(ct_table *tb, const StateDev *d_desc, int S, uint64_t *out_dom,
                                   uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                   cudaStream_t st) {
+  const int e = prof_event(tb, st);
   k_finalize<<<dim3(1, S), kFinTPB, 0, st>>>(tb->dev, d_desc, out_dom, tb->Wd, out_pruned, out_status,
                                              use_state_out);
+  prof_mark(tb, 5, e, st);
   CUDA_TRY(cudaGetLastError());
   return CT_OK;
 }
@@ -295,6 +336,7 @@ static void free_table(ct_table *tb) {
   DeviceGuard g(tb->device);
   if (tb->stream) cudaStreamSynchronize(tb->stream);
   if (tb->comm) ncclCommDestroy(tb->comm);
+  for (cudaEvent_t e : tb->ev_pool) cudaEventDestroy(e);
   if (tb->S) tb->dfree(tb->S, tb->S_bytes);
   if (tb->meta) tb->dfree(tb->meta, tb->meta_bytes);
   if (tb->own_stream && tb->stream) cudaStreamDestroy(tb->stream);
@@ -468,11 +510,12 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   dv.R = tb->R;
   dv.Wd = tb->Wd;
   dv.W = (int32_t)tb->W;
+  dv.W2 = (int32_t)((tb->W + 1) / 2);
   dv.Wp = tb->Wp;
   dv.policy = tb->policy;
   dv.use_res = tb->use_res;
   dv.use_index = tb->use_index;
-  dv.ntiles_max = (int32_t)((tb->W + kUpdTPB - 1) / kUpdTPB);
+  dv.ntiles_max = (int32_t)((dv.W2 + kUpdTPB - 1) / kUpdTPB);
   tb->lay = make_layout(tb);
 
   // ---------------- root state + supports (a1)
@@ -498,7 +541,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
     if (e != cudaSuccess) return fail(CT_ECUDA, "supports build failed: %s", cudaGetErrorString(e));
   }
   Ctl c0{};
-  c0.L = (int32_t)tb->W;
+  c0.L = tb->dev.W2;
   c0.identity = 1;
   CUDA_TRY(cudaMemcpyAsync(root->h.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice, tb->stream));
   if (tb->Wd)
@@ -867,6 +910,33 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
   o->n_residue_miss = c.nscan;
   o->words_in = c.L_in;
   o->words_out = c.L_out;
+  o->update_support_words = (int64_t)c.upd_loads;
+  o->update_table_writes = (int64_t)c.upd_writes;
+  o->filter_support_words = (int64_t)c.scan_loads;
+  return CT_OK;
+}
+
+ct_status ct_table_profile(ct_table *t, int32_t enable) {
+  if (!t) return fail(CT_EINVAL, "NULL table");
+  t->prof_on = enable != 0;
+  return CT_OK;
+}
+
+ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset) {
+  if (!t || !out) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(t->device);
+  memset(out, 0, sizeof *out);
+  CUDA_TRY(cudaDeviceSynchronize());
+  for (const auto &m : t->marks) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, t->ev_pool[m.e0], t->ev_pool[m.e1]));
+    out->launches[m.kid] += 1;
+    out->ms[m.kid] += ms;
+  }
+  if (reset) {
+    t->marks.clear();
+    t->ev_used = 0;
+  }
   return CT_OK;
 }
 

@@ -62,7 +62,16 @@ class ct_stats(ctypes.Structure):
     _fields_ = [("calls", ctypes.c_int64), ("last_status", ctypes.c_int32), ("noop", ctypes.c_int32),
                 ("n_changed", ctypes.c_int32), ("n_update_rows", ctypes.c_int32),
                 ("n_filter_items", ctypes.c_int32), ("n_residue_miss", ctypes.c_int32),
-                ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64)]
+                ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64),
+                ("update_support_words", ctypes.c_int64), ("update_table_writes", ctypes.c_int64),
+                ("filter_support_words", ctypes.c_int64)]
+
+
+class ct_kernel_times(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6)]
+
+
+KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize")
 
 
 # exported symbol -> (restype, argtypes); the CPU test checks the .so exports all of them
@@ -99,6 +108,8 @@ SIGNATURES = {
     "ct_state_stats": (I32, [P, P]),
     "ct_nccl_unique_id": (I32, [P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
+    "ct_table_profile": (I32, [P, I32]),
+    "ct_table_profile_read": (I32, [P, P, I32]),
     "ct_last_error": (ctypes.c_char_p, []),
     "ct_version": (ctypes.c_char_p, []),
 }
@@ -347,6 +358,17 @@ def ct_state_stats(state) -> ct_stats:
     s = ct_stats()
     _check(lib().ct_state_stats(state, ctypes.byref(s)), allow_fail=False)
     return s
+
+
+def ct_table_profile(table, enable: bool) -> None:
+    _check(lib().ct_table_profile(table, int(bool(enable))), allow_fail=False)
+
+
+def ct_table_profile_read(table, reset: bool = True) -> dict:
+    """{kernel: (launches, total_ms)} since the last reset."""
+    kt = ct_kernel_times()
+    _check(lib().ct_table_profile_read(table, ctypes.byref(kt), int(bool(reset))), allow_fail=False)
+    return {name: (int(kt.launches[i]), float(kt.ms[i])) for i, name in enumerate(KERNEL_SLOTS)}
 
 
 def ct_shard_range(n_tuples: int, n_shards: int, rank: int):

@@ -1,0 +1,10 @@
+set -x
+nproc
+timeout 600 python bench.py --steps 300 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
+tail -5 gpurun_out/bench.err
+cat gpurun_out/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --skip-cpu --skip-latency > gpurun_out/ncu_bench.log 2>&1
+tail -3 gpurun_out/ncu_bench.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_update -s 20 -c 2 -o gpurun_out/prof_update python bench.py --steps 5 --warmup 3 --skip-cpu --skip-latency > gpurun_out/ncu_full.log 2>&1
+tail -3 gpurun_out/ncu_full.log
+ls -la gpurun_out
