@@ -94,10 +94,13 @@ typedef struct ct_config {
   int32_t use_residues;       /* 1: probe residue word first in filter (L220)            */
   int32_t use_index;          /* 1: keep the compacted non-zero-word index (RSparseBitSet)*/
   int32_t use_graph;          /* 1: synchronous calls replay a captured CUDA graph      */
+  int32_t use_fused;          /* 1: a single-state call is one cooperative persistent   */
+                              /*    kernel (software grid barriers between phases);     */
+                              /*    0: one kernel per phase                              */
 } ct_config;
 
 /* Fill *cfg with defaults: device 0, NULL stream, default allocator, 1 shard,
- * CT_POLICY_AUTO, residues, index and graphs on. */
+ * CT_POLICY_AUTO, residues, index, graphs and the fused kernel on. */
 void ct_config_init(ct_config *cfg);
 
 /* ---------------------------------------------------------------- creation */
@@ -228,6 +231,8 @@ typedef struct ct_stats {
   int64_t update_support_words;  /* 64-bit support words loaded by updateTable          */
   int64_t update_table_writes;   /* 16-byte currTable blocks rewritten by updateTable   */
   int64_t filter_support_words;  /* support words loaded by the filter's index scans    */
+  int64_t phase_ns[5];      /* fused kernel only: device time of ingest, update, probe,  */
+                            /* scan, finalize in the last call (%globaltimer), else 0    */
 } ct_stats;
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
 
@@ -236,10 +241,11 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *out);
  * CUDA event pair around each of its kernels on the launching stream (not inside
  * captured graphs).  read() waits for the stream, returns the summed durations
  * and launch counts since the last reset, and resets them if `reset`.
- * Kernel slots: 0 ingest, 1 update, 2 probe, 3 scan, 4 combine (NCCL), 5 finalize. */
+ * Kernel slots: 0 ingest, 1 update, 2 probe, 3 scan, 4 combine (NCCL), 5 finalize,
+ * 6 fused (all phases of a single-state call in one kernel), 7 unused. */
 typedef struct ct_kernel_times {
-  int64_t launches[6];
-  double ms[6];
+  int64_t launches[8];
+  double ms[8];
 } ct_kernel_times;
 ct_status ct_table_profile(ct_table *t, int32_t enable);
 ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset);

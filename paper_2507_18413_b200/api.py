@@ -23,7 +23,7 @@ class Table:
     def __init__(self, lo, d, tuples, init_dom=None, scope=None, device: int = 0, stream=None,
                  torch_alloc: bool = True, n_shards: int = 1, shard_rank: int = 0, nccl_unique_id=None,
                  update_policy: int = C.CT_POLICY_AUTO, use_residues: bool = True, use_index: bool = True,
-                 use_graph: bool = True):
+                 use_graph: bool = True, use_fused: bool = True):
         import torch
         self.device = int(device)
         if stream is None:
@@ -34,7 +34,8 @@ class Table:
             stream_ptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         self.allocator = C.TorchAllocator(self.device) if torch_alloc else None
         cfg, self._keep = C.make_config(self.device, stream_ptr, self.allocator, n_shards, shard_rank,
-                                        nccl_unique_id, update_policy, use_residues, use_index, use_graph)
+                                        nccl_unique_id, update_policy, use_residues, use_index, use_graph,
+                                        use_fused)
         self.lo = np.ascontiguousarray(lo, np.int32)
         self.d = np.ascontiguousarray(d, np.int32)
         status, handle, root, dom = C.ct_create(self.lo, self.d, tuples, init_dom, scope, cfg)

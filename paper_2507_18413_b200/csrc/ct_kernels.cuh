@@ -1,43 +1,48 @@
 // ct_kernels.cuh -- sm_100a device code of the Compact-Table propagation path.
 //
-// One propagation of a state (Alg. 1) is five launches on
-// one stream, every size fixed at create time so the sequence can be captured
-// in a CUDA graph:
+// One propagation of a state (Alg. 1) runs five phases:
 //
-//   k_ingest   (a2)  removed ∧ dom -> Δ_x, D_x = dom ∧ ¬removed, |Δ_x|, |D_x|,
-//                    s_val, s_sup (Alg. 1 L1-3), the Δ/dom branch of each changed
-//                    var (Alg. 2), the update row list and the filter items.
-//   k_update   (a3-a5) for every active currTable word w:
-//                    T[w] &= AND_{x in s_val} (Δ ? ¬OR_{a∈Δx} S[x,a][w] : OR_{a∈Dx} S[x,a][w])
-//                    (Alg. 2; the per-variable ANDs commute, so all s_val vars
-//                    are folded in one pass), then order-preserving compaction
-//                    of the non-zero words (RSparseBitSet index) with a
-//                    single-pass chained scan; L_out = 0 <=> FAIL (Alg. 1 L5).
-//   k_probe    (a6a) residue probe for each (x,a), x in s_sup (Alg. 3 L3, L220).
-//   k_scan     (a6b) probe misses: warp-parallel intersect of S[x,a] with
-//                    currTable over the compacted index (__ballot_sync any).
-//   k_finalize (a6c-a8) prune unsupported values, lastDom <- dom, outputs.
+//   ingest   (a2)  removed ∧ dom -> Δ_x, D_x = dom ∧ ¬removed, |Δ_x|, |D_x|,
+//                  s_val, s_sup (Alg. 1 L1-3), the Δ/dom branch of each changed
+//                  var (Alg. 2), the update row list and the filter items.
+//   update   (a3-a5) for every active 16-byte currTable block b:
+//                  T[b] &= AND_{x in s_val} (Δ ? ¬OR_{a∈Δx} S[x,a][b] : OR_{a∈Dx} S[x,a][b])
+//                  (Alg. 2; the per-variable ANDs commute, so all s_val vars
+//                  are folded in one streaming pass), then order-preserving
+//                  compaction of the non-zero blocks (the RSparseBitSet index)
+//                  by a single-pass chained scan; L_out = 0 <=> FAIL (Alg. 1 L5).
+//   probe    (a6a) per (x,a), x in s_sup: residue probe (L220), then the first
+//                  kFirstScan index entries, warp-cooperatively.
+//   scan     (a6b) probe misses: chunked warp-parallel intersect of S[x,a] with
+//                  currTable over the compacted index (__ballot_sync "any").
+//   finalize (a6c-a8) prune unsupported values (Alg. 3 L3-4), lastDom <- dom,
+//                  outputs and status.
 //
-// Tuple-range sharding (a10) splits k_finalize's input: the per-row flags sup[]
-// written by k_probe/k_scan are OR-combined across shards before it runs.
-//
-// All kernels take the table by value (TableDev) and an array of per-state
-// descriptors (StateDev), indexed by blockIdx.y, so the same code serves one
-// state (gridDim.y = 1) and a batch of independent states (a9).
+// Two launch shapes share these device functions:
+//   * k_fused      one cooperative persistent kernel for a single state; the
+//                  phases are separated by software grid barriers (all blocks
+//                  are co-resident by construction of the cooperative launch);
+//   * k_ingest / k_update / k_probe / k_scan / k_finalize -- one kernel per
+//                  phase with a state dimension (blockIdx.y), used for batches
+//                  of independent states (a9).
+// Tuple-range sharding (a10) stops before finalize: the per-row flags sup[]
+// written by probe/scan are OR-combined across shards (NCCL) and finalize runs
+// as its own kernel.
 #pragma once
 #include <cstdint>
 
 namespace ctk {
 
-constexpr int kUpdTPB = 256;      // k_update threads per block = words per tile
-constexpr int kIngestTPB = 512;
+constexpr int kUpdTPB = 256;      // update threads per block = index entries per tile
+constexpr int kIngestTPB = 1024;  // block size of the standalone ingest / finalize kernels
 constexpr int kProbeTPB = 256;
 constexpr int kScanTPB = 256;
-constexpr int kFinTPB = 256;
-constexpr int kUpdUnroll = 8;     // support rows in flight per thread in k_update
+constexpr int kFinTPB = 1024;
+constexpr int kFusedTPB = 256;    // k_fused block size (= kUpdTPB)
+constexpr int kUpdUnroll = 8;     // support rows in flight per thread in update
 constexpr int kScanUnroll = 4;    // index entries (16-byte blocks) per lane per scan round
-constexpr int kFirstScan = 32 * kScanUnroll * 2;     // entries k_probe scans itself (2 rounds)
-constexpr int kScanChunk = 32 * kScanUnroll * 8;     // entries per k_scan work unit (8 rounds)
+constexpr int kFirstScan = 32 * kScanUnroll * 2;     // entries probe scans itself (2 rounds)
+constexpr int kScanChunk = 32 * kScanUnroll * 2;     // entries per scan work unit (2 rounds)
 
 constexpr uint32_t kRowMask = 0x3FFFFFFFu;   // update-list entry: row id
 constexpr uint32_t kEndBit = 1u << 30;        //   last row of its variable's group
@@ -62,8 +67,8 @@ struct TableDev {
   int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
 };
 
-// Per-state control block (device).  The first four fields persist across
-// calls (they are part of the state); the rest is per-call scratch.
+// Per-state control block (device).  The first fields up to last_status persist
+// across calls (they are part of the state); the rest is per-call scratch.
 struct Ctl {
   int32_t dead;        // 1 after CT_FAIL until restored by a copy
   int32_t parity;      // which index buffer holds the active index
@@ -79,26 +84,29 @@ struct Ctl {
   int32_t ngroups;     // |s_val|
   int32_t nitems;      // filter items
   int32_t L_in;
-  int32_t L_out;       // active words after the update (this shard)
+  int32_t L_out;       // active blocks after the update (this shard)
   int32_t tile_ctr;
-  int32_t nscan;       // residue misses queued for scanning
-  unsigned long long upd_loads;    // support words loaded by k_update (this call)
-  unsigned long long upd_writes;   // currTable words rewritten by k_update
-  unsigned long long scan_loads;   // support words loaded by k_scan
-  int32_t pad[9];
+  int32_t nscan;       // probe misses queued for scanning
+  unsigned long long upd_loads;    // support words loaded by update (this call)
+  unsigned long long upd_writes;   // currTable blocks rewritten by update
+  unsigned long long scan_loads;   // support words loaded by probe + scan
+  uint32_t bar_count;  // software grid barrier of k_fused
+  uint32_t bar_gen;
+  unsigned long long tph[6];   // k_fused phase timestamps (%globaltimer, ns), block 0
+  int32_t pad[2];
 };
 static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
 
 struct StateDev {
   Ctl *ctl;
   uint64_t *T;              // currTable [Wp]
-  int32_t *idx0, *idx1;     // compacted index double buffer [Wp]
-  int32_t *res;             // residues [R] (word ids of this shard)
+  int32_t *idx0, *idx1;     // compacted index double buffer [Wp/2]
+  int32_t *res;             // residues [R] (block ids of this shard)
   uint64_t *dom;            // current domains [Wd] (lastDom between calls)
   uint64_t *din;            // dom after the caller's removals [Wd]
   int32_t *ulist;           // update row list [R]
   int32_t *items;           // filter items (support rows) [R]
-  int32_t *scanlist;        // residue misses [R]
+  int32_t *scanlist;        // probe misses [R]
   uint8_t *sup;             // [R+1]: per-row "supported", [R] = "currTable non-empty"
   int32_t *varcnt;          // [2n]: |Δ_x|, |D_x|
   unsigned long long *tilestat;  // [ntiles_max] chained-scan tile status
@@ -112,19 +120,24 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-// Streaming read of a support word: read-only path, no L1 allocation.
-__device__ __forceinline__ uint64_t ld_sup(const uint64_t *p) {
-  uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
+// Streaming read of support words: read-only path, no L1 allocation.
 __device__ __forceinline__ ulonglong2 ld_sup2(const uint64_t *p) {
   ulonglong2 v;
   asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
   return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -137,8 +150,8 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
   return v;
 }
 
-// Exclusive block scan of a 64-bit value (two packed 32-bit counters never
-// overflow into each other here: each half sums to <= R < 2^30).
+// Exclusive block scan of a 64-bit value over NT threads (two packed 32-bit
+// counters never overflow into each other here: each half sums to <= R < 2^30).
 template <int NT>
 __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *s_warp, uint64_t &total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -164,6 +177,35 @@ __device__ __forceinline__ uint64_t block_excl_scan(uint64_t v, uint64_t *s_warp
   total = s_warp[NT / 32 - 1];
   __syncthreads();
   return base + x - v;
+}
+
+// Software grid barrier for k_fused (all blocks co-resident: cooperative launch).
+// Sense by generation counter.  The gpu-scope fences also invalidate the SM's
+// L1 (CCTL.IVALL), so after the barrier plain (L1-cached) loads see the data
+// other SMs wrote before it; that is what lets the phases use ordinary loads
+// for the update list, index and currTable.
+__device__ __forceinline__ void grid_barrier(Ctl *c) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t gen = ld_acquire_u32(&c->bar_gen);
+    __threadfence();
+    if (atomicAdd(&c->bar_count, 1u) == gridDim.x - 1) {
+      c->bar_count = 0;
+      __threadfence();
+      atomicAdd(&c->bar_gen, 1u);
+    } else {
+      while (ld_acquire_u32(&c->bar_gen) == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__host__ __device__ inline size_t ingest_smem_bytes(int n, int Wd) {
+  return (size_t)Wd * 16 + (size_t)(5 * n + 3) * 4;
+}
+__host__ __device__ inline size_t finalize_smem_bytes(int n, int Wd) {
+  return (size_t)Wd * 8 + (size_t)(3 * n + 2) * 4;
 }
 
 // ------------------------------------------------------------------ a1: supports builder
@@ -197,23 +239,35 @@ __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int
   if ((threadIdx.x & 31) == 0 && hw < n_half_words) T32[hw] = bal;
 }
 
-// ------------------------------------------------------------------ a2: ingest
-// grid (1, S), kIngestTPB threads.
-__global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateDev *__restrict__ states,
-                                                       const uint64_t *__restrict__ removed,
-                                                       int64_t removed_stride, int root_mode) {
-  const StateDev st = states[blockIdx.y];
+// ------------------------------------------------------------------ a2: ingest (one block)
+// Row-parallel: every support row decides on its own whether it enters the
+// update list (x in s_val, value in the chosen branch) and the filter list
+// (x in s_sup, value in D_x); one block scan gives the ordered positions.
+template <int NT>
+__device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
+                           int root_mode, uint64_t *smem) {
   Ctl *c = st.ctl;
-  const uint64_t *rem = removed ? removed + (int64_t)blockIdx.y * removed_stride : nullptr;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
+  uint64_t *s_din = smem;                       // D_x = dom ∧ ¬removed
+  uint64_t *s_dl = smem + Wd;                   // Δ_x = dom ∧ removed
+  int32_t *s_cd = reinterpret_cast<int32_t *>(smem + 2 * Wd);   // |Δ_x|
+  int32_t *s_cs = s_cd + n;                     // |D_x|
+  int32_t *s_ust = s_cs + n;                    // [n+1] start of x's group in the update list
+  int32_t *s_rb = s_ust + n + 1;                // [n+1] rowBase
+  int32_t *s_do = s_rb + n + 1;                 // [n+1] domOff
   __shared__ int s_dead, s_fail, s_ngroups;
-  __shared__ uint64_t s_warp[kIngestTPB / 32];
+  __shared__ uint64_t s_warp[NT / 32];
 
   if (tid == 0) {
     s_dead = c->dead;
     s_fail = 0;
     s_ngroups = 0;
   }
+  for (int i = tid; i <= n; i += NT) {
+    s_rb[i] = tb.rowBase[i];
+    s_do[i] = tb.domOff[i];
+  }
+  for (int x = tid; x < n; x += NT) s_cd[x] = s_cs[x] = 0;
   __syncthreads();
   if (s_dead) {
     if (tid == 0) {
@@ -223,102 +277,84 @@ __global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateD
     }
     return;
   }
-  // reset per-call scratch
-  for (int v = tid; v < 2 * tb.n; v += kIngestTPB) st.varcnt[v] = 0;
-  for (int r = tid; r <= tb.R; r += kIngestTPB) st.sup[r] = 0;
-  for (int k = tid; k < tb.ntiles_max; k += kIngestTPB) st.tilestat[k] = 0;
-  __syncthreads();
+  // per-call scratch
+  for (int r = tid; r <= tb.R; r += NT) st.sup[r] = 0;
+  for (int k = tid; k < tb.ntiles_max; k += NT) st.tilestat[k] = 0;
 
-  // phase 1: Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, and their sizes
-  for (int k = tid; k < tb.Wd; k += kIngestTPB) {
+  // phase 1 (Alg. 1 L1-2): Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
+  for (int k = tid; k < Wd; k += NT) {
     const uint64_t dm = st.dom[k];
     const uint64_t rm = rem ? rem[k] : 0ull;
-    const uint64_t delta = rm & dm, di = dm & ~rm;
-    st.din[k] = di;
     const int x = tb.wordVar[k];
-    if (delta) atomicAdd(&st.varcnt[2 * x], __popcll(delta));
-    if (di) atomicAdd(&st.varcnt[2 * x + 1], __popcll(di));
+    const uint64_t delta = rm & dm, di = dm & ~rm;
+    s_din[k] = di;
+    s_dl[k] = delta;
+    st.din[k] = di;
+    if (delta) atomicAdd(&s_cd[x], __popcll(delta));
+    if (di) atomicAdd(&s_cs[x], __popcll(di));
   }
   __syncthreads();
-  for (int x = tid; x < tb.n; x += kIngestTPB) {
-    if (st.varcnt[2 * x] > 0) atomicAdd(&s_ngroups, 1);
-    if (st.varcnt[2 * x + 1] == 0) s_fail = 1;     // D_x empty -> no valid tuple
+  // phase 2: per variable -- s_val membership, branch (Alg. 2), group sizes
+  int carry = 0;
+  for (int base = 0; base < n; base += NT) {
+    const int x = base + tid;
+    uint64_t ucnt = 0;
+    if (x < n) {
+      const int cd = s_cd[x], cs = s_cs[x];
+      const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+      if (cd > 0) {
+        ucnt = (uint64_t)(useDelta ? cd : cs);
+        atomicAdd(&s_ngroups, 1);
+      }
+      if (cs == 0) s_fail = 1;                    // D_x empty -> no valid tuple
+      st.varcnt[2 * x] = cd;
+      st.varcnt[2 * x + 1] = cs;
+    }
+    uint64_t total;
+    const uint64_t ex = block_excl_scan<NT>(ucnt, s_warp, total);
+    if (x < n) s_ust[x] = carry + (int)ex;
+    carry += (int)total;
   }
+  if (tid == 0) s_ust[n] = carry;
   __syncthreads();
   const bool noop = (s_ngroups == 0) && !root_mode;
-  if (s_fail || noop) {
-    if (tid == 0) {
-      c->skip = 0;
-      c->noop = noop && !s_fail;
-      c->fail_fast = s_fail;
-      c->ngroups = s_ngroups;
-      c->nrows = 0;
-      c->nitems = 0;
-      c->L_in = c->L;
-      c->L_out = 0;
-      c->tile_ctr = 0;
-      c->nscan = 0;
-      c->upd_loads = 0;
-      c->upd_writes = 0;
-      c->scan_loads = 0;
-    }
-    return;
-  }
-
-  // phase 2: update row list (s_val vars, branch rows) + filter items (s_sup)
-  uint64_t carry = 0;
-  for (int base = 0; base < tb.Wd; base += kIngestTPB) {
-    const int k = base + tid;
-    uint64_t ub = 0, fb = 0;
-    bool useDelta = false;
-    int x = 0;
-    if (k < tb.Wd) {
-      x = tb.wordVar[k];
-      const int cd = st.varcnt[2 * x], cs = st.varcnt[2 * x + 1];
-      const uint64_t di = st.din[k];
-      const uint64_t delta = st.dom[k] & ~di;
-      useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);   // Alg. 2
-      if (cd > 0) ub = useDelta ? delta : di;
-      if (cs > 1) fb = di;                                          // Alg. 1 L3: s_sup
-    }
-    const uint64_t packed = ((uint64_t)__popcll(ub) << 32) | (uint64_t)__popcll(fb);
-    uint64_t total;
-    const uint64_t excl = block_excl_scan<kIngestTPB>(packed, s_warp, total) + carry;
-    if (k < tb.Wd) {
-      int up = (int)(excl >> 32), fp = (int)(excl & 0xffffffffu);
-      const int rb = tb.rowBase[x] + (k - tb.domOff[x]) * 64;
-      const uint32_t inv = useDelta ? kInvBit : 0u;
-      while (ub) {
-        const int b = __ffsll(ub) - 1;
-        ub &= ub - 1;
-        st.ulist[up++] = (int32_t)((uint32_t)(rb + b) | inv);
+  int nrows = 0, nitems = 0;
+  if (!(s_fail || noop)) {
+    // phase 3: per support row -- update list (grouped by var, group end
+    // marked) and filter items (Alg. 1 L3: s_sup), both in row order
+    uint64_t rcarry = 0;
+    for (int base = 0; base < tb.R; base += NT) {
+      const int r = base + tid;
+      bool u = false, f = false, useDelta = false;
+      int x = 0;
+      if (r < tb.R) {
+        x = tb.rowVar[r];
+        const int a = r - s_rb[x];
+        const int w = s_do[x] + (a >> 6), b = a & 63;
+        const int cd = s_cd[x], cs = s_cs[x];
+        useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+        const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
+        u = cd > 0 && (useDelta ? inDl : inD);
+        f = cs > 1 && inD;
       }
-      while (fb) {
-        const int b = __ffsll(fb) - 1;
-        fb &= fb - 1;
-        st.items[fp++] = rb + b;
+      uint64_t total;
+      const uint64_t ex = block_excl_scan<NT>(((uint64_t)u << 32) | (uint64_t)f, s_warp, total) + rcarry;
+      if (u) {
+        const int up = (int)(ex >> 32);
+        uint32_t e = (uint32_t)r | (useDelta ? kInvBit : 0u);
+        if (up == s_ust[x + 1] - 1) e |= kEndBit;
+        st.ulist[up] = (int32_t)e;
       }
+      if (f) st.items[(int)(ex & 0xffffffffu)] = r;
+      rcarry += total;
     }
-    carry += total;
-  }
-  const int nrows = (int)(carry >> 32), nitems = (int)(carry & 0xffffffffu);
-  __syncthreads();
-  // phase 3: mark the last row of each variable's group
-  for (int base = 0; base < nrows; base += kIngestTPB) {
-    const int p = base + tid;
-    bool last = false;
-    if (p < nrows) {
-      const int r = (int)((uint32_t)st.ulist[p] & kRowMask);
-      last = (p + 1 == nrows) || tb.rowVar[(uint32_t)st.ulist[p + 1] & kRowMask] != tb.rowVar[r];
-    }
-    __syncthreads();
-    if (last) st.ulist[p] = (int32_t)((uint32_t)st.ulist[p] | kEndBit);
-    __syncthreads();
+    nrows = (int)(rcarry >> 32);
+    nitems = (int)(rcarry & 0xffffffffu);
   }
   if (tid == 0) {
     c->skip = 0;
-    c->noop = 0;
-    c->fail_fast = 0;
+    c->noop = noop && !s_fail;
+    c->fail_fast = s_fail;
     c->ngroups = s_ngroups;
     c->nrows = nrows;
     c->nitems = nitems;
@@ -364,22 +400,21 @@ __device__ __forceinline__ uint32_t tile_lookback(unsigned long long *ts, int ti
   return excl;
 }
 
-// grid (blocks, S), kUpdTPB threads; persistent over tiles of kUpdTPB active
-// 16-byte blocks ("pairs" of currTable words; the index is over pairs so every
-// support/currTable access is an aligned 128-bit vector load).
-__global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev *__restrict__ states) {
-  const StateDev st = states[blockIdx.y];
+// Block-level persistent loop over tiles of kUpdTPB index entries (16-byte
+// blocks, so every support/currTable access is an aligned 128-bit load).
+// Requires blockDim.x == kUpdTPB.
+__device__ void dev_update(const TableDev &tb, const StateDev &st) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int s_go, s_tile, s_nrows, s_L, s_ident, s_par;
   __shared__ uint32_t s_woff[kUpdTPB / 32];
   __shared__ uint32_t s_excl;
   if (tid == 0) {
-    s_go = !(c->skip | c->noop | c->fail_fast);
-    s_nrows = c->nrows;
-    s_L = c->L;
-    s_ident = c->identity;
-    s_par = c->parity;
+    s_go = !(__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast));
+    s_nrows = __ldcg(&c->nrows);
+    s_L = __ldcg(&c->L);
+    s_ident = __ldcg(&c->identity);
+    s_par = __ldcg(&c->parity);
   }
   __syncthreads();
   if (!s_go) return;
@@ -409,7 +444,7 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
       uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
       uint32_t e[kUpdUnroll];
 #pragma unroll
-      for (int u = 0; u < kUpdUnroll; ++u) e[u] = (u < nrows) ? (uint32_t)__ldg(ulist + u) : 0u;
+      for (int u = 0; u < kUpdUnroll; ++u) e[u] = (u < nrows) ? (uint32_t)ulist[u] : 0u;
       for (int p = 0; p < nrows; p += kUpdUnroll) {
         if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 128-bit block
         ulonglong2 v[kUpdUnroll];
@@ -420,7 +455,7 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
         uint32_t en[kUpdUnroll];
 #pragma unroll
         for (int u = 0; u < kUpdUnroll; ++u)
-          en[u] = (p + kUpdUnroll + u < nrows) ? (uint32_t)__ldg(ulist + p + kUpdUnroll + u) : 0u;
+          en[u] = (p + kUpdUnroll + u < nrows) ? (uint32_t)ulist[p + kUpdUnroll + u] : 0u;
 #pragma unroll
         for (int u = 0; u < kUpdUnroll; ++u) {
           if (p + u < nrows) {
@@ -483,10 +518,10 @@ __global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev 
 
 // ------------------------------------------------------------------ a6: filter
 // Warp-cooperative intersect of support row `srow` with currTable over index
-// entries [k0, k1) (Alg. 3 L3 "currTable & supports[x,a] != 0", residue-style
-// intersectIndex of CT): kScanUnroll pairs per lane per round, one
-// __ballot_sync "any" per pair.  Returns the first (lowest-entry) pair with a
-// common valid tuple, -1 if none, -2 if `supflag` was set by another warp.
+// entries [k0, k1) (Alg. 3 L3 "currTable & supports[x,a] != 0", CT's
+// intersectIndex): kScanUnroll blocks per lane per round, one __ballot_sync
+// "any" per block.  Returns the first (lowest-entry) block with a common valid
+// tuple, -1 if none, -2 if `supflag` was set by another warp meanwhile.
 __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const ulonglong2 *__restrict__ T2,
                                           const uint64_t *__restrict__ srow, int k0, int k1,
                                           const uint8_t *supflag, int lane, uint32_t &n_loads) {
@@ -500,7 +535,7 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
 #pragma unroll
     for (int q = 0; q < kScanUnroll; ++q) {
       const int k = kb + q * 32 + lane;
-      pid[q] = k < k1 ? (idx ? __ldg(idx + k) : k) : -1;
+      pid[q] = k < k1 ? (idx ? idx[k] : k) : -1;
     }
 #pragma unroll
     for (int q = 0; q < kScanUnroll; ++q) {
@@ -524,77 +559,74 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
   return -1;
 }
 
-// grid (ceil(R / warps per block), S): one warp per (x,a) item, x in s_sup:
-// residue probe, then the first kFirstScan index entries; the
-// items still unsupported go to the scan list for k_scan.
-__global__ void __launch_bounds__(kProbeTPB) k_probe(TableDev tb, const StateDev *__restrict__ states) {
-  const StateDev st = states[blockIdx.y];
+// Warp-level: items gw, gw + nw, ...: residue probe, then the
+// first kFirstScan index entries; items still unresolved go to the scan list.
+// The block with gw == 0 also publishes this shard's "non-empty" flag.
+__device__ void dev_probe(const TableDev &tb, const StateDev &st, int gw, int nw) {
   Ctl *c = st.ctl;
-  if (c->skip | c->noop | c->fail_fast) return;
-  const int Lout = c->L_out;
-  if (blockIdx.x == 0 && threadIdx.x == 0) st.sup[tb.R] = Lout > 0;
+  if (__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast)) return;
+  const int Lout = __ldcg(&c->L_out);
+  if (gw == 0 && (threadIdx.x & 31) == 0) st.sup[tb.R] = Lout > 0;
   if (Lout == 0) return;
   const int lane = threadIdx.x & 31;
-  const int item = blockIdx.x * (kProbeTPB / 32) + (threadIdx.x >> 5);
-  if (item >= c->nitems) return;
-  const int row = st.items[item];
+  const int nitems = __ldcg(&c->nitems);
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-  const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
-  if (tb.use_res) {
-    int hit = 0;
-    if (lane == 0) {
-      const int r = st.res[row];
-      const ulonglong2 t = T2[r];
-      const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
-      hit = ((t.x & s.x) | (t.y & s.y)) != 0;
-    }
-    if (__shfl_sync(0xffffffffu, hit, 0)) {
-      if (lane == 0) st.sup[row] = 1;
-      return;
-    }
-  }
   const bool compact = tb.use_index != 0;
-  const int32_t *__restrict__ idx = compact ? (c->parity ? st.idx0 : st.idx1) : nullptr;
+  const int32_t *__restrict__ idx = compact ? (__ldcg(&c->parity) ? st.idx0 : st.idx1) : nullptr;
   const int L = compact ? Lout : tb.W2;
   uint32_t n_loads = 0;
-  const int hit = scan_pairs(idx, T2, srow, 0, min(L, kFirstScan), nullptr, lane, n_loads);
-  if (lane == 0) {
-    if (hit >= 0) {
-      st.sup[row] = 1;
-      st.res[row] = hit;
-    } else if (L > kFirstScan) {
-      st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+  for (int item = gw; item < nitems; item += nw) {
+    const int row = __ldcg(st.items + item);
+    const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+    if (tb.use_res) {
+      int hit = 0;
+      if (lane == 0) {
+        const int r = st.res[row];
+        const ulonglong2 t = __ldcg(T2 + r);
+        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
+        hit = ((t.x & s.x) | (t.y & s.y)) != 0;
+      }
+      if (__shfl_sync(0xffffffffu, hit, 0)) {
+        if (lane == 0) st.sup[row] = 1;
+        continue;
+      }
     }
-    atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
+    const int hit = scan_pairs(idx, T2, srow, 0, min(L, kFirstScan), nullptr, lane, n_loads);
+    if (lane == 0) {
+      if (hit >= 0) {
+        st.sup[row] = 1;
+        st.res[row] = hit;
+      } else if (L > kFirstScan) {
+        st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+      }
+    }
   }
+  if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
 }
 
-// grid (blocks, S), kScanTPB threads: the items k_probe left unresolved, over
-// index entries [kFirstScan, L) in chunks of kScanChunk; one warp per
-// (item, chunk) unit, chunk-major so early chunks of every item go first, and
-// every round re-checks the item's flag so late chunks stop once any chunk hit.
-__global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *__restrict__ states) {
-  const StateDev st = states[blockIdx.y];
-  const Ctl *c = st.ctl;
-  if (c->skip | c->noop | c->fail_fast) return;
-  const int nscan = c->nscan;
-  const int Lout = c->L_out;
+// Warp-level: (miss, chunk) units gw, gw + nw, ... over index entries
+// [kFirstScan, L), chunk-major so early chunks of every item go first; every
+// round re-checks the item's flag so late chunks stop once any chunk hit.
+__device__ void dev_scan(const TableDev &tb, const StateDev &st, int gw, int nw) {
+  Ctl *c = st.ctl;
+  if (__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast)) return;
+  const int nscan = __ldcg(&c->nscan);
+  const int Lout = __ldcg(&c->L_out);
   if (nscan == 0 || Lout == 0) return;
   const bool compact = tb.use_index != 0;
-  const int32_t *__restrict__ idx = compact ? (c->parity ? st.idx0 : st.idx1) : nullptr;
+  const int32_t *__restrict__ idx = compact ? (__ldcg(&c->parity) ? st.idx0 : st.idx1) : nullptr;
   const int L = compact ? Lout : tb.W2;
   if (L <= kFirstScan) return;
   const int lane = threadIdx.x & 31;
   const int64_t nch = (L - kFirstScan + kScanChunk - 1) / kScanChunk;
   const int64_t total = nch * nscan;
-  const int64_t nw = (int64_t)gridDim.x * (kScanTPB / 32);
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
   uint32_t n_loads = 0;
-  for (int64_t u = (int64_t)blockIdx.x * (kScanTPB / 32) + (threadIdx.x >> 5); u < total; u += nw) {
+  for (int64_t u = gw; u < total; u += nw) {
     const int chunk = (int)(u / nscan);
     const int item = (int)(u - (int64_t)chunk * nscan);
-    const int row = st.scanlist[item];
-    int f = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
+    const int row = __ldcg(st.scanlist + item);
+    const int f = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
     if (__shfl_sync(0xffffffffu, f, 0)) continue;
     const int k0 = kFirstScan + chunk * kScanChunk;
     const int k1 = min(k0 + kScanChunk, L);
@@ -604,18 +636,115 @@ __global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *
       st.res[row] = hit;
     }
   }
-  if (lane == 0 && n_loads) atomicAdd(&st.ctl->scan_loads, (unsigned long long)n_loads);
+  if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
 }
 
-// grid (1, S), kFinTPB threads.  Writes the per-state status and outputs.
+// ------------------------------------------------------------------ a6c-a8: finalize (one block)
+// Alg. 3 L3-4: a value of x in s_sup leaves the domain iff its support row has
+// no valid tuple (sup[r] = 0 after the cross-shard OR); then lastDom <- dom.
+template <int NT>
+__device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *__restrict__ out_dom,
+                             uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status, uint64_t *smem) {
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
+  uint64_t *s_nd = smem;
+  int32_t *s_cs = reinterpret_cast<int32_t *>(smem + Wd);
+  int32_t *s_rb = s_cs + n;
+  int32_t *s_do = s_rb + n + 1;
+  __shared__ int s_status, s_noop;
+  if (tid == 0) {
+    int s;
+    if (__ldcg(&c->skip)) s = -5;                  // CT_ESTATE
+    else if (__ldcg(&c->fail_fast)) s = 1;         // CT_FAIL
+    else if (__ldcg(&c->noop)) s = 0;
+    else s = __ldcg(st.sup + tb.R) ? 0 : 1;        // global "currTable non-empty" (Alg. 1 L5)
+    s_status = s;
+    s_noop = __ldcg(&c->noop);
+  }
+  for (int k = tid; k < Wd; k += NT) s_nd[k] = __ldcg(st.din + k);
+  for (int x = tid; x < n; x += NT) s_cs[x] = __ldcg(st.varcnt + 2 * x + 1);
+  for (int i = tid; i <= n; i += NT) {
+    s_rb[i] = tb.rowBase[i];
+    s_do[i] = tb.domOff[i];
+  }
+  __syncthreads();
+  const int status = s_status;
+  if (status != 0) {
+    if (tid == 0) {
+      if (status == 1) {
+        c->dead = 1;
+        c->calls += 1;
+      }
+      c->last_status = status;
+      if (out_status) *out_status = status;
+    }
+    return;
+  }
+  const bool noop = s_noop != 0;
+  if (!noop) {
+    for (int r = tid; r < tb.R; r += NT) {
+      const uint8_t sp = __ldcg(st.sup + r);
+      const int x = tb.rowVar[r];
+      if (!sp && s_cs[x] > 1) {                  // x in s_sup (Alg. 3 L1), a unsupported
+        const int a = r - s_rb[x];
+        const int w = s_do[x] + (a >> 6);
+        const uint64_t bit = 1ull << (a & 63);
+        if (s_nd[w] & bit) atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + w), ~bit);
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < Wd; k += NT) {
+    const uint64_t nd = s_nd[k];
+    st.dom[k] = nd;
+    if (out_dom) out_dom[k] = nd;
+    if (out_pruned) out_pruned[k] = __ldcg(st.din + k) & ~nd;
+  }
+  if (tid == 0) {
+    if (!noop && tb.use_index) {
+      c->parity ^= 1;
+      c->L = __ldcg(&c->L_out);
+      c->identity = 0;
+    }
+    c->calls += 1;
+    c->last_status = 0;
+    if (out_status) *out_status = 0;
+  }
+}
+
+// ------------------------------------------------------------------ kernels: one per phase (batches)
+// grid (1, S), kIngestTPB threads, dynamic smem ingest_smem_bytes().
+__global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateDev *__restrict__ states,
+                                                       const uint64_t *__restrict__ removed,
+                                                       int64_t removed_stride, int root_mode) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const uint64_t *rem = removed ? removed + (int64_t)blockIdx.y * removed_stride : nullptr;
+  dev_ingest<kIngestTPB>(tb, states[blockIdx.y], rem, root_mode, smem);
+}
+
+// grid (blocks, S), kUpdTPB threads.
+__global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev *__restrict__ states) {
+  dev_update(tb, states[blockIdx.y]);
+}
+
+// grid (blocks, S), kProbeTPB threads: one warp per item.
+__global__ void __launch_bounds__(kProbeTPB) k_probe(TableDev tb, const StateDev *__restrict__ states) {
+  dev_probe(tb, states[blockIdx.y], blockIdx.x * (kProbeTPB / 32) + (threadIdx.x >> 5),
+            gridDim.x * (kProbeTPB / 32));
+}
+
+// grid (blocks, S), kScanTPB threads.
+__global__ void __launch_bounds__(kScanTPB) k_scan(TableDev tb, const StateDev *__restrict__ states) {
+  dev_scan(tb, states[blockIdx.y], blockIdx.x * (kScanTPB / 32) + (threadIdx.x >> 5), gridDim.x * (kScanTPB / 32));
+}
+
+// grid (1, S), kFinTPB threads, dynamic smem finalize_smem_bytes().
 __global__ void __launch_bounds__(kFinTPB) k_finalize(TableDev tb, const StateDev *__restrict__ states,
                                                       uint64_t *__restrict__ out_dom, int64_t dom_stride,
                                                       uint64_t *__restrict__ out_pruned,
                                                       int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
   const StateDev st = states[blockIdx.y];
-  Ctl *c = st.ctl;
-  const int tid = threadIdx.x;
-  __shared__ int s_status, s_noop;
   if (use_state_out) {
     out_dom = st.out + 1;
     out_pruned = st.out + 1 + tb.Wd;
@@ -625,55 +754,54 @@ __global__ void __launch_bounds__(kFinTPB) k_finalize(TableDev tb, const StateDe
     if (out_pruned) out_pruned += (int64_t)blockIdx.y * dom_stride;
     if (out_status) out_status += blockIdx.y;
   }
-  if (tid == 0) {
-    int s;
-    if (c->skip) s = -5;                         // CT_ESTATE
-    else if (c->fail_fast) s = 1;                // CT_FAIL
-    else if (c->noop) s = 0;
-    else s = st.sup[tb.R] ? 0 : 1;               // global "currTable non-empty"
-    s_status = s;
-    s_noop = c->noop;
-  }
-  __syncthreads();
-  const int status = s_status;
-  if (status != 0) {
-    if (tid == 0) {
-      if (status == 1) c->dead = 1;
-      c->last_status = status;
-      if (status == 1) c->calls += 1;
-      if (out_status) *out_status = status;
+  dev_finalize<kFinTPB>(tb, st, out_dom, out_pruned, out_status, smem);
+}
+
+// ------------------------------------------------------------------ k_fused: one state, one launch
+// Cooperative persistent kernel, kFusedTPB threads, grid <= co-resident blocks,
+// dynamic smem max(ingest, finalize).  with_finalize = 0 for sharded tables
+// (finalize runs after the cross-shard combine).
+__global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const StateDev *__restrict__ states,
+                                                     const uint64_t *__restrict__ removed, int root_mode,
+                                                     int with_finalize, uint64_t *__restrict__ out_dom,
+                                                     uint64_t *__restrict__ out_pruned,
+                                                     int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const StateDev st = states[0];
+  const int gw = blockIdx.x * (kFusedTPB / 32) + (threadIdx.x >> 5), nw = gridDim.x * (kFusedTPB / 32);
+  const bool t0 = blockIdx.x == 0 && threadIdx.x == 0;
+  unsigned long long ts[6];
+  if (t0) ts[0] = globaltimer();
+  if (blockIdx.x == 0) dev_ingest<kFusedTPB>(tb, st, removed, root_mode, smem);
+  grid_barrier(st.ctl);
+  if (t0) ts[1] = globaltimer();
+  dev_update(tb, st);
+  grid_barrier(st.ctl);
+  if (t0) ts[2] = globaltimer();
+  dev_probe(tb, st, gw, nw);
+  grid_barrier(st.ctl);
+  if (t0) ts[3] = globaltimer();
+  dev_scan(tb, st, gw, nw);
+  if (!with_finalize) {
+    if (t0) {
+      ts[4] = ts[5] = globaltimer();
+      for (int i = 0; i < 6; ++i) st.ctl->tph[i] = ts[i];
     }
     return;
   }
-  const bool noop = s_noop != 0;
-  for (int k = tid; k < tb.Wd; k += kFinTPB) {
-    const uint64_t di = st.din[k];
-    uint64_t nd = di;
-    if (!noop) {
-      const int x = tb.wordVar[k];
-      if (st.varcnt[2 * x + 1] > 1) {               // x in s_sup (Alg. 3 L1)
-        const int rb = tb.rowBase[x] + (k - tb.domOff[x]) * 64;
-        uint64_t bits = di;
-        while (bits) {
-          const int b = __ffsll(bits) - 1;
-          bits &= bits - 1;
-          if (!st.sup[rb + b]) nd &= ~(1ull << b);  // Alg. 3 L3-4
-        }
-      }
+  grid_barrier(st.ctl);
+  if (t0) ts[4] = globaltimer();
+  if (blockIdx.x == 0) {
+    if (use_state_out) {
+      out_dom = st.out + 1;
+      out_pruned = st.out + 1 + tb.Wd;
+      out_status = reinterpret_cast<int32_t *>(st.out);
     }
-    st.dom[k] = nd;
-    if (out_dom) out_dom[k] = nd;
-    if (out_pruned) out_pruned[k] = di & ~nd;
-  }
-  if (tid == 0) {
-    if (!noop && tb.use_index) {
-      c->parity ^= 1;
-      c->L = c->L_out;
-      c->identity = 0;
+    dev_finalize<kFusedTPB>(tb, st, out_dom, out_pruned, out_status, smem);
+    if (t0) {
+      ts[5] = globaltimer();
+      for (int i = 0; i < 6; ++i) st.ctl->tph[i] = ts[i];
     }
-    c->calls += 1;
-    c->last_status = 0;
-    if (out_status) *out_status = 0;
   }
 }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -102,6 +103,8 @@ struct ct_table {
   struct Mark { int kid, e0, e1; };
   std::vector<Mark> marks;
   int upd_occ = 1, scan_occ = 1;
+  int use_fused = 1, fused_grid = 1, fused_occ = 1, coop = 1, fused_grid_override = 0;
+  size_t fused_smem = 0;
   int live = 0;   // states + batches alive
 
   void *dalloc(size_t bytes) {
@@ -214,6 +217,7 @@ static int prof_event(ct_table *tb, cudaStream_t st) {
   return i;
 }
 static void prof_mark(ct_table *tb, int kid, int e0, cudaStream_t st) {
+  static_assert(sizeof(((ct_kernel_times *)nullptr)->ms) / sizeof(double) >= 7, "kernel slots");
   if (e0 < 0) return;
   const int e1 = prof_event(tb, st);
   if (e1 >= 0) tb->marks.push_back({kid, e0, e1});
@@ -235,7 +239,8 @@ static int scan_blocks(const ct_table *tb, int S) {
 static ct_status enqueue_local(ct_table *tb, const StateDev *d_desc, int S, const uint64_t *removed,
                                int root_mode, cudaStream_t st) {
   int e = prof_event(tb, st);
-  k_ingest<<<dim3(1, S), kIngestTPB, 0, st>>>(tb->dev, d_desc, removed, tb->Wd, root_mode);
+  k_ingest<<<dim3(1, S), kIngestTPB, ingest_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, d_desc, removed, tb->Wd,
+                                                                             root_mode);
   prof_mark(tb, 0, e, st);
   e = prof_event(tb, st);
   k_update<<<dim3(update_blocks(tb, S), S), kUpdTPB, 0, st>>>(tb->dev, d_desc);
@@ -265,11 +270,43 @@ static ct_status enqueue_finalize(ct_table *tb, const StateDev *d_desc, int S, u
                                   uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                   cudaStream_t st) {
   const int e = prof_event(tb, st);
-  k_finalize<<<dim3(1, S), kFinTPB, 0, st>>>(tb->dev, d_desc, out_dom, tb->Wd, out_pruned, out_status,
-                                             use_state_out);
+  k_finalize<<<dim3(1, S), kFinTPB, finalize_smem_bytes(tb->n, tb->Wd), st>>>(
+      tb->dev, d_desc, out_dom, tb->Wd, out_pruned, out_status, use_state_out);
   prof_mark(tb, 5, e, st);
   CUDA_TRY(cudaGetLastError());
   return CT_OK;
+}
+
+// One single-state call.  Fused: one cooperative launch runs every phase (the
+// finalize phase too unless the flags must first be combined across shards);
+// otherwise one kernel per phase.  local_only stops before the combine.
+static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *removed, int root_mode,
+                                uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
+                                bool local_only) {
+  cudaStream_t st = s->stream;
+  if (tb->use_fused) {
+    const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)tb->fused_grid);
+    lc.blockDim = dim3(kFusedTPB);
+    lc.dynamicSmemBytes = tb->fused_smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = tb->coop;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    const int e = prof_event(tb, st);
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_fused, tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
+                                out_dom, out_pruned, out_status, use_state_out));
+    prof_mark(tb, 6, e, st);
+    if (fin_inside || local_only) return CT_OK;
+  } else {
+    CT_TRY(enqueue_local(tb, s->d_desc, 1, removed, root_mode, st));
+    if (local_only) return CT_OK;
+  }
+  CT_TRY(enqueue_combine(tb, s->h, st));
+  return enqueue_finalize(tb, s->d_desc, 1, out_dom, out_pruned, out_status, use_state_out, st);
 }
 
 // Whole single-state call into the state's own out buffer, with host copies.
@@ -277,9 +314,7 @@ static ct_status enqueue_sync_call(ct_state *s, int root_mode) {
   ct_table *tb = s->tb;
   const size_t in_b = (size_t)tb->Wd * 8, out_b = (size_t)(1 + 2 * tb->Wd) * 8;
   if (in_b) CUDA_TRY(cudaMemcpyAsync(s->h.slot, s->h_in, in_b, cudaMemcpyHostToDevice, s->stream));
-  CT_TRY(enqueue_local(tb, s->d_desc, 1, s->h.slot, root_mode, s->stream));
-  CT_TRY(enqueue_combine(tb, s->h, s->stream));
-  CT_TRY(enqueue_finalize(tb, s->d_desc, 1, nullptr, nullptr, nullptr, 1, s->stream));
+  CT_TRY(enqueue_single(tb, s, s->h.slot, root_mode, nullptr, nullptr, nullptr, 1, false));
   CUDA_TRY(cudaMemcpyAsync(s->h_out, s->h.out, out_b, cudaMemcpyDeviceToHost, s->stream));
   return CT_OK;
 }
@@ -355,6 +390,7 @@ void ct_config_init(ct_config *cfg) {
   cfg->use_residues = 1;
   cfg->use_index = 1;
   cfg->use_graph = 1;
+  cfg->use_fused = 1;
 }
 
 ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin, int64_t *words) {
@@ -427,6 +463,9 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   tb->use_res = cfg.use_residues ? 1 : 0;
   tb->use_index = cfg.use_index ? 1 : 0;
   tb->use_graph = cfg.use_graph ? 1 : 0;
+  tb->use_fused = cfg.use_fused ? 1 : 0;
+  if (const char *ev = getenv("CT_FUSED_COOP")) tb->coop = atoi(ev) ? 1 : 0;   // experiment knob
+  if (const char *ev = getenv("CT_FUSED_GRID")) tb->fused_grid_override = atoi(ev);
   tb->n_shards = cfg.n_shards;
   tb->rank = cfg.shard_rank;
   if (cfg.alloc) {
@@ -464,6 +503,20 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb->upd_occ, k_update, kUpdTPB, 0));
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb->scan_occ, k_scan, kScanTPB, 0));
   tb->upd_occ = std::max(1, tb->upd_occ);
+  {
+    const size_t ib = ingest_smem_bytes(n, tb->Wd), fb = finalize_smem_bytes(n, tb->Wd);
+    if (std::max(ib, fb) > 200 * 1024)
+      return fail(CT_EINVAL, "table too wide for the single-block ingest (n=%d, %d domain words)", n, tb->Wd);
+    CUDA_TRY(cudaFuncSetAttribute(k_ingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(ib, 1)));
+    CUDA_TRY(cudaFuncSetAttribute(k_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(fb, 1)));
+    tb->fused_smem = std::max(ib, fb);
+    CUDA_TRY(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(tb->fused_smem, 1)));
+    int occ = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused, kFusedTPB, tb->fused_smem));
+    if (occ < 1) tb->use_fused = 0;
+    tb->fused_occ = std::max(occ, 1);
+  }
   tb->scan_occ = std::max(1, tb->scan_occ);
 
   // ---------------- NCCL (tuple-range sharding)
@@ -517,6 +570,10 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   dv.use_index = tb->use_index;
   dv.ntiles_max = (int32_t)((dv.W2 + kUpdTPB - 1) / kUpdTPB);
   tb->lay = make_layout(tb);
+  // k_fused grid: every block co-resident (cooperative); at least one block per
+  // SM for the filter phases, at most what the update can use beyond that.
+  tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, std::max(tb->sm_count, dv.ntiles_max));
+  if (tb->fused_grid_override > 0) tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, tb->fused_grid_override);
 
   // ---------------- root state + supports (a1)
   ct_state *root = nullptr;
@@ -651,15 +708,13 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
   if (tb->n_shards > 1 && !tb->comm)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
   DeviceGuard g(tb->device);
-  CT_TRY(enqueue_local(tb, s->d_desc, 1, removed, 0, s->stream));
-  CT_TRY(enqueue_combine(tb, s->h, s->stream));
-  return enqueue_finalize(tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream);
+  return enqueue_single(tb, s, removed, 0, out_dom, out_pruned, out_status, 0, false);
 }
 
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {
   if (!s) return fail(CT_EINVAL, "NULL state");
   DeviceGuard g(s->tb->device);
-  return enqueue_local(s->tb, s->d_desc, 1, removed, 0, s->stream);
+  return enqueue_single(s->tb, s, removed, 0, nullptr, nullptr, nullptr, 0, true);
 }
 
 ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes) {
@@ -913,6 +968,7 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
   o->update_support_words = (int64_t)c.upd_loads;
   o->update_table_writes = (int64_t)c.upd_writes;
   o->filter_support_words = (int64_t)c.scan_loads;
+  for (int i = 0; i < 5; ++i) o->phase_ns[i] = (c.tph[0] && c.tph[i + 1] >= c.tph[i]) ? (int64_t)(c.tph[i + 1] - c.tph[i]) : 0;
   return CT_OK;
 }
 

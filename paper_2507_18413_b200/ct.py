@@ -46,7 +46,8 @@ class ct_config(ctypes.Structure):
                 ("n_shards", ctypes.c_int32), ("shard_rank", ctypes.c_int32),
                 ("nccl_unique_id", ctypes.c_void_p),
                 ("update_policy", ctypes.c_int32), ("use_residues", ctypes.c_int32),
-                ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+                ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32),
+                ("use_fused", ctypes.c_int32)]
 
 
 class ct_table_info(ctypes.Structure):
@@ -64,14 +65,14 @@ class ct_stats(ctypes.Structure):
                 ("n_filter_items", ctypes.c_int32), ("n_residue_miss", ctypes.c_int32),
                 ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64),
                 ("update_support_words", ctypes.c_int64), ("update_table_writes", ctypes.c_int64),
-                ("filter_support_words", ctypes.c_int64)]
+                ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 5)]
 
 
 class ct_kernel_times(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64 * 6), ("ms", ctypes.c_double * 6)]
+    _fields_ = [("launches", ctypes.c_int64 * 8), ("ms", ctypes.c_double * 8)]
 
 
-KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize")
+KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize", "fused")
 
 
 # exported symbol -> (restype, argtypes); the CPU test checks the .so exports all of them
@@ -192,7 +193,8 @@ class TorchAllocator:
 
 def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1, shard_rank: int = 0,
                 nccl_unique_id: bytes | None = None, update_policy: int = CT_POLICY_AUTO,
-                use_residues: bool = True, use_index: bool = True, use_graph: bool = True):
+                use_residues: bool = True, use_index: bool = True, use_graph: bool = True,
+                use_fused: bool = True):
     cfg = ct_config()
     lib().ct_config_init(ctypes.byref(cfg))
     cfg.device = device
@@ -208,6 +210,7 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
     cfg.use_residues = int(bool(use_residues))
     cfg.use_index = int(bool(use_index))
     cfg.use_graph = int(bool(use_graph))
+    cfg.use_fused = int(bool(use_fused))
     return cfg, keep
 
 

@@ -26,8 +26,9 @@ KNOBS = [
     dict(use_residues=False),
     dict(use_index=False),
     dict(use_graph=False),
+    dict(use_fused=False),
 ]
-KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph"]
+KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph", "nofused"]
 
 
 @pytest.fixture(scope="module", autouse=True)
