@@ -94,9 +94,10 @@ typedef struct ct_config {
   int32_t use_residues;       /* 1: probe residue word first in filter (L220)            */
   int32_t use_index;          /* 1: keep the compacted non-zero-word index (RSparseBitSet)*/
   int32_t use_graph;          /* 1: synchronous calls replay a captured CUDA graph      */
-  int32_t use_fused;          /* 1: a single-state call is one cooperative persistent   */
-                              /*    kernel (software grid barriers between phases);     */
-                              /*    0: one kernel per phase                              */
+  int32_t use_fused;          /* 1: a single-state call is one kernel: one CTA for      */
+                              /*    tables of <= 8192 16-byte blocks, else a cooperative */
+                              /*    persistent grid with software barriers; 0: one      */
+                              /*    kernel per phase                                     */
 } ct_config;
 
 /* Fill *cfg with defaults: device 0, NULL stream, default allocator, 1 shard,
@@ -242,7 +243,8 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *out);
  * captured graphs).  read() waits for the stream, returns the summed durations
  * and launch counts since the last reset, and resets them if `reset`.
  * Kernel slots: 0 ingest, 1 update, 2 probe, 3 scan, 4 combine (NCCL), 5 finalize,
- * 6 fused (all phases of a single-state call in one kernel), 7 unused. */
+ * 6 fused (all phases of a single-state call in one kernel), 7 small (the same in
+ * one CTA, for tables of at most 8192 16-byte blocks). */
 typedef struct ct_kernel_times {
   int64_t launches[8];
   double ms[8];

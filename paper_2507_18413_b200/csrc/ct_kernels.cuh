@@ -700,6 +700,10 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
     if (out_dom) out_dom[k] = nd;
     if (out_pruned) out_pruned[k] = __ldcg(st.din + k) & ~nd;
   }
+  // the status word is the completion flag of the host-mapped sync path: make
+  // every thread's output writes visible system-wide before it is written
+  __threadfence_system();
+  __syncthreads();
   if (tid == 0) {
     if (!noop && tb.use_index) {
       c->parity ^= 1;
@@ -802,6 +806,171 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const State
       ts[5] = globaltimer();
       for (int i = 0; i < 6; ++i) st.ctl->tph[i] = ts[i];
     }
+  }
+}
+
+// ------------------------------------------------------------------ k_small: one state, one CTA
+// Tables of at most kSmallMaxPairs 16-byte blocks (e.g. BASELINE config 2,
+// 1e5 tuples = 782 blocks) are latency-bound: every phase runs in ONE block of
+// kSmallTPB threads, separated by __syncthreads instead of grid barriers, and
+// the compaction is a plain block scan (no look-back).  Same phase semantics
+// as k_fused; with_finalize = 0 for sharded tables.
+constexpr int kSmallTPB = 1024;
+constexpr int kSmallMaxPairs = 8192;
+
+__global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const StateDev *__restrict__ states,
+                                                       const uint64_t *__restrict__ removed, int root_mode,
+                                                       int with_finalize, uint64_t *__restrict__ out_dom,
+                                                       uint64_t *__restrict__ out_pruned,
+                                                       int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const StateDev st = states[0];
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool t0 = tid == 0;
+  unsigned long long ts[6];
+  if (t0) ts[0] = globaltimer();
+  dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
+  __syncthreads();
+  if (t0) ts[1] = globaltimer();
+  __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout;
+  __shared__ uint64_t s_warp[kSmallTPB / 32];
+  if (t0) {
+    s_go = !(c->skip | c->noop | c->fail_fast);
+    s_L = c->L;
+    s_nrows = c->nrows;
+    s_ident = c->identity;
+    s_par = c->parity;
+  }
+  __syncthreads();
+  // ---- update + compaction (Alg. 2), all in this block
+  if (s_go) {
+    const int L = s_L, nrows = s_nrows;
+    const int32_t *__restrict__ idx_in = s_par ? st.idx1 : st.idx0;
+    int32_t *__restrict__ idx_out = s_par ? st.idx0 : st.idx1;
+    const bool compact = tb.use_index != 0;
+    ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+    const int64_t Wp = tb.Wp;
+    uint32_t n_loads = 0, n_writes = 0;
+    uint64_t carry = 0;
+    for (int base = 0; base < L; base += kSmallTPB) {
+      const int k = base + tid;
+      int pid = 0;
+      bool keep = false;
+      if (k < L) {
+        pid = s_ident ? k : idx_in[k];
+        const ulonglong2 tw = T2[pid];
+        const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+        uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+        for (int p = 0; p < nrows; p += kUpdUnroll) {
+          if (((tw.x & mx) | (tw.y & my)) == 0) break;
+          uint32_t e[kUpdUnroll];
+          ulonglong2 v[kUpdUnroll];
+#pragma unroll
+          for (int u = 0; u < kUpdUnroll; ++u) e[u] = (p + u < nrows) ? (uint32_t)st.ulist[p + u] : 0u;
+#pragma unroll
+          for (int u = 0; u < kUpdUnroll; ++u)
+            v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
+          n_loads += 2 * min(kUpdUnroll, nrows - p);
+#pragma unroll
+          for (int u = 0; u < kUpdUnroll; ++u) {
+            if (p + u < nrows) {
+              ax |= v[u].x;
+              ay |= v[u].y;
+              if (e[u] & kEndBit) {
+                if (e[u] & kInvBit) {
+                  mx &= ~ax;
+                  my &= ~ay;
+                } else {
+                  mx &= ax;
+                  my &= ay;
+                }
+                ax = ay = 0;
+              }
+            }
+          }
+        }
+        const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
+        if (nt.x != tw.x || nt.y != tw.y) {
+          T2[pid] = nt;
+          ++n_writes;
+        }
+        keep = (nt.x | nt.y) != 0;
+      }
+      uint64_t total;
+      const uint64_t ex = block_excl_scan<kSmallTPB>((uint64_t)keep, s_warp, total);
+      if (compact && keep) idx_out[carry + ex] = pid;
+      carry += total;
+    }
+    n_loads = warp_sum_u32(n_loads);
+    n_writes = warp_sum_u32(n_writes);
+    if (lane == 0 && (n_loads | n_writes)) {
+      atomicAdd(&c->upd_loads, (unsigned long long)n_loads);
+      atomicAdd(&c->upd_writes, (unsigned long long)n_writes);
+    }
+    if (t0) {
+      c->L_out = (int32_t)carry;
+      s_Lout = (int32_t)carry;
+    }
+  }
+  __syncthreads();
+  if (t0) ts[2] = globaltimer();
+  // ---- filter (Alg. 3 L3, residues L220): a warp per item, full scan on a miss
+  if (s_go) {
+    const int Lout = s_Lout;
+    if (t0) st.sup[tb.R] = Lout > 0;
+    if (Lout > 0) {
+      const bool compact = tb.use_index != 0;
+      const int32_t *__restrict__ idx = compact ? (s_par ? st.idx0 : st.idx1) : nullptr;
+      const int L = compact ? Lout : tb.W2;
+      const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+      const int nitems = c->nitems;
+      uint32_t n_loads = 0;
+      for (int item = warp; item < nitems; item += kSmallTPB / 32) {
+        const int row = st.items[item];
+        const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+        if (tb.use_res) {
+          int hit = 0;
+          if (lane == 0) {
+            const int r = st.res[row];
+            const ulonglong2 t = T2[r];
+            const ulonglong2 s2 = ld_sup2(srow + 2 * (int64_t)r);
+            hit = ((t.x & s2.x) | (t.y & s2.y)) != 0;
+          }
+          if (__shfl_sync(0xffffffffu, hit, 0)) {
+            if (lane == 0) st.sup[row] = 1;
+            continue;
+          }
+        }
+        const int hit = scan_pairs(idx, T2, srow, 0, L, nullptr, lane, n_loads);
+        if (lane == 0 && hit >= 0) {
+          st.sup[row] = 1;
+          st.res[row] = hit;
+        }
+      }
+      if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
+    }
+  }
+  __syncthreads();
+  if (t0) {
+    ts[3] = ts[4] = globaltimer();
+  }
+  if (!with_finalize) {
+    if (t0) {
+      ts[5] = ts[4];
+      for (int i = 0; i < 6; ++i) c->tph[i] = ts[i];
+    }
+    return;
+  }
+  if (use_state_out) {
+    out_dom = st.out + 1;
+    out_pruned = st.out + 1 + tb.Wd;
+    out_status = reinterpret_cast<int32_t *>(st.out);
+  }
+  dev_finalize<kSmallTPB>(tb, st, out_dom, out_pruned, out_status, smem);
+  if (t0) {
+    ts[5] = globaltimer();
+    for (int i = 0; i < 6; ++i) c->tph[i] = ts[i];
   }
 }
 

@@ -19,6 +19,8 @@
 
 using namespace ctk;
 
+constexpr int32_t kPendingStatus = 0x7FFFFFFF;   // mapped status word before the kernel writes it
+
 // ------------------------------------------------------------------ errors
 static thread_local char g_err[1024] = "";
 
@@ -103,7 +105,7 @@ struct ct_table {
   struct Mark { int kid, e0, e1; };
   std::vector<Mark> marks;
   int upd_occ = 1, scan_occ = 1;
-  int use_fused = 1, fused_grid = 1, fused_occ = 1, coop = 1, fused_grid_override = 0;
+  int use_fused = 1, fused_grid = 1, fused_occ = 1, coop = 1, fused_grid_override = 0, use_small = 0;
   size_t fused_smem = 0;
   int live = 0;   // states + batches alive
 
@@ -133,6 +135,7 @@ struct ct_state {
   StateDev *d_desc = nullptr;
   uint64_t *h_in = nullptr;  // pinned [Wd]
   uint64_t *h_out = nullptr; // pinned [1 + 2 Wd]
+  uint64_t *d_in_map = nullptr, *d_out_map = nullptr;   // device aliases of h_in / h_out
   cudaGraphExec_t gexec = nullptr;
 };
 
@@ -284,7 +287,15 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                 bool local_only) {
   cudaStream_t st = s->stream;
-  if (tb->use_fused) {
+  if (tb->use_small) {
+    const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
+    const int e = prof_event(tb, st);
+    k_small<<<1, kSmallTPB, tb->fused_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode,
+                                                  fin_inside, out_dom, out_pruned, out_status, use_state_out);
+    CUDA_TRY(cudaGetLastError());
+    prof_mark(tb, 7, e, st);
+    if (fin_inside || local_only) return CT_OK;
+  } else if (tb->use_fused) {
     const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)tb->fused_grid);
@@ -312,11 +323,25 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
 // Whole single-state call into the state's own out buffer, with host copies.
 static ct_status enqueue_sync_call(ct_state *s, int root_mode) {
   ct_table *tb = s->tb;
-  const size_t in_b = (size_t)tb->Wd * 8, out_b = (size_t)(1 + 2 * tb->Wd) * 8;
-  if (in_b) CUDA_TRY(cudaMemcpyAsync(s->h.slot, s->h_in, in_b, cudaMemcpyHostToDevice, s->stream));
-  CT_TRY(enqueue_single(tb, s, s->h.slot, root_mode, nullptr, nullptr, nullptr, 1, false));
-  CUDA_TRY(cudaMemcpyAsync(s->h_out, s->h.out, out_b, cudaMemcpyDeviceToHost, s->stream));
-  return CT_OK;
+  return enqueue_single(tb, s, s->d_in_map, root_mode, nullptr, nullptr, nullptr, 1, false);
+}
+
+// Wait for a sync call: the kernel writes the status word of the mapped output
+// last (after a system-scope fence), so spinning on it replaces a stream sync.
+// The stream is polled every so often so a failed launch cannot hang the host.
+static ct_status wait_sync_call(ct_state *s) {
+  volatile int32_t *st = (volatile int32_t *)s->h_out;
+  for (uint64_t spin = 1;; ++spin) {
+    if (*st != kPendingStatus) return CT_OK;
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(s->stream);
+      if (e == cudaSuccess) {
+        if (*st != kPendingStatus) return CT_OK;
+        return fail(CT_ECUDA, "propagation finished without writing its status");
+      }
+      if (e != cudaErrorNotReady) return fail(CT_ECUDA, "propagation failed: %s", cudaGetErrorString(e));
+    }
+  }
 }
 
 // ------------------------------------------------------------------ state lifetime
@@ -343,14 +368,19 @@ static ct_status new_state(ct_table *tb, ct_state **out) {
     free_state_mem(s);
     return fail(CT_ENOMEM, "device allocation of %zu bytes for a state failed", tb->lay.total);
   }
-  if (cudaHostAlloc((void **)&s->h_in, std::max<size_t>(8, (size_t)tb->Wd * 8), cudaHostAllocDefault) !=
+  // mapped pinned staging: the sync path's kernels read `removed` from and write
+  // status + domains to host memory directly (zero-copy, no memcpy nodes)
+  if (cudaHostAlloc((void **)&s->h_in, std::max<size_t>(8, (size_t)tb->Wd * 8), cudaHostAllocMapped) !=
           cudaSuccess ||
-      cudaHostAlloc((void **)&s->h_out, (size_t)(1 + 2 * tb->Wd) * 8, cudaHostAllocDefault) != cudaSuccess) {
+      cudaHostAlloc((void **)&s->h_out, (size_t)(1 + 2 * tb->Wd) * 8, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&s->d_in_map, s->h_in, 0) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&s->d_out_map, s->h_out, 0) != cudaSuccess) {
     cudaGetLastError();
     free_state_mem(s);
-    return fail(CT_ENOMEM, "pinned host allocation failed");
+    return fail(CT_ENOMEM, "mapped pinned host allocation failed");
   }
   s->h = make_desc(tb, s->mem);
+  s->h.out = s->d_out_map;
   s->d_desc = reinterpret_cast<StateDev *>(s->mem + tb->lay.desc);
   ct_status st = CT_OK;
   // synchronous: the descriptor must be in place whichever stream uses the state first
@@ -515,6 +545,8 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused, kFusedTPB, tb->fused_smem));
     if (occ < 1) tb->use_fused = 0;
+    CUDA_TRY(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(tb->fused_smem, 1)));
     tb->fused_occ = std::max(occ, 1);
   }
   tb->scan_occ = std::max(1, tb->scan_occ);
@@ -574,6 +606,12 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   // SM for the filter phases, at most what the update can use beyond that.
   tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, std::max(tb->sm_count, dv.ntiles_max));
   if (tb->fused_grid_override > 0) tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, tb->fused_grid_override);
+  // latency-bound tables: the whole call in one CTA (k_small)
+  {
+    int small_max = kSmallMaxPairs;
+    if (const char *ev = getenv("CT_SMALL_MAX_PAIRS")) small_max = atoi(ev);
+    tb->use_small = (tb->use_fused && dv.W2 <= small_max) ? 1 : 0;
+  }
 
   // ---------------- root state + supports (a1)
   ct_state *root = nullptr;
@@ -606,7 +644,9 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
                              tb->stream));
   // root propagation: remove the holes of init_dom
   for (int k = 0; k < tb->Wd; ++k) root->h_in[k] = init_dom ? (tb->full_dom[k] & ~init_dom[k]) : 0ull;
+  *(volatile int32_t *)root->h_out = kPendingStatus;
   CT_TRY(enqueue_sync_call(root, /*root_mode=*/1));
+  CT_TRY(wait_sync_call(root));
   CUDA_TRY(cudaStreamSynchronize(tb->stream));
   const int32_t status = *(const int32_t *)root->h_out;
   if (status == CT_OK && out_dom && tb->Wd) memcpy(out_dom, root->h_out + 1, (size_t)tb->Wd * 8);
@@ -669,6 +709,7 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
     if (removed) memcpy(s->h_in, removed, (size_t)tb->Wd * 8);
     else memset(s->h_in, 0, (size_t)tb->Wd * 8);
   }
+  *(volatile int32_t *)s->h_out = kPendingStatus;
   if (tb->use_graph) {
     if (!s->gexec) {
       cudaGraph_t graph = nullptr;
@@ -691,8 +732,8 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
   } else {
     CT_TRY(enqueue_sync_call(s, 0));
   }
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  const int32_t status = *(const int32_t *)s->h_out;
+  CT_TRY(wait_sync_call(s));
+  const int32_t status = *(volatile const int32_t *)s->h_out;
   if (status == CT_OK) {
     if (out_dom && tb->Wd) memcpy(out_dom, s->h_out + 1, (size_t)tb->Wd * 8);
     if (out_pruned && tb->Wd) memcpy(out_pruned, s->h_out + 1 + tb->Wd, (size_t)tb->Wd * 8);

@@ -72,7 +72,7 @@ class ct_kernel_times(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 8), ("ms", ctypes.c_double * 8)]
 
 
-KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize", "fused")
+KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize", "fused", "small")
 
 
 # exported symbol -> (restype, argtypes); the CPU test checks the .so exports all of them

@@ -27,8 +27,9 @@ KNOBS = [
     dict(use_index=False),
     dict(use_graph=False),
     dict(use_fused=False),
+    dict(_grid_fused=True),
 ]
-KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph", "nofused"]
+KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph", "nofused", "gridfused"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -39,8 +40,16 @@ def _built():
     assert torch.cuda.is_available()
 
 
-def make(p, **kw):
-    return Table(p.lo, p.d, p.tuples, **kw)
+def make(p, _grid_fused=False, **kw):
+    """_grid_fused: force the cooperative multi-CTA kernel even for tables small
+    enough for the single-CTA one (CT_SMALL_MAX_PAIRS is read at create time)."""
+    import os
+    if _grid_fused:
+        os.environ["CT_SMALL_MAX_PAIRS"] = "0"
+    try:
+        return Table(p.lo, p.d, p.tuples, **kw)
+    finally:
+        os.environ.pop("CT_SMALL_MAX_PAIRS", None)
 
 
 # --------------------------------------------------------------------------- a1 supports builder
