@@ -200,6 +200,10 @@ ct_status ct_batch_create(ct_table *t, int32_t n_states, const ct_state *init, c
 int32_t ct_batch_size(const ct_batch *b);
 ct_status ct_batch_copy(ct_batch *b, int32_t dst_index, const ct_state *src);   /* async */
 ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src);                  /* async */
+/* Device-side restart: every state of the batch that is dead (returned CT_FAIL)
+ * becomes a copy of `src` (typically the root) -- one kernel, no host round
+ * trip, so a search driver can keep S states busy (async, batch stream). */
+ct_status ct_batch_restore_dead(ct_batch *b, const ct_state *src);
 /* Synchronous, host buffers: removed/out_dom are [S][Wd] row-major (removed may
  * be NULL); out_status int32[S] receives CT_OK / CT_FAIL / CT_ESTATE per state.
  * Returns CT_OK unless an error occurred. */

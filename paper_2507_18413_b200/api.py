@@ -127,6 +127,9 @@ class Batch:
     def copy_all(self, src: State):
         C.ct_batch_copy_all(self.handle, src.handle)
 
+    def restore_dead(self, src: State):
+        C.ct_batch_restore_dead(self.handle, src.handle)
+
     def propagate(self, removed=None):
         wd = self.table.Wd
         out = np.zeros((self.S, max(wd, 1)), np.uint64)

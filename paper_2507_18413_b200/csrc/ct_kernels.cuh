@@ -974,4 +974,15 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   }
 }
 
+// ------------------------------------------------------------------ batch restart
+// grid (S), 256 threads: state i := src (persistent prefix) iff state i is dead.
+__global__ void __launch_bounds__(256) k_restore_dead(char *__restrict__ pool, size_t pitch,
+                                                      const char *__restrict__ src, size_t persist) {
+  char *dst = pool + (size_t)blockIdx.x * pitch;
+  if (!reinterpret_cast<const Ctl *>(dst)->dead) return;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+  for (size_t k = threadIdx.x; k < persist / 16; k += blockDim.x) d4[k] = s4[k];
+}
+
 }  // namespace ctk

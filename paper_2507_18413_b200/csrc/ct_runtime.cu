@@ -914,6 +914,16 @@ ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src) {
   return CT_OK;
 }
 
+ct_status ct_batch_restore_dead(ct_batch *b, const ct_state *src) {
+  if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
+  DeviceGuard g(b->tb->device);
+  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  k_restore_dead<<<b->S, 256, 0, b->tb->stream>>>(b->mem, b->tb->lay.total, src->mem, b->tb->lay.persist);
+  CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
 ct_status ct_propagate_many_async(ct_batch *b, const uint64_t *removed, uint64_t *out_dom, int32_t *out_status) {
   if (!b) return fail(CT_EINVAL, "NULL batch");
   ct_table *tb = b->tb;

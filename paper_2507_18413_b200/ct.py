@@ -100,6 +100,7 @@ SIGNATURES = {
     "ct_batch_size": (I32, [P]),
     "ct_batch_copy": (I32, [P, I32, P]),
     "ct_batch_copy_all": (I32, [P, P]),
+    "ct_batch_restore_dead": (I32, [P, P]),
     "ct_propagate_many": (I32, [P, P, P, P]),
     "ct_propagate_many_async": (I32, [P, P, P, P]),
     "ct_batch_destroy": (None, [P]),
@@ -323,6 +324,10 @@ def ct_batch_copy(batch, index: int, state) -> None:
 
 def ct_batch_copy_all(batch, state) -> None:
     _check(lib().ct_batch_copy_all(batch, state), allow_fail=False)
+
+
+def ct_batch_restore_dead(batch, state) -> None:
+    _check(lib().ct_batch_restore_dead(batch, state), allow_fail=False)
 
 
 def ct_propagate_many(batch, removed, out_dom, out_status) -> None:

@@ -341,9 +341,12 @@ def test_batch_matches_oracle_and_single_state():
             if ok:
                 assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), (step, s)
                 cur[s] = dout
-            else:
-                b.copy(s, tab.root)
+            elif step % 2:
+                b.copy(s, tab.root)                 # host-driven restore of one slot
                 cur[s] = root_m.copy()
+            else:
+                cur[s] = root_m.copy()              # restored below by the device kernel
+        b.restore_dead(tab.root)
     b.close()
     tab.close()
 
