@@ -499,6 +499,76 @@ def run_c4(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- C5: DFS over a 12-table model
+def run_c5(args):
+    """BASELINE config 5: DFS (input_order, indomain_max, binary branching) on a
+    30-var CSP of 12 tables x 1e6 tuples (arity 4-8, planted solution), every
+    node propagated to the common fixpoint on the device (one cooperative kernel
+    per node).  value = DFS nodes/s over the first --max-nodes nodes (all
+    solutions mode, so the search does not stop at the planted one).  Replicas
+    only: a search is sequential; N > 1 runs N independent searches."""
+    import torch
+    from paper_2507_18413_b200 import Model
+    from workloads.csp import csp_model
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    m = csp_model(30, 40, 12, 1_000_000, seed=7)
+    t0 = time.perf_counter()
+    M = Model(m["vlo"], m["vd"], m["scopes"], m["tables"], device=dev)
+    build_s = time.perf_counter() - t0
+    M.search(value_order=0, max_nodes=200, max_solutions=0)           # warm-up
+    barrier(world)
+    clocks = Clocks(dev)
+    clocks.start()
+    t1 = time.perf_counter()
+    st, sol, stats = M.search(value_order=0, max_nodes=args.max_nodes, max_solutions=0)
+    wall = time.perf_counter() - t1
+    clk = clocks.stop()
+    wall_max = max_over_ranks(wall, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        from oracle.dfs import dfs as oracle_dfs
+        n_or = 12
+        t2 = time.perf_counter()
+        ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=n_or, max_solutions=0)
+        dt = time.perf_counter() - t2
+        cpu = {"value": ref["nodes"] / dt, "unit": "nodes/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {ref['nodes']} DFS nodes by oracle/dfs.py + oracle_fixpoint (C brute force), {dt:.1f} s"}
+        chk = M.search(value_order=0, max_nodes=n_or, max_solutions=0)[2]
+        cpu["trace_matches_gpu"] = (chk.nodes, chk.trace_hash) == (ref["nodes"], ref["trace_hash"])
+    wg = M.Wg
+    M.close()
+    if rank == 0:
+        line = {
+            "metric": "DFS nodes/s (C5, 12 tables x 1e6 tuples, fixpoint on device per node)",
+            "value": world * stats.nodes / wall_max, "unit": "nodes/s", "n_gpus": world, "steps": int(stats.nodes),
+            "warmup": 200, "ms_per_step": wall_max / max(stats.nodes, 1) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded CSP, planted solution, workloads/csp.py)",
+            "config": {"workload": "c5", "model": "30 vars d=40, 12 tables x 1e6 tuples, arity 4+(k mod 5), seed 7",
+                       "search": "input_order, indomain_max, binary branching, all solutions, node budget",
+                       "parallelism": "replicas" if world > 1 else "1 GPU", "build_s": round(build_s, 2)},
+            "search": {"nodes": stats.nodes, "failures": stats.failures, "solutions": stats.solutions,
+                       "table_calls": stats.table_calls, "jacobi_iterations": stats.iterations,
+                       "max_depth": stats.max_depth, "device_ms": stats.device_ms,
+                       "device_us_per_node": stats.device_ms * 1e3 / max(stats.nodes, 1),
+                       "trace_hash": hex(stats.trace_hash)},
+            "e2e": {"value": stats.nodes / wall, "unit": "nodes/s", "h2d_bytes_per_step": 8 * wg,
+                    "d2h_bytes_per_step": 8 * (4 + wg),
+                    "note": "ct_model_search is the end-to-end call: host-driven DFS, each node one fixpoint "
+                            "kernel reading the decision from / writing domains to mapped pinned memory"},
+            "clocks": clk, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args):
     world, rank, local = dist_env()
@@ -544,7 +614,8 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c4"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c4", "c5"])
+    ap.add_argument("--max-nodes", type=int, default=10_000, help="c5: DFS node budget")
     ap.add_argument("--states", type=int, default=4096, help="c4: total independent states (split over ranks)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-latency", action="store_true")
@@ -555,6 +626,8 @@ def main():
         run_reference(args)
     elif args.workload == "c4":
         run_c4(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_ours(args)
 

@@ -214,6 +214,58 @@ ct_status ct_propagate_many_async(ct_batch *b, const uint64_t *removed, uint64_t
                                   int32_t *out_status);
 void ct_batch_destroy(ct_batch *b);
 
+/* ---------------------------------------------------------------- models (several tables) */
+/* A CSP of table constraints over shared variables (PAPER.md
+ * L46-51 CSP <X, D, C>; L312-316 the engine alternates search and propagation).
+ * Every table is a ct_table on the same device; propagation to the common
+ * fixpoint runs in ONE cooperative kernel per call (Jacobi iterations over the
+ * tables: all tables' CT phases at once, shared domains ANDed after each
+ * round, until no table sees a change or one fails).
+ *   n_vars, var_lo[n_vars], var_size[n_vars]   the variables X and initial D
+ *   n_tables                                    <= 64
+ *   arity[n_tables], scopes = concatenated scope var ids (sum arity entries)
+ *   n_tuples[n_tables], tuples[k] = int32[n_tuples[k]][arity[k]] host arrays
+ *   out_dom (nullable): uint64[ct_model_dom_words] shared domains after the
+ *   root fixpoint (CT_OK) -- layout as the table domain bitmaps, one
+ *   word-aligned run per variable.
+ * Returns CT_OK, CT_FAIL (root wipe-out; the model is dead until
+ * ct_model_pop) or an error. */
+typedef struct ct_model ct_model;
+ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *var_size, int32_t n_tables,
+                          const int32_t *arity, const int32_t *scopes, const int64_t *n_tuples,
+                          const int32_t *const *tuples, const ct_config *cfg, ct_model **out,
+                          uint64_t *out_dom);
+int32_t ct_model_dom_words(const ct_model *m);
+int32_t ct_model_dom_word_offset(const ct_model *m, int32_t v);
+/* Synchronous.  dom_in (nullable, host uint64[Wg]): restrict the shared domains
+ * to dom_in (a search decision; values absent now stay absent), then propagate
+ * all tables to the common fixpoint.  out_dom (nullable) receives the shared
+ * domains on CT_OK.  On CT_FAIL the model is dead until ct_model_pop. */
+ct_status ct_model_fixpoint(ct_model *m, const uint64_t *dom_in, uint64_t *out_dom);
+ct_status ct_model_push(ct_model *m);   /* save the whole model state (trail level) */
+ct_status ct_model_pop(ct_model *m);    /* restore and drop the last saved state     */
+typedef struct ct_search_stats {
+  int64_t nodes;          /* fixpoint calls: the root plus every branch            */
+  int64_t failures;       /* of those, CT_FAIL                                      */
+  int64_t solutions;
+  int64_t table_calls;    /* non-no-op table propagations inside the fixpoints      */
+  int64_t iterations;     /* Jacobi rounds summed over the fixpoints                */
+  int64_t max_depth;
+  double device_ms;       /* kernel time summed over the fixpoints (%globaltimer)   */
+  uint64_t trace_hash;    /* FNV-1a over (depth, var, value, branch, status) per node */
+} ct_search_stats;
+/* Depth-first search with binary branching x = v / x != v,
+ * variable order input_order (lowest-index unbound variable), value order
+ * indomain_max (value_order = 0) or indomain_min (1), the paper's strategy
+ * (PAPER.md L469-477).  Stops after max_solutions solutions (<= 0: all) or
+ * max_nodes nodes (<= 0: no limit).  out_solution (nullable): int32[n_vars],
+ * the last solution found.  Returns CT_OK if a solution was found, CT_FAIL if
+ * the (explored part of the) tree has none, or an error.  The model's state is
+ * restored to what it was before the call. */
+ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
+                          int32_t *out_solution, ct_search_stats *out_stats);
+void ct_model_destroy(ct_model *m);
+
 /* ---------------------------------------------------------------- introspection */
 /* Test/measurement only.  currTable of this shard: host uint64[words]. */
 ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits);

@@ -145,3 +145,42 @@ class Batch:
         if getattr(self, "handle", None) and self.table.handle:
             C.ct_batch_destroy(self.handle)
         self.handle = None
+
+
+class Model:
+    """Several table constraints over shared variables (ct_model_*): on-device
+    Jacobi fixpoint per call, DFS search in the library."""
+
+    def __init__(self, var_lo, var_size, scopes, tables, device: int = 0, **cfg_kw):
+        self.var_lo = np.ascontiguousarray(var_lo, np.int32)
+        self.var_size = np.ascontiguousarray(var_size, np.int32)
+        cfg, self._keep = C.make_config(device, None, None, **cfg_kw)
+        self.root_status, self.handle, self.root_dom = C.ct_model_create(self.var_lo, self.var_size, scopes,
+                                                                         tables, cfg)
+        self.Wg = C.ct_model_dom_words(self.handle)
+
+    def fixpoint(self, dom_in=None):
+        out = np.zeros(max(self.Wg, 1), np.uint64)
+        din = None if dom_in is None else np.ascontiguousarray(dom_in, np.uint64)
+        st = C.ct_model_fixpoint(self.handle, din, out)
+        return st, (out[:self.Wg] if st == C.CT_OK else None)
+
+    def push(self):
+        C.ct_model_push(self.handle)
+
+    def pop(self):
+        C.ct_model_pop(self.handle)
+
+    def search(self, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1):
+        return C.ct_model_search(self.handle, int(self.var_size.size), value_order, max_nodes, max_solutions)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            C.ct_model_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -65,6 +65,7 @@ struct TableDev {
   int32_t policy;           // CT_POLICY_*
   int32_t use_res, use_index;
   int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
+  const int32_t *gword;     // [Wd] model tables only: global domain word of each domain word
 };
 
 // Per-state control block (device).  The first fields up to last_status persist
@@ -245,7 +246,7 @@ __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int
 // (x in s_sup, value in D_x); one block scan gives the ordered positions.
 template <int NT>
 __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
-                           int root_mode, uint64_t *smem) {
+                           int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
   uint64_t *s_din = smem;                       // D_x = dom ∧ ¬removed
@@ -284,7 +285,8 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
   // phase 1 (Alg. 1 L1-2): Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
   for (int k = tid; k < Wd; k += NT) {
     const uint64_t dm = st.dom[k];
-    const uint64_t rm = rem ? rem[k] : 0ull;
+    // model tables: a value is removed iff the shared (global) domain lost it
+    const uint64_t rm = gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull);
     const int x = tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     s_din[k] = di;
@@ -400,120 +402,145 @@ __device__ __forceinline__ uint32_t tile_lookback(unsigned long long *ts, int ti
   return excl;
 }
 
-// Block-level persistent loop over tiles of kUpdTPB index entries (16-byte
-// blocks, so every support/currTable access is an aligned 128-bit load).
-// Requires blockDim.x == kUpdTPB.
-__device__ void dev_update(const TableDev &tb, const StateDev &st) {
+// Per-call update parameters of one state (read once per block).
+struct UpdParams {
+  int go, nrows, L, ident, par, ntiles;
+};
+
+__device__ __forceinline__ UpdParams load_upd_params(const Ctl *c) {
+  UpdParams u;
+  u.go = !(__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast));
+  u.nrows = __ldcg(&c->nrows);
+  u.L = __ldcg(&c->L);
+  u.ident = __ldcg(&c->identity);
+  u.par = __ldcg(&c->parity);
+  u.ntiles = (u.L + kUpdTPB - 1) / kUpdTPB;
+  return u;
+}
+
+// One tile (kUpdTPB index entries = 16-byte blocks, so every support/currTable
+// access is an aligned 128-bit load) of one state's update, block-wide:
+// new currTable blocks, then the tile's slot in the order-preserving compaction
+// (chained scan over the state's tiles).  Requires blockDim.x == kUpdTPB.
+// s_woff[kUpdTPB/32] and s_excl are block-shared scratch.
+__device__ __forceinline__ void update_tile(const TableDev &tb, const StateDev &st, const UpdParams &u, int tile,
+                                            uint32_t *s_woff, uint32_t *s_excl, uint32_t &n_loads,
+                                            uint32_t &n_writes) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int s_go, s_tile, s_nrows, s_L, s_ident, s_par;
-  __shared__ uint32_t s_woff[kUpdTPB / 32];
-  __shared__ uint32_t s_excl;
-  if (tid == 0) {
-    s_go = !(__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast));
-    s_nrows = __ldcg(&c->nrows);
-    s_L = __ldcg(&c->L);
-    s_ident = __ldcg(&c->identity);
-    s_par = __ldcg(&c->parity);
-  }
-  __syncthreads();
-  if (!s_go) return;
-  const int nrows = s_nrows, L = s_L;
-  const int32_t *__restrict__ idx_in = s_par ? st.idx1 : st.idx0;
-  int32_t *__restrict__ idx_out = s_par ? st.idx0 : st.idx1;
+  const int nrows = u.nrows, L = u.L;
+  const int32_t *__restrict__ idx_in = u.par ? st.idx1 : st.idx0;
+  int32_t *__restrict__ idx_out = u.par ? st.idx0 : st.idx1;
   const bool compact = tb.use_index != 0;
-  const int ntiles = (L + kUpdTPB - 1) / kUpdTPB;
   const int32_t *__restrict__ ulist = st.ulist;
   const int64_t Wp = tb.Wp;
   ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
-  uint32_t n_loads = 0, n_writes = 0;
-
-  while (true) {
-    if (tid == 0) s_tile = atomicAdd(&c->tile_ctr, 1);
-    __syncthreads();
-    const int tile = s_tile;
-    if (tile >= ntiles) break;
-    const int k = tile * kUpdTPB + tid;
-    const bool valid = k < L;
-    int pid = 0;
-    ulonglong2 nt = make_ulonglong2(0ull, 0ull);
-    if (valid) {
-      pid = s_ident ? k : idx_in[k];
-      const ulonglong2 tw = T2[pid];
-      const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
-      uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-      uint32_t e[kUpdUnroll];
+  const int k = tile * kUpdTPB + tid;
+  const bool valid = k < L;
+  int pid = 0;
+  ulonglong2 nt = make_ulonglong2(0ull, 0ull);
+  if (valid) {
+    pid = u.ident ? k : idx_in[k];
+    const ulonglong2 tw = T2[pid];
+    const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+    uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+    uint32_t e[kUpdUnroll];
 #pragma unroll
-      for (int u = 0; u < kUpdUnroll; ++u) e[u] = (u < nrows) ? (uint32_t)ulist[u] : 0u;
-      for (int p = 0; p < nrows; p += kUpdUnroll) {
-        if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 128-bit block
-        ulonglong2 v[kUpdUnroll];
+    for (int q = 0; q < kUpdUnroll; ++q) e[q] = (q < nrows) ? (uint32_t)ulist[q] : 0u;
+    for (int p = 0; p < nrows; p += kUpdUnroll) {
+      if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 128-bit block
+      ulonglong2 v[kUpdUnroll];
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u)
-          v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
-        n_loads += 2 * min(kUpdUnroll, nrows - p);
-        uint32_t en[kUpdUnroll];
+      for (int q = 0; q < kUpdUnroll; ++q)
+        v[q] = (p + q < nrows) ? ld_sup2(col + (int64_t)(e[q] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
+      n_loads += 2 * min(kUpdUnroll, nrows - p);
+      uint32_t en[kUpdUnroll];
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u)
-          en[u] = (p + kUpdUnroll + u < nrows) ? (uint32_t)ulist[p + kUpdUnroll + u] : 0u;
+      for (int q = 0; q < kUpdUnroll; ++q)
+        en[q] = (p + kUpdUnroll + q < nrows) ? (uint32_t)ulist[p + kUpdUnroll + q] : 0u;
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u) {
-          if (p + u < nrows) {
-            ax |= v[u].x;
-            ay |= v[u].y;
-            if (e[u] & kEndBit) {
-              if (e[u] & kInvBit) {
-                mx &= ~ax;
-                my &= ~ay;
-              } else {
-                mx &= ax;
-                my &= ay;
-              }
-              ax = ay = 0;
+      for (int q = 0; q < kUpdUnroll; ++q) {
+        if (p + q < nrows) {
+          ax |= v[q].x;
+          ay |= v[q].y;
+          if (e[q] & kEndBit) {
+            if (e[q] & kInvBit) {
+              mx &= ~ax;
+              my &= ~ay;
+            } else {
+              mx &= ax;
+              my &= ay;
             }
+            ax = ay = 0;
           }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u) e[u] = en[u];
-      }
-      nt = make_ulonglong2(tw.x & mx, tw.y & my);
-      if (nt.x != tw.x || nt.y != tw.y) {
-        T2[pid] = nt;
-        ++n_writes;
-      }
+      for (int q = 0; q < kUpdUnroll; ++q) e[q] = en[q];
     }
-    const bool keep = valid && (nt.x | nt.y) != 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_woff[warp] = __popc(bal);
-    __syncthreads();
-    if (warp == 0) {
-      const uint32_t cnt = lane < kUpdTPB / 32 ? s_woff[lane] : 0u;
-      uint32_t x = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-      }
-      const uint32_t agg = __shfl_sync(0xffffffffu, x, kUpdTPB / 32 - 1);
-      if (lane < kUpdTPB / 32) s_woff[lane] = x - cnt;
-      uint32_t excl = 0;
-      if (compact) {
-        excl = tile_lookback(st.tilestat, tile, agg, lane);
-        if (lane == 0 && tile == ntiles - 1) c->L_out = (int32_t)(excl + agg);
-      } else if (lane == 0 && agg) {
-        atomicAdd(&c->L_out, (int32_t)agg);
-      }
-      if (lane == 0) s_excl = excl;
+    nt = make_ulonglong2(tw.x & mx, tw.y & my);
+    if (nt.x != tw.x || nt.y != tw.y) {
+      T2[pid] = nt;
+      ++n_writes;
     }
-    __syncthreads();
-    if (compact && keep) idx_out[s_excl + s_woff[warp] + __popc(bal & lanemask_lt())] = pid;
   }
+  const bool keep = valid && (nt.x | nt.y) != 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (lane == 0) s_woff[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t cnt = lane < kUpdTPB / 32 ? s_woff[lane] : 0u;
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t agg = __shfl_sync(0xffffffffu, x, kUpdTPB / 32 - 1);
+    if (lane < kUpdTPB / 32) s_woff[lane] = x - cnt;
+    uint32_t excl = 0;
+    if (compact) {
+      excl = tile_lookback(st.tilestat, tile, agg, lane);
+      if (lane == 0 && tile == u.ntiles - 1) c->L_out = (int32_t)(excl + agg);
+    } else if (lane == 0 && agg) {
+      atomicAdd(&c->L_out, (int32_t)agg);
+    }
+    if (lane == 0) *s_excl = excl;
+  }
+  __syncthreads();
+  if (compact && keep) idx_out[*s_excl + s_woff[warp] + __popc(bal & lanemask_lt())] = pid;
+  __syncthreads();   // s_woff / s_excl are reused by the next tile
+}
+
+__device__ __forceinline__ void flush_update_counts(Ctl *c, uint32_t n_loads, uint32_t n_writes) {
   n_loads = warp_sum_u32(n_loads);
   n_writes = warp_sum_u32(n_writes);
-  if (lane == 0 && (n_loads | n_writes)) {
+  if ((threadIdx.x & 31) == 0 && (n_loads | n_writes)) {
     atomicAdd(&c->upd_loads, (unsigned long long)n_loads);
     atomicAdd(&c->upd_writes, (unsigned long long)n_writes);
   }
+}
+
+// Block-level persistent loop over one state's tiles (atomic tile counter).
+__device__ void dev_update(const TableDev &tb, const StateDev &st) {
+  Ctl *c = st.ctl;
+  __shared__ UpdParams s_u;
+  __shared__ int s_tile;
+  __shared__ uint32_t s_woff[kUpdTPB / 32];
+  __shared__ uint32_t s_excl;
+  if (threadIdx.x == 0) s_u = load_upd_params(c);
+  __syncthreads();
+  const UpdParams u = s_u;
+  if (!u.go) return;
+  uint32_t n_loads = 0, n_writes = 0;
+  while (true) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&c->tile_ctr, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    if (tile >= u.ntiles) break;
+    update_tile(tb, st, u, tile, s_woff, &s_excl, n_loads, n_writes);
+  }
+  flush_update_counts(c, n_loads, n_writes);
 }
 
 // ------------------------------------------------------------------ a6: filter
@@ -559,84 +586,102 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
   return -1;
 }
 
-// Warp-level: items gw, gw + nw, ...: residue probe, then the
-// first kFirstScan index entries; items still unresolved go to the scan list.
-// The block with gw == 0 also publishes this shard's "non-empty" flag.
-__device__ void dev_probe(const TableDev &tb, const StateDev &st, int gw, int nw) {
-  Ctl *c = st.ctl;
-  if (__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast)) return;
-  const int Lout = __ldcg(&c->L_out);
-  if (gw == 0 && (threadIdx.x & 31) == 0) st.sup[tb.R] = Lout > 0;
-  if (Lout == 0) return;
-  const int lane = threadIdx.x & 31;
-  const int nitems = __ldcg(&c->nitems);
-  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+// Per-call filter parameters of one state.
+struct FiltParams {
+  int go, Lout, nitems, nscan, L;
+  const int32_t *idx;   // index written by this call's update (nullptr: identity)
+};
+
+__device__ __forceinline__ FiltParams load_filt_params(const TableDev &tb, const StateDev &st) {
+  const Ctl *c = st.ctl;
+  FiltParams f;
+  f.go = !(__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast));
+  f.Lout = __ldcg(&c->L_out);
+  f.nitems = __ldcg(&c->nitems);
+  f.nscan = __ldcg(&c->nscan);
   const bool compact = tb.use_index != 0;
-  const int32_t *__restrict__ idx = compact ? (__ldcg(&c->parity) ? st.idx0 : st.idx1) : nullptr;
-  const int L = compact ? Lout : tb.W2;
-  uint32_t n_loads = 0;
-  for (int item = gw; item < nitems; item += nw) {
-    const int row = __ldcg(st.items + item);
-    const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
-    if (tb.use_res) {
-      int hit = 0;
-      if (lane == 0) {
-        const int r = st.res[row];
-        const ulonglong2 t = __ldcg(T2 + r);
-        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
-        hit = ((t.x & s.x) | (t.y & s.y)) != 0;
-      }
-      if (__shfl_sync(0xffffffffu, hit, 0)) {
-        if (lane == 0) st.sup[row] = 1;
-        continue;
-      }
-    }
-    const int hit = scan_pairs(idx, T2, srow, 0, min(L, kFirstScan), nullptr, lane, n_loads);
-    if (lane == 0) {
-      if (hit >= 0) {
-        st.sup[row] = 1;
-        st.res[row] = hit;
-      } else if (L > kFirstScan) {
-        st.scanlist[atomicAdd(&c->nscan, 1)] = row;
-      }
-    }
-  }
-  if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
+  f.idx = compact ? (__ldcg(&c->parity) ? st.idx0 : st.idx1) : nullptr;
+  f.L = compact ? f.Lout : tb.W2;
+  return f;
 }
 
-// Warp-level: (miss, chunk) units gw, gw + nw, ... over index entries
-// [kFirstScan, L), chunk-major so early chunks of every item go first; every
-// round re-checks the item's flag so late chunks stop once any chunk hit.
-__device__ void dev_scan(const TableDev &tb, const StateDev &st, int gw, int nw) {
-  Ctl *c = st.ctl;
-  if (__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast)) return;
-  const int nscan = __ldcg(&c->nscan);
-  const int Lout = __ldcg(&c->L_out);
-  if (nscan == 0 || Lout == 0) return;
-  const bool compact = tb.use_index != 0;
-  const int32_t *__restrict__ idx = compact ? (__ldcg(&c->parity) ? st.idx0 : st.idx1) : nullptr;
-  const int L = compact ? Lout : tb.W2;
-  if (L <= kFirstScan) return;
+// Warp-level, one (x,a) item: residue probe, then the first
+// kFirstScan index entries; an item still unresolved goes to the scan list.
+__device__ __forceinline__ void probe_item(const TableDev &tb, const StateDev &st, const FiltParams &f, int item,
+                                           uint32_t &n_loads) {
   const int lane = threadIdx.x & 31;
-  const int64_t nch = (L - kFirstScan + kScanChunk - 1) / kScanChunk;
-  const int64_t total = nch * nscan;
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-  uint32_t n_loads = 0;
-  for (int64_t u = gw; u < total; u += nw) {
-    const int chunk = (int)(u / nscan);
-    const int item = (int)(u - (int64_t)chunk * nscan);
-    const int row = __ldcg(st.scanlist + item);
-    const int f = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
-    if (__shfl_sync(0xffffffffu, f, 0)) continue;
-    const int k0 = kFirstScan + chunk * kScanChunk;
-    const int k1 = min(k0 + kScanChunk, L);
-    const int hit = scan_pairs(idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, st.sup + row, lane, n_loads);
-    if (hit >= 0 && lane == 0) {
-      st.sup[row] = 1;
-      st.res[row] = hit;
+  const int row = __ldcg(st.items + item);
+  const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+  if (tb.use_res) {
+    int hit = 0;
+    if (lane == 0) {
+      const int r = st.res[row];
+      const ulonglong2 t = __ldcg(T2 + r);
+      const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
+      hit = ((t.x & s.x) | (t.y & s.y)) != 0;
+    }
+    if (__shfl_sync(0xffffffffu, hit, 0)) {
+      if (lane == 0) st.sup[row] = 1;
+      return;
     }
   }
-  if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
+  const int hit = scan_pairs(f.idx, T2, srow, 0, min(f.L, kFirstScan), nullptr, lane, n_loads);
+  if (lane == 0) {
+    if (hit >= 0) {
+      st.sup[row] = 1;
+      st.res[row] = hit;
+    } else if (f.L > kFirstScan) {
+      st.scanlist[atomicAdd(&st.ctl->nscan, 1)] = row;
+    }
+  }
+}
+
+// Warp-level, one (miss, chunk) unit over index entries [kFirstScan, L).
+__device__ __forceinline__ void scan_unit(const TableDev &tb, const StateDev &st, const FiltParams &f, int64_t u,
+                                          uint32_t &n_loads) {
+  const int lane = threadIdx.x & 31;
+  const int chunk = (int)(u / f.nscan);
+  const int item = (int)(u - (int64_t)chunk * f.nscan);
+  const int row = __ldcg(st.scanlist + item);
+  const int fl = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
+  if (__shfl_sync(0xffffffffu, fl, 0)) return;
+  const int k0 = kFirstScan + chunk * kScanChunk;
+  const int k1 = min(k0 + kScanChunk, f.L);
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  const int hit = scan_pairs(f.idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, st.sup + row, lane, n_loads);
+  if (hit >= 0 && lane == 0) {
+    st.sup[row] = 1;
+    st.res[row] = hit;
+  }
+}
+
+__device__ __forceinline__ int64_t scan_units(const FiltParams &f) {
+  if (!f.go || f.nscan == 0 || f.Lout == 0 || f.L <= kFirstScan) return 0;
+  return (int64_t)((f.L - kFirstScan + kScanChunk - 1) / kScanChunk) * f.nscan;
+}
+
+// Warp-level: items gw, gw + nw, ... of one state.  The warp with gw == 0 also
+// publishes this shard's "non-empty" flag.
+__device__ void dev_probe(const TableDev &tb, const StateDev &st, int gw, int nw) {
+  const FiltParams f = load_filt_params(tb, st);
+  if (!f.go) return;
+  if (gw == 0 && (threadIdx.x & 31) == 0) st.sup[tb.R] = f.Lout > 0;
+  if (f.Lout == 0) return;
+  uint32_t n_loads = 0;
+  for (int item = gw; item < f.nitems; item += nw) probe_item(tb, st, f, item, n_loads);
+  if ((threadIdx.x & 31) == 0 && n_loads) atomicAdd(&st.ctl->scan_loads, (unsigned long long)n_loads);
+}
+
+// Warp-level: (miss, chunk) units gw, gw + nw, ... chunk-major so early chunks
+// of every item go first; every round re-checks the item's flag so late chunks
+// stop once any chunk hit.
+__device__ void dev_scan(const TableDev &tb, const StateDev &st, int gw, int nw) {
+  const FiltParams f = load_filt_params(tb, st);
+  const int64_t total = scan_units(f);
+  uint32_t n_loads = 0;
+  for (int64_t u = gw; u < total; u += nw) scan_unit(tb, st, f, u, n_loads);
+  if ((threadIdx.x & 31) == 0 && n_loads) atomicAdd(&st.ctl->scan_loads, (unsigned long long)n_loads);
 }
 
 // ------------------------------------------------------------------ a6c-a8: finalize (one block)
@@ -727,7 +772,7 @@ __global__ void __launch_bounds__(kIngestTPB) k_ingest(TableDev tb, const StateD
 }
 
 // grid (blocks, S), kUpdTPB threads.
-__global__ void __launch_bounds__(kUpdTPB) k_update(TableDev tb, const StateDev *__restrict__ states) {
+__global__ void __launch_bounds__(kUpdTPB, 3) k_update(TableDev tb, const StateDev *__restrict__ states) {
   dev_update(tb, states[blockIdx.y]);
 }
 

@@ -16,6 +16,7 @@
 
 #include "ct.h"
 #include "ct_kernels.cuh"
+#include "ct_model.cuh"
 
 using namespace ctk;
 
@@ -1046,5 +1047,429 @@ ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset
   }
   return CT_OK;
 }
+
+}  // extern "C"
+
+// ================================================================== models (f1)
+struct ct_model {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int nv = 0, ntab = 0, Wg = 0;
+  std::vector<int32_t> vlo, vd, gOff;
+  std::vector<ct_table *> tabs;
+  std::vector<size_t> off;        // table k's state block inside the pool
+  char *pool = nullptr;           // all table states + shared domains (snapshot unit)
+  size_t pool_bytes = 0, gdom_off = 0;
+  char *meta = nullptr;           // TableDev[ntab] | StateDev[ntab] | ModelCtl | gword arrays
+  size_t meta_bytes = 0;
+  ModelDev md{};
+  uint64_t *h_in = nullptr, *h_out = nullptr, *d_in = nullptr, *d_out = nullptr;   // mapped pinned
+  int grid = 1;
+  size_t smem = 0;
+  std::vector<char *> snaps;      // device snapshot buffers, one per trail level
+  std::vector<std::vector<uint64_t>> mirrors;
+  int depth = 0;
+  bool dead = false;
+  std::vector<uint64_t> dom;      // host mirror of the shared domains
+  // last fixpoint's counters
+  int64_t last_iters = 0, last_calls = 0, last_ns = 0;
+};
+
+static void model_free(ct_model *m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  if (m->stream) cudaStreamSynchronize(m->stream);
+  for (char *sn : m->snaps) cudaFree(sn);
+  if (m->pool) cudaFree(m->pool);
+  if (m->meta) cudaFree(m->meta);
+  if (m->h_in) cudaFreeHost(m->h_in);
+  if (m->h_out) cudaFreeHost(m->h_out);
+  for (ct_table *t : m->tabs) free_table(t);
+  if (m->own_stream && m->stream) cudaStreamDestroy(m->stream);
+  delete m;
+}
+
+static ct_status model_launch(ct_model *m, bool with_input) {
+  *(volatile int32_t *)m->h_out = kPendingStatus;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)m->grid);
+  lc.blockDim = dim3(kFusedTPB);
+  lc.dynamicSmemBytes = m->smem;
+  lc.stream = m->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&lc, k_model_fixpoint, m->md, (const uint64_t *)(with_input ? m->d_in : nullptr),
+                              m->d_out, 1 << 20));
+  volatile int32_t *st = (volatile int32_t *)m->h_out;
+  for (uint64_t spin = 1;; ++spin) {
+    if (*st != kPendingStatus) break;
+    if ((spin & 1023) == 0) {
+      const cudaError_t e = cudaStreamQuery(m->stream);
+      if (e == cudaSuccess && *st == kPendingStatus) return fail(CT_ECUDA, "model fixpoint ended without a status");
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        return fail(CT_ECUDA, "model fixpoint failed: %s", cudaGetErrorString(e));
+    }
+  }
+  const int32_t status = *st;
+  m->last_iters = (int64_t)m->h_out[1];
+  m->last_calls = (int64_t)m->h_out[2];
+  m->last_ns = (int64_t)m->h_out[3];
+  if (status == 0) {
+    memcpy(m->dom.data(), m->h_out + 4, (size_t)m->Wg * 8);
+    return CT_OK;
+  }
+  m->dead = true;
+  return CT_FAIL;
+}
+
+extern "C" {
+
+ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *var_size, int32_t n_tables,
+                          const int32_t *arity, const int32_t *scopes, const int64_t *n_tuples,
+                          const int32_t *const *tuples, const ct_config *cfg_in, ct_model **out,
+                          uint64_t *out_dom) {
+  if (!out) return fail(CT_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_vars < 1 || !var_lo || !var_size) return fail(CT_EINVAL, "bad variables");
+  if (n_tables < 1 || n_tables > kMaxModelTables) return fail(CT_EINVAL, "n_tables must be in [1, %d]", kMaxModelTables);
+  if (!arity || !scopes || !n_tuples || !tuples) return fail(CT_EINVAL, "NULL table arrays");
+  ct_config cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else ct_config_init(&cfg);
+  if (cfg.n_shards != 1) return fail(CT_EINVAL, "models of sharded tables are not supported");
+  ct_model *m = new (std::nothrow) ct_model();
+  if (!m) return fail(CT_ENOMEM, "host allocation failed");
+  auto bail = [&](ct_status s) {
+    model_free(m);
+    return s;
+  };
+  m->device = cfg.device;
+  m->nv = n_vars;
+  m->ntab = n_tables;
+  m->vlo.assign(var_lo, var_lo + n_vars);
+  m->vd.assign(var_size, var_size + n_vars);
+  m->gOff.assign(n_vars + 1, 0);
+  for (int v = 0; v < n_vars; ++v) {
+    if (var_size[v] < 1) return bail(fail(CT_EINVAL, "var_size[%d] must be >= 1", v));
+    m->gOff[v + 1] = m->gOff[v] + (var_size[v] + 63) / 64;
+  }
+  m->Wg = m->gOff[n_vars];
+  DeviceGuard g(m->device);
+  if (cfg.stream) {
+    m->stream = (cudaStream_t)cfg.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(CT_ECUDA, "stream creation failed"));
+    m->own_stream = true;
+  }
+  cfg.stream = m->stream;
+  cfg.use_graph = 0;
+  cfg.alloc = nullptr;   // the model owns its memory (plain cudaMalloc)
+  // ---- tables (each built and propagated at its own root)
+  std::vector<uint64_t> gdom(m->Wg, 0ull);
+  for (int v = 0; v < n_vars; ++v)
+    for (int a = 0; a < var_size[v]; ++a) gdom[m->gOff[v] + a / 64] |= 1ull << (a % 64);
+  std::vector<ct_state *> roots;
+  bool root_fail = false;
+  const int32_t *sc = scopes;
+  for (int k = 0; k < n_tables; ++k) {
+    const int n = arity[k];
+    if (n < 1) return bail(fail(CT_EINVAL, "arity[%d] must be >= 1", k));
+    std::vector<int32_t> lo(n), d(n);
+    for (int i = 0; i < n; ++i) {
+      if (sc[i] < 0 || sc[i] >= n_vars) return bail(fail(CT_EINVAL, "scope of table %d names var %d", k, sc[i]));
+      lo[i] = var_lo[sc[i]];
+      d[i] = var_size[sc[i]];
+    }
+    ct_table *t = nullptr;
+    ct_state *r = nullptr;
+    ct_status s = ct_create(n, sc, lo.data(), d.data(), nullptr, n_tuples[k], tuples[k], &cfg, &t, &r, nullptr);
+    if (s < 0) {
+      for (ct_state *x : roots) free_state_mem(x);
+      return bail(s);
+    }
+    m->tabs.push_back(t);
+    roots.push_back(r);
+    if (s == CT_FAIL) root_fail = true;
+    sc += n;
+  }
+  // ---- pool: every table state + the shared domains
+  size_t o = 0;
+  for (int k = 0; k < n_tables; ++k) {
+    m->off.push_back(o);
+    o += (size_t)round_up((int64_t)m->tabs[k]->lay.total, 256);
+  }
+  m->gdom_off = o;
+  o += (size_t)round_up((int64_t)m->Wg * 8, 256);
+  m->pool_bytes = o;
+  if (cudaMalloc(&m->pool, m->pool_bytes) != cudaSuccess) {
+    for (ct_state *x : roots) free_state_mem(x);
+    return bail(fail(CT_ENOMEM, "model pool allocation failed"));
+  }
+  for (int k = 0; k < n_tables; ++k) {
+    cudaMemcpyAsync(m->pool + m->off[k], roots[k]->mem, m->tabs[k]->lay.persist, cudaMemcpyDeviceToDevice, m->stream);
+  }
+  cudaStreamSynchronize(m->stream);
+  // root domains of each table -> shared domains
+  sc = scopes;
+  for (int k = 0; k < n_tables; ++k) {
+    ct_table *t = m->tabs[k];
+    std::vector<uint64_t> rd(std::max(t->Wd, 1));
+    if (!root_fail) {
+      if (ct_state_read_dom(roots[k], rd.data()) != CT_OK) {
+        for (ct_state *x : roots) free_state_mem(x);
+        return bail(CT_ECUDA);
+      }
+      for (int i = 0; i < t->n; ++i)
+        for (int w = t->domOff[i]; w < t->domOff[i + 1]; ++w) gdom[m->gOff[sc[i]] + (w - t->domOff[i])] &= rd[w];
+    }
+    sc += t->n;
+  }
+  for (ct_state *x : roots) free_state_mem(x);
+  // ---- device metadata
+  const size_t tdev = sizeof(TableDev) * n_tables, sdev = sizeof(StateDev) * n_tables;
+  size_t gw_total = 0;
+  for (ct_table *t : m->tabs) gw_total += (size_t)std::max(t->Wd, 1);
+  m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + gw_total * 4;
+  if (cudaMalloc(&m->meta, m->meta_bytes) != cudaSuccess) return bail(fail(CT_ENOMEM, "model metadata allocation failed"));
+  cudaMemset(m->meta, 0, m->meta_bytes);
+  TableDev *d_tabs = (TableDev *)m->meta;
+  StateDev *d_sts = (StateDev *)(m->meta + tdev);
+  ModelCtl *d_mc = (ModelCtl *)(m->meta + round_up((int64_t)(tdev + sdev), 256));
+  int32_t *d_gw = (int32_t *)((char *)d_mc + 256);
+  std::vector<TableDev> htabs(n_tables);
+  std::vector<StateDev> hsts(n_tables);
+  sc = scopes;
+  size_t gpos = 0;
+  for (int k = 0; k < n_tables; ++k) {
+    ct_table *t = m->tabs[k];
+    std::vector<int32_t> gw(std::max(t->Wd, 1), 0);
+    for (int i = 0; i < t->n; ++i)
+      for (int w = t->domOff[i]; w < t->domOff[i + 1]; ++w) gw[w] = m->gOff[sc[i]] + (w - t->domOff[i]);
+    cudaMemcpy(d_gw + gpos, gw.data(), gw.size() * 4, cudaMemcpyHostToDevice);
+    htabs[k] = t->dev;
+    htabs[k].gword = d_gw + gpos;
+    hsts[k] = make_desc(t, m->pool + m->off[k]);
+    gpos += gw.size();
+    sc += t->n;
+  }
+  cudaMemcpy(d_tabs, htabs.data(), tdev, cudaMemcpyHostToDevice);
+  cudaMemcpy(d_sts, hsts.data(), sdev, cudaMemcpyHostToDevice);
+  cudaMemcpy(m->pool + m->gdom_off, gdom.data(), (size_t)m->Wg * 8, cudaMemcpyHostToDevice);
+  m->md.ntab = n_tables;
+  m->md.Wg = m->Wg;
+  m->md.tabs = d_tabs;
+  m->md.sts = d_sts;
+  m->md.gdom = (uint64_t *)(m->pool + m->gdom_off);
+  m->md.mc = d_mc;
+  m->dom = gdom;
+  // ---- launch geometry
+  size_t smem = 0;
+  int tiles = 0;
+  for (ct_table *t : m->tabs) {
+    smem = std::max({smem, ingest_smem_bytes(t->n, t->Wd), finalize_smem_bytes(t->n, t->Wd)});
+    tiles += t->dev.ntiles_max;
+  }
+  m->smem = smem;
+  CUDA_TRY(cudaFuncSetAttribute(k_model_fixpoint, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max<size_t>(smem, 1)));
+  int occ = 0, sms = 148;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_model_fixpoint, kFusedTPB, smem));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+  if (occ < 1) return bail(fail(CT_EINVAL, "model kernel does not fit on an SM"));
+  m->grid = std::min(sms * occ, std::max(sms, tiles));
+  if (cudaHostAlloc((void **)&m->h_in, (size_t)std::max(m->Wg, 1) * 8, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostAlloc((void **)&m->h_out, (size_t)(4 + m->Wg) * 8, cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&m->d_in, m->h_in, 0) != cudaSuccess ||
+      cudaHostGetDevicePointer((void **)&m->d_out, m->h_out, 0) != cudaSuccess)
+    return bail(fail(CT_ENOMEM, "mapped pinned allocation failed"));
+  *out = m;
+  if (root_fail) {
+    m->dead = true;
+    return CT_FAIL;
+  }
+  ct_status s = model_launch(m, false);
+  if (s < 0) {
+    *out = nullptr;
+    return bail(s);
+  }
+  if (s == CT_OK && out_dom) memcpy(out_dom, m->dom.data(), (size_t)m->Wg * 8);
+  return s;
+}
+
+int32_t ct_model_dom_words(const ct_model *m) { return m ? m->Wg : -1; }
+int32_t ct_model_dom_word_offset(const ct_model *m, int32_t v) {
+  if (!m || v < 0 || v >= m->nv) return -1;
+  return m->gOff[v];
+}
+
+ct_status ct_model_fixpoint(ct_model *m, const uint64_t *dom_in, uint64_t *out_dom) {
+  if (!m) return fail(CT_EINVAL, "NULL model");
+  if (m->dead) return fail(CT_ESTATE, "model is dead (last fixpoint failed); ct_model_pop restores it");
+  DeviceGuard g(m->device);
+  if (dom_in)
+    for (int w = 0; w < m->Wg; ++w) m->h_in[w] = m->dom[w] & dom_in[w];
+  const ct_status s = model_launch(m, dom_in != nullptr);
+  if (s == CT_OK && out_dom) memcpy(out_dom, m->dom.data(), (size_t)m->Wg * 8);
+  return s;
+}
+
+ct_status ct_model_push(ct_model *m) {
+  if (!m) return fail(CT_EINVAL, "NULL model");
+  DeviceGuard g(m->device);
+  if ((int)m->snaps.size() <= m->depth) {
+    char *p = nullptr;
+    if (cudaMalloc(&p, m->pool_bytes) != cudaSuccess) return fail(CT_ENOMEM, "snapshot allocation failed");
+    m->snaps.push_back(p);
+  }
+  CUDA_TRY(cudaMemcpyAsync(m->snaps[m->depth], m->pool, m->pool_bytes, cudaMemcpyDeviceToDevice, m->stream));
+  if ((int)m->mirrors.size() <= m->depth) m->mirrors.emplace_back();
+  m->mirrors[m->depth] = m->dom;
+  m->depth++;
+  return CT_OK;
+}
+
+ct_status ct_model_pop(ct_model *m) {
+  if (!m) return fail(CT_EINVAL, "NULL model");
+  if (m->depth == 0) return fail(CT_EINVAL, "ct_model_pop without a matching push");
+  DeviceGuard g(m->device);
+  m->depth--;
+  CUDA_TRY(cudaMemcpyAsync(m->pool, m->snaps[m->depth], m->pool_bytes, cudaMemcpyDeviceToDevice, m->stream));
+  m->dom = m->mirrors[m->depth];
+  m->dead = false;
+  return CT_OK;
+}
+
+namespace {
+struct Dfs {
+  ct_model *m;
+  int value_order;
+  int64_t max_nodes, max_solutions;
+  ct_search_stats st{};
+  std::vector<int32_t> sol;
+  bool stop = false;
+  ct_status err = CT_OK;
+
+  void hash(uint64_t x) {
+    for (int i = 0; i < 8; ++i) {
+      st.trace_hash ^= (x >> (8 * i)) & 0xff;
+      st.trace_hash *= 1099511628211ull;
+    }
+  }
+  void account(int depth, int var, int val, int branch, ct_status s) {
+    st.nodes++;
+    if (s == CT_FAIL) st.failures++;
+    st.table_calls += m->last_calls;
+    st.iterations += m->last_iters;
+    st.device_ms += m->last_ns * 1e-6;
+    if (depth > st.max_depth) st.max_depth = depth;
+    hash((uint64_t)depth);
+    hash((uint64_t)(int64_t)var);
+    hash((uint64_t)(int64_t)val);
+    hash((uint64_t)branch);
+    hash((uint64_t)s);
+  }
+  // the model is at an OK fixpoint here
+  void node(int depth) {
+    if (stop) return;
+    int x = -1;   // input_order: the lowest-index unbound variable
+    for (int v = 0; v < m->nv && x < 0; ++v) {
+      int c = 0;
+      for (int w = m->gOff[v]; w < m->gOff[v + 1]; ++w) c += __builtin_popcountll(m->dom[w]);
+      if (c > 1) x = v;
+    }
+    if (x < 0) {   // every variable bound: a solution
+      st.solutions++;
+      for (int v = 0; v < m->nv; ++v) {
+        int a = 0;
+        for (int w = m->gOff[v]; w < m->gOff[v + 1]; ++w)
+          if (m->dom[w]) a = (w - m->gOff[v]) * 64 + __builtin_ctzll(m->dom[w]);
+        sol[v] = m->vlo[v] + a;
+      }
+      if (max_solutions > 0 && st.solutions >= max_solutions) stop = true;
+      return;
+    }
+    // value: indomain_max (0) or indomain_min (1)
+    int a = -1;
+    if (value_order == 0) {
+      for (int w = m->gOff[x + 1] - 1; w >= m->gOff[x] && a < 0; --w)
+        if (m->dom[w]) a = (w - m->gOff[x]) * 64 + 63 - __builtin_clzll(m->dom[w]);
+    } else {
+      for (int w = m->gOff[x]; w < m->gOff[x + 1] && a < 0; ++w)
+        if (m->dom[w]) a = (w - m->gOff[x]) * 64 + __builtin_ctzll(m->dom[w]);
+    }
+    const int val = m->vlo[x] + a;
+    const int wa = m->gOff[x] + a / 64;
+    const uint64_t bit = 1ull << (a % 64);
+    for (int branch = 0; branch < 2 && !stop; ++branch) {
+      if (max_nodes > 0 && st.nodes >= max_nodes) {
+        stop = true;
+        return;
+      }
+      ct_status s = ct_model_push(m);
+      if (s < 0) {
+        err = s;
+        stop = true;
+        return;
+      }
+      std::vector<uint64_t> din(m->dom);
+      if (branch == 0) {       // x = val
+        for (int w = m->gOff[x]; w < m->gOff[x + 1]; ++w) din[w] = 0;
+        din[wa] = bit;
+      } else {                 // x != val
+        din[wa] &= ~bit;
+      }
+      s = ct_model_fixpoint(m, din.data(), nullptr);
+      if (s < 0) {
+        err = s;
+        stop = true;
+        return;
+      }
+      account(depth + 1, x, val, branch, s);
+      if (s == CT_OK) node(depth + 1);
+      if (ct_model_pop(m) < 0) {
+        err = CT_ECUDA;
+        stop = true;
+        return;
+      }
+    }
+  }
+};
+}  // namespace
+
+ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
+                          int32_t *out_solution, ct_search_stats *out_stats) {
+  if (!m) return fail(CT_EINVAL, "NULL model");
+  if (value_order < 0 || value_order > 1) return fail(CT_EINVAL, "value_order must be 0 (max) or 1 (min)");
+  Dfs d;
+  d.m = m;
+  d.value_order = value_order;
+  d.max_nodes = max_nodes;
+  d.max_solutions = max_solutions;
+  d.sol.assign(m->nv, 0);
+  d.st.trace_hash = 1469598103934665603ull;
+  if (m->dead) {
+    d.account(0, -1, 0, 2, CT_FAIL);
+  } else {
+    // the root is the model's current fixpoint (re-run: counts as the root node)
+    ct_status s = ct_model_push(m);
+    if (s < 0) return s;
+    s = ct_model_fixpoint(m, nullptr, nullptr);
+    if (s < 0) return s;
+    d.account(0, -1, 0, 2, s);
+    if (s == CT_OK) d.node(0);
+    if (ct_model_pop(m) < 0) return CT_ECUDA;
+  }
+  if (d.err < 0) return d.err;
+  if (out_stats) *out_stats = d.st;
+  if (d.st.solutions > 0 && out_solution) memcpy(out_solution, d.sol.data(), (size_t)m->nv * 4);
+  return d.st.solutions > 0 ? CT_OK : CT_FAIL;
+}
+
+void ct_model_destroy(ct_model *m) { model_free(m); }
 
 }  // extern "C"

@@ -68,6 +68,12 @@ class ct_stats(ctypes.Structure):
                 ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 5)]
 
 
+class ct_search_stats(ctypes.Structure):
+    _fields_ = [("nodes", ctypes.c_int64), ("failures", ctypes.c_int64), ("solutions", ctypes.c_int64),
+                ("table_calls", ctypes.c_int64), ("iterations", ctypes.c_int64), ("max_depth", ctypes.c_int64),
+                ("device_ms", ctypes.c_double), ("trace_hash", ctypes.c_uint64)]
+
+
 class ct_kernel_times(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 8), ("ms", ctypes.c_double * 8)]
 
@@ -112,6 +118,14 @@ SIGNATURES = {
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
     "ct_table_profile_read": (I32, [P, P, I32]),
+    "ct_model_create": (I32, [I32, P, P, I32, P, P, P, P, P, P, P]),
+    "ct_model_dom_words": (I32, [P]),
+    "ct_model_dom_word_offset": (I32, [P, I32]),
+    "ct_model_fixpoint": (I32, [P, P, P]),
+    "ct_model_push": (I32, [P]),
+    "ct_model_pop": (I32, [P]),
+    "ct_model_search": (I32, [P, I32, I64, I64, P, P]),
+    "ct_model_destroy": (None, [P]),
     "ct_last_error": (ctypes.c_char_p, []),
     "ct_version": (ctypes.c_char_p, []),
 }
@@ -390,3 +404,53 @@ def ct_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(lib().ct_nccl_unique_id(buf), allow_fail=False)
     return buf.raw
+
+
+# ---------------------------------------------------------------- models (several tables)
+def ct_model_create(var_lo, var_size, scopes, tables, cfg=None):
+    """scopes: list of int arrays; tables: list of int32[t_k][arity_k].
+    Returns (status, model, shared_dom uint64[Wg] or None)."""
+    vlo = np.ascontiguousarray(var_lo, np.int32)
+    vd = np.ascontiguousarray(var_size, np.int32)
+    ar = np.array([len(s) for s in scopes], np.int32)
+    sc = np.ascontiguousarray(np.concatenate([np.asarray(s, np.int32) for s in scopes]), np.int32)
+    tb = [np.ascontiguousarray(t, np.int32) for t in tables]
+    nt = np.array([t.shape[0] for t in tb], np.int64)
+    ptrs = (ctypes.c_void_p * len(tb))(*[t.ctypes.data if t.size else 0 for t in tb])
+    wg = int(((vd.astype(np.int64) + 63) // 64).sum())
+    out_dom = np.zeros(max(wg, 1), np.uint64)
+    m = ctypes.c_void_p()
+    st = lib().ct_model_create(int(vd.size), _np_ptr(vlo), _np_ptr(vd), len(tb), _np_ptr(ar), _np_ptr(sc),
+                               _np_ptr(nt), ctypes.cast(ptrs, ctypes.c_void_p),
+                               ctypes.byref(cfg) if cfg is not None else None, ctypes.byref(m), _np_ptr(out_dom))
+    _check(st)
+    return st, m, (out_dom[:wg] if st == CT_OK else None)
+
+
+def ct_model_dom_words(model) -> int:
+    return int(lib().ct_model_dom_words(model))
+
+
+def ct_model_fixpoint(model, dom_in, out_dom) -> int:
+    return _check(lib().ct_model_fixpoint(model, _np_ptr(dom_in), _np_ptr(out_dom)))
+
+
+def ct_model_push(model) -> None:
+    _check(lib().ct_model_push(model), allow_fail=False)
+
+
+def ct_model_pop(model) -> None:
+    _check(lib().ct_model_pop(model), allow_fail=False)
+
+
+def ct_model_search(model, n_vars: int, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1):
+    """Returns (status, solution int32[n_vars] or None, ct_search_stats)."""
+    sol = np.zeros(n_vars, np.int32)
+    stats = ct_search_stats()
+    st = _check(lib().ct_model_search(model, value_order, max_nodes, max_solutions, _np_ptr(sol),
+                                      ctypes.byref(stats)))
+    return st, (sol if st == CT_OK else None), stats
+
+
+def ct_model_destroy(model) -> None:
+    lib().ct_model_destroy(model)

@@ -1,0 +1,85 @@
+"""GPU parity of the multi-table model: the on-device Jacobi
+fixpoint and the library's DFS vs the oracle (oracle.fixpoint / oracle.dfs),
+bit-exact: same fixpoint domains, same FAIL verdicts, same node trace."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle.dfs import dfs as oracle_dfs
+from paper_2507_18413_b200 import CT_OK, CT_FAIL, CT_ESTATE, CTError, Model
+from workloads import Rng, member_to_bitmap, bitmap_to_member, table1
+from workloads.csp import csp_model
+
+pytestmark = pytest.mark.gpu
+
+
+def _model(m):
+    return Model(m["vlo"], m["vd"], m["scopes"], m["tables"])
+
+
+def test_table1_model_first_solution():
+    p = table1()
+    M = Model(p.lo, p.d, [np.arange(3)], [p.tuples])
+    st, sol, stats = M.search(value_order=0, max_solutions=1)
+    assert st == CT_OK and sol.tolist() == [3, 4, 3]          # SPEC S:L394 (derived)
+    ref = oracle_dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=1)
+    assert (stats.nodes, stats.failures, stats.trace_hash) == (ref["nodes"], ref["failures"], ref["trace_hash"])
+    st, sol, stats = M.search(value_order=0, max_solutions=0)
+    assert stats.solutions == 5
+    M.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_model_fixpoints(seed):
+    """Root fixpoint and random restrictions vs oracle.fixpoint."""
+    m = csp_model(8, 12, 5, 3000, seed=seed, arities=[3, 4, 2, 5, 3])
+    M = _model(m)
+    ok, root = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], np.ones(int(m["vd"].sum()), np.uint8))
+    assert (M.root_status == CT_OK) == ok
+    if not ok:
+        M.close()
+        return
+    assert np.array_equal(bitmap_to_member(M.root_dom, m["vd"]), root)
+    rng = Rng(100 + seed)
+    for trial in range(30):
+        keep = (rng.uniform(root.size, 4) > 0).astype(np.uint8)
+        din = root & keep
+        ok, dout = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], din)
+        M.push()
+        st, gd = M.fixpoint(member_to_bitmap(din, m["vd"]))
+        assert st == (CT_OK if ok else CT_FAIL), trial
+        if ok:
+            assert np.array_equal(bitmap_to_member(gd, m["vd"]), dout), trial
+        else:
+            with pytest.raises(CTError) as e:
+                M.fixpoint(None)
+            assert e.value.status == CT_ESTATE
+        M.pop()
+    M.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_search_all_solutions_matches_oracle(seed):
+    m = csp_model(6, 5, 4, 40, seed=50 + seed, arities=[3, 3, 2, 4])
+    M = _model(m)
+    for vo in (0, 1):
+        st, sol, stats = M.search(value_order=vo, max_solutions=0)
+        ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=vo, max_solutions=0)
+        assert stats.solutions == len(ref["solutions"])
+        assert (stats.nodes, stats.failures) == (ref["nodes"], ref["failures"])
+        assert stats.trace_hash == ref["trace_hash"]
+        if ref["solutions"]:
+            assert tuple(sol.tolist()) == ref["solutions"][-1]
+    M.close()
+
+
+def test_search_first_solution_config5_shape():
+    """Config 5 shape (30 vars, d = 40, 12 tables, arity 4-8) at 2e4 tuples per
+    table: the first 300 nodes' trace equals the oracle's."""
+    m = csp_model(30, 40, 12, 20_000, seed=7)
+    M = _model(m)
+    st, sol, stats = M.search(value_order=0, max_nodes=300, max_solutions=1)
+    ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=300, max_solutions=1)
+    assert (stats.nodes, stats.failures, stats.solutions) == (ref["nodes"], ref["failures"], len(ref["solutions"]))
+    assert stats.trace_hash == ref["trace_hash"]
+    M.close()

@@ -240,3 +240,33 @@ def test_fixpoint_vs_iterated_cartesian():
         ok, out = oracle.fixpoint(vlo, vd, scopes, tables, dom)
         ok2, out2 = fixpoint_cartesian(vlo, vd, scopes, tables, dom)
         assert ok == ok2 and (not ok or np.array_equal(out, out2))
+
+
+# --------------------------------------------------------------------------- DFS oracle (f1)
+def _tiny_model(rng, nv=4, d=3, ntab=3):
+    from workloads.csp import csp_model
+    return csp_model(nv, d, ntab, 6, seed=int(rng.below(10**6)), arities=[min(nv, 2 + k % 2) for k in range(ntab)])
+
+
+def test_dfs_all_solutions_equal_cartesian():
+    from oracle.cartesian import all_solutions
+    from oracle.dfs import dfs
+    rng = Rng(404, lanes=4)
+    for trial in range(25):
+        m = _tiny_model(rng, nv=3 + trial % 3, d=2 + trial % 3, ntab=2 + trial % 3)
+        res = dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=trial % 2, max_solutions=0)
+        exp = all_solutions(m["vlo"], m["vd"], m["scopes"], m["tables"])
+        assert sorted(res["solutions"]) == sorted(exp)
+        assert len(set(res["solutions"])) == len(res["solutions"])      # each solution once
+        assert tuple(int(v) for v in m["sigma"]) in exp                   # planted solution
+
+
+def test_dfs_table1_first_solution_and_all():
+    """SPEC S:L394-395 (derived): Table 1 alone, input_order + indomain_max ->
+    (3,4,3) = tau5 first; all solutions = exactly the 5 tuples."""
+    from oracle.dfs import dfs
+    p = table1()
+    res = dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=1)
+    assert res["last_solution"] == (3, 4, 3)
+    res = dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=0)
+    assert sorted(res["solutions"]) == sorted(tuple(int(v) for v in r) for r in p.tuples)
