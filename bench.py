@@ -240,6 +240,8 @@ def run_ours(args):
             b += 16 * c["scan"] + 2 * c["scan"]          # support + currTable words, index entries
         byts += b
     k_bytes_per_launch = byts / max(k_n, 1)
+    kernel_name = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_update") if dom_kernel in ("fused", "small") \
+        else "ctk::k_update"
     k_ms_per_launch = k_ms / max(k_n, 1)
     achieved = k_bytes_per_launch / (k_ms_per_launch / 1e3) / 1e9
     peak, peak_src = peaks()
@@ -249,7 +251,7 @@ def run_ours(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("workload") == "c3bulk" and tj.get("n_gpus", 1) == world and tj.get("kernel") == dom_kernel:
+            if tj.get("workload") == "c3bulk" and tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel_name:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -299,7 +301,7 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (1.0 GB supports streamed each step)",
                        "build_s": round(build_s, 3)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": f"ctk::k_{dom_kernel}",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
                          "bytes_per_launch": k_bytes_per_launch, "ms_per_launch": k_ms_per_launch,
                          "model_bytes_per_launch_full_rows": float(np.mean(model)),
                          "peak_source": peak_src},

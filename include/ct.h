@@ -140,6 +140,10 @@ typedef struct ct_table_info {
   int64_t row_stride_words;     /* padded words per support row on the device            */
   int64_t device_bytes;         /* supports + table metadata on the device               */
   int64_t state_bytes;          /* device bytes of one state                             */
+  int32_t kernel_path;          /* single-state launch shape: 0 one kernel per phase,      */
+                                /* 1 k_fused (grid barrier per phase), 2 k_fast (per-CTA   */
+                                /* ingest, 1-2 grid barriers), 3 k_small (one CTA)         */
+  int32_t grid;                 /* CTAs of the single-state launch                       */
 } ct_table_info;
 
 ct_status ct_table_info_get(const ct_table *t, ct_table_info *out);
@@ -288,8 +292,11 @@ typedef struct ct_stats {
   int64_t update_support_words;  /* 64-bit support words loaded by updateTable          */
   int64_t update_table_writes;   /* 16-byte currTable blocks rewritten by updateTable   */
   int64_t filter_support_words;  /* support words loaded by the filter's index scans    */
-  int64_t phase_ns[5];      /* fused kernel only: device time of ingest, update, probe,  */
-                            /* scan, finalize in the last call (%globaltimer), else 0    */
+  int64_t phase_ns[7];      /* single-state kernels only (%globaltimer of block 0, and of */
+                            /* the finishing CTA for k_fast); k_fused / k_small: ingest,  */
+                            /* update, probe, scan, finalize, 0, 0; k_fast: ingest,        */
+                            /* update (+ barrier), probe, barrier, scan, completion wait,   */
+                            /* finalize.  Not written by the per-phase kernels.            */
 } ct_stats;
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
 

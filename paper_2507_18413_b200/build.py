@@ -49,11 +49,13 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None, out: str | None = None) -> str:
+    """out: build a variant library there instead (experiments; always rebuilt)."""
+    if out is None and not force and not needs_build():
         return LIB
+    target = out or LIB
     inc, libdir = nccl_paths()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
            "-Xptxas", "-v" if verbose else "-O3",
            "-I", INCLUDE, "-I", CSRC, "-I", inc,
@@ -63,8 +65,8 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -1,0 +1,686 @@
+// ct_fast.cuh -- k_fast: one whole single-state propagation (Alg. 1-3,
+// L131-244) in ONE cooperative launch, for tables whose support-row count fits
+// every CTA's shared memory (R <= kLocalRowsMax; BASELINE config 3 has R = 800).
+//
+// What it changes against k_fused (ct_kernels.cuh), phase by phase:
+//   ingest   (a2) computed redundantly by EVERY CTA into its own shared memory:
+//                 Δ_x, D_x, |Δ_x|, |D_x| and the update / filter row lists are a
+//                 few KB derived from Wd domain words, so the update starts
+//                 without a grid barrier.  A row's list position is a popcount
+//                 over the branch words (no row-by-row block scans).  Block 0
+//                 alone also publishes the per-call state (din, varcnt, control
+//                 fields, cleared flags) that k_finalize (sharded tables) and the
+//                 stats read.
+//   update   (a3-a5) one thread per active 16-byte block, support rows in
+//                 register batches of kFastUnroll 16-byte loads (the engine that
+//                 reached 95 % of the measured copy bandwidth in tools/upd_bench.cu),
+//                 tiles of kFastTPB entries assigned statically; a tile only
+//                 publishes its survivor COUNT (__syncthreads_count).  The CTA is
+//                 kept small (<= 85 registers, a few KB of shared memory) so at
+//                 least 6 fit an SM: with a per-SM cap near the average CTAs per
+//                 SM the hardware spreads the grid unevenly and the same loop
+//                 loses ~30 % (tools/upd_bench.cu, pad=40K rows).
+//   -- grid barrier --
+//   compaction (a4) after the barrier: every CTA sums the tile counts before its
+//                 tiles (one L2 pass, block reduction), re-reads its blocks'
+//                 new currTable words and writes the order-preserving index.
+//                 No chained-scan look-back chain on the update's critical path.
+//   probe    (a6a) residue probe (L220) together with the first of up to
+//                 kSelfRounds warp rounds over the PRE-update index (complete
+//                 before the barrier, a superset of the survivors), so a value
+//                 whose support lies early in the table never waits for the new
+//                 index.  Values still unresolved are queued.
+//   -- grid barrier (only if the probe rounds cannot cover the index) --
+//   scan     (a6b) (miss, chunk) units of the new compacted index, strided over
+//                 all warps (chunk-major): the queue holds the values that need a
+//                 long or full scan, which is where the whole grid pays off.
+//   finalize (a6c-a8) by the LAST CTA to finish (a completion counter instead of
+//                 a third barrier), from the lists it holds in shared memory.
+//                 Only the synchronous call, whose outputs live in mapped host
+//                 memory, pays the system-scope fence.
+// Work counters are reduced per CTA before one global atomic each.
+#pragma once
+#include "ct_kernels.cuh"
+
+namespace ctk {
+
+constexpr int kLocalRowsMax = 4096;                    // R limit of the per-CTA lists
+#ifndef CT_FAST_TPB
+#define CT_FAST_TPB 128
+#endif
+#ifndef CT_FAST_UNROLL
+#define CT_FAST_UNROLL 10
+#endif
+#ifndef CT_FAST_MINB
+#define CT_FAST_MINB 6
+#endif
+constexpr int kFastTPB = CT_FAST_TPB;                  // k_fast threads per CTA = index entries per tile
+constexpr int kFastWarps = kFastTPB / 32;
+constexpr int kFastUnroll = CT_FAST_UNROLL;            // support rows in flight per update thread
+constexpr int kProbeUnroll = 8;                        // raw blocks per lane in the probe's first round
+constexpr int kFirstScanFast = 32 * kProbeUnroll;      // index entries per probe round
+constexpr int kSelfRounds = 4;                         // probe rounds before a miss is queued
+#ifdef CT_FAST_STOP
+constexpr int kFastStop = CT_FAST_STOP;                // experiment builds only
+#else
+constexpr int kFastStop = 0;
+#endif
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Static shared state of one k_fast CTA.
+struct FastSh {
+  int dead, fail, noop, go, ngroups, nrows, nitems;
+  int L, ident, par, Lout, nscan, last;
+  int red[kFastWarps];           // block-reduction scratch
+  uint32_t woff[kFastWarps];
+  uint64_t scan[kFastWarps];
+  unsigned long long cnt[3];     // update loads, update writes, filter loads (this CTA)
+};
+
+// Dynamic shared memory of one k_fast CTA.
+struct FastPtrs {
+  uint64_t *din;      // [Wd] D_x = dom ∧ ¬removed
+  uint64_t *dl;       // [Wd] Δ_x = dom ∧ removed; finalize reuses it for the new domains
+  uint64_t *bw;       // [Wd] update-branch words (Δ_x or D_x if x in s_val, else 0)
+  uint64_t *iw;       // [Wd] filter words (D_x if x in s_sup, else 0)
+  int32_t *upos;      // [Wd+1] exclusive prefix of popc(bw)
+  int32_t *ipos;      // [Wd+1] exclusive prefix of popc(iw)
+  int32_t *wvar;      // [Wd] variable of each domain word
+  uint32_t *ulist;    // [R]  update list (row | kEndBit | kInvBit)
+  int32_t *items;     // [R]  filter items (support rows)
+  int32_t *cd, *cs;   // [n]  |Δ_x|, |D_x|
+  int32_t *vfl;       // [n]  bit 0 Δ-branch, bit 1 x in s_val
+  int32_t *rb, *dof;  // [n+1] rowBase, domOff
+};
+
+__host__ __device__ inline size_t fast_smem_bytes(int n, int Wd, int R) {
+  return (size_t)Wd * 32 + (size_t)(Wd + 1) * 8 + (size_t)Wd * 4 + (size_t)R * 8 + (size_t)(5 * n + 2) * 4 + 16;
+}
+
+__device__ __forceinline__ FastPtrs fast_ptrs(uint64_t *smem, const TableDev &tb) {
+  FastPtrs p;
+  const int Wd = tb.Wd, n = tb.n;
+  p.din = smem;
+  p.dl = p.din + Wd;
+  p.bw = p.dl + Wd;
+  p.iw = p.bw + Wd;
+  p.upos = reinterpret_cast<int32_t *>(p.iw + Wd);
+  p.ipos = p.upos + Wd + 1;
+  p.wvar = p.ipos + Wd + 1;
+  p.ulist = reinterpret_cast<uint32_t *>(p.wvar + Wd);
+  p.items = reinterpret_cast<int32_t *>(p.ulist + tb.R);
+  p.cd = p.items + tb.R;
+  p.cs = p.cd + n;
+  p.vfl = p.cs + n;
+  p.rb = p.vfl + n;
+  p.dof = p.rb + n + 1;
+  return p;
+}
+
+// Variable owning support row r: the last x with rb[x] <= r.
+__device__ __forceinline__ int row_var(const int32_t *rb, int n, int r) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (rb[mid] <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Block-wide sum over kFastTPB threads (uses fs.red; every thread gets the total).
+__device__ __forceinline__ int fast_block_sum(int v, FastSh &fs) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) fs.red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < kFastWarps; ++w) t += fs.red[w];
+  return t;
+}
+
+// ------------------------------------------------------------------ a2: per-CTA ingest
+// Same decisions as dev_ingest (Alg. 1 L1-3, Alg. 2), results kept in this
+// CTA's shared memory; `writer` (block 0) also publishes the per-call state.
+__device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem, int root_mode,
+                           const FastPtrs &p, FastSh &fs, bool writer) {
+  constexpr int NT = kFastTPB;
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = tb.n, Wd = tb.Wd, R = tb.R;
+  if (tid == 0) {
+    fs.dead = c->dead;
+    fs.fail = 0;
+    fs.ngroups = 0;
+    fs.L = c->L;
+    fs.ident = c->identity;
+    fs.par = c->parity;
+    fs.cnt[0] = fs.cnt[1] = fs.cnt[2] = 0;
+  }
+  for (int i = tid; i <= n; i += NT) {
+    p.rb[i] = tb.rowBase[i];
+    p.dof[i] = tb.domOff[i];
+  }
+  for (int x = tid; x < n; x += NT) p.cd[x] = p.cs[x] = 0;
+  __syncthreads();
+  if (fs.dead) {
+    if (tid == 0) {
+      fs.go = 0;
+      fs.noop = 0;
+      if (writer) {
+        c->skip = 1;
+        c->noop = 0;
+        c->fail_fast = 0;
+      }
+    }
+    __syncthreads();
+    return;
+  }
+  if (writer)
+    for (int r = tid; r <= R; r += NT) st.sup[r] = 0;
+  // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
+  for (int k = tid; k < Wd; k += NT) {
+    const uint64_t dm = st.dom[k];
+    const uint64_t rm = rem ? rem[k] : 0ull;
+    const int x = tb.wordVar[k];
+    const uint64_t delta = rm & dm, di = dm & ~rm;
+    p.din[k] = di;
+    p.dl[k] = delta;
+    p.wvar[k] = x;
+    if (writer) st.din[k] = di;
+    if (delta) atomicAdd(&p.cd[x], __popcll(delta));
+    if (di) atomicAdd(&p.cs[x], __popcll(di));
+  }
+  __syncthreads();
+  // per variable: s_val (Δ_x ≠ ∅), branch (Alg. 2: Δ-branch iff |Δ_x| < |D_x|), s_sup (|D_x| > 1)
+  for (int x = tid; x < n; x += NT) {
+    const int cd = p.cd[x], cs = p.cs[x];
+    const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+    p.vfl[x] = (useDelta ? 1 : 0) | (cd > 0 ? 2 : 0);
+    if (cd > 0) atomicAdd(&fs.ngroups, 1);
+    if (cs == 0) fs.fail = 1;                   // D_x empty -> no valid tuple
+    if (writer) {
+      st.varcnt[2 * x] = cd;
+      st.varcnt[2 * x + 1] = cs;
+    }
+  }
+  __syncthreads();
+  const bool fail = fs.fail != 0;
+  const bool noop = (fs.ngroups == 0) && !root_mode;
+  int nrows = 0, nitems = 0;
+  if (!(fail || noop)) {
+    // branch / item words and their exclusive popcount prefixes (variables are
+    // contiguous word runs, so the prefix groups the lists by variable)
+    int carry_u = 0, carry_i = 0;
+    for (int base = 0; base < Wd; base += NT) {
+      const int k = base + tid;
+      int cu = 0, ci = 0;
+      if (k < Wd) {
+        const int x = p.wvar[k], fl = p.vfl[x];
+        const uint64_t b = (fl & 2) ? ((fl & 1) ? p.dl[k] : p.din[k]) : 0ull;
+        const uint64_t it = p.cs[x] > 1 ? p.din[k] : 0ull;
+        p.bw[k] = b;
+        p.iw[k] = it;
+        cu = __popcll(b);
+        ci = __popcll(it);
+      }
+      const uint64_t v = ((uint64_t)cu << 32) | (uint64_t)ci;
+      uint64_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) fs.scan[warp] = x;
+      __syncthreads();
+      uint64_t wb = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kFastWarps; ++w) {
+        if (w < warp) wb += fs.scan[w];
+        tot += fs.scan[w];
+      }
+      const uint64_t ex = wb + x - v;
+      if (k < Wd) {
+        p.upos[k] = carry_u + (int)(ex >> 32);
+        p.ipos[k] = carry_i + (int)(ex & 0xffffffffu);
+      }
+      carry_u += (int)(tot >> 32);
+      carry_i += (int)(tot & 0xffffffffu);
+      __syncthreads();
+    }
+    if (tid == 0) {
+      p.upos[Wd] = carry_u;
+      p.ipos[Wd] = carry_i;
+    }
+    nrows = carry_u;
+    nitems = carry_i;
+    __syncthreads();
+    // one task per (domain word, byte): emit the rows of its set bits in order
+    for (int j = tid; j < 8 * Wd; j += NT) {
+      const int k = j >> 3, sh = (j & 7) * 8;
+      const int x = p.wvar[k];
+      const int rbase = p.rb[x] + 64 * (k - p.dof[x]) + sh;
+      const uint64_t below = sh ? ((1ull << sh) - 1) : 0ull;
+      uint32_t ub = (uint32_t)(p.bw[k] >> sh) & 0xffu;
+      if (ub) {
+        int pos = p.upos[k] + __popcll(p.bw[k] & below);
+        const int uend = p.upos[p.dof[x + 1]] - 1;   // last entry of x's group
+        const uint32_t inv = (p.vfl[x] & 1) ? kInvBit : 0u;
+        while (ub) {
+          const int b = __ffs(ub) - 1;
+          ub &= ub - 1;
+          p.ulist[pos] = (uint32_t)(rbase + b) | inv | (pos == uend ? kEndBit : 0u);
+          ++pos;
+        }
+      }
+      uint32_t ib = (uint32_t)(p.iw[k] >> sh) & 0xffu;
+      if (ib) {
+        int pos = p.ipos[k] + __popcll(p.iw[k] & below);
+        while (ib) {
+          const int b = __ffs(ib) - 1;
+          ib &= ib - 1;
+          p.items[pos++] = rbase + b;
+        }
+      }
+    }
+  }
+  if (tid == 0) {
+    fs.nrows = nrows;
+    fs.nitems = nitems;
+    fs.noop = noop && !fail;
+    fs.go = !(fail || noop);
+    if (writer) {
+      c->skip = 0;
+      c->noop = noop && !fail;
+      c->fail_fast = fail;
+      c->ngroups = fs.ngroups;
+      c->nrows = nrows;
+      c->nitems = nitems;
+      c->L_in = fs.L;
+      c->L_out = 0;
+      c->nscan = 0;
+      c->upd_loads = 0;
+      c->upd_writes = 0;
+      c->scan_loads = 0;
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------ a3: update of one tile
+// Alg. 2 for the kFastTPB index entries of `tile` (one 16-byte block per
+// thread).  The block dies early (Alg. 2) once no valid tuple is left in
+// it (checked between batches).  The tile's survivor count goes to cnt[tile].
+__device__ __forceinline__ void fast_update_tile(const TableDev &tb, const StateDev &st, const FastSh &fs,
+                                                 const uint32_t *__restrict__ ulist, int tile,
+                                                 uint32_t *__restrict__ cnt, uint32_t &n_loads,
+                                                 uint32_t &n_writes) {
+  const int L = fs.L, nrows = fs.nrows;
+  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+  const int64_t Wp = tb.Wp;
+  const int k = tile * kFastTPB + threadIdx.x;
+  bool keep = false;
+  if (k < L) {
+    const int pid = fs.ident ? k : idx_in[k];
+    const ulonglong2 tw = T2[pid];
+    const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+    uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+    for (int p0 = 0; p0 < nrows; p0 += kFastUnroll) {
+      if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 16-byte block
+      ulonglong2 v[kFastUnroll];
+#pragma unroll
+      for (int q = 0; q < kFastUnroll; ++q)
+        v[q] = (p0 + q < nrows) ? ld_sup2(col + (int64_t)(ulist[p0 + q] & kRowMask) * Wp)
+                                : make_ulonglong2(0ull, 0ull);
+      n_loads += 2 * min(kFastUnroll, nrows - p0);
+#pragma unroll
+      for (int q = 0; q < kFastUnroll; ++q) {
+        if (p0 + q < nrows) {
+          const uint32_t e = ulist[p0 + q];
+          ax |= v[q].x;
+          ay |= v[q].y;
+          if (e & kEndBit) {
+            if (e & kInvBit) {
+              mx &= ~ax;
+              my &= ~ay;
+            } else {
+              mx &= ax;
+              my &= ay;
+            }
+            ax = ay = 0;
+          }
+        }
+      }
+    }
+    const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
+    if (nt.x != tw.x || nt.y != tw.y) {
+      T2[pid] = nt;
+      ++n_writes;
+    }
+    keep = (nt.x | nt.y) != 0;
+  }
+  const int survivors = __syncthreads_count(keep);
+  if (threadIdx.x == 0) cnt[tile] = (uint32_t)survivors;
+}
+
+// ------------------------------------------------------------------ a6a: probe of one row
+// Alg. 3 L3 for one (x,a) by a warp: is some block b with T[b] & S[x,a][b] != 0?
+// Lane 0's residue block r (L220; -1 = none) is tested together with the first
+// round; each round covers kFirstScanFast entries of the PRE-update index (its
+// blocks are a superset of the survivors, and it is complete before the
+// barrier; nullptr = identity), at most kSelfRounds rounds.  Returns the hit
+// block (r if the residue hit, else the lowest hit of the round) or -1.
+__device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, int Lin,
+                                         const ulonglong2 *__restrict__ T2, const uint64_t *__restrict__ srow,
+                                         int r, int lane, uint32_t &nl) {
+  for (int round = 0; round < kSelfRounds; ++round) {
+    const int kb = round * kFirstScanFast;
+    if (kb >= Lin) break;
+    int pid[kProbeUnroll];
+    uint64_t v[kProbeUnroll];
+#pragma unroll
+    for (int q = 0; q < kProbeUnroll; ++q) {
+      const int k = kb + q * 32 + lane;
+      pid[q] = k < Lin ? (idx_old ? idx_old[k] : k) : -1;
+    }
+    bool rh = false;
+    if (round == 0 && r >= 0) {
+      const ulonglong2 t = __ldcg(T2 + r);
+      const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
+      rh = ((t.x & s.x) | (t.y & s.y)) != 0;
+      nl += 2;
+    }
+#pragma unroll
+    for (int q = 0; q < kProbeUnroll; ++q) {
+      v[q] = 0;
+      if (pid[q] >= 0) {
+        const ulonglong2 t = __ldcg(T2 + pid[q]);
+        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)pid[q]);
+        v[q] = (t.x & s.x) | (t.y & s.y);
+      }
+    }
+    nl += 2 * min(kFirstScanFast, Lin - kb);
+    if (__any_sync(0xffffffffu, rh)) return __shfl_sync(0xffffffffu, r, 0);
+    int hit = -1;
+#pragma unroll
+    for (int q = kProbeUnroll - 1; q >= 0; --q) {
+      const unsigned b = __ballot_sync(0xffffffffu, v[q] != 0);
+      if (b) hit = __shfl_sync(0xffffffffu, pid[q], __ffs(b) - 1);
+    }
+    if (hit >= 0) return hit;
+  }
+  return -1;
+}
+
+// ------------------------------------------------------------------ a6c-a8: finalize from shared memory
+// Alg. 3 L3-4 over the filter items this CTA listed in its ingest: a value of
+// x in s_sup leaves the domain iff its row is unsupported; lastDom <- dom.
+__device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
+                             uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
+                             int32_t *__restrict__ out_status, bool sys_fence) {
+  constexpr int NT = kFastTPB;
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, Wd = tb.Wd;
+  int status;
+  if (fs.dead) status = -5;              // CT_ESTATE
+  else if (fs.fail) status = 1;          // CT_FAIL: some D_x empty
+  else if (fs.noop) status = 0;
+  else status = fs.Lout > 0 ? 0 : 1;     // currTable empty <=> FAIL (Alg. 1 L5)
+  if (status != 0) {
+    if (tid == 0) {
+      if (status == 1) {
+        c->dead = 1;
+        c->calls += 1;
+      }
+      c->last_status = status;
+      if (out_status) *out_status = status;
+    }
+    return;
+  }
+  uint64_t *s_nd = p.dl;
+  for (int k = tid; k < Wd; k += NT) s_nd[k] = p.din[k];
+  __syncthreads();
+  if (!fs.noop) {
+    for (int i = tid; i < fs.nitems; i += NT) {
+      const int r = p.items[i];
+      if (!__ldcg(st.sup + r)) {                   // x in s_sup (Alg. 3 L1), a unsupported
+        const int x = row_var(p.rb, tb.n, r);
+        const int a = r - p.rb[x];
+        const int w = p.dof[x] + (a >> 6);
+        atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + w), ~(1ull << (a & 63)));
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < Wd; k += NT) {
+    const uint64_t nd = s_nd[k];
+    st.dom[k] = nd;
+    if (out_dom) out_dom[k] = nd;
+    if (out_pruned) out_pruned[k] = p.din[k] & ~nd;
+  }
+  // the status word completes the host-mapped synchronous call: every output
+  // write must be visible system-wide before it
+  if (sys_fence) __threadfence_system();
+  __syncthreads();
+  if (tid == 0) {
+    if (!fs.noop && tb.use_index) {
+      c->parity ^= 1;
+      c->L = fs.Lout;
+      c->identity = 0;
+    }
+    c->calls += 1;
+    c->last_status = 0;
+    if (out_status) *out_status = 0;
+  }
+}
+
+// ------------------------------------------------------------------ k_fast
+// Cooperative launch (all CTAs co-resident), kFastTPB threads, dynamic smem
+// fast_smem_bytes(n, Wd, R).  with_finalize = 0 for sharded tables (the flags are
+// OR-combined across shards first and k_finalize runs after).  Filter items
+// are spread CTA-major (item i -> CTA i % grid) so few items probe on many SMs.
+__global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, const StateDev *__restrict__ states,
+                                                   const uint64_t *__restrict__ removed, int root_mode,
+                                                   int with_finalize, uint64_t *__restrict__ out_dom,
+                                                   uint64_t *__restrict__ out_pruned,
+                                                   int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ FastSh fs;
+  __shared__ StateDev s_st;   // the state's pointers live in shared memory, not in 30 registers
+  if (threadIdx.x == 0) s_st = states[0];
+  __syncthreads();
+  const StateDev &st = s_st;
+  Ctl *c = st.ctl;
+  const FastPtrs p = fast_ptrs(smem, tb);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x;
+  const int gw = blockIdx.x * kFastWarps + warp, nw = G * kFastWarps;
+  const bool t0 = blockIdx.x == 0 && tid == 0;
+  // phase timestamps of block 0 go straight to tph[] (no registers held)
+  if (t0) c->tph[0] = globaltimer();
+  cta_ingest(tb, st, removed, root_mode, p, fs, blockIdx.x == 0);
+  if (t0) {
+    const unsigned long long t = globaltimer();
+    for (int i = 1; i < 6; ++i) c->tph[i] = t;
+  }
+
+  if (fs.go) {
+    uint32_t *__restrict__ tcnt = reinterpret_cast<uint32_t *>(st.tilestat);
+    // ---- update (a3), survivor count per tile
+    const int ntiles = (fs.L + kFastTPB - 1) / kFastTPB;
+    uint32_t n_loads = 0, n_writes = 0, f_loads = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += G)
+      fast_update_tile(tb, st, fs, p.ulist, tile, tcnt, n_loads, n_writes);
+
+    const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+    const int item0 = warp * G + blockIdx.x;   // CTA-major: item i -> CTA i % G
+    if (kFastStop > 0) {
+      // experiment builds only (tools/gpu_exp.sh): 1 = update only, 2 = update +
+      // barrier, -3 = ... + compaction, -4 = ... + probe; the call then reports a
+      // made-up success
+      if (kFastStop == 2) grid_barrier(c);
+      if (t0) c->tph[2] = globaltimer();
+      if (tid == 0) {
+        fs.Lout = fs.L;
+        fs.noop = 1;   // finalize leaves the state as it was
+      }
+      __syncthreads();
+    } else {
+    grid_barrier(c);
+    if (t0) c->tph[2] = globaltimer();
+
+    // ---- compaction (a4): L_out and this CTA's tile prefixes from the tile counts
+    {
+      int tot = 0, below = 0;
+      for (int j = tid; j < ntiles; j += kFastTPB) {
+        const int v = (int)__ldcg(tcnt + j);
+        tot += v;
+        if (j < (int)blockIdx.x) below += v;
+      }
+      tot = fast_block_sum(tot, fs);
+      below = fast_block_sum(below, fs);
+      if (tid == 0) {
+        fs.Lout = tot;
+        if (blockIdx.x == 0) c->L_out = tot;
+      }
+      const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+      int32_t *__restrict__ idx_out = fs.par ? st.idx0 : st.idx1;
+      for (int tile = blockIdx.x; tile < ntiles; tile += G) {
+        if (tile != (int)blockIdx.x) {   // prefix of the next own tile: add counts [tile - G, tile)
+          int add = 0;
+          for (int j = tile - G + tid; j < tile; j += kFastTPB) add += (int)__ldcg(tcnt + j);
+          below += fast_block_sum(add, fs);
+        }
+        const int k = tile * kFastTPB + tid;
+        int pid = 0;
+        bool keep = false;
+        if (k < fs.L) {
+          pid = fs.ident ? k : idx_in[k];
+          const ulonglong2 t = __ldcg(T2 + pid);
+          keep = (t.x | t.y) != 0;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        __syncthreads();
+        if (lane == 0) fs.woff[warp] = __popc(bal);
+        __syncthreads();
+        uint32_t off = 0;
+#pragma unroll
+        for (int w = 0; w < kFastWarps; ++w)
+          if (w < warp) off += fs.woff[w];
+        if (tb.use_index && keep) idx_out[below + off + __popc(bal & lanemask_lt())] = pid;
+      }
+    }
+    __syncthreads();
+
+    // ---- probe (a6a): residue + up to kSelfRounds rounds over the pre-update index
+    const int Lout = fs.Lout;
+    const bool compact = tb.use_index != 0;
+    const int32_t *__restrict__ idx = compact ? (fs.par ? st.idx0 : st.idx1) : nullptr;
+    const int32_t *__restrict__ idx_old = fs.ident ? nullptr : (fs.par ? st.idx1 : st.idx0);
+    const int Ls = compact ? Lout : tb.W2;
+    const bool may_miss = fs.L > kSelfRounds * kFirstScanFast;   // the probe cannot cover the index
+    if (t0) st.sup[tb.R] = Lout > 0;
+    if (Lout > 0 && kFastStop != -3) {
+      for (int item = item0; item < fs.nitems; item += nw) {
+        const int row = p.items[item];
+        const int r = (tb.use_res && lane == 0) ? st.res[row] : -1;
+        uint32_t nl = 0;
+        const int hit = probe_row(idx_old, fs.L, T2, tb.S + (int64_t)row * tb.Wp, r, lane, nl);
+        if (lane == 0) {
+          f_loads += nl;
+          if (hit >= 0) {
+            st.sup[row] = 1;
+            if (hit != r) st.res[row] = hit;
+          } else if (may_miss) {
+            st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+          }
+        }
+      }
+    }
+    if (t0) c->tph[3] = c->tph[4] = globaltimer();
+    // ---- scan (a6b): misses x chunks of the compacted index, from entry 0
+    if (Lout > 0 && may_miss && kFastStop > -3) {
+      grid_barrier(c);   // index complete, misses known
+      if (t0) c->tph[4] = globaltimer();
+      if (tid == 0) fs.nscan = __ldcg(&c->nscan);
+      __syncthreads();
+      const int nscan = fs.nscan;
+      const int nch = (Ls + kScanChunk - 1) / kScanChunk;
+      const int64_t total = (int64_t)nch * nscan;
+      for (int64_t u = gw; u < total; u += nw) {   // chunk-major: early chunks of every miss first
+        const int chunk = (int)(u / nscan);
+        const int item = (int)(u - (int64_t)chunk * nscan);
+        const int row = __ldcg(st.scanlist + item);
+        const int fl = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
+        if (__shfl_sync(0xffffffffu, fl, 0)) continue;
+        const int k0 = chunk * kScanChunk;
+        const int k1 = min(k0 + kScanChunk, Ls);
+        uint32_t nl = 0;
+        const int hit = scan_pairs<kScanUnroll>(idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, st.sup + row, lane,
+                                                nl);
+        if (lane == 0) {
+          f_loads += nl;
+          if (hit >= 0) {
+            st.sup[row] = 1;
+            st.res[row] = hit;
+          }
+        }
+      }
+    }
+    if (t0) c->tph[5] = globaltimer();
+    if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
+    }   // !kFastStop
+    // per-CTA counter reduction, one fire-and-forget atomic per counter
+    n_loads = warp_sum_u32(n_loads);
+    n_writes = warp_sum_u32(n_writes);
+    if (lane == 0) {
+      if (n_loads) atomicAdd(&fs.cnt[0], (unsigned long long)n_loads);
+      if (n_writes) atomicAdd(&fs.cnt[1], (unsigned long long)n_writes);
+      if (f_loads) atomicAdd(&fs.cnt[2], (unsigned long long)f_loads);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (fs.cnt[0]) atomicAdd(&c->upd_loads, fs.cnt[0]);
+      if (fs.cnt[1]) atomicAdd(&c->upd_writes, fs.cnt[1]);
+      if (fs.cnt[2]) atomicAdd(&c->scan_loads, fs.cnt[2]);
+    }
+  }
+
+  // ---- completion: the last CTA to get here finalizes
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    fs.last = atomicAdd(&c->cta_done, 1) == G - 1;
+  }
+  __syncthreads();
+  if (!fs.last) return;
+  __threadfence();
+  if (tid == 0) {
+    c->cta_done = 0;
+    c->tph[6] = globaltimer();
+  }
+  if (with_finalize) {
+    if (use_state_out) {
+      out_dom = st.out + 1;
+      out_pruned = st.out + 1 + tb.Wd;
+      out_status = reinterpret_cast<int32_t *>(st.out);
+    }
+    cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
+  }
+  if (tid == 0) c->tph[7] = globaltimer();
+}
+
+}  // namespace ctk

@@ -93,8 +93,10 @@ struct Ctl {
   unsigned long long scan_loads;   // support words loaded by probe + scan
   uint32_t bar_count;  // software grid barrier of k_fused
   uint32_t bar_gen;
-  unsigned long long tph[6];   // k_fused phase timestamps (%globaltimer, ns), block 0
-  int32_t pad[2];
+  unsigned long long tph[8];   // phase timestamps (%globaltimer, ns); see ct_stats.phase_ns
+  int32_t cta_done;    // k_fast: CTAs done with the filter; the last one finalizes
+                       // and resets it to 0 (so a copied state always holds 0)
+  int32_t pad[1];
 };
 static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
 
@@ -549,23 +551,24 @@ __device__ void dev_update(const TableDev &tb, const StateDev &st) {
 // intersectIndex): kScanUnroll blocks per lane per round, one __ballot_sync
 // "any" per block.  Returns the first (lowest-entry) block with a common valid
 // tuple, -1 if none, -2 if `supflag` was set by another warp meanwhile.
+template <int U = kScanUnroll>
 __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const ulonglong2 *__restrict__ T2,
                                           const uint64_t *__restrict__ srow, int k0, int k1,
                                           const uint8_t *supflag, int lane, uint32_t &n_loads) {
-  for (int kb = k0; kb < k1; kb += 32 * kScanUnroll) {
+  for (int kb = k0; kb < k1; kb += 32 * U) {
     if (supflag && kb != k0) {
       const int f = lane == 0 ? *(volatile const uint8_t *)supflag : 0;
       if (__shfl_sync(0xffffffffu, f, 0)) return -2;
     }
-    int pid[kScanUnroll];
-    uint64_t v[kScanUnroll];
+    int pid[U];
+    uint64_t v[U];
 #pragma unroll
-    for (int q = 0; q < kScanUnroll; ++q) {
+    for (int q = 0; q < U; ++q) {
       const int k = kb + q * 32 + lane;
       pid[q] = k < k1 ? (idx ? idx[k] : k) : -1;
     }
 #pragma unroll
-    for (int q = 0; q < kScanUnroll; ++q) {
+    for (int q = 0; q < U; ++q) {
       if (pid[q] >= 0) {
         const ulonglong2 t = T2[pid[q]];
         const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)pid[q]);
@@ -574,10 +577,10 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
         v[q] = 0;
       }
     }
-    n_loads += 2 * min(32 * kScanUnroll, k1 - kb);
+    n_loads += 2 * min(32 * U, k1 - kb);
     int hit = -1;
 #pragma unroll
-    for (int q = kScanUnroll - 1; q >= 0; --q) {
+    for (int q = U - 1; q >= 0; --q) {
       const unsigned b = __ballot_sync(0xffffffffu, v[q] != 0);
       if (b) hit = __shfl_sync(0xffffffffu, pid[q], __ffs(b) - 1);
     }
@@ -834,7 +837,7 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const State
   if (!with_finalize) {
     if (t0) {
       ts[4] = ts[5] = globaltimer();
-      for (int i = 0; i < 6; ++i) st.ctl->tph[i] = ts[i];
+      for (int i = 0; i < 8; ++i) st.ctl->tph[i] = ts[i < 6 ? i : 5];
     }
     return;
   }
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const State
     dev_finalize<kFusedTPB>(tb, st, out_dom, out_pruned, out_status, smem);
     if (t0) {
       ts[5] = globaltimer();
-      for (int i = 0; i < 6; ++i) st.ctl->tph[i] = ts[i];
+      for (int i = 0; i < 8; ++i) st.ctl->tph[i] = ts[i < 6 ? i : 5];
     }
   }
 }
@@ -1003,7 +1006,7 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   if (!with_finalize) {
     if (t0) {
       ts[5] = ts[4];
-      for (int i = 0; i < 6; ++i) c->tph[i] = ts[i];
+      for (int i = 0; i < 8; ++i) c->tph[i] = ts[i < 6 ? i : 5];
     }
     return;
   }
@@ -1015,7 +1018,7 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   dev_finalize<kSmallTPB>(tb, st, out_dom, out_pruned, out_status, smem);
   if (t0) {
     ts[5] = globaltimer();
-    for (int i = 0; i < 6; ++i) c->tph[i] = ts[i];
+    for (int i = 0; i < 8; ++i) c->tph[i] = ts[i < 6 ? i : 5];
   }
 }
 

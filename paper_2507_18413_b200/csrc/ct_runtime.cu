@@ -17,6 +17,7 @@
 #include "ct.h"
 #include "ct_kernels.cuh"
 #include "ct_model.cuh"
+#include "ct_fast.cuh"
 
 using namespace ctk;
 
@@ -108,6 +109,8 @@ struct ct_table {
   int upd_occ = 1, scan_occ = 1;
   int use_fused = 1, fused_grid = 1, fused_occ = 1, coop = 1, fused_grid_override = 0, use_small = 0;
   size_t fused_smem = 0;
+  int use_fast = 0, fast_grid = 1;   // k_fast (ct_fast.cuh): tables with R <= kLocalRowsMax
+  size_t fast_smem = 0;
   int live = 0;   // states + batches alive
 
   void *dalloc(size_t bytes) {
@@ -296,6 +299,23 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     CUDA_TRY(cudaGetLastError());
     prof_mark(tb, 7, e, st);
     if (fin_inside || local_only) return CT_OK;
+  } else if (tb->use_fast) {
+    const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)tb->fast_grid);
+    lc.blockDim = dim3(kFastTPB);
+    lc.dynamicSmemBytes = tb->fast_smem;
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = tb->coop;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    const int e = prof_event(tb, st);
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_fast, tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
+                                out_dom, out_pruned, out_status, use_state_out));
+    prof_mark(tb, 6, e, st);
+    if (fin_inside || local_only) return CT_OK;
   } else if (tb->use_fused) {
     const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
     cudaLaunchConfig_t lc = {};
@@ -379,6 +399,12 @@ static ct_status new_state(ct_table *tb, ct_state **out) {
     cudaGetLastError();
     free_state_mem(s);
     return fail(CT_ENOMEM, "mapped pinned host allocation failed");
+  }
+  // per-call scratch starts zeroed (k_fast's tile statuses and miss list rely on it)
+  if (cudaMemsetAsync(s->mem + tb->lay.persist, 0, tb->lay.total - tb->lay.persist, tb->stream) != cudaSuccess) {
+    cudaGetLastError();
+    free_state_mem(s);
+    return fail(CT_ECUDA, "state scratch initialisation failed");
   }
   s->h = make_desc(tb, s->mem);
   s->h.out = s->d_out_map;
@@ -607,6 +633,23 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   // SM for the filter phases, at most what the update can use beyond that.
   tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, std::max(tb->sm_count, dv.ntiles_max));
   if (tb->fused_grid_override > 0) tb->fused_grid = std::min(tb->sm_count * tb->fused_occ, tb->fused_grid_override);
+  // k_fast: per-CTA ingest lists in shared memory (tables with few support rows)
+  {
+    int fast_ok = (tb->use_fused && tb->R <= kLocalRowsMax) ? 1 : 0;
+    if (const char *ev = getenv("CT_NO_FAST")) fast_ok = fast_ok && !atoi(ev);
+    if (fast_ok) {
+      tb->fast_smem = fast_smem_bytes(n, tb->Wd, tb->R);
+      CUDA_TRY(cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->fast_smem));
+      int occ = 0;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, kFastTPB, tb->fast_smem));
+      if (occ >= 1) {
+        tb->use_fast = 1;
+        const int tiles = (int)((dv.W2 + kFastTPB - 1) / kFastTPB);
+        tb->fast_grid = std::min(tb->sm_count * occ, std::max(tb->sm_count, tiles));
+        if (tb->fused_grid_override > 0) tb->fast_grid = std::min(tb->sm_count * occ, tb->fused_grid_override);
+      }
+    }
+  }
   // latency-bound tables: the whole call in one CTA (k_small)
   {
     int small_max = kSmallMaxPairs;
@@ -690,6 +733,8 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->row_stride_words = t->Wp;
   o->device_bytes = (int64_t)(t->S_bytes + t->meta_bytes);
   o->state_bytes = (int64_t)t->lay.total;
+  o->kernel_path = t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
+  o->grid = t->use_small ? 1 : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   return CT_OK;
 }
 
@@ -1020,7 +1065,7 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
   o->update_support_words = (int64_t)c.upd_loads;
   o->update_table_writes = (int64_t)c.upd_writes;
   o->filter_support_words = (int64_t)c.scan_loads;
-  for (int i = 0; i < 5; ++i) o->phase_ns[i] = (c.tph[0] && c.tph[i + 1] >= c.tph[i]) ? (int64_t)(c.tph[i + 1] - c.tph[i]) : 0;
+  for (int i = 0; i < 7; ++i) o->phase_ns[i] = (c.tph[0] && c.tph[i + 1] >= c.tph[i]) ? (int64_t)(c.tph[i + 1] - c.tph[i]) : 0;
   return CT_OK;
 }
 

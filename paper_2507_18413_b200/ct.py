@@ -19,7 +19,7 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libct_b200.so")
+LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(_PKG, "libct_b200.so")   # override: experiment builds
 
 CT_OK, CT_FAIL, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE = 0, 1, -1, -2, -3, -4, -5
 CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA = 0, 1, 2
@@ -56,7 +56,9 @@ class ct_table_info(ctypes.Structure):
                 ("n_tuples", ctypes.c_int64), ("words_total", ctypes.c_int64),
                 ("word_begin", ctypes.c_int64), ("words", ctypes.c_int64),
                 ("row_stride_words", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("state_bytes", ctypes.c_int64)]
+                ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32)]
+
+KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small"}
 
 
 class ct_stats(ctypes.Structure):
@@ -65,7 +67,7 @@ class ct_stats(ctypes.Structure):
                 ("n_filter_items", ctypes.c_int32), ("n_residue_miss", ctypes.c_int32),
                 ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64),
                 ("update_support_words", ctypes.c_int64), ("update_table_writes", ctypes.c_int64),
-                ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 5)]
+                ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 7)]
 
 
 class ct_search_stats(ctypes.Structure):

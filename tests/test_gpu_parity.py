@@ -28,8 +28,12 @@ KNOBS = [
     dict(use_graph=False),
     dict(use_fused=False),
     dict(_grid_fused=True),
+    dict(_grid_fused=True, _fast=False),
+    dict(_grid_fused=True, use_index=False),
+    dict(_grid_fused=True, use_residues=False),
 ]
-KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph", "nofused", "gridfused"]
+KNOB_IDS = ["auto", "dom", "delta", "nores", "noindex", "nograph", "nofused", "gridfused", "gridfused_v1",
+            "gridfused_noindex", "gridfused_nores"]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -40,16 +44,23 @@ def _built():
     assert torch.cuda.is_available()
 
 
-def make(p, _grid_fused=False, **kw):
-    """_grid_fused: force the cooperative multi-CTA kernel even for tables small
-    enough for the single-CTA one (CT_SMALL_MAX_PAIRS is read at create time)."""
+def make(p, _grid_fused=False, _fast=True, _grid=0, **kw):
+    """_grid_fused: force a cooperative multi-CTA kernel even for tables small
+    enough for the single-CTA one; _fast=False: the barrier-per-phase k_fused
+    instead of k_fast (both environment knobs are read at create time)."""
     import os
     if _grid_fused:
         os.environ["CT_SMALL_MAX_PAIRS"] = "0"
+    if not _fast:
+        os.environ["CT_NO_FAST"] = "1"
+    if _grid:
+        os.environ["CT_FUSED_GRID"] = str(_grid)   # fewer CTAs than tiles: several tiles per CTA
     try:
         return Table(p.lo, p.d, p.tuples, **kw)
     finally:
         os.environ.pop("CT_SMALL_MAX_PAIRS", None)
+        os.environ.pop("CT_NO_FAST", None)
+        os.environ.pop("CT_FUSED_GRID", None)
 
 
 # --------------------------------------------------------------------------- a1 supports builder
@@ -141,6 +152,19 @@ def test_walk_shapes(shape):
     tab.close()
 
 
+@pytest.mark.parametrize("path", [dict(_grid_fused=True), dict(_grid_fused=True, _grid=3),
+                                  dict(_grid_fused=True, _grid=3, _fast=False), dict(_grid_fused=True, _grid=5,
+                                                                                     use_index=False)],
+                         ids=["fast", "fast_g3", "v1_g3", "fast_g5_noindex"])
+def test_walk_multitile(path):
+    """Several update tiles per CTA (chained-scan look-back across rounds) and
+    filter scans beyond the probe's first round."""
+    p = random_table(6, 16, 300_000 + 77, seed=31)
+    tab = make(p, **path)
+    run_walk(tab, p, calls=120, seed=6, check_table_every=6)
+    tab.close()
+
+
 def test_walk_config2_full():
     """BASELINE config 2: arity 5, domain 20, 1e5 tuples, 1000 random-removal calls."""
     p = random_table(5, 20, 100_000, seed=1)
@@ -163,12 +187,13 @@ def c3():
     return random_table(8, 100, 10_000_000, seed=3)
 
 
-def test_config3_bulk_full_size(c3):
+@pytest.mark.parametrize("fast", [True, False], ids=["fast", "v1"])
+def test_config3_bulk_full_size(c3, fast):
     """BASELINE config 3 (1e7 tuples, ~1 GB supports) in the bench's launch
     configuration: root, then bulk calls from the root, each vs the oracle
     (domains, pruned set and the full currTable)."""
     p = c3
-    tab = make(p)
+    tab = make(p, _fast=fast)
     check_root(tab, p)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     rng = Rng(11)
@@ -203,9 +228,10 @@ def test_config3_bulk_full_size(c3):
     tab.close()
 
 
-def test_config3b_banded_filter_heavy():
+@pytest.mark.parametrize("fast", [True, False], ids=["fast", "v1"])
+def test_config3b_banded_filter_heavy(fast):
     p = banded_table(8, 100, 2_000_000, seed=4)
-    tab = make(p)
+    tab = make(p, _fast=fast)
     check_root(tab, p)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     rng = Rng(12)
@@ -352,14 +378,18 @@ def test_batch_matches_oracle_and_single_state():
 
 
 # --------------------------------------------------------------------------- sharded (a10)
+PATHS = {"small": dict(), "fast": dict(_grid_fused=True), "v1": dict(_grid_fused=True, _fast=False)}
+
+
+@pytest.mark.parametrize("path", list(PATHS))
 @pytest.mark.parametrize("G", [2, 3, 5])
-def test_virtual_shards_one_gpu(G):
+def test_virtual_shards_one_gpu(G, path):
     """G tuple-range shards on one device, flags OR-combined by the caller."""
     import torch
     from paper_2507_18413_b200.sharded import flags_tensor
     p = random_table(5, 20, 50_000 + 33, seed=23)
     full = make(p)
-    shards = [make(p, n_shards=G, shard_rank=g) for g in range(G)]
+    shards = [make(p, n_shards=G, shard_rank=g, **PATHS[path]) for g in range(G)]
     root_m = bitmap_to_member(full.root_dom, p.d)
     for s in shards:
         assert s.root_status == full.root_status and np.array_equal(s.root_dom, full.root_dom)
@@ -411,10 +441,11 @@ def test_virtual_shards_one_gpu(G):
     full.close()
 
 
-def test_nccl_single_rank_path():
+@pytest.mark.parametrize("path", list(PATHS))
+def test_nccl_single_rank_path(path):
     """The in-library NCCL combine (all-reduce inside the call) on a 1-rank communicator."""
     p = random_table(5, 20, 30_000, seed=29)
     nid = C.ct_nccl_unique_id()
-    tab = make(p, n_shards=1, shard_rank=0, nccl_unique_id=nid)
+    tab = make(p, n_shards=1, shard_rank=0, nccl_unique_id=nid, **PATHS[path])
     run_walk(tab, p, calls=150, seed=4, check_table_every=10)
     tab.close()
