@@ -57,9 +57,12 @@ constexpr int kLocalRowsMax = 4096;                    // R limit of the per-CTA
 constexpr int kFastTPB = CT_FAST_TPB;                  // k_fast threads per CTA = index entries per tile
 constexpr int kFastWarps = kFastTPB / 32;
 constexpr int kFastUnroll = CT_FAST_UNROLL;            // support rows in flight per update thread
-constexpr int kProbeUnroll = 8;                        // raw blocks per lane in the probe's first round
+#ifndef CT_PROBE_UNROLL
+#define CT_PROBE_UNROLL 8
+#endif
+constexpr int kProbeUnroll = CT_PROBE_UNROLL;          // index entries per lane per probe round
 constexpr int kFirstScanFast = 32 * kProbeUnroll;      // index entries per probe round
-constexpr int kSelfRounds = 4;                         // probe rounds before a miss is queued
+constexpr int kSelfRounds = 32 / kProbeUnroll;         // probe rounds before a miss is queued (1024 entries)
 #ifdef CT_FAST_STOP
 constexpr int kFastStop = CT_FAST_STOP;                // experiment builds only
 #else
@@ -136,6 +139,42 @@ __device__ __forceinline__ int row_var(const int32_t *rb, int n, int r) {
     else hi = mid - 1;
   }
   return lo;
+}
+
+// Grid barrier of k_fast (all CTAs co-resident).  A single counter that every
+// CTA increments serialises G same-address atomics at one L2 slice, and the
+// polling of a word in the same line slows them further (measured: ~15 us for
+// 611 CTAs).  Here CTA b arrives at group counter b % kBarGroups; the last
+// arrival of a group arrives at the top counter; the last top arrival resets it
+// and advances the generation word, which the waiting CTAs poll with a backoff.
+// Every counter lives in its own 128-byte line.  Counters return to 0 after
+// each barrier, so the memory only has to be zeroed once (at state creation).
+// The gpu-scope fences also invalidate L1, so later plain loads see the data
+// other CTAs wrote before the barrier.
+__device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t *gen = bar + (kBarGroups + 1) * kBarLine;
+    uint32_t *top = bar + kBarGroups * kBarLine;
+    const int G = gridDim.x, g = blockIdx.x % kBarGroups;
+    const int gsize = G / kBarGroups + (g < G % kBarGroups ? 1 : 0);
+    const int ngroups = G < kBarGroups ? G : kBarGroups;
+    const uint32_t my_gen = ld_acquire_u32(gen);
+    __threadfence();
+    uint32_t *gc = bar + g * kBarLine;
+    if (atomicAdd(gc, 1u) == (uint32_t)gsize - 1) {
+      *gc = 0;
+      __threadfence();
+      if (atomicAdd(top, 1u) == (uint32_t)ngroups - 1) {
+        *top = 0;
+        __threadfence();
+        atomicAdd(gen, 1u);
+      }
+    }
+    while (ld_acquire_u32(gen) == my_gen) __nanosleep(64);
+    __threadfence();
+  }
+  __syncthreads();
 }
 
 // Block-wide sum over kFastTPB threads (uses fs.red; every thread gets the total).
@@ -385,32 +424,37 @@ __device__ __forceinline__ void fast_update_tile(const TableDev &tb, const State
 // block (r if the residue hit, else the lowest hit of the round) or -1.
 __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, int Lin,
                                          const ulonglong2 *__restrict__ T2, const uint64_t *__restrict__ srow,
-                                         int r, int lane, uint32_t &nl) {
+                                         int r, int off, int lane, uint32_t &nl) {
   for (int round = 0; round < kSelfRounds; ++round) {
     const int kb = round * kFirstScanFast;
     if (kb >= Lin) break;
+    // every load is issued unconditionally (out-of-range entries re-read a
+    // valid one and are masked after): loads inside per-entry branches would
+    // each wait for the previous one
     int pid[kProbeUnroll];
     uint64_t v[kProbeUnroll];
 #pragma unroll
     for (int q = 0; q < kProbeUnroll; ++q) {
-      const int k = kb + q * 32 + lane;
-      pid[q] = k < Lin ? (idx_old ? idx_old[k] : k) : -1;
+      const int j = kb + q * 32 + lane;
+      int k = off + (j < Lin ? j : 0);
+      if (k >= Lin) k -= Lin;
+      pid[q] = idx_old ? idx_old[k] : k;
     }
-    bool rh = false;
-    if (round == 0 && r >= 0) {
-      const ulonglong2 t = __ldcg(T2 + r);
-      const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)r);
-      rh = ((t.x & s.x) | (t.y & s.y)) != 0;
-      nl += 2;
-    }
+    const int rr = r >= 0 ? r : pid[0];
+    const ulonglong2 tr = __ldcg(T2 + rr);
+    const ulonglong2 sr = ld_sup2(srow + 2 * (int64_t)rr);
+    ulonglong2 t[kProbeUnroll], s[kProbeUnroll];
 #pragma unroll
     for (int q = 0; q < kProbeUnroll; ++q) {
-      v[q] = 0;
-      if (pid[q] >= 0) {
-        const ulonglong2 t = __ldcg(T2 + pid[q]);
-        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)pid[q]);
-        v[q] = (t.x & s.x) | (t.y & s.y);
-      }
+      t[q] = __ldcg(T2 + pid[q]);
+      s[q] = ld_sup2(srow + 2 * (int64_t)pid[q]);
+    }
+    const bool rh = round == 0 && r >= 0 && ((tr.x & sr.x) | (tr.y & sr.y)) != 0;
+    if (round == 0 && r >= 0) nl += 2;
+#pragma unroll
+    for (int q = 0; q < kProbeUnroll; ++q) {
+      const bool in = kb + q * 32 + lane < Lin;
+      v[q] = in ? ((t[q].x & s[q].x) | (t[q].y & s[q].y)) : 0ull;
     }
     nl += 2 * min(kFirstScanFast, Lin - kb);
     if (__any_sync(0xffffffffu, rh)) return __shfl_sync(0xffffffffu, r, 0);
@@ -487,6 +531,11 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
   }
 }
 
+#ifdef CT_PROBE_DEBUG
+// experiment builds only: per-item probe timing (globaltimer and SM id)
+__device__ unsigned long long g_probe_dbg[8192][4];
+#endif
+
 // ------------------------------------------------------------------ k_fast
 // Cooperative launch (all CTAs co-resident), kFastTPB threads, dynamic smem
 // fast_smem_bytes(n, Wd, R).  with_finalize = 0 for sharded tables (the flags are
@@ -531,7 +580,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       // experiment builds only (tools/gpu_exp.sh): 1 = update only, 2 = update +
       // barrier, -3 = ... + compaction, -4 = ... + probe; the call then reports a
       // made-up success
-      if (kFastStop == 2) grid_barrier(c);
+      if (kFastStop == 2) fast_grid_barrier(st.bar);
       if (t0) c->tph[2] = globaltimer();
       if (tid == 0) {
         fs.Lout = fs.L;
@@ -539,7 +588,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
       __syncthreads();
     } else {
-    grid_barrier(c);
+    fast_grid_barrier(st.bar);
     if (t0) c->tph[2] = globaltimer();
 
     // ---- compaction (a4): L_out and this CTA's tile prefixes from the tile counts
@@ -598,7 +647,25 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         const int row = p.items[item];
         const int r = (tb.use_res && lane == 0) ? st.res[row] : -1;
         uint32_t nl = 0;
-        const int hit = probe_row(idx_old, fs.L, T2, tb.S + (int64_t)row * tb.Wp, r, lane, nl);
+#ifdef CT_PROBE_SPREAD
+        const int off = (int)(((unsigned)row * 2654435761u) % (unsigned)fs.L);
+#else
+        const int off = 0;
+#endif
+#ifdef CT_PROBE_DEBUG
+        const unsigned long long pt0 = globaltimer();
+#endif
+        const int hit = probe_row(idx_old, fs.L, T2, tb.S + (int64_t)row * tb.Wp, r, off, lane, nl);
+#ifdef CT_PROBE_DEBUG
+        if (lane == 0 && item < 8192) {
+          unsigned smid;
+          asm("mov.u32 %0, %%smid;" : "=r"(smid));
+          g_probe_dbg[item][0] = pt0;
+          g_probe_dbg[item][1] = globaltimer();
+          g_probe_dbg[item][2] = ((unsigned long long)smid << 32) | (unsigned)blockIdx.x;
+          g_probe_dbg[item][3] = ((unsigned long long)nl << 32) | (unsigned)(hit + 1);
+        }
+#endif
         if (lane == 0) {
           f_loads += nl;
           if (hit >= 0) {
@@ -613,7 +680,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     if (t0) c->tph[3] = c->tph[4] = globaltimer();
     // ---- scan (a6b): misses x chunks of the compacted index, from entry 0
     if (Lout > 0 && may_miss && kFastStop > -3) {
-      grid_barrier(c);   // index complete, misses known
+      fast_grid_barrier(st.bar);   // index complete, misses known
       if (t0) c->tph[4] = globaltimer();
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
@@ -652,11 +719,13 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       if (f_loads) atomicAdd(&fs.cnt[2], (unsigned long long)f_loads);
     }
     __syncthreads();
+#ifndef CT_FAST_NOCOUNT
     if (tid == 0) {
       if (fs.cnt[0]) atomicAdd(&c->upd_loads, fs.cnt[0]);
       if (fs.cnt[1]) atomicAdd(&c->upd_writes, fs.cnt[1]);
       if (fs.cnt[2]) atomicAdd(&c->scan_loads, fs.cnt[2]);
     }
+#endif
   }
 
   // ---- completion: the last CTA to get here finalizes

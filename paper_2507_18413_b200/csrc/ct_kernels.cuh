@@ -48,6 +48,12 @@ constexpr uint32_t kRowMask = 0x3FFFFFFFu;   // update-list entry: row id
 constexpr uint32_t kEndBit = 1u << 30;        //   last row of its variable's group
 constexpr uint32_t kInvBit = 1u << 31;        //   group uses the Δ-branch (complemented)
 
+// k_fast's grid barrier: kBarGroups arrival counters and one top counter, each
+// in its own 128-byte line, and the generation word in another.
+constexpr int kBarGroups = 16;
+constexpr int kBarLine = 32;                              // uint32 words per 128-byte line
+constexpr int kBarWords = (kBarGroups + 2) * kBarLine;
+
 constexpr unsigned long long kFlagAgg = 1ull << 62;   // chained-scan tile status
 constexpr unsigned long long kFlagPre = 2ull << 62;
 
@@ -115,6 +121,7 @@ struct StateDev {
   unsigned long long *tilestat;  // [ntiles_max] chained-scan tile status
   uint64_t *out;            // [1 + 2 Wd]: status word, dom, pruned (sync path)
   uint64_t *slot;           // [Wd] removed (sync path, filled by an H2D copy)
+  uint32_t *bar;            // [kBarWords] k_fast hierarchical grid barrier (zeroed at creation)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -560,22 +567,28 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
       const int f = lane == 0 ? *(volatile const uint8_t *)supflag : 0;
       if (__shfl_sync(0xffffffffu, f, 0)) return -2;
     }
+    // loads are issued unconditionally (an out-of-range lane re-reads entry
+    // k0 and is masked after): a load inside a per-entry branch would wait for
+    // the previous one, serialising the round
     int pid[U];
     uint64_t v[U];
+    ulonglong2 t[U], s[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
       const int k = kb + q * 32 + lane;
-      pid[q] = k < k1 ? (idx ? idx[k] : k) : -1;
+      const int kk = k < k1 ? k : k0;
+      pid[q] = idx ? idx[kk] : kk;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      if (pid[q] >= 0) {
-        const ulonglong2 t = T2[pid[q]];
-        const ulonglong2 s = ld_sup2(srow + 2 * (int64_t)pid[q]);
-        v[q] = (t.x & s.x) | (t.y & s.y);
-      } else {
-        v[q] = 0;
-      }
+      t[q] = __ldcg(T2 + pid[q]);
+      s[q] = ld_sup2(srow + 2 * (int64_t)pid[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const bool in = kb + q * 32 + lane < k1;
+      v[q] = in ? ((t[q].x & s[q].x) | (t[q].y & s[q].y)) : 0ull;
+      if (!in) pid[q] = -1;
     }
     n_loads += 2 * min(32 * U, k1 - kb);
     int hit = -1;

@@ -75,7 +75,7 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // is what ct_state_copy moves; the rest is per-call scratch.
 struct StateLayout {
   size_t ctl, T, idx0, idx1, res, dom, persist;
-  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, desc, total;
+  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, desc, total;
 };
 
 }  // namespace
@@ -183,6 +183,7 @@ static StateLayout make_layout(const ct_table *tb) {
   L.tilestat = take((size_t)std::max(ntiles, 1) * 8);
   L.out = take((size_t)(1 + 2 * tb->Wd) * 8);
   L.slot = take((size_t)tb->Wd * 8);
+  L.bar = take((size_t)kBarWords * 4);
   L.desc = take(sizeof(StateDev));
   L.total = o;
   return L;
@@ -206,6 +207,7 @@ static StateDev make_desc(const ct_table *tb, char *mem) {
   s.tilestat = reinterpret_cast<unsigned long long *>(mem + L.tilestat);
   s.out = reinterpret_cast<uint64_t *>(mem + L.out);
   s.slot = reinterpret_cast<uint64_t *>(mem + L.slot);
+  s.bar = reinterpret_cast<uint32_t *>(mem + L.bar);
   return s;
 }
 
@@ -465,6 +467,13 @@ ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64
 }
 
 const char *ct_last_error(void) { return g_err; }
+
+#ifdef CT_PROBE_DEBUG
+// experiment builds only (not declared in ct.h)
+int ct_debug_probe_read(void *out, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(out, g_probe_dbg, bytes);
+}
+#endif
 const char *ct_version(void) { return "ct_b200 0.1 (sm_100a)"; }
 
 ct_status ct_nccl_unique_id(void *out128) {

@@ -178,6 +178,37 @@ __global__ void k_word(const uint64_t *__restrict__ S, int64_t Wp, const uint32_
   T[k] = tw & m;
 }
 
+// TLB probe: warp i reads 4 KB starting at S + i * stride_words (one 16-byte load
+// per lane per round, 8 rounds in flight), like the filter's first probe round.
+__global__ void k_tlb(const uint64_t *__restrict__ S, int64_t stride_words, int nwarps, unsigned long long *out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nwarps) return;
+  const uint64_t *base = S + (int64_t)w * stride_words;
+  uint64_t acc = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const ulonglong2 v = ld2(base + 2 * (q * 32 + lane));
+    acc ^= v.x ^ v.y;
+  }
+  if (acc == 0x12345) *out = acc;
+}
+
+// dependent-load latency: lane 0 chases n pointers through buf (index in the
+// low word of each 16-byte cell); reports ns per hop from %globaltimer
+__global__ void k_lat(const uint64_t *__restrict__ buf, int n, unsigned long long *out, int use_nc) {
+  if (threadIdx.x != 0) return;
+  uint64_t i = 0;
+  unsigned long long t0, t1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int k = 0; k < n; ++k) {
+    if (use_nc) i = ld2(buf + 2 * i).x;
+    else i = __ldcg(reinterpret_cast<const ulonglong2 *>(buf) + i).x;
+  }
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+  out[0] = (t1 - t0) / n;
+  out[1] = i;
+}
+
 // copy kernel for a bandwidth reference
 __global__ void k_copy(const ulonglong2 *__restrict__ a, ulonglong2 *__restrict__ b, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) b[i] = a[i];
@@ -291,6 +322,55 @@ int main() {
   run("word U=16 tpb=256", [&] { k_word<16><<<(W + 255) / 256, 256>>>(S, Wp, ul, nrows, T, W); });
   run("word U=16 tpb=128", [&] { k_word<16><<<(W + 127) / 128, 128>>>(S, Wp, ul, nrows, T, W); });
   run("word U=32 tpb=128", [&] { k_word<32><<<(W + 127) / 128, 128>>>(S, Wp, ul, nrows, T, W); });
+  // TLB test: 400 warps x 4 KB at row starts (1.25 MB apart) vs packed (4 KB apart),
+  // each right after a full 1-GB update pass (which leaves other pages in the TLB)
+  for (int rep = 0; rep < 3; ++rep)
+    for (int mode = 0; mode < 3; ++mode) {
+      const int64_t stride = mode == 0 ? Wp : (mode == 1 ? 512 : Wp * 2);
+      const int nw = mode == 2 ? 400 : 400;
+      cudaMemcpy(T, T0, Wp * 8, cudaMemcpyDeviceToDevice);
+      k_reg<16><<<(L + 127) / 128, 128>>>(S, Wp, ul, nrows, T2, L);
+      cudaEventRecord(e0);
+      k_tlb<<<(nw * 32 + 127) / 128, 128>>>(S + 2 * 1000, stride, mode == 2 ? 400 : nw, dummy);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("tlb probe %-22s %8.2f us\n", mode == 0 ? "rows 1.25 MB apart" : (mode == 1 ? "rows 4 KB apart" : "rows 2.5 MB apart"), ms * 1e3);
+    }
+  // pointer-chase latency through a random cycle over 1 GB (DRAM) and 1 MB (L2)
+  {
+    unsigned long long *dout;
+    CK(cudaMalloc(&dout, 16));
+    uint64_t *buf;
+    const int64_t cells_big = (int64_t)R * Wp / 2, cells_small = 65536;
+    CK(cudaMalloc(&buf, cells_big * 16));
+    for (int which = 0; which < 2; ++which) {
+      const int64_t cells = which ? cells_small : cells_big;
+      const int hops = 200;
+      std::vector<uint64_t> h(2 * hops, 0);
+      // chain of `hops` random cells: cell c_k holds c_{k+1}
+      std::vector<int64_t> c(hops + 1);
+      uint64_t x = 12345;
+      for (int k = 0; k <= hops; ++k) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; c[k] = k == 0 ? 0 : (int64_t)(x % cells); }
+      for (int k = 0; k < hops; ++k) {
+        uint64_t v[2] = {(uint64_t)c[k + 1], 0};
+        CK(cudaMemcpy(buf + 2 * c[k], v, 16, cudaMemcpyHostToDevice));
+      }
+      for (int nc = 0; nc < 2; ++nc) {
+        k_lat<<<1, 32>>>(buf, hops, dout, nc);   // warm TLB / L2
+        k_lat<<<1, 32>>>(buf, hops, dout, nc);
+        unsigned long long r[2];
+        CK(cudaMemcpy(r, dout, 16, cudaMemcpyDeviceToHost));
+        printf("latency %s %s: %llu ns per dependent load\n", which ? "L2 (1 MB)" : "1 GB", nc ? "ld.nc" : "ld.cg", r[0]);
+      }
+    }
+    // the same right after a streaming pass (1 GB region, cold chain)
+    cudaMemcpy(T, T0, Wp * 8, cudaMemcpyDeviceToDevice);
+    k_reg<16><<<(L + 127) / 128, 128>>>(S, Wp, ul, nrows, T2, L);
+    cudaDeviceSynchronize();
+    cudaFree(buf);
+  }
   // references: plain read and copy of the same 1 GB
   const int64_t n16 = (int64_t)R * Wp / 2;
   {
