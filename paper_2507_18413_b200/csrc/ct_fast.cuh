@@ -199,6 +199,15 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
+  // the first domain word of this thread is loaded before anything waits, so
+  // the control fields, the table metadata and the domains cost one round trip
+  uint64_t dm0 = 0, rm0 = 0;
+  int x0 = 0;
+  if (tid < Wd) {
+    dm0 = st.dom[tid];
+    rm0 = rem ? rem[tid] : 0ull;
+    x0 = tb.wordVar[tid];
+  }
   if (tid == 0) {
     fs.dead = c->dead;
     fs.fail = 0;
@@ -231,9 +240,9 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     for (int r = tid; r <= R; r += NT) st.sup[r] = 0;
   // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
   for (int k = tid; k < Wd; k += NT) {
-    const uint64_t dm = st.dom[k];
-    const uint64_t rm = rem ? rem[k] : 0ull;
-    const int x = tb.wordVar[k];
+    const uint64_t dm = k == tid ? dm0 : st.dom[k];
+    const uint64_t rm = k == tid ? rm0 : (rem ? rem[k] : 0ull);
+    const int x = k == tid ? x0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     p.din[k] = di;
     p.dl[k] = delta;

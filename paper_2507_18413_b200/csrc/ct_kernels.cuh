@@ -581,7 +581,7 @@ __device__ __forceinline__ int scan_pairs(const int32_t *__restrict__ idx, const
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      t[q] = __ldcg(T2 + pid[q]);
+      t[q] = T2[pid[q]];   // L1-cacheable: the batch probes re-read a state's blocks
       s[q] = ld_sup2(srow + 2 * (int64_t)pid[q]);
     }
 #pragma unroll
