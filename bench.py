@@ -2,7 +2,7 @@
 """Benchmark of the Compact-Table propagation hot path on B200 (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3bulk|c4]
+                    [--workload c3bulk|c3b|c4|c5]
 
 Default workload (BASELINE config 3, "c3bulk"): random positive table, arity 8,
 domain 100, 1e7 tuples (1.0 GB of support bitsets); one step = restore the
@@ -17,12 +17,17 @@ NCCL all-reduce inside every step (strong scaling: the table is fixed).
 point, CUDA events on the library stream, max over ranks).  `e2e` = the same
 metric through the synchronous host-buffer C call ct_propagate (H2D of the
 removal set and D2H of status+domains inside every step).  `roofline` = the
-dominant kernel (k_update): bytes it loads/stores per launch (counted by the
+dominant kernel (k_fast, the whole call in one launch): bytes it loads/stores per launch (counted by the
 kernel itself) / its CUDA-event duration, against MEASURED_PEAKS.json's HBM
 copy bandwidth.  `cpu_baseline` = the CPU oracle (oracle/, plain C brute
 force) on the host cores, rank 0 at N = 1 only.  `latency` = p50/p90/p99 of
 ct_propagate on BASELINE config 2 (arity 5, domain 20, 1e5 tuples, 1000
 random-removal calls, policy P(2, 0.5)).
+
+--workload c3b: the banded C3b table (x_i = (x0*c_i + u_i) mod 100, u_i < 10);
+each step fixes x0 to one seeded value, so 630 values of x1..x7 lose every
+support and the filter scans their whole rows over the compacted index: the
+HBM-bound filterDomains workload.  c4 / c5: see run_c4 / run_c5.
 
 --impl reference times the oracle (the reference arm of this tier) on the same
 workload, rank 0 only.
@@ -115,6 +120,29 @@ def c3_problem():
     return random_table(8, 100, 10_000_000, seed=3, name="C3 random n=8 d=100 t=1e7 seed=3")
 
 
+def c3b_problem():
+    from workloads import banded_table
+    return banded_table(8, 100, 10_000_000, seed=4, name="C3b banded n=8 d=100 t=1e7 seed=4")
+
+
+def fix_patterns(root_member, d, count: int, seed: int = 12):
+    """C3b calls: remove all but one seeded value of x0."""
+    from workloads import Rng, fix_one_value_removal
+    rng = Rng(seed)
+    return [fix_one_value_removal(rng, root_member, d, var=0) for _ in range(count)]
+
+
+WORKLOADS = {
+    "c3bulk": dict(metric="propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
+                   table="arity 8, domain 100, 1e7 tuples, seed 3",
+                   step="state restore (D2D) + ct_propagate_async of a bulk removal (50% of every var)"),
+    "c3b": dict(metric="propagations/s (C3b banded ct_propagate, filter-heavy, 1e7-tuple table)",
+                table="banded arity 8, domain 100, 1e7 tuples, seed 4 (x_i = (x0*c_i + u_i) mod 100, u_i < 10)",
+                step="state restore (D2D) + ct_propagate_async fixing x0 to one seeded value "
+                     "(630 unsupported values -> full filter scans)"),
+}
+
+
 def c2_problem():
     from workloads import random_table
     return random_table(5, 20, 100_000, seed=1, name="C2 random n=5 d=20 t=1e5 seed=1")
@@ -169,7 +197,8 @@ def run_ours(args):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.cuda.current_device()
-    p = c3_problem()
+    wl = WORKLOADS[args.workload]
+    p = c3_problem() if args.workload == "c3bulk" else c3b_problem()
     nid = broadcast_nccl_id() if world > 1 else None
     t0 = time.perf_counter()
     tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=world, shard_rank=rank, nccl_unique_id=nid)
@@ -177,7 +206,7 @@ def run_ours(args):
     assert tab.root_status == CT_OK
     root_m = bitmap_to_member(tab.root_dom, p.d)
     P = 16
-    pats = bulk_patterns(root_m, p.d, P)
+    pats = bulk_patterns(root_m, p.d, P) if args.workload == "c3bulk" else fix_patterns(root_m, p.d, P)
     wd = tab.Wd
     rem_host = np.stack([member_to_bitmap(m, p.d) for m in pats])                 # [P][Wd] uint64
     rem_dev = torch.from_numpy(rem_host.view(np.int64)).to(f"cuda:{dev}")
@@ -235,9 +264,12 @@ def run_ours(args):
     byts = 0
     for k in range(args.steps):
         c = per_pat[k % P]
+        # update: support words streamed + currTable read once + rewritten blocks + index in/out;
+        # filter: the support words it loads (its currTable / index re-reads are of data
+        # already counted once, and L2-resident: not counted again)
         b = 8 * c["loads"] + 16 * c["L_in"] + 16 * c["writes"] + 4 * (c["L_in"] + c["L_out"])
         if dom_kernel in ("fused", "small"):
-            b += 16 * c["scan"] + 2 * c["scan"]          # support + currTable words, index entries
+            b += 8 * c["scan"]
         byts += b
     k_bytes_per_launch = byts / max(k_n, 1)
     kernel_name = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_update") if dom_kernel in ("fused", "small") \
@@ -251,7 +283,7 @@ def run_ours(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            if tj.get("workload") == "c3bulk" and tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel_name:
+            if tj.get("workload") == args.workload and tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel_name:
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
@@ -280,23 +312,23 @@ def run_ours(args):
 
     # ---- p50 latency on config 2 (rank 0, N=1 only; latency-bound, not sharded)
     latency = None
-    if world == 1 and not args.skip_latency:
+    if world == 1 and not args.skip_latency and args.workload == "c3bulk":
         latency = c2_latency(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
-        cpu = cpu_baseline(p, root_m, pats, budget_s=args.cpu_budget)
+        cpu = cpu_baseline(p, root_m, pats, budget_s=args.cpu_budget, what=args.workload)
 
     tab.close()
     if rank == 0:
         line = {
-            "metric": "propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
+            "metric": wl["metric"],
             "value": value, "unit": "propagations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (seeded i.i.d. table, workloads/)",
-            "config": {"workload": "c3bulk", "table": "arity 8, domain 100, 1e7 tuples, seed 3",
-                       "step": "state restore (D2D) + ct_propagate_async of a bulk removal (50% of every var)",
+            "data": "synthetic (seeded " + ("i.i.d." if args.workload == "c3bulk" else "banded") + " table, workloads/)",
+            "config": {"workload": args.workload, "table": wl["table"],
+                       "step": wl["step"],
                        "patterns": P, "parallelism": f"tuple-range shards x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (1.0 GB supports streamed each step)",
                        "build_s": round(build_s, 3)},
@@ -372,7 +404,7 @@ def c2_latency(dev):
             "api": "ct_propagate (host buffers; single-CTA kernel in a CUDA graph; zero-copy I/O)"}
 
 
-def cpu_baseline(p, root_m, pats, budget_s=12.0):
+def cpu_baseline(p, root_m, pats, budget_s=12.0, what="c3bulk"):
     import oracle
     oracle.lib()
     n = 0
@@ -383,7 +415,8 @@ def cpu_baseline(p, root_m, pats, budget_s=12.0):
         n += 1
     dt = time.perf_counter() - t0
     return {"value": n / dt, "unit": "propagations/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} full C3 bulk propagations (oracle/ct_oracle.c brute-force scan of all 1e7 tuples, "
+            "sample": f"{n} full {'C3 bulk' if what == 'c3bulk' else 'C3b banded'} propagations "
+                      f"(oracle/ct_oracle.c brute-force scan of all 1e7 tuples, "
                       f"single thread) in {dt:.1f} s", "host_nproc": os.cpu_count()}
 
 
@@ -616,7 +649,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c4", "c5"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5"])
     ap.add_argument("--max-nodes", type=int, default=10_000, help="c5: DFS node budget")
     ap.add_argument("--states", type=int, default=4096, help="c4: total independent states (split over ranks)")
     ap.add_argument("--skip-cpu", action="store_true")

@@ -58,11 +58,16 @@ constexpr int kFastTPB = CT_FAST_TPB;                  // k_fast threads per CTA
 constexpr int kFastWarps = kFastTPB / 32;
 constexpr int kFastUnroll = CT_FAST_UNROLL;            // support rows in flight per update thread
 #ifndef CT_PROBE_UNROLL
-#define CT_PROBE_UNROLL 8
+#define CT_PROBE_UNROLL 6
 #endif
 constexpr int kProbeUnroll = CT_PROBE_UNROLL;          // index entries per lane per probe round
 constexpr int kFirstScanFast = 32 * kProbeUnroll;      // index entries per probe round
-constexpr int kSelfRounds = 32 / kProbeUnroll;         // probe rounds before a miss is queued (1024 entries)
+#ifndef CT_SCAN_U
+#define CT_SCAN_U 4
+#endif
+constexpr int kScanFastU = CT_SCAN_U;                  // index entries per lane per scan unit
+constexpr int kFastChunk = 32 * kScanFastU;            // index entries per scan unit
+constexpr int kSelfRounds = (32 + kProbeUnroll - 1) / kProbeUnroll;   // probe rounds before a miss is queued (~1024 entries)
 #ifdef CT_FAST_STOP
 constexpr int kFastStop = CT_FAST_STOP;                // experiment builds only
 #else
@@ -386,14 +391,14 @@ __device__ __forceinline__ void fast_update_tile(const TableDev &tb, const State
     const ulonglong2 tw = T2[pid];
     const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
     uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-    for (int p0 = 0; p0 < nrows; p0 += kFastUnroll) {
+    int p0 = 0;
+    for (; p0 < nrows; p0 += kFastUnroll) {
       if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 16-byte block
       ulonglong2 v[kFastUnroll];
 #pragma unroll
       for (int q = 0; q < kFastUnroll; ++q)
         v[q] = (p0 + q < nrows) ? ld_sup2(col + (int64_t)(ulist[p0 + q] & kRowMask) * Wp)
                                 : make_ulonglong2(0ull, 0ull);
-      n_loads += 2 * min(kFastUnroll, nrows - p0);
 #pragma unroll
       for (int q = 0; q < kFastUnroll; ++q) {
         if (p0 + q < nrows) {
@@ -413,6 +418,7 @@ __device__ __forceinline__ void fast_update_tile(const TableDev &tb, const State
         }
       }
     }
+    n_loads += 2 * min(p0, nrows);   // rows issued before the block died or the list ended
     const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
     if (nt.x != tw.x || nt.y != tw.y) {
       T2[pid] = nt;
@@ -694,24 +700,68 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
-      const int nch = (Ls + kScanChunk - 1) / kScanChunk;
-      const int64_t total = (int64_t)nch * nscan;
-      for (int64_t u = gw; u < total; u += nw) {   // chunk-major: early chunks of every miss first
-        const int chunk = (int)(u / nscan);
-        const int item = (int)(u - (int64_t)chunk * nscan);
-        const int row = __ldcg(st.scanlist + item);
-        const int fl = lane == 0 ? *(volatile const uint8_t *)(st.sup + row) : 0;
-        if (__shfl_sync(0xffffffffu, fl, 0)) continue;
-        const int k0 = chunk * kScanChunk;
-        const int k1 = min(k0 + kScanChunk, Ls);
-        uint32_t nl = 0;
-        const int hit = scan_pairs<kScanUnroll>(idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, st.sup + row, lane,
-                                                nl);
-        if (lane == 0) {
-          f_loads += nl;
-          if (hit >= 0) {
-            st.sup[row] = 1;
-            st.res[row] = hit;
+      // work unit = (chunk of kFastChunk index entries, group of 32 misses),
+      // chunk-major.  A warp loads the chunk's index entries and currTable
+      // words ONCE and then streams the support words of every still
+      // unresolved miss of its group over them (the next miss's words are in
+      // flight while the current one is tested), so the currTable / index
+      // traffic is amortised over the group and each miss costs one round trip.
+      const int ngrp = (nscan + 31) / 32;
+      const int nch = (Ls + kFastChunk - 1) / kFastChunk;
+      const int64_t total = (int64_t)nch * ngrp;
+      for (int64_t u = gw; u < total; u += nw) {
+        const int chunk = (int)(u / ngrp), grp = (int)(u - (int64_t)chunk * ngrp);
+        const int k0 = chunk * kFastChunk;
+        const int m = grp * 32 + lane;
+        const int rowl = m < nscan ? __ldcg(st.scanlist + m) : -1;
+        const int fl = rowl >= 0 ? *(volatile const uint8_t *)(st.sup + rowl) : 1;
+        unsigned todo = __ballot_sync(0xffffffffu, fl == 0);
+        if (!todo) continue;
+        int pid[kScanFastU];
+        ulonglong2 t[kScanFastU];
+#pragma unroll
+        for (int q = 0; q < kScanFastU; ++q) {
+          const int k = k0 + q * 32 + lane;
+          const int kk = k < Ls ? k : k0;
+          pid[q] = idx ? __ldcg(idx + kk) : kk;
+        }
+#pragma unroll
+        for (int q = 0; q < kScanFastU; ++q) t[q] = T2[pid[q]];
+        const int nwords = 2 * min(kFastChunk, Ls - k0);
+        int row = __shfl_sync(0xffffffffu, rowl, __ffs(todo) - 1);
+        ulonglong2 sc[kScanFastU];
+#pragma unroll
+        for (int q = 0; q < kScanFastU; ++q) sc[q] = ld_sup2(tb.S + (int64_t)row * tb.Wp + 2 * (int64_t)pid[q]);
+        while (todo) {
+          const unsigned rest = todo & (todo - 1);
+          int row_n = row;
+          ulonglong2 sn[kScanFastU];
+          if (rest) {
+            row_n = __shfl_sync(0xffffffffu, rowl, __ffs(rest) - 1);
+#pragma unroll
+            for (int q = 0; q < kScanFastU; ++q)
+              sn[q] = ld_sup2(tb.S + (int64_t)row_n * tb.Wp + 2 * (int64_t)pid[q]);
+          }
+          int hit = -1;
+#pragma unroll
+          for (int q = kScanFastU - 1; q >= 0; --q) {
+            const bool in = k0 + q * 32 + lane < Ls;
+            const uint64_t v = in ? ((t[q].x & sc[q].x) | (t[q].y & sc[q].y)) : 0ull;
+            const unsigned b = __ballot_sync(0xffffffffu, v != 0);
+            if (b) hit = __shfl_sync(0xffffffffu, pid[q], __ffs(b) - 1);
+          }
+          if (lane == 0) {
+            f_loads += nwords;
+            if (hit >= 0) {
+              st.sup[row] = 1;
+              st.res[row] = hit;
+            }
+          }
+          todo = rest;
+          row = row_n;
+          if (rest) {
+#pragma unroll
+            for (int q = 0; q < kScanFastU; ++q) sc[q] = sn[q];
           }
         }
       }

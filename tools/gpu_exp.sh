@@ -3,14 +3,13 @@ python - <<'PY'
 import sys; sys.path.insert(0, '.')
 from paper_2507_18413_b200 import build as B
 B.build()
-V = {"pu4": ["-DCT_PROBE_UNROLL=4"], "stop3": ["-DCT_FAST_STOP=-3"], "stop4": ["-DCT_FAST_STOP=-4"], "stop4pu4": ["-DCT_FAST_STOP=-4", "-DCT_PROBE_UNROLL=4"]}
+V = {"pf1": ["-DCT_SCAN_PF=1"], "pf2": ["-DCT_SCAN_PF=2"], "pf3": ["-DCT_SCAN_PF=3"]}
 from concurrent.futures import ThreadPoolExecutor
 with ThreadPoolExecutor(7) as ex:
     list(ex.map(lambda kv: B.build(extra=kv[1], out=f'paper_2507_18413_b200/libct_b200_{kv[0]}.so'), V.items()))
 PY
-CT_TAG=full timeout 300 python tools/exp_fast.py 100
-for v in pu4 stop3 stop4 stop4pu4; do
-  CT_TAG=$v CT_LIB_PATH=paper_2507_18413_b200/libct_b200_$v.so timeout 300 python tools/exp_fast.py 100
+for v in "" pf1 pf2 pf3; do
+  if [ -z "$v" ]; then L=""; else L="paper_2507_18413_b200/libct_b200_$v.so"; fi
+  CT_LIB_PATH=$L timeout 600 python bench.py --workload c3b --steps 100 --warmup 5 --skip-cpu | python -c "import json,sys; d=json.load(sys.stdin); print('$v c3b', d['value'], d['roofline']['ms_per_launch'], d['roofline']['frac'])"
 done
 rm -f paper_2507_18413_b200/libct_b200_*.so
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "^FAILED|^E  |passed|failed" | head
