@@ -144,6 +144,9 @@ typedef struct ct_table_info {
                                 /* 1 k_fused (grid barrier per phase), 2 k_fast (per-CTA   */
                                 /* ingest, 1-2 grid barriers), 3 k_small (one CTA)         */
   int32_t grid;                 /* CTAs of the single-state launch                       */
+  int32_t batch_tile;           /* ct_propagate_many: 16-byte blocks per shared-memory    */
+                                /* support tile of the tile-major update (32, 16 or 8), or */
+                                /* 0 = one pass per state (R too large for the tile)      */
 } ct_table_info;
 
 ct_status ct_table_info_get(const ct_table *t, ct_table_info *out);
@@ -273,6 +276,8 @@ void ct_model_destroy(ct_model *m);
 /* ---------------------------------------------------------------- introspection */
 /* Test/measurement only.  currTable of this shard: host uint64[words]. */
 ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits);
+/* currTable of state i of a batch: host uint64[words]. */
+ct_status ct_batch_read_table(const ct_batch *b, int32_t i, uint64_t *out_bits);
 /* One support row (row = rowbase_i + v - lo_i) of this shard: host uint64[words]. */
 ct_status ct_table_read_supports(const ct_table *t, int32_t row, uint64_t *out_bits);
 /* Current domains of a state (its last fixpoint): host uint64[Wd]. */
@@ -299,6 +304,10 @@ typedef struct ct_stats {
                             /* finalize.  Not written by the per-phase kernels.            */
 } ct_stats;
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
+/* The same counters for every state of a batch (last ct_propagate_many call):
+ * out = host ct_stats[ct_batch_size(b)], caller-owned.  Waits for the table's
+ * stream.  phase_ns is 0 (the batch kernels do not stamp phases). */
+ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
 
 /* Per-kernel device timing (measurement only).  While enabled, every
  * *_async / ct_propagate_many call on this table's states and batches records a

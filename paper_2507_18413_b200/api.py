@@ -130,6 +130,12 @@ class Batch:
     def restore_dead(self, src: State):
         C.ct_batch_restore_dead(self.handle, src.handle)
 
+    def stats(self):
+        return C.ct_batch_stats(self.handle, self.S)
+
+    def read_table(self, index: int) -> np.ndarray:
+        return C.ct_batch_read_table(self.handle, index, int(self.table.info.words))
+
     def propagate(self, removed=None):
         wd = self.table.Wd
         out = np.zeros((self.S, max(wd, 1)), np.uint64)

@@ -1,0 +1,440 @@
+// ct_batch.cuh -- batched propagation of S independent states of ONE table
+// (ct_propagate_many), tile-major.
+//
+// The per-state kernels of ct_kernels.cuh give every state its own pass over
+// its currTable, so each (support row, 16-byte block) pair is fetched once per
+// state that needs it: on BASELINE config 4 (4096 states, 37.5 MB of supports)
+// that is ~6.9 GB of support words per step, which does not stay in L2 next to
+// 512 MB of streamed currTables.  Here the work is ordered the other way round:
+//
+//   k_bupdate  (a3-a5) a CTA owns a column tile of kTW 16-byte blocks, stages
+//              ALL R support rows of that tile in shared memory once (R·kTW·16
+//              bytes), then streams the currTable blocks of a whole range of
+//              states through it.  Lanes map to (state, block): 32/kTW states
+//              per warp, every support access is a conflict-free 16-byte
+//              shared-memory load, every currTable access a coalesced 16-byte
+//              global load.  Alg. 2 per block as in
+//              update_tile: the per-variable OR of the listed rows, complemented
+//              for the Δ-branch, ANDed over the changed variables, the block
+//              dies early (L175) once nothing valid is left in it.
+//              Batch states are DENSE: the update visits every block of the
+//              state (a zero block costs one 16-byte read and no support load),
+//              so there is no per-state index to compact; after the call the
+//              state's index is the identity over its W2 blocks.
+//   k_bprobe   (a6a) one THREAD per (state, filter item): residue probe
+//              (PAPER.md L220): T[res] & S[x,a][res] != 0 settles the value,
+//              else the next few blocks; a miss goes to a global miss list.
+//   k_bscan    (a6b) a warp per miss over the first blocks, then (miss, chunk)
+//              units over the rest for the misses still open.
+//   k_bingest / k_bfinalize: dev_ingest / dev_finalize (ct_kernels.cuh) with
+//              128-thread CTAs, one per state.
+#pragma once
+#include "ct_kernels.cuh"
+
+namespace ctk {
+
+constexpr int kBTPB = 1024;        // k_bupdate threads per CTA
+constexpr int kBSmallTPB = 128;    // k_bingest / k_bfinalize threads per CTA (one state each)
+constexpr int kBProbeTPB = 256;
+constexpr int kBScanTPB = 256;
+
+// Device view of a batch: S state blocks of `pitch` bytes in one pool, field
+// offsets from ct_runtime.cu's StateLayout.
+struct BatchDev {
+  char *pool;
+  int64_t pitch;
+  int64_t o_ctl, o_T, o_ulist, o_items, o_res, o_sup, o_scan, o_idx0, o_idx1, o_bmask;
+  int32_t *bgo;              // [S] per call: update-list length, or -1 if the state does not update
+  int2 *miss, *miss2;        // [S·R] global lists of (state, row) probe misses (pass 0 / pass 1 of k_bscan)
+  int32_t *nmiss, *nmiss2;   // their lengths (zeroed by k_bingest)
+};
+
+__device__ __forceinline__ Ctl *bctl(const BatchDev &b, int s) {
+  return reinterpret_cast<Ctl *>(b.pool + (int64_t)s * b.pitch + b.o_ctl);
+}
+template <typename T>
+__device__ __forceinline__ T *bfield(const BatchDev &b, int s, int64_t off) {
+  return reinterpret_cast<T *>(b.pool + (int64_t)s * b.pitch + off);
+}
+
+// ------------------------------------------------------------------ a2: ingest, one CTA per state
+__global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const StateDev *__restrict__ states,
+                                                       const uint64_t *__restrict__ removed,
+                                                       int64_t removed_stride, int32_t *__restrict__ bgo,
+                                                       int32_t *__restrict__ bd_nmiss, int32_t *__restrict__ bd_nmiss2) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const StateDev &st = states[blockIdx.x];
+  const uint64_t *rem = removed ? removed + (int64_t)blockIdx.x * removed_stride : nullptr;
+  dev_ingest<kBSmallTPB>(tb, st, rem, 0, smem);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *bd_nmiss = 0;
+    *bd_nmiss2 = 0;
+  }
+  if (threadIdx.x == 0) {   // the thread that wrote the control fields
+    Ctl *c = st.ctl;
+    const bool go = !(c->skip | c->noop | c->fail_fast);
+    bgo[blockIdx.x] = go ? c->nrows : -1;
+  }
+}
+
+// ------------------------------------------------------------------ a3-a5: tile-major update
+// 16-byte shared-memory load at a 32-bit shared address.
+__device__ __forceinline__ ulonglong2 lds128(uint32_t addr) {
+  ulonglong2 v;
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "r"(addr));
+  return v;
+}
+
+// One state's tile when the tile is a full warp (kTW = 32): every lane works on
+// the same state, so the walk over the update list is warp-uniform and split
+// at the variable-group ends (one ballot per 32 entries).  Per row: a shuffle
+// of the row's byte offset, a 16-byte shared load and 3-input ORs, four rows
+// per step.  Lanes whose block is already dead keep loading (no predicate, no
+// branch): their mask only shrinks, so their result stays 0.  `s_lane` =
+// shared address of this lane's column of row 0, `zrow` = byte offset of the
+// all-zero row R.  Returns the new block value; adds to `nl` (on every lane)
+// the rows the warp's live blocks needed.
+__device__ __forceinline__ ulonglong2 tile32_state(uint32_t s_lane, uint32_t zrow, const uint32_t *ul, int nr,
+                                                   uint32_t ev, ulonglong2 tw, bool live, uint32_t &nl) {
+  const int lane = threadIdx.x & 31;
+  uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+  if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+  for (int p0 = 0; p0 < nr; p0 += 32) {
+    if (p0 > 0) ev = p0 + lane < nr ? __ldcg(ul + p0 + lane) : 0u;
+    const int cnt = min(32, nr - p0);
+    const uint32_t rbyte = (ev & kRowMask) * 512u;          // entry `lane`: its row's byte offset in s_sup
+    unsigned ends = __ballot_sync(0xffffffffu, (ev & kEndBit) != 0u);
+    if (cnt < 32) ends &= (1u << cnt) - 1u;
+    int q = 0;
+    while (q < cnt) {
+      const int qe = ends ? __ffs(ends) - 1 : cnt - 1;     // last entry of this group in the chunk
+      // four rows per step; entries past the group's end read the zero row
+      for (int k = q; k <= qe; k += 4) {
+        uint32_t r0 = __shfl_sync(0xffffffffu, rbyte, k), r1 = __shfl_sync(0xffffffffu, rbyte, (k + 1) & 31);
+        uint32_t r2 = __shfl_sync(0xffffffffu, rbyte, (k + 2) & 31), r3 = __shfl_sync(0xffffffffu, rbyte, (k + 3) & 31);
+        if (k + 1 > qe) r1 = zrow;
+        if (k + 2 > qe) r2 = zrow;
+        if (k + 3 > qe) r3 = zrow;
+        const ulonglong2 v0 = lds128(s_lane + r0), v1 = lds128(s_lane + r1);
+        const ulonglong2 v2 = lds128(s_lane + r2), v3 = lds128(s_lane + r3);
+        ax |= v0.x | v1.x;
+        ay |= v0.y | v1.y;
+        ax |= v2.x | v3.x;
+        ay |= v2.y | v3.y;
+      }
+      nl += (uint32_t)(qe - q + 1) * (uint32_t)__popc(__ballot_sync(0xffffffffu, live));   // warp total
+      if (ends) {                                           // the group ends here: AND its mask in
+        const bool inv = (__shfl_sync(0xffffffffu, ev, qe) & kInvBit) != 0u;
+        if (inv) {
+          mx &= ~ax;
+          my &= ~ay;
+        } else {
+          mx &= ax;
+          my &= ay;
+        }
+        ax = ay = 0;
+        live = live && ((tw.x & mx) | (tw.y & my)) != 0;   // Alg. 2, per block
+        ends &= ends - 1u;
+        if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+      }
+      q = qe + 1;
+    }
+  }
+  return make_ulonglong2(tw.x & mx, tw.y & my);
+}
+
+// Persistent: CTA c processes the contiguous unit range [U·c/G, U·(c+1)/G) of
+// the U = ntiles·nchunk units (tile-major: unit u = (tile u / nchunk, state
+// chunk u % nchunk)), so it reloads its shared support tile at most a few
+// times.  Dynamic shared memory: R·kTW 16-byte entries.  Per (state, tile) the
+// survivor bits go to the state's block bitmap (k_bcompact builds the index).
+template <int kTW>
+__global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, int S, int ntiles, int nchunk,
+                                                     int chunk_states) {
+  extern __shared__ __align__(16) ulonglong2 s_sup[];   // [R + 1][kTW], row R = 0
+  constexpr int SPW = 32 / kTW;                         // states per warp
+  const int R = tb.R, W2 = tb.W2;
+  const int64_t Wp = tb.Wp, Wp2 = tb.Wp / 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int sub = lane / kTW, bl = lane % kTW;
+  const uint32_t s_lane = (uint32_t)__cvta_generic_to_shared(s_sup) + 16u * (uint32_t)bl;
+  const int64_t units = (int64_t)ntiles * nchunk;
+  const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+  int cur_tile = -1;
+  for (int64_t u = u0; u < u1; ++u) {
+    const int tile = (int)(u / nchunk), chunk = (int)(u - (int64_t)tile * nchunk);
+    if (tile != cur_tile) {
+      __syncthreads();   // every warp is done with the previous tile
+      for (int i = threadIdx.x; i < (R + 1) * kTW; i += blockDim.x) {
+        const int row = i / kTW;
+        const int64_t blk = (int64_t)tile * kTW + (i - row * kTW);
+        s_sup[i] = (row < R && blk < Wp2) ? ld_sup2(tb.S + (int64_t)row * Wp + 2 * blk)
+                                          : make_ulonglong2(0ull, 0ull);
+      }
+      __syncthreads();
+      cur_tile = tile;
+    }
+    const int s0 = chunk * chunk_states, s1 = min(S, s0 + chunk_states);
+    const int blk = tile * kTW + bl;
+    const bool inblk = blk < W2;
+    // software pipeline: the next state's go word, currTable block and first
+    // update-list entries are in flight while the current state is processed
+    int s = s0 + warp * SPW + sub;
+    const int step = nwarps * SPW;
+    int go_n = -1;
+    ulonglong2 tw_n = make_ulonglong2(0ull, 0ull);
+    uint32_t ev_n = 0;
+    auto fetch = [&](int ss) {
+      go_n = -1;
+      tw_n = make_ulonglong2(0ull, 0ull);
+      ev_n = 0;
+      if (ss < s1) {
+        go_n = __ldcg(bd.bgo + ss);
+        if (inblk) tw_n = __ldcg(bfield<ulonglong2>(bd, ss, bd.o_T) + blk);
+        if (bl < R) ev_n = __ldcg(bfield<uint32_t>(bd, ss, bd.o_ulist) + bl);
+      }
+    };
+    fetch(s);
+    for (int base = s0 + warp * SPW; base < s1; base += step, s += step) {
+      const int nr = go_n;
+      const ulonglong2 tw = tw_n;
+      uint32_t ev = ev_n;
+      fetch(s + step);
+      const bool upd = nr >= 0 && inblk;         // this lane's block takes part in the update
+      const bool had = upd && (tw.x | tw.y) != 0;
+      uint32_t nl = 0;
+      const uint32_t *ul = bfield<uint32_t>(bd, min(s, S - 1), bd.o_ulist);
+      ulonglong2 nt;
+      if constexpr (kTW == 32) {
+        if (nr < 0) continue;                    // warp-uniform: one state per warp
+        nt = tile32_state(s_lane, (uint32_t)R * 512u, ul, nr, ev, tw, had, nl);
+      } else {
+        bool live = had;
+        uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+        const int maxn = __reduce_max_sync(0xffffffffu, live ? nr : 0);
+        for (int p0 = 0; p0 < maxn; p0 += kTW) {
+          if (p0 > 0) ev = (nr >= 0 && p0 + bl < nr) ? __ldcg(ul + p0 + bl) : 0u;
+          const int cnt = min(kTW, maxn - p0);
+          for (int q0 = 0; q0 < cnt; q0 += 8) {
+#pragma unroll
+            for (int q = q0; q < q0 + 8; ++q) {
+              const uint32_t e = __shfl_sync(0xffffffffu, ev, sub * kTW + (q & (kTW - 1)));
+              if (live && p0 + q < nr && q < kTW) {
+                const ulonglong2 v = s_sup[(e & kRowMask) * kTW + bl];
+                ++nl;
+                ax |= v.x;
+                ay |= v.y;
+                if (e & kEndBit) {
+                  if (e & kInvBit) {
+                    mx &= ~ax;
+                    my &= ~ay;
+                  } else {
+                    mx &= ax;
+                    my &= ay;
+                  }
+                  ax = ay = 0;
+                  live = ((tw.x & mx) | (tw.y & my)) != 0;   // Alg. 2, per block
+                }
+              }
+            }
+          }
+          if (!__any_sync(0xffffffffu, live)) break;
+        }
+        nt = make_ulonglong2(tw.x & mx, tw.y & my);
+      }
+      const bool wr = had && (nt.x != tw.x || nt.y != tw.y);
+      if (wr) bfield<ulonglong2>(bd, s, bd.o_T)[blk] = nt;
+      const bool keep = had && (nt.x | nt.y) != 0;
+      const unsigned bk = __ballot_sync(0xffffffffu, keep), bw = __ballot_sync(0xffffffffu, wr);
+      if constexpr (kTW < 32) {
+#pragma unroll
+        for (int o = 1; o < kTW; o <<= 1) nl += __shfl_xor_sync(0xffffffffu, nl, o);
+      }
+      if (bl == 0 && nr >= 0) {
+        // survivor bits of this tile -> bits [tile·kTW, tile·kTW + kTW) of the bitmap
+        uint8_t *bm = bfield<uint8_t>(bd, s, bd.o_bmask);
+        const unsigned bits = kTW == 32 ? bk : (bk >> (sub * kTW)) & ((1u << kTW) - 1u);
+        if (kTW == 32) reinterpret_cast<uint32_t *>(bm)[tile] = bits;
+        else if (kTW == 16) reinterpret_cast<uint16_t *>(bm)[tile] = (uint16_t)bits;
+        else bm[tile] = (uint8_t)bits;
+        Ctl *c = bctl(bd, s);
+        const unsigned smask = kTW == 32 ? 0xffffffffu : (((1u << kTW) - 1u) << (sub * kTW));
+        const int cw = __popc(bw & smask);
+        if (nl) atomicAdd(&c->upd_loads, 2ull * nl);
+        if (cw) atomicAdd(&c->upd_writes, (unsigned long long)cw);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a4: index compaction, one CTA per state
+// The order-preserving index of the non-zero blocks (RSparseBitSet, SURVEY
+// §8(a) a4) from the survivor bitmap k_bupdate wrote: a block scan of the
+// words' popcounts, then every thread expands its word's set bits.  Writes
+// L_out; the index goes to the buffer the single-state path would write (so a
+// batch state continues exactly like a single state).
+__global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev bd) {
+  const int s = blockIdx.x;
+  if (__ldcg(bd.bgo + s) < 0) return;
+  __shared__ uint64_t s_warp[kBSmallTPB / 32];
+  Ctl *c = bctl(bd, s);
+  const uint32_t *bm = bfield<const uint32_t>(bd, s, bd.o_bmask);
+  int32_t *idx_out = bfield<int32_t>(bd, s, __ldcg(&c->parity) ? bd.o_idx0 : bd.o_idx1);
+  const int nw = (tb.W2 + 31) >> 5;
+  uint64_t carry = 0;
+  for (int base = 0; base < nw; base += kBSmallTPB) {
+    const int k = base + threadIdx.x;
+    uint32_t w = k < nw ? __ldcg(bm + k) : 0u;
+    uint64_t total;
+    const uint64_t ex = block_excl_scan<kBSmallTPB>((uint64_t)__popc(w), s_warp, total);
+    if (tb.use_index) {
+      int pos = (int)(carry + ex);
+      while (w) {
+        const int b = __ffs(w) - 1;
+        w &= w - 1u;
+        idx_out[pos++] = k * 32 + b;
+      }
+    }
+    carry += total;
+  }
+  if (threadIdx.x == 0) c->L_out = (int32_t)carry;
+}
+
+// ------------------------------------------------------------------ a6a: residue probe, one thread per item
+// Appends (state, row) to a global miss list, one atomic per warp.
+__device__ __forceinline__ void bmiss_push(const BatchDev &bd, int2 *list, int *count, bool miss, int s, int row) {
+  const unsigned m = __ballot_sync(0xffffffffu, miss);
+  if (!m) return;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (miss) list[base + __popc(m & lanemask_lt())] = make_int2(s, row);
+}
+
+// grid = ceil(S·Rp / kBProbeTPB), Rp = max(R, 1): thread (s, i) takes item i
+// of state s.  Residue probe; on a miss the same thread tries
+// the kBProbeNext blocks after the residue (all loads in flight together: on
+// tables with spread-out supports a support is usually a few blocks away), and
+// only then queues the item for k_bscan.  Thread (s, 0) also publishes
+// "currTable non-empty" (sup[R]).
+constexpr int kBProbeNext = 4;
+__global__ void __launch_bounds__(kBProbeTPB) k_bprobe(TableDev tb, BatchDev bd, int S) {
+  const int Rp = max(tb.R, 1), W2 = tb.W2;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int s = (int)(gid / Rp), i = (int)(gid - (int64_t)s * Rp);
+  bool miss = false;
+  int row = 0;
+  if (s < S && __ldcg(bd.bgo + s) >= 0) {
+    Ctl *c = bctl(bd, s);
+    const int Lout = __ldcg(&c->L_out);
+    uint8_t *sup = bfield<uint8_t>(bd, s, bd.o_sup);
+    if (i == 0) sup[tb.R] = Lout > 0;
+    if (Lout > 0 && i < __ldcg(&c->nitems)) {
+      row = __ldcg(bfield<int32_t>(bd, s, bd.o_items) + i);
+      miss = true;
+      if (tb.use_res) {
+        int32_t *res = bfield<int32_t>(bd, s, bd.o_res);
+        const ulonglong2 *T2 = bfield<const ulonglong2>(bd, s, bd.o_T);
+        const uint64_t *srow = tb.S + (int64_t)row * tb.Wp;
+        const int r = __ldcg(res + row);
+        const ulonglong2 t = __ldcg(T2 + r);
+        const ulonglong2 v = ld_sup2(srow + 2 * (int64_t)r);
+        if (((t.x & v.x) | (t.y & v.y)) != 0) {
+          sup[row] = 1;
+          miss = false;
+        } else {
+          int blk[kBProbeNext];
+          ulonglong2 tn[kBProbeNext], vn[kBProbeNext];
+#pragma unroll
+          for (int q = 0; q < kBProbeNext; ++q) {
+            int k = r + 1 + q;
+            blk[q] = k < W2 ? k : k % W2;
+          }
+#pragma unroll
+          for (int q = 0; q < kBProbeNext; ++q) {
+            tn[q] = __ldcg(T2 + blk[q]);
+            vn[q] = ld_sup2(srow + 2 * (int64_t)blk[q]);
+          }
+          int hit = -1;
+#pragma unroll
+          for (int q = kBProbeNext - 1; q >= 0; --q)
+            if (((tn[q].x & vn[q].x) | (tn[q].y & vn[q].y)) != 0) hit = blk[q];
+          if (hit >= 0) {
+            sup[row] = 1;
+            res[row] = hit;
+            miss = false;
+          }
+        }
+      }
+      if (miss) atomicAdd(&c->nscan, 1);
+    }
+  }
+  bmiss_push(bd, bd.miss, bd.nmiss, miss, s, row);
+}
+
+// ------------------------------------------------------------------ a6b: scan of the probe misses
+// Pass 0: one warp per miss of the global list, rounds of 32·kScanUnroll
+// blocks from block 0 (CT's intersectIndex over the dense index), at most
+// kBScanRounds rounds; a miss still unresolved goes to the second list.
+// Pass 1: (miss, chunk) units of the second list, chunk-major over the
+// remaining blocks (long scans: values that lost every support, correlated
+// tables), each re-checking the miss's flag between rounds.
+constexpr int kBScanRounds = 4;
+constexpr int kBScanFirst = kBScanRounds * 32 * kScanUnroll;   // blocks scanned by pass 0
+__global__ void __launch_bounds__(kBScanTPB) k_bscan(TableDev tb, BatchDev bd, int pass) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (kBScanTPB / 32) + (threadIdx.x >> 5), nw = gridDim.x * (kBScanTPB / 32);
+  const int Lmax = tb.W2;   // chunks are laid out over the largest possible index
+  const int nm = __ldcg(pass == 0 ? bd.nmiss : bd.nmiss2);
+  const int2 *list = pass == 0 ? bd.miss : bd.miss2;
+  const int nch = pass == 0 ? 1 : (Lmax > kBScanFirst ? (Lmax - kBScanFirst + kScanChunk - 1) / kScanChunk : 0);
+  const int64_t total = (int64_t)nm * nch;
+  for (int64_t u = gw; u < total; u += nw) {
+    const int chunk = (int)(u / nm);
+    const int2 e = __ldcg(list + (int)(u - (int64_t)chunk * nm));
+    const int s = e.x, row = e.y;
+    uint8_t *sup = bfield<uint8_t>(bd, s, bd.o_sup);
+    int k0 = 0, k1 = 0;
+    if (pass != 0) {
+      const int fl = lane == 0 ? *(volatile const uint8_t *)(sup + row) : 0;
+      if (__shfl_sync(0xffffffffu, fl, 0)) continue;
+      k0 = kBScanFirst + chunk * kScanChunk;
+      k1 = k0 + kScanChunk;
+    }
+    uint32_t n_loads = 0;
+    const ulonglong2 *T2 = bfield<const ulonglong2>(bd, s, bd.o_T);
+    const int32_t *idx = tb.use_index ? bfield<const int32_t>(bd, s, __ldcg(&bctl(bd, s)->parity) ? bd.o_idx0 : bd.o_idx1)
+                                      : nullptr;
+    const int L = tb.use_index ? __ldcg(&bctl(bd, s)->L_out) : tb.W2;
+    if (pass == 0) k1 = min(L, kBScanFirst);
+    else k1 = min(k1, L);
+    if (k0 >= k1) continue;
+    const int hit = scan_pairs(idx, T2, tb.S + (int64_t)row * tb.Wp, k0, k1, pass ? sup + row : nullptr, lane,
+                               n_loads);
+    if (lane == 0) {
+      if (hit >= 0) {
+        sup[row] = 1;
+        bfield<int32_t>(bd, s, bd.o_res)[row] = hit;
+      } else if (pass == 0 && L > kBScanFirst) {   // (L: this state's index length)
+        bd.miss2[atomicAdd(bd.nmiss2, 1)] = e;
+      }
+      if (n_loads) atomicAdd(&bctl(bd, s)->scan_loads, (unsigned long long)n_loads);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ a6c-a8: finalize, one CTA per state
+__global__ void __launch_bounds__(kBSmallTPB) k_bfinalize(TableDev tb, const StateDev *__restrict__ states,
+                                                         uint64_t *__restrict__ out_dom, int64_t dom_stride,
+                                                         int32_t *__restrict__ out_status) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const StateDev &st = states[blockIdx.x];
+  if (out_dom) out_dom += (int64_t)blockIdx.x * dom_stride;
+  if (out_status) out_status += blockIdx.x;
+  dev_finalize<kBSmallTPB>(tb, st, out_dom, nullptr, out_status, smem);
+}
+
+__host__ __device__ inline size_t bupdate_smem_bytes(int R, int tw) { return (size_t)(R + 1) * tw * 16; }
+
+}  // namespace ctk

@@ -703,7 +703,9 @@ __device__ void dev_scan(const TableDev &tb, const StateDev &st, int gw, int nw)
 // ------------------------------------------------------------------ a6c-a8: finalize (one block)
 // Alg. 3 L3-4: a value of x in s_sup leaves the domain iff its support row has
 // no valid tuple (sup[r] = 0 after the cross-shard OR); then lastDom <- dom.
-template <int NT>
+// kDense: the state was updated densely (batch path, ct_batch.cuh): its index
+// becomes the identity over all W2 blocks instead of the compacted one.
+template <int NT, bool kDense = false>
 __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *__restrict__ out_dom,
                              uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status, uint64_t *smem) {
   Ctl *c = st.ctl;
@@ -766,7 +768,10 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
   __threadfence_system();
   __syncthreads();
   if (tid == 0) {
-    if (!noop && tb.use_index) {
+    if (!noop && kDense) {
+      c->L = tb.W2;
+      c->identity = 1;
+    } else if (!noop && tb.use_index) {
       c->parity ^= 1;
       c->L = __ldcg(&c->L_out);
       c->identity = 0;

@@ -18,6 +18,7 @@
 #include "ct_kernels.cuh"
 #include "ct_model.cuh"
 #include "ct_fast.cuh"
+#include "ct_batch.cuh"
 
 using namespace ctk;
 
@@ -75,7 +76,7 @@ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 // is what ct_state_copy moves; the rest is per-call scratch.
 struct StateLayout {
   size_t ctl, T, idx0, idx1, res, dom, persist;
-  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, desc, total;
+  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, bmask, desc, total;
 };
 
 }  // namespace
@@ -111,6 +112,8 @@ struct ct_table {
   size_t fused_smem = 0;
   int use_fast = 0, fast_grid = 1;   // k_fast (ct_fast.cuh): tables with R <= kLocalRowsMax
   size_t fast_smem = 0;
+  int bt_tw = 0, bt_grid = 0;        // tile-major batch update (ct_batch.cuh): tile width, 0 = per-state kernels
+  size_t bt_smem = 0;
   int live = 0;   // states + batches alive
 
   void *dalloc(size_t bytes) {
@@ -155,6 +158,10 @@ struct ct_batch {
   int32_t *h_status = nullptr;                  // pinned [S]
   uint64_t *d_in = nullptr, *d_dom = nullptr;   // device [S][Wd]
   int32_t *d_status = nullptr;
+  int32_t *d_bgo = nullptr;                     // device [S] (tile-major path)
+  int2 *d_miss = nullptr;                       // device [2][S·R] miss lists + 2 counters
+  size_t miss_bytes = 0;
+  BatchDev bd{};
 };
 
 // ------------------------------------------------------------------ layout / descriptors
@@ -184,6 +191,7 @@ static StateLayout make_layout(const ct_table *tb) {
   L.out = take((size_t)(1 + 2 * tb->Wd) * 8);
   L.slot = take((size_t)tb->Wd * 8);
   L.bar = take((size_t)kBarWords * 4);
+  L.bmask = take((size_t)(tb->dev.W2 + 31) / 32 * 4);   // batch path: survivor bit per 16-byte block
   L.desc = take(sizeof(StateDev));
   L.total = o;
   return L;
@@ -659,6 +667,41 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
       }
     }
   }
+  // batches: tile-major update with the support tile in shared memory when all
+  // R rows of a tile of >= 8 blocks fit (ct_batch.cuh)
+  {
+    int legacy = 0;
+    if (const char *ev = getenv("CT_BATCH_LEGACY")) legacy = atoi(ev);
+    const size_t cap = 200 * 1024;
+    int tw = 0;
+    if (!legacy && tb->R >= 1) {
+      if (bupdate_smem_bytes(tb->R, 32) <= cap) tw = 32;
+      else if (bupdate_smem_bytes(tb->R, 16) <= cap) tw = 16;
+      else if (bupdate_smem_bytes(tb->R, 8) <= cap) tw = 8;
+    }
+    if (tw) {
+      tb->bt_smem = bupdate_smem_bytes(tb->R, tw);
+      int occ = 0;
+      if (tw == 32) {
+        CUDA_TRY(cudaFuncSetAttribute(k_bupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->bt_smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bupdate<32>, kBTPB, tb->bt_smem));
+      } else if (tw == 16) {
+        CUDA_TRY(cudaFuncSetAttribute(k_bupdate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->bt_smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bupdate<16>, kBTPB, tb->bt_smem));
+      } else {
+        CUDA_TRY(cudaFuncSetAttribute(k_bupdate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->bt_smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bupdate<8>, kBTPB, tb->bt_smem));
+      }
+      const size_t ib = ingest_smem_bytes(n, tb->Wd), fb = finalize_smem_bytes(n, tb->Wd);
+      CUDA_TRY(cudaFuncSetAttribute(k_bingest, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(ib, 1)));
+      CUDA_TRY(cudaFuncSetAttribute(k_bfinalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)std::max<size_t>(fb, 1)));
+      if (occ >= 1) {
+        tb->bt_tw = tw;
+        tb->bt_grid = tb->sm_count * occ;
+      }
+    }
+  }
   // latency-bound tables: the whole call in one CTA (k_small)
   {
     int small_max = kSmallMaxPairs;
@@ -744,6 +787,7 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->state_bytes = (int64_t)t->lay.total;
   o->kernel_path = t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
   o->grid = t->use_small ? 1 : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
+  o->batch_tile = t->bt_tw;
   return CT_OK;
 }
 
@@ -912,6 +956,8 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
     if (b->d_in) tb->dfree(b->d_in, io);
     if (b->d_dom) tb->dfree(b->d_dom, io);
     if (b->d_status) tb->dfree(b->d_status, (size_t)n_states * 4);
+    if (b->d_bgo) tb->dfree(b->d_bgo, (size_t)n_states * 4);
+    if (b->d_miss) tb->dfree(b->d_miss, b->miss_bytes);
     if (b->h_in) cudaFreeHost(b->h_in);
     if (b->h_dom) cudaFreeHost(b->h_dom);
     if (b->h_status) cudaFreeHost(b->h_status);
@@ -923,7 +969,10 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_in = (uint64_t *)tb->dalloc(io);
   b->d_dom = (uint64_t *)tb->dalloc(io);
   b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
-  if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status)
+  b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
+  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 16;
+  b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
+  if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status || !b->d_bgo || !b->d_miss)
     return cleanup(fail(CT_ENOMEM, "device allocation of a %d-state batch (%zu bytes) failed", n_states, b->bytes));
   if (cudaHostAlloc((void **)&b->h_in, std::max<size_t>(io, 8), 0) != cudaSuccess ||
       cudaHostAlloc((void **)&b->h_dom, std::max<size_t>(io, 8), 0) != cudaSuccess ||
@@ -933,6 +982,28 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   }
   b->h.resize(n_states);
   for (int i = 0; i < n_states; ++i) b->h[i] = make_desc(tb, b->mem + (size_t)i * tb->lay.total);
+  {
+    const StateLayout &L = tb->lay;
+    BatchDev &bd = b->bd;
+    bd.pool = b->mem;
+    bd.pitch = (int64_t)L.total;
+    bd.o_ctl = (int64_t)L.ctl;
+    bd.o_T = (int64_t)L.T;
+    bd.o_ulist = (int64_t)L.ulist;
+    bd.o_items = (int64_t)L.items;
+    bd.o_res = (int64_t)L.res;
+    bd.o_sup = (int64_t)L.sup;
+    bd.o_scan = (int64_t)L.scanlist;
+    bd.o_idx0 = (int64_t)L.idx0;
+    bd.o_idx1 = (int64_t)L.idx1;
+    bd.o_bmask = (int64_t)L.bmask;
+    bd.bgo = b->d_bgo;
+    const size_t nm = (size_t)n_states * std::max(tb->R, 1);
+    bd.miss = b->d_miss;
+    bd.miss2 = b->d_miss + nm;
+    bd.nmiss = reinterpret_cast<int32_t *>(b->d_miss + 2 * nm);
+    bd.nmiss2 = bd.nmiss + 1;
+  }
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
   if (init->stream != tb->stream) cudaStreamSynchronize(init->stream);
@@ -979,10 +1050,58 @@ ct_status ct_batch_restore_dead(ct_batch *b, const ct_state *src) {
   return CT_OK;
 }
 
+// Tile-major batch call (ct_batch.cuh): ingest, update, probe, scan, finalize.
+static ct_status enqueue_batch_tiled(ct_batch *b, const uint64_t *removed, uint64_t *out_dom, int32_t *out_status) {
+  ct_table *tb = b->tb;
+  cudaStream_t st = tb->stream;
+  const int S = b->S;
+  int e = prof_event(tb, st);
+  k_bingest<<<S, kBSmallTPB, ingest_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, b->d_desc, removed, tb->Wd, b->d_bgo,
+                                                                     b->bd.nmiss, b->bd.nmiss2);
+  prof_mark(tb, 0, e, st);
+  const int tw = tb->bt_tw;
+  const int ntiles = (int)((tb->dev.W2 + tw - 1) / tw);
+  const int G = tb->bt_grid;
+  const int spw = 32 / tw;
+  // units = tiles x state chunks: >= 16 per CTA for balance, chunks of at least
+  // 4 states per warp slot so every warp of a CTA has work
+  int nchunk = std::max(1, (16 * G + ntiles - 1) / std::max(ntiles, 1));
+  const int min_chunk = 4 * (kBTPB / 32) * spw;
+  nchunk = std::max(1, std::min(nchunk, (S + min_chunk - 1) / min_chunk));
+  const int chunk_states = (S + nchunk - 1) / nchunk;
+  nchunk = (S + chunk_states - 1) / chunk_states;
+  e = prof_event(tb, st);
+  if (ntiles > 0) {
+    if (tw == 32)
+      k_bupdate<32><<<G, kBTPB, tb->bt_smem, st>>>(tb->dev, b->bd, S, ntiles, nchunk, chunk_states);
+    else if (tw == 16)
+      k_bupdate<16><<<G, kBTPB, tb->bt_smem, st>>>(tb->dev, b->bd, S, ntiles, nchunk, chunk_states);
+    else
+      k_bupdate<8><<<G, kBTPB, tb->bt_smem, st>>>(tb->dev, b->bd, S, ntiles, nchunk, chunk_states);
+  }
+  k_bcompact<<<S, kBSmallTPB, 0, st>>>(tb->dev, b->bd);
+  prof_mark(tb, 1, e, st);
+  e = prof_event(tb, st);
+  const int64_t pth = (int64_t)S * std::max(tb->R, 1);
+  k_bprobe<<<(unsigned)((pth + kBProbeTPB - 1) / kBProbeTPB), kBProbeTPB, 0, st>>>(tb->dev, b->bd, S);
+  prof_mark(tb, 2, e, st);
+  e = prof_event(tb, st);
+  k_bscan<<<tb->sm_count * 8, kBScanTPB, 0, st>>>(tb->dev, b->bd, 0);
+  k_bscan<<<tb->sm_count * 8, kBScanTPB, 0, st>>>(tb->dev, b->bd, 1);
+  prof_mark(tb, 3, e, st);
+  e = prof_event(tb, st);
+  k_bfinalize<<<S, kBSmallTPB, finalize_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, b->d_desc, out_dom, tb->Wd,
+                                                                         out_status);
+  prof_mark(tb, 5, e, st);
+  CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
 ct_status ct_propagate_many_async(ct_batch *b, const uint64_t *removed, uint64_t *out_dom, int32_t *out_status) {
   if (!b) return fail(CT_EINVAL, "NULL batch");
   ct_table *tb = b->tb;
   DeviceGuard g(tb->device);
+  if (tb->bt_tw) return enqueue_batch_tiled(b, removed, out_dom, out_status);
   CT_TRY(enqueue_local(tb, b->d_desc, b->S, removed, 0, tb->stream));
   return enqueue_finalize(tb, b->d_desc, b->S, out_dom, nullptr, out_status, 0, tb->stream);
 }
@@ -1022,6 +1141,8 @@ void ct_batch_destroy(ct_batch *b) {
   tb->dfree(b->d_in, io);
   tb->dfree(b->d_dom, io);
   tb->dfree(b->d_status, (size_t)b->S * 4);
+  tb->dfree(b->d_bgo, (size_t)b->S * 4);
+  tb->dfree(b->d_miss, b->miss_bytes);
   cudaFreeHost(b->h_in);
   cudaFreeHost(b->h_dom);
   cudaFreeHost(b->h_status);
@@ -1035,6 +1156,15 @@ ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
   DeviceGuard g(s->tb->device);
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->tb->W) CUDA_TRY(cudaMemcpy(out_bits, s->h.T, (size_t)s->tb->W * 8, cudaMemcpyDeviceToHost));
+  return CT_OK;
+}
+
+ct_status ct_batch_read_table(const ct_batch *b, int32_t i, uint64_t *out_bits) {
+  if (!b || !out_bits) return fail(CT_EINVAL, "NULL argument");
+  if (i < 0 || i >= b->S) return fail(CT_EINVAL, "batch index %d out of range", i);
+  DeviceGuard g(b->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
+  if (b->tb->W) CUDA_TRY(cudaMemcpy(out_bits, b->h[(size_t)i].T, (size_t)b->tb->W * 8, cudaMemcpyDeviceToHost));
   return CT_OK;
 }
 
@@ -1055,12 +1185,7 @@ ct_status ct_state_read_dom(const ct_state *s, uint64_t *out_dom) {
   return CT_OK;
 }
 
-ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
-  if (!s || !o) return fail(CT_EINVAL, "NULL argument");
-  DeviceGuard g(s->tb->device);
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  Ctl c;
-  CUDA_TRY(cudaMemcpy(&c, s->h.ctl, sizeof c, cudaMemcpyDeviceToHost));
+static void stats_from_ctl(const Ctl &c, ct_stats *o) {
   memset(o, 0, sizeof *o);
   o->calls = c.calls;
   o->last_status = c.last_status;
@@ -1075,6 +1200,26 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
   o->update_table_writes = (int64_t)c.upd_writes;
   o->filter_support_words = (int64_t)c.scan_loads;
   for (int i = 0; i < 7; ++i) o->phase_ns[i] = (c.tph[0] && c.tph[i + 1] >= c.tph[i]) ? (int64_t)(c.tph[i + 1] - c.tph[i]) : 0;
+}
+
+ct_status ct_state_stats(const ct_state *s, ct_stats *o) {
+  if (!s || !o) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(s->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  Ctl c;
+  CUDA_TRY(cudaMemcpy(&c, s->h.ctl, sizeof c, cudaMemcpyDeviceToHost));
+  stats_from_ctl(c, o);
+  return CT_OK;
+}
+
+ct_status ct_batch_stats(const ct_batch *b, ct_stats *o) {
+  if (!b || !o) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(b->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
+  std::vector<Ctl> c((size_t)b->S);
+  CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,
+                        cudaMemcpyDeviceToHost));
+  for (int i = 0; i < b->S; ++i) stats_from_ctl(c[(size_t)i], o + i);
   return CT_OK;
 }
 

@@ -56,7 +56,8 @@ class ct_table_info(ctypes.Structure):
                 ("n_tuples", ctypes.c_int64), ("words_total", ctypes.c_int64),
                 ("word_begin", ctypes.c_int64), ("words", ctypes.c_int64),
                 ("row_stride_words", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
-                ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32)]
+                ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32),
+                ("batch_tile", ctypes.c_int32)]
 
 KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small"}
 
@@ -116,6 +117,8 @@ SIGNATURES = {
     "ct_table_read_supports": (I32, [P, I32, P]),
     "ct_state_read_dom": (I32, [P, P]),
     "ct_state_stats": (I32, [P, P]),
+    "ct_batch_stats": (I32, [P, P]),
+    "ct_batch_read_table": (I32, [P, I32, P]),
     "ct_nccl_unique_id": (I32, [P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
@@ -366,6 +369,12 @@ def ct_state_read_table(state, n_words: int) -> np.ndarray:
     return out[:n_words]
 
 
+def ct_batch_read_table(batch, index: int, n_words: int) -> np.ndarray:
+    out = np.zeros(max(n_words, 1), dtype=np.uint64)
+    _check(lib().ct_batch_read_table(batch, int(index), _np_ptr(out)), allow_fail=False)
+    return out[:n_words]
+
+
 def ct_table_read_supports(table, row: int, n_words: int) -> np.ndarray:
     out = np.zeros(max(n_words, 1), dtype=np.uint64)
     _check(lib().ct_table_read_supports(table, row, _np_ptr(out)), allow_fail=False)
@@ -382,6 +391,13 @@ def ct_state_stats(state) -> ct_stats:
     s = ct_stats()
     _check(lib().ct_state_stats(state, ctypes.byref(s)), allow_fail=False)
     return s
+
+
+def ct_batch_stats(batch, n_states: int):
+    """Per-state counters of a batch's last ct_propagate_many (list of ct_stats)."""
+    arr = (ct_stats * max(int(n_states), 1))()
+    _check(lib().ct_batch_stats(batch, arr), allow_fail=False)
+    return list(arr)[:n_states]
 
 
 def ct_table_profile(table, enable: bool) -> None:

@@ -342,16 +342,49 @@ def test_confluence_two_calls_vs_one():
 
 
 # --------------------------------------------------------------------------- batched (a9)
-def test_batch_matches_oracle_and_single_state():
-    p = random_table(6, 50, 200_000, seed=5)
-    tab = make(p)
-    S = 96
+# (arity, domain, tuples, lo): tile widths 32 (R <= 400), 16 (R <= 800), 8
+# (R <= 1600) and the per-state kernels beyond; R < 32; blocks not a multiple
+# of the tile width; a single 16-byte block.
+BATCH_SHAPES = {
+    "c4like": (6, 50, 200_000, 0),
+    "tw16": (8, 90, 120_000 + 77, 3),
+    "tw8": (10, 140, 60_000 + 5, -2),
+    "perstate": (12, 150, 30_000 + 1, 0),
+    "tinyR": (3, 7, 5_000 + 13, 1),
+    "oneblock": (4, 6, 100, 0),
+}
+BATCH_PATHS = {"tiled": {}, "legacy": {"CT_BATCH_LEGACY": "1"}}
+
+
+def make_env(p, env, **kw):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return make(p, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def batch_walk(tab, p, S, steps, seed, check_table=False, from_states=None):
+    """S independent policy-P(2, 0.5) walks through ct_propagate_many, each state
+    checked against the oracle (status, domains; currTable if asked); FAILed
+    slots are restored by ct_batch_copy (odd steps) or ct_batch_restore_dead."""
     b = tab.batch(S)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     cur = [root_m.copy() for _ in range(S)]
-    rngs = [Rng(1000 + s, lanes=1) for s in range(S)]
+    if from_states is not None:                   # slots initialised from single states
+        for s, (st, m) in from_states.items():
+            b.copy(s, st)
+            cur[s] = m.copy()
+    rngs = [Rng(seed + s, lanes=1) for s in range(S)]
     from workloads.policies import walk_removal
-    for step in range(12):
+    nfail = 0
+    for step in range(steps):
         rem = np.zeros((S, tab.Wd), np.uint64)
         exp = []
         for s in range(S):
@@ -359,21 +392,102 @@ def test_batch_matches_oracle_and_single_state():
             if r is None:
                 r = np.zeros(p.R, np.uint8)
             rem[s] = member_to_bitmap(r, p.d)
-            exp.append(oracle_call(p, cur[s] & (1 - r)))
+            exp.append(oracle_call(p, cur[s] & (1 - r), want_valid=check_table))
         status, doms = b.propagate(rem)
         for s in range(S):
-            ok, dout, _ = exp[s]
+            ok, dout, valid = exp[s]
             assert status[s] == (CT_OK if ok else CT_FAIL), (step, s)
             if ok:
                 assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), (step, s)
+                if check_table:
+                    assert np.array_equal(bits_to_bool(b.read_table(s), p.t), valid), (step, s)
                 cur[s] = dout
-            elif step % 2:
-                b.copy(s, tab.root)                 # host-driven restore of one slot
-                cur[s] = root_m.copy()
             else:
-                cur[s] = root_m.copy()              # restored below by the device kernel
+                nfail += 1
+                if step % 2:
+                    b.copy(s, tab.root)             # host-driven restore of one slot
+                cur[s] = root_m.copy()              # (even steps: restored by the device kernel)
         b.restore_dead(tab.root)
     b.close()
+    return nfail
+
+
+@pytest.mark.parametrize("path", list(BATCH_PATHS))
+@pytest.mark.parametrize("shape", list(BATCH_SHAPES))
+def test_batch_matches_oracle(shape, path):
+    n, d, t, lo = BATCH_SHAPES[shape]
+    p = random_table(n, d, t, seed=5, lo=lo)
+    tab = make_env(p, BATCH_PATHS[path])
+    tw = {"c4like": 32, "tw16": 16, "tw8": 8, "perstate": 0, "tinyR": 32, "oneblock": 32}[shape]
+    assert tab.info.batch_tile == (tw if path == "tiled" else 0)
+    batch_walk(tab, p, S=67, steps=10, seed=1000, check_table=(shape in ("c4like", "tinyR", "oneblock")))
+    tab.close()
+
+
+@pytest.mark.parametrize("knob", ["dom", "delta", "nores", "noindex"])
+def test_batch_knobs(knob):
+    kw = {"dom": dict(update_policy=CT_POLICY_DOM), "delta": dict(update_policy=CT_POLICY_DELTA),
+          "nores": dict(use_residues=False), "noindex": dict(use_index=False)}[knob]
+    p = random_table(6, 30, 40_000, seed=9)
+    tab = make(p, **kw)
+    batch_walk(tab, p, S=40, steps=8, seed=2000, check_table=True)
+    tab.close()
+
+
+def test_batch_banded_filter_scans():
+    """Correlated (banded) table: fixing x0 leaves most values of the other
+    variables unsupported, so the batch filter runs full scans."""
+    p = banded_table(5, 40, 50_000, seed=4)
+    tab = make(p)
+    S = 40
+    b = tab.batch(S)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rem = np.zeros((S, tab.Wd), np.uint64)
+    exp = []
+    for s in range(S):
+        r = fix_one_value_removal(Rng(300 + s, lanes=1), root_m, p.d, var=s % p.n)
+        rem[s] = member_to_bitmap(r, p.d)
+        exp.append(oracle_call(p, root_m & (1 - r), want_valid=True))
+    status, doms = b.propagate(rem)
+    for s in range(S):
+        ok, dout, valid = exp[s]
+        assert status[s] == (CT_OK if ok else CT_FAIL)
+        if ok:
+            assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), s
+            assert np.array_equal(bits_to_bool(b.read_table(s), p.t), valid), s
+    st = b.stats()
+    assert sum(x.n_residue_miss for x in st) > 0
+    b.close()
+    tab.close()
+
+
+def test_batch_slots_from_compacted_states():
+    """Slots copied from single states that carry a compacted index (k_fast /
+    k_small history) continue correctly in the dense batch path, and a batch
+    state equals the same state propagated alone."""
+    p = random_table(6, 50, 200_000, seed=5)
+    tab = make(p)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rng = Rng(55, lanes=1)
+    from workloads.policies import walk_removal
+    singles = {}
+    for s in (0, 3, 7):
+        st = tab.root.clone()
+        cur = root_m.copy()
+        for _ in range(2):
+            r = walk_removal(rng, cur, p.d, q=0.3)
+            ok, dout, _ = oracle_call(p, cur & (1 - r))
+            status, dom, _ = st.propagate(member_to_bitmap(r, p.d))
+            assert status == (CT_OK if ok else CT_FAIL)
+            if not ok:
+                st.copy_from(tab.root)
+                cur = root_m.copy()
+            else:
+                cur = dout
+        singles[s] = (st, cur)
+    batch_walk(tab, p, S=9, steps=6, seed=3000, check_table=True, from_states=singles)
+    for st, _ in singles.values():
+        st.close()
     tab.close()
 
 
