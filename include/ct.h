@@ -306,8 +306,15 @@ typedef struct ct_stats {
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
 /* The same counters for every state of a batch (last ct_propagate_many call):
  * out = host ct_stats[ct_batch_size(b)], caller-owned.  Waits for the table's
- * stream.  phase_ns is 0 (the batch kernels do not stamp phases). */
+ * stream.  phase_ns is 0 (the batch kernels do not stamp phases); with the
+ * tile-major update (ct_table_info.batch_tile > 0) update_support_words and
+ * update_table_writes are per batch only, see ct_batch_work. */
 ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
+/* Whole-batch work of the last ct_propagate_many (tile-major path): out4 =
+ * host int64[4] = {64-bit support words the update OR-ed, 16-byte currTable
+ * blocks it rewrote, support words the filter scans loaded, residue-probe
+ * misses}; all -1 on the per-state path.  Waits for the table's stream. */
+ct_status ct_batch_work(const ct_batch *b, int64_t *out4);
 
 /* Per-kernel device timing (measurement only).  While enabled, every
  * *_async / ct_propagate_many call on this table's states and batches records a

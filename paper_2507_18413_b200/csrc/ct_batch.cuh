@@ -44,9 +44,13 @@ struct BatchDev {
   char *pool;
   int64_t pitch;
   int64_t o_ctl, o_T, o_ulist, o_items, o_res, o_sup, o_scan, o_idx0, o_idx1, o_bmask;
-  int32_t *bgo;              // [S] per call: update-list length, or -1 if the state does not update
+  int64_t o_plist;           // padded update list (kTW = 32 path), see k_bingest
+  int32_t plist_po;          // its first padded entry (uint32 index)
+  int32_t *bgo;              // [S] per call: (groups << 20) | update-list length, or -1 if the state does not update
   int2 *miss, *miss2;        // [S·R] global lists of (state, row) probe misses (pass 0 / pass 1 of k_bscan)
   int32_t *nmiss, *nmiss2;   // their lengths (zeroed by k_bingest)
+  unsigned long long *work;  // [2] this call, whole batch: update support words, currTable blocks
+                             // rewritten (zeroed by k_bingest)
 };
 
 __device__ __forceinline__ Ctl *bctl(const BatchDev &b, int s) {
@@ -58,23 +62,70 @@ __device__ __forceinline__ T *bfield(const BatchDev &b, int s, int64_t off) {
 }
 
 // ------------------------------------------------------------------ a2: ingest, one CTA per state
+// dev_ingest (Alg. 1 L1-3, Alg. 2), then, for the kTW = 32 update, the
+// update list re-laid out for it: each variable group padded to a multiple of
+// 4 entries with the all-zero row R, entries stored as shared-memory byte
+// offsets (row · 512), and a group table
+//   plist[0] = G, plist[4 + g] = padded start | real size << 16 | Δ-branch << 31,
+//   plist[4 + G] = padded total,  plist[po + k] = padded entry k.
+// The per-state work of the layout is paid once per call, not once per tile.
 __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const StateDev *__restrict__ states,
                                                        const uint64_t *__restrict__ removed,
-                                                       int64_t removed_stride, int32_t *__restrict__ bgo,
-                                                       int32_t *__restrict__ bd_nmiss, int32_t *__restrict__ bd_nmiss2) {
+                                                       int64_t removed_stride, BatchDev bd, int build_plist) {
   extern __shared__ __align__(16) uint64_t smem[];
   const StateDev &st = states[blockIdx.x];
   const uint64_t *rem = removed ? removed + (int64_t)blockIdx.x * removed_stride : nullptr;
   dev_ingest<kBSmallTPB>(tb, st, rem, 0, smem);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    *bd_nmiss = 0;
-    *bd_nmiss2 = 0;
+  if (blockIdx.x == 0 && threadIdx.x < 2) {
+    if (threadIdx.x == 0) {
+      *bd.nmiss = 0;
+      *bd.nmiss2 = 0;
+    }
+    bd.work[threadIdx.x] = 0;
   }
+  __shared__ int s_go, s_nrows;
   if (threadIdx.x == 0) {   // the thread that wrote the control fields
     Ctl *c = st.ctl;
-    const bool go = !(c->skip | c->noop | c->fail_fast);
-    bgo[blockIdx.x] = go ? c->nrows : -1;
+    s_go = !(c->skip | c->noop | c->fail_fast);
+    s_nrows = c->nrows;
   }
+  __syncthreads();
+  const int n = tb.n, Wd = tb.Wd;
+  int G = 0;
+  if (s_go && build_plist) {
+    // dev_ingest's shared arrays: |Δ_x|, |D_x| and the group starts of the update list
+    const int32_t *s_cd = reinterpret_cast<const int32_t *>(smem + 2 * Wd);
+    const int32_t *s_cs = s_cd + n;
+    const int32_t *s_ust = s_cs + n;
+    __shared__ uint64_t s_warp[kBSmallTPB / 32];
+    uint32_t *pl = bfield<uint32_t>(bd, blockIdx.x, bd.o_plist);
+    const uint32_t zrow = (uint32_t)tb.R * 512u;
+    uint64_t carry = 0;
+    for (int base = 0; base < n; base += kBSmallTPB) {
+      const int x = base + threadIdx.x;
+      int sz = 0;
+      if (x < n) sz = s_ust[x + 1] - s_ust[x];
+      const uint64_t v = sz ? ((uint64_t)((sz + 3) & ~3) << 32) | 1ull : 0ull;
+      uint64_t total;
+      const uint64_t ex = block_excl_scan<kBSmallTPB>(v, s_warp, total) + carry;
+      if (sz) {
+        const int g = (int)(ex & 0xffffffffu);
+        const int pst = (int)(ex >> 32);
+        const bool useDelta = tb.policy == 2 || (tb.policy == 0 && s_cd[x] < s_cs[x]);
+        pl[4 + g] = (uint32_t)pst | ((uint32_t)sz << 16) | (useDelta ? 0x80000000u : 0u);
+        const uint32_t *ul = reinterpret_cast<const uint32_t *>(st.ulist);
+        const int psz = (sz + 3) & ~3;
+        for (int j = 0; j < psz; ++j) pl[bd.plist_po + pst + j] = j < sz ? (ul[s_ust[x] + j] & kRowMask) * 512u : zrow;
+      }
+      carry += total;
+    }
+    G = (int)(carry & 0xffffffffu);
+    if (threadIdx.x == 0) {
+      pl[0] = (uint32_t)G;
+      pl[4 + G] = (uint32_t)(carry >> 32);
+    }
+  }
+  if (threadIdx.x == 0) bd.bgo[blockIdx.x] = s_go ? (G << 20) | s_nrows : -1;
 }
 
 // ------------------------------------------------------------------ a3-a5: tile-major update
@@ -143,6 +194,50 @@ __device__ __forceinline__ ulonglong2 tile32_state(uint32_t s_lane, uint32_t zro
   return make_ulonglong2(tw.x & mx, tw.y & my);
 }
 
+// The same from the padded list (k_bingest): `gt` = lane g holds group g's
+// table entry (lane G: the padded total), `pe` = lane k holds padded entry k
+// of the chunk starting at entry 0; later chunks are loaded from `pl`.  Every
+// group is a multiple of 4 entries, so a step of 4 rows never needs a bound.
+__device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, const uint32_t *pl, int G, uint32_t gt,
+                                                    uint32_t pe, ulonglong2 tw, bool live, uint32_t &nl) {
+  const int lane = threadIdx.x & 31;
+  uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+  if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+  int chunk = 0;
+  uint32_t ge = __shfl_sync(0xffffffffu, gt, 0);
+  for (int g = 0; g < G; ++g) {
+    const uint32_t gn = __shfl_sync(0xffffffffu, gt, g + 1);
+    const int en = (int)(gn & 0xffffu);
+    for (int k = (int)(ge & 0xffffu); k < en;) {
+      if ((k >> 5) != chunk) {                                 // warp-uniform, once per 32 entries
+        chunk = k >> 5;
+        pe = __ldcg(pl + chunk * 32 + lane);
+      }
+      const int kend = min(en, (chunk + 1) * 32);
+      for (; k < kend; k += 4) {
+        const int kk = k & 31;
+        const uint32_t r0 = __shfl_sync(0xffffffffu, pe, kk), r1 = __shfl_sync(0xffffffffu, pe, kk + 1);
+        const uint32_t r2 = __shfl_sync(0xffffffffu, pe, kk + 2), r3 = __shfl_sync(0xffffffffu, pe, kk + 3);
+        const ulonglong2 v0 = lds128(s_lane + r0), v1 = lds128(s_lane + r1);
+        const ulonglong2 v2 = lds128(s_lane + r2), v3 = lds128(s_lane + r3);
+        ax |= v0.x | v1.x;
+        ay |= v0.y | v1.y;
+        ax |= v2.x | v3.x;
+        ay |= v2.y | v3.y;
+      }
+    }
+    nl += ((ge >> 16) & 0x7fffu) * (uint32_t)__popc(__ballot_sync(0xffffffffu, live));   // warp total
+    const uint64_t inv = (ge & 0x80000000u) ? ~0ull : 0ull;   // Δ-branch: AND the complement
+    mx &= ax ^ inv;
+    my &= ay ^ inv;
+    ax = ay = 0;
+    live = live && ((tw.x & mx) | (tw.y & my)) != 0;          // Alg. 2, per block
+    if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+    ge = gn;
+  }
+  return make_ulonglong2(tw.x & mx, tw.y & my);
+}
+
 // Persistent: CTA c processes the contiguous unit range [U·c/G, U·(c+1)/G) of
 // the U = ntiles·nchunk units (tile-major: unit u = (tile u / nchunk, state
 // chunk u % nchunk)), so it reloads its shared support tile at most a few
@@ -161,6 +256,7 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
   const int64_t units = (int64_t)ntiles * nchunk;
   const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
   int cur_tile = -1;
+  uint32_t w_loads = 0, w_writes = 0;   // this lane's share of the batch work counters
   for (int64_t u = u0; u < u1; ++u) {
     const int tile = (int)(u / nchunk), chunk = (int)(u - (int64_t)tile * nchunk);
     if (tile != cur_tile) {
@@ -183,31 +279,47 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
     const int step = nwarps * SPW;
     int go_n = -1;
     ulonglong2 tw_n = make_ulonglong2(0ull, 0ull);
-    uint32_t ev_n = 0;
+    uint32_t ev_n = 0, gt_n = 0;
     auto fetch = [&](int ss) {
       go_n = -1;
       tw_n = make_ulonglong2(0ull, 0ull);
-      ev_n = 0;
+      ev_n = gt_n = 0;
       if (ss < s1) {
+        const char *sb = bd.pool + (int64_t)ss * bd.pitch;
         go_n = __ldcg(bd.bgo + ss);
-        if (inblk) tw_n = __ldcg(bfield<ulonglong2>(bd, ss, bd.o_T) + blk);
-        if (bl < R) ev_n = __ldcg(bfield<uint32_t>(bd, ss, bd.o_ulist) + bl);
+        if (inblk) tw_n = __ldcg(reinterpret_cast<const ulonglong2 *>(sb + bd.o_T) + blk);
+        if constexpr (kTW == 32) {
+          const uint32_t *pl = reinterpret_cast<const uint32_t *>(sb + bd.o_plist);
+          gt_n = __ldcg(pl + 4 + lane);
+          ev_n = __ldcg(pl + bd.plist_po + lane);
+        } else {
+          if (bl < R) ev_n = __ldcg(reinterpret_cast<const uint32_t *>(sb + bd.o_ulist) + bl);
+        }
       }
     };
     fetch(s);
     for (int base = s0 + warp * SPW; base < s1; base += step, s += step) {
-      const int nr = go_n;
+      const int go = go_n;
+      const int nr = go < 0 ? -1 : (go & 0xfffff);
       const ulonglong2 tw = tw_n;
       uint32_t ev = ev_n;
+      const uint32_t gt = gt_n;
       fetch(s + step);
       const bool upd = nr >= 0 && inblk;         // this lane's block takes part in the update
       const bool had = upd && (tw.x | tw.y) != 0;
       uint32_t nl = 0;
-      const uint32_t *ul = bfield<uint32_t>(bd, min(s, S - 1), bd.o_ulist);
+      char *sb = bd.pool + (int64_t)min(s, S - 1) * bd.pitch;
+      const uint32_t *ul = reinterpret_cast<const uint32_t *>(sb + bd.o_ulist);
       ulonglong2 nt;
       if constexpr (kTW == 32) {
         if (nr < 0) continue;                    // warp-uniform: one state per warp
-        nt = tile32_state(s_lane, (uint32_t)R * 512u, ul, nr, ev, tw, had, nl);
+        const int G = go >> 20;
+        if (G < 32) {
+          nt = tile32_padded(s_lane, reinterpret_cast<const uint32_t *>(sb + bd.o_plist) + bd.plist_po, G, gt, ev,
+                             tw, had, nl);
+        } else {                                 // > 31 changed variables: the plain list
+          nt = tile32_state(s_lane, (uint32_t)R * 512u, ul, nr, __ldcg(ul + lane), tw, had, nl);
+        }
       } else {
         bool live = had;
         uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
@@ -243,57 +355,69 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
         nt = make_ulonglong2(tw.x & mx, tw.y & my);
       }
       const bool wr = had && (nt.x != tw.x || nt.y != tw.y);
-      if (wr) bfield<ulonglong2>(bd, s, bd.o_T)[blk] = nt;
+      if (wr) reinterpret_cast<ulonglong2 *>(sb + bd.o_T)[blk] = nt;
       const bool keep = had && (nt.x | nt.y) != 0;
-      const unsigned bk = __ballot_sync(0xffffffffu, keep), bw = __ballot_sync(0xffffffffu, wr);
-      if constexpr (kTW < 32) {
-#pragma unroll
-        for (int o = 1; o < kTW; o <<= 1) nl += __shfl_xor_sync(0xffffffffu, nl, o);
+      const unsigned bk = __ballot_sync(0xffffffffu, keep);
+      w_writes += wr ? 1u : 0u;
+      if constexpr (kTW == 32) {
+        if (lane == 0) w_loads += nl;     // nl is the warp total here
+      } else {
+        w_loads += nl;                    // per lane
       }
       if (bl == 0 && nr >= 0) {
         // survivor bits of this tile -> bits [tile·kTW, tile·kTW + kTW) of the bitmap
-        uint8_t *bm = bfield<uint8_t>(bd, s, bd.o_bmask);
+        uint8_t *bm = reinterpret_cast<uint8_t *>(sb + bd.o_bmask);
         const unsigned bits = kTW == 32 ? bk : (bk >> (sub * kTW)) & ((1u << kTW) - 1u);
         if (kTW == 32) reinterpret_cast<uint32_t *>(bm)[tile] = bits;
         else if (kTW == 16) reinterpret_cast<uint16_t *>(bm)[tile] = (uint16_t)bits;
         else bm[tile] = (uint8_t)bits;
-        Ctl *c = bctl(bd, s);
-        const unsigned smask = kTW == 32 ? 0xffffffffu : (((1u << kTW) - 1u) << (sub * kTW));
-        const int cw = __popc(bw & smask);
-        if (nl) atomicAdd(&c->upd_loads, 2ull * nl);
-        if (cw) atomicAdd(&c->upd_writes, (unsigned long long)cw);
       }
     }
+  }
+  // batch work counters: one reduction per warp for the whole launch
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    w_loads += __shfl_xor_sync(0xffffffffu, w_loads, o);
+    w_writes += __shfl_xor_sync(0xffffffffu, w_writes, o);
+  }
+  if (lane == 0) {
+    if (w_loads) atomicAdd(bd.work + 0, 2ull * w_loads);
+    if (w_writes) atomicAdd(bd.work + 1, (unsigned long long)w_writes);
   }
 }
 
 // ------------------------------------------------------------------ a4: index compaction, one CTA per state
 // The order-preserving index of the non-zero blocks (RSparseBitSet, SURVEY
-// §8(a) a4) from the survivor bitmap k_bupdate wrote: a block scan of the
-// words' popcounts, then every thread expands its word's set bits.  Writes
-// L_out; the index goes to the buffer the single-state path would write (so a
-// batch state continues exactly like a single state).
+// §8(a) a4) from the survivor bitmap k_bupdate wrote, 128 bitmap words (4096
+// blocks) per round: a block scan of the words' popcounts, then every warp
+// expands 32 words, one word per step with the lanes as its bits, so the index
+// stores are coalesced.  Writes L_out; the index goes to the buffer the
+// single-state path would write (a batch state continues like a single state).
 __global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev bd) {
   const int s = blockIdx.x;
   if (__ldcg(bd.bgo + s) < 0) return;
   __shared__ uint64_t s_warp[kBSmallTPB / 32];
+  __shared__ uint32_t s_word[kBSmallTPB], s_pre[kBSmallTPB];
   Ctl *c = bctl(bd, s);
   const uint32_t *bm = bfield<const uint32_t>(bd, s, bd.o_bmask);
   int32_t *idx_out = bfield<int32_t>(bd, s, __ldcg(&c->parity) ? bd.o_idx0 : bd.o_idx1);
   const int nw = (tb.W2 + 31) >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint64_t carry = 0;
   for (int base = 0; base < nw; base += kBSmallTPB) {
     const int k = base + threadIdx.x;
-    uint32_t w = k < nw ? __ldcg(bm + k) : 0u;
+    const uint32_t w = k < nw ? __ldcg(bm + k) : 0u;
     uint64_t total;
     const uint64_t ex = block_excl_scan<kBSmallTPB>((uint64_t)__popc(w), s_warp, total);
     if (tb.use_index) {
-      int pos = (int)(carry + ex);
-      while (w) {
-        const int b = __ffs(w) - 1;
-        w &= w - 1u;
-        idx_out[pos++] = k * 32 + b;
+      s_word[threadIdx.x] = w;
+      s_pre[threadIdx.x] = (uint32_t)(carry + ex);
+      __syncthreads();
+      for (int j = warp * 32; j < warp * 32 + 32; ++j) {
+        const uint32_t wj = s_word[j];
+        if ((wj >> lane) & 1u) idx_out[s_pre[j] + __popc(wj & lanemask_lt())] = (base + j) * 32 + lane;
       }
+      __syncthreads();
     }
     carry += total;
   }

@@ -72,11 +72,13 @@ struct DeviceGuard {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+inline int plist_po(int n) { return 4 + (int)round_up(n + 1, 4); }
+
 // Byte layout of one state's device block.  The persistent prefix [0, persist)
 // is what ct_state_copy moves; the rest is per-call scratch.
 struct StateLayout {
   size_t ctl, T, idx0, idx1, res, dom, persist;
-  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, bmask, desc, total;
+  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, bmask, plist, desc, total;
 };
 
 }  // namespace
@@ -192,6 +194,7 @@ static StateLayout make_layout(const ct_table *tb) {
   L.slot = take((size_t)tb->Wd * 8);
   L.bar = take((size_t)kBarWords * 4);
   L.bmask = take((size_t)(tb->dev.W2 + 31) / 32 * 4);   // batch path: survivor bit per 16-byte block
+  L.plist = take((size_t)(plist_po(tb->n) + tb->R + 3 * tb->n + 36) * 4);   // batch path: padded update list
   L.desc = take(sizeof(StateDev));
   L.total = o;
   return L;
@@ -970,7 +973,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_dom = (uint64_t *)tb->dalloc(io);
   b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
-  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 16;
+  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64;
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
   if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status || !b->d_bgo || !b->d_miss)
     return cleanup(fail(CT_ENOMEM, "device allocation of a %d-state batch (%zu bytes) failed", n_states, b->bytes));
@@ -997,12 +1000,15 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
     bd.o_idx0 = (int64_t)L.idx0;
     bd.o_idx1 = (int64_t)L.idx1;
     bd.o_bmask = (int64_t)L.bmask;
+    bd.o_plist = (int64_t)L.plist;
+    bd.plist_po = plist_po(tb->n);
     bd.bgo = b->d_bgo;
     const size_t nm = (size_t)n_states * std::max(tb->R, 1);
     bd.miss = b->d_miss;
     bd.miss2 = b->d_miss + nm;
     bd.nmiss = reinterpret_cast<int32_t *>(b->d_miss + 2 * nm);
     bd.nmiss2 = bd.nmiss + 1;
+    bd.work = reinterpret_cast<unsigned long long *>(b->d_miss + 2 * nm + 2);   // 16-byte aligned
   }
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
@@ -1056,8 +1062,8 @@ static ct_status enqueue_batch_tiled(ct_batch *b, const uint64_t *removed, uint6
   cudaStream_t st = tb->stream;
   const int S = b->S;
   int e = prof_event(tb, st);
-  k_bingest<<<S, kBSmallTPB, ingest_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, b->d_desc, removed, tb->Wd, b->d_bgo,
-                                                                     b->bd.nmiss, b->bd.nmiss2);
+  k_bingest<<<S, kBSmallTPB, ingest_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, b->d_desc, removed, tb->Wd, b->bd,
+                                                                     tb->bt_tw == 32 ? 1 : 0);
   prof_mark(tb, 0, e, st);
   const int tw = tb->bt_tw;
   const int ntiles = (int)((tb->dev.W2 + tw - 1) / tw);
@@ -1156,6 +1162,30 @@ ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
   DeviceGuard g(s->tb->device);
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->tb->W) CUDA_TRY(cudaMemcpy(out_bits, s->h.T, (size_t)s->tb->W * 8, cudaMemcpyDeviceToHost));
+  return CT_OK;
+}
+
+ct_status ct_batch_work(const ct_batch *b, int64_t *out4) {
+  if (!b || !out4) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(b->tb->device);
+  CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
+  if (!b->tb->bt_tw) {
+    for (int i = 0; i < 4; ++i) out4[i] = -1;
+    return CT_OK;
+  }
+  CUDA_TRY(cudaMemcpy(out4, b->bd.work, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  // filter side: summed over the states' own counters
+  std::vector<Ctl> c((size_t)b->S);
+  CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,
+                        cudaMemcpyDeviceToHost));
+  out4[2] = out4[3] = 0;
+  std::vector<int32_t> bgo((size_t)b->S);
+  CUDA_TRY(cudaMemcpy(bgo.data(), b->d_bgo, (size_t)b->S * 4, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < b->S; ++i) {
+    if (bgo[(size_t)i] < 0) continue;   // the state did not run the filter this call
+    out4[2] += (int64_t)c[(size_t)i].scan_loads;
+    out4[3] += c[(size_t)i].nscan;
+  }
   return CT_OK;
 }
 

@@ -119,6 +119,7 @@ SIGNATURES = {
     "ct_state_stats": (I32, [P, P]),
     "ct_batch_stats": (I32, [P, P]),
     "ct_batch_read_table": (I32, [P, I32, P]),
+    "ct_batch_work": (I32, [P, P]),
     "ct_nccl_unique_id": (I32, [P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
@@ -367,6 +368,14 @@ def ct_state_read_table(state, n_words: int) -> np.ndarray:
     out = np.zeros(max(n_words, 1), dtype=np.uint64)
     _check(lib().ct_state_read_table(state, _np_ptr(out)), allow_fail=False)
     return out[:n_words]
+
+
+def ct_batch_work(batch) -> dict:
+    """Whole-batch work counters of the last ct_propagate_many (include/ct.h)."""
+    out = np.zeros(4, dtype=np.int64)
+    _check(lib().ct_batch_work(batch, _np_ptr(out)), allow_fail=False)
+    return dict(update_support_words=int(out[0]), update_table_writes=int(out[1]),
+                filter_support_words=int(out[2]), probe_misses=int(out[3]))
 
 
 def ct_batch_read_table(batch, index: int, n_words: int) -> np.ndarray:
