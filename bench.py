@@ -237,8 +237,6 @@ def run_ours(args):
     barrier(world)
     torch.cuda.synchronize()
     clocks.start()
-    C.ct_table_profile(tab.handle, True)
-    C.ct_table_profile_read(tab.handle, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for k in range(args.steps):
@@ -247,12 +245,18 @@ def run_ours(args):
     ev1.synchronize()
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
-    prof = C.ct_table_profile_read(tab.handle, reset=True)
-    C.ct_table_profile(tab.handle, False)
     clk = clocks.stop()
     barrier(world)
     ms_max = max_over_ranks(ms, world)
     value = args.steps / (ms_max / 1e3)
+    # per-kernel device times (roofline): the same steps again with CUDA events
+    # around every kernel launch, outside the timed region above
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    for k in range(args.steps):
+        step(k)
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    C.ct_table_profile(tab.handle, False)
 
     # roofline of the dominant kernel.  Fused path: k_fused runs every phase of a
     # call (ingest, update + compaction, probe, scan, finalize) in one launch, so
@@ -472,27 +476,33 @@ def run_c4(args):
     for k in range(args.warmup):
         step(k)
     tab.root.synchronize()
+    b.work(reset=True)
     clocks = Clocks(dev)
     barrier(world)
     torch.cuda.synchronize()
     clocks.start()
-    C.ct_table_profile(tab.handle, True)
-    C.ct_table_profile_read(tab.handle, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fails = 0
     ev0.record(stream)
     for k in range(args.steps):
         step(k)
     ev1.record(stream)
     ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
-    prof = C.ct_table_profile_read(tab.handle, reset=True)
-    C.ct_table_profile(tab.handle, False)
     clk = clocks.stop()
+    work = b.work(reset=True)                     # summed over the timed steps (device counters)
     barrier(world)
     ms_max = max_over_ranks(ms, world)
     total_states = args.states
     value = total_states * args.steps / (ms_max / 1e3)
+    # per-kernel device times: a second pass of the same number of steps with
+    # CUDA events around every kernel (kept out of the timed region above)
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    for k in range(args.steps):
+        step(k)
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    C.ct_table_profile(tab.handle, False)
+    b.work(reset=True)
     # e2e through the synchronous host-buffer call
     e2e_steps = max(5, min(args.steps, 20))
     host = [x.copy() for x in pats]
@@ -508,6 +518,30 @@ def run_c4(args):
     kernel_ms = {k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()}
     upd_n, upd_ms = prof["update"]
     launches = sum(v[0] for v in prof.values())
+    if tab.info.batch_tile:
+        launches += upd_n + prof["scan"][0]    # k_bcompact shares the update slot, k_bscan runs 2 passes per slot
+    roofline = None
+    if tab.info.batch_tile and upd_n:
+        # dominant kernel: the tile-major update (k_bupdate + k_bcompact, one event pair).
+        # HBM bytes it must move: every currTable block of every updating state read,
+        # rewritten blocks written, the support tiles staged into shared memory, the
+        # survivor bitmap written and read back by the compaction (index writes not counted).
+        steps = args.steps
+        hbm = (16 * (work["table_blocks_read"] + work["table_blocks_written"]) + work["support_bytes_staged"]
+               + 2 * work["table_blocks_read"] // 8) / steps
+        smem = 8 * work["update_support_words"] / steps
+        t = upd_ms / upd_n / 1e3
+        peak, peak_src = peaks()
+        smem_peak = 148 * 128 * 1.965          # GB/s: SMs x 128 B/cycle (B300_MICROARCH.md LDS table) x max SM clock
+        roofline = {"bound": "hbm", "achieved": hbm / t / 1e9, "peak": peak, "unit": "GB/s",
+                    "frac": hbm / t / 1e9 / peak, "traffic": None,
+                    "kernel": f"ctk::k_bupdate<{tab.info.batch_tile}> + ctk::k_bcompact",
+                    "bytes_per_launch": hbm, "ms_per_launch": t * 1e3, "peak_source": peak_src,
+                    "smem": {"achieved": smem / t / 1e9, "peak": smem_peak, "frac": smem / t / 1e9 / smem_peak,
+                             "bytes_per_launch": smem,
+                             "note": "support words OR-ed by Alg. 2, served from the shared-memory tile "
+                                     "(SURVEY B_upd support term); the kernel is bound by shared-memory "
+                                     "loads + issue, not by HBM"}}
     tab.close()
     if rank == 0:
         line = {
@@ -522,6 +556,7 @@ def run_c4(args):
                        "parallelism": f"states split over {world} GPUs, no communication",
                        "l2": "per-state currTables 512 MB > L2; supports 37.5 MB L2-resident by design"},
             "kernel_ms_per_launch": kernel_ms, "update_ms_per_launch": upd_ms / max(upd_n, 1),
+            "roofline": roofline, "work_per_step": {k: v / args.steps for k, v in work.items() if k.startswith(("update", "table", "support"))},
             "e2e": {"value": total_states * e2e_steps / e2e_s, "unit": "state-propagations/s",
                     "h2d_bytes_per_step": 8 * tab.Wd * total_states,
                     "d2h_bytes_per_step": (8 * tab.Wd + 4) * total_states, "steps": e2e_steps,

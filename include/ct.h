@@ -310,11 +310,14 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *out);
  * tile-major update (ct_table_info.batch_tile > 0) update_support_words and
  * update_table_writes are per batch only, see ct_batch_work. */
 ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
-/* Whole-batch work of the last ct_propagate_many (tile-major path): out4 =
- * host int64[4] = {64-bit support words the update OR-ed, 16-byte currTable
- * blocks it rewrote, support words the filter scans loaded, residue-probe
- * misses}; all -1 on the per-state path.  Waits for the table's stream. */
-ct_status ct_batch_work(const ct_batch *b, int64_t *out4);
+/* Work counters of the tile-major batch path (measurement only).  out6 = host
+ * int64[6]: [0] 64-bit support words the update OR-ed (from shared memory),
+ * [1] 16-byte currTable blocks it read, [2] blocks it rewrote, [3] support
+ * bytes staged from global into shared memory -- [0..3] summed over all calls
+ * since the last reset (reset != 0 zeroes them after the read); [4] support
+ * words the filter scans loaded and [5] residue-probe misses, both of the last
+ * call.  All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
+ct_status ct_batch_work(ct_batch *b, int64_t *out6, int32_t reset);
 
 /* Per-kernel device timing (measurement only).  While enabled, every
  * *_async / ct_propagate_many call on this table's states and batches records a

@@ -133,8 +133,8 @@ class Batch:
     def stats(self):
         return C.ct_batch_stats(self.handle, self.S)
 
-    def work(self) -> dict:
-        return C.ct_batch_work(self.handle)
+    def work(self, reset: bool = False) -> dict:
+        return C.ct_batch_work(self.handle, reset)
 
     def read_table(self, index: int) -> np.ndarray:
         return C.ct_batch_read_table(self.handle, index, int(self.table.info.words))

@@ -49,8 +49,9 @@ struct BatchDev {
   int32_t *bgo;              // [S] per call: (groups << 20) | update-list length, or -1 if the state does not update
   int2 *miss, *miss2;        // [S·R] global lists of (state, row) probe misses (pass 0 / pass 1 of k_bscan)
   int32_t *nmiss, *nmiss2;   // their lengths (zeroed by k_bingest)
-  unsigned long long *work;  // [2] this call, whole batch: update support words, currTable blocks
-                             // rewritten (zeroed by k_bingest)
+  unsigned long long *work;  // [4] whole batch, summed over calls until ct_batch_work resets them:
+                             // update support words, currTable blocks read, blocks rewritten,
+                             // support bytes staged into shared memory
 };
 
 __device__ __forceinline__ Ctl *bctl(const BatchDev &b, int s) {
@@ -76,12 +77,9 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
   const StateDev &st = states[blockIdx.x];
   const uint64_t *rem = removed ? removed + (int64_t)blockIdx.x * removed_stride : nullptr;
   dev_ingest<kBSmallTPB>(tb, st, rem, 0, smem);
-  if (blockIdx.x == 0 && threadIdx.x < 2) {
-    if (threadIdx.x == 0) {
-      *bd.nmiss = 0;
-      *bd.nmiss2 = 0;
-    }
-    bd.work[threadIdx.x] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *bd.nmiss = 0;
+    *bd.nmiss2 = 0;
   }
   __shared__ int s_go, s_nrows;
   if (threadIdx.x == 0) {   // the thread that wrote the control fields
@@ -256,7 +254,8 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
   const int64_t units = (int64_t)ntiles * nchunk;
   const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
   int cur_tile = -1;
-  uint32_t w_loads = 0, w_writes = 0;   // this lane's share of the batch work counters
+  uint32_t w_loads = 0, w_writes = 0, w_reads = 0;   // this lane's share of the batch work counters
+  unsigned long long w_staged = 0;
   for (int64_t u = u0; u < u1; ++u) {
     const int tile = (int)(u / nchunk), chunk = (int)(u - (int64_t)tile * nchunk);
     if (tile != cur_tile) {
@@ -269,6 +268,7 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
       }
       __syncthreads();
       cur_tile = tile;
+      w_staged += (unsigned long long)(R + 1) * kTW * 16;
     }
     const int s0 = chunk * chunk_states, s1 = min(S, s0 + chunk_states);
     const int blk = tile * kTW + bl;
@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
       const bool keep = had && (nt.x | nt.y) != 0;
       const unsigned bk = __ballot_sync(0xffffffffu, keep);
       w_writes += wr ? 1u : 0u;
+      w_reads += upd ? 1u : 0u;
       if constexpr (kTW == 32) {
         if (lane == 0) w_loads += nl;     // nl is the warp total here
       } else {
@@ -379,11 +380,14 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
   for (int o = 16; o > 0; o >>= 1) {
     w_loads += __shfl_xor_sync(0xffffffffu, w_loads, o);
     w_writes += __shfl_xor_sync(0xffffffffu, w_writes, o);
+    w_reads += __shfl_xor_sync(0xffffffffu, w_reads, o);
   }
   if (lane == 0) {
     if (w_loads) atomicAdd(bd.work + 0, 2ull * w_loads);
-    if (w_writes) atomicAdd(bd.work + 1, (unsigned long long)w_writes);
+    if (w_reads) atomicAdd(bd.work + 1, (unsigned long long)w_reads);
+    if (w_writes) atomicAdd(bd.work + 2, (unsigned long long)w_writes);
   }
+  if (threadIdx.x == 0 && w_staged) atomicAdd(bd.work + 3, w_staged);
 }
 
 // ------------------------------------------------------------------ a4: index compaction, one CTA per state
@@ -406,7 +410,9 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev b
   uint64_t carry = 0;
   for (int base = 0; base < nw; base += kBSmallTPB) {
     const int k = base + threadIdx.x;
-    const uint32_t w = k < nw ? __ldcg(bm + k) : 0u;
+    uint32_t w = k < nw ? __ldcg(bm + k) : 0u;
+    // k_bupdate writes only the tiles' bits: bits of the last word past W2 are never written
+    if (k == nw - 1 && (tb.W2 & 31)) w &= (1u << (tb.W2 & 31)) - 1u;
     uint64_t total;
     const uint64_t ex = block_excl_scan<kBSmallTPB>((uint64_t)__popc(w), s_warp, total);
     if (tb.use_index) {

@@ -372,62 +372,55 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   __syncthreads();
 }
 
-// ------------------------------------------------------------------ a3: update of one tile
-// Alg. 2 for the kFastTPB index entries of `tile` (one 16-byte block per
-// thread).  The block dies early (Alg. 2) once no valid tuple is left in
-// it (checked between batches).  The tile's survivor count goes to cnt[tile].
-__device__ __forceinline__ void fast_update_tile(const TableDev &tb, const StateDev &st, const FastSh &fs,
-                                                 const uint32_t *__restrict__ ulist, int tile,
-                                                 uint32_t *__restrict__ cnt, uint32_t &n_loads,
-                                                 uint32_t &n_writes) {
-  const int L = fs.L, nrows = fs.nrows;
+// ------------------------------------------------------------------ a3: update of one index entry
+// Alg. 2 for index entry k (one 16-byte block per thread).  The block dies
+// early (Alg. 2) once no valid tuple is left in it (checked between
+// batches).  Returns whether the block keeps a valid tuple.
+__device__ __forceinline__ bool fast_update_entry(const TableDev &tb, const StateDev &st, const FastSh &fs,
+                                                  const uint32_t *__restrict__ ulist, int k, uint32_t &n_loads,
+                                                  uint32_t &n_writes) {
+  const int nrows = fs.nrows;
   const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
   ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
   const int64_t Wp = tb.Wp;
-  const int k = tile * kFastTPB + threadIdx.x;
-  bool keep = false;
-  if (k < L) {
-    const int pid = fs.ident ? k : idx_in[k];
-    const ulonglong2 tw = T2[pid];
-    const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
-    uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-    int p0 = 0;
-    for (; p0 < nrows; p0 += kFastUnroll) {
-      if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 16-byte block
-      ulonglong2 v[kFastUnroll];
+  const int pid = fs.ident ? k : idx_in[k];
+  const ulonglong2 tw = T2[pid];
+  const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+  uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+  int p0 = 0;
+  for (; p0 < nrows; p0 += kFastUnroll) {
+    if (((tw.x & mx) | (tw.y & my)) == 0) break;   // Alg. 2, per 16-byte block
+    ulonglong2 v[kFastUnroll];
 #pragma unroll
-      for (int q = 0; q < kFastUnroll; ++q)
-        v[q] = (p0 + q < nrows) ? ld_sup2(col + (int64_t)(ulist[p0 + q] & kRowMask) * Wp)
-                                : make_ulonglong2(0ull, 0ull);
+    for (int q = 0; q < kFastUnroll; ++q)
+      v[q] = (p0 + q < nrows) ? ld_sup2(col + (int64_t)(ulist[p0 + q] & kRowMask) * Wp)
+                              : make_ulonglong2(0ull, 0ull);
 #pragma unroll
-      for (int q = 0; q < kFastUnroll; ++q) {
-        if (p0 + q < nrows) {
-          const uint32_t e = ulist[p0 + q];
-          ax |= v[q].x;
-          ay |= v[q].y;
-          if (e & kEndBit) {
-            if (e & kInvBit) {
-              mx &= ~ax;
-              my &= ~ay;
-            } else {
-              mx &= ax;
-              my &= ay;
-            }
-            ax = ay = 0;
+    for (int q = 0; q < kFastUnroll; ++q) {
+      if (p0 + q < nrows) {
+        const uint32_t e = ulist[p0 + q];
+        ax |= v[q].x;
+        ay |= v[q].y;
+        if (e & kEndBit) {
+          if (e & kInvBit) {
+            mx &= ~ax;
+            my &= ~ay;
+          } else {
+            mx &= ax;
+            my &= ay;
           }
+          ax = ay = 0;
         }
       }
     }
-    n_loads += 2 * min(p0, nrows);   // rows issued before the block died or the list ended
-    const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
-    if (nt.x != tw.x || nt.y != tw.y) {
-      T2[pid] = nt;
-      ++n_writes;
-    }
-    keep = (nt.x | nt.y) != 0;
   }
-  const int survivors = __syncthreads_count(keep);
-  if (threadIdx.x == 0) cnt[tile] = (uint32_t)survivors;
+  n_loads += 2 * min(p0, nrows);   // rows issued before the block died or the list ended
+  const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
+  if (nt.x != tw.x || nt.y != tw.y) {
+    T2[pid] = nt;
+    ++n_writes;
+  }
+  return (nt.x | nt.y) != 0;
 }
 
 // ------------------------------------------------------------------ a6a: probe of one row
@@ -439,8 +432,8 @@ __device__ __forceinline__ void fast_update_tile(const TableDev &tb, const State
 // block (r if the residue hit, else the lowest hit of the round) or -1.
 __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, int Lin,
                                          const ulonglong2 *__restrict__ T2, const uint64_t *__restrict__ srow,
-                                         int r, int off, int lane, uint32_t &nl) {
-  for (int round = 0; round < kSelfRounds; ++round) {
+                                         int r, int off, int lane, uint32_t &nl, int round0 = 0, int rstep = 1) {
+  for (int round = round0; round < kSelfRounds; round += rstep) {
     const int kb = round * kFirstScanFast;
     if (kb >= Lin) break;
     // every load is issued unconditionally (out-of-range entries re-read a
@@ -464,8 +457,8 @@ __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, in
       t[q] = __ldcg(T2 + pid[q]);
       s[q] = ld_sup2(srow + 2 * (int64_t)pid[q]);
     }
-    const bool rh = round == 0 && r >= 0 && ((tr.x & sr.x) | (tr.y & sr.y)) != 0;
-    if (round == 0 && r >= 0) nl += 2;
+    const bool rh = round == round0 && r >= 0 && ((tr.x & sr.x) | (tr.y & sr.y)) != 0;
+    if (round == round0 && r >= 0) nl += 2;
 #pragma unroll
     for (int q = 0; q < kProbeUnroll; ++q) {
       const bool in = kb + q * 32 + lane < Lin;
@@ -550,6 +543,18 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
 // experiment builds only: per-item probe timing (globaltimer and SM id)
 __device__ unsigned long long g_probe_dbg[8192][4];
 #endif
+#ifdef CT_FAST_TRACE
+// experiment builds only: per-CTA phase timestamps of the last k_fast call
+__device__ unsigned long long g_fast_trace[4096][10];
+#define FAST_TRACE(i) \
+  do {                                                                        \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_fast_trace[blockIdx.x][i] = globaltimer(); \
+  } while (0)
+#else
+#define FAST_TRACE(i) \
+  do {                \
+  } while (0)
+#endif
 
 // ------------------------------------------------------------------ k_fast
 // Cooperative launch (all CTAs co-resident), kFastTPB threads, dynamic smem
@@ -575,7 +580,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
   const bool t0 = blockIdx.x == 0 && tid == 0;
   // phase timestamps of block 0 go straight to tph[] (no registers held)
   if (t0) c->tph[0] = globaltimer();
+  FAST_TRACE(0);
   cta_ingest(tb, st, removed, root_mode, p, fs, blockIdx.x == 0);
+  FAST_TRACE(1);
   if (t0) {
     const unsigned long long t = globaltimer();
     for (int i = 1; i < 6; ++i) c->tph[i] = t;
@@ -583,14 +590,24 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
 
   if (fs.go) {
     uint32_t *__restrict__ tcnt = reinterpret_cast<uint32_t *>(st.tilestat);
-    // ---- update (a3), survivor count per tile
-    const int ntiles = (fs.L + kFastTPB - 1) / kFastTPB;
+    // ---- update (a3): CTA c owns index entries [c·ts, (c+1)·ts), ts = ceil(L / G)
+    // (an equal share per CTA, so every SM streams the same number of blocks),
+    // walked kFastTPB at a time; the CTA's survivor count goes to tcnt[c]
+    const int ts = (fs.L + G - 1) / G;
+    const int k_lo = min(fs.L, (int)blockIdx.x * ts), k_hi = min(fs.L, k_lo + ts);
     uint32_t n_loads = 0, n_writes = 0, f_loads = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += G)
-      fast_update_tile(tb, st, fs, p.ulist, tile, tcnt, n_loads, n_writes);
+    {
+      int kept = 0;
+      for (int base = k_lo; base < k_hi; base += kFastTPB) {
+        const int k = base + tid;
+        const bool keep = k < k_hi && fast_update_entry(tb, st, fs, p.ulist, k, n_loads, n_writes);
+        kept += __syncthreads_count(keep);
+      }
+      if (tid == 0) tcnt[blockIdx.x] = (uint32_t)kept;
+    }
+    FAST_TRACE(2);
 
     const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-    const int item0 = warp * G + blockIdx.x;   // CTA-major: item i -> CTA i % G
     if (kFastStop > 0) {
       // experiment builds only (tools/gpu_exp.sh): 1 = update only, 2 = update +
       // barrier, -3 = ... + compaction, -4 = ... + probe; the call then reports a
@@ -605,11 +622,12 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     } else {
     fast_grid_barrier(st.bar);
     if (t0) c->tph[2] = globaltimer();
+    FAST_TRACE(3);
 
-    // ---- compaction (a4): L_out and this CTA's tile prefixes from the tile counts
+    // ---- compaction (a4): L_out and this CTA's prefix from the per-CTA counts
     {
       int tot = 0, below = 0;
-      for (int j = tid; j < ntiles; j += kFastTPB) {
+      for (int j = tid; j < G; j += kFastTPB) {
         const int v = (int)__ldcg(tcnt + j);
         tot += v;
         if (j < (int)blockIdx.x) below += v;
@@ -622,16 +640,11 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
       const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
       int32_t *__restrict__ idx_out = fs.par ? st.idx0 : st.idx1;
-      for (int tile = blockIdx.x; tile < ntiles; tile += G) {
-        if (tile != (int)blockIdx.x) {   // prefix of the next own tile: add counts [tile - G, tile)
-          int add = 0;
-          for (int j = tile - G + tid; j < tile; j += kFastTPB) add += (int)__ldcg(tcnt + j);
-          below += fast_block_sum(add, fs);
-        }
-        const int k = tile * kFastTPB + tid;
+      for (int base = k_lo; base < k_hi; base += kFastTPB) {
+        const int k = base + tid;
         int pid = 0;
         bool keep = false;
-        if (k < fs.L) {
+        if (k < k_hi) {
           pid = fs.ident ? k : idx_in[k];
           const ulonglong2 t = __ldcg(T2 + pid);
           keep = (t.x | t.y) != 0;
@@ -640,16 +653,23 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         __syncthreads();
         if (lane == 0) fs.woff[warp] = __popc(bal);
         __syncthreads();
-        uint32_t off = 0;
+        uint32_t off = 0, all = 0;
 #pragma unroll
-        for (int w = 0; w < kFastWarps; ++w)
+        for (int w = 0; w < kFastWarps; ++w) {
           if (w < warp) off += fs.woff[w];
+          all += fs.woff[w];
+        }
         if (tb.use_index && keep) idx_out[below + off + __popc(bal & lanemask_lt())] = pid;
+        below += (int)all;
       }
     }
     __syncthreads();
+    FAST_TRACE(4);
 
-    // ---- probe (a6a): residue + up to kSelfRounds rounds over the pre-update index
+    // ---- probe (a6a): residue + up to kSelfRounds rounds over the pre-update index.
+    // Item i goes to CTA i % G; when there are few items per CTA, wpi warps of
+    // the CTA share one item and take its rounds round-robin (warp q: rounds q,
+    // q + wpi, ...), so an item costs one round trip instead of several.
     const int Lout = fs.Lout;
     const bool compact = tb.use_index != 0;
     const int32_t *__restrict__ idx = compact ? (fs.par ? st.idx0 : st.idx1) : nullptr;
@@ -658,45 +678,48 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     const bool may_miss = fs.L > kSelfRounds * kFirstScanFast;   // the probe cannot cover the index
     if (t0) st.sup[tb.R] = Lout > 0;
     if (Lout > 0 && kFastStop != -3) {
-      for (int item = item0; item < fs.nitems; item += nw) {
-        const int row = p.items[item];
-        const int r = (tb.use_res && lane == 0) ? st.res[row] : -1;
-        uint32_t nl = 0;
-#ifdef CT_PROBE_SPREAD
-        const int off = (int)(((unsigned)row * 2654435761u) % (unsigned)fs.L);
-#else
-        const int off = 0;
-#endif
-#ifdef CT_PROBE_DEBUG
-        const unsigned long long pt0 = globaltimer();
-#endif
-        const int hit = probe_row(idx_old, fs.L, T2, tb.S + (int64_t)row * tb.Wp, r, off, lane, nl);
-#ifdef CT_PROBE_DEBUG
-        if (lane == 0 && item < 8192) {
-          unsigned smid;
-          asm("mov.u32 %0, %%smid;" : "=r"(smid));
-          g_probe_dbg[item][0] = pt0;
-          g_probe_dbg[item][1] = globaltimer();
-          g_probe_dbg[item][2] = ((unsigned long long)smid << 32) | (unsigned)blockIdx.x;
-          g_probe_dbg[item][3] = ((unsigned long long)nl << 32) | (unsigned)(hit + 1);
+      const int per_cta = (fs.nitems - (int)blockIdx.x + G - 1) / G;   // items of this CTA
+      const int wpi = per_cta <= 1 ? kFastWarps : per_cta <= 2 ? kFastWarps / 2 : 1;
+      const int slots = kFastWarps / wpi, slot = warp / wpi, q = warp % wpi;
+      for (int j0 = 0; j0 < per_cta; j0 += slots) {
+        const int j = j0 + slot;
+        const int item = (int)blockIdx.x + j * G;
+        int hit = -1, row = 0, r = -1;
+        if (j < per_cta) {
+          row = p.items[item];
+          r = (tb.use_res && lane == 0 && q == 0) ? st.res[row] : -1;
+          uint32_t nl = 0;
+          hit = probe_row(idx_old, fs.L, T2, tb.S + (int64_t)row * tb.Wp, r, 0, lane, nl, q, wpi);
+          if (lane == 0) {
+            f_loads += nl;
+            if (hit >= 0) {
+              st.sup[row] = 1;
+              if (hit != r) st.res[row] = hit;
+            }
+          }
         }
-#endif
-        if (lane == 0) {
-          f_loads += nl;
-          if (hit >= 0) {
-            st.sup[row] = 1;
-            if (hit != r) st.res[row] = hit;
-          } else if (may_miss) {
-            st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+        if (wpi == 1) {
+          if (j < per_cta && lane == 0 && hit < 0 && may_miss) st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+        } else {
+          // the item is a miss only if none of its wpi warps found a support
+          __syncthreads();
+          if (lane == 0) fs.red[warp] = hit >= 0;
+          __syncthreads();
+          if (j < per_cta && q == 0 && lane == 0 && may_miss) {
+            int any = 0;
+            for (int w = warp; w < warp + wpi; ++w) any |= fs.red[w];
+            if (!any) st.scanlist[atomicAdd(&c->nscan, 1)] = row;
           }
         }
       }
     }
     if (t0) c->tph[3] = c->tph[4] = globaltimer();
+    FAST_TRACE(5);
     // ---- scan (a6b): misses x chunks of the compacted index, from entry 0
     if (Lout > 0 && may_miss && kFastStop > -3) {
       fast_grid_barrier(st.bar);   // index complete, misses known
       if (t0) c->tph[4] = globaltimer();
+      FAST_TRACE(6);
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
@@ -767,6 +790,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
     }
     if (t0) c->tph[5] = globaltimer();
+    FAST_TRACE(7);
     if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
     }   // !kFastStop
     // per-CTA counter reduction, one fire-and-forget atomic per counter
@@ -789,6 +813,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
 
   // ---- completion: the last CTA to get here finalizes
   __syncthreads();
+  FAST_TRACE(8);
   if (tid == 0) {
     __threadfence();
     fs.last = atomicAdd(&c->cta_done, 1) == G - 1;

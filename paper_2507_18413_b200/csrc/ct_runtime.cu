@@ -189,7 +189,8 @@ static StateLayout make_layout(const ct_table *tb) {
   L.scanlist = take((size_t)tb->R * 4);
   L.sup = take((size_t)tb->R + 1);
   L.varcnt = take((size_t)tb->n * 8);
-  L.tilestat = take((size_t)std::max(ntiles, 1) * 8);
+  // chained-scan tile statuses (k_fused) / per-CTA survivor counts (k_fast, <= 16 CTAs per SM)
+  L.tilestat = take(std::max((size_t)std::max(ntiles, 1) * 8, (size_t)tb->sm_count * 16 * 4));
   L.out = take((size_t)(1 + 2 * tb->Wd) * 8);
   L.slot = take((size_t)tb->Wd * 8);
   L.bar = take((size_t)kBarWords * 4);
@@ -485,6 +486,11 @@ int ct_debug_probe_read(void *out, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(out, g_probe_dbg, bytes);
 }
 #endif
+#ifdef CT_FAST_TRACE
+int ct_debug_trace_read(void *out, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(out, g_fast_trace, bytes);
+}
+#endif
 const char *ct_version(void) { return "ct_b200 0.1 (sm_100a)"; }
 
 ct_status ct_nccl_unique_id(void *out128) {
@@ -664,8 +670,10 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fast, kFastTPB, tb->fast_smem));
       if (occ >= 1) {
         tb->use_fast = 1;
-        const int tiles = (int)((dv.W2 + kFastTPB - 1) / kFastTPB);
-        tb->fast_grid = std::min(tb->sm_count * occ, std::max(tb->sm_count, tiles));
+        // an equal number of CTAs per SM, enough that one CTA's share of the
+        // largest index (W2 entries) is at most kFastTPB entries
+        const int per_sm = (int)((dv.W2 + (int64_t)tb->sm_count * kFastTPB - 1) / ((int64_t)tb->sm_count * kFastTPB));
+        tb->fast_grid = tb->sm_count * std::max(1, std::min(occ, per_sm));
         if (tb->fused_grid_override > 0) tb->fast_grid = std::min(tb->sm_count * occ, tb->fused_grid_override);
       }
     }
@@ -975,6 +983,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64;
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
+  if (b->d_miss && cudaMemset(b->d_miss, 0, b->miss_bytes) != cudaSuccess) cudaGetLastError();
   if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status || !b->d_bgo || !b->d_miss)
     return cleanup(fail(CT_ENOMEM, "device allocation of a %d-state batch (%zu bytes) failed", n_states, b->bytes));
   if (cudaHostAlloc((void **)&b->h_in, std::max<size_t>(io, 8), 0) != cudaSuccess ||
@@ -1013,6 +1022,8 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
   if (init->stream != tb->stream) cudaStreamSynchronize(init->stream);
+  // per-call scratch starts zeroed, as for single states
+  if (cudaMemsetAsync(b->mem, 0, b->bytes, tb->stream) != cudaSuccess) return cleanup(fail(CT_ECUDA, "batch memset failed"));
   for (int i = 0; i < n_states; ++i)
     if (cudaMemcpyAsync(b->mem + (size_t)i * tb->lay.total, init->mem, tb->lay.persist, cudaMemcpyDeviceToDevice,
                         tb->stream) != cudaSuccess)
@@ -1165,26 +1176,25 @@ ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
   return CT_OK;
 }
 
-ct_status ct_batch_work(const ct_batch *b, int64_t *out4) {
-  if (!b || !out4) return fail(CT_EINVAL, "NULL argument");
+ct_status ct_batch_work(ct_batch *b, int64_t *out6, int32_t reset) {
+  if (!b || !out6) return fail(CT_EINVAL, "NULL argument");
   DeviceGuard g(b->tb->device);
   CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
-  if (!b->tb->bt_tw) {
-    for (int i = 0; i < 4; ++i) out4[i] = -1;
-    return CT_OK;
-  }
-  CUDA_TRY(cudaMemcpy(out4, b->bd.work, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  // filter side: summed over the states' own counters
+  for (int i = 0; i < 6; ++i) out6[i] = -1;
+  if (!b->tb->bt_tw) return CT_OK;
+  CUDA_TRY(cudaMemcpy(out6, b->bd.work, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 4 * sizeof(int64_t)));
+  // filter side of the last call: summed over the states' own counters
   std::vector<Ctl> c((size_t)b->S);
   CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,
                         cudaMemcpyDeviceToHost));
-  out4[2] = out4[3] = 0;
   std::vector<int32_t> bgo((size_t)b->S);
   CUDA_TRY(cudaMemcpy(bgo.data(), b->d_bgo, (size_t)b->S * 4, cudaMemcpyDeviceToHost));
+  out6[4] = out6[5] = 0;
   for (int i = 0; i < b->S; ++i) {
-    if (bgo[(size_t)i] < 0) continue;   // the state did not run the filter this call
-    out4[2] += (int64_t)c[(size_t)i].scan_loads;
-    out4[3] += c[(size_t)i].nscan;
+    if (bgo[(size_t)i] < 0) continue;   // the state did not run the filter in the last call
+    out6[4] += (int64_t)c[(size_t)i].scan_loads;
+    out6[5] += c[(size_t)i].nscan;
   }
   return CT_OK;
 }

@@ -119,7 +119,7 @@ SIGNATURES = {
     "ct_state_stats": (I32, [P, P]),
     "ct_batch_stats": (I32, [P, P]),
     "ct_batch_read_table": (I32, [P, I32, P]),
-    "ct_batch_work": (I32, [P, P]),
+    "ct_batch_work": (I32, [P, P, I32]),
     "ct_nccl_unique_id": (I32, [P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
@@ -370,12 +370,13 @@ def ct_state_read_table(state, n_words: int) -> np.ndarray:
     return out[:n_words]
 
 
-def ct_batch_work(batch) -> dict:
-    """Whole-batch work counters of the last ct_propagate_many (include/ct.h)."""
-    out = np.zeros(4, dtype=np.int64)
-    _check(lib().ct_batch_work(batch, _np_ptr(out)), allow_fail=False)
-    return dict(update_support_words=int(out[0]), update_table_writes=int(out[1]),
-                filter_support_words=int(out[2]), probe_misses=int(out[3]))
+def ct_batch_work(batch, reset: bool = False) -> dict:
+    """Work counters of the tile-major batch path (include/ct.h)."""
+    out = np.zeros(6, dtype=np.int64)
+    _check(lib().ct_batch_work(batch, _np_ptr(out), int(bool(reset))), allow_fail=False)
+    keys = ("update_support_words", "table_blocks_read", "table_blocks_written", "support_bytes_staged",
+            "filter_support_words", "probe_misses")
+    return {k: int(v) for k, v in zip(keys, out)}
 
 
 def ct_batch_read_table(batch, index: int, n_words: int) -> np.ndarray:

@@ -28,13 +28,13 @@ for k in range(40):
             tot[f] = tot.get(f, 0) + sum(getattr(s, f) for s in ss)
         tot["fail"] = tot.get("fail", 0) + int((st.cpu().numpy() == 1).sum())
         tot["dead_in"] = tot.get("dead_in", 0) + sum(1 for s in ss if s.last_status == -5)
-        for kk, vv in b.work().items():
+        for kk, vv in b.work(reset=True).items():
             tot["work_" + kk] = tot.get("work_" + kk, 0) + vv
     b.restore_dead(tab.root)
 prof = C.ct_table_profile_read(tab.handle, reset=True)
 steps = 20
 print(json.dumps({k: v / steps for k, v in tot.items()}))
 print(json.dumps({k: round(v[1] / max(v[0], 1), 4) for k, v in prof.items() if v[0]}))
-sw = tot["work_update_support_words"] if tot["work_update_support_words"] >= 0 else tot["update_support_words"]
+sw = tot["work_update_support_words"]
 print("update support words/step %.1f MB" % (8 * sw / steps / 1e6))
 tab.close()
