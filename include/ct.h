@@ -142,7 +142,9 @@ typedef struct ct_table_info {
   int64_t state_bytes;          /* device bytes of one state                             */
   int32_t kernel_path;          /* single-state launch shape: 0 one kernel per phase,      */
                                 /* 1 k_fused (grid barrier per phase), 2 k_fast (per-CTA   */
-                                /* ingest, 1-2 grid barriers), 3 k_small (one CTA)         */
+                                /* ingest, 1-2 grid barriers), 3 k_small (one CTA),        */
+                                /* 4 k_wide (one CTA + a thread-per-item filter grid: many */
+                                /* support rows over few words, e.g. the paper's LIN sets) */
   int32_t grid;                 /* CTAs of the single-state launch                       */
   int32_t batch_tile;           /* ct_propagate_many: 16-byte blocks per shared-memory    */
                                 /* support tile of the tile-major update (32, 16 or 8), or */
@@ -326,7 +328,7 @@ ct_status ct_batch_work(ct_batch *b, int64_t *out6, int32_t reset);
  * and launch counts since the last reset, and resets them if `reset`.
  * Kernel slots: 0 ingest, 1 update, 2 probe, 3 scan, 4 combine (NCCL), 5 finalize,
  * 6 fused (all phases of a single-state call in one kernel), 7 small (the same in
- * one CTA, for tables of at most 8192 16-byte blocks). */
+ * one CTA, for tables of at most 8192 16-byte blocks; also k_wide + k_wide_filter). */
 typedef struct ct_kernel_times {
   int64_t launches[8];
   double ms[8];

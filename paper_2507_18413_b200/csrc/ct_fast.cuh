@@ -85,15 +85,18 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// Static shared state of one k_fast CTA.
-struct FastSh {
+// Static shared state of one k_fast CTA (NW warps; k_wide uses the same ingest
+// with 32 warps).
+template <int NW>
+struct FastShT {
   int dead, fail, noop, go, ngroups, nrows, nitems;
   int L, ident, par, Lout, nscan, last;
-  int red[kFastWarps];           // block-reduction scratch
-  uint32_t woff[kFastWarps];
-  uint64_t scan[kFastWarps];
+  int red[NW];                   // block-reduction scratch
+  uint32_t woff[NW];
+  uint64_t scan[NW];
   unsigned long long cnt[3];     // update loads, update writes, filter loads (this CTA)
 };
+using FastSh = FastShT<kFastWarps>;
 
 // Dynamic shared memory of one k_fast CTA.
 struct FastPtrs {
@@ -198,9 +201,9 @@ __device__ __forceinline__ int fast_block_sum(int v, FastSh &fs) {
 // ------------------------------------------------------------------ a2: per-CTA ingest
 // Same decisions as dev_ingest (Alg. 1 L1-3, Alg. 2), results kept in this
 // CTA's shared memory; `writer` (block 0) also publishes the per-call state.
+template <int NT = kFastTPB>
 __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem, int root_mode,
-                           const FastPtrs &p, FastSh &fs, bool writer) {
-  constexpr int NT = kFastTPB;
+                           const FastPtrs &p, FastShT<NT / 32> &fs, bool writer) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
@@ -241,8 +244,10 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     __syncthreads();
     return;
   }
-  if (writer)
-    for (int r = tid; r <= R; r += NT) st.sup[r] = 0;
+  if (writer) {   // sup[0..R] = 0, 16 bytes per store (sup is 256-byte aligned)
+    uint4 *s4 = reinterpret_cast<uint4 *>(st.sup);
+    for (int r = tid; r < (R + 16) / 16; r += NT) s4[r] = make_uint4(0u, 0u, 0u, 0u);
+  }
   // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
   for (int k = tid; k < Wd; k += NT) {
     const uint64_t dm = k == tid ? dm0 : st.dom[k];
@@ -300,7 +305,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
       __syncthreads();
       uint64_t wb = 0, tot = 0;
 #pragma unroll
-      for (int w = 0; w < kFastWarps; ++w) {
+      for (int w = 0; w < NT / 32; ++w) {
         if (w < warp) wb += fs.scan[w];
         tot += fs.scan[w];
       }

@@ -875,6 +875,81 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const State
   }
 }
 
+// ------------------------------------------------------------------ a3-a4 in one block
+// updateTable (Alg. 2) over the L active blocks and the order-preserving
+// compaction of the survivors into the other index buffer, by ONE block of NT
+// threads (tables of at most kSmallMaxPairs blocks).  Returns L_out.  Adds the
+// work counters to the state.  s_warp: NT/32 words of shared scratch.
+template <int NT>
+__device__ int block_update(const TableDev &tb, const StateDev &st, int L, int nrows, int ident, int par,
+                            uint64_t *s_warp) {
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int32_t *__restrict__ idx_in = par ? st.idx1 : st.idx0;
+  int32_t *__restrict__ idx_out = par ? st.idx0 : st.idx1;
+  const bool compact = tb.use_index != 0;
+  ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+  const int64_t Wp = tb.Wp;
+  uint32_t n_loads = 0, n_writes = 0;
+  uint64_t carry = 0;
+  for (int base = 0; base < L; base += NT) {
+    const int k = base + tid;
+    int pid = 0;
+    bool keep = false;
+    if (k < L) {
+      pid = ident ? k : idx_in[k];
+      const ulonglong2 tw = T2[pid];
+      const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+      uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
+      for (int p = 0; p < nrows; p += kUpdUnroll) {
+        if (((tw.x & mx) | (tw.y & my)) == 0) break;
+        uint32_t e[kUpdUnroll];
+        ulonglong2 v[kUpdUnroll];
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u) e[u] = (p + u < nrows) ? (uint32_t)st.ulist[p + u] : 0u;
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u)
+          v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
+        n_loads += 2 * min(kUpdUnroll, nrows - p);
+#pragma unroll
+        for (int u = 0; u < kUpdUnroll; ++u) {
+          if (p + u < nrows) {
+            ax |= v[u].x;
+            ay |= v[u].y;
+            if (e[u] & kEndBit) {
+              if (e[u] & kInvBit) {
+                mx &= ~ax;
+                my &= ~ay;
+              } else {
+                mx &= ax;
+                my &= ay;
+              }
+              ax = ay = 0;
+            }
+          }
+        }
+      }
+      const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
+      if (nt.x != tw.x || nt.y != tw.y) {
+        T2[pid] = nt;
+        ++n_writes;
+      }
+      keep = (nt.x | nt.y) != 0;
+    }
+    uint64_t total;
+    const uint64_t ex = block_excl_scan<NT>((uint64_t)keep, s_warp, total);
+    if (compact && keep) idx_out[carry + ex] = pid;
+    carry += total;
+  }
+  n_loads = warp_sum_u32(n_loads);
+  n_writes = warp_sum_u32(n_writes);
+  if (lane == 0 && (n_loads | n_writes)) {
+    atomicAdd(&c->upd_loads, (unsigned long long)n_loads);
+    atomicAdd(&c->upd_writes, (unsigned long long)n_writes);
+  }
+  return (int)carry;
+}
+
 // ------------------------------------------------------------------ k_small: one state, one CTA
 // Tables of at most kSmallMaxPairs 16-byte blocks (e.g. BASELINE config 2,
 // 1e5 tuples = 782 blocks) are latency-bound: every phase runs in ONE block of
@@ -911,72 +986,10 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   __syncthreads();
   // ---- update + compaction (Alg. 2), all in this block
   if (s_go) {
-    const int L = s_L, nrows = s_nrows;
-    const int32_t *__restrict__ idx_in = s_par ? st.idx1 : st.idx0;
-    int32_t *__restrict__ idx_out = s_par ? st.idx0 : st.idx1;
-    const bool compact = tb.use_index != 0;
-    ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
-    const int64_t Wp = tb.Wp;
-    uint32_t n_loads = 0, n_writes = 0;
-    uint64_t carry = 0;
-    for (int base = 0; base < L; base += kSmallTPB) {
-      const int k = base + tid;
-      int pid = 0;
-      bool keep = false;
-      if (k < L) {
-        pid = s_ident ? k : idx_in[k];
-        const ulonglong2 tw = T2[pid];
-        const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
-        uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-        for (int p = 0; p < nrows; p += kUpdUnroll) {
-          if (((tw.x & mx) | (tw.y & my)) == 0) break;
-          uint32_t e[kUpdUnroll];
-          ulonglong2 v[kUpdUnroll];
-#pragma unroll
-          for (int u = 0; u < kUpdUnroll; ++u) e[u] = (p + u < nrows) ? (uint32_t)st.ulist[p + u] : 0u;
-#pragma unroll
-          for (int u = 0; u < kUpdUnroll; ++u)
-            v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
-          n_loads += 2 * min(kUpdUnroll, nrows - p);
-#pragma unroll
-          for (int u = 0; u < kUpdUnroll; ++u) {
-            if (p + u < nrows) {
-              ax |= v[u].x;
-              ay |= v[u].y;
-              if (e[u] & kEndBit) {
-                if (e[u] & kInvBit) {
-                  mx &= ~ax;
-                  my &= ~ay;
-                } else {
-                  mx &= ax;
-                  my &= ay;
-                }
-                ax = ay = 0;
-              }
-            }
-          }
-        }
-        const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
-        if (nt.x != tw.x || nt.y != tw.y) {
-          T2[pid] = nt;
-          ++n_writes;
-        }
-        keep = (nt.x | nt.y) != 0;
-      }
-      uint64_t total;
-      const uint64_t ex = block_excl_scan<kSmallTPB>((uint64_t)keep, s_warp, total);
-      if (compact && keep) idx_out[carry + ex] = pid;
-      carry += total;
-    }
-    n_loads = warp_sum_u32(n_loads);
-    n_writes = warp_sum_u32(n_writes);
-    if (lane == 0 && (n_loads | n_writes)) {
-      atomicAdd(&c->upd_loads, (unsigned long long)n_loads);
-      atomicAdd(&c->upd_writes, (unsigned long long)n_writes);
-    }
+    const int Lout = block_update<kSmallTPB>(tb, st, s_L, s_nrows, s_ident, s_par, s_warp);
     if (t0) {
-      c->L_out = (int32_t)carry;
-      s_Lout = (int32_t)carry;
+      c->L_out = Lout;
+      s_Lout = Lout;
     }
   }
   __syncthreads();

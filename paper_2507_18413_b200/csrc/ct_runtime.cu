@@ -19,6 +19,7 @@
 #include "ct_model.cuh"
 #include "ct_fast.cuh"
 #include "ct_batch.cuh"
+#include "ct_wide.cuh"
 
 using namespace ctk;
 
@@ -114,6 +115,8 @@ struct ct_table {
   size_t fused_smem = 0;
   int use_fast = 0, fast_grid = 1;   // k_fast (ct_fast.cuh): tables with R <= kLocalRowsMax
   size_t fast_smem = 0;
+  int use_wide = 0;                  // k_wide + k_wide_filter (ct_wide.cuh): many rows, few words
+  size_t wide_smem = 0;
   int bt_tw = 0, bt_grid = 0;        // tile-major batch update (ct_batch.cuh): tile width, 0 = per-state kernels
   size_t bt_smem = 0;
   int live = 0;   // states + batches alive
@@ -305,7 +308,17 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                 bool local_only) {
   cudaStream_t st = s->stream;
-  if (tb->use_small) {
+  if (tb->use_wide) {
+    const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
+    const int e = prof_event(tb, st);
+    k_wide<<<1, kWideTPB, tb->wide_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
+                                               out_dom, out_pruned, out_status, use_state_out);
+    k_wide_filter<<<(unsigned)std::max(1, (tb->R + kWideFiltTPB - 1) / kWideFiltTPB), kWideFiltTPB, 0, st>>>(
+        tb->dev, (const StateDev *)s->d_desc, fin_inside, out_dom, out_pruned, out_status, use_state_out);
+    CUDA_TRY(cudaGetLastError());
+    prof_mark(tb, 7, e, st);
+    if (fin_inside || local_only) return CT_OK;
+  } else if (tb->use_small) {
     const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
     const int e = prof_event(tb, st);
     k_small<<<1, kSmallTPB, tb->fused_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode,
@@ -384,6 +397,10 @@ static void free_state_mem(ct_state *s) {
   if (!s) return;
   ct_table *tb = s->tb;
   DeviceGuard g(tb->device);
+  // a synchronous call returns once its status word is visible, which the last
+  // CTA may write before its final stores: wait for the stream before the
+  // memory goes back to the allocator (the torch hook does not synchronize)
+  if (s->stream) cudaStreamSynchronize(s->stream);
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   if (s->h_in) cudaFreeHost(s->h_in);
   if (s->h_out) cudaFreeHost(s->h_out);
@@ -719,6 +736,18 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
     if (const char *ev = getenv("CT_SMALL_MAX_PAIRS")) small_max = atoi(ev);
     tb->use_small = (tb->use_fused && dv.W2 <= small_max) ? 1 : 0;
   }
+  // ... unless the filter dominates: many support rows over few words (k_wide)
+  {
+    int wide_ok = (tb->use_small && tb->R >= kWideMinRows) ? 1 : 0;
+    if (const char *ev = getenv("CT_NO_WIDE")) wide_ok = wide_ok && !atoi(ev);
+    if (const char *ev = getenv("CT_WIDE")) wide_ok = (tb->use_fused && dv.W2 <= kSmallMaxPairs && atoi(ev)) ? 1 : wide_ok;
+    tb->wide_smem = wide_smem_bytes(n, tb->Wd);
+    if (wide_ok && tb->wide_smem <= 200 * 1024) {
+      CUDA_TRY(cudaFuncSetAttribute(k_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->wide_smem));
+      tb->use_wide = 1;
+      tb->use_small = 0;
+    }
+  }
 
   // ---------------- root state + supports (a1)
   ct_state *root = nullptr;
@@ -796,8 +825,8 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->row_stride_words = t->Wp;
   o->device_bytes = (int64_t)(t->S_bytes + t->meta_bytes);
   o->state_bytes = (int64_t)t->lay.total;
-  o->kernel_path = t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
-  o->grid = t->use_small ? 1 : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
+  o->kernel_path = t->use_wide ? 4 : t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
+  o->grid = t->use_wide ? 1 : t->use_small ? 1 : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   o->batch_tile = t->bt_tw;
   return CT_OK;
 }

@@ -59,7 +59,7 @@ class ct_table_info(ctypes.Structure):
                 ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("batch_tile", ctypes.c_int32)]
 
-KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small"}
+KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small", 4: "k_wide"}
 
 
 class ct_stats(ctypes.Structure):

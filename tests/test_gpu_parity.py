@@ -44,10 +44,11 @@ def _built():
     assert torch.cuda.is_available()
 
 
-def make(p, _grid_fused=False, _fast=True, _grid=0, **kw):
+def make(p, _grid_fused=False, _fast=True, _grid=0, _wide=None, **kw):
     """_grid_fused: force a cooperative multi-CTA kernel even for tables small
     enough for the single-CTA one; _fast=False: the barrier-per-phase k_fused
-    instead of k_fast (both environment knobs are read at create time)."""
+    instead of k_fast; _wide=True/False: force / forbid the k_wide shape (all
+    environment knobs are read at create time)."""
     import os
     if _grid_fused:
         os.environ["CT_SMALL_MAX_PAIRS"] = "0"
@@ -55,12 +56,15 @@ def make(p, _grid_fused=False, _fast=True, _grid=0, **kw):
         os.environ["CT_NO_FAST"] = "1"
     if _grid:
         os.environ["CT_FUSED_GRID"] = str(_grid)   # fewer CTAs than tiles: several tiles per CTA
+    if _wide is True:
+        os.environ["CT_WIDE"] = "1"
+    elif _wide is False:
+        os.environ["CT_NO_WIDE"] = "1"
     try:
         return Table(p.lo, p.d, p.tuples, **kw)
     finally:
-        os.environ.pop("CT_SMALL_MAX_PAIRS", None)
-        os.environ.pop("CT_NO_FAST", None)
-        os.environ.pop("CT_FUSED_GRID", None)
+        for k in ("CT_SMALL_MAX_PAIRS", "CT_NO_FAST", "CT_FUSED_GRID", "CT_WIDE", "CT_NO_WIDE"):
+            os.environ.pop(k, None)
 
 
 # --------------------------------------------------------------------------- a1 supports builder
@@ -247,6 +251,56 @@ def test_config3b_banded_filter_heavy(fast):
         s = st.stats()
         assert s.n_residue_miss > 0          # this workload exercises the full scans
     st.close()
+    tab.close()
+
+
+# --------------------------------------------------------------------------- f2: paper-shaped (LIN) tables, k_wide
+@pytest.mark.parametrize("preset", ["lin_b", "lin_eb"])
+def test_lin_knapsack_walk(preset):
+    """Knapsack-configuration tables shaped like the paper's LIN_B / LIN_EB sets
+    (Table tbl:instances): many support rows, few words,
+    filter-heavy -> the k_wide shape.  Policy P(2, 0.5) walk, every call vs the
+    oracle (status, domains, pruned, currTable every 10 calls)."""
+    from workloads import knapsack_table, LIN_PRESETS
+    p = knapsack_table(seed=21, **LIN_PRESETS[preset])
+    tab = make(p)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == "k_wide"
+    nfail, _ = run_walk(tab, p, calls=120, seed=31, check_table_every=10)
+    assert nfail > 0
+    tab.close()
+
+
+def test_lin_knapsack_assignments():
+    """Search-like calls on a LIN table: fix one variable to one of its values
+    (the x = v branch of the paper's DFS), from the root."""
+    from workloads import knapsack_table, LIN_PRESETS
+    p = knapsack_table(seed=22, n=90, max_dom=400, t=6000)
+    tab = make(p)
+    root_ok, root_m = check_root(tab, p)
+    rng = Rng(41, lanes=1)
+    st = tab.root.clone()
+    for k in range(40):
+        rem = fix_one_value_removal(rng, root_m, p.d, var=k % p.n)
+        ok, dout, valid = oracle_call(p, root_m & (1 - rem), want_valid=True)
+        st.copy_from(tab.root)
+        status, dom, _ = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL), k
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout), k
+            assert np.array_equal(bits_to_bool(st.read_table(), p.t), valid), k
+    st.close()
+    tab.close()
+
+
+@pytest.mark.parametrize("knob", ["auto", "dom", "delta", "nores", "noindex", "nograph"])
+def test_wide_forced_random(knob):
+    """k_wide forced on an i.i.d. table (few rows) under every knob."""
+    kw = {"auto": {}, "dom": dict(update_policy=CT_POLICY_DOM), "delta": dict(update_policy=CT_POLICY_DELTA),
+          "nores": dict(use_residues=False), "noindex": dict(use_index=False), "nograph": dict(use_graph=False)}[knob]
+    p = random_table(5, 20, 60_000 + 7, seed=13, lo=-4)
+    tab = make(p, _wide=True, **kw)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == "k_wide"
+    run_walk(tab, p, calls=80, seed=17, check_table_every=8)
     tab.close()
 
 
@@ -494,7 +548,8 @@ def test_batch_slots_from_compacted_states():
 
 
 # --------------------------------------------------------------------------- sharded (a10)
-PATHS = {"small": dict(), "fast": dict(_grid_fused=True), "v1": dict(_grid_fused=True, _fast=False)}
+PATHS = {"small": dict(), "fast": dict(_grid_fused=True), "v1": dict(_grid_fused=True, _fast=False),
+         "wide": dict(_wide=True)}
 
 
 @pytest.mark.parametrize("path", list(PATHS))

@@ -87,3 +87,21 @@ def test_policies():
     assert rem.reshape(5, 20).sum(axis=1).tolist() == [10] * 5
     single = np.zeros(100, np.uint8); single[::20] = 1
     assert walk_removal(rng, single, d) is None
+
+
+def test_knapsack_table_shape_and_invariants():
+    """f2 generator: every row is a feasible bounded-knapsack
+    configuration, values inside the declared domains, deterministic per seed,
+    preset sizes as in Table tbl:instances (L476-486)."""
+    import numpy as np
+    from workloads import knapsack_table, LIN_PRESETS
+    p = knapsack_table(seed=3, n=40, max_dom=100, t=500)
+    w, cap = p.meta["weights"], p.meta["capacity"]
+    assert p.tuples.shape == (500, 40) and p.d.max() == 100
+    assert (p.tuples >= 0).all() and (p.tuples < p.d[None, :]).all()
+    assert ((p.tuples.astype(np.int64) * w[None, :]).sum(1) <= cap).all()
+    assert (p.tuples.sum(1) > 0).mean() > 0.9
+    q = knapsack_table(seed=3, n=40, max_dom=100, t=500)
+    assert np.array_equal(p.tuples, q.tuples) and np.array_equal(p.d, q.d)
+    assert LIN_PRESETS["lin_b"]["max_dom"] == 600 and 80 <= LIN_PRESETS["lin_b"]["n"] <= 150
+    assert LIN_PRESETS["lin_eb"]["max_dom"] == 800 and 100 <= LIN_PRESETS["lin_eb"]["n"] <= 200

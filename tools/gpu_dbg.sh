@@ -1,3 +1,4 @@
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
-python tools/repro_tw8.py 2>&1 | tail -3
-for i in 1 2 3; do timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | grep -E "^FAILED|passed|failed" | head -3; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "lin_ or wide or virtual" 2>&1 | grep -E "^FAILED|^E  |passed|failed" | head -20
+python tools/exp_lin.py lin_b
+python tools/exp_lin.py lin_eb

@@ -6,7 +6,10 @@ Shapes:
   C3  random positive table n=8, d=100, t=1e7, i.i.d. rows (seed 3);
   C3b banded table n=8, d=100, t=1e7: x0 uniform, x_i = (x0*c_i + u_i) mod d,
       u_i in [0, 10) (seed 4) -- the correlated extreme that forces full scans;
-  C4  random positive table n=6, d=50, t=1e6 (seed 5).
+  C4  random positive table n=6, d=50, t=1e6 (seed 5);
+  LIN knapsack-configuration tables shaped like the paper's LIN_B / LIN_EB
+      sets (Table tbl:instances L476-486): 80-200 variables,
+      max domain size 600-800, 5e3-1.5e4 tuples.
 Rows are i.i.d. (duplicates allowed).  The paper's own instances
 (bounded-knapsack tables) are not published; these generators
 bracket that regime (SURVEY §8(d) "Workload structure vs the paper").
@@ -92,3 +95,39 @@ def banded_table(n: int, d: int, t: int, seed: int, band: int = 10, coeffs=BANDE
             tuples[j0:j1, i] = (x0 * coeffs[i - 1] + r[:, i]) % d
     return Problem(name or f"banded_n{n}_t{t}_s{seed}", np.zeros(n, np.int32),
                    np.full(n, d, np.int32), tuples, seed)
+
+
+# PAPER.md Table tbl:instances (L476-486): variables, max domain size, tuples
+LIN_PRESETS = {"lin_b": dict(n=120, max_dom=600, t=10_000), "lin_eb": dict(n=160, max_dom=800, t=15_000)}
+
+
+def knapsack_table(n: int, max_dom: int, t: int, seed: int, kmax: int = 8, name: str | None = None) -> Problem:
+    """Bounded-knapsack configurations: item i has weight w_i
+    and bound b_i (domain of x_i = {0..b_i}, d_i = b_i + 1 <= max_dom, item 0 at
+    the maximum); a row is one configuration x with sum w_i x_i <= capacity.
+    Reading (the paper does not publish its generator or seeds):
+    each row packs k ~ U[1, kmax] random items in order, item i gets a count
+    uniform in [1, min(b_i, remaining // w_i)] (skipped if none fits), every
+    other item 0.  Stream order: w (n draws), b (n draws), then per row: k, and
+    per pick: item, count.  Rows are sparse, so value 0 is supported almost
+    everywhere and most other values by only a few rows -- the filter-heavy,
+    many-rows / few-words regime of the paper's instances."""
+    rng = Rng(seed)
+    w = rng.uniform(n, 50).astype(np.int64) + 1
+    b = rng.uniform(n, max_dom - 1).astype(np.int64) + 1
+    b[0] = max_dom - 1
+    cap = int(np.sort(w * b)[n // 2])            # the median item at its bound fits
+    tuples = np.zeros((int(t), n), dtype=np.int32)
+    for j in range(int(t)):
+        k = int(rng.below(kmax)) + 1
+        rem = cap
+        for _ in range(k):
+            i = int(rng.below(n))
+            hi = min(int(b[i]) - int(tuples[j, i]), rem // int(w[i]))
+            if hi < 1:
+                continue
+            c = int(rng.below(hi)) + 1
+            tuples[j, i] += c
+            rem -= c * int(w[i])
+    return Problem(name or f"knapsack_n{n}_d{max_dom}_t{t}_s{seed}", np.zeros(n, np.int32),
+                   (b + 1).astype(np.int32), tuples, seed, meta=dict(weights=w, capacity=cap))
