@@ -2,7 +2,7 @@
 """Benchmark of the Compact-Table propagation hot path on B200 (BASELINE.json).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c3bulk|c3b|c4|c5]
+                    [--workload c3bulk|c3b|c4|c5|lin]
 
 Default workload (BASELINE config 3, "c3bulk"): random positive table, arity 8,
 domain 100, 1e7 tuples (1.0 GB of support bitsets); one step = restore the
@@ -27,7 +27,8 @@ random-removal calls, policy P(2, 0.5)).
 --workload c3b: the banded C3b table (x_i = (x0*c_i + u_i) mod 100, u_i < 10);
 each step fixes x0 to one seeded value, so 630 values of x1..x7 lose every
 support and the filter scans their whole rows over the compacted index: the
-HBM-bound filterDomains workload.  c4 / c5: see run_c4 / run_c5.
+HBM-bound filterDomains workload.  c4 / c5 / lin: see run_c4 /
+run_c5 / run_lin (lin = the paper-shaped knapsack table).
 
 --impl reference times the oracle (the reference arm of this tier) on the same
 workload, rank 0 only.
@@ -114,6 +115,22 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(workload, world, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summarize.py), or None."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        allj = json.load(open(tpath))
+        if "workload" in allj:
+            allj = {allj["workload"]: allj}
+        tj = allj.get(workload) or {}
+        if tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel:
+            return tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------- workloads
 def c3_problem():
     from workloads import random_table
@@ -157,6 +174,180 @@ def bulk_patterns(root_member, d, count: int, seed: int = 11):
     from workloads import Rng, bulk_removal
     rng = Rng(seed)
     return [bulk_removal(rng, root_member, d, q=0.5) for _ in range(count)]
+
+
+# ---------------------------------------------------------------- f2: LIN-shaped (knapsack) table
+def run_lin(args):
+    """a knapsack-configuration table shaped like the paper's
+    LIN_B set (Table tbl:instances: 120 variables, max domain
+    600, 1e4 tuples; many support rows over few words, filter-heavy) driven by a
+    policy P(2, 0.5) walk (restore the root after FAIL or when solved).  The
+    walk is first run with the synchronous host-buffer call (e2e and per-call
+    latency), recording every call's removal set and restores; the same
+    sequence is then replayed with the device-buffer call for the device-timed
+    value (identical states: the library is deterministic).  Latency-bound:
+    the roofline object reports the bytes the kernels count against HBM peak
+    only for completeness.  Replicas only (one table per GPU, no collective)."""
+    import ctypes
+    import torch
+    from paper_2507_18413_b200 import CT_OK, Table
+    from paper_2507_18413_b200 import ct as C
+    from workloads import Rng, knapsack_table, LIN_PRESETS, member_to_bitmap, bitmap_to_member
+    from workloads.policies import walk_removal
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    preset = LIN_PRESETS["lin_b"]
+    p = knapsack_table(seed=21, **preset)
+    t0 = time.perf_counter()
+    tab = Table(p.lo, p.d, p.tuples, device=dev)
+    build_s = time.perf_counter() - t0
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    wd = tab.Wd
+    n_calls = args.steps
+    # ---- e2e + latency: the synchronous C call on host buffers, recording the walk
+    st = tab.root.clone()
+    rem = np.zeros(wd, np.uint64)
+    out = np.zeros(wd, np.uint64)
+    pr = np.zeros(wd, np.uint64)
+    fn = C.lib().ct_propagate
+    cargs = (st.handle, rem.ctypes.data_as(ctypes.c_void_p), out.ctypes.data_as(ctypes.c_void_p),
+             pr.ctypes.data_as(ctypes.c_void_p))
+    rng = Rng(2, lanes=1)
+    cur = root_m.copy()
+    seq = []             # (restore_before, removal bitmap)
+    lat = []
+    restore = False
+    fails = solved = 0
+    t_e2e = 0.0
+    k = 0
+    while len(seq) < args.warmup + n_calls:
+        r = walk_removal(rng, cur, p.d)
+        if r is None:
+            cur = root_m.copy()
+            restore = True
+            solved += 1
+            continue
+        rem[:] = member_to_bitmap(r, p.d)
+        if restore:
+            st.copy_from(tab.root)
+        a = time.perf_counter()
+        s = fn(*cargs)
+        b = time.perf_counter()
+        if s < 0:
+            raise RuntimeError(C.ct_last_error())
+        if len(seq) >= args.warmup:
+            lat.append((b - a) * 1e6)
+            t_e2e += b - a
+        seq.append((restore, rem.copy()))
+        restore = False
+        if s == CT_OK:
+            cur = bitmap_to_member(out, p.d)
+        else:
+            fails += 1
+            cur = root_m.copy()
+            restore = True
+    st.close()
+    # ---- device-timed replay (device buffers, async), same sequence
+    work = tab.root.clone()
+    rem_dev = torch.from_numpy(np.stack([x[1] for x in seq]).view(np.int64)).to(f"cuda:{dev}")
+    od = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    sd = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+    stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+
+    def replay(lo, hi):
+        for i in range(lo, hi):
+            if seq[i][0]:
+                work.copy_from(tab.root)
+            work.propagate_async(rem_dev[i], od, None, sd)
+
+    replay(0, args.warmup)
+    work.synchronize()
+    clocks = Clocks(dev)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    replay(args.warmup, len(seq))
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
+    value = world * n_calls / (ms_max / 1e3)
+    # per-kernel times + kernel-counted bytes: replay once more with events, reading stats per call
+    work.copy_from(tab.root)
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    byts = 0
+    for i in range(args.warmup, len(seq)):
+        if seq[i][0]:
+            work.copy_from(tab.root)
+        work.propagate_async(rem_dev[i], od, None, sd)
+        s_ = work.stats()
+        byts += 8 * (s_.update_support_words + s_.filter_support_words) + 16 * (s_.words_in + s_.update_table_writes) \
+            + 4 * (s_.words_in + s_.words_out) + 32 * s_.n_filter_items
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    C.ct_table_profile(tab.handle, False)
+    kname = C.KERNEL_PATHS.get(tab.info.kernel_path)
+    k_n, k_ms = prof["small"]
+    peak, peak_src = peaks()
+    t_k = k_ms / max(k_n, 1) / 1e3
+    cpu = None
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        import oracle
+        oracle.lib()
+        cur = root_m.copy()
+        n = 0
+        t1 = time.perf_counter()
+        i = 0
+        while time.perf_counter() - t1 < min(args.cpu_budget, 10.0) or n == 0:
+            restore_, r = seq[i % len(seq)]
+            if restore_:
+                cur = root_m.copy()
+            ok, dout, _ = oracle.gac(p.lo, p.d, p.tuples, cur & (1 - bitmap_to_member(r, p.d)))
+            cur = dout if ok else root_m.copy()
+            n += 1
+            i += 1
+        dt = time.perf_counter() - t1
+        cpu = {"value": n / dt, "unit": "propagations/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {n} calls of the same walk (oracle/ct_oracle.c brute-force scan of the 1e4 "
+                         f"tuples, single thread) in {dt:.1f} s", "host_nproc": os.cpu_count()}
+    q = lambda xs, f: sorted(xs)[min(len(xs) - 1, int(f * len(xs)))]
+    tab.close()
+    if rank == 0:
+        line = {
+            "metric": "propagations/s (LIN_B-shaped knapsack table, P(2,0.5) walk, ct_propagate)",
+            "value": value, "unit": "propagations/s", "n_gpus": world, "steps": n_calls, "warmup": args.warmup,
+            "ms_per_step": ms_max / n_calls, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u64", "data": "synthetic (seeded knapsack configurations, workloads.knapsack_table)",
+            "config": {"workload": "lin", "table": f"knapsack n={p.n}, max domain {preset['max_dom']}, "
+                                                   f"t={p.t}, R={p.R} support rows, {tab.info.words} words, seed 21",
+                       "step": "restore after FAIL/solved (D2D) + ct_propagate_async of a P(2,0.5) removal",
+                       "kernel_path": kname, "parallelism": "1 GPU" if world == 1 else f"{world} replicas",
+                       "l2": "table (supports 0.03 GB) L2-resident: latency-bound regime", "build_s": round(build_s, 3),
+                       "fails": fails, "restores_solved": solved},
+            "roofline": {"bound": "hbm", "achieved": byts / max(k_n, 1) / t_k / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": byts / max(k_n, 1) / t_k / 1e9 / peak, "traffic": None,
+                         "kernel": "ctk::k_wide + ctk::k_wide_filter" if kname == "k_wide" else "ctk::" + str(kname),
+                         "bytes_per_launch": byts / max(k_n, 1), "ms_per_launch": t_k * 1e3, "peak_source": peak_src,
+                         "note": "latency-bound: a call moves ~0.1-1 MB; the number that matters is latency"},
+            "e2e": {"value": n_calls / t_e2e, "unit": "propagations/s", "h2d_bytes_per_step": 8 * wd,
+                    "d2h_bytes_per_step": 8 * (1 + 2 * wd), "steps": n_calls,
+                    "api": "ct_propagate (host buffers; mapped I/O; CUDA graph)"},
+            "latency": {"calls": len(lat), "p50_us": q(lat, 0.5), "p90_us": q(lat, 0.9), "p99_us": q(lat, 0.99)},
+            "gpu_launches": 2 * n_calls if kname == "k_wide" else n_calls,
+            "clocks": clk, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- distributed
@@ -282,15 +473,7 @@ def run_ours(args):
     achieved = k_bytes_per_launch / (k_ms_per_launch / 1e3) / 1e9
     peak, peak_src = peaks()
     model = [16 * c["L_in"] * (c["rows"] + 2) for c in per_pat]                # SURVEY §8(d) B_upd (16-B blocks)
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            if tj.get("workload") == args.workload and tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel_name:
-                traffic = tj.get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    traffic = ncu_traffic(args.workload, world, kernel_name)
     kernel_ms = {k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()}
     step_ms = ms_max / args.steps
     launches = sum(v[0] for k, v in prof.items() if k != "combine")
@@ -534,7 +717,9 @@ def run_c4(args):
         peak, peak_src = peaks()
         smem_peak = 148 * 128 * 1.965          # GB/s: SMs x 128 B/cycle (B300_MICROARCH.md LDS table) x max SM clock
         roofline = {"bound": "hbm", "achieved": hbm / t / 1e9, "peak": peak, "unit": "GB/s",
-                    "frac": hbm / t / 1e9 / peak, "traffic": None,
+                    "frac": hbm / t / 1e9 / peak,
+                    "traffic": ncu_traffic("c4", world, f"ctk::k_bupdate<{tab.info.batch_tile}>"),
+                    "traffic_kernel": f"ctk::k_bupdate<{tab.info.batch_tile}> only (ncu)",
                     "kernel": f"ctk::k_bupdate<{tab.info.batch_tile}> + ctk::k_bcompact",
                     "bytes_per_launch": hbm, "ms_per_launch": t * 1e3, "peak_source": peak_src,
                     "smem": {"achieved": smem / t / 1e9, "peak": smem_peak, "frac": smem / t / 1e9 / smem_peak,
@@ -684,7 +869,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5", "lin"])
     ap.add_argument("--max-nodes", type=int, default=10_000, help="c5: DFS node budget")
     ap.add_argument("--states", type=int, default=4096, help="c4: total independent states (split over ranks)")
     ap.add_argument("--skip-cpu", action="store_true")
@@ -698,6 +883,8 @@ def main():
         run_c4(args)
     elif args.workload == "c5":
         run_c5(args)
+    elif args.workload == "lin":
+        run_lin(args)
     else:
         run_ours(args)
 

@@ -441,8 +441,11 @@ static ct_status new_state(ct_table *tb, ct_state **out) {
   s->h.out = s->d_out_map;
   s->d_desc = reinterpret_cast<StateDev *>(s->mem + tb->lay.desc);
   ct_status st = CT_OK;
-  // synchronous: the descriptor must be in place whichever stream uses the state first
-  if (cudaMemcpy(s->d_desc, &s->h, sizeof(StateDev), cudaMemcpyHostToDevice) != cudaSuccess) {
+  // after the scratch memset on the same stream (the descriptor lives in the
+  // scratch region), then synchronous: it must be in place whichever stream
+  // uses the state first
+  if (cudaMemcpyAsync(s->d_desc, &s->h, sizeof(StateDev), cudaMemcpyHostToDevice, tb->stream) != cudaSuccess ||
+      cudaStreamSynchronize(tb->stream) != cudaSuccess) {
     st = fail(CT_ECUDA, "descriptor upload failed: %s", cudaGetErrorString(cudaGetLastError()));
   }
   if (st != CT_OK) {

@@ -107,7 +107,15 @@ def main():
         tj = {"workload": a.workload, "n_gpus": 1, "kernel": a.kernel, "round": a.round,
               "dram_bytes_per_launch": sum(per) / len(per), "launches_captured": len(per),
               "source": os.path.basename(a.full)}
-        json.dump(tj, open(os.path.join(prof, "ncu_traffic.json"), "w"), indent=1)
+        tpath = os.path.join(prof, "ncu_traffic.json")
+        try:
+            allj = json.load(open(tpath))
+            if "workload" in allj:            # old single-entry format
+                allj = {allj["workload"]: allj}
+        except Exception:
+            allj = {}
+        allj[a.workload] = tj
+        json.dump(allj, open(tpath, "w"), indent=1)
         md.append(f"DRAM traffic per launch (read + write): {tj['dram_bytes_per_launch'] / 1e6:.1f} MB")
     open(os.path.join(prof, f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
     print("\n".join(md))
