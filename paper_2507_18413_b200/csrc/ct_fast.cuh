@@ -149,40 +149,57 @@ __device__ __forceinline__ int row_var(const int32_t *rb, int n, int r) {
   return lo;
 }
 
-// Grid barrier of k_fast (all CTAs co-resident).  A single counter that every
-// CTA increments serialises G same-address atomics at one L2 slice, and the
-// polling of a word in the same line slows them further (measured: ~15 us for
-// 611 CTAs).  Here CTA b arrives at group counter b % kBarGroups; the last
-// arrival of a group arrives at the top counter; the last top arrival resets it
-// and advances the generation word, which the waiting CTAs poll with a backoff.
-// Every counter lives in its own 128-byte line.  Counters return to 0 after
-// each barrier, so the memory only has to be zeroed once (at state creation).
-// The gpu-scope fences also invalidate L1, so later plain loads see the data
-// other CTAs wrote before the barrier.
-__device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
+// Grid barrier of k_fast (all CTAs co-resident).  Arrival counters taken with
+// acq_rel atomics (release: this CTA's writes are visible before it counts;
+// acquire + the L1 invalidate ptxas emits with it: it then reads the others'
+// writes), one arrival counter, and a generation word with one copy per group
+// of CTAs in lines of its own that the waiting CTAs poll (polling a counter's
+// own line, or 740 CTAs polling one line, slows the release).  The last arrival resets the
+// counter, optionally publishes `mode` = leader_mode() in a third line, and
+// bumps the generation with a release store; every CTA returns the mode and
+// `leader` tells the releasing CTA it was the last.  Counters return to 0
+// after each barrier, so the memory only has to be zeroed once (at state
+// creation).
+__device__ __forceinline__ uint32_t atom_add_acqrel(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <typename F>
+__device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mode, int &leader, int *s_mode) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    uint32_t *gen = bar + (kBarGroups + 1) * kBarLine;
-    uint32_t *top = bar + kBarGroups * kBarLine;
-    const int G = gridDim.x, g = blockIdx.x % kBarGroups;
-    const int gsize = G / kBarGroups + (g < G % kBarGroups ? 1 : 0);
-    const int ngroups = G < kBarGroups ? G : kBarGroups;
-    const uint32_t my_gen = ld_acquire_u32(gen);
-    __threadfence();
-    uint32_t *gc = bar + g * kBarLine;
-    if (atomicAdd(gc, 1u) == (uint32_t)gsize - 1) {
-      *gc = 0;
-      __threadfence();
-      if (atomicAdd(top, 1u) == (uint32_t)ngroups - 1) {
-        *top = 0;
-        __threadfence();
-        atomicAdd(gen, 1u);
-      }
+    uint32_t *cnt = bar;
+    uint32_t *mode = bar + (kBarGroups + 2) * kBarLine;
+    // the generation word has kBarGroups copies (lines 1..kBarGroups): each CTA
+    // polls its group's copy, so the polling is spread over several L2 slices
+    uint32_t *mygen = bar + (1 + blockIdx.x % kBarGroups) * kBarLine;
+    const uint32_t my_gen = ld_acquire_u32(mygen);
+    int last = 0;
+    if (atom_add_acqrel(cnt, 1u) == gridDim.x - 1) {
+      *cnt = 0;
+      *mode = (uint32_t)leader_mode();
+      __threadfence();   // one release fence for all the generation copies
+      for (int g = 0; g < kBarGroups; ++g) *(volatile uint32_t *)(bar + (1 + g) * kBarLine) = my_gen + 1;
+      last = 1;
+    } else {
+      while (ld_acquire_u32(mygen) == my_gen) __nanosleep(32);
     }
-    while (ld_acquire_u32(gen) == my_gen) __nanosleep(64);
-    __threadfence();
+    *s_mode = (int)__ldcg(mode);
+    leader = last;
   }
   __syncthreads();
+  return *s_mode;
+}
+
+__device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
+  __shared__ int s_mode;
+  int leader;
+  fast_grid_barrier_mode(bar, [] { return 0; }, leader, &s_mode);
 }
 
 // Block-wide sum over kFastTPB threads (uses fs.red; every thread gets the total).
@@ -611,6 +628,17 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       if (tid == 0) tcnt[blockIdx.x] = (uint32_t)kept;
     }
     FAST_TRACE(2);
+#ifndef CT_FAST_NOCOUNT
+    // update work counters now, while CTAs still finish at different times
+    // (740 same-address atomics at the end of the call cost ~2 us)
+    {
+      const uint32_t wl = warp_sum_u32(n_loads), ww = warp_sum_u32(n_writes);
+      if (lane == 0) {
+        if (wl) atomicAdd(&c->upd_loads, (unsigned long long)wl);
+        if (ww) atomicAdd(&c->upd_writes, (unsigned long long)ww);
+      }
+    }
+#endif
 
     const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
     if (kFastStop > 0) {
@@ -720,11 +748,25 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     }
     if (t0) c->tph[3] = c->tph[4] = globaltimer();
     FAST_TRACE(5);
-    // ---- scan (a6b): misses x chunks of the compacted index, from entry 0
+#ifndef CT_FAST_NOCOUNT
+    if (lane == 0 && f_loads) atomicAdd(&c->scan_loads, (unsigned long long)f_loads);   // probe rounds
+#endif
+    f_loads = 0;
+    // ---- scan (a6b): misses x chunks of the compacted index, from entry 0.
+    // The barrier's last arrival knows every probe is done: with no miss it
+    // releases the others with mode 1 (they exit) and finalizes at once.
     if (Lout > 0 && may_miss && kFastStop > -3) {
-      fast_grid_barrier(st.bar);   // index complete, misses known
+      int leader = 0;
+      const int mode = fast_grid_barrier_mode(st.bar, [&] { return __ldcg(&c->nscan) == 0 ? 1 : 0; }, leader,
+                                              &fs.nscan);
       if (t0) c->tph[4] = globaltimer();
       FAST_TRACE(6);
+      if (mode == 1) {
+        if (tid == 0) fs.last = leader;
+        __syncthreads();
+        if (!fs.last) return;   // the leader finalizes
+        goto finalize;
+      }
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
@@ -798,21 +840,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     FAST_TRACE(7);
     if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
     }   // !kFastStop
-    // per-CTA counter reduction, one fire-and-forget atomic per counter
-    n_loads = warp_sum_u32(n_loads);
-    n_writes = warp_sum_u32(n_writes);
-    if (lane == 0) {
-      if (n_loads) atomicAdd(&fs.cnt[0], (unsigned long long)n_loads);
-      if (n_writes) atomicAdd(&fs.cnt[1], (unsigned long long)n_writes);
-      if (f_loads) atomicAdd(&fs.cnt[2], (unsigned long long)f_loads);
-    }
-    __syncthreads();
+    // scan work counter, one atomic per warp that scanned
 #ifndef CT_FAST_NOCOUNT
-    if (tid == 0) {
-      if (fs.cnt[0]) atomicAdd(&c->upd_loads, fs.cnt[0]);
-      if (fs.cnt[1]) atomicAdd(&c->upd_writes, fs.cnt[1]);
-      if (fs.cnt[2]) atomicAdd(&c->scan_loads, fs.cnt[2]);
-    }
+    if (lane == 0 && f_loads) atomicAdd(&c->scan_loads, (unsigned long long)f_loads);
 #endif
   }
 
@@ -826,10 +856,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
   __syncthreads();
   if (!fs.last) return;
   __threadfence();
-  if (tid == 0) {
-    c->cta_done = 0;
-    c->tph[6] = globaltimer();
-  }
+  if (tid == 0) c->cta_done = 0;
+finalize:
+  if (tid == 0) c->tph[6] = globaltimer();
   if (with_finalize) {
     if (use_state_out) {
       out_dom = st.out + 1;

@@ -52,7 +52,7 @@ constexpr uint32_t kInvBit = 1u << 31;        //   group uses the Δ-branch (com
 // in its own 128-byte line, and the generation word in another.
 constexpr int kBarGroups = 16;
 constexpr int kBarLine = 32;                              // uint32 words per 128-byte line
-constexpr int kBarWords = (kBarGroups + 2) * kBarLine;
+constexpr int kBarWords = (kBarGroups + 3) * kBarLine;   // + one line for the leader's mode word
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;   // chained-scan tile status
 constexpr unsigned long long kFlagPre = 2ull << 62;
