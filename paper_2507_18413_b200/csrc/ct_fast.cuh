@@ -762,6 +762,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       if (t0) c->tph[4] = globaltimer();
       FAST_TRACE(6);
       if (mode == 1) {
+        if (t0) c->tph[5] = globaltimer();   // no scan phase
         if (tid == 0) fs.last = leader;
         __syncthreads();
         if (!fs.last) return;   // the leader finalizes

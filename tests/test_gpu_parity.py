@@ -304,6 +304,56 @@ def test_wide_forced_random(knob):
     tab.close()
 
 
+# --------------------------------------------------------------------------- launch-shape boundaries
+@pytest.mark.parametrize("t,expect", [(8192 * 128, "k_small"), (8192 * 128 + 1, "k_fast")])
+def test_boundary_small_vs_fast(t, expect):
+    """W2 = 8192 blocks is the last table of the one-CTA shape; one tuple more
+    takes the cooperative grid."""
+    p = random_table(3, 6, t, seed=61)
+    tab = make(p)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == expect
+    run_walk(tab, p, calls=25, seed=62, check_table_every=6)
+    tab.close()
+
+
+@pytest.mark.parametrize("d,expect", [(2048, "k_fast"), (2049, "k_fused")])
+def test_boundary_fast_rows(d, expect):
+    """k_fast keeps the per-CTA lists in shared memory up to R = 4096 rows."""
+    p = random_table(2, d, 1_200_000 + 3, seed=63)
+    tab = make(p)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == expect
+    run_walk(tab, p, calls=25, seed=64, check_table_every=6)
+    tab.close()
+
+
+@pytest.mark.parametrize("d,expect", [(1023, "k_small"), (1024, "k_wide")])
+def test_boundary_wide_rows(d, expect):
+    """k_wide takes over from k_small at R = 2048 support rows."""
+    p = random_table(2, d, 300_000 + 9, seed=65)
+    tab = make(p)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == expect
+    run_walk(tab, p, calls=40, seed=66, check_table_every=8)
+    tab.close()
+
+
+def test_fast_ranges_beyond_one_pass():
+    """A table whose index exceeds 148 SMs x 6 CTAs x 128 entries: every k_fast
+    CTA walks its range in several passes (W2 = 125 000 blocks)."""
+    p = random_table(2, 8, 16_000_000, seed=67)
+    tab = make(p)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == "k_fast"
+    assert (p.t + 127) // 128 > tab.info.grid * 128
+    run_walk(tab, p, calls=8, seed=68, check_table_every=4)
+    tab.close()
+
+
+def test_batch_single_state():
+    p = random_table(4, 12, 30_000, seed=69)
+    tab = make(p)
+    batch_walk(tab, p, S=1, steps=6, seed=70, check_table=True)
+    tab.close()
+
+
 # --------------------------------------------------------------------------- edge cases
 def test_empty_table_root_fail():
     tab = Table([0, 0], [3, 3], np.zeros((0, 2), np.int32))
