@@ -273,6 +273,19 @@ typedef struct ct_search_stats {
  * restored to what it was before the call. */
 ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
                           int32_t *out_solution, ct_search_stats *out_stats);
+/* The same search with an explicit driver: 0 = device-resident (the whole DFS
+ * in one cooperative kernel: decisions, trail snapshots of all table states,
+ * fixpoints and backtracking stay on the GPU; falls back to the host driver if
+ * the trail would exceed 512 levels or the model has a push pending), 1 =
+ * host-driven (one fixpoint launch per node).  Identical results and node
+ * traces; ct_model_search uses driver 0 (environment CT_HOST_DFS=1: 1).
+ * device_ms is then the whole kernel's time. */
+ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
+                             int32_t driver, int32_t *out_solution, ct_search_stats *out_stats);
+/* Measurement only: ns the last device-resident search spent in each phase,
+ * out6 = {ingest, update, probe, scan, finalize, trail copies} (block 0's
+ * clock, barriers included); -1 if no device search ran. */
+ct_status ct_model_search_phases(const ct_model *m, int64_t *out6);
 void ct_model_destroy(ct_model *m);
 
 /* ---------------------------------------------------------------- introspection */

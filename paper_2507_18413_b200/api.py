@@ -180,8 +180,10 @@ class Model:
     def pop(self):
         C.ct_model_pop(self.handle)
 
-    def search(self, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1):
-        return C.ct_model_search(self.handle, int(self.var_size.size), value_order, max_nodes, max_solutions)
+    def search(self, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1, driver=None):
+        """driver: None (library default: device-resident DFS), "device" or "host"."""
+        d = {None: None, "device": 0, "host": 1}[driver]
+        return C.ct_model_search(self.handle, int(self.var_size.size), value_order, max_nodes, max_solutions, d)
 
     def close(self):
         if getattr(self, "handle", None):

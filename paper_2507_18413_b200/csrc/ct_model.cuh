@@ -10,7 +10,7 @@
 // scope lost no value since its last run is a no-op; the loop stops when every
 // table is a no-op (greatest common fixpoint, unique -- SURVEY Q22) or one fails.
 #pragma once
-#include "ct_kernels.cuh"
+#include "ct_fast.cuh"
 
 namespace ctk {
 
@@ -25,8 +25,11 @@ struct ModelCtl {
   int32_t status;
   long long table_calls;         // non-no-op table propagations in the last fixpoint
   unsigned long long t0, t1;     // %globaltimer at start / end
-  int32_t pad[16];
+  unsigned long long ph[6];      // device search: ns in ingest, update, probe, scan, finalize, trail copies
+  int32_t changed[2];            // the shared domains lost a value in the iteration, by parity
+  int32_t pad[2];
 };
+static_assert(sizeof(ModelCtl) <= 256, "ModelCtl must fit its 256-byte slot");
 
 struct ModelDev {
   int32_t ntab, Wg;
@@ -34,21 +37,69 @@ struct ModelDev {
   const StateDev *sts;    // [ntab]
   uint64_t *gdom;         // [Wg] shared domains
   ModelCtl *mc;
+  uint32_t *bar;          // [kBarWords] grid barrier (k_fast's), zeroed at creation
 };
 
-__device__ __forceinline__ void model_barrier(ModelCtl *mc) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t gen = ld_acquire_u32(&mc->bar_gen);
-    __threadfence();
-    if (atomicAdd(&mc->bar_count, 1u) == gridDim.x - 1) {
-      mc->bar_count = 0;
-      __threadfence();
-      atomicAdd(&mc->bar_gen, 1u);
-    } else {
-      while (ld_acquire_u32(&mc->bar_gen) == gen) __nanosleep(20);
+// k_fast's grid barrier (one acq_rel arrival counter, per-group generation copies)
+#define model_barrier(mc) fast_grid_barrier(md.bar)
+
+// probe_item with the residue probe and the first round of the scan issued
+// together (one round trip for most items instead of two).
+__device__ __forceinline__ void probe_item_fused(const TableDev &tb, const StateDev &st, const FiltParams &f,
+                                                 int item, uint32_t &n_loads) {
+  const int lane = threadIdx.x & 31;
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  const int row = __ldcg(st.items + item);
+  const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+  const int r = (tb.use_res && lane == 0) ? st.res[row] : -1;
+  const int L1 = min(f.L, 32 * kScanUnroll);   // the first round
+  int pid[kScanUnroll];
+#pragma unroll
+  for (int q = 0; q < kScanUnroll; ++q) {
+    const int k = q * 32 + lane;
+    pid[q] = f.idx ? f.idx[k < L1 ? k : 0] : (k < L1 ? k : 0);
+  }
+  const int rr = r >= 0 ? r : pid[0];
+  const ulonglong2 tr = __ldcg(T2 + rr), sr = ld_sup2(srow + 2 * (int64_t)rr);
+  ulonglong2 t[kScanUnroll], sv[kScanUnroll];
+#pragma unroll
+  for (int q = 0; q < kScanUnroll; ++q) {
+    t[q] = __ldcg(T2 + pid[q]);
+    sv[q] = ld_sup2(srow + 2 * (int64_t)pid[q]);
+  }
+  n_loads += 2 * L1;
+  if (__any_sync(0xffffffffu, r >= 0 && ((tr.x & sr.x) | (tr.y & sr.y)) != 0)) {
+    if (lane == 0) st.sup[row] = 1;
+    return;
+  }
+  int hit = -1;
+#pragma unroll
+  for (int q = kScanUnroll - 1; q >= 0; --q) {
+    const bool in = q * 32 + lane < L1;
+    const unsigned b = __ballot_sync(0xffffffffu, in && ((t[q].x & sv[q].x) | (t[q].y & sv[q].y)) != 0);
+    if (b) hit = __shfl_sync(0xffffffffu, pid[q], __ffs(b) - 1);
+  }
+  if (hit < 0 && f.L > L1) hit = scan_pairs(f.idx, T2, srow, L1, min(f.L, kFirstScan), nullptr, lane, n_loads);
+  if (lane == 0) {
+    if (hit >= 0) {
+      st.sup[row] = 1;
+      st.res[row] = hit;
+    } else if (f.L > kFirstScan) {
+      st.scanlist[atomicAdd(&st.ctl->nscan, 1)] = row;
     }
-    __threadfence();
+  }
+}
+
+// Exclusive prefix of the per-table unit counts (thread 0, shared memory only),
+// then a block barrier.
+__device__ __forceinline__ void model_prefix(const int64_t *cnt, int64_t *pre, int ntab) {
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int k = 0; k < ntab; ++k) {
+      pre[k] = acc;
+      acc += cnt[k];
+    }
+    pre[ntab] = acc;
   }
   __syncthreads();
 }
@@ -60,43 +111,40 @@ __device__ __forceinline__ int find_table(const int64_t *pre, int ntab, int64_t 
   return k;
 }
 
-// grid <= co-resident blocks (cooperative), kFusedTPB threads, dynamic smem =
-// max over tables of ingest/finalize smem.  gdom_in (nullable, may be host
-// mapped): new shared domains for this node (a search decision).  out (may be
-// host mapped): [0] status (int32, written last), [1] Jacobi iterations,
-// [2] non-no-op table propagations, [3] kernel ns, [4 ..) shared domains.
-__global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, const uint64_t *__restrict__ gdom_in,
-                                                                 uint64_t *__restrict__ out, int max_iters) {
-  extern __shared__ __align__(16) uint64_t smem[];
+// The Jacobi fixpoint of the model from the current shared domains (md.gdom,
+// already set and visible: the caller ends its set-up with a grid barrier, and
+// block 0 has reset the control fields).  Every CTA of the cooperative grid
+// calls it; it returns after a final grid barrier with mc->fail set iff some
+// table failed.  Dynamic smem: max over tables of ingest/finalize smem.
+__device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *smem) {
   ModelCtl *mc = md.mc;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int gw = blockIdx.x * (kFusedTPB / 32) + (tid >> 5), nw = gridDim.x * (kFusedTPB / 32);
   __shared__ UpdParams s_up[kMaxModelTables];
   __shared__ FiltParams s_fp[kMaxModelTables];
   __shared__ int64_t s_pre[kMaxModelTables + 1];
+  __shared__ int64_t s_cnt[kMaxModelTables];
   __shared__ int s_tile;
   __shared__ uint32_t s_woff[kUpdTPB / 32];
   __shared__ uint32_t s_excl;
   __shared__ int s_brk;
   const int ntab = md.ntab;
-
-  if (blockIdx.x == 0) {
-    if (gdom_in)
-      for (int w = tid; w < md.Wg; w += kFusedTPB) md.gdom[w] = gdom_in[w];
-    if (tid == 0) {
-      mc->t0 = globaltimer();
-      mc->fail = 0;
-      mc->iters = 0;
-      mc->table_calls = 0;
-      mc->active[0] = mc->active[1] = 0;
-      mc->tile_ctr = 0;
+  const bool t0 = blockIdx.x == 0 && tid == 0;
+  unsigned long long tp = t0 ? globaltimer() : 0ull;
+  auto lap = [&](int i) {
+    if (t0) {
+      const unsigned long long t = globaltimer();
+      mc->ph[i] += t - tp;
+      tp = t;
     }
-  }
-  model_barrier(mc);
+  };
 
   for (int it = 0; it < max_iters; ++it) {
     // ---- ingest (a2): one block per table, removals = values the shared domains lost
-    if (blockIdx.x == 0 && tid == 0) mc->active[(it + 1) & 1] = 0;
+    if (blockIdx.x == 0 && tid == 0) {
+      mc->active[(it + 1) & 1] = 0;
+      mc->changed[it & 1] = 0;
+    }
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       dev_ingest<kFusedTPB>(md.tabs[k], md.sts[k], nullptr, 0, smem, md.gdom);
       __syncthreads();
@@ -107,6 +155,7 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
       }
     }
     model_barrier(mc);
+    lap(0);
     if (tid == 0) s_brk = __ldcg(&mc->fail) || __ldcg(&mc->active[it & 1]) == 0;
     __syncthreads();
     if (s_brk) break;
@@ -115,16 +164,13 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
       mc->table_calls += __ldcg(&mc->active[it & 1]);
     }
     // ---- update (a3-a5): tiles of all tables pooled over the grid
-    if (tid == 0) {
-      int64_t acc = 0;
-      for (int k = 0; k < ntab; ++k) {
-        s_up[k] = load_upd_params(md.sts[k].ctl);
-        s_pre[k] = acc;
-        acc += s_up[k].go ? s_up[k].ntiles : 0;
-      }
-      s_pre[ntab] = acc;
+    // (every table's parameters loaded by its own thread: one round trip)
+    if (tid < ntab) {
+      s_up[tid] = load_upd_params(md.sts[tid].ctl);
+      s_cnt[tid] = s_up[tid].go ? s_up[tid].ntiles : 0;
     }
     __syncthreads();
+    model_prefix(s_cnt, s_pre, ntab);
     {
       uint32_t n_loads = 0, n_writes = 0;
       while (true) {
@@ -137,38 +183,45 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
       }
     }
     model_barrier(mc);
+    lap(1);
     if (blockIdx.x == 0 && tid == 0) mc->tile_ctr = 0;
     // ---- probe (a6a): items of all tables pooled over the warps
-    if (tid == 0) {
-      int64_t acc = 0;
-      for (int k = 0; k < ntab; ++k) {
-        s_fp[k] = load_filt_params(md.tabs[k], md.sts[k]);
-        s_pre[k] = acc;
-        acc += (s_fp[k].go && s_fp[k].Lout > 0) ? s_fp[k].nitems : 0;
-      }
-      s_pre[ntab] = acc;
+    if (tid < ntab) {
+      s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
+      s_cnt[tid] = (s_fp[tid].go && s_fp[tid].Lout > 0) ? s_fp[tid].nitems : 0;
     }
     __syncthreads();
+    model_prefix(s_cnt, s_pre, ntab);
     if (blockIdx.x == 0 && tid < ntab && s_fp[tid].go) md.sts[tid].sup[md.tabs[tid].R] = s_fp[tid].Lout > 0;
     {
       uint32_t n_loads = 0;
       for (int64_t g = gw; g < s_pre[ntab]; g += nw) {
         const int k = find_table(s_pre, ntab, g);
-        probe_item(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads);
+        probe_item_fused(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads);
       }
     }
-    model_barrier(mc);
+    // the barrier's last arrival checks whether any table queued a miss; if
+    // none did, every CTA skips the scan phase and its barrier
+    {
+      int leader = 0;
+      const int mode = fast_grid_barrier_mode(
+          md.bar,
+          [&] {
+            int any = 0;
+            for (int k = 0; k < ntab && !any; ++k) any = __ldcg(&md.sts[k].ctl->nscan) > 0;
+            return any ? 0 : 1;
+          },
+          leader, &s_brk);
+      lap(2);
+      if (mode == 1) goto finalize_phase;
+    }
     // ---- scan (a6b): misses x chunks of all tables pooled over the warps
-    if (tid == 0) {
-      int64_t acc = 0;
-      for (int k = 0; k < ntab; ++k) {
-        s_fp[k] = load_filt_params(md.tabs[k], md.sts[k]);
-        s_pre[k] = acc;
-        acc += scan_units(s_fp[k]);
-      }
-      s_pre[ntab] = acc;
+    if (tid < ntab) {
+      s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
+      s_cnt[tid] = scan_units(s_fp[tid]);
     }
     __syncthreads();
+    model_prefix(s_cnt, s_pre, ntab);
     {
       uint32_t n_loads = 0;
       for (int64_t g = gw; g < s_pre[ntab]; g += nw) {
@@ -177,6 +230,8 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
       }
     }
     model_barrier(mc);
+    lap(3);
+  finalize_phase:
     // ---- finalize (a6c-a7): one block per table; AND the new domains into the shared ones
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const TableDev &tb = md.tabs[k];
@@ -189,17 +244,54 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
         for (int w = tid; w < tb.Wd; w += kFusedTPB) {
           const uint64_t nd = __ldcg(st.dom + w);
           const uint64_t g0 = __ldcg(md.gdom + tb.gword[w]);
-          if ((g0 & nd) != g0) atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + tb.gword[w]), nd);
+          if ((g0 & nd) != g0) {
+            const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + tb.gword[w]), nd);
+            if ((old & nd) != old) mc->changed[it & 1] = 1;
+          }
         }
       }
       __syncthreads();
     }
     model_barrier(mc);
-    if (tid == 0) s_brk = __ldcg(&mc->fail);
+    lap(4);
+    // stop on a failure, or at the fixpoint: no table removed a value from the
+    // shared domains, so every table is a no-op in the next iteration
+    if (tid == 0) s_brk = __ldcg(&mc->fail) || !__ldcg(&mc->changed[it & 1]);
     __syncthreads();
     if (s_brk) break;
   }
   model_barrier(mc);
+}
+
+// Block 0: reset the per-fixpoint control fields (before a grid barrier).
+__device__ __forceinline__ void model_reset_ctl(ModelCtl *mc) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    mc->fail = 0;
+    mc->iters = 0;
+    mc->table_calls = 0;
+    mc->active[0] = mc->active[1] = 0;
+    mc->tile_ctr = 0;
+  }
+}
+
+// grid <= co-resident blocks (cooperative), kFusedTPB threads, dynamic smem =
+// max over tables of ingest/finalize smem.  gdom_in (nullable, may be host
+// mapped): new shared domains for this node (a search decision).  out (may be
+// host mapped): [0] status (int32, written last), [1] Jacobi iterations,
+// [2] non-no-op table propagations, [3] kernel ns, [4 ..) shared domains.
+__global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, const uint64_t *__restrict__ gdom_in,
+                                                                 uint64_t *__restrict__ out, int max_iters) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  ModelCtl *mc = md.mc;
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0) {
+    if (gdom_in)
+      for (int w = tid; w < md.Wg; w += kFusedTPB) md.gdom[w] = gdom_in[w];
+    if (tid == 0) mc->t0 = globaltimer();
+  }
+  model_reset_ctl(mc);
+  model_barrier(mc);
+  model_fixpoint_dev(md, max_iters, smem);
   if (blockIdx.x == 0) {
     const int status = __ldcg(&mc->fail) ? 1 : 0;
     if (status == 0)
@@ -215,7 +307,232 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_fixpoint(ModelDev md, co
     __syncthreads();
     if (tid == 0) *reinterpret_cast<int32_t *>(out) = status;
   }
-  (void)lane;
+}
+
+// ------------------------------------------------------------------ device-resident DFS (config 5)
+// The whole search in ONE cooperative launch: binary branching x = v / x != v,
+// input_order (lowest-index unbound variable), indomain_max / indomain_min
+// (SPEC S:L391), each node propagated to the common
+// fixpoint with model_fixpoint_dev.  The trail is a snapshot of the state pool
+// per level (all table states + shared domains), copied by the whole grid.
+// Every CTA runs the same control flow (it depends only on the shared domains
+// and the fixpoint verdicts, both read after grid barriers), so no decision
+// has to be broadcast; block 0 thread 0 keeps the statistics, the trace hash
+// (FNV-1a over (depth, var, value, branch, status), as the host driver) and
+// the last solution.
+constexpr int kSearchMaxLevels = 512;
+
+struct SearchDev {
+  uint4 *pool;                 // state pool, pool16 16-byte words
+  int64_t pool16;
+  uint4 *snaps;                // [levels][pool16]
+  int32_t levels;
+  const int32_t *gOff;         // [nv + 1] first shared-domain word of each variable
+  const int32_t *vlo;          // [nv]
+  int32_t nv, value_order;
+  int64_t max_nodes, max_solutions;
+  long long *out;              // [0] status (last), [1] nodes, [2] failures, [3] solutions, [4] table calls,
+                               // [5] iterations, [6] max depth, [7] device ns, [8] trace hash,
+                               // [9] error (1: deeper than `levels`), [10..15] ns per phase (ingest,
+                               // update, probe, scan, finalize, trail copies), [16 ..) last solution (nv)
+};
+
+__device__ __forceinline__ void search_copy(uint4 *dst, const uint4 *src, int64_t n16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) dst[i] = __ldcg(src + i);
+}
+
+struct SearchFrame {
+  int32_t x, a, branch, pad;
+};
+
+// Control state of the search, one copy per CTA (identical in every CTA).
+struct SearchCtl {
+  int state, d, x, a, fail, err;
+  long long nodes, failures, solutions, calls, iters, maxd;
+  unsigned long long hash;
+};
+
+enum { kSExpand = 0, kSBranch = 1, kSPop = 2, kSReturn = 3, kSDone = 4 };
+
+__device__ __forceinline__ void search_fnv(unsigned long long &h, unsigned long long v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= 1099511628211ull;
+  }
+}
+
+// thread 0: count one fixpoint node (same fields and hash as the host driver)
+__device__ __forceinline__ void search_account(SearchCtl &c, const ModelCtl *mc, int depth, int var, int val,
+                                               int branch, int fail) {
+  c.nodes++;
+  if (fail) c.failures++;
+  c.calls += __ldcg(&mc->table_calls);
+  c.iters += __ldcg(&mc->iters);
+  if (depth > c.maxd) c.maxd = depth;
+  search_fnv(c.hash, (unsigned long long)depth);
+  search_fnv(c.hash, (unsigned long long)(long long)var);
+  search_fnv(c.hash, (unsigned long long)(long long)val);
+  search_fnv(c.hash, (unsigned long long)branch);
+  search_fnv(c.hash, (unsigned long long)(fail ? 1 : 0));
+}
+
+// grid <= co-resident blocks (cooperative; same geometry as k_model_fixpoint),
+// kFusedTPB threads, dynamic smem = max(fixpoint smem, 8 * Wg).
+__global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, SearchDev sd) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ SearchFrame fr[kSearchMaxLevels];
+  __shared__ SearchCtl c;
+  ModelCtl *mc = md.mc;
+  const int tid = threadIdx.x;
+  const unsigned long long t_start = globaltimer();
+  // one fixpoint from the current shared domains; every CTA gets the verdict
+  auto fixpoint = [&]() {
+    model_reset_ctl(mc);
+    model_barrier(mc);
+    model_fixpoint_dev(md, 1 << 20, smem);
+    if (tid == 0) c.fail = __ldcg(&mc->fail);
+    __syncthreads();
+  };
+  if (blockIdx.x == 0 && tid == 0)
+    for (int i = 0; i < 6; ++i) mc->ph[i] = 0;
+  if (tid == 0) {
+    c.d = 0;
+    c.err = 0;
+    c.nodes = c.failures = c.solutions = c.calls = c.iters = c.maxd = 0;
+    c.hash = 1469598103934665603ull;
+  }
+  // the root: trail level 0, fixpoint of the current domains
+  search_copy(sd.snaps, sd.pool, sd.pool16);
+  fixpoint();
+  if (tid == 0) {
+    search_account(c, mc, 0, -1, 0, 2, c.fail);
+    c.state = c.fail ? kSDone : kSExpand;
+  }
+  __syncthreads();
+  while (c.state != kSDone) {
+    const int state = c.state;
+    if (state == kSExpand) {
+      // the node at depth d is an OK fixpoint: pick x (input_order) and a
+      // (indomain_max / min); the shared domains go to shared memory first
+      for (int w = tid; w < md.Wg; w += kFusedTPB) smem[w] = __ldcg(md.gdom + w);
+      __syncthreads();
+      if (tid == 0) {
+        int x = -1, a = -1;
+        for (int v = 0; v < sd.nv && x < 0; ++v) {
+          int cnt = 0;
+          for (int w = sd.gOff[v]; w < sd.gOff[v + 1]; ++w) cnt += __popcll(smem[w]);
+          if (cnt > 1) x = v;
+        }
+        if (x >= 0) {
+          if (sd.value_order == 0) {
+            for (int w = sd.gOff[x + 1] - 1; w >= sd.gOff[x] && a < 0; --w)
+              if (smem[w]) a = (w - sd.gOff[x]) * 64 + 63 - __clzll(smem[w]);
+          } else {
+            for (int w = sd.gOff[x]; w < sd.gOff[x + 1] && a < 0; ++w)
+              if (smem[w]) a = (w - sd.gOff[x]) * 64 + __ffsll(smem[w]) - 1;
+          }
+          if (c.d + 1 >= sd.levels) {   // the trail is full: report, stop
+            c.err = 1;
+            c.state = kSDone;
+          } else {
+            fr[c.d].x = x;
+            fr[c.d].a = a;
+            fr[c.d].branch = 0;
+            c.state = kSBranch;
+          }
+        } else {   // every variable bound: a solution
+          c.solutions++;
+          if (blockIdx.x == 0)
+            for (int v = 0; v < sd.nv; ++v) {
+              int av = 0;
+              for (int w = sd.gOff[v]; w < sd.gOff[v + 1]; ++w)
+                if (smem[w]) av = (w - sd.gOff[v]) * 64 + __ffsll(smem[w]) - 1;
+              sd.out[16 + v] = sd.vlo[v] + av;
+            }
+          c.state = (sd.max_solutions > 0 && c.solutions >= sd.max_solutions) ? kSDone : kSReturn;
+        }
+      }
+      __syncthreads();
+    } else if (state == kSBranch) {
+      const SearchFrame f = fr[c.d];
+      if (f.branch == 2) {
+        if (tid == 0) c.state = kSReturn;
+        __syncthreads();
+        continue;
+      }
+      if (sd.max_nodes > 0 && c.nodes >= sd.max_nodes) {
+        if (tid == 0) c.state = kSDone;
+        __syncthreads();
+        continue;
+      }
+      // push: trail level d + 1 = the state before this branch
+      const unsigned long long tc = globaltimer();
+      search_copy(sd.snaps + (int64_t)(c.d + 1) * sd.pool16, sd.pool, sd.pool16);
+      model_barrier(mc);   // the snapshot is complete before the domains change
+      if (blockIdx.x == 0 && tid == 0) mc->ph[5] += globaltimer() - tc;
+      // block 0 applies the decision to the shared domains (visible to all
+      // after the fixpoint's opening barrier)
+      if (blockIdx.x == 0) {
+        const int w0 = sd.gOff[f.x], w1 = sd.gOff[f.x + 1];
+        const int wa = w0 + f.a / 64;
+        const uint64_t bit = 1ull << (f.a % 64);
+        for (int w = w0 + tid; w < w1; w += kFusedTPB) {
+          const uint64_t dw = md.gdom[w];
+          md.gdom[w] = f.branch == 0 ? (w == wa ? bit : 0ull) : (w == wa ? dw & ~bit : dw);
+        }
+      }
+      fixpoint();
+      if (tid == 0) {
+        search_account(c, mc, c.d + 1, f.x, sd.vlo[f.x] + f.a, f.branch, c.fail);
+        if (!c.fail) {
+          c.d += 1;
+          c.state = kSExpand;
+        } else {
+          c.state = kSPop;
+        }
+      }
+      __syncthreads();
+    } else if (state == kSPop) {
+      // restore the state before the branch, then the next branch
+      const unsigned long long tc = globaltimer();
+      search_copy(sd.pool, sd.snaps + (int64_t)(c.d + 1) * sd.pool16, sd.pool16);
+      model_barrier(mc);
+      if (blockIdx.x == 0 && tid == 0) mc->ph[5] += globaltimer() - tc;
+      if (tid == 0) {
+        fr[c.d].branch += 1;
+        c.state = kSBranch;
+      }
+      __syncthreads();
+    } else {   // kSReturn: the node at depth d is done
+      if (tid == 0) {
+        if (c.d == 0) {
+          c.state = kSDone;
+        } else {
+          c.d -= 1;
+          c.state = kSPop;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // leave the model as it was before the search (trail level 0)
+  search_copy(sd.pool, sd.snaps, sd.pool16);
+  model_barrier(mc);
+  if (blockIdx.x == 0 && tid == 0) {
+    sd.out[1] = c.nodes;
+    sd.out[2] = c.failures;
+    sd.out[3] = c.solutions;
+    sd.out[4] = c.calls;
+    sd.out[5] = c.iters;
+    sd.out[6] = c.maxd;
+    sd.out[7] = (long long)(globaltimer() - t_start);
+    sd.out[8] = (long long)c.hash;
+    sd.out[9] = c.err;
+    for (int i = 0; i < 6; ++i) sd.out[10 + i] = (long long)mc->ph[i];
+    __threadfence_system();
+    sd.out[0] = c.err ? -1 : (c.solutions > 0 ? 0 : 1);
+  }
 }
 
 }  // namespace ctk

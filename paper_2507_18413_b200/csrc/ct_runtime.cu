@@ -1345,6 +1345,13 @@ struct ct_model {
   std::vector<uint64_t> dom;      // host mirror of the shared domains
   // last fixpoint's counters
   int64_t last_iters = 0, last_calls = 0, last_ns = 0;
+  // device-resident search (k_model_search), set up on first use
+  uint4 *snap_dev = nullptr;
+  int levels = 0;
+  int32_t *d_goff = nullptr, *d_vlo = nullptr;
+  long long *h_sout = nullptr, *d_sout = nullptr;   // mapped [16 + nv]
+  int sgrid = 0;
+  size_t ssmem = 0;
 };
 
 static void model_free(ct_model *m) {
@@ -1352,6 +1359,9 @@ static void model_free(ct_model *m) {
   DeviceGuard g(m->device);
   if (m->stream) cudaStreamSynchronize(m->stream);
   for (char *sn : m->snaps) cudaFree(sn);
+  if (m->snap_dev) cudaFree(m->snap_dev);
+  if (m->d_goff) cudaFree(m->d_goff);
+  if (m->h_sout) cudaFreeHost(m->h_sout);
   if (m->pool) cudaFree(m->pool);
   if (m->meta) cudaFree(m->meta);
   if (m->h_in) cudaFreeHost(m->h_in);
@@ -1505,7 +1515,8 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   const size_t tdev = sizeof(TableDev) * n_tables, sdev = sizeof(StateDev) * n_tables;
   size_t gw_total = 0;
   for (ct_table *t : m->tabs) gw_total += (size_t)std::max(t->Wd, 1);
-  m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + gw_total * 4;
+  m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + round_up((int64_t)gw_total * 4, 256) +
+                  (size_t)kBarWords * 4;
   if (cudaMalloc(&m->meta, m->meta_bytes) != cudaSuccess) return bail(fail(CT_ENOMEM, "model metadata allocation failed"));
   cudaMemset(m->meta, 0, m->meta_bytes);
   TableDev *d_tabs = (TableDev *)m->meta;
@@ -1537,6 +1548,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   m->md.sts = d_sts;
   m->md.gdom = (uint64_t *)(m->pool + m->gdom_off);
   m->md.mc = d_mc;
+  m->md.bar = (uint32_t *)((char *)d_gw + round_up((int64_t)gw_total * 4, 256));
   m->dom = gdom;
   // ---- launch geometry
   size_t smem = 0;
@@ -1712,10 +1724,112 @@ struct Dfs {
 };
 }  // namespace
 
+// Device-resident DFS: one cooperative launch (k_model_search).  Returns
+// CT_OK / CT_FAIL like the host driver or an error; *fallback = true if the
+// host driver must run instead (trail too short, no memory for it).
+static ct_status model_search_device(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
+                                     int32_t *out_solution, ct_search_stats *out_stats, bool *fallback) {
+  *fallback = false;
+  DeviceGuard g(m->device);
+  const int64_t pool16 = (int64_t)((m->pool_bytes + 15) / 16);
+  if (!m->snap_dev) {
+    int64_t vals = 1;
+    for (int v = 0; v < m->nv; ++v) vals += m->vd[v];
+    m->levels = (int)std::min<int64_t>(kSearchMaxLevels, vals);
+    if (cudaMalloc(&m->snap_dev, (size_t)m->levels * pool16 * 16) != cudaSuccess) {
+      cudaGetLastError();
+      m->snap_dev = nullptr;
+      *fallback = true;
+      return CT_OK;
+    }
+    std::vector<int32_t> gv(m->gOff);
+    gv.insert(gv.end(), m->vlo.begin(), m->vlo.end());
+    CUDA_TRY(cudaMalloc(&m->d_goff, gv.size() * 4));
+    CUDA_TRY(cudaMemcpy(m->d_goff, gv.data(), gv.size() * 4, cudaMemcpyHostToDevice));
+    m->d_vlo = m->d_goff + m->gOff.size();
+    CUDA_TRY(cudaHostAlloc((void **)&m->h_sout, (size_t)(16 + m->nv) * 8, cudaHostAllocMapped));
+    CUDA_TRY(cudaHostGetDevicePointer((void **)&m->d_sout, m->h_sout, 0));
+    m->ssmem = std::max(m->smem, (size_t)m->Wg * 8);
+    CUDA_TRY(cudaFuncSetAttribute(k_model_search, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(m->ssmem, 1)));
+    int occ = 0, sms = 148;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_model_search, kFusedTPB, m->ssmem));
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device));
+    if (occ < 1) {
+      *fallback = true;
+      return CT_OK;
+    }
+    m->sgrid = std::min(m->grid, sms * occ);
+  }
+  SearchDev sd{};
+  sd.pool = reinterpret_cast<uint4 *>(m->pool);
+  sd.pool16 = pool16;
+  sd.snaps = m->snap_dev;
+  sd.levels = m->levels;
+  sd.gOff = m->d_goff;
+  sd.vlo = m->d_vlo;
+  sd.nv = m->nv;
+  sd.value_order = value_order;
+  sd.max_nodes = max_nodes;
+  sd.max_solutions = max_solutions;
+  sd.out = m->d_sout;
+  volatile long long *st = m->h_sout;
+  *st = kPendingStatus;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)m->sgrid);
+  lc.blockDim = dim3(kFusedTPB);
+  lc.dynamicSmemBytes = m->ssmem;
+  lc.stream = m->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&lc, k_model_search, m->md, sd));
+  CUDA_TRY(cudaStreamSynchronize(m->stream));
+  if (*st == kPendingStatus) return fail(CT_ECUDA, "device search ended without a status");
+  if (m->h_sout[9]) {   // deeper than the trail: the host driver takes over
+    *fallback = true;
+    return CT_OK;
+  }
+  ct_search_stats o{};
+  o.nodes = m->h_sout[1];
+  o.failures = m->h_sout[2];
+  o.solutions = m->h_sout[3];
+  o.table_calls = m->h_sout[4];
+  o.iterations = m->h_sout[5];
+  o.max_depth = m->h_sout[6];
+  o.device_ms = (double)m->h_sout[7] * 1e-6;
+  o.trace_hash = (uint64_t)m->h_sout[8];
+  if (out_stats) *out_stats = o;
+  if (o.solutions > 0 && out_solution)
+    for (int v = 0; v < m->nv; ++v) out_solution[v] = (int32_t)m->h_sout[16 + v];
+  return o.solutions > 0 ? CT_OK : CT_FAIL;
+}
+
+ct_status ct_model_search_phases(const ct_model *m, int64_t *out6) {
+  if (!m || !out6) return fail(CT_EINVAL, "NULL argument");
+  for (int i = 0; i < 6; ++i) out6[i] = m->h_sout ? (int64_t)m->h_sout[10 + i] : -1;
+  return CT_OK;
+}
+
 ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
                           int32_t *out_solution, ct_search_stats *out_stats) {
+  int driver = 0;
+  if (const char *ev = getenv("CT_HOST_DFS")) driver = atoi(ev) ? 1 : 0;
+  return ct_model_search_ex(m, value_order, max_nodes, max_solutions, driver, out_solution, out_stats);
+}
+
+ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
+                             int32_t driver, int32_t *out_solution, ct_search_stats *out_stats) {
   if (!m) return fail(CT_EINVAL, "NULL model");
   if (value_order < 0 || value_order > 1) return fail(CT_EINVAL, "value_order must be 0 (max) or 1 (min)");
+  if (driver == 0 && !m->dead && m->depth == 0) {
+    bool fallback = false;
+    const ct_status s = model_search_device(m, value_order, max_nodes, max_solutions, out_solution, out_stats,
+                                            &fallback);
+    if (!fallback) return s;
+  }
   Dfs d;
   d.m = m;
   d.value_order = value_order;

@@ -131,6 +131,8 @@ SIGNATURES = {
     "ct_model_push": (I32, [P]),
     "ct_model_pop": (I32, [P]),
     "ct_model_search": (I32, [P, I32, I64, I64, P, P]),
+    "ct_model_search_ex": (I32, [P, I32, I64, I64, I32, P, P]),
+    "ct_model_search_phases": (I32, [P, P]),
     "ct_model_destroy": (None, [P]),
     "ct_last_error": (ctypes.c_char_p, []),
     "ct_version": (ctypes.c_char_p, []),
@@ -471,13 +473,25 @@ def ct_model_pop(model) -> None:
     _check(lib().ct_model_pop(model), allow_fail=False)
 
 
-def ct_model_search(model, n_vars: int, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1):
-    """Returns (status, solution int32[n_vars] or None, ct_search_stats)."""
+def ct_model_search(model, n_vars: int, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1,
+                    driver: int | None = None):
+    """Returns (status, solution int32[n_vars] or None, ct_search_stats).
+    driver: None = library default (device-resident), 0 = device, 1 = host."""
     sol = np.zeros(n_vars, np.int32)
     stats = ct_search_stats()
-    st = _check(lib().ct_model_search(model, value_order, max_nodes, max_solutions, _np_ptr(sol),
-                                      ctypes.byref(stats)))
+    if driver is None:
+        st = _check(lib().ct_model_search(model, value_order, max_nodes, max_solutions, _np_ptr(sol),
+                                          ctypes.byref(stats)))
+    else:
+        st = _check(lib().ct_model_search_ex(model, value_order, max_nodes, max_solutions, int(driver),
+                                             _np_ptr(sol), ctypes.byref(stats)))
     return st, (sol if st == CT_OK else None), stats
+
+
+def ct_model_search_phases(model) -> dict:
+    out = np.zeros(6, np.int64)
+    _check(lib().ct_model_search_phases(model, _np_ptr(out)), allow_fail=False)
+    return dict(zip(("ingest", "update", "probe", "scan", "finalize", "trail"), (int(x) for x in out)))
 
 
 def ct_model_destroy(model) -> None:

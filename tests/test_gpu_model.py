@@ -20,7 +20,7 @@ def _model(m):
 def test_table1_model_first_solution():
     p = table1()
     M = Model(p.lo, p.d, [np.arange(3)], [p.tuples])
-    st, sol, stats = M.search(value_order=0, max_solutions=1)
+    st, sol, stats = M.search(value_order=0, max_solutions=1)   # device-resident driver
     assert st == CT_OK and sol.tolist() == [3, 4, 3]          # SPEC S:L394 (derived)
     ref = oracle_dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=1)
     assert (stats.nodes, stats.failures, stats.trace_hash) == (ref["nodes"], ref["failures"], ref["trace_hash"])
@@ -58,12 +58,13 @@ def test_random_model_fixpoints(seed):
     M.close()
 
 
+@pytest.mark.parametrize("driver", ["device", "host"])
 @pytest.mark.parametrize("seed", range(6))
-def test_search_all_solutions_matches_oracle(seed):
+def test_search_all_solutions_matches_oracle(seed, driver):
     m = csp_model(6, 5, 4, 40, seed=50 + seed, arities=[3, 3, 2, 4])
     M = _model(m)
     for vo in (0, 1):
-        st, sol, stats = M.search(value_order=vo, max_solutions=0)
+        st, sol, stats = M.search(value_order=vo, max_solutions=0, driver=driver)
         ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=vo, max_solutions=0)
         assert stats.solutions == len(ref["solutions"])
         assert (stats.nodes, stats.failures) == (ref["nodes"], ref["failures"])
@@ -78,8 +79,35 @@ def test_search_first_solution_config5_shape():
     table: the first 300 nodes' trace equals the oracle's."""
     m = csp_model(30, 40, 12, 20_000, seed=7)
     M = _model(m)
-    st, sol, stats = M.search(value_order=0, max_nodes=300, max_solutions=1)
-    ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=300, max_solutions=1)
-    assert (stats.nodes, stats.failures, stats.solutions) == (ref["nodes"], ref["failures"], len(ref["solutions"]))
-    assert stats.trace_hash == ref["trace_hash"]
+    for driver in ("device", "host"):
+        st, sol, stats = M.search(value_order=0, max_nodes=300, max_solutions=1, driver=driver)
+        ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=300, max_solutions=1)
+        assert (stats.nodes, stats.failures, stats.solutions) == (ref["nodes"], ref["failures"], len(ref["solutions"]))
+        assert stats.trace_hash == ref["trace_hash"]
+    M.close()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_device_and_host_drivers_agree(seed):
+    """The device-resident DFS and the host-driven one walk the same tree:
+    every counter, the trace hash and the solution agree, and the model is
+    left as it was (a fixpoint after the search equals one before it)."""
+    m = csp_model(10, 8, 6, 400, seed=80 + seed, arities=[3, 4, 2, 5, 3, 4])
+    M = _model(m)
+    if M.root_status != CT_OK:
+        M.close()
+        return
+    root = M.root_dom.copy()
+    for vo, mx_sol, mx_nodes in ((0, 0, 0), (1, 1, 0), (0, 0, 57)):
+        a = M.search(value_order=vo, max_solutions=mx_sol, max_nodes=mx_nodes, driver="device")
+        b = M.search(value_order=vo, max_solutions=mx_sol, max_nodes=mx_nodes, driver="host")
+        assert a[0] == b[0]
+        for f in ("nodes", "failures", "solutions", "table_calls", "iterations", "max_depth", "trace_hash"):
+            assert getattr(a[2], f) == getattr(b[2], f), f
+        if a[1] is not None:
+            assert np.array_equal(a[1], b[1])
+        M.push()
+        st, gd = M.fixpoint(None)
+        assert st == CT_OK and np.array_equal(gd, root)
+        M.pop()
     M.close()
