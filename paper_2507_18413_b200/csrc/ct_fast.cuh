@@ -46,13 +46,13 @@ namespace ctk {
 
 constexpr int kLocalRowsMax = 4096;                    // R limit of the per-CTA lists
 #ifndef CT_FAST_TPB
-#define CT_FAST_TPB 128
+#define CT_FAST_TPB 256
 #endif
 #ifndef CT_FAST_UNROLL
-#define CT_FAST_UNROLL 10
+#define CT_FAST_UNROLL 12
 #endif
 #ifndef CT_FAST_MINB
-#define CT_FAST_MINB 6
+#define CT_FAST_MINB 3
 #endif
 constexpr int kFastTPB = CT_FAST_TPB;                  // k_fast threads per CTA = index entries per tile
 constexpr int kFastWarps = kFastTPB / 32;
