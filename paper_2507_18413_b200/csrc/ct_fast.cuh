@@ -90,7 +90,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int NW>
 struct FastShT {
   int dead, fail, noop, go, ngroups, nrows, nitems;
-  int L, ident, par, Lout, nscan, last;
+  int L, ident, par, Lout, nscan, last, below;
   int red[NW];                   // block-reduction scratch
   uint32_t woff[NW];
   uint64_t scan[NW];
@@ -445,6 +445,40 @@ __device__ __forceinline__ bool fast_update_entry(const TableDev &tb, const Stat
   return (nt.x | nt.y) != 0;
 }
 
+// ------------------------------------------------------------------ a4: index entries of one CTA's range
+// The survivors of entries [k_lo, k_hi) go to the new index at positions
+// fs.below + rank (order-preserving: fs.below = survivors of all lower CTAs).
+__device__ __forceinline__ void fast_compact_range(const TableDev &tb, const StateDev &st, FastSh &fs, int k_lo,
+                                                   int k_hi) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  int32_t *__restrict__ idx_out = fs.par ? st.idx0 : st.idx1;
+  int below = fs.below;
+  for (int base = k_lo; base < k_hi; base += kFastTPB) {
+    const int k = base + tid;
+    int pid = 0;
+    bool keep = false;
+    if (k < k_hi) {
+      pid = fs.ident ? k : idx_in[k];
+      const ulonglong2 t = __ldcg(T2 + pid);
+      keep = (t.x | t.y) != 0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncthreads();
+    if (lane == 0) fs.woff[warp] = __popc(bal);
+    __syncthreads();
+    uint32_t off = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kFastWarps; ++w) {
+      if (w < warp) off += fs.woff[w];
+      all += fs.woff[w];
+    }
+    if (keep) idx_out[below + off + __popc(bal & lanemask_lt())] = pid;
+    below += (int)all;
+  }
+}
+
 // ------------------------------------------------------------------ a6a: probe of one row
 // Alg. 3 L3 for one (x,a) by a warp: is some block b with T[b] & S[x,a][b] != 0?
 // Lane 0's residue block r (L220; -1 = none) is tested together with the first
@@ -610,6 +644,8 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     for (int i = 1; i < 6; ++i) c->tph[i] = t;
   }
 
+  bool compact_after = false;   // the leader of a no-miss call writes its index entries after finalizing
+  int leader_k_lo = 0, leader_k_hi = 0;
   if (fs.go) {
     uint32_t *__restrict__ tcnt = reinterpret_cast<uint32_t *>(st.tilestat);
     // ---- update (a3): CTA c owns index entries [c·ts, (c+1)·ts), ts = ceil(L / G)
@@ -657,7 +693,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     if (t0) c->tph[2] = globaltimer();
     FAST_TRACE(3);
 
-    // ---- compaction (a4): L_out and this CTA's prefix from the per-CTA counts
+    // ---- compaction (a4), part A: L_out and this CTA's prefix from the
+    // per-CTA counts (the index entries themselves are written later, off the
+    // critical path of a call without probe misses)
     {
       int tot = 0, below = 0;
       for (int j = tid; j < G; j += kFastTPB) {
@@ -669,31 +707,8 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       below = fast_block_sum(below, fs);
       if (tid == 0) {
         fs.Lout = tot;
+        fs.below = below;
         if (blockIdx.x == 0) c->L_out = tot;
-      }
-      const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
-      int32_t *__restrict__ idx_out = fs.par ? st.idx0 : st.idx1;
-      for (int base = k_lo; base < k_hi; base += kFastTPB) {
-        const int k = base + tid;
-        int pid = 0;
-        bool keep = false;
-        if (k < k_hi) {
-          pid = fs.ident ? k : idx_in[k];
-          const ulonglong2 t = __ldcg(T2 + pid);
-          keep = (t.x | t.y) != 0;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        __syncthreads();
-        if (lane == 0) fs.woff[warp] = __popc(bal);
-        __syncthreads();
-        uint32_t off = 0, all = 0;
-#pragma unroll
-        for (int w = 0; w < kFastWarps; ++w) {
-          if (w < warp) off += fs.woff[w];
-          all += fs.woff[w];
-        }
-        if (tb.use_index && keep) idx_out[below + off + __popc(bal & lanemask_lt())] = pid;
-        below += (int)all;
       }
     }
     __syncthreads();
@@ -754,7 +769,8 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     f_loads = 0;
     // ---- scan (a6b): misses x chunks of the compacted index, from entry 0.
     // The barrier's last arrival knows every probe is done: with no miss it
-    // releases the others with mode 1 (they exit) and finalizes at once.
+    // releases the others with mode 1 (they write their index entries and
+    // exit) and finalizes at once, then writes its own entries.
     if (Lout > 0 && may_miss && kFastStop > -3) {
       int leader = 0;
       const int mode = fast_grid_barrier_mode(st.bar, [&] { return __ldcg(&c->nscan) == 0 ? 1 : 0; }, leader,
@@ -765,9 +781,18 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         if (t0) c->tph[5] = globaltimer();   // no scan phase
         if (tid == 0) fs.last = leader;
         __syncthreads();
-        if (!fs.last) return;   // the leader finalizes
+        if (!fs.last) {
+          if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
+          return;
+        }
+        compact_after = tb.use_index != 0;
+        leader_k_lo = k_lo;
+        leader_k_hi = k_hi;
         goto finalize;
       }
+      // misses: the whole new index first (the scans read it)
+      if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
+      fast_grid_barrier(st.bar);
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
@@ -837,6 +862,8 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         }
       }
     }
+    if (!(Lout > 0 && may_miss && kFastStop > -3) && tb.use_index && kFastStop == 0)
+      fast_compact_range(tb, st, fs, k_lo, k_hi);   // no scan phase: write the index now
     if (t0) c->tph[5] = globaltimer();
     FAST_TRACE(7);
     if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
@@ -869,6 +896,10 @@ finalize:
     cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
   }
   if (tid == 0) c->tph[7] = globaltimer();
+  if (compact_after) {   // the leader's own index entries, after the outputs
+    __syncthreads();
+    fast_compact_range(tb, st, fs, leader_k_lo, leader_k_hi);
+  }
 }
 
 }  // namespace ctk
