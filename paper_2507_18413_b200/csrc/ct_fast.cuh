@@ -67,6 +67,10 @@ constexpr int kFirstScanFast = 32 * kProbeUnroll;      // index entries per prob
 #endif
 constexpr int kScanFastU = CT_SCAN_U;                  // index entries per lane per scan unit
 constexpr int kFastChunk = 32 * kScanFastU;            // index entries per scan unit
+#ifndef CT_SCAN_GROUP
+#define CT_SCAN_GROUP 8
+#endif
+constexpr int kScanGroup = CT_SCAN_GROUP;              // probe misses per scan unit (<= 32)
 constexpr int kSelfRounds = (32 + kProbeUnroll - 1) / kProbeUnroll;   // probe rounds before a miss is queued (~1024 entries)
 #ifdef CT_FAST_STOP
 constexpr int kFastStop = CT_FAST_STOP;                // experiment builds only
@@ -386,6 +390,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
       c->L_in = fs.L;
       c->L_out = 0;
       c->nscan = 0;
+      c->tile_ctr = 0;   // k_fast: the scan's unit counter
       c->upd_loads = 0;
       c->upd_writes = 0;
       c->scan_loads = 0;
@@ -632,7 +637,6 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
   const FastPtrs p = fast_ptrs(smem, tb);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x;
-  const int gw = blockIdx.x * kFastWarps + warp, nw = G * kFastWarps;
   const bool t0 = blockIdx.x == 0 && tid == 0;
   // phase timestamps of block 0 go straight to tph[] (no registers held)
   if (t0) c->tph[0] = globaltimer();
@@ -796,20 +800,28 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
-      // work unit = (chunk of kFastChunk index entries, group of 32 misses),
+      // work unit = (chunk of kFastChunk index entries, group of kScanGroup misses),
       // chunk-major.  A warp loads the chunk's index entries and currTable
       // words ONCE and then streams the support words of every still
       // unresolved miss of its group over them (the next miss's words are in
       // flight while the current one is tested), so the currTable / index
       // traffic is amortised over the group and each miss costs one round trip.
-      const int ngrp = (nscan + 31) / 32;
+      const int ngrp = (nscan + kScanGroup - 1) / kScanGroup;
       const int nch = (Ls + kFastChunk - 1) / kFastChunk;
       const int64_t total = (int64_t)nch * ngrp;
-      for (int64_t u = gw; u < total; u += nw) {
+      // units handed out dynamically (one atomic per unit and warp): their cost
+      // varies with how many misses of the group are still open, and a
+      // static split of ~2-3 units per warp left the last warps ~40 us behind;
+      // small groups keep one unit short (each open miss costs a round trip)
+      for (;;) {
+        int64_t u = 0;
+        if (lane == 0) u = atomicAdd(&c->tile_ctr, 1);
+        u = __shfl_sync(0xffffffffu, (int)u, 0);
+        if (u >= total) break;
         const int chunk = (int)(u / ngrp), grp = (int)(u - (int64_t)chunk * ngrp);
         const int k0 = chunk * kFastChunk;
-        const int m = grp * 32 + lane;
-        const int rowl = m < nscan ? __ldcg(st.scanlist + m) : -1;
+        const int m = grp * kScanGroup + lane;
+        const int rowl = (lane < kScanGroup && m < nscan) ? __ldcg(st.scanlist + m) : -1;
         const int fl = rowl >= 0 ? *(volatile const uint8_t *)(st.sup + rowl) : 1;
         unsigned todo = __ballot_sync(0xffffffffu, fl == 0);
         if (!todo) continue;

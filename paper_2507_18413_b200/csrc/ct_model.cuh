@@ -27,7 +27,9 @@ struct ModelCtl {
   unsigned long long t0, t1;     // %globaltimer at start / end
   unsigned long long ph[6];      // device search: ns in ingest, update, probe, scan, finalize, trail copies
   int32_t changed[2];            // the shared domains lost a value in the iteration, by parity
-  int32_t pad[2];
+  int32_t failp[2];              // a table failed in the iteration, by parity (loop control: a CTA
+                                 // already in the next iteration must not change what a slower
+                                 // one reads at the end of this one)
 };
 static_assert(sizeof(ModelCtl) <= 256, "ModelCtl must fit its 256-byte slot");
 
@@ -143,6 +145,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     // ---- ingest (a2): one block per table, removals = values the shared domains lost
     if (blockIdx.x == 0 && tid == 0) {
       mc->active[(it + 1) & 1] = 0;
+      mc->failp[(it + 1) & 1] = 0;
       mc->changed[it & 1] = 0;
     }
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
@@ -150,13 +153,16 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       __syncthreads();
       if (tid == 0) {
         const Ctl *c = md.sts[k].ctl;
-        if (c->fail_fast) atomicExch(&mc->fail, 1);
+        if (c->fail_fast) atomicExch(&mc->failp[it & 1], 1);
         else if (!c->noop && !c->skip) atomicAdd(&mc->active[it & 1], 1);
       }
     }
     model_barrier(mc);
     lap(0);
-    if (tid == 0) s_brk = __ldcg(&mc->fail) || __ldcg(&mc->active[it & 1]) == 0;
+    if (tid == 0) {
+      s_brk = __ldcg(&mc->failp[it & 1]) || __ldcg(&mc->active[it & 1]) == 0;
+      if (s_brk && blockIdx.x == 0) mc->fail = __ldcg(&mc->failp[it & 1]);   // read after the final barrier
+    }
     __syncthreads();
     if (s_brk) break;
     if (blockIdx.x == 0 && tid == 0) {
@@ -239,7 +245,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       dev_finalize<kFusedTPB>(tb, st, nullptr, nullptr, nullptr, smem);
       __syncthreads();
       if (__ldcg(&st.ctl->last_status) != 0) {
-        if (tid == 0) atomicExch(&mc->fail, 1);
+        if (tid == 0) atomicExch(&mc->failp[it & 1], 1);
       } else {
         for (int w = tid; w < tb.Wd; w += kFusedTPB) {
           const uint64_t nd = __ldcg(st.dom + w);
@@ -256,17 +262,21 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     lap(4);
     // stop on a failure, or at the fixpoint: no table removed a value from the
     // shared domains, so every table is a no-op in the next iteration
-    if (tid == 0) s_brk = __ldcg(&mc->fail) || !__ldcg(&mc->changed[it & 1]);
+    if (tid == 0) {
+      s_brk = __ldcg(&mc->failp[it & 1]) || !__ldcg(&mc->changed[it & 1]);
+      if (s_brk && blockIdx.x == 0) mc->fail = __ldcg(&mc->failp[it & 1]);
+    }
     __syncthreads();
     if (s_brk) break;
   }
-  model_barrier(mc);
+  model_barrier(mc);   // mc->fail (the verdict) is read after this barrier
 }
 
 // Block 0: reset the per-fixpoint control fields (before a grid barrier).
 __device__ __forceinline__ void model_reset_ctl(ModelCtl *mc) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     mc->fail = 0;
+    mc->failp[0] = mc->failp[1] = 0;
     mc->iters = 0;
     mc->table_calls = 0;
     mc->active[0] = mc->active[1] = 0;

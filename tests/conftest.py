@@ -13,6 +13,19 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
+def pytest_collection_modifyitems(config, items):
+    # a GPU test that hangs (e.g. a grid barrier that never completes) must
+    # fail the run, not stall it: per-test limit with the thread method, which
+    # also works while the main thread is blocked in a CUDA call
+    try:
+        import pytest_timeout  # noqa: F401
+    except ImportError:
+        return
+    for it in items:
+        if it.get_closest_marker("gpu") and not it.get_closest_marker("timeout"):
+            it.add_marker(pytest.mark.timeout(240, method="thread"))
+
+
 @pytest.fixture(scope="session")
 def golden_dir():
     return os.path.join(ROOT, "tests", "golden")
