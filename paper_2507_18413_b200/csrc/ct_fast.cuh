@@ -585,10 +585,11 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
     if (out_pruned) out_pruned[k] = p.din[k] & ~nd;
   }
   // the status word completes the host-mapped synchronous call: every output
-  // write must be visible system-wide before it
-  if (sys_fence) __threadfence_system();
+  // write must be visible system-wide before it (block barrier, then ONE
+  // cumulative system-scope fence by the thread that writes the status)
   __syncthreads();
   if (tid == 0) {
+    if (sys_fence) __threadfence_system();
     if (!fs.noop && tb.use_index) {
       c->parity ^= 1;
       c->L = fs.Lout;

@@ -763,11 +763,15 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
     if (out_dom) out_dom[k] = nd;
     if (out_pruned) out_pruned[k] = __ldcg(st.din + k) & ~nd;
   }
-  // the status word is the completion flag of the host-mapped sync path: make
-  // every thread's output writes visible system-wide before it is written
-  __threadfence_system();
+  // the status word is the completion flag of the host-mapped sync path: every
+  // thread's output writes must be visible system-wide before it.  The block
+  // barrier makes them observed by thread 0, whose one system-scope fence is
+  // cumulative (one MEMBAR.SYS instead of one per thread).
   __syncthreads();
   if (tid == 0) {
+#ifndef CT_NO_SYSFENCE
+    if (out_status) __threadfence_system();
+#endif
     if (!noop && kDense) {
       c->L = tb.W2;
       c->identity = 1;

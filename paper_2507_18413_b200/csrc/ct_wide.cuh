@@ -67,9 +67,9 @@ __device__ void wide_write_ok(const TableDev &tb, const StateDev &st, uint64_t *
     if (out_dom) out_dom[k] = nd;
     if (out_pruned) out_pruned[k] = __ldcg(st.din + k) & ~nd;
   }
-  if (sys_fence) __threadfence_system();
-  __syncthreads();
+  __syncthreads();   // then one cumulative system-scope fence by the status writer
   if (threadIdx.x == 0) {
+    if (sys_fence) __threadfence_system();
     if (flip_index && tb.use_index) {
       c->parity ^= 1;
       c->L = Lout;
