@@ -954,6 +954,64 @@ __device__ int block_update(const TableDev &tb, const StateDev &st, int L, int n
   return (int)carry;
 }
 
+// ------------------------------------------------------------------ a6c-a8 inside one CTA after dev_ingest
+// dev_finalize for a kernel whose single CTA also ran dev_ingest: the status
+// is known, D (dom after the removals), |D_x|, rowBase and domOff are still in
+// the ingest's shared-memory layout, so nothing is re-read from the state.
+template <int NT>
+__device__ void small_finalize(const TableDev &tb, const StateDev &st, int status, bool noop, int Lout,
+                               uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
+                               int32_t *__restrict__ out_status, uint64_t *smem) {
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
+  const uint64_t *s_din = smem;                                         // dev_ingest: D_x
+  uint64_t *s_nd = smem + Wd;                                           // (was Δ_x)
+  const int32_t *s_cs = reinterpret_cast<const int32_t *>(smem + 2 * Wd) + n;
+  const int32_t *s_rb = s_cs + n + (n + 1);
+  const int32_t *s_do = s_rb + n + 1;
+  if (status != 0) {
+    if (tid == 0) {
+      if (status == 1) {
+        c->dead = 1;
+        c->calls += 1;
+      }
+      c->last_status = status;
+      if (out_status) *out_status = status;
+    }
+    return;
+  }
+  for (int k = tid; k < Wd; k += NT) s_nd[k] = s_din[k];
+  __syncthreads();
+  if (!noop) {
+    for (int r = tid; r < tb.R; r += NT) {
+      const int x = tb.rowVar[r];
+      if (!__ldcg(st.sup + r) && s_cs[x] > 1) {   // x in s_sup (Alg. 3 L1), a unsupported
+        const int a = r - s_rb[x];
+        atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + s_do[x] + (a >> 6)), ~(1ull << (a & 63)));
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = tid; k < Wd; k += NT) {
+    const uint64_t nd = s_nd[k];
+    st.dom[k] = nd;
+    if (out_dom) out_dom[k] = nd;
+    if (out_pruned) out_pruned[k] = s_din[k] & ~nd;
+  }
+  __syncthreads();   // then one cumulative system-scope fence by the status writer
+  if (tid == 0) {
+    if (out_status) __threadfence_system();
+    if (!noop && tb.use_index) {
+      c->parity ^= 1;
+      c->L = Lout;
+      c->identity = 0;
+    }
+    c->calls += 1;
+    c->last_status = 0;
+    if (out_status) *out_status = 0;
+  }
+}
+
 // ------------------------------------------------------------------ k_small: one state, one CTA
 // Tables of at most kSmallMaxPairs 16-byte blocks (e.g. BASELINE config 2,
 // 1e5 tuples = 782 blocks) are latency-bound: every phase runs in ONE block of
@@ -978,10 +1036,11 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
   __syncthreads();
   if (t0) ts[1] = globaltimer();
-  __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout;
+  __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout, s_pre;
   __shared__ uint64_t s_warp[kSmallTPB / 32];
   if (t0) {
     s_go = !(c->skip | c->noop | c->fail_fast);
+    s_pre = c->skip ? -5 : c->fail_fast ? 1 : c->noop ? 2 : 0;   // status known before the update (2: no-op)
     s_L = c->L;
     s_nrows = c->nrows;
     s_ident = c->identity;
@@ -1050,7 +1109,8 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
     out_pruned = st.out + 1 + tb.Wd;
     out_status = reinterpret_cast<int32_t *>(st.out);
   }
-  dev_finalize<kSmallTPB>(tb, st, out_dom, out_pruned, out_status, smem);
+  const int status = s_pre == 2 ? 0 : s_pre != 0 ? s_pre : (s_Lout > 0 ? 0 : 1);
+  small_finalize<kSmallTPB>(tb, st, status, s_pre == 2, s_Lout, out_dom, out_pruned, out_status, smem);
   if (t0) {
     ts[5] = globaltimer();
     for (int i = 0; i < 8; ++i) c->tph[i] = ts[i < 6 ? i : 5];
