@@ -268,6 +268,13 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
   __shared__ int s_dead, s_fail, s_ngroups;
   __shared__ uint64_t s_warp[NT / 32];
 
+  // this thread's first domain word and removal word are loaded before
+  // anything waits: the removals may sit in mapped host memory (sync call)
+  uint64_t dm0 = 0, rm0 = 0;
+  if (tid < Wd) {
+    dm0 = st.dom[tid];
+    rm0 = gdom ? ~__ldcg(gdom + tb.gword[tid]) : (rem ? rem[tid] : 0ull);
+  }
   if (tid == 0) {
     s_dead = c->dead;
     s_fail = 0;
@@ -293,9 +300,9 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
 
   // phase 1 (Alg. 1 L1-2): Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
   for (int k = tid; k < Wd; k += NT) {
-    const uint64_t dm = st.dom[k];
+    const uint64_t dm = k == tid ? dm0 : st.dom[k];
     // model tables: a value is removed iff the shared (global) domain lost it
-    const uint64_t rm = gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull);
+    const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
     const int x = tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     s_din[k] = di;
@@ -377,6 +384,140 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
     c->upd_writes = 0;
     c->scan_loads = 0;
   }
+}
+
+// ------------------------------------------------------------------ a2: ingest by one warp
+// dev_ingest's decisions and outputs (same lists in the same order, same
+// shared-memory layout) computed by warp 0 alone, with warp-level scans
+// instead of block scans: for one-CTA calls on small tables (k_small) the
+// ingest is latency-bound and 32 lanes cover its few words and rows.  Every
+// thread of the block calls it; it ends with a block barrier.
+__device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
+                            int root_mode, uint64_t *smem) {
+  Ctl *c = st.ctl;
+  const int n = tb.n, Wd = tb.Wd, R = tb.R;
+  uint64_t *s_din = smem;
+  uint64_t *s_dl = smem + Wd;
+  int32_t *s_cd = reinterpret_cast<int32_t *>(smem + 2 * Wd);
+  int32_t *s_cs = s_cd + n;
+  int32_t *s_ust = s_cs + n;
+  int32_t *s_rb = s_ust + n + 1;
+  int32_t *s_do = s_rb + n + 1;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    uint64_t dm0 = 0, rm0 = 0;
+    if (lane < Wd) {
+      dm0 = st.dom[lane];
+      rm0 = rem ? rem[lane] : 0ull;
+    }
+    const int dead = __shfl_sync(0xffffffffu, lane == 0 ? c->dead : 0, 0);
+    for (int i = lane; i <= n; i += 32) {
+      s_rb[i] = tb.rowBase[i];
+      s_do[i] = tb.domOff[i];
+    }
+    for (int x = lane; x < n; x += 32) s_cd[x] = s_cs[x] = 0;
+    if (dead) {
+      if (lane == 0) {
+        c->skip = 1;
+        c->noop = 0;
+        c->fail_fast = 0;
+      }
+    } else {
+      uint4 *s4 = reinterpret_cast<uint4 *>(st.sup);   // sup[0..R] = 0 (256-byte aligned)
+      for (int r = lane; r < (R + 16) / 16; r += 32) s4[r] = make_uint4(0u, 0u, 0u, 0u);
+      __syncwarp();
+      // Alg. 1 L1-2: Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
+      for (int k = lane; k < Wd; k += 32) {
+        const uint64_t dm = k == lane ? dm0 : st.dom[k];
+        const uint64_t rm = k == lane ? rm0 : (rem ? rem[k] : 0ull);
+        const int x = tb.wordVar[k];
+        const uint64_t delta = rm & dm, di = dm & ~rm;
+        s_din[k] = di;
+        s_dl[k] = delta;
+        st.din[k] = di;
+        if (delta) atomicAdd(&s_cd[x], __popcll(delta));
+        if (di) atomicAdd(&s_cs[x], __popcll(di));
+      }
+      __syncwarp();
+      // per variable: s_val, branch (Alg. 2), group sizes -> group starts
+      int carry = 0, ngroups = 0, fail = 0;
+      for (int base = 0; base < n; base += 32) {
+        const int x = base + lane;
+        int ucnt = 0;
+        if (x < n) {
+          const int cd = s_cd[x], cs = s_cs[x];
+          const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+          if (cd > 0) ucnt = useDelta ? cd : cs;
+          ngroups += cd > 0;
+          fail |= cs == 0;
+          st.varcnt[2 * x] = cd;
+          st.varcnt[2 * x + 1] = cs;
+        }
+        int incl = ucnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (x < n) s_ust[x] = carry + incl - ucnt;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) s_ust[n] = carry;
+      ngroups = __reduce_add_sync(0xffffffffu, ngroups);
+      fail = __reduce_or_sync(0xffffffffu, fail);
+      __syncwarp();
+      const bool noop = ngroups == 0 && !root_mode;
+      int nrows = 0, nitems = 0;
+      if (!(fail || noop)) {
+        // per support row: update list (grouped by var, group end marked) and
+        // filter items (Alg. 1 L3: s_sup), both in row order
+        int ucarry = 0, icarry = 0;
+        for (int base = 0; base < R; base += 32) {
+          const int r = base + lane;
+          bool u = false, f = false, useDelta = false;
+          int x = 0;
+          if (r < R) {
+            x = tb.rowVar[r];
+            const int a = r - s_rb[x];
+            const int w = s_do[x] + (a >> 6), b = a & 63;
+            const int cd = s_cd[x], cs = s_cs[x];
+            useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+            const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
+            u = cd > 0 && (useDelta ? inDl : inD);
+            f = cs > 1 && inD;
+          }
+          const unsigned bu = __ballot_sync(0xffffffffu, u), bf = __ballot_sync(0xffffffffu, f);
+          if (u) {
+            const int up = ucarry + __popc(bu & lanemask_lt());
+            uint32_t e = (uint32_t)r | (useDelta ? kInvBit : 0u);
+            if (up == s_ust[x + 1] - 1) e |= kEndBit;
+            st.ulist[up] = (int32_t)e;
+          }
+          if (f) st.items[icarry + __popc(bf & lanemask_lt())] = r;
+          ucarry += __popc(bu);
+          icarry += __popc(bf);
+        }
+        nrows = ucarry;
+        nitems = icarry;
+      }
+      if (lane == 0) {
+        c->skip = 0;
+        c->noop = noop && !fail;
+        c->fail_fast = fail;
+        c->ngroups = ngroups;
+        c->nrows = nrows;
+        c->nitems = nitems;
+        c->L_in = c->L;
+        c->L_out = 0;
+        c->tile_ctr = 0;
+        c->nscan = 0;
+        c->upd_loads = 0;
+        c->upd_writes = 0;
+        c->scan_loads = 0;
+      }
+    }
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ a3-a5: update + compaction
@@ -1019,6 +1160,7 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
 // the compaction is a plain block scan (no look-back).  Same phase semantics
 // as k_fused; with_finalize = 0 for sharded tables.
 constexpr int kSmallTPB = 1024;
+constexpr int kWarpIngestMaxRows = 1024;   // k_small ingests with one warp up to this many support rows
 constexpr int kSmallMaxPairs = 8192;
 
 __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const StateDev *__restrict__ states,
@@ -1033,7 +1175,8 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   const bool t0 = tid == 0;
   unsigned long long ts[6];
   if (t0) ts[0] = globaltimer();
-  dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
+  if (tb.R <= kWarpIngestMaxRows) warp_ingest(tb, st, removed, root_mode, smem);
+  else dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
   __syncthreads();
   if (t0) ts[1] = globaltimer();
   __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout, s_pre;
