@@ -49,6 +49,7 @@ struct BatchDev {
   int32_t *bgo;              // [S] per call: (groups << 20) | update-list length, or -1 if the state does not update
   int2 *miss, *miss2;        // [S·R] global lists of (state, row) probe misses (pass 0 / pass 1 of k_bscan)
   int32_t *nmiss, *nmiss2;   // their lengths (zeroed by k_bingest)
+  int2 *sinfo;               // [S] per call: (index buffer parity, L_out) of each state, from k_bcompact
   unsigned long long *work;  // [4] whole batch, summed over calls until ct_batch_work resets them:
                              // update support words, currTable blocks read, blocks rewritten,
                              // support bytes staged into shared memory
@@ -427,7 +428,10 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev b
     }
     carry += total;
   }
-  if (threadIdx.x == 0) c->L_out = (int32_t)carry;
+  if (threadIdx.x == 0) {
+    c->L_out = (int32_t)carry;
+    bd.sinfo[s] = make_int2(__ldcg(&c->parity), (int)carry);
+  }
 }
 
 // ------------------------------------------------------------------ a6a: residue probe, one thread per item
@@ -512,8 +516,83 @@ __global__ void __launch_bounds__(kBProbeTPB) k_bprobe(TableDev tb, BatchDev bd,
 // tables), each re-checking the miss's flag between rounds.
 constexpr int kBScanRounds = 4;
 constexpr int kBScanFirst = kBScanRounds * 32 * kScanUnroll;   // blocks scanned by pass 0
+// Pass 0 with a HALF warp per miss (16 lanes x kScanUnroll entries = 64 index
+// entries per round, the two halves of a warp on two misses), the next miss's
+// list entry and index parameters loaded while the current one is scanned.
+__device__ void bscan_pass0(const TableDev &tb, const BatchDev &bd, int gw, int nw) {
+  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  const int nm = __ldcg(bd.nmiss);
+  constexpr int kR = 16 * kScanUnroll;   // entries per round
+  auto fetch = [&](int m, int2 &e, int2 &inf) {
+    e = make_int2(0, 0);
+    inf = make_int2(0, 0);
+    if (m < nm) {
+      e = __ldcg(bd.miss + m);
+      inf = __ldcg(bd.sinfo + e.x);
+    }
+  };
+  int2 e, inf, e_n, inf_n;
+  int m = 2 * gw + half;
+  fetch(m, e, inf);
+  for (int mb = 2 * gw; mb < nm; mb += 2 * nw, m += 2 * nw) {
+    fetch(m + 2 * nw, e_n, inf_n);
+    const bool valid = m < nm;
+    const int s = e.x, row = e.y;
+    const int L = valid ? (tb.use_index ? inf.y : tb.W2) : 0;
+    const int Lf = min(L, kBScanFirst);
+    const int32_t *idx = tb.use_index ? bfield<const int32_t>(bd, s, inf.x ? bd.o_idx0 : bd.o_idx1) : nullptr;
+    const ulonglong2 *T2 = bfield<const ulonglong2>(bd, s, bd.o_T);
+    const uint64_t *srow = tb.S + (int64_t)row * tb.Wp;
+    int hit = -1;
+    uint32_t n_loads = 0;
+    bool active = valid && Lf > 0;
+    for (int k0 = 0; __any_sync(0xffffffffu, active); k0 += kR) {
+      int pid[kScanUnroll];
+      bool in[kScanUnroll];
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        const int k = k0 + q * 16 + hl;
+        in[q] = active && k < Lf;
+        pid[q] = in[q] ? (idx ? __ldcg(idx + k) : k) : 0;
+      }
+      ulonglong2 t[kScanUnroll], v[kScanUnroll];
+#pragma unroll
+      for (int q = 0; q < kScanUnroll; ++q) {
+        t[q] = in[q] ? __ldcg(T2 + pid[q]) : make_ulonglong2(0ull, 0ull);
+        v[q] = in[q] ? ld_sup2(srow + 2 * (int64_t)pid[q]) : make_ulonglong2(0ull, 0ull);
+      }
+      if (active) n_loads += 2 * max(0, min(kR, Lf - k0));
+#pragma unroll
+      for (int q = kScanUnroll - 1; q >= 0; --q) {
+        const unsigned b = __ballot_sync(0xffffffffu, ((t[q].x & v[q].x) | (t[q].y & v[q].y)) != 0);
+        const unsigned hb = (b >> (16 * half)) & 0xffffu;
+        const int src = hb ? (16 * half + __ffs(hb) - 1) : lane;
+        const int p = __shfl_sync(0xffffffffu, pid[q], src);
+        if (hb && active) hit = p;
+      }
+      if (hit >= 0 || k0 + kR >= Lf) active = false;
+    }
+    if (valid && hl == 0) {
+      uint8_t *sup = bfield<uint8_t>(bd, s, bd.o_sup);
+      if (hit >= 0) {
+        sup[row] = 1;
+        bfield<int32_t>(bd, s, bd.o_res)[row] = hit;
+      } else if (L > kBScanFirst) {
+        bd.miss2[atomicAdd(bd.nmiss2, 1)] = e;
+      }
+      if (n_loads) atomicAdd(&bctl(bd, s)->scan_loads, (unsigned long long)n_loads);
+    }
+    e = e_n;
+    inf = inf_n;
+  }
+}
+
 __global__ void __launch_bounds__(kBScanTPB) k_bscan(TableDev tb, BatchDev bd, int pass) {
   const int lane = threadIdx.x & 31;
+  if (pass == 0) {
+    bscan_pass0(tb, bd, blockIdx.x * (kBScanTPB / 32) + (threadIdx.x >> 5), gridDim.x * (kBScanTPB / 32));
+    return;
+  }
   const int gw = blockIdx.x * (kBScanTPB / 32) + (threadIdx.x >> 5), nw = gridDim.x * (kBScanTPB / 32);
   const int Lmax = tb.W2;   // chunks are laid out over the largest possible index
   const int nm = __ldcg(pass == 0 ? bd.nmiss : bd.nmiss2);

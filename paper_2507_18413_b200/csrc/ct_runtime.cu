@@ -1013,7 +1013,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_dom = (uint64_t *)tb->dalloc(io);
   b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
-  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64;
+  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64 + (size_t)n_states * sizeof(int2);
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
   if (b->d_miss && cudaMemset(b->d_miss, 0, b->miss_bytes) != cudaSuccess) cudaGetLastError();
   if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status || !b->d_bgo || !b->d_miss)
@@ -1050,6 +1050,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
     bd.nmiss = reinterpret_cast<int32_t *>(b->d_miss + 2 * nm);
     bd.nmiss2 = bd.nmiss + 1;
     bd.work = reinterpret_cast<unsigned long long *>(b->d_miss + 2 * nm + 2);   // 16-byte aligned
+    bd.sinfo = b->d_miss + 2 * nm + 8;                                            // after work[4]
   }
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
@@ -1135,7 +1136,7 @@ static ct_status enqueue_batch_tiled(ct_batch *b, const uint64_t *removed, uint6
   k_bprobe<<<(unsigned)((pth + kBProbeTPB - 1) / kBProbeTPB), kBProbeTPB, 0, st>>>(tb->dev, b->bd, S);
   prof_mark(tb, 2, e, st);
   e = prof_event(tb, st);
-  k_bscan<<<tb->sm_count * 8, kBScanTPB, 0, st>>>(tb->dev, b->bd, 0);
+  k_bscan<<<tb->sm_count * 16, kBScanTPB, 0, st>>>(tb->dev, b->bd, 0);
   k_bscan<<<tb->sm_count * 8, kBScanTPB, 0, st>>>(tb->dev, b->bd, 1);
   prof_mark(tb, 3, e, st);
   e = prof_event(tb, st);
