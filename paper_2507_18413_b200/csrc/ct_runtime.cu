@@ -313,8 +313,19 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     const int e = prof_event(tb, st);
     k_wide<<<1, kWideTPB, tb->wide_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
                                                out_dom, out_pruned, out_status, use_state_out);
-    k_wide_filter<<<(unsigned)std::max(1, (tb->R + kWideFiltTPB - 1) / kWideFiltTPB), kWideFiltTPB, 0, st>>>(
-        tb->dev, (const StateDev *)s->d_desc, fin_inside, out_dom, out_pruned, out_status, use_state_out);
+    // programmatic dependent launch: the filter grid is scheduled while k_wide
+    // runs and waits for it at griddepcontrol.wait, hiding its launch latency
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)std::max(1, (tb->R + kWideFiltTPB - 1) / kWideFiltTPB));
+    lc.blockDim = dim3(kWideFiltTPB);
+    lc.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_wide_filter, tb->dev, (const StateDev *)s->d_desc, fin_inside, out_dom,
+                                out_pruned, out_status, use_state_out));
     CUDA_TRY(cudaGetLastError());
     prof_mark(tb, 7, e, st);
     if (fin_inside || local_only) return CT_OK;

@@ -96,6 +96,9 @@ __global__ void __launch_bounds__(kWideTPB, 1) k_wide(TableDev tb, const StateDe
   Ctl *c = st.ctl;
   const int tid = threadIdx.x;
   const bool t0 = tid == 0;
+  // let the dependent k_wide_filter grid launch now (it waits for this grid's
+  // completion and memory flush at griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (t0) c->tph[0] = globaltimer();
   if (use_state_out) {
     out_dom = st.out + 1;
@@ -167,6 +170,9 @@ __global__ void __launch_bounds__(kWideFiltTPB) k_wide_filter(TableDev tb, const
   __shared__ int s_last;
   __shared__ int s_cnt[kWideFiltTPB / 32];
   __shared__ int32_t s_miss[kWideFiltTPB];
+  // launched as a programmatic dependent of k_wide: wait until it completed
+  // and its writes are visible (a no-op when launched normally)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const StateDev &st = states[0];
   Ctl *c = st.ctl;
   const bool go = !(__ldcg(&c->skip) | __ldcg(&c->noop) | __ldcg(&c->fail_fast)) && __ldcg(&c->L_out) > 0;
