@@ -670,13 +670,23 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     }
     FAST_TRACE(2);
 #ifndef CT_FAST_NOCOUNT
-    // update work counters now, while CTAs still finish at different times
-    // (740 same-address atomics at the end of the call cost ~2 us)
+    // update work counters now, while CTAs still finish at different times,
+    // reduced per CTA first: when every CTA finishes its (short) update at
+    // once, one same-address atomic per warp serialised into ~3.5 us before
+    // barrier 1
     {
       const uint32_t wl = warp_sum_u32(n_loads), ww = warp_sum_u32(n_writes);
-      if (lane == 0) {
-        if (wl) atomicAdd(&c->upd_loads, (unsigned long long)wl);
-        if (ww) atomicAdd(&c->upd_writes, (unsigned long long)ww);
+      if (lane == 0) fs.red[warp] = (int)wl;
+      if (lane == 0) fs.woff[warp] = ww;
+      __syncthreads();
+      if (tid == 0) {
+        unsigned long long tl = 0, tw = 0;
+        for (int w = 0; w < kFastWarps; ++w) {
+          tl += (uint32_t)fs.red[w];
+          tw += fs.woff[w];
+        }
+        if (tl) atomicAdd(&c->upd_loads, tl);
+        if (tw) atomicAdd(&c->upd_writes, tw);
       }
     }
 #endif
