@@ -206,6 +206,21 @@ __device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
   fast_grid_barrier_mode(bar, [] { return 0; }, leader, &s_mode);
 }
 
+// Adds a per-thread counter to a global 64-bit counter with ONE atomic per CTA
+// (warp sums, then thread 0); every thread of the block must call it.
+__device__ __forceinline__ void cta_count(uint32_t v, unsigned long long *dst, FastSh &fs) {
+  v = warp_sum_u32(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) fs.woff[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kFastWarps; ++w) t += fs.woff[w];
+    if (t) atomicAdd(dst, t);
+  }
+  __syncthreads();   // fs.woff is free again
+}
+
 // Block-wide sum over kFastTPB threads (uses fs.red; every thread gets the total).
 __device__ __forceinline__ int fast_block_sum(int v, FastSh &fs) {
 #pragma unroll
@@ -688,6 +703,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         if (tl) atomicAdd(&c->upd_loads, tl);
         if (tw) atomicAdd(&c->upd_writes, tw);
       }
+      __syncthreads();   // fs.red / fs.woff are free again
     }
 #endif
 
@@ -779,7 +795,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     if (t0) c->tph[3] = c->tph[4] = globaltimer();
     FAST_TRACE(5);
 #ifndef CT_FAST_NOCOUNT
-    if (lane == 0 && f_loads) atomicAdd(&c->scan_loads, (unsigned long long)f_loads);   // probe rounds
+    cta_count(lane == 0 ? f_loads : 0u, &c->scan_loads, fs);   // probe rounds
 #endif
     f_loads = 0;
     // ---- scan (a6b): misses x chunks of the compacted index, from entry 0.
@@ -891,9 +907,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     FAST_TRACE(7);
     if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
     }   // !kFastStop
-    // scan work counter, one atomic per warp that scanned
+    // scan work counter, one atomic per CTA
 #ifndef CT_FAST_NOCOUNT
-    if (lane == 0 && f_loads) atomicAdd(&c->scan_loads, (unsigned long long)f_loads);
+    cta_count(lane == 0 ? f_loads : 0u, &c->scan_loads, fs);
 #endif
   }
 
