@@ -1748,6 +1748,7 @@ static ct_status model_search_device(ct_model *m, int32_t value_order, int64_t m
     int64_t vals = 1;
     for (int v = 0; v < m->nv; ++v) vals += m->vd[v];
     m->levels = (int)std::min<int64_t>(kSearchMaxLevels, vals);
+    if (const char *ev = getenv("CT_SEARCH_LEVELS")) m->levels = std::max(2, std::min(m->levels, atoi(ev)));   // tests
     if (cudaMalloc(&m->snap_dev, (size_t)m->levels * pool16 * 16) != cudaSuccess) {
       cudaGetLastError();
       m->snap_dev = nullptr;

@@ -111,3 +111,24 @@ def test_device_and_host_drivers_agree(seed):
         assert st == CT_OK and np.array_equal(gd, root)
         M.pop()
     M.close()
+
+
+def test_device_search_falls_back_when_the_trail_is_short():
+    """A trail shorter than the search depth (CT_SEARCH_LEVELS, read when the
+    device search is first set up) makes the device driver stop and the host
+    driver rerun the search: same results as a plain host-driven search."""
+    import os
+    m = csp_model(6, 5, 4, 40, seed=51, arities=[3, 3, 2, 4])
+    os.environ["CT_SEARCH_LEVELS"] = "3"
+    try:
+        M = _model(m)
+        a = M.search(value_order=0, max_solutions=0, driver="device")
+    finally:
+        os.environ.pop("CT_SEARCH_LEVELS", None)
+    b = M.search(value_order=0, max_solutions=0, driver="host")
+    ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_solutions=0)
+    assert b[2].max_depth > 2                      # the trail was too short for this tree
+    for f in ("nodes", "failures", "solutions", "trace_hash"):
+        assert getattr(a[2], f) == getattr(b[2], f), f
+    assert a[2].trace_hash == ref["trace_hash"]
+    M.close()
