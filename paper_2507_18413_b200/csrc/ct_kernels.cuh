@@ -1260,15 +1260,48 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   }
 }
 
+// ------------------------------------------------------------------ state copies (backtracking)
+// Byte offsets / sizes of the persistent fields of a state block.
+struct CopyLayout {
+  int64_t T_bytes;           // currTable: W2 16-byte blocks
+  int64_t o_T, o_idx0, o_idx1, o_res, o_dom;
+  int64_t res_bytes, dom_bytes;
+};
+
+// Copies what a state needs from src to dst (threads [t0, t0 + nt) of the
+// caller): the control block, currTable, the ACTIVE index buffer (only its L
+// entries, none for an identity index), residues and domains -- not the
+// other, scratch index buffer nor the per-call scratch.
+__device__ __forceinline__ void copy_state_fields(char *__restrict__ dst, const char *__restrict__ src,
+                                                  const CopyLayout &cl, int64_t t0, int64_t nt) {
+  const Ctl *sc = reinterpret_cast<const Ctl *>(src);
+  const int ident = __ldcg(&sc->identity), par = __ldcg(&sc->parity), L = __ldcg(&sc->L);
+  const int64_t idx_bytes = ident ? 0 : (int64_t)L * 4;
+  const int64_t o_idx = par ? cl.o_idx1 : cl.o_idx0;
+  // segments, each a multiple of 16 bytes (the layout pads every field to 256)
+  const int64_t seg_off[5] = {0, cl.o_T, o_idx, cl.o_res, cl.o_dom};
+  const int64_t seg_len[5] = {256, cl.T_bytes, (idx_bytes + 15) / 16 * 16, (cl.res_bytes + 15) / 16 * 16,
+                              (cl.dom_bytes + 15) / 16 * 16};
+  for (int g = 0; g < 5; ++g) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src + seg_off[g]);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst + seg_off[g]);
+    for (int64_t k = t0; k < seg_len[g] / 16; k += nt) d4[k] = __ldcg(s4 + k);
+  }
+}
+
+// ct_state_copy / ct_state_clone: one state, the whole grid.
+__global__ void __launch_bounds__(256) k_state_copy(char *__restrict__ dst, const char *__restrict__ src,
+                                                    CopyLayout cl) {
+  copy_state_fields(dst, src, cl, (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+}
+
 // ------------------------------------------------------------------ batch restart
-// grid (S), 256 threads: state i := src (persistent prefix) iff state i is dead.
+// grid (S), 256 threads: state i := src iff state i is dead.
 __global__ void __launch_bounds__(256) k_restore_dead(char *__restrict__ pool, size_t pitch,
-                                                      const char *__restrict__ src, size_t persist) {
+                                                      const char *__restrict__ src, CopyLayout cl) {
   char *dst = pool + (size_t)blockIdx.x * pitch;
   if (!reinterpret_cast<const Ctl *>(dst)->dead) return;
-  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-  uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-  for (size_t k = threadIdx.x; k < persist / 16; k += blockDim.x) d4[k] = s4[k];
+  copy_state_fields(dst, src, cl, threadIdx.x, blockDim.x);
 }
 
 }  // namespace ctk
