@@ -83,15 +83,18 @@ class State:
     def copy_from(self, src: "State") -> None:
         C.ct_state_copy(self.handle, src.handle)
 
-    def propagate(self, removed=None):
+    def propagate(self, removed=None, out=None, pruned=None):
         """Synchronous host call.  Returns (status, dom, pruned); dom/pruned are
-        None unless status == CT_OK."""
+        None unless status == CT_OK.  out / pruned: optional preallocated
+        uint64[Wd] host arrays (reused across calls by latency-sensitive callers)."""
         wd = self.table.Wd
-        out = np.zeros(max(wd, 1), np.uint64)
-        pr = np.zeros(max(wd, 1), np.uint64)
+        if out is None:
+            out = np.zeros(max(wd, 1), np.uint64)
+        if pruned is None:
+            pruned = np.zeros(max(wd, 1), np.uint64)
         rem = None if removed is None else np.ascontiguousarray(removed, np.uint64)
-        st = C.ct_propagate(self.handle, rem, out, pr)
-        return (st, out[:wd], pr[:wd]) if st == C.CT_OK else (st, None, None)
+        st = C.ct_propagate(self.handle, rem, out, pruned)
+        return (st, out[:wd], pruned[:wd]) if st == C.CT_OK else (st, None, None)
 
     def propagate_async(self, removed, out_dom=None, out_pruned=None, out_status=None):
         C.ct_propagate_async(self.handle, removed, out_dom, out_pruned, out_status)

@@ -174,7 +174,7 @@ def _check(status: int, allow_fail: bool = True) -> int:
 
 
 def _np_ptr(a):
-    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
 
 
 def _dev_ptr(t):
