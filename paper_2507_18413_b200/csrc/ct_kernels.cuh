@@ -393,7 +393,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
 // ingest is latency-bound and 32 lanes cover its few words and rows.  Every
 // thread of the block calls it; it ends with a block barrier.
 __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
-                            int root_mode, uint64_t *smem) {
+                            int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr) {
   Ctl *c = st.ctl;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
   uint64_t *s_din = smem;
@@ -408,7 +408,8 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
     uint64_t dm0 = 0, rm0 = 0;
     if (lane < Wd) {
       dm0 = st.dom[lane];
-      rm0 = rem ? rem[lane] : 0ull;
+      // model tables: a value is removed iff the shared (global) domain lost it
+      rm0 = gdom ? ~__ldcg(gdom + tb.gword[lane]) : (rem ? rem[lane] : 0ull);
     }
     const int dead = __shfl_sync(0xffffffffu, lane == 0 ? c->dead : 0, 0);
     for (int i = lane; i <= n; i += 32) {
@@ -425,11 +426,12 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
     } else {
       uint4 *s4 = reinterpret_cast<uint4 *>(st.sup);   // sup[0..R] = 0 (256-byte aligned)
       for (int r = lane; r < (R + 16) / 16; r += 32) s4[r] = make_uint4(0u, 0u, 0u, 0u);
+      for (int k = lane; k < tb.ntiles_max; k += 32) st.tilestat[k] = 0;   // chained-scan tile statuses
       __syncwarp();
       // Alg. 1 L1-2: Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
       for (int k = lane; k < Wd; k += 32) {
         const uint64_t dm = k == lane ? dm0 : st.dom[k];
-        const uint64_t rm = k == lane ? rm0 : (rem ? rem[k] : 0ull);
+        const uint64_t rm = k == lane ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
         const int x = tb.wordVar[k];
         const uint64_t delta = rm & dm, di = dm & ~rm;
         s_din[k] = di;
@@ -857,13 +859,16 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
   int32_t *s_do = s_rb + n + 1;
   __shared__ int s_status, s_noop;
   if (tid == 0) {
+    // the four flags are loaded together (one round trip, not a chain)
+    const int skip = __ldcg(&c->skip), ff = __ldcg(&c->fail_fast), noop = __ldcg(&c->noop);
+    const int nonempty = __ldcg(st.sup + tb.R);
     int s;
-    if (__ldcg(&c->skip)) s = -5;                  // CT_ESTATE
-    else if (__ldcg(&c->fail_fast)) s = 1;         // CT_FAIL
-    else if (__ldcg(&c->noop)) s = 0;
-    else s = __ldcg(st.sup + tb.R) ? 0 : 1;        // global "currTable non-empty" (Alg. 1 L5)
+    if (skip) s = -5;                  // CT_ESTATE
+    else if (ff) s = 1;                // CT_FAIL
+    else if (noop) s = 0;
+    else s = nonempty ? 0 : 1;         // global "currTable non-empty" (Alg. 1 L5)
     s_status = s;
-    s_noop = __ldcg(&c->noop);
+    s_noop = noop;
   }
   for (int k = tid; k < Wd; k += NT) s_nd[k] = __ldcg(st.din + k);
   for (int x = tid; x < n; x += NT) s_cs[x] = __ldcg(st.varcnt + 2 * x + 1);

@@ -248,7 +248,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
         if (tid == 0) atomicExch(&mc->failp[it & 1], 1);
       } else {
         for (int w = tid; w < tb.Wd; w += kFusedTPB) {
-          const uint64_t nd = __ldcg(st.dom + w);
+          const uint64_t nd = smem[w];   // dev_finalize's new domains (also stored in st.dom)
           const uint64_t g0 = __ldcg(md.gdom + tb.gword[w]);
           if ((g0 & nd) != g0) {
             const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + tb.gword[w]), nd);
