@@ -27,6 +27,7 @@ struct ModelCtl {
   unsigned long long t0, t1;     // %globaltimer at start / end
   unsigned long long ph[6];      // device search: ns in ingest, update, probe, scan, finalize, trail copies
   int32_t changed[2];            // the shared domains lost a value in the iteration, by parity
+  int32_t miss[2];               // some probe queued a miss in the iteration, by parity
   int32_t failp[2];              // a table failed in the iteration, by parity (loop control: a CTA
                                  // already in the next iteration must not change what a slower
                                  // one reads at the end of this one)
@@ -48,7 +49,7 @@ struct ModelDev {
 // probe_item with the residue probe and the first round of the scan issued
 // together (one round trip for most items instead of two).
 __device__ __forceinline__ void probe_item_fused(const TableDev &tb, const StateDev &st, const FiltParams &f,
-                                                 int item, uint32_t &n_loads) {
+                                                 int item, uint32_t &n_loads, int32_t *miss_flag) {
   const int lane = threadIdx.x & 31;
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
   const int row = __ldcg(st.items + item);
@@ -88,6 +89,7 @@ __device__ __forceinline__ void probe_item_fused(const TableDev &tb, const State
       st.res[row] = hit;
     } else if (f.L > kFirstScan) {
       st.scanlist[atomicAdd(&st.ctl->nscan, 1)] = row;
+      *miss_flag = 1;
     }
   }
 }
@@ -146,6 +148,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     if (blockIdx.x == 0 && tid == 0) {
       mc->active[(it + 1) & 1] = 0;
       mc->failp[(it + 1) & 1] = 0;
+      mc->miss[(it + 1) & 1] = 0;
       mc->changed[it & 1] = 0;
     }
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
@@ -203,7 +206,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       uint32_t n_loads = 0;
       for (int64_t g = gw; g < s_pre[ntab]; g += nw) {
         const int k = find_table(s_pre, ntab, g);
-        probe_item_fused(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads);
+        probe_item_fused(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads, &mc->miss[it & 1]);
       }
     }
     // the barrier's last arrival checks whether any table queued a miss; if
@@ -212,11 +215,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       int leader = 0;
       const int mode = fast_grid_barrier_mode(
           md.bar,
-          [&] {
-            int any = 0;
-            for (int k = 0; k < ntab && !any; ++k) any = __ldcg(&md.sts[k].ctl->nscan) > 0;
-            return any ? 0 : 1;
-          },
+          [&] { return __ldcg(&mc->miss[it & 1]) ? 0 : 1; },
           leader, &s_brk);
       lap(2);
       if (mode == 1) goto finalize_phase;
@@ -277,6 +276,7 @@ __device__ __forceinline__ void model_reset_ctl(ModelCtl *mc) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     mc->fail = 0;
     mc->failp[0] = mc->failp[1] = 0;
+    mc->miss[0] = mc->miss[1] = 0;
     mc->iters = 0;
     mc->table_calls = 0;
     mc->active[0] = mc->active[1] = 0;
