@@ -197,12 +197,17 @@ __device__ __forceinline__ ulonglong2 tile32_state(uint32_t s_lane, uint32_t zro
 // table entry (lane G: the padded total), `pe` = lane k holds padded entry k
 // of the chunk starting at entry 0; later chunks are loaded from `pl`.  Every
 // group is a multiple of 4 entries, so a step of 4 rows never needs a bound.
-__device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, const uint32_t *pl, int G, uint32_t gt,
-                                                    uint32_t pe, ulonglong2 tw, bool live, uint32_t &nl) {
+__device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s_pl, const uint32_t *pl, int G,
+                                                    uint32_t gt, uint32_t pe, ulonglong2 tw, bool live,
+                                                    uint32_t &nl) {
   const int lane = threadIdx.x & 31;
   uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
   if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+  // the current 32 entries live in this warp's shared slot: four row offsets
+  // per broadcast 16-byte load instead of four shuffles
   int chunk = 0;
+  s_pl[lane] = pe;
+  __syncwarp();
   uint32_t ge = __shfl_sync(0xffffffffu, gt, 0);
   for (int g = 0; g < G; ++g) {
     const uint32_t gn = __shfl_sync(0xffffffffu, gt, g + 1);
@@ -210,15 +215,16 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, const uint3
     for (int k = (int)(ge & 0xffffu); k < en;) {
       if ((k >> 5) != chunk) {                                 // warp-uniform, once per 32 entries
         chunk = k >> 5;
-        pe = __ldcg(pl + chunk * 32 + lane);
+        const uint32_t v = __ldcg(pl + chunk * 32 + lane);
+        __syncwarp();
+        s_pl[lane] = v;
+        __syncwarp();
       }
       const int kend = min(en, (chunk + 1) * 32);
       for (; k < kend; k += 4) {
-        const int kk = k & 31;
-        const uint32_t r0 = __shfl_sync(0xffffffffu, pe, kk), r1 = __shfl_sync(0xffffffffu, pe, kk + 1);
-        const uint32_t r2 = __shfl_sync(0xffffffffu, pe, kk + 2), r3 = __shfl_sync(0xffffffffu, pe, kk + 3);
-        const ulonglong2 v0 = lds128(s_lane + r0), v1 = lds128(s_lane + r1);
-        const ulonglong2 v2 = lds128(s_lane + r2), v3 = lds128(s_lane + r3);
+        const uint4 r = *reinterpret_cast<const uint4 *>(s_pl + (k & 31));
+        const ulonglong2 v0 = lds128(s_lane + r.x), v1 = lds128(s_lane + r.y);
+        const ulonglong2 v2 = lds128(s_lane + r.z), v3 = lds128(s_lane + r.w);
         ax |= v0.x | v1.x;
         ay |= v0.y | v1.y;
         ax |= v2.x | v3.x;
@@ -231,9 +237,13 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, const uint3
     my &= ay ^ inv;
     ax = ay = 0;
     live = live && ((tw.x & mx) | (tw.y & my)) != 0;          // Alg. 2, per block
-    if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
+    if (!__any_sync(0xffffffffu, live)) {
+      __syncwarp();
+      return make_ulonglong2(0ull, 0ull);
+    }
     ge = gn;
   }
+  __syncwarp();   // the slot is rewritten for the next state
   return make_ulonglong2(tw.x & mx, tw.y & my);
 }
 
@@ -246,6 +256,7 @@ template <int kTW>
 __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, int S, int ntiles, int nchunk,
                                                      int chunk_states) {
   extern __shared__ __align__(16) ulonglong2 s_sup[];   // [R + 1][kTW], row R = 0
+  __shared__ __align__(16) uint32_t s_plw[kBTPB];        // per warp: 32 update-list entries (kTW = 32 path)
   constexpr int SPW = 32 / kTW;                         // states per warp
   const int R = tb.R, W2 = tb.W2;
   const int64_t Wp = tb.Wp, Wp2 = tb.Wp / 2;
@@ -316,8 +327,8 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
         if (nr < 0) continue;                    // warp-uniform: one state per warp
         const int G = go >> 20;
         if (G < 32) {
-          nt = tile32_padded(s_lane, reinterpret_cast<const uint32_t *>(sb + bd.o_plist) + bd.plist_po, G, gt, ev,
-                             tw, had, nl);
+          nt = tile32_padded(s_lane, s_plw + 32 * warp, reinterpret_cast<const uint32_t *>(sb + bd.o_plist) + bd.plist_po,
+                             G, gt, ev, tw, had, nl);
         } else {                                 // > 31 changed variables: the plain list
           nt = tile32_state(s_lane, (uint32_t)R * 512u, ul, nr, __ldcg(ul + lane), tw, had, nl);
         }
