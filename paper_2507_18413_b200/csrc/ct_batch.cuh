@@ -221,8 +221,10 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s
         __syncwarp();
       }
       const int kend = min(en, (chunk + 1) * 32);
-      for (; k < kend; k += 4) {
-        const uint4 r = *reinterpret_cast<const uint4 *>(s_pl + (k & 31));
+      const uint4 *rp = reinterpret_cast<const uint4 *>(s_pl + (k & 31));
+      const int nsteps = (kend - k) >> 2;
+      for (int i = 0; i < nsteps; ++i) {
+        const uint4 r = rp[i];
         const ulonglong2 v0 = lds128(s_lane + r.x), v1 = lds128(s_lane + r.y);
         const ulonglong2 v2 = lds128(s_lane + r.z), v3 = lds128(s_lane + r.w);
         ax |= v0.x | v1.x;
@@ -230,6 +232,7 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s
         ax |= v2.x | v3.x;
         ay |= v2.y | v3.y;
       }
+      k = kend;
     }
     nl += ((ge >> 16) & 0x7fffu) * (uint32_t)__popc(__ballot_sync(0xffffffffu, live));   // warp total
     const uint64_t inv = (ge & 0x80000000u) ? ~0ull : 0ull;   // Δ-branch: AND the complement
