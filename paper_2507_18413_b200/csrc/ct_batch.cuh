@@ -222,7 +222,9 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s
       }
       const int kend = min(en, (chunk + 1) * 32);
       const uint4 *rp = reinterpret_cast<const uint4 *>(s_pl + (k & 31));
-      const int nsteps = (kend - k) >> 2;
+      // dead lanes drop out: a quarter-warp with no live block costs no
+      // shared-memory wavefront
+      const int nsteps = live ? (kend - k) >> 2 : 0;
       for (int i = 0; i < nsteps; ++i) {
         const uint4 r = rp[i];
         const ulonglong2 v0 = lds128(s_lane + r.x), v1 = lds128(s_lane + r.y);
