@@ -168,8 +168,12 @@ int32_t ct_dom_word_offset(const ct_table *t, int32_t i);   /* first word of var
 ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
                        uint64_t *out_pruned);
 
-/* Asynchronous, device buffers, enqueued on the state's stream; nothing is
- * copied to or from the host and the call does not wait.
+/* Asynchronous, device-accessible buffers, enqueued on the state's stream; the
+ * call does not wait.  The buffers may be device memory or pinned host memory
+ * (cudaHostAlloc / cudaMallocHost).  A host `removed` is copied into the
+ * state's device slot by one stream-ordered DMA (pageable memory is accepted
+ * but the copy then blocks); host outputs are written in place by the kernel
+ * (zero-copy).  So a caller can keep many host-buffer calls in flight.
  *   removed     device uint64[Wd] (NULL = nothing removed)
  *   out_dom     device uint64[Wd] or NULL
  *   out_pruned  device uint64[Wd] or NULL

@@ -927,6 +927,19 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
   if (tb->n_shards > 1 && !tb->comm)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
   DeviceGuard g(tb->device);
+  // removals in host memory: one DMA into the state's device slot (stream
+  // ordered) instead of every CTA reading them over the host link
+  if (removed && tb->Wd) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, removed) != cudaSuccess) {
+      cudaGetLastError();
+      a.type = cudaMemoryTypeUnregistered;
+    }
+    if (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered) {
+      CUDA_TRY(cudaMemcpyAsync(s->h.slot, removed, (size_t)tb->Wd * 8, cudaMemcpyHostToDevice, s->stream));
+      removed = s->h.slot;
+    }
+  }
   return enqueue_single(tb, s, removed, 0, out_dom, out_pruned, out_status, 0, false);
 }
 

@@ -181,8 +181,10 @@ def _dev_ptr(t):
     if t is None:
         return None
     if hasattr(t, "data_ptr"):
-        if not t.is_cuda or not t.is_contiguous():
-            raise ValueError("device buffers must be contiguous CUDA tensors")
+        # device memory, or pinned host memory (device-accessible under unified
+        # addressing: the kernels read / write it in place, zero-copy)
+        if not (t.is_cuda or t.is_pinned()) or not t.is_contiguous():
+            raise ValueError("device buffers must be contiguous CUDA tensors or pinned host tensors")
         return ctypes.c_void_p(t.data_ptr())
     return ctypes.c_void_p(int(t))
 

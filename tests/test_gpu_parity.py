@@ -226,8 +226,53 @@ def test_config3_bulk_full_size(c3, fast):
             assert int(sd.item()) == (CT_OK if ok else CT_FAIL)
             if ok:
                 assert np.array_equal(bitmap_to_member(outd.cpu().numpy().view(np.uint64), p.d), dout)
+            # and on pinned host buffers (zero-copy; bench.py's e2e calls)
+            st.copy_from(tab.root)
+            remh = torch.from_numpy(member_to_bitmap(rem, p.d).view(np.int64)).pin_memory()
+            outh = torch.zeros(wd, dtype=torch.int64).pin_memory()
+            prh = torch.zeros(wd, dtype=torch.int64).pin_memory()
+            sh = torch.full((1,), -1, dtype=torch.int32).pin_memory()
+            st.propagate_async(remh, outh, prh, sh)
+            st.synchronize()
+            assert int(sh.item()) == (CT_OK if ok else CT_FAIL)
+            if ok:
+                assert np.array_equal(bitmap_to_member(outh.numpy().view(np.uint64), p.d), dout)
+                assert np.array_equal(bitmap_to_member(prh.numpy().view(np.uint64), p.d), din & (1 - dout))
             out_dev_checked = True
     # a few walk calls continuing from the last bulk state
+    st.close()
+    tab.close()
+
+
+@pytest.mark.parametrize("path", [dict(), dict(_grid_fused=True), dict(_grid_fused=True, _fast=False),
+                                  dict(_wide=True)], ids=["small", "fast", "fused", "wide"])
+def test_pipelined_pinned_host_calls(path):
+    """Many ct_propagate_async calls in flight on pinned host buffers (the
+    kernels read the removals from and write status/domains/pruned to host
+    memory), each from the root, checked against the oracle after one sync."""
+    import torch
+    p = random_table(4, 40, 30_000, seed=17)
+    tab = make(p, **path)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rng = Rng(5)
+    st = tab.root.clone()
+    n, wd = 24, tab.Wd
+    rems = [bulk_removal(rng, root_m, p.d, q=0.3) for _ in range(n)]
+    h_rem = torch.from_numpy(np.stack([member_to_bitmap(r, p.d) for r in rems]).view(np.int64)).pin_memory()
+    h_dom = torch.zeros((n, wd), dtype=torch.int64).pin_memory()
+    h_pr = torch.zeros((n, wd), dtype=torch.int64).pin_memory()
+    h_st = torch.full((n,), -1, dtype=torch.int32).pin_memory()
+    for k in range(n):
+        st.copy_from(tab.root)
+        st.propagate_async(h_rem[k], h_dom[k], h_pr[k], h_st[k])
+    st.synchronize()
+    for k in range(n):
+        din = root_m & (1 - rems[k])
+        ok, dout, _ = oracle_call(p, din)
+        assert int(h_st[k]) == (CT_OK if ok else CT_FAIL), k
+        if ok:
+            assert np.array_equal(bitmap_to_member(h_dom[k].numpy().view(np.uint64), p.d), dout), k
+            assert np.array_equal(bitmap_to_member(h_pr[k].numpy().view(np.uint64), p.d), din & (1 - dout)), k
     st.close()
     tab.close()
 

@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "pipelined or config3_bulk or walk_small" > gpurun_out/tests.log 2>&1; echo "rc=$?"; tail -3 gpurun_out/tests.log
+timeout 600 python bench.py --steps 200 --warmup 10 --skip-cpu --skip-latency 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e'])"
