@@ -271,11 +271,16 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
   // this thread's first domain word and removal word are loaded before
   // anything waits: the removals may sit in mapped host memory (sync call)
   uint64_t dm0 = 0, rm0 = 0;
+  int wv0 = 0, rv0 = 0;   // this thread's first word's / row's variable, in flight with the rest
   if (tid < Wd) {
     dm0 = st.dom[tid];
     rm0 = gdom ? ~__ldcg(gdom + tb.gword[tid]) : (rem ? rem[tid] : 0ull);
+    wv0 = tb.wordVar[tid];
   }
+  if (tid < tb.R) rv0 = tb.rowVar[tid];
+  __shared__ int s_L;
   if (tid == 0) {
+    s_L = c->L;
     s_dead = c->dead;
     s_fail = 0;
     s_ngroups = 0;
@@ -303,7 +308,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
     const uint64_t dm = k == tid ? dm0 : st.dom[k];
     // model tables: a value is removed iff the shared (global) domain lost it
     const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
-    const int x = tb.wordVar[k];
+    const int x = k == tid ? wv0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     s_din[k] = di;
     s_dl[k] = delta;
@@ -346,7 +351,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
       bool u = false, f = false, useDelta = false;
       int x = 0;
       if (r < tb.R) {
-        x = tb.rowVar[r];
+        x = r == tid ? rv0 : tb.rowVar[r];
         const int a = r - s_rb[x];
         const int w = s_do[x] + (a >> 6), b = a & 63;
         const int cd = s_cd[x], cs = s_cs[x];
@@ -376,7 +381,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
     c->ngroups = s_ngroups;
     c->nrows = nrows;
     c->nitems = nitems;
-    c->L_in = c->L;
+    c->L_in = s_L;
     c->L_out = 0;
     c->tile_ctr = 0;
     c->nscan = 0;
@@ -848,20 +853,30 @@ __device__ void dev_scan(const TableDev &tb, const StateDev &st, int gw, int nw)
 // no valid tuple (sup[r] = 0 after the cross-shard OR); then lastDom <- dom.
 // kDense: the state was updated densely (batch path, ct_batch.cuh): its index
 // becomes the identity over all W2 blocks instead of the compacted one.
+// Returns the call's status (every thread).  All inputs are final when it is
+// entered, so they are loaded in one round trip up front.
 template <int NT, bool kDense = false>
-__device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *__restrict__ out_dom,
-                             uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status, uint64_t *smem) {
+__device__ int dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *__restrict__ out_dom,
+                            uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status, uint64_t *smem) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
   uint64_t *s_nd = smem;
   int32_t *s_cs = reinterpret_cast<int32_t *>(smem + Wd);
   int32_t *s_rb = s_cs + n;
   int32_t *s_do = s_rb + n + 1;
-  __shared__ int s_status, s_noop;
+  __shared__ int s_status, s_noop, s_lout;
+  // this thread's first support row (flag + variable)
+  uint8_t sp0 = 1;
+  int x0 = 0;
+  if (tid < tb.R) {
+    sp0 = __ldcg(st.sup + tid);
+    x0 = tb.rowVar[tid];
+  }
   if (tid == 0) {
-    // the four flags are loaded together (one round trip, not a chain)
+    // the flags are loaded together (one round trip, not a chain)
     const int skip = __ldcg(&c->skip), ff = __ldcg(&c->fail_fast), noop = __ldcg(&c->noop);
     const int nonempty = __ldcg(st.sup + tb.R);
+    s_lout = __ldcg(&c->L_out);
     int s;
     if (skip) s = -5;                  // CT_ESTATE
     else if (ff) s = 1;                // CT_FAIL
@@ -887,13 +902,13 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
       c->last_status = status;
       if (out_status) *out_status = status;
     }
-    return;
+    return status;
   }
   const bool noop = s_noop != 0;
   if (!noop) {
     for (int r = tid; r < tb.R; r += NT) {
-      const uint8_t sp = __ldcg(st.sup + r);
-      const int x = tb.rowVar[r];
+      const uint8_t sp = r == tid ? sp0 : __ldcg(st.sup + r);
+      const int x = r == tid ? x0 : tb.rowVar[r];
       if (!sp && s_cs[x] > 1) {                  // x in s_sup (Alg. 3 L1), a unsupported
         const int a = r - s_rb[x];
         const int w = s_do[x] + (a >> 6);
@@ -923,13 +938,14 @@ __device__ void dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *_
       c->identity = 1;
     } else if (!noop && tb.use_index) {
       c->parity ^= 1;
-      c->L = __ldcg(&c->L_out);
+      c->L = s_lout;
       c->identity = 0;
     }
     c->calls += 1;
     c->last_status = 0;
     if (out_status) *out_status = 0;
   }
+  return 0;
 }
 
 // ------------------------------------------------------------------ kernels: one per phase (batches)

@@ -241,16 +241,15 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const TableDev &tb = md.tabs[k];
       const StateDev &st = md.sts[k];
-      dev_finalize<kFusedTPB>(tb, st, nullptr, nullptr, nullptr, smem);
-      __syncthreads();
-      if (__ldcg(&st.ctl->last_status) != 0) {
+      const int gw0 = tid < tb.Wd ? tb.gword[tid] : 0;   // in flight during dev_finalize
+      if (dev_finalize<kFusedTPB>(tb, st, nullptr, nullptr, nullptr, smem) != 0) {
         if (tid == 0) atomicExch(&mc->failp[it & 1], 1);
       } else {
         for (int w = tid; w < tb.Wd; w += kFusedTPB) {
           const uint64_t nd = smem[w];   // dev_finalize's new domains (also stored in st.dom)
-          const uint64_t g0 = __ldcg(md.gdom + tb.gword[w]);
-          if ((g0 & nd) != g0) {
-            const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + tb.gword[w]), nd);
+          const int gw = w == tid ? gw0 : tb.gword[w];
+          if (nd != ~0ull) {
+            const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + gw), nd);
             if ((old & nd) != old) mc->changed[it & 1] = 1;
           }
         }
