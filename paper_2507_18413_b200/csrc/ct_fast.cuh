@@ -94,7 +94,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int NW>
 struct FastShT {
   int dead, fail, noop, go, ngroups, nrows, nitems;
-  int L, ident, par, Lout, nscan, last, below;
+  int L, ident, par, Lout, nscan, last, below, anymiss;
   int red[NW];                   // block-reduction scratch
   uint32_t woff[NW];
   uint64_t scan[NW];
@@ -158,9 +158,11 @@ __device__ __forceinline__ int row_var(const int32_t *rb, int n, int r) {
 // acquire + the L1 invalidate ptxas emits with it: it then reads the others'
 // writes), one arrival counter, and a generation word with one copy per group
 // of CTAs in lines of its own that the waiting CTAs poll (polling a counter's
-// own line, or 740 CTAs polling one line, slows the release).  The last arrival resets the
-// counter, optionally publishes `mode` = leader_mode() in a third line, and
-// bumps the generation with a release store; every CTA returns the mode and
+// own line, or 740 CTAs polling one line, slows the release).  Each CTA may
+// add a 0/1 flag (*extra_flag, a shared int) with its arrival (e.g. "I queued a probe miss").  The
+// last arrival resets the counter, computes the one-bit `mode` =
+// leader_mode(sum of the flags) and bumps the generation, whose low bit
+// carries the mode (no second word to read after the release); every CTA returns the mode and
 // `leader` tells the releasing CTA it was the last.  Counters return to 0
 // after each barrier, so the memory only has to be zeroed once (at state
 // creation).
@@ -174,26 +176,31 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
 }
 
 template <typename F>
-__device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mode, int &leader, int *s_mode) {
-  __syncthreads();
+__device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mode, int &leader, int *s_mode,
+                                                      const int *extra_flag = nullptr) {
+  __syncthreads();   // also orders the block's writes of *extra_flag before thread 0 reads it
   if (threadIdx.x == 0) {
+    const uint32_t extra = (extra_flag && *(volatile const int *)extra_flag) ? 1u : 0u;
     uint32_t *cnt = bar;
-    uint32_t *mode = bar + (kBarGroups + 2) * kBarLine;
     // the generation word has kBarGroups copies (lines 1..kBarGroups): each CTA
-    // polls its group's copy, so the polling is spread over several L2 slices
+    // polls its group's copy, so the polling is spread over several L2 slices.
+    // Its low bit carries the mode, so nobody reads a second word after release.
     uint32_t *mygen = bar + (1 + blockIdx.x % kBarGroups) * kBarLine;
     const uint32_t my_gen = ld_acquire_u32(mygen);
     int last = 0;
-    if (atom_add_acqrel(cnt, 1u) == gridDim.x - 1) {
+    uint32_t g;
+    // low 16 bits: arrivals; high bits: the sum of the CTAs' `extra` (0/1 flags)
+    const uint32_t old = atom_add_acqrel(cnt, 1u + (extra << 16));
+    if ((old & 0xffffu) == gridDim.x - 1) {
       *cnt = 0;
-      *mode = (uint32_t)leader_mode();
+      g = ((((my_gen >> 1) + 1u) << 1)) | ((uint32_t)leader_mode((old >> 16) + extra) & 1u);
       __threadfence();   // one release fence for all the generation copies
-      for (int g = 0; g < kBarGroups; ++g) *(volatile uint32_t *)(bar + (1 + g) * kBarLine) = my_gen + 1;
+      for (int q = 0; q < kBarGroups; ++q) *(volatile uint32_t *)(bar + (1 + q) * kBarLine) = g;
       last = 1;
     } else {
-      while (ld_acquire_u32(mygen) == my_gen) __nanosleep(32);
+      while ((g = ld_acquire_u32(mygen)) == my_gen) __nanosleep(32);
     }
-    *s_mode = (int)__ldcg(mode);
+    *s_mode = (int)(g & 1u);
     leader = last;
   }
   __syncthreads();
@@ -203,7 +210,7 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
 __device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
   __shared__ int s_mode;
   int leader;
-  fast_grid_barrier_mode(bar, [] { return 0; }, leader, &s_mode);
+  fast_grid_barrier_mode(bar, [](uint32_t) { return 0; }, leader, &s_mode);
 }
 
 // Adds a per-thread counter to a global 64-bit counter with ONE atomic per CTA
@@ -256,6 +263,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     fs.dead = c->dead;
     fs.fail = 0;
     fs.ngroups = 0;
+    fs.anymiss = 0;
     fs.L = c->L;
     fs.ident = c->identity;
     fs.par = c->parity;
@@ -778,7 +786,10 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
           }
         }
         if (wpi == 1) {
-          if (j < per_cta && lane == 0 && hit < 0 && may_miss) st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+          if (j < per_cta && lane == 0 && hit < 0 && may_miss) {
+            st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+            fs.anymiss = 1;
+          }
         } else {
           // the item is a miss only if none of its wpi warps found a support
           __syncthreads();
@@ -787,7 +798,10 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
           if (j < per_cta && q == 0 && lane == 0 && may_miss) {
             int any = 0;
             for (int w = warp; w < warp + wpi; ++w) any |= fs.red[w];
-            if (!any) st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+            if (!any) {
+              st.scanlist[atomicAdd(&c->nscan, 1)] = row;
+              fs.anymiss = 1;
+            }
           }
         }
       }
@@ -804,8 +818,8 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     // exit) and finalizes at once, then writes its own entries.
     if (Lout > 0 && may_miss && kFastStop > -3) {
       int leader = 0;
-      const int mode = fast_grid_barrier_mode(st.bar, [&] { return __ldcg(&c->nscan) == 0 ? 1 : 0; }, leader,
-                                              &fs.nscan);
+      const int mode = fast_grid_barrier_mode(st.bar, [](uint32_t misses) { return misses == 0 ? 1 : 0; }, leader,
+                                              &fs.nscan, &fs.anymiss);
       if (t0) c->tph[4] = globaltimer();
       FAST_TRACE(6);
       if (mode == 1) {

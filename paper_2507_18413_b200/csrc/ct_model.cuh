@@ -132,6 +132,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
   __shared__ uint32_t s_woff[kUpdTPB / 32];
   __shared__ uint32_t s_excl;
   __shared__ int s_brk;
+  __shared__ int s_miss;   // this CTA queued a probe miss (summed by the barrier)
   const int ntab = md.ntab;
   const bool t0 = blockIdx.x == 0 && tid == 0;
   unsigned long long tp = t0 ? globaltimer() : 0ull;
@@ -199,6 +200,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
       s_cnt[tid] = (s_fp[tid].go && s_fp[tid].Lout > 0) ? s_fp[tid].nitems : 0;
     }
+    if (tid == 0) s_miss = 0;
     __syncthreads();
     model_prefix(s_cnt, s_pre, ntab);
     if (blockIdx.x == 0 && tid < ntab && s_fp[tid].go) md.sts[tid].sup[md.tabs[tid].R] = s_fp[tid].Lout > 0;
@@ -206,7 +208,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       uint32_t n_loads = 0;
       for (int64_t g = gw; g < s_pre[ntab]; g += nw) {
         const int k = find_table(s_pre, ntab, g);
-        probe_item_fused(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads, &mc->miss[it & 1]);
+        probe_item_fused(md.tabs[k], md.sts[k], s_fp[k], (int)(g - s_pre[k]), n_loads, &s_miss);
       }
     }
     // the barrier's last arrival checks whether any table queued a miss; if
@@ -214,9 +216,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     {
       int leader = 0;
       const int mode = fast_grid_barrier_mode(
-          md.bar,
-          [&] { return __ldcg(&mc->miss[it & 1]) ? 0 : 1; },
-          leader, &s_brk);
+          md.bar, [](uint32_t misses) { return misses ? 0 : 1; }, leader, &s_brk, &s_miss);
       lap(2);
       if (mode == 1) goto finalize_phase;
     }
