@@ -935,7 +935,10 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
       cudaGetLastError();
       a.type = cudaMemoryTypeUnregistered;
     }
-    if (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered) {
+    // (pinned removals read in place by every CTA instead: C3 bulk e2e 8.7k vs
+    // 9.8k with the DMA; CT_HOST_ZERO_COPY=1 selects it for experiments)
+    static const bool zero_copy = getenv("CT_HOST_ZERO_COPY") != nullptr;
+    if (a.type == cudaMemoryTypeUnregistered || (a.type == cudaMemoryTypeHost && !zero_copy)) {
       CUDA_TRY(cudaMemcpyAsync(s->h.slot, removed, (size_t)tb->Wd * 8, cudaMemcpyHostToDevice, s->stream));
       removed = s->h.slot;
     }
