@@ -128,7 +128,6 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
   __shared__ FiltParams s_fp[kMaxModelTables];
   __shared__ int64_t s_pre[kMaxModelTables + 1];
   __shared__ int64_t s_cnt[kMaxModelTables];
-  __shared__ int s_tile;
   __shared__ uint32_t s_woff[kUpdTPB / 32];
   __shared__ uint32_t s_excl;
   __shared__ int s_brk;
@@ -183,11 +182,10 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     model_prefix(s_cnt, s_pre, ntab);
     {
       uint32_t n_loads = 0, n_writes = 0;
-      while (true) {
-        if (tid == 0) s_tile = atomicAdd(&mc->tile_ctr, 1);
-        __syncthreads();
-        const int g = s_tile;
-        if (g >= s_pre[ntab]) break;
+      // static round-robin over the pooled tiles (no counter round trip per
+      // tile; every CTA takes its tiles in increasing order, so the chained
+      // scan's look-back only ever waits on lower tiles already taken)
+      for (int64_t g = blockIdx.x; g < s_pre[ntab]; g += gridDim.x) {
         const int k = find_table(s_pre, ntab, g);
         update_tile(md.tabs[k], md.sts[k], s_up[k], (int)(g - s_pre[k]), s_woff, &s_excl, n_loads, n_writes);
       }
