@@ -473,11 +473,15 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, Sear
         __syncthreads();
         continue;
       }
-      // push: trail level d + 1 = the state before this branch
-      const unsigned long long tc = globaltimer();
-      search_copy(sd.snaps + (int64_t)(c.d + 1) * sd.pool16, sd.pool, sd.pool16);
-      model_barrier(mc);   // the snapshot is complete before the domains change
-      if (blockIdx.x == 0 && tid == 0) mc->ph[5] += globaltimer() - tc;
+      // push: trail level d + 1 = the state before this branch.  The second
+      // branch comes straight from kSPop, which restored the pool FROM that
+      // level (and ended with a barrier): the snapshot already holds it.
+      if (f.branch == 0) {
+        const unsigned long long tc = globaltimer();
+        search_copy(sd.snaps + (int64_t)(c.d + 1) * sd.pool16, sd.pool, sd.pool16);
+        model_barrier(mc);   // the snapshot is complete before the domains change
+        if (blockIdx.x == 0 && tid == 0) mc->ph[5] += globaltimer() - tc;
+      }
       // block 0 applies the decision to the shared domains (visible to all
       // after the fixpoint's opening barrier)
       if (blockIdx.x == 0) {
