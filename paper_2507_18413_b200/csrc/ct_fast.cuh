@@ -159,7 +159,8 @@ __device__ __forceinline__ int row_var(const int32_t *rb, int n, int r) {
 // writes), one arrival counter, and a generation word with one copy per group
 // of CTAs in lines of its own that the waiting CTAs poll (polling a counter's
 // own line, or 740 CTAs polling one line, slows the release).  Each CTA may
-// add a 0/1 flag (*extra_flag, a shared int) with its arrival (e.g. "I queued a probe miss").  The
+// add a small count (*extra_flag, a shared int; the sum over the grid must stay
+// below 2^16) with its arrival (e.g. "I queued a probe miss").  The
 // last arrival resets the counter, computes the one-bit `mode` =
 // leader_mode(sum of the flags) and bumps the generation, whose low bit
 // carries the mode (no second word to read after the release); every CTA returns the mode and
@@ -180,7 +181,7 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
                                                       const int *extra_flag = nullptr) {
   __syncthreads();   // also orders the block's writes of *extra_flag before thread 0 reads it
   if (threadIdx.x == 0) {
-    const uint32_t extra = (extra_flag && *(volatile const int *)extra_flag) ? 1u : 0u;
+    const uint32_t extra = extra_flag ? (uint32_t)*(volatile const int *)extra_flag : 0u;
     uint32_t *cnt = bar;
     // the generation word has kBarGroups copies (lines 1..kBarGroups): each CTA
     // polls its group's copy, so the polling is spread over several L2 slices.
@@ -189,7 +190,7 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
     const uint32_t my_gen = ld_acquire_u32(mygen);
     int last = 0;
     uint32_t g;
-    // low 16 bits: arrivals; high bits: the sum of the CTAs' `extra` (0/1 flags)
+    // low 16 bits: arrivals; high 16 bits: the sum of the CTAs' `extra` values
     const uint32_t old = atom_add_acqrel(cnt, 1u + (extra << 16));
     if ((old & 0xffffu) == gridDim.x - 1) {
       *cnt = 0;

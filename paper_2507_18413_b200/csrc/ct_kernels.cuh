@@ -253,9 +253,11 @@ __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int
 // Row-parallel: every support row decides on its own whether it enters the
 // update list (x in s_val, value in the chosen branch) and the filter list
 // (x in s_sup, value in D_x); one block scan gives the ordered positions.
+// Returns (every thread) 0: the call updates, 1: no-op, 2: FAIL (a domain
+// became empty), 3: the state is dead (skip).
 template <int NT>
-__device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
-                           int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr) {
+__device__ int dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
+                          int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
   uint64_t *s_din = smem;                       // D_x = dom ∧ ¬removed
@@ -297,7 +299,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
       c->noop = 0;
       c->fail_fast = 0;
     }
-    return;
+    return 3;
   }
   // per-call scratch
   for (int r = tid; r <= tb.R; r += NT) st.sup[r] = 0;
@@ -389,6 +391,7 @@ __device__ void dev_ingest(const TableDev &tb, const StateDev &st, const uint64_
     c->upd_writes = 0;
     c->scan_loads = 0;
   }
+  return s_fail ? 2 : (noop ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ a2: ingest by one warp

@@ -132,6 +132,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
   __shared__ uint32_t s_excl;
   __shared__ int s_brk;
   __shared__ int s_miss;   // this CTA queued a probe miss (summed by the barrier)
+  __shared__ int s_cnt_ing, s_cnt_fin;   // this CTA's ingest / finalize verdicts (summed by the barrier)
   const int ntab = md.ntab;
   const bool t0 = blockIdx.x == 0 && tid == 0;
   unsigned long long tp = t0 ? globaltimer() : 0ull;
@@ -144,33 +145,34 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
   };
 
   for (int it = 0; it < max_iters; ++it) {
-    // ---- ingest (a2): one block per table, removals = values the shared domains lost
-    if (blockIdx.x == 0 && tid == 0) {
-      mc->active[(it + 1) & 1] = 0;
-      mc->failp[(it + 1) & 1] = 0;
-      mc->miss[(it + 1) & 1] = 0;
-      mc->changed[it & 1] = 0;
-    }
+    // ---- ingest (a2): one block per table, removals = values the shared domains lost.
+    // Each CTA's verdicts ride on its barrier arrival (active tables + 256 x
+    // failed tables); the releasing CTA decides whether the fixpoint stops
+    // (a FAIL, or no table has anything to do) and keeps the statistics.
+    if (tid == 0) s_cnt_ing = 0;
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
-      dev_ingest<kFusedTPB>(md.tabs[k], md.sts[k], nullptr, 0, smem, md.gdom);
+      const int r = dev_ingest<kFusedTPB>(md.tabs[k], md.sts[k], nullptr, 0, smem, md.gdom);
       __syncthreads();
-      if (tid == 0) {
-        const Ctl *c = md.sts[k].ctl;
-        if (c->fail_fast) atomicExch(&mc->failp[it & 1], 1);
-        else if (!c->noop && !c->skip) atomicAdd(&mc->active[it & 1], 1);
-      }
+      if (tid == 0) s_cnt_ing += r == 2 ? 256 : (r == 0 ? 1 : 0);
     }
-    model_barrier(mc);
-    lap(0);
-    if (tid == 0) {
-      s_brk = __ldcg(&mc->failp[it & 1]) || __ldcg(&mc->active[it & 1]) == 0;
-      if (s_brk && blockIdx.x == 0) mc->fail = __ldcg(&mc->failp[it & 1]);   // read after the final barrier
-    }
-    __syncthreads();
-    if (s_brk) break;
-    if (blockIdx.x == 0 && tid == 0) {
-      mc->iters = it + 1;
-      mc->table_calls += __ldcg(&mc->active[it & 1]);
+    {
+      int leader = 0;
+      const int brk = fast_grid_barrier_mode(
+          md.bar,
+          [&](uint32_t v) {
+            const uint32_t active = v & 255u, fails = v >> 8;
+            const int b = fails > 0 || active == 0;
+            if (b) {
+              mc->fail = fails > 0;
+            } else {
+              mc->iters = it + 1;
+              mc->table_calls = __ldcg(&mc->table_calls) + (int)active;
+            }
+            return b;
+          },
+          leader, &s_brk, &s_cnt_ing);
+      lap(0);
+      if (brk) break;
     }
     // ---- update (a3-a5): tiles of all tables pooled over the grid
     // (every table's parameters loaded by its own thread: one round trip)
@@ -235,37 +237,47 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     model_barrier(mc);
     lap(3);
   finalize_phase:
-    // ---- finalize (a6c-a7): one block per table; AND the new domains into the shared ones
+    // ---- finalize (a6c-a7): one block per table; AND the new domains into the shared ones.
+    // Verdicts on the barrier arrival again: CTAs that removed a value from
+    // the shared domains + 256 x failed tables.
+    if (tid == 0) s_cnt_fin = 0;
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const TableDev &tb = md.tabs[k];
       const StateDev &st = md.sts[k];
       const int gw0 = tid < tb.Wd ? tb.gword[tid] : 0;   // in flight during dev_finalize
       if (dev_finalize<kFusedTPB>(tb, st, nullptr, nullptr, nullptr, smem) != 0) {
-        if (tid == 0) atomicExch(&mc->failp[it & 1], 1);
+        if (tid == 0) atomicAdd(&s_cnt_fin, 256);
       } else {
         for (int w = tid; w < tb.Wd; w += kFusedTPB) {
           const uint64_t nd = smem[w];   // dev_finalize's new domains (also stored in st.dom)
           const int gw = w == tid ? gw0 : tb.gword[w];
           if (nd != ~0ull) {
             const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + gw), nd);
-            if ((old & nd) != old) mc->changed[it & 1] = 1;
+            if ((old & nd) != old) atomicOr(&s_cnt_fin, 1);
           }
         }
       }
       __syncthreads();
     }
-    model_barrier(mc);
-    lap(4);
-    // stop on a failure, or at the fixpoint: no table removed a value from the
-    // shared domains, so every table is a no-op in the next iteration
-    if (tid == 0) {
-      s_brk = __ldcg(&mc->failp[it & 1]) || !__ldcg(&mc->changed[it & 1]);
-      if (s_brk && blockIdx.x == 0) mc->fail = __ldcg(&mc->failp[it & 1]);
+    {
+      // stop on a failure, or at the fixpoint: no table removed a value from
+      // the shared domains, so every table is a no-op in the next iteration
+      int leader = 0;
+      const int brk = fast_grid_barrier_mode(
+          md.bar,
+          [&](uint32_t v) {
+            const int b = (v >> 8) > 0 || (v & 255u) == 0;
+            if (b) mc->fail = (v >> 8) > 0;
+            return b;
+          },
+          leader, &s_brk, &s_cnt_fin);
+      lap(4);
+      if (brk) break;
     }
-    __syncthreads();
-    if (s_brk) break;
   }
-  model_barrier(mc);   // mc->fail (the verdict) is read after this barrier
+  // the verdict and the statistics were written by the releasing CTA of the
+  // deciding barrier: every CTA reads them after returning.  (The caller must
+  // pass another grid barrier before the next model_reset_ctl.)
 }
 
 // Block 0: reset the per-fixpoint control fields (before a grid barrier).
