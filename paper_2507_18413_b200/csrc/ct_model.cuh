@@ -17,20 +17,14 @@ namespace ctk {
 constexpr int kMaxModelTables = 64;
 
 struct ModelCtl {
-  uint32_t bar_count, bar_gen;   // grid barrier
-  int32_t active[2];             // tables with work, by iteration parity
   int32_t fail;
   int32_t iters;                 // Jacobi iterations of the last fixpoint
-  int32_t tile_ctr;              // pooled update tiles
   int32_t status;
   long long table_calls;         // non-no-op table propagations in the last fixpoint
   unsigned long long t0, t1;     // %globaltimer at start / end
   unsigned long long ph[6];      // device search: ns in ingest, update, probe, scan, finalize, trail copies
-  int32_t changed[2];            // the shared domains lost a value in the iteration, by parity
-  int32_t miss[2];               // some probe queued a miss in the iteration, by parity
-  int32_t failp[2];              // a table failed in the iteration, by parity (loop control: a CTA
-                                 // already in the next iteration must not change what a slower
-                                 // one reads at the end of this one)
+  // (the per-iteration verdicts -- active / failed tables, probe misses,
+  // shared-domain changes -- travel on the grid barrier's arrivals)
 };
 static_assert(sizeof(ModelCtl) <= 256, "ModelCtl must fit its 256-byte slot");
 
@@ -194,7 +188,6 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     }
     model_barrier(mc);
     lap(1);
-    if (blockIdx.x == 0 && tid == 0) mc->tile_ctr = 0;
     // ---- probe (a6a): items of all tables pooled over the warps
     if (tid < ntab) {
       s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
@@ -284,12 +277,8 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
 __device__ __forceinline__ void model_reset_ctl(ModelCtl *mc) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     mc->fail = 0;
-    mc->failp[0] = mc->failp[1] = 0;
-    mc->miss[0] = mc->miss[1] = 0;
     mc->iters = 0;
     mc->table_calls = 0;
-    mc->active[0] = mc->active[1] = 0;
-    mc->tile_ctr = 0;
   }
 }
 
