@@ -72,6 +72,7 @@ struct TableDev {
   int32_t use_res, use_index;
   int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
   const int32_t *gword;     // [Wd] model tables only: global domain word of each domain word
+  const int32_t *gshared;   // [Wd] model tables only: 1 if another table also constrains the word's variable
 };
 
 // Per-state control block (device).  The first fields up to last_status persist

@@ -237,7 +237,8 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const TableDev &tb = md.tabs[k];
       const StateDev &st = md.sts[k];
-      const int gw0 = tid < tb.Wd ? tb.gword[tid] : 0;   // in flight during dev_finalize
+      // in flight during dev_finalize
+      const int gw0 = tid < tb.Wd ? tb.gword[tid] : 0, gs0 = tid < tb.Wd ? tb.gshared[tid] : 0;
       if (dev_finalize<kFusedTPB>(tb, st, nullptr, nullptr, nullptr, smem) != 0) {
         if (tid == 0) atomicAdd(&s_cnt_fin, 256);
       } else {
@@ -246,7 +247,10 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
           const int gw = w == tid ? gw0 : tb.gword[w];
           if (nd != ~0ull) {
             const uint64_t old = atomicAnd(reinterpret_cast<unsigned long long *>(md.gdom + gw), nd);
-            if ((old & nd) != old) atomicOr(&s_cnt_fin, 1);
+            // a removal counts as a change only if another table constrains
+            // the variable: a variable of this table alone cannot make any
+            // table active in the next iteration (this one already has nd)
+            if ((old & nd) != old && (w == tid ? gs0 : tb.gshared[w])) atomicOr(&s_cnt_fin, 1);
           }
         }
       }

@@ -1567,7 +1567,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   const size_t tdev = sizeof(TableDev) * n_tables, sdev = sizeof(StateDev) * n_tables;
   size_t gw_total = 0;
   for (ct_table *t : m->tabs) gw_total += (size_t)std::max(t->Wd, 1);
-  m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + round_up((int64_t)gw_total * 4, 256) +
+  m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + 2 * round_up((int64_t)gw_total * 4, 256) +
                   (size_t)kBarWords * 4;
   if (cudaMalloc(&m->meta, m->meta_bytes) != cudaSuccess) return bail(fail(CT_ENOMEM, "model metadata allocation failed"));
   cudaMemset(m->meta, 0, m->meta_bytes);
@@ -1575,18 +1575,30 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   StateDev *d_sts = (StateDev *)(m->meta + tdev);
   ModelCtl *d_mc = (ModelCtl *)(m->meta + round_up((int64_t)(tdev + sdev), 256));
   int32_t *d_gw = (int32_t *)((char *)d_mc + 256);
+  int32_t *d_gs = (int32_t *)((char *)d_gw + round_up((int64_t)gw_total * 4, 256));
+  std::vector<int32_t> var_uses(n_vars, 0);   // scope positions per variable over all tables
+  sc = scopes;
+  for (int k = 0; k < n_tables; ++k) {
+    for (int i = 0; i < m->tabs[k]->n; ++i) var_uses[sc[i]]++;
+    sc += m->tabs[k]->n;
+  }
   std::vector<TableDev> htabs(n_tables);
   std::vector<StateDev> hsts(n_tables);
   sc = scopes;
   size_t gpos = 0;
   for (int k = 0; k < n_tables; ++k) {
     ct_table *t = m->tabs[k];
-    std::vector<int32_t> gw(std::max(t->Wd, 1), 0);
+    std::vector<int32_t> gw(std::max(t->Wd, 1), 0), gs(std::max(t->Wd, 1), 0);
     for (int i = 0; i < t->n; ++i)
-      for (int w = t->domOff[i]; w < t->domOff[i + 1]; ++w) gw[w] = m->gOff[sc[i]] + (w - t->domOff[i]);
+      for (int w = t->domOff[i]; w < t->domOff[i + 1]; ++w) {
+        gw[w] = m->gOff[sc[i]] + (w - t->domOff[i]);
+        gs[w] = var_uses[sc[i]] > 1;
+      }
     cudaMemcpy(d_gw + gpos, gw.data(), gw.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_gs + gpos, gs.data(), gs.size() * 4, cudaMemcpyHostToDevice);
     htabs[k] = t->dev;
     htabs[k].gword = d_gw + gpos;
+    htabs[k].gshared = d_gs + gpos;
     hsts[k] = make_desc(t, m->pool + m->off[k]);
     gpos += gw.size();
     sc += t->n;
@@ -1600,7 +1612,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   m->md.sts = d_sts;
   m->md.gdom = (uint64_t *)(m->pool + m->gdom_off);
   m->md.mc = d_mc;
-  m->md.bar = (uint32_t *)((char *)d_gw + round_up((int64_t)gw_total * 4, 256));
+  m->md.bar = (uint32_t *)((char *)d_gs + round_up((int64_t)gw_total * 4, 256));
   m->dom = gdom;
   // ---- launch geometry
   size_t smem = 0;
