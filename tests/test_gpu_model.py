@@ -132,3 +132,61 @@ def test_device_search_falls_back_when_the_trail_is_short():
         assert getattr(a[2], f) == getattr(b[2], f), f
     assert a[2].trace_hash == ref["trace_hash"]
     M.close()
+
+
+@pytest.mark.parametrize("grid", [1, 3])
+def test_model_grid_smaller_than_table_count(grid):
+    """Model kernels on fewer CTAs than tables (CT_MODEL_GRID, read at model
+    creation): one CTA ingests / finalizes several tables, so its barrier
+    arrival carries several tables' verdicts.  Fixpoints and the DFS trace vs
+    the oracle."""
+    import os
+    m = csp_model(10, 8, 6, 400, seed=91, arities=[3, 4, 2, 5, 3, 4])
+    os.environ["CT_MODEL_GRID"] = str(grid)
+    try:
+        M = _model(m)
+    finally:
+        os.environ.pop("CT_MODEL_GRID", None)
+    ok, root = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], np.ones(int(m["vd"].sum()), np.uint8))
+    assert (M.root_status == CT_OK) == ok
+    if ok:
+        rng = Rng(7)
+        for trial in range(10):
+            din = root & (rng.uniform(root.size, 3) > 0).astype(np.uint8)
+            ok2, dout = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], din)
+            M.push()
+            st, gd = M.fixpoint(member_to_bitmap(din, m["vd"]))
+            assert st == (CT_OK if ok2 else CT_FAIL), trial
+            if ok2:
+                assert np.array_equal(bitmap_to_member(gd, m["vd"]), dout), trial
+            M.pop()
+        for driver in ("device", "host"):
+            st, sol, stats = M.search(value_order=0, max_solutions=0, driver=driver)
+            ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_solutions=0)
+            assert (stats.nodes, stats.failures, stats.solutions) == (ref["nodes"], ref["failures"],
+                                                                      len(ref["solutions"]))
+            assert stats.trace_hash == ref["trace_hash"]
+    M.close()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_private_variables_fixpoint_and_search(seed):
+    """Most variables constrained by one table only (8 variables, scopes of
+    3 + 3 + 2, i.e. independent tables): removals on such a variable do not
+    count as a shared-domain change (the fixpoint may stop a round earlier);
+    domains and the first 1500 DFS nodes' trace still equal the oracle's (the
+    full tree has ~1e5 solutions)."""
+    m = csp_model(8, 6, 3, 120, seed=300 + seed, arities=[3, 3, 2])
+    M = _model(m)
+    ok, root = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], np.ones(int(m["vd"].sum()), np.uint8))
+    assert (M.root_status == CT_OK) == ok
+    if ok:
+        assert np.array_equal(bitmap_to_member(M.root_dom, m["vd"]), root)
+        for vo in (0, 1):
+            st, sol, stats = M.search(value_order=vo, max_solutions=0, max_nodes=1500, driver="device")
+            ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=vo, max_solutions=0,
+                             max_nodes=1500)
+            assert (stats.nodes, stats.failures, stats.solutions) == (ref["nodes"], ref["failures"],
+                                                                      len(ref["solutions"]))
+            assert stats.trace_hash == ref["trace_hash"]
+    M.close()
