@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -1
+timeout 300 python tools/exp_c2.py 2>&1 | tail -3
