@@ -49,7 +49,7 @@ constexpr int kLocalRowsMax = 4096;                    // R limit of the per-CTA
 #define CT_FAST_TPB 256
 #endif
 #ifndef CT_FAST_UNROLL
-#define CT_FAST_UNROLL 12
+#define CT_FAST_UNROLL 16
 #endif
 #ifndef CT_FAST_MINB
 #define CT_FAST_MINB 3
