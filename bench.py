@@ -124,7 +124,11 @@ def ncu_traffic(workload, world, kernel):
         if "workload" in allj:
             allj = {allj["workload"]: allj}
         tj = allj.get(workload) or {}
-        if tj.get("n_gpus", 1) == world and tj.get("kernel") == kernel:
+
+        def base(name):   # "void ctk::k_bupdate<32>" / "k_bupdate" -> "k_bupdate"
+            return str(name).replace("void ", "").split("::")[-1].split("<")[0].strip()
+
+        if tj.get("n_gpus", 1) == world and base(tj.get("kernel")) == base(kernel):
             return tj.get("dram_bytes_per_launch")
     except Exception:
         pass
