@@ -39,7 +39,10 @@ constexpr int kProbeTPB = 256;
 constexpr int kScanTPB = 256;
 constexpr int kFinTPB = 1024;
 constexpr int kFusedTPB = 256;    // k_fused block size (= kUpdTPB)
-constexpr int kUpdUnroll = 8;     // support rows in flight per thread in update
+#ifndef CT_UPD_UNROLL
+#define CT_UPD_UNROLL 4
+#endif
+constexpr int kUpdUnroll = CT_UPD_UNROLL;   // support rows in flight per thread in update
 constexpr int kScanUnroll = 4;    // index entries (16-byte blocks) per lane per scan round
 constexpr int kFirstScan = 32 * kScanUnroll * 2;     // entries probe scans itself (2 rounds)
 constexpr int kScanChunk = 32 * kScanUnroll * 2;     // entries per scan work unit (2 rounds)
