@@ -20,6 +20,14 @@ Parity status per function:
   supports_row   pinned: Table 1(b) rows printed in PAPER.md L97-104.
   fixpoint       pinned: all-solutions of tiny multi-table models vs Cartesian
                  enumeration of the whole model.
+  gac / fixpoint with threads > 1 (oracle_gac_split): the same scan over
+                 contiguous tuple slices, results OR-ed; pinned equal to the
+                 single-thread functions on random instances.
+  dfs (dfs.py)   pinned: all-solutions == Cartesian enumeration; solutions in
+                 descending (indomain_max) / ascending (indomain_min)
+                 lexicographic order (input_order, sound propagation); the
+                 hand-derived Table 1 node trace; full-binary-tree node count
+                 nodes = 2 (failures + solutions) - 1; FNV-1a test vector.
 """
 from __future__ import annotations
 
@@ -41,7 +49,7 @@ def build(force: bool = False) -> str:
     """Compile ct_oracle.c with gcc (plain -O2, single-threaded)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-pthread", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -59,6 +67,10 @@ def lib():
             L.oracle_supports_row.restype = None
             L.oracle_fixpoint.argtypes = [ctypes.c_int32, P, P, ctypes.c_int32, P, P, P, P, P]
             L.oracle_fixpoint.restype = ctypes.c_int
+            L.oracle_gac_split.argtypes = [ctypes.c_int32, P, P, ctypes.c_int64, P, P, P, P, ctypes.c_int32]
+            L.oracle_gac_split.restype = ctypes.c_int
+            L.oracle_fixpoint_split.argtypes = [ctypes.c_int32, P, P, ctypes.c_int32, P, P, P, P, P, ctypes.c_int32]
+            L.oracle_fixpoint_split.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -67,8 +79,18 @@ def _p(a):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def gac(lo, d, tuples, dom_in, want_valid: bool = False):
+def host_threads() -> int:
+    """Host cores this process may use (sched_getaffinity)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:
+        return max(1, os.cpu_count() or 1)
+
+
+def gac(lo, d, tuples, dom_in, want_valid: bool = False, threads: int = 1):
     """Oracle GAC.  dom_in: uint8[R] (byte per value, see ct_oracle.c).
+    threads > 1: the tuple scan split over that many host threads
+    (oracle_gac_split: union of per-slice results, pinned to threads = 1).
     Returns (ok: bool, dom_out: uint8[R] or None on FAIL, valid: uint8[t] or None)."""
     lo = np.ascontiguousarray(lo, dtype=np.int32)
     d = np.ascontiguousarray(d, dtype=np.int32)
@@ -79,7 +101,9 @@ def gac(lo, d, tuples, dom_in, want_valid: bool = False):
     assert dom_in.size == int(d.sum())
     dom_out = np.zeros(int(d.sum()), dtype=np.uint8)
     valid = np.zeros(max(t, 1), dtype=np.uint8) if want_valid else None
-    r = lib().oracle_gac(n, _p(lo), _p(d), t, _p(tuples) if t else None, _p(dom_in), _p(dom_out),
+    r = lib().oracle_gac_split(n, _p(lo), _p(d), t, _p(tuples) if t else None, _p(dom_in), _p(dom_out),
+                               _p(valid) if want_valid else None, int(threads)) if threads > 1 else \
+        lib().oracle_gac(n, _p(lo), _p(d), t, _p(tuples) if t else None, _p(dom_in), _p(dom_out),
                          _p(valid) if want_valid else None)
     if r < 0:
         raise ValueError("oracle_gac: bad arguments")
@@ -94,7 +118,7 @@ def supports_row(tuples, i: int, value: int):
     return out[:t]
 
 
-def fixpoint(vlo, vd, scopes, tables, dom):
+def fixpoint(vlo, vd, scopes, tables, dom, threads: int = 1):
     """Multi-table fixpoint.  scopes: list of int arrays (global var ids);
     tables: list of int32[t_k][ar_k]; dom: uint8[sum vd] (modified copy returned).
     Returns (ok, dom_out or None)."""
@@ -108,9 +132,14 @@ def fixpoint(vlo, vd, scopes, tables, dom):
     sc_ptrs = (ctypes.c_void_p * ntab)(*[x.ctypes.data for x in sc])
     tb_ptrs = (ctypes.c_void_p * ntab)(*[x.ctypes.data if x.size else 0 for x in tb])
     out = np.ascontiguousarray(dom, dtype=np.uint8).copy()
-    r = lib().oracle_fixpoint(int(vd.size), _p(vlo), _p(vd), ntab, _p(ar),
-                              ctypes.cast(sc_ptrs, ctypes.c_void_p), _p(tt),
-                              ctypes.cast(tb_ptrs, ctypes.c_void_p), _p(out))
+    if threads > 1:
+        r = lib().oracle_fixpoint_split(int(vd.size), _p(vlo), _p(vd), ntab, _p(ar),
+                                        ctypes.cast(sc_ptrs, ctypes.c_void_p), _p(tt),
+                                        ctypes.cast(tb_ptrs, ctypes.c_void_p), _p(out), int(threads))
+    else:
+        r = lib().oracle_fixpoint(int(vd.size), _p(vlo), _p(vd), ntab, _p(ar),
+                                  ctypes.cast(sc_ptrs, ctypes.c_void_p), _p(tt),
+                                  ctypes.cast(tb_ptrs, ctypes.c_void_p), _p(out))
     if r < 0:
         raise ValueError("oracle_fixpoint: bad arguments")
     return bool(r), (out if r else None)

@@ -31,6 +31,7 @@
  * rowbase_i + (v - lo_i) is 1 iff v is in the domain.  tuples is int32
  * [t][n] row-major.
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -71,6 +72,63 @@ int oracle_gac(int32_t n, const int32_t *lo, const int32_t *d, int64_t t,
     return any_valid;
 }
 
+/*
+ * The same definition with the tuple scan split into `nthreads` contiguous
+ * ranges (timing on all host cores, and parity at the configs' full sizes):
+ * V is the union of the ranges' valid sets and D_out the union of their
+ * projections, so every range is one oracle_gac call on its slice of the
+ * tuples and the results are OR-ed.  nthreads <= 1 is oracle_gac itself.
+ * Pinned to oracle_gac on random instances (tests/test_oracle.py).
+ */
+typedef struct {
+    int32_t n; const int32_t *lo, *d; int64_t t; const int32_t *tuples;
+    const uint8_t *dom_in; uint8_t *dom_out; uint8_t *valid_out; int result;
+} gac_slice;
+
+static void *gac_slice_run(void *arg)
+{
+    gac_slice *a = (gac_slice *)arg;
+    a->result = oracle_gac(a->n, a->lo, a->d, a->t, a->tuples, a->dom_in, a->dom_out, a->valid_out);
+    return NULL;
+}
+
+int oracle_gac_split(int32_t n, const int32_t *lo, const int32_t *d, int64_t t,
+                     const int32_t *tuples, const uint8_t *dom_in, uint8_t *dom_out,
+                     uint8_t *valid_out, int32_t nthreads)
+{
+    if (n < 1) return -1;
+    if (nthreads <= 1 || t < 2 * (int64_t)nthreads)
+        return oracle_gac(n, lo, d, t, tuples, dom_in, dom_out, valid_out);
+    int64_t R = 0;
+    for (int32_t i = 0; i < n; ++i) R += d[i];
+    gac_slice *sl = (gac_slice *)calloc((size_t)nthreads, sizeof(gac_slice));
+    pthread_t *th = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    uint8_t *outs = (uint8_t *)calloc((size_t)nthreads * (size_t)(R > 0 ? R : 1), 1);
+    if (!sl || !th || !outs) { free(sl); free(th); free(outs); return -1; }
+    for (int32_t k = 0; k < nthreads; ++k) {
+        int64_t j0 = t * k / nthreads, j1 = t * (k + 1) / nthreads;
+        sl[k].n = n; sl[k].lo = lo; sl[k].d = d; sl[k].t = j1 - j0;
+        sl[k].tuples = tuples + j0 * (int64_t)n; sl[k].dom_in = dom_in;
+        sl[k].dom_out = outs + (size_t)k * (size_t)(R > 0 ? R : 1);
+        sl[k].valid_out = valid_out ? valid_out + j0 : NULL;
+        if (pthread_create(&th[k], NULL, gac_slice_run, &sl[k]) != 0) gac_slice_run(&sl[k]), th[k] = 0;
+    }
+    int any = 0, bad = 0;
+    for (int32_t k = 0; k < nthreads; ++k) {
+        if (th[k]) pthread_join(th[k], NULL);
+        if (sl[k].result < 0) bad = 1;
+        if (sl[k].result == 1) any = 1;
+    }
+    if (any && !bad) {
+        memset(dom_out, 0, (size_t)R);
+        for (int32_t k = 0; k < nthreads; ++k)
+            if (sl[k].result == 1)
+                for (int64_t r = 0; r < R; ++r) dom_out[r] |= sl[k].dom_out[r];
+    }
+    free(sl); free(th); free(outs);
+    return bad ? -1 : any;
+}
+
 /* One row of the static supports matrix, by its definition:
  * out[j] = 1 iff tau_j[i] = value.  (Used to pin the CUDA supports builder.) */
 void oracle_supports_row(int32_t n, int64_t t, const int32_t *tuples,
@@ -91,9 +149,9 @@ void oracle_supports_row(int32_t n, int64_t t, const int32_t *tuples,
  * ar[k], scope scope[k][0..ar-1] (global var ids), t[k] tuples at tuples[k].
  * Returns 1 OK (dom updated in place), 0 FAIL, -1 bad args.
  */
-int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t ntab,
-                    const int32_t *ar, const int32_t *const *scope, const int64_t *t,
-                    const int32_t *const *tuples, uint8_t *dom)
+int oracle_fixpoint_split(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t ntab,
+                          const int32_t *ar, const int32_t *const *scope, const int64_t *t,
+                          const int32_t *const *tuples, uint8_t *dom, int32_t nthreads)
 {
     int64_t *vbase = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nv + 1));
     if (!vbase) return -1;
@@ -116,7 +174,7 @@ int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t n
                 memcpy(din + off, dom + vbase[scope[k][i]], (size_t)d[i]);
                 off += d[i];
             }
-            int r = oracle_gac(n, lo, d, t[k], tuples[k], din, dout, NULL);
+            int r = oracle_gac_split(n, lo, d, t[k], tuples[k], din, dout, NULL, nthreads);
             if (r != 1) {
                 result = r;
             } else {
@@ -134,4 +192,12 @@ int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t n
     }
     free(vbase);
     return result;
+}
+
+/* The fixpoint with one thread per table call (the plain definition). */
+int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t ntab,
+                    const int32_t *ar, const int32_t *const *scope, const int64_t *t,
+                    const int32_t *const *tuples, uint8_t *dom)
+{
+    return oracle_fixpoint_split(nv, vlo, vd, ntab, ar, scope, t, tuples, dom, 1);
 }

@@ -13,7 +13,14 @@ little-endian words (depth, var, value, branch, status) of every node, root
 first (var = -1, branch = 2).
 
 Pinned (tests/test_oracle.py): all-solutions == Cartesian enumeration of the
-whole model on tiny models; Table 1 alone gives (3, 4, 3) first.
+whole model on tiny models; solutions appear in descending (indomain_max) or
+ascending (indomain_min) lexicographic order -- with input_order the variables
+before the branching one are bound, the left branch takes the largest
+(smallest) value and sound propagation keeps every solution, so this order
+pins both the variable and the value order; the node trace of Table 1 alone
+(all solutions, indomain_max) derived by hand from Table 1(a) (P:L81-85);
+nodes = 2 (failures + solutions) - 1 (every OK non-solution node has exactly
+two children when all solutions are enumerated); the FNV-1a 64 test vector.
 """
 from __future__ import annotations
 
@@ -21,7 +28,7 @@ import numpy as np
 
 from . import fixpoint
 
-FNV_OFF = 1469598103934665603
+FNV_OFF = 14695981039346656037   # 0xcbf29ce484222325, the FNV-1a 64 offset basis
 FNV_PRIME = 1099511628211
 M64 = (1 << 64) - 1
 
@@ -30,20 +37,26 @@ class _Hash:
     def __init__(self):
         self.h = FNV_OFF
 
+    def byte(self, b: int):
+        self.h ^= b & 0xFF
+        self.h = (self.h * FNV_PRIME) & M64
+
     def word(self, x: int):
         x &= M64
         for i in range(8):
-            self.h ^= (x >> (8 * i)) & 0xFF
-            self.h = (self.h * FNV_PRIME) & M64
+            self.byte(x >> (8 * i))
 
 
-def dfs(vlo, vd, scopes, tables, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1):
-    """Returns dict(status, solutions=[...], nodes, failures, trace_hash, last_solution)."""
+def dfs(vlo, vd, scopes, tables, value_order: int = 0, max_nodes: int = 0, max_solutions: int = 1,
+        threads: int = 1, keep_trace: bool = False):
+    """Returns dict(status, solutions=[...], nodes, failures, trace_hash, last_solution[, trace]).
+    threads: host threads of each table's GAC scan (oracle.fixpoint); keep_trace:
+    also return the node records (depth, var, value, branch, status)."""
     vlo = np.asarray(vlo, np.int32)
     vd = np.asarray(vd, np.int32)
     base = np.concatenate([[0], np.cumsum(vd)]).astype(int)
     H = _Hash()
-    st = dict(nodes=0, failures=0, solutions=[], stop=False)
+    st = dict(nodes=0, failures=0, solutions=[], stop=False, trace=[])
 
     def account(depth, var, val, branch, ok):
         st["nodes"] += 1
@@ -52,6 +65,8 @@ def dfs(vlo, vd, scopes, tables, value_order: int = 0, max_nodes: int = 0, max_s
             st["failures"] += 1
         for w in (depth, var, val, branch, status):
             H.word(w)
+        if keep_trace:
+            st["trace"].append((depth, var, val, branch, status))
 
     def node(dom, depth):
         if st["stop"]:
@@ -81,16 +96,19 @@ def dfs(vlo, vd, scopes, tables, value_order: int = 0, max_nodes: int = 0, max_s
                 din[base[x] + a] = 1
             else:
                 din[base[x] + a] = 0
-            ok, dout = fixpoint(vlo, vd, scopes, tables, din)
+            ok, dout = fixpoint(vlo, vd, scopes, tables, din, threads=threads)
             account(depth + 1, x, val, branch, ok)
             if ok:
                 node(dout, depth + 1)
 
     dom0 = np.ones(int(vd.sum()), np.uint8)
-    ok, root = fixpoint(vlo, vd, scopes, tables, dom0)
+    ok, root = fixpoint(vlo, vd, scopes, tables, dom0, threads=threads)
     account(0, -1, 0, 2, ok)
     if ok:
         node(root, 0)
     sols = st["solutions"]
-    return dict(status=0 if sols else 1, solutions=sols, nodes=st["nodes"], failures=st["failures"],
-                trace_hash=H.h, last_solution=(sols[-1] if sols else None))
+    out = dict(status=0 if sols else 1, solutions=sols, nodes=st["nodes"], failures=st["failures"],
+               trace_hash=H.h, last_solution=(sols[-1] if sols else None))
+    if keep_trace:
+        out["trace"] = st["trace"]
+    return out

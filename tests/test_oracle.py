@@ -270,3 +270,89 @@ def test_dfs_table1_first_solution_and_all():
     assert res["last_solution"] == (3, 4, 3)
     res = dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=0)
     assert sorted(res["solutions"]) == sorted(tuple(int(v) for v in r) for r in p.tuples)
+
+
+def test_dfs_lexicographic_order_and_node_identity():
+    """input_order + indomain_max with sound propagation emits solutions in
+    descending lexicographic order (ascending for indomain_min), PAPER.md
+    L469-477; and with all solutions enumerated every OK non-solution node
+    has two children, so nodes = 2 (failures + solutions) - 1."""
+    from oracle.cartesian import all_solutions
+    from oracle.dfs import dfs
+    rng = Rng(405, lanes=4)
+    n_nonempty = 0
+    for trial in range(30):
+        m = _tiny_model(rng, nv=3 + trial % 3, d=2 + trial % 3, ntab=2 + trial % 3)
+        exp = all_solutions(m["vlo"], m["vd"], m["scopes"], m["tables"])
+        for vo in (0, 1):
+            res = dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=vo, max_solutions=0)
+            assert res["solutions"] == sorted(exp, reverse=(vo == 0)), (trial, vo)
+            assert res["nodes"] == 2 * (res["failures"] + len(res["solutions"])) - 1, (trial, vo)
+        n_nonempty += len(exp) > 1
+    assert n_nonempty >= 10
+
+
+def test_dfs_table1_hand_trace():
+    """Table 1 alone (tau1..tau5 = (3,1,1), (1,2,3), (2,3,3), (1,4,1), (3,4,3),
+    read off Table 1(a)/(b)), all solutions, input_order +
+    indomain_max; every record (depth, var, value, branch 0: x = v / 1: x != v /
+    2: root, status) derived by hand: a single GAC table never fails after a
+    branch, so the search only splits."""
+    from oracle.dfs import dfs, _Hash
+    p = table1()
+    res = dfs(p.lo, p.d, [np.arange(3)], [p.tuples], value_order=0, max_solutions=0, keep_trace=True)
+    assert res["trace"] == [
+        (0, -1, 0, 2, 0),     # root: x1 = {1,2,3}, x2 = {1..4}, x3 = {1,3}
+        (1, 0, 3, 0, 0),      # x1 = 3: tau1, tau5
+        (2, 1, 4, 0, 0),      # x2 = 4: tau5 -> solution (3,4,3)
+        (2, 1, 4, 1, 0),      # x2 != 4: tau1 -> solution (3,1,1)
+        (1, 0, 3, 1, 0),      # x1 != 3: tau2, tau3, tau4
+        (2, 0, 2, 0, 0),      # x1 = 2: tau3 -> solution (2,3,3)
+        (2, 0, 2, 1, 0),      # x1 != 2 -> x1 = 1: tau2, tau4
+        (3, 1, 4, 0, 0),      # x2 = 4: tau4 -> solution (1,4,1)
+        (3, 1, 4, 1, 0),      # x2 != 4: tau2 -> solution (1,2,3)
+    ]
+    assert res["solutions"] == [(3, 4, 3), (3, 1, 1), (2, 3, 3), (1, 4, 1), (1, 2, 3)]
+    assert res["nodes"] == 9 and res["failures"] == 0
+    h = _Hash()
+    for rec in res["trace"]:
+        for w in rec:
+            h.word(w)
+    assert h.h == res["trace_hash"]
+
+
+def test_fnv1a_64_test_vector():
+    """FNV-1a 64 (offset 0xcbf29ce484222325, prime 0x100000001b3) of b"foobar"
+    is 0x85944171f73967e8 (the published FNV test vector)."""
+    from oracle.dfs import _Hash, FNV_OFF, FNV_PRIME
+    assert FNV_OFF == 0xcbf29ce484222325 and FNV_PRIME == 0x100000001b3
+    h = _Hash()
+    for b in b"foobar":
+        h.byte(b)
+    assert h.h == 0x85944171f73967e8
+
+
+def test_split_oracle_equals_single_thread():
+    """oracle_gac_split (tuple slices over host threads, results OR-ed) ==
+    oracle_gac, and the split fixpoint == the plain one."""
+    rng = Rng(406, lanes=4)
+    for trial in range(40):
+        n = 1 + trial % 6
+        d = 2 + trial % 9
+        t = int(rng.below(3000)) + (0 if trial % 7 else 0)
+        p = random_table(n, d, t, seed=trial + 900, lo=trial % 3 - 1)
+        din = (rng.uniform(p.R, 4) > 0).astype(np.uint8)
+        a = oracle.gac(p.lo, p.d, p.tuples, din, want_valid=True)
+        for th in (2, 3, 8):
+            b = oracle.gac(p.lo, p.d, p.tuples, din, want_valid=True, threads=th)
+            assert a[0] == b[0]
+            assert np.array_equal(a[2], b[2])
+            if a[0]:
+                assert np.array_equal(a[1], b[1])
+    from workloads.csp import csp_model
+    for trial in range(10):
+        m = csp_model(6, 5, 4, 400, seed=trial + 77)
+        dom = np.ones(int(np.sum(m["vd"])), np.uint8)
+        r1 = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], dom)
+        r2 = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], dom, threads=4)
+        assert r1[0] == r2[0] and (not r1[0] or np.array_equal(r1[1], r2[1]))
