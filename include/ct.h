@@ -55,6 +55,8 @@ extern "C" {
 typedef enum ct_status {
   CT_OK = 0,        /* GAC fixpoint reached; outputs written                        */
   CT_FAIL = 1,      /* no valid tuple (currTable = 0); outputs not written          */
+  CT_PENDING = 2,   /* ct_create of a caller-combined shard: the root's local phase  */
+                    /* ran; combine its flags, then ct_propagate_apply_async(root)   */
   CT_EINVAL = -1,   /* invalid argument (message in ct_last_error)                   */
   CT_ENOMEM = -2,   /* device or pinned-host allocation failed                      */
   CT_ECUDA = -3,    /* a CUDA runtime call failed                                   */
@@ -124,7 +126,14 @@ void ct_config_init(ct_config *cfg);
  *   out_table, out_root   receive the handles (also on CT_FAIL)
  *   out_dom     host uint64[Wd]: root domains on CT_OK; may be NULL
  * Returns CT_OK, CT_FAIL (root wipe-out; the root state is dead) or an error
- * (no handles are returned on error). */
+ * (no handles are returned on error).
+ * Caller-combined shards (n_shards > 1, nccl_unique_id NULL): the root's GAC
+ * needs every shard's flags, so ct_create runs only the root's LOCAL phase
+ * and returns CT_PENDING without writing out_dom.  The caller then ORs the
+ * root's flags across shards (ct_state_flags) and calls
+ * ct_propagate_apply_async(root, ...), whose out_status is the root verdict
+ * (CT_OK / CT_FAIL) and whose out_dom are the root domains.  Until that apply
+ * is enqueued the root cannot be propagated, cloned or copied (CT_ESTATE). */
 ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
                     const int32_t *dom_size, const uint64_t *init_dom, int64_t n_tuples,
                     const int32_t *tuples, const ct_config *cfg, ct_table **out_table,
@@ -190,7 +199,8 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
  * pointer returned by ct_state_flags.  The caller ORs the flag arrays of all
  * shards element-wise (e.g. an all-reduce with MAX over uint8) into every
  * shard's flags, then calls apply, which finishes the call exactly as the
- * unsharded path would. */
+ * unsharded path would.  The root of a caller-combined shard table goes through
+ * the same combine + apply once after ct_create (CT_PENDING above). */
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed);
 ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes);
 ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned,
@@ -199,7 +209,11 @@ ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out
 /* ---------------------------------------------------------------- states */
 ct_status ct_state_clone(const ct_state *src, ct_state **out);       /* new state = src      */
 ct_status ct_state_copy(ct_state *dst, const ct_state *src);         /* dst := src (async,   */
-                                                                    /* device to device)    */
+                                                                    /* device to device);   */
+/* with distinct streams, dst's stream first waits for src's earlier work and
+ * src's stream then waits for the copy, so either state may be used next on
+ * its own stream.  Batch copies (ct_batch_copy*, ct_batch_restore_dead,
+ * ct_batch_create) order src's stream after the copy the same way. */
 ct_status ct_state_set_stream(ct_state *s, void *stream);            /* cudaStream_t          */
 void *ct_state_stream(const ct_state *s);
 ct_status ct_synchronize(ct_state *s);                               /* wait for its stream   */

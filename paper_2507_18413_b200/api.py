@@ -92,12 +92,12 @@ class State:
             out = np.zeros(max(wd, 1), np.uint64)
         if pruned is None:
             pruned = np.zeros(max(wd, 1), np.uint64)
-        rem = None if removed is None else np.ascontiguousarray(removed, np.uint64)
-        st = C.ct_propagate(self.handle, rem, out, pruned)
+        rem = None if removed is None else np.ascontiguousarray(removed, np.uint64).reshape(-1)
+        st = C.ct_propagate(self.handle, rem, out, pruned, wd=wd)
         return (st, out[:wd], pruned[:wd]) if st == C.CT_OK else (st, None, None)
 
     def propagate_async(self, removed, out_dom=None, out_pruned=None, out_status=None):
-        C.ct_propagate_async(self.handle, removed, out_dom, out_pruned, out_status)
+        C.ct_propagate_async(self.handle, removed, out_dom, out_pruned, out_status, wd=self.table.Wd)
 
     def read_table(self) -> np.ndarray:
         return C.ct_state_read_table(self.handle, int(self.table.info.words))

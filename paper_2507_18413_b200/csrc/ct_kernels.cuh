@@ -1328,7 +1328,12 @@ __global__ void __launch_bounds__(256) k_state_copy(char *__restrict__ dst, cons
 __global__ void __launch_bounds__(256) k_restore_dead(char *__restrict__ pool, size_t pitch,
                                                       const char *__restrict__ src, CopyLayout cl) {
   char *dst = pool + (size_t)blockIdx.x * pitch;
-  if (!reinterpret_cast<const Ctl *>(dst)->dead) return;
+  // one read of `dead` for the whole block: the copy overwrites dst's control
+  // block (dead = 0), so a thread reading it after that write would skip its share
+  __shared__ int s_dead;
+  if (threadIdx.x == 0) s_dead = reinterpret_cast<const Ctl *>(dst)->dead;
+  __syncthreads();
+  if (!s_dead) return;
   copy_state_fields(dst, src, cl, threadIdx.x, blockDim.x);
 }
 

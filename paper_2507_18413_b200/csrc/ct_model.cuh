@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, Sear
     c.d = 0;
     c.err = 0;
     c.nodes = c.failures = c.solutions = c.calls = c.iters = c.maxd = 0;
-    c.hash = 1469598103934665603ull;
+    c.hash = 14695981039346656037ull;
   }
   // the root: trail level 0, fixpoint of the current domains
   search_copy(sd.snaps, sd.pool, sd.pool16);

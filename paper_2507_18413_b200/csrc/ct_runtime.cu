@@ -149,6 +149,7 @@ struct ct_state {
   uint64_t *h_out = nullptr; // pinned [1 + 2 Wd]
   uint64_t *d_in_map = nullptr, *d_out_map = nullptr;   // device aliases of h_in / h_out
   cudaGraphExec_t gexec = nullptr;
+  bool pending = false;      // root of a caller-combined shard before its first apply
 };
 
 struct ct_batch {
@@ -248,6 +249,18 @@ static ct_status launch_state_copy(const ct_table *tb, char *dst, const char *sr
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)tb->sm_count * 4, bytes / 4096));
   k_state_copy<<<grid, 256, 0, st>>>(dst, src, copy_layout(tb));
   CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
+// `waiter` waits for the work enqueued so far on `producer` (no-op if equal).
+static ct_status order_after(cudaStream_t waiter, cudaStream_t producer) {
+  if (waiter == producer) return CT_OK;
+  cudaEvent_t ev;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  cudaError_t e = cudaEventRecord(ev, producer);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(waiter, ev, 0);
+  cudaEventDestroy(ev);
+  if (e != cudaSuccess) return fail(CT_ECUDA, "stream ordering failed: %s", cudaGetErrorString(e));
   return CT_OK;
 }
 
@@ -819,6 +832,15 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
                              tb->stream));
   // root propagation: remove the holes of init_dom
   for (int k = 0; k < tb->Wd; ++k) root->h_in[k] = init_dom ? (tb->full_dom[k] & ~init_dom[k]) : 0ull;
+  if (tb->n_shards > 1 && !tb->comm) {
+    // caller-combined shard: the root verdict needs every shard's flags, so only
+    // the local phase runs here; the caller combines and applies (include/ct.h)
+    CT_TRY(enqueue_single(tb, root, root->d_in_map, /*root_mode=*/1, nullptr, nullptr, nullptr, 0, true));
+    CUDA_TRY(cudaStreamSynchronize(tb->stream));   // h_in is reused by later calls
+    root->pending = true;
+    *out_table = tb;
+    return CT_PENDING;
+  }
   *(volatile int32_t *)root->h_out = kPendingStatus;
   CT_TRY(enqueue_sync_call(root, /*root_mode=*/1));
   CT_TRY(wait_sync_call(root));
@@ -948,6 +970,7 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
 
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  if (s->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   DeviceGuard g(s->tb->device);
   return enqueue_single(s->tb, s, removed, 0, nullptr, nullptr, nullptr, 0, true);
 }
@@ -962,12 +985,15 @@ ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes) {
 ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status) {
   if (!s) return fail(CT_EINVAL, "NULL state");
   DeviceGuard g(s->tb->device);
-  return enqueue_finalize(s->tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream);
+  CT_TRY(enqueue_finalize(s->tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream));
+  s->pending = false;
+  return CT_OK;
 }
 
 // ------------------------------------------------------------------ states
 ct_status ct_state_clone(const ct_state *src, ct_state **out) {
   if (!src || !out) return fail(CT_EINVAL, "NULL argument");
+  if (src->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   ct_table *tb = src->tb;
   DeviceGuard g(tb->device);
   ct_state *s = nullptr;
@@ -986,15 +1012,12 @@ ct_status ct_state_copy(ct_state *dst, const ct_state *src) {
   if (!dst || !src) return fail(CT_EINVAL, "NULL argument");
   if (dst->tb != src->tb) return fail(CT_ESTATE, "states belong to different tables");
   if (dst == src) return CT_OK;
+  if (src->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   DeviceGuard g(dst->tb->device);
-  if (src->stream != dst->stream) {
-    cudaEvent_t ev;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    cudaEventRecord(ev, src->stream);
-    cudaStreamWaitEvent(dst->stream, ev, 0);
-    cudaEventDestroy(ev);
-  }
-  return launch_state_copy(dst->tb, dst->mem, src->mem, dst->stream);
+  CT_TRY(order_after(dst->stream, src->stream));   // the copy reads src after its earlier work
+  CT_TRY(launch_state_copy(dst->tb, dst->mem, src->mem, dst->stream));
+  dst->pending = false;
+  return order_after(src->stream, dst->stream);    // src's next writes wait for the copy
 }
 
 ct_status ct_state_set_stream(ct_state *s, void *stream) {
@@ -1066,7 +1089,8 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64 + (size_t)n_states * sizeof(int2);
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
-  if (b->d_miss && cudaMemset(b->d_miss, 0, b->miss_bytes) != cudaSuccess) cudaGetLastError();
+  if (b->d_miss && cudaMemsetAsync(b->d_miss, 0, b->miss_bytes, tb->stream) != cudaSuccess)
+    return cleanup(fail(CT_ECUDA, "batch counter initialisation failed"));
   if (!b->mem || !b->d_desc || !b->d_in || !b->d_dom || !b->d_status || !b->d_bgo || !b->d_miss)
     return cleanup(fail(CT_ENOMEM, "device allocation of a %d-state batch (%zu bytes) failed", n_states, b->bytes));
   if (cudaHostAlloc((void **)&b->h_in, std::max<size_t>(io, 8), 0) != cudaSuccess ||
@@ -1105,13 +1129,15 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   }
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
-  if (init->stream != tb->stream) cudaStreamSynchronize(init->stream);
+  if (init->pending) return cleanup(fail(CT_ESTATE, "init state is a pending shard root"));
+  if (order_after(tb->stream, init->stream) != CT_OK) return cleanup(CT_ECUDA);
   // per-call scratch starts zeroed, as for single states
   if (cudaMemsetAsync(b->mem, 0, b->bytes, tb->stream) != cudaSuccess) return cleanup(fail(CT_ECUDA, "batch memset failed"));
   for (int i = 0; i < n_states; ++i)
     if (cudaMemcpyAsync(b->mem + (size_t)i * tb->lay.total, init->mem, tb->lay.persist, cudaMemcpyDeviceToDevice,
                         tb->stream) != cudaSuccess)
       return cleanup(fail(CT_ECUDA, "batch init copy failed"));
+  if (order_after(init->stream, tb->stream) != CT_OK) return cleanup(CT_ECUDA);
   tb->live++;
   *out = b;
   return CT_OK;
@@ -1123,32 +1149,35 @@ ct_status ct_batch_copy(ct_batch *b, int32_t i, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
   if (i < 0 || i >= b->S) return fail(CT_EINVAL, "batch index %d out of range", i);
+  if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
   DeviceGuard g(b->tb->device);
-  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  CT_TRY(order_after(b->tb->stream, src->stream));
   CUDA_TRY(cudaMemcpyAsync(b->mem + (size_t)i * b->tb->lay.total, src->mem, b->tb->lay.persist,
                            cudaMemcpyDeviceToDevice, b->tb->stream));
-  return CT_OK;
+  return order_after(src->stream, b->tb->stream);
 }
 
 ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
+  if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
   DeviceGuard g(b->tb->device);
-  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  CT_TRY(order_after(b->tb->stream, src->stream));
   const size_t pitch = b->tb->lay.total;
   CUDA_TRY(cudaMemcpy2DAsync(b->mem, pitch, src->mem, 0, b->tb->lay.persist, (size_t)b->S,
                              cudaMemcpyDeviceToDevice, b->tb->stream));
-  return CT_OK;
+  return order_after(src->stream, b->tb->stream);
 }
 
 ct_status ct_batch_restore_dead(ct_batch *b, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
+  if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
   DeviceGuard g(b->tb->device);
-  if (src->stream != b->tb->stream) cudaStreamSynchronize(src->stream);
+  CT_TRY(order_after(b->tb->stream, src->stream));
   k_restore_dead<<<b->S, 256, 0, b->tb->stream>>>(b->mem, b->tb->lay.total, src->mem, copy_layout(b->tb));
   CUDA_TRY(cudaGetLastError());
-  return CT_OK;
+  return order_after(src->stream, b->tb->stream);
 }
 
 // Tile-major batch call (ct_batch.cuh): ingest, update, probe, scan, finalize.
@@ -1906,7 +1935,7 @@ ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes
   d.max_nodes = max_nodes;
   d.max_solutions = max_solutions;
   d.sol.assign(m->nv, 0);
-  d.st.trace_hash = 1469598103934665603ull;
+  d.st.trace_hash = 14695981039346656037ull;
   if (m->dead) {
     d.account(0, -1, 0, 2, CT_FAIL);
   } else {

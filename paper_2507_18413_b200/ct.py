@@ -22,8 +22,9 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(_PKG, "libct_b200.so")   # override: experiment builds
 
 CT_OK, CT_FAIL, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE = 0, 1, -1, -2, -3, -4, -5
+CT_PENDING = 2   # ct_create of a caller-combined shard: combine the root's flags, then apply
 CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA = 0, 1, 2
-STATUS_NAMES = {0: "OK", 1: "FAIL", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE"}
+STATUS_NAMES = {0: "OK", 1: "FAIL", 2: "PENDING", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE"}
 
 
 class CTError(RuntimeError):
@@ -246,8 +247,16 @@ def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None):
     d = np.ascontiguousarray(d, dtype=np.int32)
     tuples = np.ascontiguousarray(tuples, dtype=np.int32)
     n = int(d.size)
-    t = int(tuples.shape[0]) if tuples.ndim == 2 else 0
+    if lo.ndim != 1 or d.ndim != 1 or lo.size != n:
+        raise ValueError(f"lo and d must be 1-D of the same length (got {lo.shape}, {d.shape})")
+    if tuples.ndim != 2 or (tuples.shape[0] > 0 and tuples.shape[1] != n):
+        raise ValueError(f"tuples must be int32[t][{n}] (got shape {tuples.shape})")
+    t = int(tuples.shape[0])
     wd = int(((d.astype(np.int64) + 63) // 64).sum())
+    if init_dom is not None and np.asarray(init_dom).size < wd:
+        raise ValueError(f"init_dom needs {wd} words")
+    if scope is not None and np.asarray(scope).size != n:
+        raise ValueError(f"scope needs {n} entries")
     out_dom = np.zeros(max(wd, 1), dtype=np.uint64)
     sc = None if scope is None else np.ascontiguousarray(scope, dtype=np.int32)
     idom = None if init_dom is None else np.ascontiguousarray(init_dom, dtype=np.uint64)
@@ -257,6 +266,16 @@ def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None):
                          ctypes.byref(tab), ctypes.byref(root), _np_ptr(out_dom))
     _check(st)
     return st, tab, root, (out_dom[:wd] if st == CT_OK else None)
+
+
+def _need_words(name, a, n):
+    if a is not None and (a.ndim != 1 or a.size < n):
+        raise ValueError(f"{name} must be a 1-D host array of >= {n} uint64 words (got {a.shape})")
+
+
+def _need_dev_words(name, t, n):
+    if t is not None and hasattr(t, "numel") and t.numel() * t.element_size() < 8 * n:
+        raise ValueError(f"{name} must hold >= {n} 64-bit words")
 
 
 def ct_table_info_get(table) -> ct_table_info:
@@ -273,14 +292,21 @@ def ct_dom_word_offset(table, i: int) -> int:
     return int(lib().ct_dom_word_offset(table, i))
 
 
-def ct_propagate(state, removed, out_dom, out_pruned=None) -> int:
+def ct_propagate(state, removed, out_dom, out_pruned=None, wd: int | None = None) -> int:
     """Host numpy buffers (uint64[Wd]); returns CT_OK / CT_FAIL (raises on errors,
-    including CT_ESTATE)."""
+    including CT_ESTATE).  wd: the table's Wd, if given the buffers are length-checked."""
+    if wd is not None:
+        for nm, a in (("removed", removed), ("out_dom", out_dom), ("out_pruned", out_pruned)):
+            _need_words(nm, a, wd)
     return _check(lib().ct_propagate(state, _np_ptr(removed), _np_ptr(out_dom), _np_ptr(out_pruned)))
 
 
-def ct_propagate_async(state, removed, out_dom=None, out_pruned=None, out_status=None) -> int:
-    """Device tensors; enqueue only."""
+def ct_propagate_async(state, removed, out_dom=None, out_pruned=None, out_status=None,
+                       wd: int | None = None) -> int:
+    """Device tensors; enqueue only.  wd: if given, tensor buffers are length-checked."""
+    if wd is not None:
+        for nm, a in (("removed", removed), ("out_dom", out_dom), ("out_pruned", out_pruned)):
+            _need_dev_words(nm, a, wd)
     return _check(lib().ct_propagate_async(state, _dev_ptr(removed), _dev_ptr(out_dom), _dev_ptr(out_pruned),
                                            _dev_ptr(out_status)), allow_fail=False)
 

@@ -53,8 +53,46 @@ def broadcast_nccl_id(group=None) -> bytes:
 def combine_flags_(flags, group=None):
     """In-place OR of shard flags across ranks (all-reduce MAX on uint8)."""
     import torch.distributed as dist
-    dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
+    if flags.device.type == "cuda" and dist.get_backend(group) != "nccl":
+        # host-side collectives (gloo): stage through host memory
+        h = flags.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+        flags.copy_(h)
+    else:
+        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=group)
     return flags
+
+
+def apply_async(state_handle, wd: int, device: int):
+    """ct_propagate_apply_async into fresh device buffers; returns (status, dom, pruned) tensors."""
+    import torch
+    dev = torch.device("cuda", device)
+    out = torch.zeros(max(wd, 1), dtype=torch.int64, device=dev)
+    pr = torch.zeros(max(wd, 1), dtype=torch.int64, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    C.ct_propagate_apply_async(state_handle, out, pr, status)
+    return status, out, pr
+
+
+def finish_pending_root(table: Table, combine) -> None:
+    """Caller-combined shards: ct_create returned CT_PENDING after the root's
+    local phase (include/ct.h).  `combine(flags_tensor)` ORs the root's flags
+    across the shards in place; the apply then gives the root verdict/domains."""
+    import torch
+    if table.root_status != C.CT_PENDING:
+        return
+    h = table.root.handle
+    stream = torch.cuda.ExternalStream(C.ct_state_stream(h), device=torch.device("cuda", table.device))
+    stream.synchronize()
+    combine(flags_tensor(h))
+    torch.cuda.synchronize(table.device)
+    status, out, _ = apply_async(h, table.Wd, table.device)
+    stream.synchronize()
+    st = int(status.item())
+    if st < 0:
+        raise C.CTError(st, "sharded root apply")
+    table.root_status = st
+    table.root_dom = out[:table.Wd].cpu().numpy().view(np.uint64).copy() if st == C.CT_OK else None
 
 
 class ShardedTable:
@@ -69,7 +107,11 @@ class ShardedTable:
         nid = broadcast_nccl_id(group) if mode == "nccl" else None
         self.table = Table(lo, d, tuples, device=dev, n_shards=self.world, shard_rank=self.rank,
                            nccl_unique_id=nid, **kw)
+        if mode != "nccl":
+            finish_pending_root(self.table, lambda f: combine_flags_(f, self.group))
         self.root = self.table.root
+        self.root_status = self.table.root_status
+        self.root_dom = self.table.root_dom
         self.Wd = self.table.Wd
 
     def propagate(self, state, removed=None):
@@ -82,15 +124,12 @@ class ShardedTable:
         rem = torch.zeros(max(wd, 1), dtype=torch.int64, device=dev)
         if removed is not None and wd:
             rem[:wd] = torch.from_numpy(np.ascontiguousarray(removed, np.uint64).view(np.int64))
-        out = torch.zeros(max(wd, 1), dtype=torch.int64, device=dev)
-        pr = torch.zeros(max(wd, 1), dtype=torch.int64, device=dev)
-        status = torch.zeros(1, dtype=torch.int32, device=dev)
         stream = torch.cuda.ExternalStream(C.ct_state_stream(state.handle), device=dev)
         torch.cuda.current_stream(dev).synchronize()
         C.ct_propagate_local_async(state.handle, rem)
         with torch.cuda.stream(stream):
             combine_flags_(flags_tensor(state.handle), self.group)
-            C.ct_propagate_apply_async(state.handle, out, pr, status)
+            status, out, pr = apply_async(state.handle, wd, self.table.device)
         stream.synchronize()
         st = int(status.item())
         if st < 0:

@@ -647,61 +647,113 @@ PATHS = {"small": dict(), "fast": dict(_grid_fused=True), "v1": dict(_grid_fused
          "wide": dict(_wide=True)}
 
 
-@pytest.mark.parametrize("path", list(PATHS))
-@pytest.mark.parametrize("G", [2, 3, 5])
-def test_virtual_shards_one_gpu(G, path):
-    """G tuple-range shards on one device, flags OR-combined by the caller."""
+def _skewed_table(kind):
+    """Shard-hostile tables: rows sorted by x0 (values of x0 live in one shard
+    only), a two-block table whose halves support disjoint values, and a table
+    so small that shard 0 owns no tuple word at G = 2 (ct_shard_range)."""
+    from workloads.tables import Problem
+    if kind == "iid":
+        return random_table(5, 20, 50_000 + 33, seed=23)
+    if kind == "sorted":
+        p = random_table(5, 20, 50_000 + 33, seed=24)
+        order = np.argsort(p.tuples[:, 0], kind="stable")
+        return Problem("sorted_by_x0", p.lo, p.d, np.ascontiguousarray(p.tuples[order]), 24)
+    if kind == "halves":
+        t = np.zeros((2048, 2), np.int32)
+        t[1024:] = 1
+        return Problem("halves", np.zeros(2, np.int32), np.array([2, 2], np.int32), t, 0)
+    if kind == "tiny":
+        p = random_table(3, 6, 1000, seed=25)
+        return p
+    raise KeyError(kind)
+
+
+def _combine_virtual(states):
+    """Caller-side OR of the shard flags (all-reduce MAX over uint8), on one GPU."""
     import torch
     from paper_2507_18413_b200.sharded import flags_tensor
-    p = random_table(5, 20, 50_000 + 33, seed=23)
+    for st in states:
+        st.synchronize()
+    fl = [flags_tensor(st.handle) for st in states]
+    comb = torch.stack(fl).amax(dim=0)
+    for f in fl:
+        f.copy_(comb)
+    torch.cuda.synchronize()
+
+
+def _apply_virtual(states, wd):
+    import torch
+    outs = []
+    for st in states:
+        od = torch.zeros(max(wd, 1), dtype=torch.int64, device="cuda")
+        pd = torch.zeros(max(wd, 1), dtype=torch.int64, device="cuda")
+        sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+        C.ct_propagate_apply_async(st.handle, od, pd, sd)
+        st.synchronize()
+        outs.append((int(sd.item()), od.cpu().numpy().view(np.uint64)[:wd], pd.cpu().numpy().view(np.uint64)[:wd]))
+    return outs
+
+
+@pytest.mark.parametrize("path", list(PATHS))
+@pytest.mark.parametrize("G", [2, 3, 5])
+@pytest.mark.parametrize("kind", ["iid", "sorted", "halves", "tiny"])
+def test_virtual_shards_one_gpu(G, path, kind):
+    """G tuple-range shards on one device, flags OR-combined by the caller --
+    the root included: ct_create returns CT_PENDING after the root's local phase
+    and the root verdict comes from the combine + apply (include/ct.h).  Tables
+    whose values are supported in one shard only, and shards with no tuple."""
+    from paper_2507_18413_b200 import CT_PENDING
+    p = _skewed_table(kind)
     full = make(p)
     shards = [make(p, n_shards=G, shard_rank=g, **PATHS[path]) for g in range(G)]
-    root_m = bitmap_to_member(full.root_dom, p.d)
+    ok0, root_o = oracle_call(p, np.ones(p.R, np.uint8))[:2]
+    assert (full.root_status == CT_OK) == ok0
     for s in shards:
-        assert s.root_status == full.root_status and np.array_equal(s.root_dom, full.root_dom)
+        assert s.root_status == CT_PENDING and s.root_dom is None
+        with pytest.raises(CTError) as e:        # unusable until applied
+            s.root.clone()
+        assert e.value.status == CT_ESTATE
+    wd = full.Wd
+    roots = [s.root for s in shards]
+    _combine_virtual(roots)
+    for sd, od, _ in _apply_virtual(roots, wd):
+        assert sd == (CT_OK if ok0 else CT_FAIL)
+        if ok0:
+            assert np.array_equal(bitmap_to_member(od, p.d), root_o)
     # the shards tile the table
     rngs = [C.ct_shard_range(p.t, G, g) for g in range(G)]
     assert rngs[0][0] == 0 and sum(w for _, w in rngs) == (p.t + 63) // 64
+    if not ok0:
+        return
     states = [s.root.clone() for s in shards]
     rng = Rng(77)
-    wd = full.Wd
-    cur = root_m.copy()
+    cur = root_o.copy()
     from workloads.policies import walk_removal
+    import torch
     for k in range(60):
         r = walk_removal(rng, cur, p.d)
         if r is None:
             for st, s in zip(states, shards):
                 st.copy_from(s.root)
-            cur = root_m.copy()
+            cur = root_o.copy()
             continue
-        ok, dout, _ = oracle_call(p, cur & (1 - r))
+        din = cur & (1 - r)
+        ok, dout, _ = oracle_call(p, din)
         remd = torch.from_numpy(member_to_bitmap(r, p.d).view(np.int64)).cuda()
         for st in states:
             C.ct_propagate_local_async(st.handle, remd)
-        for st in states:
-            st.synchronize()
-        fl = [flags_tensor(st.handle) for st in states]
-        comb = torch.stack(fl).amax(dim=0)
-        for f in fl:
-            f.copy_(comb)
-        torch.cuda.synchronize()
-        outs = []
-        for st in states:
-            od = torch.zeros(wd, dtype=torch.int64, device="cuda")
-            sd = torch.zeros(1, dtype=torch.int32, device="cuda")
-            C.ct_propagate_apply_async(st.handle, od, None, sd)
-            st.synchronize()
-            outs.append((int(sd.item()), od.cpu().numpy().view(np.uint64)))
-        for sd, od in outs:
+        _combine_virtual(states)
+        for sd, od, pd in _apply_virtual(states, wd):
             assert sd == (CT_OK if ok else CT_FAIL), k
             if ok:
                 assert np.array_equal(bitmap_to_member(od, p.d), dout), k
+                assert np.array_equal(bitmap_to_member(pd, p.d), din & (1 - dout)), k
         if ok:
             cur = dout
         else:
             for st, s in zip(states, shards):
                 st.copy_from(s.root)
-            cur = root_m.copy()
+            cur = root_o.copy()
     for s in shards:
         s.close()
     full.close()
