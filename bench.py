@@ -379,21 +379,30 @@ def barrier(world):
 
 
 # ---------------------------------------------------------------- our arm
-def run_ours(args):
+def algorithmic_bytes(table_words_in, table_words_out, rows, kept_items, removed_values):
+    """SURVEY §8(d) per-call model at 64-bit-word granularity (the method's own
+    minimum, residue-independent): B_upd = 8 L_in (sum_x r_x + 2) (support
+    words of the chosen branch's rows over the active words + currTable read
+    and write), B_filt = 8 K + 8 L_out Rm (one residue probe per kept value of
+    s_sup + a full scan of every removed value's row over the surviving words)."""
+    return 8 * table_words_in * (rows + 2) + 8 * kept_items + 8 * table_words_out * removed_values
+
+
+def nonzero_words(bits):
+    return int(np.count_nonzero(bits))
+
+
+def measure_c3(workload, args, dev, world, rank, full=True):
+    """One C3-family workload (c3bulk or c3b): device-timed steps, per-kernel
+    times, kernel-counted and algorithmic bytes; with full=True also the e2e
+    host-buffer runs.  Returns a dict (rank 0's view; times max over ranks)."""
     import torch
     from paper_2507_18413_b200 import CT_OK, Table
     from paper_2507_18413_b200 import ct as C
     from paper_2507_18413_b200.sharded import broadcast_nccl_id
     from workloads import member_to_bitmap, bitmap_to_member
 
-    world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.cuda.current_device()
-    wl = WORKLOADS[args.workload]
-    p = c3_problem() if args.workload == "c3bulk" else c3b_problem()
+    p = c3_problem() if workload == "c3bulk" else c3b_problem()
     nid = broadcast_nccl_id() if world > 1 else None
     t0 = time.perf_counter()
     tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=world, shard_rank=rank, nccl_unique_id=nid)
@@ -401,7 +410,7 @@ def run_ours(args):
     assert tab.root_status == CT_OK
     root_m = bitmap_to_member(tab.root_dom, p.d)
     P = 16
-    pats = bulk_patterns(root_m, p.d, P) if args.workload == "c3bulk" else fix_patterns(root_m, p.d, P)
+    pats = bulk_patterns(root_m, p.d, P) if workload == "c3bulk" else fix_patterns(root_m, p.d, P)
     wd = tab.Wd
     rem_host = np.stack([member_to_bitmap(m, p.d) for m in pats])                 # [P][Wd] uint64
     rem_dev = torch.from_numpy(rem_host.view(np.int64)).to(f"cuda:{dev}")
@@ -415,15 +424,36 @@ def run_ours(args):
         work.copy_from(tab.root)
         work.propagate_async(rem_dev[k % P], out_dom, out_pr, status)
 
-    # per-pattern work counters (deterministic; untimed): bytes k_update moves
+    # per-pattern work counters (deterministic; untimed) and the SURVEY §8(d)
+    # algorithmic bytes from the call's inputs/outputs (active words before /
+    # after = non-zero words of this shard's currTable; rows of the chosen
+    # branches; kept / removed values of s_sup)
+    L_root = nonzero_words(tab.root.read_table())
+    d_np = np.asarray(p.d)
+    rb = np.concatenate([[0], np.cumsum(d_np)])
     per_pat = []
     for k in range(P):
         step(k)
         s = work.stats()
         assert s.last_status == CT_OK
+        dout = bitmap_to_member(out_dom.cpu().numpy().view(np.uint64), p.d)
+        din = root_m & (1 - pats[k])
+        rows = kept = removed = 0
+        for i in range(p.n):
+            di = int(din[rb[i]:rb[i + 1]].sum())
+            dl = int((root_m[rb[i]:rb[i + 1]] & pats[k][rb[i]:rb[i + 1]]).sum())
+            if dl:
+                rows += dl if dl < di else di                   # Alg. 2 L163 branch (tie -> dom)
+            if di > 1:                                          # x in s_sup
+                ko = int(dout[rb[i]:rb[i + 1]].sum())
+                kept += ko
+                removed += di - ko
+        L_out = nonzero_words(work.read_table())
         per_pat.append(dict(L_in=s.words_in, L_out=s.words_out, rows=s.n_update_rows,
                             loads=s.update_support_words, writes=s.update_table_writes,
-                            scan=s.filter_support_words, miss=s.n_residue_miss))
+                            scan=s.filter_support_words, miss=s.n_residue_miss,
+                            alg=algorithmic_bytes(L_root, L_out, rows, kept, removed),
+                            words_in=L_root, words_out=L_out, removed_values=removed, kept_values=kept))
     for k in range(args.warmup):
         step(k)
     work.synchronize()
@@ -452,37 +482,51 @@ def run_ours(args):
         step(k)
     prof = C.ct_table_profile_read(tab.handle, reset=True)
     C.ct_table_profile(tab.handle, False)
+    phases = work.stats().phase_ns
 
-    # roofline of the dominant kernel.  Fused path: k_fused runs every phase of a
-    # call (ingest, update + compaction, probe, scan, finalize) in one launch, so
-    # its bytes are the update's plus the filter's.  Per-kernel path: k_update.
-    # Bytes are counted by the kernels themselves: support words loaded, currTable
-    # blocks read/written, index entries read/written (no model, no estimate).
     dom_kernel = next((k for k in ("fused", "small") if prof.get(k, (0, 0.0))[0]), "update")
     k_n, k_ms = prof[dom_kernel]
-    byts = 0
+    counted = alg = 0
     for k in range(args.steps):
         c = per_pat[k % P]
-        # update: support words streamed + currTable read once + rewritten blocks + index in/out;
-        # filter: the support words it loads (its currTable / index re-reads are of data
-        # already counted once, and L2-resident: not counted again)
         b = 8 * c["loads"] + 16 * c["L_in"] + 16 * c["writes"] + 4 * (c["L_in"] + c["L_out"])
         if dom_kernel in ("fused", "small"):
             b += 8 * c["scan"]
-        byts += b
-    k_bytes_per_launch = byts / max(k_n, 1)
+        counted += b
+        alg += c["alg"]
     kernel_name = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_update") if dom_kernel in ("fused", "small") \
         else "ctk::k_update"
     k_ms_per_launch = k_ms / max(k_n, 1)
-    achieved = k_bytes_per_launch / (k_ms_per_launch / 1e3) / 1e9
+    k_s = k_ms_per_launch / 1e3
     peak, peak_src = peaks()
-    model = [16 * c["L_in"] * (c["rows"] + 2) for c in per_pat]                # SURVEY §8(d) B_upd (16-B blocks)
-    traffic = ncu_traffic(args.workload, world, kernel_name)
-    kernel_ms = {k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()}
+    alg_pl = alg / max(k_n, 1)
+    counted_pl = counted / max(k_n, 1)
+    traffic = ncu_traffic(workload, world, kernel_name)
     step_ms = ms_max / args.steps
-    launches = sum(v[0] for k, v in prof.items() if k != "combine")
+    roofline = {"bound": "hbm", "achieved": alg_pl / k_s / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": alg_pl / k_s / 1e9 / peak, "traffic": traffic, "kernel": kernel_name,
+                "algorithmic_bytes_per_launch": alg_pl, "ms_per_launch": k_ms_per_launch,
+                "counted_bytes_per_launch": counted_pl,
+                "counted_frac": counted_pl / k_s / 1e9 / peak,
+                "dram_frac": (traffic / k_s / 1e9 / peak) if traffic else None,
+                "bytes_model": "SURVEY §8(d): 8 L_in (sum r_x + 2) + 8 K + 8 L_out Rm at 64-bit-word granularity "
+                               "(L = non-zero currTable words of the call's input / output)",
+                "peak_source": peak_src}
+    out = dict(p=p, tab=tab, work=work, root_m=root_m, pats=pats, rem_host=rem_host, value=value,
+               ms_per_step=step_ms, build_s=build_s, roofline=roofline, clocks=clk, per_pat=per_pat,
+               kernel_ms={k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()},
+               kernel_share=k_ms_per_launch / step_ms,
+               launches=sum(v[0] for k, v in prof.items() if k != "combine") + args.steps,   # + k_state_copy per step
+               phase_ns=[int(x) for x in phases])
+    if full:
+        out["e2e"] = measure_c3_e2e(tab, work, rem_host, P, wd, args, world)
+    return out
 
-    # ---- e2e: the synchronous host-buffer C call (H2D + D2H inside every step)
+
+def measure_c3_e2e(tab, work, rem_host, P, wd, args, world):
+    """e2e through the public API on host buffers (H2D of the removal set and
+    D2H of status + domains + pruned inside every step)."""
+    import torch
     e2e_steps = max(50, min(args.steps, 400))
     host_rems = [rem_host[k % P].copy() for k in range(e2e_steps)]
     barrier(world)
@@ -495,7 +539,7 @@ def run_ours(args):
     o_dom, o_pr = np.zeros(wd, np.uint64), np.zeros(wd, np.uint64)
     for k in range(e2e_steps):
         work.copy_from(tab.root)
-        st_, dom_, pr_ = work.propagate(host_rems[k], o_dom, o_pr)
+        work.propagate(host_rems[k], o_dom, o_pr)
     t2 = time.perf_counter()
     e2e_sync_s = max_over_ranks(t2 - t1, world)
     # the same calls kept in flight: ct_propagate_async on pinned host buffers
@@ -525,46 +569,114 @@ def run_ours(args):
     if n_ok != e2e_steps:
         raise RuntimeError(f"e2e: {e2e_steps - n_ok} calls left no status")
     e2e_s = max_over_ranks(t2 - t1, world)
-    e2e = {"value": e2e_steps / e2e_s, "unit": "propagations/s", "h2d_bytes_per_step": 8 * wd,
-           "d2h_bytes_per_step": 4 + 16 * wd, "steps": e2e_steps,
-           "api": "ct_propagate_async on pinned host buffers (removal DMA'd in, status/domains/pruned "
-                  "written to host memory by the kernel), calls pipelined, every status checked on the host",
-           "host_enqueue_us_per_step": t_enq / e2e_steps * 1e6,
-           "sync_call": {"value": e2e_steps / e2e_sync_s, "unit": "propagations/s",
-                         "api": "ct_propagate (host buffers, pinned staging, CUDA graph, waits per call)",
-                         "d2h_bytes_per_step": 8 * (1 + 2 * wd)}}
+    return {"value": e2e_steps / e2e_s, "unit": "propagations/s", "h2d_bytes_per_step": 8 * wd,
+            "d2h_bytes_per_step": 4 + 16 * wd, "steps": e2e_steps,
+            "api": "ct_propagate_async on pinned host buffers (removal DMA'd in, status/domains/pruned "
+                   "written to host memory by the kernel), calls pipelined, every status checked on the host",
+            "host_enqueue_us_per_step": t_enq / e2e_steps * 1e6,
+            "sync_call": {"value": e2e_steps / e2e_sync_s, "unit": "propagations/s",
+                          "api": "ct_propagate (host buffers, pinned staging, CUDA graph, waits per call)",
+                          "d2h_bytes_per_step": 8 * (1 + 2 * wd)}}
 
-    # ---- p50 latency on config 2 (rank 0, N=1 only; latency-bound, not sharded)
-    latency = None
-    if world == 1 and not args.skip_latency and args.workload == "c3bulk":
-        latency = c2_latency(dev)
 
+def sharded_overhead(m, args, dev):
+    """N = 1: the same C3 bulk steps through the SHARDED code path (a 1-rank NCCL
+    communicator: k_fast without finalize, ncclAllReduce of the R+1 flags,
+    k_finalize) vs the unsharded single launch, and the Amdahl projection to 8
+    GPUs (the update streams 1/G of the table, the rest is fixed)."""
+    import torch
+    from paper_2507_18413_b200 import Table
+    from paper_2507_18413_b200 import ct as C
+    p, wd = m["p"], m["tab"].Wd
+    tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=1, shard_rank=0, nccl_unique_id=C.ct_nccl_unique_id())
+    rem_dev = torch.from_numpy(m["rem_host"].view(np.int64)).to(f"cuda:{dev}")
+    od = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    sd = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+    w = tab.root.clone()
+    stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+    P = len(m["rem_host"])
+
+    def run(n):
+        for k in range(n):
+            w.copy_from(tab.root)
+            w.propagate_async(rem_dev[k % P], od, None, sd)
+
+    run(args.warmup)
+    w.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    run(args.steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    t_sh = ev0.elapsed_time(ev1) / args.steps * 1e3               # us per step
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    run(args.steps)
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    tab.close()
+    t1 = m["ms_per_step"] * 1e3
+    ph = m["phase_ns"]                                             # k_fast: ingest, update(+barrier), ...
+    t_upd = ph[1] / 1e3 if ph and ph[1] > 0 else None
+    proj = {}
+    if t_upd:
+        fixed = t1 - t_upd
+        for g in (2, 4, 8):
+            proj[str(g)] = t1 / (t_upd / g + fixed + max(0.0, t_sh - t1))
+    return {"unsharded_us_per_step": t1, "sharded_path_us_per_step": t_sh, "overhead_us": t_sh - t1,
+            "kernels_us_per_launch": {k: (v[1] / v[0] * 1e3 if v[0] else None) for k, v in prof.items() if v[0]},
+            "update_phase_us": t_upd,
+            "amdahl_projected_speedup": proj,
+            "note": "1-rank NCCL communicator on one GPU: the launch/collective cost a sharded call adds; "
+                    "projection = T1 / (T_update/G + (T1 - T_update) + overhead), not a measurement"}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    wl = WORKLOADS[args.workload]
+    m = measure_c3(args.workload, args, dev, world, rank, full=True)
+    p, root_m, pats = m["p"], m["root_m"], m["pats"]
+    latency = filt = shov = None
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline(p, root_m, pats, budget_s=args.cpu_budget, what=args.workload)
-
-    tab.close()
+    m["tab"].close()
+    if world == 1 and not args.skip_latency and args.workload == "c3bulk":
+        latency = c2_latency(dev)
+    if args.workload == "c3bulk" and not args.skip_filter:
+        # the filter-heavy C3b line, so the filterDomains roofline is in every default run
+        f = measure_c3("c3b", args, dev, world, rank, full=False)
+        filt = {"workload": "c3b", "table": WORKLOADS["c3b"]["table"], "step": WORKLOADS["c3b"]["step"],
+                "value": f["value"], "unit": "propagations/s", "ms_per_step": f["ms_per_step"],
+                "roofline": f["roofline"], "kernel_share_of_step": f["kernel_share"],
+                "kernel_ms_per_launch": f["kernel_ms"], "workload_counters": f["per_pat"][0],
+                "phase_ns": f["phase_ns"], "clocks": f["clocks"]}
+        f["tab"].close()
+    if world == 1 and args.workload == "c3bulk" and not args.skip_sharded:
+        shov = sharded_overhead(m, args, dev)
     if rank == 0:
         line = {
             "metric": wl["metric"],
-            "value": value, "unit": "propagations/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+            "value": m["value"], "unit": "propagations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded " + ("i.i.d." if args.workload == "c3bulk" else "banded") + " table, workloads/)",
             "config": {"workload": args.workload, "table": wl["table"],
                        "step": wl["step"],
-                       "patterns": P, "parallelism": f"tuple-range shards x{world}" if world > 1 else "1 GPU",
+                       "patterns": 16, "parallelism": f"tuple-range shards x{world}" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (1.0 GB supports streamed each step)",
-                       "build_s": round(build_s, 3)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": kernel_name,
-                         "bytes_per_launch": k_bytes_per_launch, "ms_per_launch": k_ms_per_launch,
-                         "model_bytes_per_launch_full_rows": float(np.mean(model)),
-                         "peak_source": peak_src},
-            "kernel_ms_per_launch": kernel_ms,
-            "kernel_share_of_step": k_ms_per_launch / step_ms,
-            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "latency": latency,
-            "cpu_baseline": cpu, "workload_counters": per_pat[0],
+                       "build_s": round(m["build_s"], 3)},
+            "roofline": m["roofline"],
+            "kernel_ms_per_launch": m["kernel_ms"],
+            "kernel_share_of_step": m["kernel_share"],
+            "e2e": m["e2e"], "gpu_launches": m["launches"], "clocks": m["clocks"], "latency": latency,
+            "filter": filt, "sharded_overhead": shov,
+            "cpu_baseline": cpu, "workload_counters": m["per_pat"][0],
         }
         print(json.dumps(line))
     if world > 1:
@@ -628,44 +740,42 @@ def c2_latency(dev):
             "api": "ct_propagate (host buffers; single-CTA kernel in a CUDA graph; zero-copy I/O)"}
 
 
-def cpu_baseline(p, root_m, pats, budget_s=12.0, what="c3bulk"):
+def _time_oracle(p, root_m, pats, budget_s, threads):
     import oracle
-    oracle.lib()
     n = 0
     t0 = time.perf_counter()
     while time.perf_counter() - t0 < budget_s or n == 0:
-        rem = pats[n % len(pats)]
-        oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - rem))
+        oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - pats[n % len(pats)]), threads=threads)
         n += 1
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "propagations/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n} full {'C3 bulk' if what == 'c3bulk' else 'C3b banded'} propagations "
-                      f"(oracle/ct_oracle.c brute-force scan of all 1e7 tuples, "
-                      f"single thread) in {dt:.1f} s", "host_nproc": os.cpu_count()}
+    return n, time.perf_counter() - t0
+
+
+def cpu_baseline(p, root_m, pats, budget_s=12.0, what="c3bulk"):
+    """The oracle (oracle/ct_oracle.c, brute-force tuple scan) on the same calls,
+    on every host core this process may use (oracle_gac_split) and on one core."""
+    import oracle
+    oracle.lib()
+    cores = oracle.host_threads()
+    n1, dt1 = _time_oracle(p, root_m, pats, budget_s / 3, 1)
+    n, dt = _time_oracle(p, root_m, pats, budget_s * 2 / 3, cores)
+    name = "C3 bulk" if what == "c3bulk" else "C3b banded"
+    return {"value": n / dt, "unit": "propagations/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} full {name} propagations (oracle_gac_split: brute-force scan of all 1e7 tuples "
+                      f"split over {cores} threads) in {dt:.1f} s",
+            "single_core": {"value": n1 / dt1, "unit": "propagations/s", "cores": 1,
+                            "sample": f"{n1} calls (oracle_gac, one thread) in {dt1:.1f} s"},
+            "host_nproc": os.cpu_count()}
 
 
 # ---------------------------------------------------------------- C4: batched independent states
 def c4_patterns(p, S, count, seed=6):
-    """State-independent seeded removals [count][S][Wd] (as member arrays -> bitmaps):
+    """State-independent seeded removals [count][S][Wd] (workloads.policies.batch_coin_removals):
     per state, 2 random variables, each value removed with probability 1/2.
     Values already absent are ignored by the library (include/ct.h), so the same
     pattern applies to any state; states walk down until FAIL and are restarted
     on the device (ct_batch_restore_dead)."""
-    from workloads import Rng, member_to_bitmap
-    from workloads.layout import row_bases
-    rng = Rng(seed)
-    rb = row_bases(p.d)
-    pats = []
-    for k in range(count):
-        vars_ = rng.uniform(S * 2, p.n).reshape(S, 2)
-        coin = rng.uniform(S * 2 * int(p.d.max()), 2).reshape(S, 2, int(p.d.max()))
-        rem = np.zeros((S, p.R), np.uint8)
-        for j in range(2):
-            for x in range(p.n):
-                sel = vars_[:, j] == x
-                rem[sel, rb[x]:rb[x + 1]] |= coin[sel, j, :p.d[x]].astype(np.uint8)
-        pats.append(np.stack([member_to_bitmap(r, p.d) for r in rem]))
-    return pats
+    from workloads.policies import batch_coin_removals
+    return batch_coin_removals(p.n, p.d, S, count, seed=seed)
 
 
 def run_c4(args):
@@ -832,13 +942,17 @@ def run_c5(args):
     assert (hst.nodes, hst.trace_hash) == (stats.nodes, stats.trace_hash)
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
+        import oracle
         from oracle.dfs import dfs as oracle_dfs
-        n_or = 12
+        cores = oracle.host_threads()
+        n_or = 60
         t2 = time.perf_counter()
-        ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=n_or, max_solutions=0)
+        ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_nodes=n_or, max_solutions=0,
+                         threads=cores)
         dt = time.perf_counter() - t2
-        cpu = {"value": ref["nodes"] / dt, "unit": "nodes/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {ref['nodes']} DFS nodes by oracle/dfs.py + oracle_fixpoint (C brute force), {dt:.1f} s"}
+        cpu = {"value": ref["nodes"] / dt, "unit": "nodes/s", "cores": cores, "kind": "oracle",
+               "sample": f"first {ref['nodes']} DFS nodes by oracle/dfs.py + oracle_fixpoint_split (C brute force, "
+                         f"tuple scans over {cores} threads), {dt:.1f} s"}
         chk = M.search(value_order=0, max_nodes=n_or, max_solutions=0)[2]
         cpu["trace_matches_gpu"] = (chk.nodes, chk.trace_hash) == (ref["nodes"], ref["trace_hash"])
     wg = M.Wg
@@ -874,59 +988,213 @@ def run_c5(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- f3: placement ablation
+def record_walk(tab, p, n_calls, seed=2):
+    """A policy-P(2, 0.5) walk driven by the device-resident library (synchronous
+    host calls): [(restore_before, removal bitmap, status, out_dom)]."""
+    from paper_2507_18413_b200 import CT_OK
+    from workloads import Rng, member_to_bitmap, bitmap_to_member
+    from workloads.policies import walk_removal
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    st = tab.root.clone()
+    rng = Rng(seed, lanes=1)
+    cur, restore, seq = root_m.copy(), False, []
+    while len(seq) < n_calls:
+        r = walk_removal(rng, cur, p.d)
+        if r is None:
+            cur, restore = root_m.copy(), True
+            continue
+        if restore:
+            st.copy_from(tab.root)
+        rem = member_to_bitmap(r, p.d)
+        status, dom, _ = st.propagate(rem)
+        seq.append((restore, rem, status, None if dom is None else dom.copy()))
+        restore = status != CT_OK
+        cur = bitmap_to_member(dom, p.d) if status == CT_OK else root_m.copy()
+    st.close()
+    return seq
+
+
+def run_placement(args):
+    """SURVEY §8(f) f3 / PAPER.md L320-330, L432-436, L558-561: the same recorded
+    P(2, 0.5) walk replayed through the paper's serial CT (host), CT^u (device
+    update), CT^f (device filter), CT^uf (both, the paper's per-call currTable /
+    mask / removal-bitmap transfers) and this library's device-resident call,
+    on C2 and on the LIN_B-shaped knapsack table.  Per placement: calls/s and
+    the per-call split into host work, H2D, kernels and D2H (CUDA events), and
+    the bytes moved.  Every replayed call's status and domains are checked
+    against the recording.  1 GPU (replicas only at N > 1)."""
+    import torch
+    from paper_2507_18413_b200 import HostTable, Table, CT_OK
+    from workloads import knapsack_table, LIN_PRESETS
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    n_calls = max(50, args.steps)
+    probs = {"c2": c2_problem(), "lin_b": knapsack_table(seed=21, **LIN_PRESETS["lin_b"])}
+    out = {}
+    clocks = Clocks(dev)
+    clocks.start()
+    for name, p in probs.items():
+        tab = Table(p.lo, p.d, p.tuples, device=dev)
+        seq = record_walk(tab, p, args.warmup + n_calls)
+        res = {}
+        # device-resident (this library): ct_propagate on host buffers
+        st = tab.root.clone()
+        od, pr = np.zeros(tab.Wd, np.uint64), np.zeros(tab.Wd, np.uint64)
+        for k, (restore, rem, _, _) in enumerate(seq[:args.warmup]):
+            if restore:
+                st.copy_from(tab.root)
+            st.propagate(rem, od, pr)
+        t0 = time.perf_counter()
+        for k, (restore, rem, status, dom) in enumerate(seq[args.warmup:]):
+            if restore:
+                st.copy_from(tab.root)
+            s_, d_, _ = st.propagate(rem, od, pr)
+        dt = time.perf_counter() - t0
+        res["resident"] = {"calls_per_s": n_calls / dt, "us_per_call": dt / n_calls * 1e6,
+                           "h2d_bytes_per_call": 8 * tab.Wd, "d2h_bytes_per_call": 8 * (1 + 2 * tab.Wd),
+                           "what": "ct_propagate: state resident in HBM, removal in / status + domains out "
+                                   "(mapped pinned memory, one CUDA graph)"}
+        st.close()
+        tab.close()
+        for place in ("host", "u", "f", "uf"):
+            ht = HostTable(p.lo, p.d, p.tuples, placement=place, device=dev)
+            hs = ht.root.clone()
+            od = np.zeros(ht.Wd, np.uint64)
+            for restore, rem, _, _ in seq[:args.warmup]:
+                if restore:
+                    hs.copy_from(ht.root)
+                hs.propagate(rem, od)
+            ht.stats(reset=True)
+            mism = 0
+            t0 = time.perf_counter()
+            for restore, rem, status, dom in seq[args.warmup:]:
+                if restore:
+                    hs.copy_from(ht.root)
+                s_, d_, _ = hs.propagate(rem, od)
+                if s_ != status or (s_ == CT_OK and not np.array_equal(d_, dom)):
+                    mism += 1
+            dt = time.perf_counter() - t0
+            stt = ht.stats(reset=True)
+            c = max(stt["calls"], 1)
+            res[place] = {"calls_per_s": n_calls / dt, "us_per_call": dt / n_calls * 1e6,
+                          "host_us_per_call": stt["host_ms"] / c * 1e3, "h2d_us_per_call": stt["h2d_ms"] / c * 1e3,
+                          "kernel_us_per_call": stt["kernel_ms"] / c * 1e3, "d2h_us_per_call": stt["d2h_ms"] / c * 1e3,
+                          "h2d_bytes_per_call": stt["h2d_bytes"] / c, "d2h_bytes_per_call": stt["d2h_bytes"] / c,
+                          "kernel_launches": stt["kernel_launches"], "mismatches_vs_resident": mism}
+            if stt["kernel_ms"] > 0:
+                res[place]["copy_share_of_kernel"] = {"h2d": stt["h2d_ms"] / stt["kernel_ms"],
+                                                      "d2h": stt["d2h_ms"] / stt["kernel_ms"]}
+            ht.close()
+        out[name] = {"table": f"n={p.n}, t={p.t}, R={p.R}", "calls": n_calls, "placements": res,
+                     "speedup_vs_serial_ct": {k: res[k]["calls_per_s"] / res["host"]["calls_per_s"] for k in res}}
+    clk = clocks.stop()
+    if rank == 0:
+        v = out["c2"]["placements"]["resident"]["calls_per_s"]
+        line = {"metric": "propagations/s per CT placement (serial CT, CT^u, CT^f, CT^uf, device-resident)",
+                "value": v, "unit": "propagations/s", "n_gpus": world, "steps": n_calls, "warmup": args.warmup,
+                "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "u64", "data": "synthetic (C2 i.i.d. table; LIN_B-shaped knapsack table), recorded P(2,0.5) walks",
+                "config": {"workload": "placement", "value_is": "C2, device-resident ct_propagate (host buffers)",
+                           "parallelism": "1 GPU" if world == 1 else f"{world} replicas"},
+                "placement": out, "e2e": {"value": v, "unit": "propagations/s", "h2d_bytes_per_step": 8 * 5,
+                                          "d2h_bytes_per_step": 8 * 11},
+                "gpu_launches": None, "clocks": clk,
+                "paper_context": "PAPER.md L432-436: CT^u can underperform the serial CT (transfers); L558-561: "
+                                 "H2D up to 50 %, D2H up to 80 % of kernel time (RTX 4090)"}
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args):
+    """The reference arm of this tier: the oracle (oracle/ct_oracle.c) timed as it
+    stands on the box's host cores (all of them, oracle_gac_split), rank 0 only,
+    on the C3 bulk calls; each step is a bounded sample of the workload."""
     world, rank, local = dist_env()
     if rank != 0:
         return
     import oracle
-    from workloads import bitmap_to_member, full_member
+    from workloads import full_member
     oracle.lib()
+    cores = oracle.host_threads()
     p = c3_problem()
-    ok, root_m, _ = oracle.gac(p.lo, p.d, p.tuples, full_member(p.d))
+    ok, root_m, _ = oracle.gac(p.lo, p.d, p.tuples, full_member(p.d), threads=cores)
     pats = bulk_patterns(root_m, p.d, 16)
-    # one full oracle call costs ~0.1-0.3 s; if K+W of them would exceed ~120 s,
-    # each step runs on a contiguous tuple slice and the rate is scaled by t/slice.
+    # if K+W full calls would exceed ~120 s, each step runs on a contiguous tuple
+    # slice and the rate is scaled by t/slice (the scan is linear in t)
     t0 = time.perf_counter()
-    oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - pats[0]))
+    oracle.gac(p.lo, p.d, p.tuples, root_m & (1 - pats[0]), threads=cores)
     est = time.perf_counter() - t0
     frac = min(1.0, 120.0 / max(1e-9, est * (args.steps + args.warmup)))
     ts = max(1, int(p.t * frac))
     tup = p.tuples[:ts]
     for k in range(args.warmup):
-        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]))
+        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]), threads=cores)
     t1 = time.perf_counter()
     for k in range(args.steps):
-        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]))
+        oracle.gac(p.lo, p.d, tup, root_m & (1 - pats[k % 16]), threads=cores)
     dt = time.perf_counter() - t1
     value = args.steps / (dt * (p.t / ts))
-    sample = (f"{args.steps} C3 bulk propagations by the CPU oracle over "
+    sample = (f"{args.steps} C3 bulk propagations by the CPU oracle (tuple scan split over {cores} threads) over "
               + ("all 1e7 tuples" if ts == p.t else f"the first {ts} of 1e7 tuples, time scaled by t/{ts} (linear scan)"))
-    line = {"impl": "reference", "metric": "propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
+    line = {"impl": "reference", "metric": WORKLOADS["c3bulk"]["metric"],
             "value": value, "unit": "propagations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dt / args.steps * 1e3 * (p.t / ts), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8", "data": "synthetic (seeded i.i.d. table, workloads/)",
             "config": {"workload": "c3bulk", "table": "arity 8, domain 100, 1e7 tuples, seed 3"},
-            "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "propagations/s", "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "propagations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def launch_ranks(n):
+    """`bench.py --gpus N` outside a launcher: start N ranks of this same command
+    under torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous);
+    rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="GPUs (ranks); without a launcher, bench.py starts them itself")
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5", "lin"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5", "lin", "placement"])
     ap.add_argument("--max-nodes", type=int, default=10_000, help="c5: DFS node budget")
     ap.add_argument("--states", type=int, default=4096, help="c4: total independent states (split over ranks)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-latency", action="store_true")
+    ap.add_argument("--skip-filter", action="store_true", help="default line: no C3b filter sub-object")
+    ap.add_argument("--skip-sharded", action="store_true", help="default line: no sharded-path overhead probe")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and (args.gpus or 1) > 1:
+        sys.exit(launch_ranks(args.gpus))
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    args.gpus = world
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "c4":
@@ -935,6 +1203,8 @@ def main():
         run_c5(args)
     elif args.workload == "lin":
         run_lin(args)
+    elif args.workload == "placement":
+        run_placement(args)
     else:
         run_ours(args)
 

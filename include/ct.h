@@ -367,6 +367,44 @@ typedef struct ct_kernel_times {
 ct_status ct_table_profile(ct_table *t, int32_t enable);
 ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset);
 
+/* ---------------------------------------------------------------- placement ablation
+ * The paper's serial CT propagator and its GPU-offloaded derivatives
+ * (§4), for the placement ablation only -- a separate,
+ * explicitly selected engine; ct_propagate never routes through it:
+ *   CT_PLACE_HOST  serial CT on the host: Alg. 1-3, RSparseBitSet currTable,
+ *                  residues
+ *   CT_PLACE_U     CT^u: currTable + s_val + domains to the device, the mask
+ *                  (dom-branch OR per changed variable, AND over them) built
+ *                  by a kernel and copied back, ANDed on the host; host filter
+ *
+ *   CT_PLACE_F     CT^f: host update; currTable + domains to the device, a
+ *                  kernel returns the removal bitmap
+ *   CT_PLACE_UF    CT^uf: both kernels with the paper's per-call transfers
+ *
+ * Semantics are ct_create / ct_propagate's (same domain-bitmap layout, same
+ * results; CT_FAIL kills the state until ct_host_copy).  Host buffers only;
+ * every call is synchronous.  cfg: device, stream, update_policy are used. */
+enum { CT_PLACE_HOST = 0, CT_PLACE_U = 1, CT_PLACE_F = 2, CT_PLACE_UF = 3 };
+typedef struct ct_host_table ct_host_table;
+typedef struct ct_host_state ct_host_state;
+ct_status ct_host_create(int32_t n_vars, const int32_t *dom_lo, const int32_t *dom_size, const uint64_t *init_dom,
+                         int64_t n_tuples, const int32_t *tuples, int32_t placement, const ct_config *cfg,
+                         ct_host_table **out_table, ct_host_state **out_root, uint64_t *out_dom);
+ct_status ct_host_propagate(ct_host_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned);
+ct_status ct_host_clone(const ct_host_state *src, ct_host_state **out);
+ct_status ct_host_copy(ct_host_state *dst, const ct_host_state *src);
+int32_t ct_host_dom_words(const ct_host_table *t);
+/* Per-table accounting since the last reset: host time of the propagator's own
+ * work, CUDA-event times of the copies and kernels, bytes moved. */
+typedef struct ct_place_stats {
+  int64_t calls, noops, kernel_launches;
+  int64_t h2d_bytes, d2h_bytes;
+  double host_ms, h2d_ms, kernel_ms, d2h_ms;
+} ct_place_stats;
+ct_status ct_host_stats(ct_host_table *t, ct_place_stats *out, int32_t reset);
+void ct_host_state_destroy(ct_host_state *s);
+void ct_host_table_destroy(ct_host_table *t);   /* destroy its states first */
+
 /* Tuple-range partition used by sharded tables (host-only, no device needed):
  * shard `rank` of `n_shards` owns currTable words [*word_begin, *word_begin +
  * *words) of the ceil(n_tuples/64) words, i.e. tuples [64*begin, min(64*(begin

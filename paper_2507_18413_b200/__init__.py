@@ -8,4 +8,4 @@ from .ct import (  # noqa: F401
     CT_OK, CT_FAIL, CT_PENDING, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE,
     CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA, CTError,
 )
-from .api import Table, State, Batch, Model  # noqa: F401
+from .api import Table, State, Batch, Model, HostTable, HostState  # noqa: F401

@@ -12,6 +12,7 @@ torch.cuda.Stream owned by the table (pass `stream=` to share one).
 """
 from __future__ import annotations
 
+import ctypes
 import weakref
 
 import numpy as np
@@ -198,3 +199,68 @@ class Model:
             self.close()
         except Exception:
             pass
+
+
+class HostTable:
+    """The paper's serial CT and its GPU-offloaded derivatives (placement
+    ablation; include/ct.h ct_host_*): placement "host" (serial CT),
+    "u" (CT^u), "f" (CT^f) or "uf" (CT^uf).  Same call semantics as Table."""
+
+    def __init__(self, lo, d, tuples, placement: str = "host", init_dom=None, device: int = 0,
+                 update_policy: int = C.CT_POLICY_AUTO):
+        self.placement = placement
+        cfg = None
+        if placement != "host":
+            cfg, _ = C.make_config(device, None, None, update_policy=update_policy)
+        else:
+            cfg = C.ct_config()
+            C.lib().ct_config_init(ctypes.byref(cfg))
+            cfg.update_policy = update_policy
+        self.root_status, self.handle, self._root, self.root_dom = C.ct_host_create(
+            lo, d, tuples, C.PLACEMENTS[placement], init_dom=init_dom, cfg=cfg)
+        self.Wd = int(C.lib().ct_host_dom_words(self.handle))
+        self._states = [self._root]
+        self.root = HostState(self, self._root)
+
+    def stats(self, reset: bool = False) -> dict:
+        return C.ct_host_stats(self.handle, reset)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            for h in self._states:
+                C.ct_host_state_destroy(h)
+            self._states = []
+            C.ct_host_table_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostState:
+    def __init__(self, table: HostTable, handle):
+        self.table = table
+        self.handle = handle
+
+    def clone(self) -> "HostState":
+        h = C.ct_host_clone(self.handle)
+        self.table._states.append(h)
+        return HostState(self.table, h)
+
+    def copy_from(self, src: "HostState") -> None:
+        C.ct_host_copy(self.handle, src.handle)
+
+    def propagate(self, removed=None, out=None, pruned=None):
+        wd = self.table.Wd
+        if out is None:
+            out = np.zeros(max(wd, 1), np.uint64)
+        if pruned is None:
+            pruned = np.zeros(max(wd, 1), np.uint64)
+        rem = None if removed is None else np.ascontiguousarray(removed, np.uint64).reshape(-1)
+        if rem is not None and rem.size < wd:
+            raise ValueError(f"removed needs {wd} words")
+        st = C.ct_host_propagate(self.handle, rem, out, pruned)
+        return (st, out[:wd], pruned[:wd]) if st == C.CT_OK else (st, None, None)

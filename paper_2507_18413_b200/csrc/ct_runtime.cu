@@ -1957,3 +1957,6 @@ ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes
 void ct_model_destroy(ct_model *m) { model_free(m); }
 
 }  // extern "C"
+
+// ================================================================== placement ablation (f3)
+#include "ct_placement.cuh"

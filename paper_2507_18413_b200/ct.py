@@ -82,6 +82,16 @@ class ct_kernel_times(ctypes.Structure):
     _fields_ = [("launches", ctypes.c_int64 * 8), ("ms", ctypes.c_double * 8)]
 
 
+class ct_place_stats(ctypes.Structure):
+    _fields_ = [("calls", ctypes.c_int64), ("noops", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("host_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("d2h_ms", ctypes.c_double)]
+
+
+CT_PLACE_HOST, CT_PLACE_U, CT_PLACE_F, CT_PLACE_UF = 0, 1, 2, 3
+PLACEMENTS = {"host": CT_PLACE_HOST, "u": CT_PLACE_U, "f": CT_PLACE_F, "uf": CT_PLACE_UF}
+
 KERNEL_SLOTS = ("ingest", "update", "probe", "scan", "combine", "finalize", "fused", "small")
 
 
@@ -135,6 +145,14 @@ SIGNATURES = {
     "ct_model_search_ex": (I32, [P, I32, I64, I64, I32, P, P]),
     "ct_model_search_phases": (I32, [P, P]),
     "ct_model_destroy": (None, [P]),
+    "ct_host_create": (I32, [I32, P, P, P, I64, P, I32, P, P, P, P]),
+    "ct_host_propagate": (I32, [P, P, P, P]),
+    "ct_host_clone": (I32, [P, P]),
+    "ct_host_copy": (I32, [P, P]),
+    "ct_host_dom_words": (I32, [P]),
+    "ct_host_stats": (I32, [P, P, I32]),
+    "ct_host_state_destroy": (None, [P]),
+    "ct_host_table_destroy": (None, [P]),
     "ct_last_error": (ctypes.c_char_p, []),
     "ct_version": (ctypes.c_char_p, []),
 }
@@ -524,3 +542,54 @@ def ct_model_search_phases(model) -> dict:
 
 def ct_model_destroy(model) -> None:
     lib().ct_model_destroy(model)
+
+
+# ---------------------------------------------------------------- placement ablation
+def ct_host_create(lo, d, tuples, placement: int, init_dom=None, cfg=None):
+    """Returns (status, table, root, root_dom or None)."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.int32)
+    tuples = np.ascontiguousarray(tuples, dtype=np.int32)
+    n = int(d.size)
+    if lo.ndim != 1 or d.ndim != 1 or lo.size != n:
+        raise ValueError("lo and d must be 1-D of the same length")
+    if tuples.ndim != 2 or (tuples.shape[0] > 0 and tuples.shape[1] != n):
+        raise ValueError(f"tuples must be int32[t][{n}] (got shape {tuples.shape})")
+    t = int(tuples.shape[0])
+    wd = int(((d.astype(np.int64) + 63) // 64).sum())
+    out_dom = np.zeros(max(wd, 1), dtype=np.uint64)
+    idom = None if init_dom is None else np.ascontiguousarray(init_dom, dtype=np.uint64)
+    tab, root = ctypes.c_void_p(), ctypes.c_void_p()
+    st = lib().ct_host_create(n, _np_ptr(lo), _np_ptr(d), _np_ptr(idom), t, _np_ptr(tuples) if t else None,
+                              int(placement), ctypes.byref(cfg) if cfg is not None else None,
+                              ctypes.byref(tab), ctypes.byref(root), _np_ptr(out_dom))
+    _check(st)
+    return st, tab, root, (out_dom[:wd] if st == CT_OK else None)
+
+
+def ct_host_propagate(state, removed, out_dom, out_pruned=None) -> int:
+    return _check(lib().ct_host_propagate(state, _np_ptr(removed), _np_ptr(out_dom), _np_ptr(out_pruned)))
+
+
+def ct_host_clone(state):
+    out = ctypes.c_void_p()
+    _check(lib().ct_host_clone(state, ctypes.byref(out)), allow_fail=False)
+    return out
+
+
+def ct_host_copy(dst, src) -> None:
+    _check(lib().ct_host_copy(dst, src), allow_fail=False)
+
+
+def ct_host_stats(table, reset: bool = False) -> dict:
+    s = ct_place_stats()
+    _check(lib().ct_host_stats(table, ctypes.byref(s), int(bool(reset))), allow_fail=False)
+    return {k: getattr(s, k) for k, _ in ct_place_stats._fields_}
+
+
+def ct_host_state_destroy(state) -> None:
+    lib().ct_host_state_destroy(state)
+
+
+def ct_host_table_destroy(table) -> None:
+    lib().ct_host_table_destroy(table)

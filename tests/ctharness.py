@@ -15,8 +15,12 @@ from workloads.layout import bits_to_bool
 from workloads.policies import walk_removal
 
 
-def oracle_call(p, member_in, want_valid=False):
-    return oracle.gac(p.lo, p.d, p.tuples, member_in, want_valid=want_valid)
+def oracle_call(p, member_in, want_valid=False, threads=None):
+    """threads: host threads of the oracle's tuple scan (default: 1 for small
+    tables, every core this process may use from 1e6 tuples on)."""
+    if threads is None:
+        threads = oracle.host_threads() if p.t >= 1_000_000 else 1
+    return oracle.gac(p.lo, p.d, p.tuples, member_in, want_valid=want_valid, threads=threads)
 
 
 def check_root(tab: Table, p):

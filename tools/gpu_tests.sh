@@ -1,2 +1,13 @@
-python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/tests.log 2>&1; tail -3 gpurun_out/tests.log
+#!/bin/bash
+# GPU test pass on a gpurun box: build, then pytest -m gpu (args forwarded).
+# Usage: gpurun -- 'bash tools/gpu_tests.sh TAG [pytest args...]'
+TAG=${1:-run}; shift
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nproc > $OUT/nproc.txt
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo build failed; tail -30 $OUT/build.log; exit 1; }
+timeout 3300 python -m pytest tests -m gpu -q -rf -p no:cacheprovider "$@" > $OUT/pytest.log 2>&1
+rc=$?
+echo "pytest rc=$rc" >> $OUT/pytest.log
+tail -40 $OUT/pytest.log
+exit $rc

@@ -12,6 +12,9 @@ bench.py (no oracle) they come from the library's own output.
   Returns None when every variable is a singleton (walk solved -> restore root).
 * fix_one_value_removal (C3b banded): remove all but one seeded present value of
   one variable.
+* batch_coin_removals (C4 batched steps): per state, 2 random variables, each
+  value removed with probability 1/2; state-independent bitmaps (values already
+  absent are ignored by the library), [count][S][Wd] uint64.
 """
 from __future__ import annotations
 
@@ -63,3 +66,23 @@ def fix_one_value_removal(rng: Rng, member: np.ndarray, d, var: int = 0) -> np.n
         if v != keep:
             rem[rb[var] + v] = 1
     return rem
+
+
+def batch_coin_removals(n: int, d, S: int, count: int, seed: int = 6):
+    """[count] arrays of [S][Wd] uint64 removal bitmaps (C4)."""
+    from .layout import member_to_bitmap
+    d = np.asarray(d)
+    rng = Rng(seed)
+    rb = row_bases(d)
+    R = int(d.sum())
+    pats = []
+    for _ in range(count):
+        vars_ = rng.uniform(S * 2, n).reshape(S, 2)
+        coin = rng.uniform(S * 2 * int(d.max()), 2).reshape(S, 2, int(d.max()))
+        rem = np.zeros((S, R), np.uint8)
+        for j in range(2):
+            for x in range(n):
+                sel = vars_[:, j] == x
+                rem[sel, rb[x]:rb[x + 1]] |= coin[sel, j, :d[x]].astype(np.uint8)
+        pats.append(np.stack([member_to_bitmap(r, d) for r in rem]))
+    return pats
