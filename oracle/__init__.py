@@ -23,6 +23,13 @@ Parity status per function:
   gac / fixpoint with threads > 1 (oracle_gac_split): the same scan over
                  contiguous tuple slices, results OR-ed; pinned equal to the
                  single-thread functions on random instances.
+  gac_short      pinned: expansion of every short tuple into the product of its
+                 cells, then `gac` (positive) and Cartesian enumeration; a
+                 star-free table equals `gac`; all-star closed form.
+  gac_negative   pinned: Cartesian enumeration of the complement relation
+                 (product of the initial domains minus the list), then `gac`;
+                 empty list / full list / one-value-slab closed forms;
+                 duplicate and out-of-range invariance.
   dfs (dfs.py)   pinned: all-solutions == Cartesian enumeration; solutions in
                  descending (indomain_max) / ascending (indomain_min)
                  lexicographic order (input_order, sound propagation); the
@@ -71,6 +78,10 @@ def lib():
             L.oracle_gac_split.restype = ctypes.c_int
             L.oracle_fixpoint_split.argtypes = [ctypes.c_int32, P, P, ctypes.c_int32, P, P, P, P, P, ctypes.c_int32]
             L.oracle_fixpoint_split.restype = ctypes.c_int
+            L.oracle_gac_short.argtypes = [ctypes.c_int32, P, P, ctypes.c_int64, P, P, P, P]
+            L.oracle_gac_short.restype = ctypes.c_int
+            L.oracle_gac_negative.argtypes = [ctypes.c_int32, P, P, ctypes.c_int64, P, P, P, P]
+            L.oracle_gac_negative.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -143,3 +154,47 @@ def fixpoint(vlo, vd, scopes, tables, dom, threads: int = 1):
     if r < 0:
         raise ValueError("oracle_fixpoint: bad arguments")
     return bool(r), (out if r else None)
+
+
+STAR = -2147483648   # a short-table cell standing for every value (ct_oracle.c ORACLE_STAR)
+
+
+def gac_short(lo, d, tuples, dom_in, want_valid: bool = False):
+    """Oracle GAC on a short table (cells == STAR match any value; ct_oracle.c
+    oracle_gac_short).  Returns (ok, dom_out uint8[R] or None, valid uint8[t] or None)."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.int32)
+    tuples = np.ascontiguousarray(tuples, dtype=np.int32)
+    dom_in = np.ascontiguousarray(dom_in, dtype=np.uint8)
+    n = int(d.size)
+    t = int(tuples.shape[0]) if tuples.ndim == 2 else 0
+    dom_out = np.zeros(int(d.sum()), dtype=np.uint8)
+    valid = np.zeros(max(t, 1), dtype=np.uint8) if want_valid else None
+    r = lib().oracle_gac_short(n, _p(lo), _p(d), t, _p(tuples) if t else None, _p(dom_in), _p(dom_out),
+                               _p(valid) if want_valid else None)
+    if r < 0:
+        raise ValueError("oracle_gac_short: bad arguments")
+    return bool(r), (dom_out if r else None), (valid[:t] if want_valid else None)
+
+
+_neg_lock = threading.Lock()   # oracle_gac_negative's qsort comparator reads one global
+
+
+def gac_negative(lo, d, tuples, dom_in):
+    """Oracle GAC on a negative table (the tuples are the forbidden assignments;
+    ct_oracle.c oracle_gac_negative).  Returns (ok, dom_out or None, n_valid),
+    n_valid = distinct forbidden tuples inside dom_in."""
+    lo = np.ascontiguousarray(lo, dtype=np.int32)
+    d = np.ascontiguousarray(d, dtype=np.int32)
+    tuples = np.ascontiguousarray(tuples, dtype=np.int32)
+    dom_in = np.ascontiguousarray(dom_in, dtype=np.uint8)
+    n = int(d.size)
+    t = int(tuples.shape[0]) if tuples.ndim == 2 else 0
+    dom_out = np.zeros(int(d.sum()), dtype=np.uint8)
+    nv = np.zeros(1, dtype=np.int64)
+    with _neg_lock:
+        r = lib().oracle_gac_negative(n, _p(lo), _p(d), t, _p(tuples) if t else None, _p(dom_in),
+                                      _p(dom_out), _p(nv))
+    if r < 0:
+        raise ValueError("oracle_gac_negative: bad arguments")
+    return bool(r), (dom_out if r else None), int(nv[0])

@@ -75,3 +75,25 @@ def all_solutions(vlo, vd, scopes, tables):
         if all(tuple(a[v] for v in sc) in rel for sc, rel in zip(scopes, rels)):
             sols.append(a)
     return sols
+
+
+def short_to_positive(lo, d, tuples, star):
+    """Expand every short tuple into the Cartesian product of its cells (a star
+    cell = the variable's whole initial domain): the positive table that the
+    short table denotes (PAPER.md L66-68 footnote)."""
+    rows = set()
+    for row in np.asarray(tuples).reshape(-1, len(d)):
+        cells = [range(int(lo[i]), int(lo[i]) + int(d[i])) if int(v) == star else [int(v)]
+                 for i, v in enumerate(row)]
+        rows.update(itertools.product(*cells))
+    out = np.array(sorted(rows), dtype=np.int32)
+    return out.reshape(-1, len(d))
+
+
+def negative_to_positive(lo, d, tuples):
+    """The positive table of a negative one: every assignment of the initial
+    domains that the list does not forbid (PAPER.md L66-68 footnote)."""
+    forbidden = {tuple(int(v) for v in row) for row in np.asarray(tuples).reshape(-1, len(d))}
+    ranges = [range(int(lo[i]), int(lo[i]) + int(d[i])) for i in range(len(d))]
+    rows = [a for a in itertools.product(*ranges) if a not in forbidden]
+    return np.array(rows, dtype=np.int32).reshape(-1, len(d))

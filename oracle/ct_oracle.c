@@ -201,3 +201,146 @@ int oracle_fixpoint(int32_t nv, const int32_t *vlo, const int32_t *vd, int32_t n
 {
     return oracle_fixpoint_split(nv, vlo, vd, ntab, ar, scope, t, tuples, dom, 1);
 }
+
+/*
+ * ---------------------------------------------------------------- f4: short and
+ * negative tables (PAPER.md L66-68 and its footnote: "A table
+ * c is positive if its tuples list the allowed values for var(c).  A table
+ * explicitly listing the disallowed tuples is said negative.  A table is short
+ * if more than one domain value can be specified in each cell.").  The paper
+ * defines the tables and leaves their propagation to the cited CT extensions;
+ * GAC itself is still L52-55 on the relation the table denotes.
+ */
+
+/* Short tables: a cell holding ORACLE_STAR (INT32_MIN) stands for every value
+ * of its variable's initial domain (reading R-f4a: the star cell, the
+ * short-table form the cited extension propagates); any other cell is one value.
+ * A short tuple denotes the Cartesian product of its cells, so rel(c) is the
+ * union of those products and, by L52-55:
+ *   V = { j : every cell of tau_j meets D_in(x_i) }   (the products meeting D);
+ *   FAIL iff V is empty;
+ *   D_out(x_i) = union over j in V of (cell_j[i] intersect D_in(x_i)).
+ * valid_out (may be NULL): t bytes, 1 iff tau_j in V.  Returns 1/0/-1 as
+ * oracle_gac. */
+#define ORACLE_STAR (-2147483647 - 1)
+
+int oracle_gac_short(int32_t n, const int32_t *lo, const int32_t *d, int64_t t,
+                     const int32_t *tuples, const uint8_t *dom_in, uint8_t *dom_out,
+                     uint8_t *valid_out)
+{
+    if (n < 1) return -1;
+    int64_t *rowbase = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    uint8_t *nonempty = (uint8_t *)malloc((size_t)n);
+    if (!rowbase || !nonempty) { free(rowbase); free(nonempty); return -1; }
+    int64_t R = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        rowbase[i] = R;
+        nonempty[i] = 0;
+        for (int32_t a = 0; a < d[i]; ++a) if (dom_in[R + a]) nonempty[i] = 1;
+        R += d[i];
+    }
+    uint8_t *acc = (uint8_t *)calloc((size_t)(R > 0 ? R : 1), 1);
+    if (!acc) { free(rowbase); free(nonempty); return -1; }
+    int any_valid = 0;
+    for (int64_t j = 0; j < t; ++j) {
+        const int32_t *tau = tuples + j * (int64_t)n;
+        int valid = 1;
+        for (int32_t i = 0; i < n; ++i) {
+            if (tau[i] == ORACLE_STAR) {                      /* meets D iff D nonempty */
+                if (!nonempty[i]) { valid = 0; break; }
+            } else {
+                int64_t v = (int64_t)tau[i] - lo[i];
+                if (v < 0 || v >= d[i] || !dom_in[rowbase[i] + v]) { valid = 0; break; }
+            }
+        }
+        if (valid_out) valid_out[j] = (uint8_t)valid;
+        if (valid) {
+            any_valid = 1;
+            for (int32_t i = 0; i < n; ++i) {
+                if (tau[i] == ORACLE_STAR) {
+                    for (int32_t a = 0; a < d[i]; ++a)
+                        if (dom_in[rowbase[i] + a]) acc[rowbase[i] + a] = 1;
+                } else {
+                    acc[rowbase[i] + ((int64_t)tau[i] - lo[i])] = 1;
+                }
+            }
+        }
+    }
+    if (any_valid) memcpy(dom_out, acc, (size_t)R);
+    free(acc); free(rowbase); free(nonempty);
+    return any_valid;
+}
+
+/* Negative tables: the tuples list the FORBIDDEN assignments, so rel(c) is the
+ * product of the initial domains minus that list (duplicates list one tuple
+ * once; a tuple with a value outside [lo_i, lo_i + d_i) forbids nothing).  By
+ * L52-55, value a of x_i is supported iff some assignment of D_in with x_i = a
+ * is not forbidden, i.e. iff
+ *   c[i][a] = |{ distinct forbidden tau in D_in(x_1) x ... x D_in(x_n) : tau[i] = a }|
+ * is smaller than P_i = prod over k != i of |D_in(x_k)|, the number of such
+ * assignments.  FAIL iff some D_out(x_i) is empty.  The count is the definition
+ * written out; duplicates are removed by sorting the tuple list (qsort).
+ * nvalid_out (may be NULL): |distinct forbidden tuples inside D_in|. */
+static int32_t g_cmp_n;
+static int cmp_tuple(const void *a, const void *b)
+{
+    const int32_t *x = (const int32_t *)a, *y = (const int32_t *)b;
+    for (int32_t i = 0; i < g_cmp_n; ++i) {
+        if (x[i] < y[i]) return -1;
+        if (x[i] > y[i]) return 1;
+    }
+    return 0;
+}
+
+int oracle_gac_negative(int32_t n, const int32_t *lo, const int32_t *d, int64_t t,
+                        const int32_t *tuples, const uint8_t *dom_in, uint8_t *dom_out,
+                        int64_t *nvalid_out)
+{
+    if (n < 1) return -1;
+    int64_t *rowbase = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    double *size = (double *)malloc(sizeof(double) * (size_t)n);
+    if (!rowbase || !size) { free(rowbase); free(size); return -1; }
+    int64_t R = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        rowbase[i] = R;
+        size[i] = 0;
+        for (int32_t a = 0; a < d[i]; ++a) size[i] += dom_in[R + a] ? 1 : 0;
+        R += d[i];
+    }
+    int32_t *sorted = (int32_t *)malloc(sizeof(int32_t) * (size_t)(t > 0 ? t * n : 1));
+    int64_t *cnt = (int64_t *)calloc((size_t)(R > 0 ? R : 1), sizeof(int64_t));
+    if (!sorted || !cnt) { free(rowbase); free(size); free(sorted); free(cnt); return -1; }
+    if (t > 0) memcpy(sorted, tuples, sizeof(int32_t) * (size_t)(t * n));
+    g_cmp_n = n;   /* single-threaded by construction: the caller serialises */
+    if (t > 1) qsort(sorted, (size_t)t, sizeof(int32_t) * (size_t)n, cmp_tuple);
+    int64_t nvalid = 0;
+    for (int64_t j = 0; j < t; ++j) {
+        const int32_t *tau = sorted + j * (int64_t)n;
+        if (j > 0 && cmp_tuple(tau - n, tau) == 0) continue;     /* duplicate */
+        int inside = 1;
+        for (int32_t i = 0; i < n; ++i) {
+            int64_t v = (int64_t)tau[i] - lo[i];
+            if (v < 0 || v >= d[i] || !dom_in[rowbase[i] + v]) { inside = 0; break; }
+        }
+        if (!inside) continue;
+        ++nvalid;
+        for (int32_t i = 0; i < n; ++i) cnt[rowbase[i] + ((int64_t)tau[i] - lo[i])] += 1;
+    }
+    /* P_i in double: exact while < 2^53, and every count is <= t < 2^53, so the
+     * comparison c < P_i is exact whenever it can be false */
+    int ok = 1;
+    for (int32_t i = 0; i < n && ok; ++i) {
+        double P = 1.0;
+        for (int32_t k = 0; k < n; ++k) if (k != i) P *= size[k];
+        int any = 0;
+        for (int32_t a = 0; a < d[i]; ++a) {
+            uint8_t keep = (uint8_t)(dom_in[rowbase[i] + a] && (double)cnt[rowbase[i] + a] < P);
+            dom_out[rowbase[i] + a] = keep;
+            any |= keep;
+        }
+        if (!any) ok = 0;
+    }
+    if (nvalid_out) *nvalid_out = nvalid;
+    free(rowbase); free(size); free(sorted); free(cnt);
+    return ok;
+}
