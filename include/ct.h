@@ -139,6 +139,41 @@ ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
                     const int32_t *tuples, const ct_config *cfg, ct_table **out_table,
                     ct_state **out_root, uint64_t *out_dom);
 
+/* ---------------------------------------------------------------- f4: short and negative tables
+ * PAPER.md L66-68 and its footnote: "A table c is positive if its tuples list
+ * the allowed values for var(c).  A table explicitly listing the disallowed
+ * tuples is said negative.  A table is short if more than one domain value can
+ * be specified in each cell."  The paper evaluates positive tables only; these
+ * kinds are the extensions it names, with GAC still defined
+ * by L52-55 on the relation the table denotes.
+ *   CT_TABLE_POSITIVE  ct_create's table.
+ *   CT_TABLE_SHORT     a cell equal to CT_STAR matches every value of its
+ *                      variable (the tuple denotes the product of its cells);
+ *                      any other cell is one value as for a positive table.
+ *                      Same state, batch, sharding and async calls as positive
+ *                      tables; a column holding a star always takes Alg. 2's
+ *                      dom-branch (the Δ-branch would drop star tuples).
+ *   CT_TABLE_NEGATIVE  the tuples are the FORBIDDEN assignments: rel(c) is the
+ *                      product of the initial domains minus the list.  Value a
+ *                      of x is pruned iff every assignment of the current
+ *                      domains with x = a is listed (a count of valid listed
+ *                      tuples per (x,a) against prod_{y != x} |D_y|); CT_FAIL
+ *                      iff every assignment is listed.  Duplicate tuples are
+ *                      merged at creation (ct_state_read_table then addresses
+ *                      the distinct tuples in order of first occurrence).
+ *                      Single-state calls only (ct_propagate, _async, clone,
+ *                      copy): ct_batch_create, n_shards > 1 and the
+ *                      local/apply calls return CT_EINVAL.
+ * ct_create_table(kind, ...) takes ct_create's arguments; ct_create(...) is
+ * ct_create_table(CT_TABLE_POSITIVE, ...).  CT_STAR is an ordinary
+ * out-of-range value for the other kinds. */
+enum { CT_TABLE_POSITIVE = 0, CT_TABLE_SHORT = 1, CT_TABLE_NEGATIVE = 2 };
+#define CT_STAR INT32_MIN
+ct_status ct_create_table(int32_t kind, int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
+                          const int32_t *dom_size, const uint64_t *init_dom, int64_t n_tuples,
+                          const int32_t *tuples, const ct_config *cfg, ct_table **out_table,
+                          ct_state **out_root, uint64_t *out_dom);
+
 typedef struct ct_table_info {
   int32_t n_vars, n_rows;       /* n, R = sum d_i (support rows)          */
   int32_t dom_words;            /* Wd                                                    */
@@ -153,7 +188,8 @@ typedef struct ct_table_info {
                                 /* 1 k_fused (grid barrier per phase), 2 k_fast (per-CTA   */
                                 /* ingest, 1-2 grid barriers), 3 k_small (one CTA),        */
                                 /* 4 k_wide (one CTA + a thread-per-item filter grid: many */
-                                /* support rows over few words, e.g. the paper's LIN sets) */
+                                /* support rows over few words, e.g. the paper's LIN sets), */
+                                /* 5 negative table (ingest, update, plan, count, finalize) */
   int32_t grid;                 /* CTAs of the single-state launch                       */
   int32_t batch_tile;           /* ct_propagate_many: 16-byte blocks per shared-memory    */
                                 /* support tile of the tile-major update (32, 16 or 8), or */
@@ -413,6 +449,17 @@ void ct_host_table_destroy(ct_host_table *t);   /* destroy its states first */
  * table exactly.  Returns CT_EINVAL on bad arguments. */
 ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin,
                          int64_t *words);
+
+/* Spin watchdog (diagnostics).  Every software grid barrier and chained-scan
+ * look-back of the kernels traps after waiting 4 s (the call then fails with
+ * CT_ECUDA instead of hanging the GPU).  attach: give `device`'s kernels a
+ * host-mapped buffer to record, before trapping, which CTA waited where (its
+ * kind, polled words, location marker, barrier count) and every CTA's location
+ * and barrier count.  read: copy up to n_words of that buffer (no CUDA call, so
+ * it works while a kernel spins); word 0 == 0xD1A6D1A6 once a report is
+ * complete.  Returns the words copied. */
+ct_status ct_debug_diag_attach(int32_t device);
+int64_t ct_debug_diag_read(uint64_t *out, int64_t n_words);
 
 /* NCCL bootstrap helper: writes a fresh 128-byte ncclUniqueId (rank 0 calls it
  * and broadcasts the bytes, e.g. with torch.distributed). */

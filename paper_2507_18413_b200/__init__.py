@@ -7,5 +7,6 @@ from . import ct  # noqa: F401  (C names: ct.ct_create, ct.ct_propagate, ...)
 from .ct import (  # noqa: F401
     CT_OK, CT_FAIL, CT_PENDING, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE,
     CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA, CTError,
+    CT_TABLE_POSITIVE, CT_TABLE_SHORT, CT_TABLE_NEGATIVE, CT_STAR,
 )
 from .api import Table, State, Batch, Model, HostTable, HostState  # noqa: F401

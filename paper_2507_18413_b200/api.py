@@ -24,7 +24,9 @@ class Table:
     def __init__(self, lo, d, tuples, init_dom=None, scope=None, device: int = 0, stream=None,
                  torch_alloc: bool = True, n_shards: int = 1, shard_rank: int = 0, nccl_unique_id=None,
                  update_policy: int = C.CT_POLICY_AUTO, use_residues: bool = True, use_index: bool = True,
-                 use_graph: bool = True, use_fused: bool = True):
+                 use_graph: bool = True, use_fused: bool = True, kind: str | int = "positive"):
+        """kind: "positive" (ct_create), "short" (cells == CT_STAR match any value)
+        or "negative" (the tuples are the forbidden assignments) -- include/ct.h f4."""
         import torch
         self.device = int(device)
         if stream is None:
@@ -39,7 +41,8 @@ class Table:
                                         use_fused)
         self.lo = np.ascontiguousarray(lo, np.int32)
         self.d = np.ascontiguousarray(d, np.int32)
-        status, handle, root, dom = C.ct_create(self.lo, self.d, tuples, init_dom, scope, cfg)
+        self.kind = C.TABLE_KINDS[kind] if isinstance(kind, str) else int(kind)
+        status, handle, root, dom = C.ct_create(self.lo, self.d, tuples, init_dom, scope, cfg, kind=self.kind)
         self.handle = handle
         self._states = weakref.WeakSet()
         self._batches = weakref.WeakSet()

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
       if (sz) {
         const int g = (int)(ex & 0xffffffffu);
         const int pst = (int)(ex >> 32);
-        const bool useDelta = tb.policy == 2 || (tb.policy == 0 && s_cd[x] < s_cs[x]);
+        const bool useDelta = use_delta(tb, x, s_cd[x], s_cs[x]);
         pl[4 + g] = (uint32_t)pst | ((uint32_t)sz << 16) | (useDelta ? 0x80000000u : 0u);
         const uint32_t *ul = reinterpret_cast<const uint32_t *>(st.ulist);
         const int psz = (sz + 3) & ~3;

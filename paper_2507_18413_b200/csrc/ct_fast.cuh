@@ -199,10 +199,15 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
       for (int q = 0; q < kBarGroups; ++q) *(volatile uint32_t *)(bar + (1 + q) * kBarLine) = g;
       last = 1;
     } else {
-      while ((g = ld_acquire_u32(mygen)) == my_gen) __nanosleep(32);
+      SpinGuard sg;
+      while ((g = ld_acquire_u32(mygen)) == my_gen) {
+        __nanosleep(32);
+        spin_check(sg, 3, my_gen, *(volatile uint32_t *)cnt, old);
+      }
     }
     *s_mode = (int)(g & 1u);
     leader = last;
+    if (blockIdx.x < kDiagCtas) g_bseq[blockIdx.x] += 1;
   }
   __syncthreads();
   return *s_mode;
@@ -310,7 +315,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   // per variable: s_val (Δ_x ≠ ∅), branch (Alg. 2: Δ-branch iff |Δ_x| < |D_x|), s_sup (|D_x| > 1)
   for (int x = tid; x < n; x += NT) {
     const int cd = p.cd[x], cs = p.cs[x];
-    const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+    const bool useDelta = use_delta(tb, x, cd, cs);
     p.vfl[x] = (useDelta ? 1 : 0) | (cd > 0 ? 2 : 0);
     if (cd > 0) atomicAdd(&fs.ngroups, 1);
     if (cs == 0) fs.fail = 1;                   // D_x empty -> no valid tuple

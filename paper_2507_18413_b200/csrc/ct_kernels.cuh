@@ -47,6 +47,7 @@ constexpr int kScanUnroll = 4;    // index entries (16-byte blocks) per lane per
 constexpr int kFirstScan = 32 * kScanUnroll * 2;     // entries probe scans itself (2 rounds)
 constexpr int kScanChunk = 32 * kScanUnroll * 2;     // entries per scan work unit (2 rounds)
 
+constexpr int32_t kStar = INT32_MIN;          // short-table wildcard cell (CT_STAR, include/ct.h)
 constexpr uint32_t kRowMask = 0x3FFFFFFFu;   // update-list entry: row id
 constexpr uint32_t kEndBit = 1u << 30;        //   last row of its variable's group
 constexpr uint32_t kInvBit = 1u << 31;        //   group uses the Δ-branch (complemented)
@@ -76,7 +77,16 @@ struct TableDev {
   int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
   const int32_t *gword;     // [Wd] model tables only: global domain word of each domain word
   const int32_t *gshared;   // [Wd] model tables only: 1 if another table also constrains the word's variable
+  const int32_t *domOnly;   // [n] or nullptr: 1 if x's column has a star cell (short tables, f4), so the
+                            // Δ-branch (which drops every tuple whose row has a removed value) is unsound
+                            // for x: a star tuple is in every row of x and must survive
 };
+
+// Alg. 2: Δ-branch iff |Δ_x| < |D_x| (CT_POLICY_AUTO), or forced by the
+// policy -- never for a starred column of a short table.
+__device__ __forceinline__ bool use_delta(const TableDev &tb, int x, int cd, int cs) {
+  return (tb.policy == 2 || (tb.policy == 0 && cd < cs)) && !(tb.domOnly && tb.domOnly[x]);
+}
 
 // Per-state control block (device).  The first fields up to last_status persist
 // across calls (they are part of the state); the rest is per-call scratch.
@@ -107,6 +117,10 @@ struct Ctl {
   int32_t cta_done;    // k_fast: CTAs done with the filter; the last one finalizes
                        // and resets it to 0 (so a copied state always holds 0)
   int32_t pad[1];
+  // negative tables (ct_neg.cuh): valid forbidden tuples after the last call
+  // (persists; copied with the state) and this call's running count
+  unsigned long long nvalid;
+  unsigned long long nvalid_new;
 };
 static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
 
@@ -126,6 +140,10 @@ struct StateDev {
   uint64_t *out;            // [1 + 2 Wd]: status word, dom, pruned (sync path)
   uint64_t *slot;           // [Wd] removed (sync path, filled by an H2D copy)
   uint32_t *bar;            // [kBarWords] k_fast hierarchical grid barrier (zeroed at creation)
+  // negative tables only (nullptr otherwise; ct_neg.cuh)
+  uint64_t *pend;           // [Wd] values the last filter pruned whose tuples are still in currTable
+  unsigned long long *cnt;  // [R] per-row count of valid forbidden tuples (this call)
+  unsigned long long *prod; // [n] P_x = prod over y != x of |D_y| (saturating)
 };
 
 // ------------------------------------------------------------------ helpers
@@ -162,6 +180,70 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// ------------------------------------------------------------------ spin watchdog
+// Every software grid barrier and chained-scan look-back polls through
+// spin_check: after kSpinLimitNs of waiting the CTA records where it waits
+// (kind, its location marker, the words it polls) into the host-mapped
+// diagnostic buffer (ct_debug_diag_attach / _read), the first reporter also
+// copies every CTA's location and barrier count, and the kernel traps -- a lost
+// arrival then surfaces as CT_ECUDA instead of a GPU spinning forever.
+constexpr unsigned long long kSpinLimitNs = 4000000000ull;   // 4 s: phases take us to ms
+constexpr int kDiagCtas = 4096;
+__device__ unsigned long long *g_diag;     // host-mapped [kDiagWords] or nullptr
+__device__ uint32_t g_loc[kDiagCtas];      // per-CTA location marker (phase code)
+__device__ uint32_t g_bseq[kDiagCtas];     // per-CTA grid-barrier count
+__device__ uint32_t g_diag_n;              // reports written
+constexpr int kDiagWords = 64 + 16 * 8 + 2 * kDiagCtas;   // header, 16 reports, loc + bseq
+
+__device__ __forceinline__ void set_loc(uint32_t code) {
+  if (threadIdx.x == 0 && blockIdx.x < kDiagCtas) g_loc[blockIdx.x] = code;
+}
+
+__device__ __noinline__ void spin_report(uint32_t kind, unsigned long long a, unsigned long long b,
+                                         unsigned long long c) {
+  unsigned long long *d = g_diag;
+  if (!d) return;
+  const uint32_t k = atomicAdd(&g_diag_n, 1u);
+  if (k < 16) {
+    unsigned long long *r = d + 64 + 8 * k;
+    r[0] = kind;
+    r[1] = blockIdx.x;
+    r[2] = a;
+    r[3] = b;
+    r[4] = c;
+    r[5] = blockIdx.x < kDiagCtas ? *(volatile uint32_t *)&g_loc[blockIdx.x] : 0;
+    r[6] = blockIdx.x < kDiagCtas ? *(volatile uint32_t *)&g_bseq[blockIdx.x] : 0;
+    r[7] = gridDim.x;
+  }
+  if (k == 0) {
+    const int G = min((int)gridDim.x, kDiagCtas);
+    for (int i = 0; i < G; ++i) {
+      d[64 + 128 + i] = *(volatile uint32_t *)&g_loc[i];
+      d[64 + 128 + kDiagCtas + i] = *(volatile uint32_t *)&g_bseq[i];
+    }
+  }
+  __threadfence_system();
+  if (k == 0) d[0] = 0xD1A6D1A6ull;   // header: a report is complete
+  __threadfence_system();
+}
+
+struct SpinGuard {
+  unsigned long long t0 = 0;
+  uint32_t n = 0;
+};
+__device__ __forceinline__ void spin_check(SpinGuard &g, uint32_t kind, unsigned long long a, unsigned long long b,
+                                           unsigned long long c) {
+  if ((++g.n & 255u) != 0) return;
+  const unsigned long long t = globaltimer();
+  if (g.t0 == 0) {
+    g.t0 = t;
+    return;
+  }
+  if (t - g.t0 < kSpinLimitNs) return;
+  spin_report(kind, a, b, c);
+  __trap();
 }
 
 // Exclusive block scan of a 64-bit value over NT threads (two packed 32-bit
@@ -208,7 +290,11 @@ __device__ __forceinline__ void grid_barrier(Ctl *c) {
       __threadfence();
       atomicAdd(&c->bar_gen, 1u);
     } else {
-      while (ld_acquire_u32(&c->bar_gen) == gen) __nanosleep(20);
+      SpinGuard sg;
+      while (ld_acquire_u32(&c->bar_gen) == gen) {
+        __nanosleep(20);
+        spin_check(sg, 1, gen, c->bar_count, 0);
+      }
     }
     __threadfence();
   }
@@ -227,11 +313,12 @@ __host__ __device__ inline size_t finalize_smem_bytes(int n, int Wd) {
 // every in-range value (cell ([x_i,v], j) = 1 iff tau_j[i] = v),
 // and the in-range validity of tau_j into the initial currTable (one ballot
 // per 32 tuples -> one 32-bit half-word).  Out-of-range values create no row
-// bit and make the tuple invalid forever.
+// bit and make the tuple invalid forever.  A star cell (short
+// tables, f4) sets bit j in every row of x_i.
 __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int n,
                         const int32_t *__restrict__ lo, const int32_t *__restrict__ d,
                         const int32_t *__restrict__ rowBase, uint64_t *__restrict__ S, int64_t Wp,
-                        uint32_t *__restrict__ T32, int64_t n_half_words) {
+                        uint32_t *__restrict__ T32, int64_t n_half_words, int allow_star) {
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = j < t_local;
   if (valid) {
@@ -239,6 +326,12 @@ __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int
     const uint64_t bit = 1ull << (j & 63);
     const int64_t word = j >> 6;
     for (int i = 0; i < n; ++i) {
+      if (allow_star && tau[i] == kStar) {   // short table: the cell matches every value of x_i
+        for (int a = 0; a < d[i]; ++a)
+          atomicOr(reinterpret_cast<unsigned long long *>(S + (int64_t)(rowBase[i] + a) * Wp + word),
+                   (unsigned long long)bit);
+        continue;
+      }
       const int64_t v = (int64_t)tau[i] - lo[i];
       if (v >= 0 && v < d[i]) {
         atomicOr(reinterpret_cast<unsigned long long *>(S + (int64_t)(rowBase[i] + v) * Wp + word),
@@ -311,9 +404,14 @@ __device__ int dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t
 
   // phase 1 (Alg. 1 L1-2): Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes
   for (int k = tid; k < Wd; k += NT) {
-    const uint64_t dm = k == tid ? dm0 : st.dom[k];
+    uint64_t dm = k == tid ? dm0 : st.dom[k];
     // model tables: a value is removed iff the shared (global) domain lost it
-    const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
+    uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
+    if (st.pend) {   // negative table: values the last filter pruned leave currTable now
+      const uint64_t pd = st.pend[k];
+      dm |= pd;
+      rm |= pd;
+    }
     const int x = k == tid ? wv0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     s_din[k] = di;
@@ -330,7 +428,7 @@ __device__ int dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t
     uint64_t ucnt = 0;
     if (x < n) {
       const int cd = s_cd[x], cs = s_cs[x];
-      const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+      const bool useDelta = use_delta(tb, x, cd, cs);
       if (cd > 0) {
         ucnt = (uint64_t)(useDelta ? cd : cs);
         atomicAdd(&s_ngroups, 1);
@@ -361,7 +459,7 @@ __device__ int dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t
         const int a = r - s_rb[x];
         const int w = s_do[x] + (a >> 6), b = a & 63;
         const int cd = s_cd[x], cs = s_cs[x];
-        useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+        useDelta = use_delta(tb, x, cd, cs);
         const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
         u = cd > 0 && (useDelta ? inDl : inD);
         f = cs > 1 && inD;
@@ -460,7 +558,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         int ucnt = 0;
         if (x < n) {
           const int cd = s_cd[x], cs = s_cs[x];
-          const bool useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+          const bool useDelta = use_delta(tb, x, cd, cs);
           if (cd > 0) ucnt = useDelta ? cd : cs;
           ngroups += cd > 0;
           fail |= cs == 0;
@@ -495,7 +593,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
             const int a = r - s_rb[x];
             const int w = s_do[x] + (a >> 6), b = a & 63;
             const int cd = s_cd[x], cs = s_cs[x];
-            useDelta = tb.policy == 2 || (tb.policy == 0 && cd < cs);
+            useDelta = use_delta(tb, x, cd, cs);
             const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
             u = cd > 0 && (useDelta ? inDl : inD);
             f = cs > 1 && inD;
@@ -548,8 +646,10 @@ __device__ __forceinline__ uint32_t tile_lookback(unsigned long long *ts, int ti
     const int p = base - lane;
     unsigned long long s = kFlagPre;   // before tile 0: prefix 0
     if (p >= 0) {
+      SpinGuard sg;
       do {
         s = ld_acquire(ts + p);
+        if ((s >> 62) == 0) spin_check(sg, 2, (unsigned long long)tile, (unsigned long long)p, 0);
       } while ((s >> 62) == 0);
     }
     const unsigned pre = __ballot_sync(0xffffffffu, (s >> 62) == 2);

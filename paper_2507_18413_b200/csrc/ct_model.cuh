@@ -143,6 +143,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     // Each CTA's verdicts ride on its barrier arrival (active tables + 256 x
     // failed tables); the releasing CTA decides whether the fixpoint stops
     // (a FAIL, or no table has anything to do) and keeps the statistics.
+    set_loc(0x10000000u | ((uint32_t)it << 8) | 1u);
     if (tid == 0) s_cnt_ing = 0;
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const int r = dev_ingest<kFusedTPB>(md.tabs[k], md.sts[k], nullptr, 0, smem, md.gdom);
@@ -168,6 +169,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       lap(0);
       if (brk) break;
     }
+    set_loc(0x10000000u | ((uint32_t)it << 8) | 2u);
     // ---- update (a3-a5): tiles of all tables pooled over the grid
     // (every table's parameters loaded by its own thread: one round trip)
     if (tid < ntab) {
@@ -188,6 +190,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     }
     model_barrier(mc);
     lap(1);
+    set_loc(0x10000000u | ((uint32_t)it << 8) | 3u);
     // ---- probe (a6a): items of all tables pooled over the warps
     if (tid < ntab) {
       s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
@@ -213,6 +216,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
       lap(2);
       if (mode == 1) goto finalize_phase;
     }
+    set_loc(0x10000000u | ((uint32_t)it << 8) | 4u);
     // ---- scan (a6b): misses x chunks of all tables pooled over the warps
     if (tid < ntab) {
       s_fp[tid] = load_filt_params(md.tabs[tid], md.sts[tid]);
@@ -233,6 +237,7 @@ __device__ void model_fixpoint_dev(const ModelDev &md, int max_iters, uint64_t *
     // ---- finalize (a6c-a7): one block per table; AND the new domains into the shared ones.
     // Verdicts on the barrier arrival again: CTAs that removed a value from
     // the shared domains + 256 x failed tables.
+    set_loc(0x10000000u | ((uint32_t)it << 8) | 5u);
     if (tid == 0) s_cnt_fin = 0;
     for (int k = blockIdx.x; k < ntab; k += gridDim.x) {
       const TableDev &tb = md.tabs[k];
@@ -424,6 +429,7 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, Sear
   __syncthreads();
   while (c.state != kSDone) {
     const int state = c.state;
+    set_loc(0x20000000u | ((uint32_t)state << 16) | ((uint32_t)c.d & 0xffffu));
     if (state == kSExpand) {
       // the node at depth d is an OK fixpoint: pick x (input_order) and a
       // (indomain_max / min); the shared domains go to shared memory first
@@ -466,6 +472,12 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, Sear
         }
       }
       __syncthreads();
+      // every CTA read the shared domains above; unless the next step is the
+      // branch (whose snapshot barrier comes first), the next step may restore
+      // the pool -- shared domains included -- so no CTA may move on before all
+      // have read them (else a late CTA reads restored domains, picks another
+      // step, and the grid's control flow splits)
+      if (c.state != kSBranch) model_barrier(mc);
     } else if (state == kSBranch) {
       const SearchFrame f = fr[c.d];
       if (f.branch == 2) {

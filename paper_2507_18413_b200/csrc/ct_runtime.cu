@@ -20,6 +20,7 @@
 #include "ct_fast.cuh"
 #include "ct_batch.cuh"
 #include "ct_wide.cuh"
+#include "ct_neg.cuh"
 
 using namespace ctk;
 
@@ -79,7 +80,7 @@ inline int plist_po(int n) { return 4 + (int)round_up(n + 1, 4); }
 // is what ct_state_copy moves; the rest is per-call scratch.
 struct StateLayout {
   size_t ctl, T, idx0, idx1, res, dom, persist;
-  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, bmask, plist, desc, total;
+  size_t din, ulist, items, scanlist, sup, varcnt, tilestat, out, slot, bar, bmask, plist, cnt, prod, desc, total;
 };
 
 }  // namespace
@@ -91,6 +92,7 @@ struct ct_table {
   ct_allocator alloc{};
   bool has_alloc = false;
   int n = 0, R = 0, Wd = 0;
+  int kind = CT_TABLE_POSITIVE;      // CT_TABLE_* (f4: short / negative tables)
   int64_t t = 0, Wtot = 0, wbeg = 0, W = 0, Wp = 0, t_local = 0;
   int policy = 0, use_res = 1, use_index = 1, use_graph = 1;
   int n_shards = 1, rank = 0;
@@ -119,6 +121,7 @@ struct ct_table {
   size_t wide_smem = 0;
   int bt_tw = 0, bt_grid = 0;        // tile-major batch update (ct_batch.cuh): tile width, 0 = per-state kernels
   size_t bt_smem = 0;
+  int neg_occ = 1;                   // k_neg_count CTAs per SM (negative tables)
   int live = 0;   // states + batches alive
 
   void *dalloc(size_t bytes) {
@@ -185,7 +188,9 @@ static StateLayout make_layout(const ct_table *tb) {
   L.idx0 = take(tb->Wp / 2 * 4);   // index over 16-byte blocks
   L.idx1 = take(tb->Wp / 2 * 4);
   L.res = take((size_t)tb->R * 4);
-  L.dom = take((size_t)tb->Wd * 8);
+  // negative tables: dom is followed by pend[Wd] (values pruned by the last
+  // filter whose tuples are still in currTable; part of the state)
+  L.dom = take((size_t)tb->Wd * 8 * (tb->kind == CT_TABLE_NEGATIVE ? 2 : 1));
   L.persist = o;
   L.din = take((size_t)tb->Wd * 8);
   L.ulist = take((size_t)tb->R * 4);
@@ -200,6 +205,8 @@ static StateLayout make_layout(const ct_table *tb) {
   L.bar = take((size_t)kBarWords * 4);
   L.bmask = take((size_t)(tb->dev.W2 + 31) / 32 * 4);   // batch path: survivor bit per 16-byte block
   L.plist = take((size_t)(plist_po(tb->n) + tb->R + 3 * tb->n + 36) * 4);   // batch path: padded update list
+  L.cnt = take(tb->kind == CT_TABLE_NEGATIVE ? (size_t)tb->R * 8 : 0);   // negative tables: row counts
+  L.prod = take(tb->kind == CT_TABLE_NEGATIVE ? (size_t)tb->n * 8 : 0);  //   and P_x
   L.desc = take(sizeof(StateDev));
   L.total = o;
   return L;
@@ -224,6 +231,11 @@ static StateDev make_desc(const ct_table *tb, char *mem) {
   s.out = reinterpret_cast<uint64_t *>(mem + L.out);
   s.slot = reinterpret_cast<uint64_t *>(mem + L.slot);
   s.bar = reinterpret_cast<uint32_t *>(mem + L.bar);
+  if (tb->kind == CT_TABLE_NEGATIVE) {
+    s.pend = s.dom + tb->Wd;
+    s.cnt = reinterpret_cast<unsigned long long *>(mem + L.cnt);
+    s.prod = reinterpret_cast<unsigned long long *>(mem + L.prod);
+  }
   return s;
 }
 
@@ -237,7 +249,7 @@ static CopyLayout copy_layout(const ct_table *tb) {
   cl.o_res = (int64_t)L.res;
   cl.o_dom = (int64_t)L.dom;
   cl.res_bytes = (int64_t)tb->R * 4;
-  cl.dom_bytes = (int64_t)tb->Wd * 8;
+  cl.dom_bytes = (int64_t)tb->Wd * 8 * (tb->kind == CT_TABLE_NEGATIVE ? 2 : 1);   // + pend
   return cl;
 }
 
@@ -339,6 +351,32 @@ static ct_status enqueue_finalize(ct_table *tb, const StateDev *d_desc, int S, u
   return CT_OK;
 }
 
+// One call on a negative table (ct_neg.cuh).
+static ct_status enqueue_neg(ct_table *tb, ct_state *s, const uint64_t *removed, int root_mode, uint64_t *out_dom,
+                             uint64_t *out_pruned, int32_t *out_status, int use_state_out) {
+  cudaStream_t st = s->stream;
+  const StateDev *d = s->d_desc;
+  int e = prof_event(tb, st);
+  k_ingest<<<dim3(1, 1), kIngestTPB, ingest_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, d, removed, tb->Wd,
+                                                                              root_mode);
+  prof_mark(tb, 0, e, st);
+  e = prof_event(tb, st);
+  k_update<<<dim3(update_blocks(tb, 1), 1), kUpdTPB, 0, st>>>(tb->dev, d);
+  prof_mark(tb, 1, e, st);
+  e = prof_event(tb, st);
+  k_neg_plan<<<1, kIngestTPB, (size_t)std::max(tb->n, 1) * 8, st>>>(tb->dev, d);
+  prof_mark(tb, 2, e, st);
+  e = prof_event(tb, st);
+  k_neg_count<<<tb->sm_count * tb->neg_occ, kNegTPB, 0, st>>>(tb->dev, d);
+  prof_mark(tb, 3, e, st);
+  e = prof_event(tb, st);
+  k_neg_finalize<<<1, kFinTPB, finalize_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, d, out_dom, out_pruned,
+                                                                          out_status, use_state_out);
+  prof_mark(tb, 5, e, st);
+  CUDA_TRY(cudaGetLastError());
+  return CT_OK;
+}
+
 // One single-state call.  Fused: one cooperative launch runs every phase (the
 // finalize phase too unless the flags must first be combined across shards);
 // otherwise one kernel per phase.  local_only stops before the combine.
@@ -346,6 +384,10 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                 bool local_only) {
   cudaStream_t st = s->stream;
+  if (tb->kind == CT_TABLE_NEGATIVE) {   // ct_neg.cuh: shared ingest + update, counting filter
+    CT_TRY(enqueue_neg(tb, s, removed, root_mode, out_dom, out_pruned, out_status, use_state_out));
+    return CT_OK;
+  }
   if (tb->use_wide) {
     const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
     const int e = prof_event(tb, st);
@@ -560,6 +602,29 @@ int ct_debug_trace_read(void *out, size_t bytes) {
   return (int)cudaMemcpyFromSymbol(out, g_fast_trace, bytes);
 }
 #endif
+// Spin-watchdog diagnostics (ct_kernels.cuh spin_report): one host-mapped
+// buffer per process, attached to a device's g_diag.
+static unsigned long long *g_diag_host = nullptr;
+ct_status ct_debug_diag_attach(int32_t device) {
+  DeviceGuard g(device);
+  if (!g_diag_host) {
+    CUDA_TRY(cudaHostAlloc((void **)&g_diag_host, sizeof(unsigned long long) * kDiagWords, cudaHostAllocMapped |
+                                                                                             cudaHostAllocPortable));
+    memset(g_diag_host, 0, sizeof(unsigned long long) * kDiagWords);
+  }
+  unsigned long long *dp = nullptr;
+  CUDA_TRY(cudaHostGetDevicePointer((void **)&dp, g_diag_host, 0));
+  CUDA_TRY(cudaMemcpyToSymbol(g_diag, &dp, sizeof dp));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return CT_OK;
+}
+int64_t ct_debug_diag_read(uint64_t *out, int64_t n_words) {
+  if (!g_diag_host || !out) return 0;
+  const int64_t n = std::min<int64_t>(n_words, kDiagWords);
+  for (int64_t i = 0; i < n; ++i) out[i] = ((volatile unsigned long long *)g_diag_host)[i];
+  return n;
+}
+
 const char *ct_version(void) { return "ct_b200 0.1 (sm_100a)"; }
 
 ct_status ct_nccl_unique_id(void *out128) {
@@ -571,13 +636,50 @@ ct_status ct_nccl_unique_id(void *out128) {
   return CT_OK;
 }
 
-static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom_lo, const int32_t *dom_size,
-                             const uint64_t *init_dom, int64_t n_tuples, const int32_t *tuples,
-                             const ct_config *cfg_in, ct_table **out_table, ct_state **out_root,
-                             uint64_t *out_dom, ct_table *tb) {
+// Negative tables list each forbidden assignment once (ct_neg.cuh counts
+// currTable bits): the distinct tuples in order of first occurrence.  Rows are
+// grouped by a 64-bit hash (sort of (hash, index) pairs), equal hashes compared
+// exactly.
+static std::vector<int32_t> distinct_tuples(int32_t n, int64_t t, const int32_t *tuples) {
+  std::vector<std::pair<uint64_t, int64_t>> h((size_t)t);
+  for (int64_t j = 0; j < t; ++j) {
+    uint64_t x = 0x9E3779B97F4A7C15ull;
+    for (int i = 0; i < n; ++i) {
+      x ^= (uint32_t)tuples[j * n + i];
+      x *= 0xBF58476D1CE4E5B9ull;
+      x ^= x >> 31;
+    }
+    h[(size_t)j] = {x, j};
+  }
+  std::sort(h.begin(), h.end());
+  std::vector<char> keep((size_t)t, 1);
+  for (size_t a = 0; a < h.size();) {
+    size_t b = a + 1;
+    while (b < h.size() && h[b].first == h[a].first) ++b;
+    for (size_t i = a + 1; i < b; ++i)       // run sorted by index: keep each row's first occurrence
+      for (size_t k = a; k < i; ++k)
+        if (keep[(size_t)h[k].second] &&
+            !memcmp(tuples + h[i].second * n, tuples + h[k].second * n, sizeof(int32_t) * (size_t)n)) {
+          keep[(size_t)h[i].second] = 0;
+          break;
+        }
+    a = b;
+  }
+  std::vector<int32_t> out;
+  for (int64_t j = 0; j < t; ++j)
+    if (keep[(size_t)j]) out.insert(out.end(), tuples + j * n, tuples + (j + 1) * n);
+  return out;
+}
+
+static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, const int32_t *dom_lo,
+                             const int32_t *dom_size, const uint64_t *init_dom, int64_t n_tuples,
+                             const int32_t *tuples, const ct_config *cfg_in, ct_table **out_table,
+                             ct_state **out_root, uint64_t *out_dom, ct_table *tb) {
   ct_config cfg;
   if (cfg_in) cfg = *cfg_in;
   else ct_config_init(&cfg);
+  if (kind != CT_TABLE_POSITIVE && kind != CT_TABLE_SHORT && kind != CT_TABLE_NEGATIVE)
+    return fail(CT_EINVAL, "bad table kind %d", kind);
 
   // ---------------- validation (include/ct.h)
   if (n < 1) return fail(CT_EINVAL, "n_vars must be >= 1 (got %d)", n);
@@ -602,12 +704,29 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
     if (std::adjacent_find(sc.begin(), sc.end()) != sc.end())
       return fail(CT_EINVAL, "duplicate variable in scope (var(c) is a set, PAPER.md L48)");
   }
+  if (kind == CT_TABLE_NEGATIVE && cfg.n_shards != 1)
+    return fail(CT_EINVAL, "negative tables are not sharded (their filter counts; the shard combine is an OR)");
+  std::vector<int32_t> distinct;
+  if (kind == CT_TABLE_NEGATIVE && n_tuples > 0) {
+    distinct = distinct_tuples(n, n_tuples, tuples);
+    n_tuples = (int64_t)distinct.size() / n;
+    tuples = distinct.data();
+  }
+  // short tables: a column with a star cell never takes the Δ-branch (use_delta)
+  std::vector<int32_t> dom_only;
+  if (kind == CT_TABLE_SHORT) {
+    dom_only.assign(n, 0);
+    for (int64_t j = 0; j < n_tuples; ++j)
+      for (int i = 0; i < n; ++i)
+        if (tuples[j * n + i] == CT_STAR) dom_only[i] = 1;
+  }
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
   if (cfg.device < 0 || cfg.device >= ndev) return fail(CT_EINVAL, "device %d not present (%d devices)", cfg.device, ndev);
 
   // ---------------- geometry
   tb->device = cfg.device;
+  tb->kind = kind;
   tb->n = n;
   tb->R = (int)R;
   tb->t = n_tuples;
@@ -615,7 +734,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   tb->use_res = cfg.use_residues ? 1 : 0;
   tb->use_index = cfg.use_index ? 1 : 0;
   tb->use_graph = cfg.use_graph ? 1 : 0;
-  tb->use_fused = cfg.use_fused ? 1 : 0;
+  tb->use_fused = (cfg.use_fused && kind != CT_TABLE_NEGATIVE) ? 1 : 0;   // negative: ct_neg.cuh's kernels
   if (const char *ev = getenv("CT_FUSED_COOP")) tb->coop = atoi(ev) ? 1 : 0;   // experiment knob
   if (const char *ev = getenv("CT_FUSED_GRID")) tb->fused_grid_override = atoi(ev);
   tb->n_shards = cfg.n_shards;
@@ -672,6 +791,13 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
     tb->fused_occ = std::max(occ, 1);
   }
   tb->scan_occ = std::max(1, tb->scan_occ);
+  if (kind == CT_TABLE_NEGATIVE) {
+    CUDA_TRY(cudaFuncSetAttribute(k_neg_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(n, 1) * 8));
+    CUDA_TRY(cudaFuncSetAttribute(k_neg_finalize, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)std::max<size_t>(finalize_smem_bytes(n, tb->Wd), 1)));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb->neg_occ, k_neg_count, kNegTPB, 0));
+    tb->neg_occ = std::max(1, tb->neg_occ);
+  }
 
   // ---------------- NCCL (tuple-range sharding)
   if (cfg.nccl_unique_id) {
@@ -693,6 +819,8 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   meta.insert(meta.end(), rowVar.begin(), rowVar.end());             // [.., +R)
   meta.insert(meta.end(), tb->lo.begin(), tb->lo.end());
   meta.insert(meta.end(), tb->d.begin(), tb->d.end());
+  const size_t dom_only_at = meta.size();
+  meta.insert(meta.end(), dom_only.begin(), dom_only.end());
   tb->meta_bytes = meta.size() * 4;
   tb->meta = tb->dalloc(tb->meta_bytes);
   if (!tb->meta) return fail(CT_ENOMEM, "device allocation of table metadata failed");
@@ -701,6 +829,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   const int32_t *d_rowBase = m, *d_domOff = m + n + 1, *d_wordVar = m + 2 * n + 2;
   const int32_t *d_rowVar = d_wordVar + std::max(tb->Wd, 1);
   const int32_t *d_lo = d_rowVar + std::max(tb->R, 1), *d_d = d_lo + n;
+  const bool any_star = std::find(dom_only.begin(), dom_only.end(), 1) != dom_only.end();
 
   tb->S_bytes = (size_t)tb->R * (size_t)tb->Wp * 8;
   tb->S = (uint64_t *)tb->dalloc(tb->S_bytes);
@@ -720,6 +849,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   dv.W2 = (int32_t)((tb->W + 1) / 2);
   dv.Wp = tb->Wp;
   dv.policy = tb->policy;
+  dv.domOnly = any_star ? m + dom_only_at : nullptr;
   dv.use_res = tb->use_res;
   dv.use_index = tb->use_index;
   dv.ntiles_max = (int32_t)((dv.W2 + kUpdTPB - 1) / kUpdTPB);
@@ -816,7 +946,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
       const int64_t blocks = (tb->t_local + threads - 1) / threads;
       k_build<<<(unsigned)blocks, threads, 0, tb->stream>>>((const int32_t *)d_tup, tb->t_local, n, d_lo, d_d,
                                                             d_rowBase, tb->S, tb->Wp, (uint32_t *)root->h.T,
-                                                            2 * tb->Wp);
+                                                            2 * tb->Wp, kind == CT_TABLE_SHORT ? 1 : 0);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(tb->stream);   // tuples freed below
@@ -826,6 +956,7 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   Ctl c0{};
   c0.L = tb->dev.W2;
   c0.identity = 1;
+  c0.nvalid = (unsigned long long)tb->t_local;   // negative tables: bound on the root's valid forbidden tuples
   CUDA_TRY(cudaMemcpyAsync(root->h.ctl, &c0, sizeof c0, cudaMemcpyHostToDevice, tb->stream));
   if (tb->Wd)
     CUDA_TRY(cudaMemcpyAsync(root->h.dom, tb->full_dom.data(), (size_t)tb->Wd * 8, cudaMemcpyHostToDevice,
@@ -851,17 +982,18 @@ static ct_status create_impl(int32_t n, const int32_t *scope, const int32_t *dom
   return status == CT_OK ? CT_OK : CT_FAIL;
 }
 
-ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo, const int32_t *dom_size,
-                    const uint64_t *init_dom, int64_t n_tuples, const int32_t *tuples, const ct_config *cfg,
-                    ct_table **out_table, ct_state **out_root, uint64_t *out_dom) {
+ct_status ct_create_table(int32_t kind, int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
+                          const int32_t *dom_size, const uint64_t *init_dom, int64_t n_tuples,
+                          const int32_t *tuples, const ct_config *cfg, ct_table **out_table, ct_state **out_root,
+                          uint64_t *out_dom) {
   if (out_table) *out_table = nullptr;
   if (out_root) *out_root = nullptr;
   ct_table *tb = new (std::nothrow) ct_table();
   if (!tb) return fail(CT_ENOMEM, "host allocation failed");
   ct_state *root = nullptr;
   ct_table *tab = nullptr;
-  ct_status s = create_impl(n_vars, scope, dom_lo, dom_size, init_dom, n_tuples, tuples, cfg, &tab, &root,
-                            out_dom, tb);
+  ct_status s = create_impl(kind, n_vars, scope, dom_lo, dom_size, init_dom, n_tuples, tuples, cfg, &tab,
+                            &root, out_dom, tb);
   if (s < 0) {
     if (root) free_state_mem(root);
     free_table(tb);
@@ -870,6 +1002,13 @@ ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo,
   *out_table = tab;
   *out_root = root;
   return s;
+}
+
+ct_status ct_create(int32_t n_vars, const int32_t *scope, const int32_t *dom_lo, const int32_t *dom_size,
+                    const uint64_t *init_dom, int64_t n_tuples, const int32_t *tuples, const ct_config *cfg,
+                    ct_table **out_table, ct_state **out_root, uint64_t *out_dom) {
+  return ct_create_table(CT_TABLE_POSITIVE, n_vars, scope, dom_lo, dom_size, init_dom, n_tuples, tuples, cfg,
+                         out_table, out_root, out_dom);
 }
 
 ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
@@ -886,8 +1025,10 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->row_stride_words = t->Wp;
   o->device_bytes = (int64_t)(t->S_bytes + t->meta_bytes);
   o->state_bytes = (int64_t)t->lay.total;
-  o->kernel_path = t->use_wide ? 4 : t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
-  o->grid = t->use_wide ? 1 : t->use_small ? 1 : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
+  o->kernel_path = t->kind == CT_TABLE_NEGATIVE ? 5 : t->use_wide ? 4 : t->use_small ? 3 : t->use_fast ? 2
+                  : t->use_fused ? 1 : 0;
+  o->grid = t->kind == CT_TABLE_NEGATIVE ? t->sm_count * t->neg_occ : t->use_wide ? 1 : t->use_small ? 1
+          : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   o->batch_tile = t->bt_tw;
   return CT_OK;
 }
@@ -970,6 +1111,7 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
 
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  if (s->tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "negative tables have no shard-local phase");
   if (s->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   DeviceGuard g(s->tb->device);
   return enqueue_single(s->tb, s, removed, 0, nullptr, nullptr, nullptr, 0, true);
@@ -984,6 +1126,7 @@ ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes) {
 
 ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  if (s->tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "negative tables have no shard-local phase");
   DeviceGuard g(s->tb->device);
   CT_TRY(enqueue_finalize(s->tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream));
   s->pending = false;
@@ -1059,6 +1202,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   if (init->tb != tb) return fail(CT_ESTATE, "init state belongs to another table");
   if (n_states < 1 || n_states > 65535) return fail(CT_EINVAL, "n_states must be in [1, 65535]");
   if (tb->n_shards > 1) return fail(CT_EINVAL, "batches of sharded tables are not supported");
+  if (tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "batches of negative tables are not supported");
   DeviceGuard g(tb->device);
   ct_batch *b = new (std::nothrow) ct_batch();
   if (!b) return fail(CT_ENOMEM, "host allocation failed");

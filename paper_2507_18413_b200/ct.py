@@ -24,6 +24,9 @@ LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(_PKG, "libct_b200.so") 
 CT_OK, CT_FAIL, CT_EINVAL, CT_ENOMEM, CT_ECUDA, CT_ENCCL, CT_ESTATE = 0, 1, -1, -2, -3, -4, -5
 CT_PENDING = 2   # ct_create of a caller-combined shard: combine the root's flags, then apply
 CT_POLICY_AUTO, CT_POLICY_DOM, CT_POLICY_DELTA = 0, 1, 2
+CT_TABLE_POSITIVE, CT_TABLE_SHORT, CT_TABLE_NEGATIVE = 0, 1, 2   # f4 (include/ct.h)
+TABLE_KINDS = {"positive": CT_TABLE_POSITIVE, "short": CT_TABLE_SHORT, "negative": CT_TABLE_NEGATIVE}
+CT_STAR = -2147483648   # short-table wildcard cell (INT32_MIN)
 STATUS_NAMES = {0: "OK", 1: "FAIL", 2: "PENDING", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE"}
 
 
@@ -60,7 +63,7 @@ class ct_table_info(ctypes.Structure):
                 ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32),
                 ("batch_tile", ctypes.c_int32)]
 
-KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small", 4: "k_wide"}
+KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small", 4: "k_wide", 5: "negative"}
 
 
 class ct_stats(ctypes.Structure):
@@ -101,6 +104,9 @@ I32, I64 = ctypes.c_int32, ctypes.c_int64
 SIGNATURES = {
     "ct_config_init": (None, [P]),
     "ct_create": (I32, [I32, P, P, P, P, I64, P, P, P, P, P]),
+    "ct_create_table": (I32, [I32, I32, P, P, P, P, I64, P, P, P, P, P]),
+    "ct_debug_diag_attach": (I32, [I32]),
+    "ct_debug_diag_read": (I64, [P, I64]),
     "ct_table_info_get": (I32, [P, P]),
     "ct_dom_words": (I32, [P]),
     "ct_dom_word_offset": (I32, [P, I32]),
@@ -259,8 +265,9 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
 
 
 # ---------------------------------------------------------------- C names
-def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None):
-    """Returns (status, table, root, root_dom).  root_dom: uint64[Wd] or None on FAIL."""
+def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None, kind: int = CT_TABLE_POSITIVE):
+    """Returns (status, table, root, root_dom).  root_dom: uint64[Wd] or None on FAIL.
+    kind != CT_TABLE_POSITIVE calls ct_create_table (f4: short / negative tables)."""
     lo = np.ascontiguousarray(lo, dtype=np.int32)
     d = np.ascontiguousarray(d, dtype=np.int32)
     tuples = np.ascontiguousarray(tuples, dtype=np.int32)
@@ -279,9 +286,9 @@ def ct_create(lo, d, tuples, init_dom=None, scope=None, cfg=None):
     sc = None if scope is None else np.ascontiguousarray(scope, dtype=np.int32)
     idom = None if init_dom is None else np.ascontiguousarray(init_dom, dtype=np.uint64)
     tab, root = ctypes.c_void_p(), ctypes.c_void_p()
-    st = lib().ct_create(n, _np_ptr(sc), _np_ptr(lo), _np_ptr(d), _np_ptr(idom), t,
-                         _np_ptr(tuples) if t else None, ctypes.byref(cfg) if cfg is not None else None,
-                         ctypes.byref(tab), ctypes.byref(root), _np_ptr(out_dom))
+    args = (n, _np_ptr(sc), _np_ptr(lo), _np_ptr(d), _np_ptr(idom), t, _np_ptr(tuples) if t else None,
+            ctypes.byref(cfg) if cfg is not None else None, ctypes.byref(tab), ctypes.byref(root), _np_ptr(out_dom))
+    st = lib().ct_create(*args) if kind == CT_TABLE_POSITIVE else lib().ct_create_table(int(kind), *args)
     _check(st)
     return st, tab, root, (out_dom[:wd] if st == CT_OK else None)
 
@@ -593,3 +600,37 @@ def ct_host_state_destroy(state) -> None:
 
 def ct_host_table_destroy(table) -> None:
     lib().ct_host_table_destroy(table)
+
+
+def ct_debug_diag_attach(device: int = 0) -> None:
+    """Spin-watchdog diagnostics buffer for `device` (include/ct.h)."""
+    _check(lib().ct_debug_diag_attach(int(device)), allow_fail=False)
+
+
+def ct_debug_diag_read(n_words: int = 64 + 128 + 2 * 4096) -> np.ndarray:
+    out = np.zeros(n_words, np.uint64)
+    n = int(lib().ct_debug_diag_read(_np_ptr(out), n_words))
+    return out[:n]
+
+
+def ct_debug_diag_summary() -> str:
+    """Human-readable watchdog report ('' if none)."""
+    d = ct_debug_diag_read()
+    if d.size == 0 or int(d[0]) != 0xD1A6D1A6:
+        return ""
+    lines = []
+    for k in range(16):
+        r = d[64 + 8 * k: 64 + 8 * k + 8]
+        if int(r[0]) == 0:
+            continue
+        lines.append(f"report {k}: kind={int(r[0])} cta={int(r[1])} a={int(r[2])} b={int(r[3])} c={int(r[4])} "
+                     f"loc={int(r[5]):#x} bseq={int(r[6])} grid={int(r[7])}")
+    G = int(d[64 + 7])
+    loc = d[64 + 128: 64 + 128 + G]
+    bseq = d[64 + 128 + 4096: 64 + 128 + 4096 + G]
+    from collections import Counter
+    lines.append("loc histogram: " + ", ".join(f"{int(k):#x} x{v}" for k, v in Counter(loc.tolist()).items()))
+    lines.append("bseq histogram: " + ", ".join(f"{int(k)} x{v}" for k, v in Counter(bseq.tolist()).items()))
+    odd = [i for i in range(G) if bseq[i] != np.bincount(bseq.astype(np.int64)).argmax()]
+    lines.append(f"CTAs off the majority barrier count: {odd[:32]}")
+    return "\n".join(lines)

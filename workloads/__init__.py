@@ -7,6 +7,7 @@ both sides of a parity check may import ("input recipe").
 from .rng import Rng, splitmix64  # noqa: F401
 from .tables import (  # noqa: F401
     table1, random_table, banded_table, knapsack_table, LIN_PRESETS, Problem,
+    short_table, negative_table, STAR,
 )
 from .layout import (  # noqa: F401
     member_to_bitmap, bitmap_to_member, dom_word_offsets, full_member,

@@ -131,3 +131,33 @@ def knapsack_table(n: int, max_dom: int, t: int, seed: int, kmax: int = 8, name:
             rem -= c * int(w[i])
     return Problem(name or f"knapsack_n{n}_d{max_dom}_t{t}_s{seed}", np.zeros(n, np.int32),
                    (b + 1).astype(np.int32), tuples, seed, meta=dict(weights=w, capacity=cap))
+
+
+STAR = -2147483648   # short-table wildcard cell (include/ct.h CT_STAR = INT32_MIN)
+
+
+def short_table(n: int, d, t: int, seed: int, p_star: float = 0.1, lo=0, name: str | None = None) -> Problem:
+    """f4 short table (PAPER.md L66-68 footnote): random_table(n, d, t, seed, lo),
+    then each cell independently becomes STAR with probability p_star (a second
+    stream, Rng(seed + 1), one draw per cell in row-major order:
+    u < p_star * 2^20 of uniform [0, 2^20))."""
+    p = random_table(n, d, t, seed, lo=lo)
+    rng = Rng(seed + 1)
+    tuples = p.tuples
+    chunk = max(1, (1 << 22) // n)
+    thr = int(p_star * (1 << 20))
+    for j0 in range(0, p.t, chunk):
+        j1 = min(p.t, j0 + chunk)
+        u = rng.uniform((j1 - j0) * n, 1 << 20).reshape(j1 - j0, n)
+        tuples[j0:j1][u < thr] = STAR
+    return Problem(name or f"short_n{n}_t{t}_p{p_star}_s{seed}", p.lo, p.d, tuples, seed,
+                   meta=dict(p_star=p_star))
+
+
+def negative_table(n: int, d, t: int, seed: int, lo=0, name: str | None = None) -> Problem:
+    """f4 negative table: t forbidden assignments drawn i.i.d. over the product of
+    [lo_i, lo_i + d_i) (random_table's stream; duplicates kept -- the library and
+    the oracle merge them).  Dense lists (t comparable to prod d_i) make values
+    lose all their allowed assignments once the domains shrink."""
+    p = random_table(n, d, t, seed, lo=lo)
+    return Problem(name or f"negative_n{n}_t{t}_s{seed}", p.lo, p.d, p.tuples, seed)
