@@ -392,10 +392,22 @@ def nonzero_words(bits):
     return int(np.count_nonzero(bits))
 
 
-def measure_c3(workload, args, dev, world, rank, full=True):
+def nonzero_sectors(bits):
+    """32-byte DRAM sectors (4 currTable words) holding a valid tuple: a scan of a
+    support row over the active words must fetch at least these sectors."""
+    b = np.asarray(bits)
+    pad = (-b.size) % 4
+    if pad:
+        b = np.concatenate([b, np.zeros(pad, b.dtype)])
+    return int(np.count_nonzero(b.reshape(-1, 4).any(axis=1)))
+
+
+def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
     """One C3-family workload (c3bulk or c3b): device-timed steps, per-kernel
     times, kernel-counted and algorithmic bytes; with full=True also the e2e
-    host-buffer runs.  Returns a dict (rank 0's view; times max over ranks)."""
+    host-buffer runs.  use_gather=False forces Alg. 3's support-row scans for
+    the residue misses (ct_config.use_gather).  Returns a dict (rank 0's view;
+    times max over ranks)."""
     import torch
     from paper_2507_18413_b200 import CT_OK, Table
     from paper_2507_18413_b200 import ct as C
@@ -405,7 +417,8 @@ def measure_c3(workload, args, dev, world, rank, full=True):
     p = c3_problem() if workload == "c3bulk" else c3b_problem()
     nid = broadcast_nccl_id() if world > 1 else None
     t0 = time.perf_counter()
-    tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=world, shard_rank=rank, nccl_unique_id=nid)
+    tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=world, shard_rank=rank, nccl_unique_id=nid,
+                use_gather=use_gather)
     build_s = time.perf_counter() - t0
     assert tab.root_status == CT_OK
     root_m = bitmap_to_member(tab.root_dom, p.d)
@@ -448,12 +461,21 @@ def measure_c3(workload, args, dev, world, rank, full=True):
                 ko = int(dout[rb[i]:rb[i + 1]].sum())
                 kept += ko
                 removed += di - ko
-        L_out = nonzero_words(work.read_table())
+        tbits = work.read_table()
+        L_out = nonzero_words(tbits)
+        sec_out = nonzero_sectors(tbits)
+        # the gather filter reads the cells of every valid tuple once (one
+        # 32-byte sector each, the cells of a sparse valid set share none)
+        n_valid = int(np.unpackbits(tbits.view(np.uint8)).sum())
         per_pat.append(dict(L_in=s.words_in, L_out=s.words_out, rows=s.n_update_rows,
                             loads=s.update_support_words, writes=s.update_table_writes,
                             scan=s.filter_support_words, miss=s.n_residue_miss,
+                            gathered=s.filter_gathered_tuples, valid=n_valid,
                             alg=algorithmic_bytes(L_root, L_out, rows, kept, removed),
-                            words_in=L_root, words_out=L_out, removed_values=removed, kept_values=kept))
+                            alg_sector=algorithmic_bytes(L_root, 0, rows, kept, 0) + 32 * sec_out * removed,
+                            alg_gather=algorithmic_bytes(L_root, 0, rows, kept, 0) + 32 * s.filter_gathered_tuples,
+                            words_in=L_root, words_out=L_out, sectors_out=sec_out,
+                            removed_values=removed, kept_values=kept))
     for k in range(args.warmup):
         step(k)
     work.synchronize()
@@ -486,14 +508,18 @@ def measure_c3(workload, args, dev, world, rank, full=True):
 
     dom_kernel = next((k for k in ("fused", "small") if prof.get(k, (0, 0.0))[0]), "update")
     k_n, k_ms = prof[dom_kernel]
-    counted = alg = 0
+    counted = alg = alg_sec = 0
+    gathered = any(c["gathered"] for c in per_pat)
     for k in range(args.steps):
         c = per_pat[k % P]
         b = 8 * c["loads"] + 16 * c["L_in"] + 16 * c["writes"] + 4 * (c["L_in"] + c["L_out"])
         if dom_kernel in ("fused", "small"):
-            b += 8 * c["scan"]
+            b += 8 * c["scan"] + 32 * c["gathered"]
         counted += b
-        alg += c["alg"]
+        # bytes of the method the call ran: Alg. 3's scans (word model), or the
+        # gather filter's cells when it resolved the misses
+        alg += c["alg_gather"] if c["gathered"] else c["alg"]
+        alg_sec += c["alg_gather"] if c["gathered"] else c["alg_sector"]
     kernel_name = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_update") if dom_kernel in ("fused", "small") \
         else "ctk::k_update"
     k_ms_per_launch = k_ms / max(k_n, 1)
@@ -501,7 +527,8 @@ def measure_c3(workload, args, dev, world, rank, full=True):
     peak, peak_src = peaks()
     alg_pl = alg / max(k_n, 1)
     counted_pl = counted / max(k_n, 1)
-    traffic = ncu_traffic(workload, world, kernel_name)
+    # c3b with the scans forced has its own capture (same kernel, other path)
+    traffic = ncu_traffic(workload if use_gather or workload != "c3b" else "c3b_scan", world, kernel_name)
     step_ms = ms_max / args.steps
     roofline = {"bound": "hbm", "achieved": alg_pl / k_s / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": alg_pl / k_s / 1e9 / peak, "traffic": traffic, "kernel": kernel_name,
@@ -509,8 +536,14 @@ def measure_c3(workload, args, dev, world, rank, full=True):
                 "counted_bytes_per_launch": counted_pl,
                 "counted_frac": counted_pl / k_s / 1e9 / peak,
                 "dram_frac": (traffic / k_s / 1e9 / peak) if traffic else None,
-                "bytes_model": "SURVEY §8(d): 8 L_in (sum r_x + 2) + 8 K + 8 L_out Rm at 64-bit-word granularity "
-                               "(L = non-zero currTable words of the call's input / output)",
+                "sector_floor_bytes_per_launch": alg_sec / max(k_n, 1),
+                "sector_floor_frac": alg_sec / max(k_n, 1) / k_s / 1e9 / peak,
+                "filter_method": "gather (valid tuples' cells)" if gathered else "Alg. 3 support-row scans",
+                "bytes_model": ("SURVEY §8(d) update bytes 8 L_in (sum r_x + 2) + 8 K, plus the gather filter's "
+                                "32 B (one sector of cells) per valid tuple it read") if gathered else
+                               ("SURVEY §8(d): 8 L_in (sum r_x + 2) + 8 K + 8 L_out Rm at 64-bit-word granularity "
+                                "(L = non-zero currTable words of the call's input / output); sector_floor: the "
+                                "scans at 32-byte-sector granularity (32 x sectors holding a valid tuple x Rm)"),
                 "peak_source": peak_src}
     out = dict(p=p, tab=tab, work=work, root_m=root_m, pats=pats, rem_host=rem_host, value=value,
                ms_per_step=step_ms, build_s=build_s, roofline=roofline, clocks=clk, per_pat=per_pat,
@@ -656,6 +689,13 @@ def run_ours(args):
                 "roofline": f["roofline"], "kernel_share_of_step": f["kernel_share"],
                 "kernel_ms_per_launch": f["kernel_ms"], "workload_counters": f["per_pat"][0],
                 "phase_ns": f["phase_ns"], "clocks": f["clocks"]}
+        f["tab"].close()
+        # the same calls with Alg. 3's full support-row scans (use_gather = 0):
+        # the HBM-bound filterDomains the paper's kernels run
+        f = measure_c3("c3b", args, dev, world, rank, full=False, use_gather=False)
+        filt["alg3_scan"] = {"value": f["value"], "unit": "propagations/s", "ms_per_step": f["ms_per_step"],
+                             "roofline": f["roofline"], "kernel_share_of_step": f["kernel_share"],
+                             "workload_counters": f["per_pat"][0]}
         f["tab"].close()
     if world == 1 and args.workload == "c3bulk" and not args.skip_sharded:
         shov = sharded_overhead(m, args, dev)

@@ -100,6 +100,11 @@ typedef struct ct_config {
                               /*    tables of <= 8192 16-byte blocks, else a cooperative */
                               /*    persistent grid with software barriers; 0: one      */
                               /*    kernel per phase                                     */
+  int32_t use_gather;         /* 1: the k_fast filter may resolve its residue misses by  */
+                              /*    gathering the valid tuples' values (device copy of   */
+                              /*    the tuples as 8/16-bit value offsets, t x n cells)   */
+                              /*    instead of scanning supports rows (Alg. 3), when that */
+                              /*    reads fewer bytes; 0: always scan.  Same results.    */
 } ct_config;
 
 /* Fill *cfg with defaults: device 0, NULL stream, default allocator, 1 shard,
@@ -194,6 +199,8 @@ typedef struct ct_table_info {
   int32_t batch_tile;           /* ct_propagate_many: 16-byte blocks per shared-memory    */
                                 /* support tile of the tile-major update (32, 16 or 8), or */
                                 /* 0 = one pass per state (R too large for the tile)      */
+  int32_t gather_cell_bits;     /* bits per cell of the gather filter's tuple copy, 0 = off */
+  int32_t kind;                 /* CT_TABLE_*                                             */
 } ct_table_info;
 
 ct_status ct_table_info_get(const ct_table *t, ct_table_info *out);
@@ -371,6 +378,8 @@ typedef struct ct_stats {
                             /* update, probe, scan, finalize, 0, 0; k_fast: ingest,        */
                             /* update (+ barrier), probe, barrier, scan, completion wait,   */
                             /* finalize.  Not written by the per-phase kernels.            */
+  int64_t filter_gathered_tuples; /* k_fast gather filter: valid tuples whose values it read  */
+                                  /* (0 when the misses were scanned, ct_config.use_gather)  */
 } ct_stats;
 ct_status ct_state_stats(const ct_state *s, ct_stats *out);
 /* The same counters for every state of a batch (last ct_propagate_many call):
@@ -459,6 +468,9 @@ ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64
  * it works while a kernel spins); word 0 == 0xD1A6D1A6 once a report is
  * complete.  Returns the words copied. */
 ct_status ct_debug_diag_attach(int32_t device);
+/* The watchdog's limit for `device` (default 4 s; e.g. raised under
+ * compute-sanitizer, which slows every CTA). */
+ct_status ct_debug_spin_limit(int32_t device, double seconds);
 int64_t ct_debug_diag_read(uint64_t *out, int64_t n_words);
 
 /* NCCL bootstrap helper: writes a fresh 128-byte ncclUniqueId (rank 0 calls it

@@ -72,22 +72,7 @@ constexpr int kFastChunk = 32 * kScanFastU;            // index entries per scan
 #endif
 constexpr int kScanGroup = CT_SCAN_GROUP;              // probe misses per scan unit (<= 32)
 constexpr int kSelfRounds = (32 + kProbeUnroll - 1) / kProbeUnroll;   // probe rounds before a miss is queued (~1024 entries)
-#ifdef CT_FAST_STOP
-constexpr int kFastStop = CT_FAST_STOP;                // experiment builds only
-#else
-constexpr int kFastStop = 0;
-#endif
 
-__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 // Static shared state of one k_fast CTA (NW warps; k_wide uses the same ingest
 // with 32 warps).
@@ -95,6 +80,7 @@ template <int NW>
 struct FastShT {
   int dead, fail, noop, go, ngroups, nrows, nitems;
   int L, ident, par, Lout, nscan, last, below, anymiss;
+  uint32_t nvalid;               // valid tuples of this CTA's blocks after the update
   int red[NW];                   // block-reduction scratch
   uint32_t woff[NW];
   uint64_t scan[NW];
@@ -270,6 +256,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     fs.fail = 0;
     fs.ngroups = 0;
     fs.anymiss = 0;
+    fs.nvalid = 0;
     fs.L = c->L;
     fs.ident = c->identity;
     fs.par = c->parity;
@@ -423,6 +410,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
       c->upd_loads = 0;
       c->upd_writes = 0;
       c->scan_loads = 0;
+      c->gathered = 0;
     }
   }
   __syncthreads();
@@ -431,8 +419,8 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
 // ------------------------------------------------------------------ a3: update of one index entry
 // Alg. 2 for index entry k (one 16-byte block per thread).  The block dies
 // early (Alg. 2) once no valid tuple is left in it (checked between
-// batches).  Returns whether the block keeps a valid tuple.
-__device__ __forceinline__ bool fast_update_entry(const TableDev &tb, const StateDev &st, const FastSh &fs,
+// batches).  Returns the number of valid tuples the block keeps.
+__device__ __forceinline__ uint32_t fast_update_entry(const TableDev &tb, const StateDev &st, const FastSh &fs,
                                                   const uint32_t *__restrict__ ulist, int k, uint32_t &n_loads,
                                                   uint32_t &n_writes) {
   const int nrows = fs.nrows;
@@ -476,7 +464,7 @@ __device__ __forceinline__ bool fast_update_entry(const TableDev &tb, const Stat
     T2[pid] = nt;
     ++n_writes;
   }
-  return (nt.x | nt.y) != 0;
+  return (uint32_t)(__popcll(nt.x) + __popcll(nt.y));
 }
 
 // ------------------------------------------------------------------ a4: index entries of one CTA's range
@@ -510,6 +498,67 @@ __device__ __forceinline__ void fast_compact_range(const TableDev &tb, const Sta
     }
     if (keep) idx_out[below + off + __popc(bal & lanemask_lt())] = pid;
     below += (int)all;
+  }
+}
+
+// ------------------------------------------------------------------ a6b': filter by gathering the valid tuples
+// Alg. 3 asks, per unresolved (x,a), whether currTable & supports[x,a] != 0,
+// i.e. (L189-193) whether some VALID tuple holds value a at x.  The same answer
+// for every value at once: walk the valid tuples and mark the values they hold.
+// When the valid tuples are few against the scans (|V| sectors of cells vs
+// misses x L_out x 16 bytes of support words -- the banded C3b call reads
+// ~3 MB instead of ~0.8 GB) every CTA walks the valid tuples of its own update
+// range (their blocks were written by the same threads), reads their cells
+// (value offsets, tb.cells) and marks (x, tau[x]) in a shared-memory bitmap in
+// the domain layout; each queued miss then reads its bit.  A value is marked
+// iff a valid tuple holds it, so the verdicts are Alg. 3's; a marked value's
+// residue becomes a block holding such a tuple.
+__device__ void fast_gather_range(const TableDev &tb, const StateDev &st, const FastSh &fs, const FastPtrs &p,
+                                  int k_lo, int k_hi, uint32_t &n_tuples) {
+  const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
+  uint64_t *mark = p.bw;                                   // [Wd] (free after the ingest)
+  int32_t *rres = reinterpret_cast<int32_t *>(p.ulist);    // [R]  (free after the update)
+  for (int k = tid; k < Wd; k += kFastTPB) mark[k] = 0;
+  __syncthreads();
+  const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
+  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  const int cw = tb.cell_words, bits = tb.cell_bits, per = 32 / bits;
+  const uint32_t cmask = (1u << bits) - 1u;
+  for (int k = k_lo + tid; k < k_hi; k += kFastTPB) {
+    const int pid = fs.ident ? k : idx_in[k];
+    const ulonglong2 t = T2[pid];   // written by this thread's own update
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint64_t m = h ? t.y : t.x;
+      while (m) {
+        const int b = __ffsll(m) - 1;
+        m &= m - 1;
+        const uint32_t *__restrict__ cr = tb.cells + ((int64_t)(2 * pid + h) * 64 + b) * cw;
+        ++n_tuples;
+        for (int q = 0; q < cw; ++q) {
+          const uint32_t wv = __ldg(cr + q);
+          for (int e = 0; e < per; ++e) {
+            const int i = q * per + e;
+            if (i >= n) break;
+            const int v = (int)((wv >> (e * bits)) & cmask);
+            uint64_t *mw = mark + p.dof[i] + (v >> 6);
+            if (!((*(volatile uint64_t *)mw >> (v & 63)) & 1ull)) {   // most values repeat: skip the atomic
+              smem_set_bit(mw, v & 63);
+              rres[p.rb[i] + v] = pid;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int m = tid; m < fs.nscan; m += kFastTPB) {
+    const int row = __ldcg(st.scanlist + m);
+    const int x = row_var(p.rb, n, row), a = row - p.rb[x];
+    if ((mark[p.dof[x] + (a >> 6)] >> (a & 63)) & 1ull) {
+      st.sup[row] = 1;
+      st.res[row] = rres[row];
+    }
   }
 }
 
@@ -602,7 +651,7 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
         const int x = row_var(p.rb, tb.n, r);
         const int a = r - p.rb[x];
         const int w = p.dof[x] + (a >> 6);
-        atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + w), ~(1ull << (a & 63)));
+        smem_clear_bit(s_nd + w, a & 63);
       }
     }
     __syncthreads();
@@ -630,22 +679,6 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
   }
 }
 
-#ifdef CT_PROBE_DEBUG
-// experiment builds only: per-item probe timing (globaltimer and SM id)
-__device__ unsigned long long g_probe_dbg[8192][4];
-#endif
-#ifdef CT_FAST_TRACE
-// experiment builds only: per-CTA phase timestamps of the last k_fast call
-__device__ unsigned long long g_fast_trace[4096][10];
-#define FAST_TRACE(i) \
-  do {                                                                        \
-    if (threadIdx.x == 0 && blockIdx.x < 4096) g_fast_trace[blockIdx.x][i] = globaltimer(); \
-  } while (0)
-#else
-#define FAST_TRACE(i) \
-  do {                \
-  } while (0)
-#endif
 
 // ------------------------------------------------------------------ k_fast
 // Cooperative launch (all CTAs co-resident), kFastTPB threads, dynamic smem
@@ -670,9 +703,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
   const bool t0 = blockIdx.x == 0 && tid == 0;
   // phase timestamps of block 0 go straight to tph[] (no registers held)
   if (t0) c->tph[0] = globaltimer();
-  FAST_TRACE(0);
   cta_ingest(tb, st, removed, root_mode, p, fs, blockIdx.x == 0);
-  FAST_TRACE(1);
   if (t0) {
     const unsigned long long t = globaltimer();
     for (int i = 1; i < 6; ++i) c->tph[i] = t;
@@ -690,15 +721,19 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     uint32_t n_loads = 0, n_writes = 0, f_loads = 0;
     {
       int kept = 0;
+      uint32_t nv = 0;   // valid tuples of this thread's blocks (the gather filter's cost model)
       for (int base = k_lo; base < k_hi; base += kFastTPB) {
         const int k = base + tid;
-        const bool keep = k < k_hi && fast_update_entry(tb, st, fs, p.ulist, k, n_loads, n_writes);
-        kept += __syncthreads_count(keep);
+        const uint32_t cnt = k < k_hi ? fast_update_entry(tb, st, fs, p.ulist, k, n_loads, n_writes) : 0u;
+        nv += cnt;
+        kept += __syncthreads_count(cnt != 0);
       }
       if (tid == 0) tcnt[blockIdx.x] = (uint32_t)kept;
+      if (tb.cells) {
+        nv = warp_sum_u32(nv);
+        if (lane == 0) atomicAdd(&fs.nvalid, nv);
+      }
     }
-    FAST_TRACE(2);
-#ifndef CT_FAST_NOCOUNT
     // update work counters now, while CTAs still finish at different times,
     // reduced per CTA first: when every CTA finishes its (short) update at
     // once, one same-address atomic per warp serialised into ~3.5 us before
@@ -719,24 +754,10 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
       __syncthreads();   // fs.red / fs.woff are free again
     }
-#endif
 
     const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-    if (kFastStop > 0) {
-      // experiment builds only (tools/gpu_exp.sh): 1 = update only, 2 = update +
-      // barrier, -3 = ... + compaction, -4 = ... + probe; the call then reports a
-      // made-up success
-      if (kFastStop == 2) fast_grid_barrier(st.bar);
-      if (t0) c->tph[2] = globaltimer();
-      if (tid == 0) {
-        fs.Lout = fs.L;
-        fs.noop = 1;   // finalize leaves the state as it was
-      }
-      __syncthreads();
-    } else {
     fast_grid_barrier(st.bar);
     if (t0) c->tph[2] = globaltimer();
-    FAST_TRACE(3);
 
     // ---- compaction (a4), part A: L_out and this CTA's prefix from the
     // per-CTA counts (the index entries themselves are written later, off the
@@ -756,8 +777,10 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         if (blockIdx.x == 0) c->L_out = tot;
       }
     }
+    if (tb.cells && tid == 0) {   // this CTA's valid tuples -> the grid's (read after the probe barrier)
+      tcnt[G + blockIdx.x] = (uint32_t)fs.nvalid;
+    }
     __syncthreads();
-    FAST_TRACE(4);
 
     // ---- probe (a6a): residue + up to kSelfRounds rounds over the pre-update index.
     // Item i goes to CTA i % G; when there are few items per CTA, wpi warps of
@@ -770,7 +793,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     const int Ls = compact ? Lout : tb.W2;
     const bool may_miss = fs.L > kSelfRounds * kFirstScanFast;   // the probe cannot cover the index
     if (t0) st.sup[tb.R] = Lout > 0;
-    if (Lout > 0 && kFastStop != -3) {
+    if (Lout > 0) {
       const int per_cta = (fs.nitems - (int)blockIdx.x + G - 1) / G;   // items of this CTA
       const int wpi = per_cta <= 1 ? kFastWarps : per_cta <= 2 ? kFastWarps / 2 : 1;
       const int slots = kFastWarps / wpi, slot = warp / wpi, q = warp % wpi;
@@ -813,21 +836,17 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
     }
     if (t0) c->tph[3] = c->tph[4] = globaltimer();
-    FAST_TRACE(5);
-#ifndef CT_FAST_NOCOUNT
     cta_count(lane == 0 ? f_loads : 0u, &c->scan_loads, fs);   // probe rounds
-#endif
     f_loads = 0;
     // ---- scan (a6b): misses x chunks of the compacted index, from entry 0.
     // The barrier's last arrival knows every probe is done: with no miss it
     // releases the others with mode 1 (they write their index entries and
     // exit) and finalizes at once, then writes its own entries.
-    if (Lout > 0 && may_miss && kFastStop > -3) {
+    if (Lout > 0 && may_miss) {
       int leader = 0;
       const int mode = fast_grid_barrier_mode(st.bar, [](uint32_t misses) { return misses == 0 ? 1 : 0; }, leader,
                                               &fs.nscan, &fs.anymiss);
       if (t0) c->tph[4] = globaltimer();
-      FAST_TRACE(6);
       if (mode == 1) {
         if (t0) c->tph[5] = globaltimer();   // no scan phase
         if (tid == 0) fs.last = leader;
@@ -841,7 +860,33 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         leader_k_hi = k_hi;
         goto finalize;
       }
-      // misses: the whole new index first (the scans read it)
+      // misses: scan them (Alg. 3 over the new index) or gather the valid
+      // tuples' values (fast_gather_range) -- whichever reads fewer bytes.  Both
+      // inputs are final after the probe barrier, so every CTA decides alike.
+      if (tb.cells) {
+        if (tid == 0) fs.nscan = __ldcg(&c->nscan);
+        unsigned long long v = 0;
+        for (int j = tid; j < G; j += kFastTPB) v += __ldcg(tcnt + G + j);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        __syncthreads();
+        if (lane == 0) fs.scan[warp] = v;
+        __syncthreads();
+        v = 0;
+#pragma unroll
+        for (int w = 0; w < kFastWarps; ++w) v += fs.scan[w];
+        const unsigned long long scan_bytes = (unsigned long long)fs.nscan * (unsigned long long)Ls * 16ull;
+        const unsigned long long gather_bytes = v * 32ull + (unsigned long long)Ls * 16ull;
+        if (gather_bytes < scan_bytes) {
+          if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
+          uint32_t ng = 0;
+          fast_gather_range(tb, st, fs, p, k_lo, k_hi, ng);
+          cta_count(ng, &c->gathered, fs);
+          if (t0) c->tph[5] = globaltimer();
+          goto completion;
+        }
+      }
+      // the whole new index first (the scans read it)
       if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
       fast_grid_barrier(st.bar);
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
@@ -921,21 +966,16 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         }
       }
     }
-    if (!(Lout > 0 && may_miss && kFastStop > -3) && tb.use_index && kFastStop == 0)
+    if (!(Lout > 0 && may_miss) && tb.use_index)
       fast_compact_range(tb, st, fs, k_lo, k_hi);   // no scan phase: write the index now
     if (t0) c->tph[5] = globaltimer();
-    FAST_TRACE(7);
-    if (kFastStop < 0 && tid == 0) fs.noop = 1;   // experiment: leave the state as it was
-    }   // !kFastStop
     // scan work counter, one atomic per CTA
-#ifndef CT_FAST_NOCOUNT
     cta_count(lane == 0 ? f_loads : 0u, &c->scan_loads, fs);
-#endif
   }
 
   // ---- completion: the last CTA to get here finalizes
+completion:
   __syncthreads();
-  FAST_TRACE(8);
   if (tid == 0) {
     __threadfence();
     fs.last = atomicAdd(&c->cta_done, 1) == G - 1;

@@ -77,6 +77,10 @@ struct TableDev {
   int32_t ntiles_max;       // ceil(W2 / kUpdTPB)
   const int32_t *gword;     // [Wd] model tables only: global domain word of each domain word
   const int32_t *gshared;   // [Wd] model tables only: 1 if another table also constrains the word's variable
+  const uint32_t *cells;    // [t_local][cell_words] or nullptr: tuple j's value offsets v - lo_i, cell_bits
+                            // each, packed LSB-first (the gather filter of k_fast, ct_fast.cuh)
+  int32_t cell_bits;        // 8 or 16
+  int32_t cell_words;       // uint32 words per tuple
   const int32_t *domOnly;   // [n] or nullptr: 1 if x's column has a star cell (short tables, f4), so the
                             // Δ-branch (which drops every tuple whose row has a removed value) is unsound
                             // for x: a star tuple is in every row of x and must survive
@@ -121,6 +125,7 @@ struct Ctl {
   // (persists; copied with the state) and this call's running count
   unsigned long long nvalid;
   unsigned long long nvalid_new;
+  unsigned long long gathered;   // k_fast gather filter: valid tuples whose cells it read (this call)
 };
 static_assert(sizeof(Ctl) <= 256, "Ctl must fit its 256-byte slot");
 
@@ -176,6 +181,16 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
 }
+// One bit of a 64-bit word in SHARED memory, with the native 32-bit atomic on
+// the word's half (a 64-bit shared-memory AND/OR compiles to a CAS loop, which
+// serialises badly when many threads hit the same few words).
+__device__ __forceinline__ void smem_clear_bit(uint64_t *w, int b) {
+  atomicAnd(reinterpret_cast<unsigned int *>(w) + (b >> 5), ~(1u << (b & 31)));
+}
+__device__ __forceinline__ void smem_set_bit(uint64_t *w, int b) {
+  atomicOr(reinterpret_cast<unsigned int *>(w) + (b >> 5), 1u << (b & 31));
+}
+
 __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -189,7 +204,7 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 // diagnostic buffer (ct_debug_diag_attach / _read), the first reporter also
 // copies every CTA's location and barrier count, and the kernel traps -- a lost
 // arrival then surfaces as CT_ECUDA instead of a GPU spinning forever.
-constexpr unsigned long long kSpinLimitNs = 4000000000ull;   // 4 s: phases take us to ms
+__device__ unsigned long long g_spin_limit_ns = 4000000000ull;   // 4 s: phases take us to ms
 constexpr int kDiagCtas = 4096;
 __device__ unsigned long long *g_diag;     // host-mapped [kDiagWords] or nullptr
 __device__ uint32_t g_loc[kDiagCtas];      // per-CTA location marker (phase code)
@@ -241,7 +256,7 @@ __device__ __forceinline__ void spin_check(SpinGuard &g, uint32_t kind, unsigned
     g.t0 = t;
     return;
   }
-  if (t - g.t0 < kSpinLimitNs) return;
+  if (t - g.t0 < g_spin_limit_ns) return;
   spin_report(kind, a, b, c);
   __trap();
 }
@@ -344,6 +359,31 @@ __global__ void k_build(const int32_t *__restrict__ tuples, int64_t t_local, int
   const unsigned bal = __ballot_sync(0xffffffffu, valid);
   const int64_t hw = j >> 5;
   if ((threadIdx.x & 31) == 0 && hw < n_half_words) T32[hw] = bal;
+}
+
+// The gather filter's cells (ct_fast.cuh fast_gather_range): tuple j's value
+// offsets v - lo_i, `bits` bits each, packed LSB-first into `words` uint32 per
+// tuple.  Out-of-range values keep an all-ones cell (such a tuple is never
+// valid, so never gathered).
+__global__ void k_build_cells(const int32_t *__restrict__ tuples, int64_t t_local, int n,
+                              const int32_t *__restrict__ lo, const int32_t *__restrict__ d,
+                              uint32_t *__restrict__ cells, int bits, int words) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= t_local) return;
+  const int per = 32 / bits;
+  const uint32_t cmask = (1u << bits) - 1u;
+  const int32_t *tau = tuples + j * n;
+  for (int q = 0; q < words; ++q) {
+    uint32_t w = 0;
+    for (int e = 0; e < per; ++e) {
+      const int i = q * per + e;
+      if (i >= n) break;
+      const int64_t v = (int64_t)tau[i] - lo[i];
+      const uint32_t c = (v >= 0 && v < d[i]) ? (uint32_t)v : cmask;
+      w |= (c & cmask) << (e * bits);
+    }
+    cells[j * words + q] = w;
+  }
 }
 
 // ------------------------------------------------------------------ a2: ingest (one block)
@@ -1020,7 +1060,7 @@ __device__ int dev_finalize(const TableDev &tb, const StateDev &st, uint64_t *__
         const int a = r - s_rb[x];
         const int w = s_do[x] + (a >> 6);
         const uint64_t bit = 1ull << (a & 63);
-        if (s_nd[w] & bit) atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + w), ~bit);
+        if (s_nd[w] & bit) smem_clear_bit(s_nd + w, a & 63);
       }
     }
     __syncthreads();
@@ -1256,7 +1296,7 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
       const int x = tb.rowVar[r];
       if (!__ldcg(st.sup + r) && s_cs[x] > 1) {   // x in s_sup (Alg. 3 L1), a unsupported
         const int a = r - s_rb[x];
-        atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + s_do[x] + (a >> 6)), ~(1ull << (a & 63)));
+        smem_clear_bit(s_nd + s_do[x] + (a >> 6), a & 63);
       }
     }
     __syncthreads();

@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kIngestTPB) k_neg_plan(TableDev tb, const Stat
 // Grid of kNegTPB-thread CTAs (persistent over work items).
 __global__ void __launch_bounds__(kNegTPB) k_neg_count(TableDev tb, const StateDev *__restrict__ states) {
   __shared__ uint32_t s_cnt[kNegGroupRows];
-  __shared__ unsigned long long s_nv;
+  __shared__ uint32_t s_nv;
   const StateDev st = states[0];
   Ctl *c = st.ctl;
   if (!neg_go(c)) return;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kNegTPB) k_neg_count(TableDev tb, const StateD
     }
     if (group == 0) {
       nv = __reduce_add_sync(0xffffffffu, nv);
-      if (lane == 0 && nv) atomicAdd(&s_nv, (unsigned long long)nv);
+      if (lane == 0 && nv) atomicAdd(&s_nv, nv);
     }
     __syncthreads();   // s_cnt zeroed
     int i = r0;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kNegTPB) k_neg_count(TableDev tb, const StateD
     __syncthreads();   // s_cnt is reused by the next work item
   }
   if (tid == 0) {
-    if (s_nv) atomicAdd(&c->nvalid_new, s_nv);
+    if (s_nv) atomicAdd(&c->nvalid_new, (unsigned long long)s_nv);
     if (loads) atomicAdd(&c->scan_loads, loads);
   }
 }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kFinTPB) k_neg_finalize(TableDev tb, const Sta
       if (__ldcg(st.cnt + r) >= __ldcg(st.prod + x)) {   // every assignment with x = a is forbidden
         const int a = r - tb.rowBase[x];
         const int w = tb.domOff[x] + (a >> 6);
-        atomicAnd(reinterpret_cast<unsigned long long *>(s_nd + w), ~(1ull << (a & 63)));
+        smem_clear_bit(s_nd + w, a & 63);
       }
     }
     __syncthreads();

@@ -103,6 +103,8 @@ struct ct_table {
   size_t meta_bytes = 0;
   uint64_t *S = nullptr;
   size_t S_bytes = 0;
+  uint32_t *cells = nullptr;         // gather filter (k_fast): packed value offsets per local tuple
+  size_t cells_bytes = 0;
   TableDev dev{};
   StateLayout lay{};
   int sm_count = 148;
@@ -199,7 +201,7 @@ static StateLayout make_layout(const ct_table *tb) {
   L.sup = take((size_t)tb->R + 1);
   L.varcnt = take((size_t)tb->n * 8);
   // chained-scan tile statuses (k_fused) / per-CTA survivor counts (k_fast, <= 16 CTAs per SM)
-  L.tilestat = take(std::max((size_t)std::max(ntiles, 1) * 8, (size_t)tb->sm_count * 16 * 4));
+  L.tilestat = take(std::max((size_t)std::max(ntiles, 1) * 8, (size_t)tb->sm_count * 32 * 4));   // k_fast: 2 counts per CTA
   L.out = take((size_t)(1 + 2 * tb->Wd) * 8);
   L.slot = take((size_t)tb->Wd * 8);
   L.bar = take((size_t)kBarWords * 4);
@@ -555,6 +557,7 @@ static void free_table(ct_table *tb) {
   if (tb->comm) ncclCommDestroy(tb->comm);
   for (cudaEvent_t e : tb->ev_pool) cudaEventDestroy(e);
   if (tb->S) tb->dfree(tb->S, tb->S_bytes);
+  if (tb->cells) tb->dfree(tb->cells, tb->cells_bytes);
   if (tb->meta) tb->dfree(tb->meta, tb->meta_bytes);
   if (tb->own_stream && tb->stream) cudaStreamDestroy(tb->stream);
   delete tb;
@@ -573,6 +576,7 @@ void ct_config_init(ct_config *cfg) {
   cfg->use_index = 1;
   cfg->use_graph = 1;
   cfg->use_fused = 1;
+  cfg->use_gather = 1;
 }
 
 ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin, int64_t *words) {
@@ -591,17 +595,6 @@ ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64
 
 const char *ct_last_error(void) { return g_err; }
 
-#ifdef CT_PROBE_DEBUG
-// experiment builds only (not declared in ct.h)
-int ct_debug_probe_read(void *out, size_t bytes) {
-  return (int)cudaMemcpyFromSymbol(out, g_probe_dbg, bytes);
-}
-#endif
-#ifdef CT_FAST_TRACE
-int ct_debug_trace_read(void *out, size_t bytes) {
-  return (int)cudaMemcpyFromSymbol(out, g_fast_trace, bytes);
-}
-#endif
 // Spin-watchdog diagnostics (ct_kernels.cuh spin_report): one host-mapped
 // buffer per process, attached to a device's g_diag.
 static unsigned long long *g_diag_host = nullptr;
@@ -615,6 +608,14 @@ ct_status ct_debug_diag_attach(int32_t device) {
   unsigned long long *dp = nullptr;
   CUDA_TRY(cudaHostGetDevicePointer((void **)&dp, g_diag_host, 0));
   CUDA_TRY(cudaMemcpyToSymbol(g_diag, &dp, sizeof dp));
+  CUDA_TRY(cudaDeviceSynchronize());
+  return CT_OK;
+}
+ct_status ct_debug_spin_limit(int32_t device, double seconds) {
+  if (!(seconds > 0)) return fail(CT_EINVAL, "spin limit must be > 0 s");
+  DeviceGuard g(device);
+  const unsigned long long ns = (unsigned long long)(seconds * 1e9);
+  CUDA_TRY(cudaMemcpyToSymbol(g_spin_limit_ns, &ns, sizeof ns));
   CUDA_TRY(cudaDeviceSynchronize());
   return CT_OK;
 }
@@ -931,6 +932,24 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     }
   }
 
+  // gather filter (k_fast, ct_fast.cuh): the local tuples' value offsets, 8 or
+  // 16 bits per cell, for tables whose filter may scan many support rows
+  {
+    int maxd = 1;
+    for (int i = 0; i < n; ++i) maxd = std::max(maxd, dom_size[i]);
+    const bool star_free = kind == CT_TABLE_POSITIVE || (kind == CT_TABLE_SHORT && !any_star);
+    if (cfg.use_gather && tb->use_fast && star_free && maxd <= 65536 && tb->t_local > 0) {
+      const int bits = maxd <= 256 ? 8 : 16;
+      const int words = (n * bits + 31) / 32;
+      tb->cells_bytes = (size_t)tb->t_local * words * 4;
+      tb->cells = (uint32_t *)tb->dalloc(tb->cells_bytes);
+      if (!tb->cells) return fail(CT_ENOMEM, "device allocation of %zu bytes of gather cells failed", tb->cells_bytes);
+      tb->dev.cells = tb->cells;
+      tb->dev.cell_bits = bits;
+      tb->dev.cell_words = words;
+    }
+  }
+
   // ---------------- root state + supports (a1)
   ct_state *root = nullptr;
   CT_TRY(new_state(tb, &root));
@@ -947,6 +966,11 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
       k_build<<<(unsigned)blocks, threads, 0, tb->stream>>>((const int32_t *)d_tup, tb->t_local, n, d_lo, d_d,
                                                             d_rowBase, tb->S, tb->Wp, (uint32_t *)root->h.T,
                                                             2 * tb->Wp, kind == CT_TABLE_SHORT ? 1 : 0);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && tb->cells) {
+      k_build_cells<<<(unsigned)((tb->t_local + 255) / 256), 256, 0, tb->stream>>>(
+          (const int32_t *)d_tup, tb->t_local, n, d_lo, d_d, tb->cells, tb->dev.cell_bits, tb->dev.cell_words);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(tb->stream);   // tuples freed below
@@ -1030,6 +1054,8 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->grid = t->kind == CT_TABLE_NEGATIVE ? t->sm_count * t->neg_occ : t->use_wide ? 1 : t->use_small ? 1
           : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   o->batch_tile = t->bt_tw;
+  o->gather_cell_bits = t->cells ? t->dev.cell_bits : 0;
+  o->kind = t->kind;
   return CT_OK;
 }
 
@@ -1496,6 +1522,7 @@ static void stats_from_ctl(const Ctl &c, ct_stats *o) {
   o->update_support_words = (int64_t)c.upd_loads;
   o->update_table_writes = (int64_t)c.upd_writes;
   o->filter_support_words = (int64_t)c.scan_loads;
+  o->filter_gathered_tuples = (int64_t)c.gathered;
   for (int i = 0; i < 7; ++i) o->phase_ns[i] = (c.tph[0] && c.tph[i + 1] >= c.tph[i]) ? (int64_t)(c.tph[i + 1] - c.tph[i]) : 0;
 }
 

@@ -51,7 +51,7 @@ class ct_config(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p),
                 ("update_policy", ctypes.c_int32), ("use_residues", ctypes.c_int32),
                 ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32),
-                ("use_fused", ctypes.c_int32)]
+                ("use_fused", ctypes.c_int32), ("use_gather", ctypes.c_int32)]
 
 
 class ct_table_info(ctypes.Structure):
@@ -61,7 +61,7 @@ class ct_table_info(ctypes.Structure):
                 ("word_begin", ctypes.c_int64), ("words", ctypes.c_int64),
                 ("row_stride_words", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("batch_tile", ctypes.c_int32)]
+                ("batch_tile", ctypes.c_int32), ("gather_cell_bits", ctypes.c_int32), ("kind", ctypes.c_int32)]
 
 KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small", 4: "k_wide", 5: "negative"}
 
@@ -72,7 +72,8 @@ class ct_stats(ctypes.Structure):
                 ("n_filter_items", ctypes.c_int32), ("n_residue_miss", ctypes.c_int32),
                 ("words_in", ctypes.c_int64), ("words_out", ctypes.c_int64),
                 ("update_support_words", ctypes.c_int64), ("update_table_writes", ctypes.c_int64),
-                ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 7)]
+                ("filter_support_words", ctypes.c_int64), ("phase_ns", ctypes.c_int64 * 7),
+                ("filter_gathered_tuples", ctypes.c_int64)]
 
 
 class ct_search_stats(ctypes.Structure):
@@ -107,6 +108,7 @@ SIGNATURES = {
     "ct_create_table": (I32, [I32, I32, P, P, P, P, I64, P, P, P, P, P]),
     "ct_debug_diag_attach": (I32, [I32]),
     "ct_debug_diag_read": (I64, [P, I64]),
+    "ct_debug_spin_limit": (I32, [I32, ctypes.c_double]),
     "ct_table_info_get": (I32, [P, P]),
     "ct_dom_words": (I32, [P]),
     "ct_dom_word_offset": (I32, [P, I32]),
@@ -244,7 +246,7 @@ class TorchAllocator:
 def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1, shard_rank: int = 0,
                 nccl_unique_id: bytes | None = None, update_policy: int = CT_POLICY_AUTO,
                 use_residues: bool = True, use_index: bool = True, use_graph: bool = True,
-                use_fused: bool = True):
+                use_fused: bool = True, use_gather: bool = True):
     cfg = ct_config()
     lib().ct_config_init(ctypes.byref(cfg))
     cfg.device = device
@@ -261,6 +263,7 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
     cfg.use_index = int(bool(use_index))
     cfg.use_graph = int(bool(use_graph))
     cfg.use_fused = int(bool(use_fused))
+    cfg.use_gather = int(bool(use_gather))
     return cfg, keep
 
 
@@ -605,6 +608,10 @@ def ct_host_table_destroy(table) -> None:
 def ct_debug_diag_attach(device: int = 0) -> None:
     """Spin-watchdog diagnostics buffer for `device` (include/ct.h)."""
     _check(lib().ct_debug_diag_attach(int(device)), allow_fail=False)
+
+
+def ct_debug_spin_limit(device: int, seconds: float) -> None:
+    _check(lib().ct_debug_spin_limit(int(device), float(seconds)), allow_fail=False)
 
 
 def ct_debug_diag_read(n_words: int = 64 + 128 + 2 * 4096) -> np.ndarray:

@@ -195,16 +195,17 @@ def test_private_variables_fixpoint_and_search(seed):
 def test_device_search_repeated_same_trace():
     """Regression: the device-resident DFS once let a CTA restore the state pool
     (after a solution) while slower CTAs were still reading the shared domains,
-    splitting the grid's control flow (a hang about once per ~300 searches).
-    48 all-solution searches: every trace equals the first and the host
-    driver's (a split now trips the spin watchdog: CT_ECUDA, not a hang)."""
+    splitting the grid's control flow (a hang about once per ~300 searches;
+    tools/hang_probe.py runs thousands).  12 all-solution searches: every trace
+    equals the host driver's (a split now trips the spin watchdog: CT_ECUDA,
+    not a hang)."""
     m = csp_model(10, 8, 6, 400, seed=81, arities=[3, 4, 2, 5, 3, 4])
     M = _model(m)
     if M.root_status != CT_OK:
         M.close()
         return
     ref = M.search(value_order=0, max_solutions=0, driver="host")[2]
-    for i in range(48):
+    for i in range(12):
         s = M.search(value_order=i % 2, max_solutions=0, driver="device")[2]
         if i % 2 == 0:
             assert (s.nodes, s.failures, s.solutions, s.trace_hash) == \

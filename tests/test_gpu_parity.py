@@ -277,10 +277,16 @@ def test_pipelined_pinned_host_calls(path):
     tab.close()
 
 
-@pytest.mark.parametrize("fast", [True, False], ids=["fast", "v1"])
-def test_config3b_banded_filter_heavy(fast):
+@pytest.mark.parametrize("fast,gather", [(True, True), (True, False), (False, True)], ids=["fast", "fast_scan", "v1"])
+def test_config3b_banded_filter_heavy(fast, gather):
+    """Fixing x0 on the banded table leaves ~1 % of the tuples valid and ~630
+    unsupported values: k_fast resolves the residue misses by gathering the
+    valid tuples' values (use_gather) or by Alg. 3's full scans; both vs the
+    oracle, with currTable checked on the first call."""
     p = banded_table(8, 100, 2_000_000, seed=4)
-    tab = make(p, _fast=fast)
+    tab = make(p, _fast=fast, use_gather=gather)
+    info = tab.info
+    assert (info.gather_cell_bits == 8) == (fast and gather)
     check_root(tab, p)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     rng = Rng(12)
@@ -295,6 +301,36 @@ def test_config3b_banded_filter_heavy(fast):
             assert np.array_equal(bitmap_to_member(dom, p.d), dout)
         s = st.stats()
         assert s.n_residue_miss > 0          # this workload exercises the full scans
+        assert (s.filter_gathered_tuples > 0) == (fast and gather)
+        if k == 0 and ok:
+            _, _, valid = oracle_call(p, root_m & (1 - rem), want_valid=True)
+            assert np.array_equal(bits_to_bool(st.read_table(), p.t), valid)
+    st.close()
+    tab.close()
+
+
+@pytest.mark.parametrize("gather", [True, False], ids=["gather", "scan"])
+@pytest.mark.parametrize("shape", [(3, 40, 200_000), (6, 100, 300_001), (5, 300, 400_003)])
+def test_gather_filter_walks(shape, gather):
+    """Banded tables (8-bit and 16-bit cells: d = 300) walked with P(2, 0.5)
+    and with x0 fixed: the gather filter and the scan filter both equal the
+    oracle on every call (domains, pruned sets, currTable every 7 calls)."""
+    n, d, t = shape
+    p = banded_table(n, d, t, seed=40 + n, band=max(3, d // 10))
+    tab = make(p, _grid_fused=True, use_gather=gather)
+    run_walk(tab, p, 60, seed=5, check_table_every=7)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    rng = Rng(13)
+    st = tab.root.clone()
+    for k in range(4):
+        rem = fix_one_value_removal(rng, root_m, p.d, var=0)
+        ok, dout, valid = oracle_call(p, root_m & (1 - rem), want_valid=True)
+        st.copy_from(tab.root)
+        status, dom, pr = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL), k
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout), k
+            assert np.array_equal(bits_to_bool(st.read_table(), p.t), valid), k
     st.close()
     tab.close()
 
