@@ -1152,6 +1152,135 @@ def run_placement(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- f4: short and negative tables
+def run_f4(args, kind):
+    """f4: a C3-shaped short table (arity 8,
+    domain 100, 1e7 tuples, 2 % star cells) or a negative table (arity 4,
+    domain 60, 1e7 forbidden assignments drawn over the 1.3e7-point product),
+    16 seeded bulk removals (half of every variable's values) from the root,
+    one restore + ct_propagate_async per step, device-timed; the first pattern
+    is checked against the oracle (untimed).  N > 1: independent replicas."""
+    import torch
+    import oracle
+    from paper_2507_18413_b200 import CT_OK, CT_FAIL, Table
+    from paper_2507_18413_b200 import ct as C
+    from workloads import member_to_bitmap, bitmap_to_member, short_table, negative_table
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    if kind == "short":
+        p = short_table(8, 100, 10_000_000, seed=3, p_star=0.02)
+        desc = "short: arity 8, domain 100, 1e7 tuples, 2 % star cells, seed 3"
+    else:
+        p = negative_table(4, 60, 10_000_000, seed=13)
+        desc = "negative: arity 4, domain 60, 1e7 forbidden tuples i.i.d. over the 1.3e7-point product, seed 13"
+    t0 = time.perf_counter()
+    tab = Table(p.lo, p.d, p.tuples, device=dev, kind=kind)
+    build_s = time.perf_counter() - t0
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    P = 16
+    pats = bulk_patterns(root_m, p.d, P)
+    rem_host = np.stack([member_to_bitmap(m, p.d) for m in pats])
+    rem_dev = torch.from_numpy(rem_host.view(np.int64)).to(f"cuda:{dev}")
+    wd = tab.Wd
+    out_dom = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    out_pr = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
+    status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+    work = tab.root.clone()
+    stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+
+    def step(k):
+        work.copy_from(tab.root)
+        work.propagate_async(rem_dev[k % P], out_dom, out_pr, status)
+
+    # parity of the first pattern (untimed)
+    step(0)
+    work.synchronize()
+    din = root_m & (1 - pats[0])
+    if kind == "short":
+        ok, dout, _ = oracle.gac_short(p.lo, p.d, p.tuples, din)
+    else:
+        ok, dout, _ = oracle.gac_negative(p.lo, p.d, p.tuples, din)
+    got = int(status.cpu()[0])
+    parity = got == (CT_OK if ok else CT_FAIL) and (not ok or np.array_equal(
+        bitmap_to_member(out_dom.cpu().numpy().view(np.uint64), p.d), dout))
+    per_pat = []
+    for k in range(P):
+        step(k)
+        s_ = work.stats()
+        per_pat.append(dict(L_in=s_.words_in, L_out=s_.words_out, rows=s_.n_update_rows, items=s_.n_filter_items,
+                            upd=s_.update_support_words, filt=s_.filter_support_words, writes=s_.update_table_writes,
+                            gathered=s_.filter_gathered_tuples))
+    for k in range(args.warmup):
+        step(k)
+    work.synchronize()
+    clocks = Clocks(dev)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for k in range(args.steps):
+        step(k)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    barrier(world)
+    ms_max = max_over_ranks(ms, world)
+    C.ct_table_profile(tab.handle, True)
+    C.ct_table_profile_read(tab.handle, reset=True)
+    for k in range(args.steps):
+        step(k)
+    prof = C.ct_table_profile_read(tab.handle, reset=True)
+    C.ct_table_profile(tab.handle, False)
+    peak, peak_src = peaks()
+    if kind == "short":
+        kname, slot = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_fast"), "fused"
+        if not prof.get("fused", (0, 0))[0]:
+            slot = "small"
+        b = [8 * c["upd"] + 16 * c["L_in"] + 16 * c["writes"] + 8 * c["filt"] + 32 * c["gathered"] +
+             4 * (c["L_in"] + c["L_out"]) for c in per_pat]
+        model = ("counted: 8 x support words loaded (update + filter) + 16 B per index entry read / block "
+                 "rewritten + 4 B index entries + 32 B per gathered tuple")
+    else:
+        kname, slot = "ctk::k_neg_count", "scan"
+        b = [8 * c["filt"] + 16 * c["L_out"] for c in per_pat]
+        model = ("k_neg_count: 16 B per (count row, active block) + the active currTable blocks once "
+                 "(SURVEY §8(d)-style: rows counted x L_out x 16 + 16 L_out)")
+    n_l, k_ms = prof.get(slot, (0, 0.0))
+    k_ms_pl = k_ms / max(n_l, 1)
+    bytes_pl = sum(b[k % P] for k in range(args.steps)) / max(args.steps, 1)
+    roofline = {"bound": "hbm", "achieved": bytes_pl / (k_ms_pl / 1e3) / 1e9 if k_ms_pl else None, "peak": peak,
+                "unit": "GB/s", "frac": (bytes_pl / (k_ms_pl / 1e3) / 1e9 / peak) if k_ms_pl else None,
+                "traffic": ncu_traffic(kind, world, kname), "kernel": kname, "bytes_per_launch": bytes_pl,
+                "ms_per_launch": k_ms_pl, "bytes_model": model, "peak_source": peak_src}
+    value = args.steps * world / (ms_max / 1e3)
+    if rank == 0:
+        line = {"metric": f"propagations/s (f4 {kind} table, bulk ct_propagate from the root)", "value": value,
+                "unit": "propagations/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, workloads.%s_table)" % kind,
+                "config": {"workload": kind if kind == "short" else "neg", "table": desc,
+                           "step": "state restore (D2D) + ct_propagate_async of a bulk removal (50 % of every var)",
+                           "patterns": P, "parallelism": "1 GPU" if world == 1 else f"{world} replicas",
+                           "kernel_path": C.KERNEL_PATHS.get(tab.info.kernel_path), "build_s": round(build_s, 3),
+                           "l2": "inputs larger than L2"},
+                "roofline": roofline,
+                "kernel_ms_per_launch": {k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()},
+                "parity_first_pattern": bool(parity), "workload_counters": per_pat[0],
+                "gpu_launches": sum(v[0] for k, v in prof.items()) + args.steps, "clocks": clk,
+                "e2e": None, "cpu_baseline": None}
+        print(json.dumps(line))
+    tab.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args):
     """The reference arm of this tier: the oracle (oracle/ct_oracle.c) timed as it
@@ -1219,7 +1348,7 @@ def main():
     ap.add_argument("--steps", type=int, default=500)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5", "lin", "placement"])
+    ap.add_argument("--workload", default="c3bulk", choices=["c3bulk", "c3b", "c4", "c5", "lin", "placement", "short", "neg"])
     ap.add_argument("--max-nodes", type=int, default=10_000, help="c5: DFS node budget")
     ap.add_argument("--states", type=int, default=4096, help="c4: total independent states (split over ranks)")
     ap.add_argument("--skip-cpu", action="store_true")
@@ -1245,6 +1374,8 @@ def main():
         run_lin(args)
     elif args.workload == "placement":
         run_placement(args)
+    elif args.workload in ("short", "neg"):
+        run_f4(args, "short" if args.workload == "short" else "negative")
     else:
         run_ours(args)
 

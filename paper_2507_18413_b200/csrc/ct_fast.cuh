@@ -524,29 +524,63 @@ __device__ void fast_gather_range(const TableDev &tb, const StateDev &st, const 
   const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
   const int cw = tb.cell_words, bits = tb.cell_bits, per = 32 / bits;
   const uint32_t cmask = (1u << bits) - 1u;
+  // per thread: its entries' valid tuples in batches of kGatherBatch, every
+  // batch's cell loads issued before any is used (one DRAM round trip per
+  // batch instead of one per cell word)
+  constexpr int kGatherBatch = 4;
+  const auto mark_word = [&](uint32_t wv, int q, int pid) {
+    for (int e = 0; e < per; ++e) {
+      const int i = q * per + e;
+      if (i >= n) break;
+      const int v = (int)((wv >> (e * bits)) & cmask);
+      uint64_t *mw = mark + p.dof[i] + (v >> 6);
+      if (!((*(volatile uint64_t *)mw >> (v & 63)) & 1ull)) {   // most values repeat: skip the atomic
+        // the one thread that sets the bit records the residue
+        unsigned int *m32 = reinterpret_cast<unsigned int *>(mw) + ((v & 63) >> 5);
+        const unsigned int bit = 1u << (v & 31);
+        if (!(atomicOr(m32, bit) & bit)) rres[p.rb[i] + v] = pid;
+      }
+    }
+  };
   for (int k = k_lo + tid; k < k_hi; k += kFastTPB) {
     const int pid = fs.ident ? k : idx_in[k];
     const ulonglong2 t = T2[pid];   // written by this thread's own update
+    uint64_t m0 = t.x, m1 = t.y;
+    while (m0 | m1) {
+      int64_t j[kGatherBatch];
+      int nb = 0;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      uint64_t m = h ? t.y : t.x;
-      while (m) {
-        const int b = __ffsll(m) - 1;
-        m &= m - 1;
-        const uint32_t *__restrict__ cr = tb.cells + ((int64_t)(2 * pid + h) * 64 + b) * cw;
-        ++n_tuples;
-        for (int q = 0; q < cw; ++q) {
-          const uint32_t wv = __ldg(cr + q);
-          for (int e = 0; e < per; ++e) {
-            const int i = q * per + e;
-            if (i >= n) break;
-            const int v = (int)((wv >> (e * bits)) & cmask);
-            uint64_t *mw = mark + p.dof[i] + (v >> 6);
-            if (!((*(volatile uint64_t *)mw >> (v & 63)) & 1ull)) {   // most values repeat: skip the atomic
-              smem_set_bit(mw, v & 63);
-              rres[p.rb[i] + v] = pid;
-            }
+      for (int b = 0; b < kGatherBatch; ++b) {
+        j[b] = -1;
+        if (m0) {
+          j[b] = (int64_t)(2 * pid) * 64 + (__ffsll(m0) - 1);
+          m0 &= m0 - 1;
+        } else if (m1) {
+          j[b] = (int64_t)(2 * pid + 1) * 64 + (__ffsll(m1) - 1);
+          m1 &= m1 - 1;
+        }
+        nb += j[b] >= 0;
+      }
+      n_tuples += nb;
+      if (cw == 2) {   // the common case (n <= 8 at 8 bits, n <= 4 at 16): 2 words per tuple, 8 loads in flight
+        uint2 w[kGatherBatch];
+#pragma unroll
+        for (int b = 0; b < kGatherBatch; ++b)
+          w[b] = j[b] >= 0 ? __ldg(reinterpret_cast<const uint2 *>(tb.cells + j[b] * 2)) : make_uint2(0u, 0u);
+#pragma unroll
+        for (int b = 0; b < kGatherBatch; ++b)
+          if (j[b] >= 0) {
+            mark_word(w[b].x, 0, pid);
+            mark_word(w[b].y, 1, pid);
           }
+      } else {
+        for (int q = 0; q < cw; ++q) {
+          uint32_t w[kGatherBatch];
+#pragma unroll
+          for (int b = 0; b < kGatherBatch; ++b) w[b] = j[b] >= 0 ? __ldg(tb.cells + j[b] * cw + q) : 0u;
+#pragma unroll
+          for (int b = 0; b < kGatherBatch; ++b)
+            if (j[b] >= 0) mark_word(w[b], q, pid);
         }
       }
     }
@@ -864,6 +898,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       // tuples' values (fast_gather_range) -- whichever reads fewer bytes.  Both
       // inputs are final after the probe barrier, so every CTA decides alike.
       if (tb.cells) {
+        __syncthreads();   // every thread has read the barrier's mode from fs.nscan
         if (tid == 0) fs.nscan = __ldcg(&c->nscan);
         unsigned long long v = 0;
         for (int j = tid; j < G; j += kFastTPB) v += __ldcg(tcnt + G + j);

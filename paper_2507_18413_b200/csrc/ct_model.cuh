@@ -427,9 +427,13 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_model_search(ModelDev md, Sear
     c.state = c.fail ? kSDone : kSExpand;
   }
   __syncthreads();
-  while (c.state != kSDone) {
+  while (true) {
     const int state = c.state;
     set_loc(0x20000000u | ((uint32_t)state << 16) | ((uint32_t)c.d & 0xffffu));
+    // every thread has read the state (and the step before it read c) before
+    // thread 0 may change it below
+    __syncthreads();
+    if (state == kSDone) break;
     if (state == kSExpand) {
       // the node at depth d is an OK fixpoint: pick x (input_order) and a
       // (indomain_max / min); the shared domains go to shared memory first

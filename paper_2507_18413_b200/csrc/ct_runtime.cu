@@ -1743,6 +1743,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
     for (ct_state *x : roots) free_state_mem(x);
     return bail(fail(CT_ENOMEM, "model pool allocation failed"));
   }
+  cudaMemsetAsync(m->pool, 0, m->pool_bytes, m->stream);   // scratch too: trail snapshots copy whole states
   for (int k = 0; k < n_tables; ++k) {
     cudaMemcpyAsync(m->pool + m->off[k], roots[k]->mem, m->tabs[k]->lay.persist, cudaMemcpyDeviceToDevice, m->stream);
   }
