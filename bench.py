@@ -1191,6 +1191,7 @@ def run_f4(args, kind):
     status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
     work = tab.root.clone()
     stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+    torch.cuda.synchronize()   # the tensors above were filled on torch's stream
 
     def step(k):
         work.copy_from(tab.root)

@@ -162,9 +162,14 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// rank / count: this CTA's rank among the `count` CTAs that meet at `bar`
+// (default: the whole grid; the grouped model fixpoint uses per-table groups).
 template <typename F>
 __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mode, int &leader, int *s_mode,
-                                                      const int *extra_flag = nullptr) {
+                                                      const int *extra_flag = nullptr, int rank = -1,
+                                                      int count = -1) {
+  if (rank < 0) rank = blockIdx.x;
+  if (count < 0) count = gridDim.x;
   __syncthreads();   // also orders the block's writes of *extra_flag before thread 0 reads it
   if (threadIdx.x == 0) {
     const uint32_t extra = extra_flag ? (uint32_t)*(volatile const int *)extra_flag : 0u;
@@ -172,13 +177,13 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
     // the generation word has kBarGroups copies (lines 1..kBarGroups): each CTA
     // polls its group's copy, so the polling is spread over several L2 slices.
     // Its low bit carries the mode, so nobody reads a second word after release.
-    uint32_t *mygen = bar + (1 + blockIdx.x % kBarGroups) * kBarLine;
+    uint32_t *mygen = bar + (1 + rank % kBarGroups) * kBarLine;
     const uint32_t my_gen = ld_acquire_u32(mygen);
     int last = 0;
     uint32_t g;
     // low 16 bits: arrivals; high 16 bits: the sum of the CTAs' `extra` values
     const uint32_t old = atom_add_acqrel(cnt, 1u + (extra << 16));
-    if ((old & 0xffffu) == gridDim.x - 1) {
+    if ((old & 0xffffu) == (uint32_t)count - 1) {
       *cnt = 0;
       g = ((((my_gen >> 1) + 1u) << 1)) | ((uint32_t)leader_mode((old >> 16) + extra) & 1u);
       __threadfence();   // one release fence for all the generation copies
@@ -199,10 +204,10 @@ __device__ __forceinline__ int fast_grid_barrier_mode(uint32_t *bar, F leader_mo
   return *s_mode;
 }
 
-__device__ __forceinline__ void fast_grid_barrier(uint32_t *bar) {
+__device__ __forceinline__ void fast_grid_barrier(uint32_t *bar, int rank = -1, int count = -1) {
   __shared__ int s_mode;
   int leader;
-  fast_grid_barrier_mode(bar, [](uint32_t) { return 0; }, leader, &s_mode);
+  fast_grid_barrier_mode(bar, [](uint32_t) { return 0; }, leader, &s_mode, nullptr, rank, count);
 }
 
 // Adds a per-thread counter to a global 64-bit counter with ONE atomic per CTA
@@ -238,7 +243,7 @@ __device__ __forceinline__ int fast_block_sum(int v, FastSh &fs) {
 // CTA's shared memory; `writer` (block 0) also publishes the per-call state.
 template <int NT = kFastTPB>
 __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem, int root_mode,
-                           const FastPtrs &p, FastShT<NT / 32> &fs, bool writer) {
+                           const FastPtrs &p, FastShT<NT / 32> &fs, bool writer, const uint64_t *gdom = nullptr) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
@@ -248,7 +253,8 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   int x0 = 0;
   if (tid < Wd) {
     dm0 = st.dom[tid];
-    rm0 = rem ? rem[tid] : 0ull;
+    // model tables: a value is removed iff the shared (global) domain lost it
+    rm0 = gdom ? ~__ldcg(gdom + tb.gword[tid]) : (rem ? rem[tid] : 0ull);
     x0 = tb.wordVar[tid];
   }
   if (tid == 0) {
@@ -288,7 +294,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
   for (int k = tid; k < Wd; k += NT) {
     const uint64_t dm = k == tid ? dm0 : st.dom[k];
-    const uint64_t rm = k == tid ? rm0 : (rem ? rem[k] : 0ull);
+    const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
     const int x = k == tid ? x0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     p.din[k] = di;
@@ -653,9 +659,10 @@ __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, in
 // ------------------------------------------------------------------ a6c-a8: finalize from shared memory
 // Alg. 3 L3-4 over the filter items this CTA listed in its ingest: a value of
 // x in s_sup leaves the domain iff its row is unsupported; lastDom <- dom.
-__device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
-                             uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
-                             int32_t *__restrict__ out_status, bool sys_fence) {
+// Returns the status; on CT_OK the new domains are left in p.dl (s_nd).
+__device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
+                            uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
+                            int32_t *__restrict__ out_status, bool sys_fence) {
   constexpr int NT = kFastTPB;
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, Wd = tb.Wd;
@@ -673,7 +680,7 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
       c->last_status = status;
       if (out_status) *out_status = status;
     }
-    return;
+    return status;
   }
   uint64_t *s_nd = p.dl;
   for (int k = tid; k < Wd; k += NT) s_nd[k] = p.din[k];
@@ -711,6 +718,7 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
     c->last_status = 0;
     if (out_status) *out_status = 0;
   }
+  return 0;
 }
 
 
@@ -719,25 +727,25 @@ __device__ void cta_finalize(const TableDev &tb, const StateDev &st, const FastP
 // fast_smem_bytes(n, Wd, R).  with_finalize = 0 for sharded tables (the flags are
 // OR-combined across shards first and k_finalize runs after).  Filter items
 // are spread CTA-major (item i -> CTA i % grid) so few items probe on many SMs.
-__global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, const StateDev *__restrict__ states,
-                                                   const uint64_t *__restrict__ removed, int root_mode,
-                                                   int with_finalize, uint64_t *__restrict__ out_dom,
-                                                   uint64_t *__restrict__ out_pruned,
-                                                   int32_t *__restrict__ out_status, int use_state_out) {
-  extern __shared__ __align__(16) uint64_t smem[];
-  __shared__ FastSh fs;
-  __shared__ StateDev s_st;   // the state's pointers live in shared memory, not in 30 registers
-  if (threadIdx.x == 0) s_st = states[0];
-  __syncthreads();
-  const StateDev &st = s_st;
+// One whole single-state call by the G CTAs (ranks 0..G-1) that share the
+// state: k_fast runs it on the whole grid, the grouped model fixpoint
+// (ct_model.cuh) on one table's group of CTAs.  gdom != nullptr: a model
+// table (removals = values the shared domains lost; no outputs).  Returns the
+// call's status on the CTA that finalized (the last to finish), kNotFinalizer
+// on the others; with_finalize = 0 (sharded tables) always kNotFinalizer.
+constexpr int kNotFinalizer = -100;
+__device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st, FastSh &fs, const FastPtrs &p,
+                                         const uint64_t *__restrict__ removed, const uint64_t *gdom, int root_mode,
+                                         int with_finalize, uint64_t *__restrict__ out_dom,
+                                         uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status,
+                                         int use_state_out, const int rank, const int G) {
   Ctl *c = st.ctl;
-  const FastPtrs p = fast_ptrs(smem, tb);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  const bool t0 = blockIdx.x == 0 && tid == 0;
-  // phase timestamps of block 0 go straight to tph[] (no registers held)
+  const bool t0 = rank == 0 && tid == 0;
+  int fstatus = kNotFinalizer;
+  // phase timestamps of rank 0 go straight to tph[] (no registers held)
   if (t0) c->tph[0] = globaltimer();
-  cta_ingest(tb, st, removed, root_mode, p, fs, blockIdx.x == 0);
+  cta_ingest(tb, st, removed, root_mode, p, fs, rank == 0, gdom);
   if (t0) {
     const unsigned long long t = globaltimer();
     for (int i = 1; i < 6; ++i) c->tph[i] = t;
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     // (an equal share per CTA, so every SM streams the same number of blocks),
     // walked kFastTPB at a time; the CTA's survivor count goes to tcnt[c]
     const int ts = (fs.L + G - 1) / G;
-    const int k_lo = min(fs.L, (int)blockIdx.x * ts), k_hi = min(fs.L, k_lo + ts);
+    const int k_lo = min(fs.L, rank * ts), k_hi = min(fs.L, k_lo + ts);
     uint32_t n_loads = 0, n_writes = 0, f_loads = 0;
     {
       int kept = 0;
@@ -762,7 +770,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         nv += cnt;
         kept += __syncthreads_count(cnt != 0);
       }
-      if (tid == 0) tcnt[blockIdx.x] = (uint32_t)kept;
+      if (tid == 0) tcnt[rank] = (uint32_t)kept;
       if (tb.cells) {
         nv = warp_sum_u32(nv);
         if (lane == 0) atomicAdd(&fs.nvalid, nv);
@@ -790,7 +798,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     }
 
     const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-    fast_grid_barrier(st.bar);
+    fast_grid_barrier(st.bar, rank, G);
     if (t0) c->tph[2] = globaltimer();
 
     // ---- compaction (a4), part A: L_out and this CTA's prefix from the
@@ -801,18 +809,18 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       for (int j = tid; j < G; j += kFastTPB) {
         const int v = (int)__ldcg(tcnt + j);
         tot += v;
-        if (j < (int)blockIdx.x) below += v;
+        if (j < rank) below += v;
       }
       tot = fast_block_sum(tot, fs);
       below = fast_block_sum(below, fs);
       if (tid == 0) {
         fs.Lout = tot;
         fs.below = below;
-        if (blockIdx.x == 0) c->L_out = tot;
+        if (rank == 0) c->L_out = tot;
       }
     }
     if (tb.cells && tid == 0) {   // this CTA's valid tuples -> the grid's (read after the probe barrier)
-      tcnt[G + blockIdx.x] = (uint32_t)fs.nvalid;
+      tcnt[G + rank] = (uint32_t)fs.nvalid;
     }
     __syncthreads();
 
@@ -828,12 +836,12 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     const bool may_miss = fs.L > kSelfRounds * kFirstScanFast;   // the probe cannot cover the index
     if (t0) st.sup[tb.R] = Lout > 0;
     if (Lout > 0) {
-      const int per_cta = (fs.nitems - (int)blockIdx.x + G - 1) / G;   // items of this CTA
+      const int per_cta = (fs.nitems - rank + G - 1) / G;   // items of this CTA
       const int wpi = per_cta <= 1 ? kFastWarps : per_cta <= 2 ? kFastWarps / 2 : 1;
       const int slots = kFastWarps / wpi, slot = warp / wpi, q = warp % wpi;
       for (int j0 = 0; j0 < per_cta; j0 += slots) {
         const int j = j0 + slot;
-        const int item = (int)blockIdx.x + j * G;
+        const int item = rank + j * G;
         int hit = -1, row = 0, r = -1;
         if (j < per_cta) {
           row = p.items[item];
@@ -879,7 +887,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
     if (Lout > 0 && may_miss) {
       int leader = 0;
       const int mode = fast_grid_barrier_mode(st.bar, [](uint32_t misses) { return misses == 0 ? 1 : 0; }, leader,
-                                              &fs.nscan, &fs.anymiss);
+                                              &fs.nscan, &fs.anymiss, rank, G);
       if (t0) c->tph[4] = globaltimer();
       if (mode == 1) {
         if (t0) c->tph[5] = globaltimer();   // no scan phase
@@ -887,7 +895,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
         __syncthreads();
         if (!fs.last) {
           if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
-          return;
+          return kNotFinalizer;
         }
         compact_after = tb.use_index != 0;
         leader_k_lo = k_lo;
@@ -923,7 +931,7 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
       }
       // the whole new index first (the scans read it)
       if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
-      fast_grid_barrier(st.bar);
+      fast_grid_barrier(st.bar, rank, G);
       if (tid == 0) fs.nscan = __ldcg(&c->nscan);
       __syncthreads();
       const int nscan = fs.nscan;
@@ -1016,7 +1024,7 @@ completion:
     fs.last = atomicAdd(&c->cta_done, 1) == G - 1;
   }
   __syncthreads();
-  if (!fs.last) return;
+  if (!fs.last) return kNotFinalizer;
   __threadfence();
   if (tid == 0) c->cta_done = 0;
 finalize:
@@ -1027,13 +1035,30 @@ finalize:
       out_pruned = st.out + 1 + tb.Wd;
       out_status = reinterpret_cast<int32_t *>(st.out);
     }
-    cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
+    fstatus = cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
   }
   if (tid == 0) c->tph[7] = globaltimer();
   if (compact_after) {   // the leader's own index entries, after the outputs
     __syncthreads();
     fast_compact_range(tb, st, fs, leader_k_lo, leader_k_hi);
   }
+  return fstatus;
+}
+
+// grid = co-resident CTAs (cooperative launch), kFastTPB threads, dynamic smem
+// fast_smem_bytes(n, Wd, R).
+__global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, const StateDev *__restrict__ states,
+                                                   const uint64_t *__restrict__ removed, int root_mode,
+                                                   int with_finalize, uint64_t *__restrict__ out_dom,
+                                                   uint64_t *__restrict__ out_pruned,
+                                                   int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ FastSh fs;
+  __shared__ StateDev s_st;   // the state's pointers live in shared memory, not in 30 registers
+  if (threadIdx.x == 0) s_st = states[0];
+  __syncthreads();
+  fast_call(tb, s_st, fs, fast_ptrs(smem, tb), removed, nullptr, root_mode, with_finalize, out_dom, out_pruned,
+            out_status, use_state_out, (int)blockIdx.x, (int)gridDim.x);
 }
 
 }  // namespace ctk

@@ -542,8 +542,16 @@ __device__ int dev_ingest(const TableDev &tb, const StateDev &st, const uint64_t
 // instead of block scans: for one-CTA calls on small tables (k_small) the
 // ingest is latency-bound and 32 lanes cover its few words and rows.  Every
 // thread of the block calls it; it ends with a block barrier.
+// Shared-memory copies of what warp_ingest publishes (k_small keeps the whole
+// call on chip: no global round trip between its phases).
+struct SmallSh {
+  int32_t *ulist, *items;   // [R] each
+  int skip, noop, fail, nrows, nitems, L, ident, par;
+};
+
 __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem,
-                            int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr) {
+                            int root_mode, uint64_t *smem, const uint64_t *gdom = nullptr,
+                            SmallSh *sh = nullptr) {
   Ctl *c = st.ctl;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
   uint64_t *s_din = smem;
@@ -572,6 +580,11 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         c->skip = 1;
         c->noop = 0;
         c->fail_fast = 0;
+        if (sh) {
+          sh->skip = 1;
+          sh->noop = 0;
+          sh->fail = 0;
+        }
       }
     } else {
       uint4 *s4 = reinterpret_cast<uint4 *>(st.sup);   // sup[0..R] = 0 (256-byte aligned)
@@ -643,9 +656,13 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
             const int up = ucarry + __popc(bu & lanemask_lt());
             uint32_t e = (uint32_t)r | (useDelta ? kInvBit : 0u);
             if (up == s_ust[x + 1] - 1) e |= kEndBit;
-            st.ulist[up] = (int32_t)e;
+            if (sh) sh->ulist[up] = (int32_t)e;
+            else st.ulist[up] = (int32_t)e;
           }
-          if (f) st.items[icarry + __popc(bf & lanemask_lt())] = r;
+          if (f) {
+            if (sh) sh->items[icarry + __popc(bf & lanemask_lt())] = r;
+            else st.items[icarry + __popc(bf & lanemask_lt())] = r;
+          }
           ucarry += __popc(bu);
           icarry += __popc(bf);
         }
@@ -653,13 +670,24 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         nitems = icarry;
       }
       if (lane == 0) {
+        const int L0 = c->L;
+        if (sh) {
+          sh->skip = 0;
+          sh->noop = noop && !fail;
+          sh->fail = fail;
+          sh->nrows = nrows;
+          sh->nitems = nitems;
+          sh->L = L0;
+          sh->ident = c->identity;
+          sh->par = c->parity;
+        }
         c->skip = 0;
         c->noop = noop && !fail;
         c->fail_fast = fail;
         c->ngroups = ngroups;
         c->nrows = nrows;
         c->nitems = nitems;
-        c->L_in = c->L;
+        c->L_in = L0;
         c->L_out = 0;
         c->tile_ctr = 0;
         c->nscan = 0;
@@ -1193,9 +1221,10 @@ __global__ void __launch_bounds__(kFusedTPB, 3) k_fused(TableDev tb, const State
 // compaction of the survivors into the other index buffer, by ONE block of NT
 // threads (tables of at most kSmallMaxPairs blocks).  Returns L_out.  Adds the
 // work counters to the state.  s_warp: NT/32 words of shared scratch.
-template <int NT>
+template <int NT, int U = kUpdUnroll>
 __device__ int block_update(const TableDev &tb, const StateDev &st, int L, int nrows, int ident, int par,
-                            uint64_t *s_warp) {
+                            uint64_t *s_warp, const int32_t *ulist = nullptr, int pid0 = -1) {
+  if (!ulist) ulist = st.ulist;
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31;
   const int32_t *__restrict__ idx_in = par ? st.idx1 : st.idx0;
@@ -1210,22 +1239,23 @@ __device__ int block_update(const TableDev &tb, const StateDev &st, int L, int n
     int pid = 0;
     bool keep = false;
     if (k < L) {
-      pid = ident ? k : idx_in[k];
+      // pid0: this thread's first index entry, prefetched by the caller
+      pid = ident ? k : (base == 0 && pid0 >= 0 ? pid0 : idx_in[k]);
       const ulonglong2 tw = T2[pid];
       const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
       uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-      for (int p = 0; p < nrows; p += kUpdUnroll) {
-        if (((tw.x & mx) | (tw.y & my)) == 0) break;
-        uint32_t e[kUpdUnroll];
-        ulonglong2 v[kUpdUnroll];
+      for (int p = 0; p < nrows; p += U) {
+        if (p > 0 && ((tw.x & mx) | (tw.y & my)) == 0) break;
+        uint32_t e[U];
+        ulonglong2 v[U];
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u) e[u] = (p + u < nrows) ? (uint32_t)st.ulist[p + u] : 0u;
+        for (int u = 0; u < U; ++u) e[u] = (p + u < nrows) ? (uint32_t)ulist[p + u] : 0u;
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u)
+        for (int u = 0; u < U; ++u)
           v[u] = (p + u < nrows) ? ld_sup2(col + (int64_t)(e[u] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
-        n_loads += 2 * min(kUpdUnroll, nrows - p);
+        n_loads += 2 * min(U, nrows - p);
 #pragma unroll
-        for (int u = 0; u < kUpdUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
           if (p + u < nrows) {
             ax |= v[u].x;
             ay |= v[u].y;
@@ -1270,7 +1300,8 @@ __device__ int block_update(const TableDev &tb, const StateDev &st, int L, int n
 template <int NT>
 __device__ void small_finalize(const TableDev &tb, const StateDev &st, int status, bool noop, int Lout,
                                uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
-                               int32_t *__restrict__ out_status, uint64_t *smem) {
+                               int32_t *__restrict__ out_status, uint64_t *smem,
+                               const uint8_t *s_sup = nullptr) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
   const uint64_t *s_din = smem;                                         // dev_ingest: D_x
@@ -1294,7 +1325,7 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
   if (!noop) {
     for (int r = tid; r < tb.R; r += NT) {
       const int x = tb.rowVar[r];
-      if (!__ldcg(st.sup + r) && s_cs[x] > 1) {   // x in s_sup (Alg. 3 L1), a unsupported
+      if (!(s_sup ? s_sup[r] : __ldcg(st.sup + r)) && s_cs[x] > 1) {   // x in s_sup (Alg. 3 L1), a unsupported
         const int a = r - s_rb[x];
         smem_clear_bit(s_nd + s_do[x] + (a >> 6), a & 63);
       }
@@ -1331,6 +1362,17 @@ constexpr int kSmallTPB = 1024;
 constexpr int kWarpIngestMaxRows = 1024;   // k_small ingests with one warp up to this many support rows
 constexpr int kSmallMaxPairs = 8192;
 
+// Dynamic shared memory of k_small: the ingest / finalize region, then (warp
+// ingest only) the update list, the filter items, the residues and the
+// support flags, so no phase re-reads what an earlier one produced.
+__host__ __device__ inline size_t small_region_bytes(int n, int Wd) {
+  const size_t a = ingest_smem_bytes(n, Wd), b = finalize_smem_bytes(n, Wd);
+  return ((a > b ? a : b) + 15) / 16 * 16;
+}
+__host__ __device__ inline size_t small_smem_bytes(int n, int Wd, int R) {
+  return small_region_bytes(n, Wd) + (size_t)R * 12 + (size_t)R + 32;
+}
+
 __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const StateDev *__restrict__ states,
                                                        const uint64_t *__restrict__ removed, int root_mode,
                                                        int with_finalize, uint64_t *__restrict__ out_dom,
@@ -1341,78 +1383,139 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool t0 = tid == 0;
-  unsigned long long ts[6];
-  if (t0) ts[0] = globaltimer();
-  if (tb.R <= kWarpIngestMaxRows) warp_ingest(tb, st, removed, root_mode, smem);
-  else dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
-  __syncthreads();
-  if (t0) ts[1] = globaltimer();
-  __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout, s_pre;
-  __shared__ uint64_t s_warp[kSmallTPB / 32];
-  if (t0) {
-    s_go = !(c->skip | c->noop | c->fail_fast);
-    s_pre = c->skip ? -5 : c->fail_fast ? 1 : c->noop ? 2 : 0;   // status known before the update (2: no-op)
-    s_L = c->L;
-    s_nrows = c->nrows;
-    s_ident = c->identity;
-    s_par = c->parity;
+  const int R = tb.R;
+  const bool onchip = R <= kWarpIngestMaxRows;   // lists, residues and flags in shared memory
+  __shared__ SmallSh sh;
+  char *ext = reinterpret_cast<char *>(smem) + small_region_bytes(tb.n, tb.Wd);
+  int32_t *s_res = reinterpret_cast<int32_t *>(ext) + 2 * R;
+  uint8_t *s_sup = reinterpret_cast<uint8_t *>(s_res + R);
+  if (t0) c->tph[0] = globaltimer();   // phase stamps straight to the state (no registers held)
+  // everything the later phases need from the state is requested now, in
+  // flight while warp 0 ingests: the residues, and each thread's first entry
+  // of both index buffers (the parity is not known yet)
+  int pid0a = -1, pid0b = -1;
+  if (onchip) {
+    sh.ulist = reinterpret_cast<int32_t *>(ext);
+    sh.items = sh.ulist + R;
+    for (int r = tid; r < R; r += kSmallTPB) {
+      s_res[r] = st.res[r];
+      s_sup[r] = 0;
+    }
+    if (tid < tb.W2) {
+      pid0a = st.idx0[tid];
+      pid0b = st.idx1[tid];
+    }
+    if (tb.R <= kWarpIngestMaxRows) warp_ingest(tb, st, removed, root_mode, smem, nullptr, &sh);
+  } else {
+    dev_ingest<kSmallTPB>(tb, st, removed, root_mode, smem);
   }
   __syncthreads();
-  // ---- update + compaction (Alg. 2), all in this block
+  if (t0) c->tph[1] = globaltimer();
+  __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout, s_pre, s_nitems;
+  __shared__ uint64_t s_warp[kSmallTPB / 32];
+  if (t0) {
+    if (onchip) {
+      s_go = !(sh.skip | sh.noop | sh.fail);
+      s_pre = sh.skip ? -5 : sh.fail ? 1 : sh.noop ? 2 : 0;   // status known before the update (2: no-op)
+      s_L = sh.L;
+      s_nrows = sh.nrows;
+      s_ident = sh.ident;
+      s_par = sh.par;
+      s_nitems = sh.nitems;
+    } else {
+      s_go = !(c->skip | c->noop | c->fail_fast);
+      s_pre = c->skip ? -5 : c->fail_fast ? 1 : c->noop ? 2 : 0;
+      s_L = c->L;
+      s_nrows = c->nrows;
+      s_ident = c->identity;
+      s_par = c->parity;
+      s_nitems = c->nitems;
+    }
+  }
+  __syncthreads();
+  // ---- update + compaction (Alg. 2), all in this block; every listed row's
+  // words are loaded together with the block's currTable word (one round trip)
   if (s_go) {
-    const int Lout = block_update<kSmallTPB>(tb, st, s_L, s_nrows, s_ident, s_par, s_warp);
+    const int Lout = onchip ? block_update<kSmallTPB, 8>(tb, st, s_L, s_nrows, s_ident, s_par, s_warp, sh.ulist,
+                                                          s_par ? pid0b : pid0a)
+                            : block_update<kSmallTPB>(tb, st, s_L, s_nrows, s_ident, s_par, s_warp);
     if (t0) {
       c->L_out = Lout;
       s_Lout = Lout;
     }
   }
   __syncthreads();
-  if (t0) ts[2] = globaltimer();
-  // ---- filter (Alg. 3 L3, residues L220): a warp per item, full scan on a miss
+  if (t0) c->tph[2] = globaltimer();
+  // ---- filter (Alg. 3 L3, residues L220): residue probes of every item at
+  // once (rows and residues from shared memory: one round trip), then a warp
+  // per miss over the new index
   if (s_go) {
     const int Lout = s_Lout;
-    if (t0) st.sup[tb.R] = Lout > 0;
+    if (t0) st.sup[R] = Lout > 0;
     if (Lout > 0) {
       const bool compact = tb.use_index != 0;
       const int32_t *__restrict__ idx = compact ? (s_par ? st.idx0 : st.idx1) : nullptr;
       const int L = compact ? Lout : tb.W2;
       const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-      const int nitems = c->nitems;
+      const int nitems = s_nitems;
       uint32_t n_loads = 0;
-      for (int item = warp; item < nitems; item += kSmallTPB / 32) {
-        const int row = st.items[item];
-        const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
-        if (tb.use_res) {
-          int hit = 0;
-          if (lane == 0) {
-            const int r = st.res[row];
+      if (onchip) {
+        // thread i probes item i's residue
+        for (int i = tid; i < nitems; i += kSmallTPB) {
+          const int row = sh.items[i];
+          const int r = s_res[row];
+          bool hit = false;
+          if (tb.use_res) {
             const ulonglong2 t = T2[r];
-            const ulonglong2 s2 = ld_sup2(srow + 2 * (int64_t)r);
+            const ulonglong2 s2 = ld_sup2(tb.S + (int64_t)row * tb.Wp + 2 * (int64_t)r);
             hit = ((t.x & s2.x) | (t.y & s2.y)) != 0;
           }
-          if (__shfl_sync(0xffffffffu, hit, 0)) {
-            if (lane == 0) st.sup[row] = 1;
-            continue;
+          s_sup[row] = hit ? 1 : 0;
+        }
+        __syncthreads();
+        for (int item = warp; item < nitems; item += kSmallTPB / 32) {
+          const int row = sh.items[item];
+          if (s_sup[row]) continue;
+          const int hit = scan_pairs(idx, T2, tb.S + (int64_t)row * tb.Wp, 0, L, nullptr, lane, n_loads);
+          if (lane == 0 && hit >= 0) {
+            s_sup[row] = 1;
+            st.res[row] = hit;
           }
         }
-        const int hit = scan_pairs(idx, T2, srow, 0, L, nullptr, lane, n_loads);
-        if (lane == 0 && hit >= 0) {
-          st.sup[row] = 1;
-          st.res[row] = hit;
+        __syncthreads();
+        if (!with_finalize)   // sharded: k_finalize reads the flags after the combine
+          for (int i = tid; i < nitems; i += kSmallTPB) st.sup[sh.items[i]] = s_sup[sh.items[i]];
+      } else {
+        for (int item = warp; item < nitems; item += kSmallTPB / 32) {
+          const int row = st.items[item];
+          const uint64_t *__restrict__ srow = tb.S + (int64_t)row * tb.Wp;
+          if (tb.use_res) {
+            int hit = 0;
+            if (lane == 0) {
+              const int r = st.res[row];
+              const ulonglong2 t = T2[r];
+              const ulonglong2 s2 = ld_sup2(srow + 2 * (int64_t)r);
+              hit = ((t.x & s2.x) | (t.y & s2.y)) != 0;
+            }
+            if (__shfl_sync(0xffffffffu, hit, 0)) {
+              if (lane == 0) st.sup[row] = 1;
+              continue;
+            }
+          }
+          const int hit = scan_pairs(idx, T2, srow, 0, L, nullptr, lane, n_loads);
+          if (lane == 0 && hit >= 0) {
+            st.sup[row] = 1;
+            st.res[row] = hit;
+          }
         }
       }
       if (lane == 0 && n_loads) atomicAdd(&c->scan_loads, (unsigned long long)n_loads);
     }
   }
   __syncthreads();
-  if (t0) {
-    ts[3] = ts[4] = globaltimer();
-  }
+  if (t0) c->tph[3] = c->tph[4] = globaltimer();
   if (!with_finalize) {
-    if (t0) {
-      ts[5] = ts[4];
-      for (int i = 0; i < 8; ++i) c->tph[i] = ts[i < 6 ? i : 5];
-    }
+    if (t0) c->tph[5] = c->tph[6] = c->tph[7] = c->tph[4];
     return;
   }
   if (use_state_out) {
@@ -1421,11 +1524,9 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
     out_status = reinterpret_cast<int32_t *>(st.out);
   }
   const int status = s_pre == 2 ? 0 : s_pre != 0 ? s_pre : (s_Lout > 0 ? 0 : 1);
-  small_finalize<kSmallTPB>(tb, st, status, s_pre == 2, s_Lout, out_dom, out_pruned, out_status, smem);
-  if (t0) {
-    ts[5] = globaltimer();
-    for (int i = 0; i < 8; ++i) c->tph[i] = ts[i < 6 ? i : 5];
-  }
+  small_finalize<kSmallTPB>(tb, st, status, s_pre == 2, s_Lout, out_dom, out_pruned, out_status, smem,
+                            onchip ? s_sup : nullptr);
+  if (t0) c->tph[5] = c->tph[6] = c->tph[7] = globaltimer();
 }
 
 // ------------------------------------------------------------------ state copies (backtracking)

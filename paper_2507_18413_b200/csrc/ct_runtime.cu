@@ -116,7 +116,7 @@ struct ct_table {
   std::vector<Mark> marks;
   int upd_occ = 1, scan_occ = 1;
   int use_fused = 1, fused_grid = 1, fused_occ = 1, coop = 1, fused_grid_override = 0, use_small = 0;
-  size_t fused_smem = 0;
+  size_t fused_smem = 0, small_smem = 0;
   int use_fast = 0, fast_grid = 1;   // k_fast (ct_fast.cuh): tables with R <= kLocalRowsMax
   size_t fast_smem = 0;
   int use_wide = 0;                  // k_wide + k_wide_filter (ct_wide.cuh): many rows, few words
@@ -414,7 +414,7 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
   } else if (tb->use_small) {
     const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
     const int e = prof_event(tb, st);
-    k_small<<<1, kSmallTPB, tb->fused_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode,
+    k_small<<<1, kSmallTPB, tb->small_smem, st>>>(tb->dev, (const StateDev *)s->d_desc, removed, root_mode,
                                                   fin_inside, out_dom, out_pruned, out_status, use_state_out);
     CUDA_TRY(cudaGetLastError());
     prof_mark(tb, 7, e, st);
@@ -787,8 +787,9 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     int occ = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused, kFusedTPB, tb->fused_smem));
     if (occ < 1) tb->use_fused = 0;
-    CUDA_TRY(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)std::max<size_t>(tb->fused_smem, 1)));
+    tb->small_smem = small_smem_bytes(n, tb->Wd, (int)R);
+    if (tb->small_smem <= 200 * 1024)
+      CUDA_TRY(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->small_smem));
     tb->fused_occ = std::max(occ, 1);
   }
   tb->scan_occ = std::max(1, tb->scan_occ);
@@ -931,6 +932,7 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
       tb->use_small = 0;
     }
   }
+  if (tb->use_small && tb->small_smem > 200 * 1024) tb->use_small = 0;   // k_small's on-chip lists do not fit
 
   // gather filter (k_fast, ct_fast.cuh): the local tuples' value offsets, 8 or
   // 16 bits per cell, for tables whose filter may scan many support rows

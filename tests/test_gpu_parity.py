@@ -221,6 +221,7 @@ def test_config3_bulk_full_size(c3, fast):
             remd = torch.from_numpy(member_to_bitmap(rem, p.d).view(np.int64)).cuda()
             outd = torch.zeros(wd, dtype=torch.int64, device="cuda")
             sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()   # torch's copies / memsets run on its own stream, the call on the state's
             st.propagate_async(remd, outd, None, sd)
             st.synchronize()
             assert int(sd.item()) == (CT_OK if ok else CT_FAIL)
@@ -724,6 +725,7 @@ def _apply_virtual(states, wd):
         od = torch.zeros(max(wd, 1), dtype=torch.int64, device="cuda")
         pd = torch.zeros(max(wd, 1), dtype=torch.int64, device="cuda")
         sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
         C.ct_propagate_apply_async(st.handle, od, pd, sd)
         st.synchronize()
         outs.append((int(sd.item()), od.cpu().numpy().view(np.uint64)[:wd], pd.cpu().numpy().view(np.uint64)[:wd]))
@@ -776,6 +778,7 @@ def test_virtual_shards_one_gpu(G, path, kind):
         din = cur & (1 - r)
         ok, dout, _ = oracle_call(p, din)
         remd = torch.from_numpy(member_to_bitmap(r, p.d).view(np.int64)).cuda()
+        torch.cuda.synchronize()   # the H2D copy runs on torch's stream, the calls on the states' streams
         for st in states:
             C.ct_propagate_local_async(st.handle, remd)
         _combine_virtual(states)

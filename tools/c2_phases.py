@@ -40,3 +40,32 @@ print(json.dumps({"kernel_path": C.KERNEL_PATHS[tab.info.kernel_path],
                   "phase_p50_us": dict(zip(["ingest", "update", "probe", "scan", "finalize", "p5", "p6"], np.median(ph, 0).tolist())),
                   "phase_mean_us": dict(zip(["ingest", "update", "probe", "scan", "finalize", "p5", "p6"], ph.mean(0).tolist())),
                   "counters_mean": dict(zip(["L_in", "L_out", "rows", "items", "miss"], cnt.mean(0).tolist()))}))
+
+# the same walk with device-resident buffers (ct_propagate_async): the phase
+# times without the mapped host-memory read of the removals and the
+# system-scope fence of the synchronous path
+import torch
+rem_d = torch.zeros(wd, dtype=torch.int64, device="cuda")
+out_d = torch.zeros(wd, dtype=torch.int64, device="cuda")
+st_d = torch.zeros(1, dtype=torch.int32, device="cuda")
+st2 = tab.root.clone()
+rng = Rng(2, lanes=1)
+cur = root_m.copy()
+ph2 = []
+for k in range(600):
+    r = walk_removal(rng, cur, p.d)
+    if r is None:
+        st2.copy_from(tab.root); cur = root_m.copy(); continue
+    rem_d.copy_(torch.from_numpy(member_to_bitmap(r, p.d).view(np.int64)))
+    torch.cuda.synchronize()
+    st2.propagate_async(rem_d, out_d, None, st_d)
+    st2.synchronize()
+    if k >= 100:
+        ph2.append([v / 1e3 for v in st2.stats().phase_ns])
+    if int(st_d.cpu()[0]) == CT_OK:
+        cur = bitmap_to_member(out_d.cpu().numpy().view(np.uint64), p.d)
+    else:
+        st2.copy_from(tab.root); cur = root_m.copy()
+ph2 = np.array(ph2)
+print(json.dumps({"async_device_buffers": {"device_total_p50_us": float(np.median(ph2.sum(1))),
+                  "phase_p50_us": dict(zip(["ingest", "update", "probe", "scan", "finalize", "p5", "p6"], np.median(ph2, 0).tolist()))}}))
