@@ -156,10 +156,11 @@ def fix_patterns(root_member, d, count: int, seed: int = 12):
 WORKLOADS = {
     "c3bulk": dict(metric="propagations/s (C3 bulk ct_propagate, 1e7-tuple table)",
                    table="arity 8, domain 100, 1e7 tuples, seed 3",
-                   step="state restore (D2D) + ct_propagate_async of a bulk removal (50% of every var)"),
+                   step="ct_propagate_from_async(work, root) of a bulk removal (50% of every var); the root "
+                        "is only read, so a step needs no restore copy"),
     "c3b": dict(metric="propagations/s (C3b banded ct_propagate, filter-heavy, 1e7-tuple table)",
                 table="banded arity 8, domain 100, 1e7 tuples, seed 4 (x_i = (x0*c_i + u_i) mod 100, u_i < 10)",
-                step="state restore (D2D) + ct_propagate_async fixing x0 to one seeded value "
+                step="ct_propagate_from_async(work, root) fixing x0 to one seeded value "
                      "(630 unsupported values -> full filter scans)"),
 }
 
@@ -432,10 +433,12 @@ def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
     status = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
     work = tab.root.clone()
     stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
+    torch.cuda.synchronize()   # the tensors above were filled on torch's stream
 
     def step(k):
-        work.copy_from(tab.root)
-        work.propagate_async(rem_dev[k % P], out_dom, out_pr, status)
+        # one call from the root into the work state (ct_propagate_from_async:
+        # the root is only read, so no restore copy per step)
+        work.propagate_from_async(tab.root, rem_dev[k % P], out_dom, out_pr, status)
 
     # per-pattern work counters (deterministic; untimed) and the SURVEY §8(d)
     # algorithmic bytes from the call's inputs/outputs (active words before /
@@ -549,7 +552,7 @@ def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
                ms_per_step=step_ms, build_s=build_s, roofline=roofline, clocks=clk, per_pat=per_pat,
                kernel_ms={k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()},
                kernel_share=k_ms_per_launch / step_ms,
-               launches=sum(v[0] for k, v in prof.items() if k != "combine") + args.steps,   # + k_state_copy per step
+               launches=sum(v[0] for k, v in prof.items() if k != "combine"),
                phase_ns=[int(x) for x in phases])
     if full:
         out["e2e"] = measure_c3_e2e(tab, work, rem_host, P, wd, args, world)
@@ -586,15 +589,13 @@ def measure_c3_e2e(tab, work, rem_host, P, wd, args, world):
     ptrs = [(h_rem[k].data_ptr(), h_dom[k].data_ptr(), h_pr[k].data_ptr(), h_st[k].data_ptr())
             for k in range(e2e_steps)]   # raw pinned addresses: no per-call tensor marshalling
     for k in range(5):
-        work.copy_from(tab.root)
-        work.propagate_async(*ptrs[k])
+        work.propagate_from_async(tab.root, *ptrs[k])
     work.synchronize()
     h_st.fill_(-1)
     barrier(world)
     t1 = time.perf_counter()
     for k in range(e2e_steps):
-        work.copy_from(tab.root)
-        work.propagate_async(*ptrs[k])
+        work.propagate_from_async(tab.root, *ptrs[k])
     t_enq = time.perf_counter() - t1
     work.synchronize()
     n_ok = int((h_st >= 0).sum())
@@ -604,8 +605,9 @@ def measure_c3_e2e(tab, work, rem_host, P, wd, args, world):
     e2e_s = max_over_ranks(t2 - t1, world)
     return {"value": e2e_steps / e2e_s, "unit": "propagations/s", "h2d_bytes_per_step": 8 * wd,
             "d2h_bytes_per_step": 4 + 16 * wd, "steps": e2e_steps,
-            "api": "ct_propagate_async on pinned host buffers (removal DMA'd in, status/domains/pruned "
-                   "written to host memory by the kernel), calls pipelined, every status checked on the host",
+            "api": "ct_propagate_from_async(work, root) on pinned host buffers (removal DMA'd in, status/"
+                   "domains/pruned written to host memory by the kernel), calls pipelined, every status checked "
+                   "on the host",
             "host_enqueue_us_per_step": t_enq / e2e_steps * 1e6,
             "sync_call": {"value": e2e_steps / e2e_sync_s, "unit": "propagations/s",
                           "api": "ct_propagate (host buffers, pinned staging, CUDA graph, waits per call)",
@@ -631,8 +633,7 @@ def sharded_overhead(m, args, dev):
 
     def run(n):
         for k in range(n):
-            w.copy_from(tab.root)
-            w.propagate_async(rem_dev[k % P], od, None, sd)
+            w.propagate_from_async(tab.root, rem_dev[k % P], od, None, sd)
 
     run(args.warmup)
     w.synchronize()

@@ -235,6 +235,18 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
 ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
                              uint64_t *out_pruned, int32_t *out_status);
 
+/* The same call with the input taken from another state of the table: dst
+ * becomes the result of propagating `removed` from src (src is only read), as
+ * ct_state_copy(dst, src) + ct_propagate_async(dst, ...) would produce, in
+ * one pass: on the k_fast launch shape (ct_table_info.kernel_path 2) the
+ * update reads src's currTable and index and writes dst's, so the restore of a
+ * search node costs no separate copy (the solver's trail, PAPER.md L276,
+ * L312); other shapes copy first.  dst == src is ct_propagate_async.  Buffers
+ * and status as ct_propagate_async; dst's stream waits for src's earlier
+ * work, src's stream waits for the call. */
+ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint64_t *removed,
+                                  uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status);
+
 /* Tuple-range sharding with a caller-side combine (n_shards > 1 and no NCCL id,
  * or for testing several shards on one device).  local: phases a2-a6 on this
  * shard's words, leaving R+1 flag bytes (per support row: "supported by a valid

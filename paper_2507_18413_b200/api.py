@@ -101,6 +101,11 @@ class State:
         st = C.ct_propagate(self.handle, rem, out, pruned, wd=wd)
         return (st, out[:wd], pruned[:wd]) if st == C.CT_OK else (st, None, None)
 
+    def propagate_from_async(self, src: "State", removed, out_dom=None, out_pruned=None, out_status=None):
+        """This state := `src` propagated with `removed` (ct_propagate_from_async)."""
+        C.ct_propagate_from_async(self.handle, src.handle, removed, out_dom, out_pruned, out_status,
+                                  wd=self.table.Wd)
+
     def propagate_async(self, removed, out_dom=None, out_pruned=None, out_status=None):
         C.ct_propagate_async(self.handle, removed, out_dom, out_pruned, out_status, wd=self.table.Wd)
 

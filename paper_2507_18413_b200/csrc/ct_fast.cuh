@@ -81,6 +81,9 @@ struct FastShT {
   int dead, fail, noop, go, ngroups, nrows, nitems;
   int L, ident, par, Lout, nscan, last, below, anymiss;
   uint32_t nvalid;               // valid tuples of this CTA's blocks after the update
+  const StateDev *in;            // the call's INPUT state (the state itself, or the source of ct_propagate_from)
+  int from;                      // 1: input and output states differ
+  long long calls;               // the input state's call count
   int red[NW];                   // block-reduction scratch
   uint32_t woff[NW];
   uint64_t scan[NW];
@@ -243,8 +246,11 @@ __device__ __forceinline__ int fast_block_sum(int v, FastSh &fs) {
 // CTA's shared memory; `writer` (block 0) also publishes the per-call state.
 template <int NT = kFastTPB>
 __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_t *__restrict__ rem, int root_mode,
-                           const FastPtrs &p, FastShT<NT / 32> &fs, bool writer, const uint64_t *gdom = nullptr) {
+                           const FastPtrs &p, FastShT<NT / 32> &fs, bool writer, const uint64_t *gdom = nullptr,
+                           const StateDev *src = nullptr) {
   Ctl *c = st.ctl;
+  const StateDev &in = src ? *src : st;   // ct_propagate_from: read the source, write st
+  const Ctl *ci = in.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = tb.n, Wd = tb.Wd, R = tb.R;
   // the first domain word of this thread is loaded before anything waits, so
@@ -252,20 +258,23 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   uint64_t dm0 = 0, rm0 = 0;
   int x0 = 0;
   if (tid < Wd) {
-    dm0 = st.dom[tid];
+    dm0 = in.dom[tid];
     // model tables: a value is removed iff the shared (global) domain lost it
     rm0 = gdom ? ~__ldcg(gdom + tb.gword[tid]) : (rem ? rem[tid] : 0ull);
     x0 = tb.wordVar[tid];
   }
   if (tid == 0) {
-    fs.dead = c->dead;
+    fs.dead = ci->dead;
     fs.fail = 0;
     fs.ngroups = 0;
     fs.anymiss = 0;
     fs.nvalid = 0;
-    fs.L = c->L;
-    fs.ident = c->identity;
-    fs.par = c->parity;
+    fs.L = ci->L;
+    fs.ident = ci->identity;
+    fs.par = ci->parity;
+    fs.in = &in;
+    fs.from = src != nullptr;
+    fs.calls = ci->calls;
     fs.cnt[0] = fs.cnt[1] = fs.cnt[2] = 0;
   }
   for (int i = tid; i <= n; i += NT) {
@@ -290,10 +299,20 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   if (writer) {   // sup[0..R] = 0, 16 bytes per store (sup is 256-byte aligned)
     uint4 *s4 = reinterpret_cast<uint4 *>(st.sup);
     for (int r = tid; r < (R + 16) / 16; r += NT) s4[r] = make_uint4(0u, 0u, 0u, 0u);
+    if (src) {   // the residues and the persistent control fields start as the source's
+      for (int r = tid; r < R; r += NT) st.res[r] = in.res[r];
+      if (tid == 0) {
+        c->dead = ci->dead;
+        c->parity = ci->parity;
+        c->identity = ci->identity;
+        c->L = ci->L;
+        c->calls = ci->calls;
+      }
+    }
   }
   // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
   for (int k = tid; k < Wd; k += NT) {
-    const uint64_t dm = k == tid ? dm0 : st.dom[k];
+    const uint64_t dm = k == tid ? dm0 : in.dom[k];
     const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
     const int x = k == tid ? x0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
@@ -430,11 +449,12 @@ __device__ __forceinline__ uint32_t fast_update_entry(const TableDev &tb, const 
                                                   const uint32_t *__restrict__ ulist, int k, uint32_t &n_loads,
                                                   uint32_t &n_writes) {
   const int nrows = fs.nrows;
-  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  const StateDev &in = *fs.in;
+  const int32_t *__restrict__ idx_in = fs.par ? in.idx1 : in.idx0;
   ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
   const int64_t Wp = tb.Wp;
   const int pid = fs.ident ? k : idx_in[k];
-  const ulonglong2 tw = T2[pid];
+  const ulonglong2 tw = reinterpret_cast<const ulonglong2 *>(in.T)[pid];
   const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
   uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
   int p0 = 0;
@@ -466,11 +486,36 @@ __device__ __forceinline__ uint32_t fast_update_entry(const TableDev &tb, const 
   }
   n_loads += 2 * min(p0, nrows);   // rows issued before the block died or the list ended
   const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
-  if (nt.x != tw.x || nt.y != tw.y) {
+  if (nt.x != tw.x || nt.y != tw.y || fs.from) {
     T2[pid] = nt;
     ++n_writes;
   }
   return (uint32_t)(__popcll(nt.x) + __popcll(nt.y));
+}
+
+// ct_propagate_from: blocks outside the source's index are zero in the source
+// but stale in the output, so each CTA zeroes the gaps between its own index
+// entries (the last CTA with entries also after the last one; rank 0 all of
+// them when the index is empty): disjoint ranges, no barrier.
+__device__ __forceinline__ void fast_zero_gaps(const TableDev &tb, const StateDev &st, const FastSh &fs, int k_lo,
+                                               int k_hi, int rank) {
+  ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+  const ulonglong2 z = make_ulonglong2(0ull, 0ull);
+  const int W2 = tb.W2, L = fs.L;
+  const bool last = (k_lo < k_hi && k_hi == L) || (L == 0 && rank == 0);
+  if (fs.ident) {   // entries 0..L-1
+    if (last)
+      for (int b = L + threadIdx.x; b < W2; b += blockDim.x) T2[b] = z;
+    return;
+  }
+  const int32_t *__restrict__ idx = fs.par ? fs.in->idx1 : fs.in->idx0;
+  for (int k = k_lo + threadIdx.x; k < k_hi; k += blockDim.x) {
+    const int prev = k == 0 ? -1 : idx[k - 1];
+    const int cur = idx[k];
+    for (int b = prev + 1; b < cur; ++b) T2[b] = z;
+  }
+  if (last)
+    for (int b = (L > 0 ? idx[L - 1] + 1 : 0) + threadIdx.x; b < W2; b += blockDim.x) T2[b] = z;
 }
 
 // ------------------------------------------------------------------ a4: index entries of one CTA's range
@@ -480,7 +525,7 @@ __device__ __forceinline__ void fast_compact_range(const TableDev &tb, const Sta
                                                    int k_hi) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  const int32_t *__restrict__ idx_in = fs.par ? fs.in->idx1 : fs.in->idx0;
   int32_t *__restrict__ idx_out = fs.par ? st.idx0 : st.idx1;
   int below = fs.below;
   for (int base = k_lo; base < k_hi; base += kFastTPB) {
@@ -527,7 +572,7 @@ __device__ void fast_gather_range(const TableDev &tb, const StateDev &st, const 
   for (int k = tid; k < Wd; k += kFastTPB) mark[k] = 0;
   __syncthreads();
   const ulonglong2 *__restrict__ T2 = reinterpret_cast<const ulonglong2 *>(st.T);
-  const int32_t *__restrict__ idx_in = fs.par ? st.idx1 : st.idx0;
+  const int32_t *__restrict__ idx_in = fs.par ? fs.in->idx1 : fs.in->idx0;
   const int cw = tb.cell_words, bits = tb.cell_bits, per = 32 / bits;
   const uint32_t cmask = (1u << bits) - 1u;
   // per thread: its entries' valid tuples in batches of kGatherBatch, every
@@ -663,6 +708,8 @@ __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, in
 __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
                             uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
                             int32_t *__restrict__ out_status, bool sys_fence) {
+  // ct_propagate_from: the output state's persistent fields are the input's,
+  // advanced by this call (in place this is the same as updating them)
   constexpr int NT = kFastTPB;
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, Wd = tb.Wd;
@@ -673,9 +720,9 @@ __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPt
   else status = fs.Lout > 0 ? 0 : 1;     // currTable empty <=> FAIL (Alg. 1 L5)
   if (status != 0) {
     if (tid == 0) {
-      if (status == 1) {
+      if (status == 1 || fs.from) {   // a dead source leaves a dead output
         c->dead = 1;
-        c->calls += 1;
+        c->calls = fs.calls + (status == 1 ? 1 : 0);
       }
       c->last_status = status;
       if (out_status) *out_status = status;
@@ -710,11 +757,16 @@ __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPt
   if (tid == 0) {
     if (sys_fence) __threadfence_system();
     if (!fs.noop && tb.use_index) {
-      c->parity ^= 1;
+      c->parity = fs.par ^ 1;
       c->L = fs.Lout;
       c->identity = 0;
+    } else if (fs.from) {   // the source's index (copied by fast_call) and geometry
+      c->parity = fs.par;
+      c->L = fs.L;
+      c->identity = fs.ident;
     }
-    c->calls += 1;
+    if (fs.from) c->dead = 0;
+    c->calls = fs.calls + 1;
     c->last_status = 0;
     if (out_status) *out_status = 0;
   }
@@ -738,14 +790,15 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
                                          const uint64_t *__restrict__ removed, const uint64_t *gdom, int root_mode,
                                          int with_finalize, uint64_t *__restrict__ out_dom,
                                          uint64_t *__restrict__ out_pruned, int32_t *__restrict__ out_status,
-                                         int use_state_out, const int rank, const int G) {
+                                         int use_state_out, const int rank, const int G,
+                                         const StateDev *src = nullptr) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool t0 = rank == 0 && tid == 0;
   int fstatus = kNotFinalizer;
   // phase timestamps of rank 0 go straight to tph[] (no registers held)
   if (t0) c->tph[0] = globaltimer();
-  cta_ingest(tb, st, removed, root_mode, p, fs, rank == 0, gdom);
+  cta_ingest(tb, st, removed, root_mode, p, fs, rank == 0, gdom, src);
   if (t0) {
     const unsigned long long t = globaltimer();
     for (int i = 1; i < 6; ++i) c->tph[i] = t;
@@ -775,6 +828,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
         nv = warp_sum_u32(nv);
         if (lane == 0) atomicAdd(&fs.nvalid, nv);
       }
+      if (fs.from) fast_zero_gaps(tb, st, fs, k_lo, k_hi, rank);
     }
     // update work counters now, while CTAs still finish at different times,
     // reduced per CTA first: when every CTA finishes its (short) update at
@@ -831,7 +885,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
     const int Lout = fs.Lout;
     const bool compact = tb.use_index != 0;
     const int32_t *__restrict__ idx = compact ? (fs.par ? st.idx0 : st.idx1) : nullptr;
-    const int32_t *__restrict__ idx_old = fs.ident ? nullptr : (fs.par ? st.idx1 : st.idx0);
+    const int32_t *__restrict__ idx_old = fs.ident ? nullptr : (fs.par ? fs.in->idx1 : fs.in->idx0);
     const int Ls = compact ? Lout : tb.W2;
     const bool may_miss = fs.L > kSelfRounds * kFirstScanFast;   // the probe cannot cover the index
     if (t0) st.sup[tb.R] = Lout > 0;
@@ -1014,6 +1068,20 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
     if (t0) c->tph[5] = globaltimer();
     // scan work counter, one atomic per CTA
     cta_count(lane == 0 ? f_loads : 0u, &c->scan_loads, fs);
+  } else if (fs.from && fs.noop) {
+    // ct_propagate_from with nothing to propagate: the output becomes a copy of
+    // the source (its index entries and their blocks, the gaps zeroed)
+    const int ts = (fs.L + G - 1) / G;
+    const int k_lo = min(fs.L, rank * ts), k_hi = min(fs.L, k_lo + ts);
+    const StateDev &in = *fs.in;
+    const int32_t *__restrict__ idx_in = fs.par ? in.idx1 : in.idx0;
+    int32_t *__restrict__ idx_out = fs.par ? st.idx1 : st.idx0;
+    for (int k = k_lo + tid; k < k_hi; k += kFastTPB) {
+      const int pid = fs.ident ? k : idx_in[k];
+      reinterpret_cast<ulonglong2 *>(st.T)[pid] = reinterpret_cast<const ulonglong2 *>(in.T)[pid];
+      if (!fs.ident) idx_out[k] = pid;
+    }
+    fast_zero_gaps(tb, st, fs, k_lo, k_hi, rank);
   }
 
   // ---- completion: the last CTA to get here finalizes
@@ -1051,14 +1119,18 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
                                                    const uint64_t *__restrict__ removed, int root_mode,
                                                    int with_finalize, uint64_t *__restrict__ out_dom,
                                                    uint64_t *__restrict__ out_pruned,
-                                                   int32_t *__restrict__ out_status, int use_state_out) {
+                                                   int32_t *__restrict__ out_status, int use_state_out,
+                                                   const StateDev *__restrict__ src_state) {
   extern __shared__ __align__(16) uint64_t smem[];
   __shared__ FastSh fs;
-  __shared__ StateDev s_st;   // the state's pointers live in shared memory, not in 30 registers
-  if (threadIdx.x == 0) s_st = states[0];
+  __shared__ StateDev s_st, s_src;   // the states' pointers live in shared memory, not in registers
+  if (threadIdx.x == 0) {
+    s_st = states[0];
+    if (src_state) s_src = src_state[0];
+  }
   __syncthreads();
   fast_call(tb, s_st, fs, fast_ptrs(smem, tb), removed, nullptr, root_mode, with_finalize, out_dom, out_pruned,
-            out_status, use_state_out, (int)blockIdx.x, (int)gridDim.x);
+            out_status, use_state_out, (int)blockIdx.x, (int)gridDim.x, src_state ? &s_src : nullptr);
 }
 
 }  // namespace ctk

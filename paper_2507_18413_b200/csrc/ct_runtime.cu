@@ -382,10 +382,16 @@ static ct_status enqueue_neg(ct_table *tb, ct_state *s, const uint64_t *removed,
 // One single-state call.  Fused: one cooperative launch runs every phase (the
 // finalize phase too unless the flags must first be combined across shards);
 // otherwise one kernel per phase.  local_only stops before the combine.
+// src (ct_propagate_from): the call's input state; the output is s.  k_fast
+// reads src and writes s directly; every other launch shape copies first.
 static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *removed, int root_mode,
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
-                                bool local_only) {
+                                bool local_only, const ct_state *src = nullptr) {
   cudaStream_t st = s->stream;
+  if (src && !(tb->use_fast && !tb->use_wide && !tb->use_small && tb->kind != CT_TABLE_NEGATIVE)) {
+    CT_TRY(launch_state_copy(tb, s->mem, src->mem, st));
+    src = nullptr;
+  }
   if (tb->kind == CT_TABLE_NEGATIVE) {   // ct_neg.cuh: shared ingest + update, counting filter
     CT_TRY(enqueue_neg(tb, s, removed, root_mode, out_dom, out_pruned, out_status, use_state_out));
     return CT_OK;
@@ -433,7 +439,8 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     lc.numAttrs = 1;
     const int e = prof_event(tb, st);
     CUDA_TRY(cudaLaunchKernelEx(&lc, k_fast, tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
-                                out_dom, out_pruned, out_status, use_state_out));
+                                out_dom, out_pruned, out_status, use_state_out,
+                                src ? (const StateDev *)src->d_desc : (const StateDev *)nullptr));
     prof_mark(tb, 6, e, st);
     if (fin_inside || local_only) return CT_OK;
   } else if (tb->use_fused) {
@@ -1135,6 +1142,32 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
     }
   }
   return enqueue_single(tb, s, removed, 0, out_dom, out_pruned, out_status, 0, false);
+}
+
+ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint64_t *removed, uint64_t *out_dom,
+                                  uint64_t *out_pruned, int32_t *out_status) {
+  if (!dst || !src) return fail(CT_EINVAL, "NULL state");
+  if (dst == src) return ct_propagate_async(dst, removed, out_dom, out_pruned, out_status);
+  ct_table *tb = dst->tb;
+  if (src->tb != tb) return fail(CT_ESTATE, "states belong to different tables");
+  if (tb->n_shards > 1 && !tb->comm)
+    return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
+  if (src->pending || dst->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine and apply first");
+  DeviceGuard g(tb->device);
+  CT_TRY(order_after(dst->stream, src->stream));   // src's earlier work first
+  if (removed && tb->Wd) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, removed) != cudaSuccess) {
+      cudaGetLastError();
+      a.type = cudaMemoryTypeUnregistered;
+    }
+    if (a.type == cudaMemoryTypeUnregistered || a.type == cudaMemoryTypeHost) {
+      CUDA_TRY(cudaMemcpyAsync(dst->h.slot, removed, (size_t)tb->Wd * 8, cudaMemcpyHostToDevice, dst->stream));
+      removed = dst->h.slot;
+    }
+  }
+  CT_TRY(enqueue_single(tb, dst, removed, 0, out_dom, out_pruned, out_status, 0, false, src));
+  return order_after(const_cast<ct_state *>(src)->stream, dst->stream);   // src's next writes wait for the call
 }
 
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {

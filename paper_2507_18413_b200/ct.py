@@ -115,6 +115,7 @@ SIGNATURES = {
     "ct_propagate": (I32, [P, P, P, P]),
     "ct_propagate_async": (I32, [P, P, P, P, P]),
     "ct_propagate_local_async": (I32, [P, P]),
+    "ct_propagate_from_async": (I32, [P, P, P, P, P, P]),
     "ct_state_flags": (I32, [P, P, P]),
     "ct_propagate_apply_async": (I32, [P, P, P, P]),
     "ct_state_clone": (I32, [P, P]),
@@ -337,6 +338,16 @@ def ct_propagate_async(state, removed, out_dom=None, out_pruned=None, out_status
             _need_dev_words(nm, a, wd)
     return _check(lib().ct_propagate_async(state, _dev_ptr(removed), _dev_ptr(out_dom), _dev_ptr(out_pruned),
                                            _dev_ptr(out_status)), allow_fail=False)
+
+
+def ct_propagate_from_async(dst, src, removed, out_dom=None, out_pruned=None, out_status=None,
+                            wd: int | None = None) -> int:
+    """dst := src propagated with `removed` (include/ct.h); device or pinned buffers, enqueue only."""
+    if wd is not None:
+        for nm, a in (("removed", removed), ("out_dom", out_dom), ("out_pruned", out_pruned)):
+            _need_dev_words(nm, a, wd)
+    return _check(lib().ct_propagate_from_async(dst, src, _dev_ptr(removed), _dev_ptr(out_dom), _dev_ptr(out_pruned),
+                                                _dev_ptr(out_status)), allow_fail=False)
 
 
 def ct_propagate_local_async(state, removed) -> int:

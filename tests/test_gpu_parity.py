@@ -16,6 +16,7 @@ from paper_2507_18413_b200 import ct as C
 from workloads import (Rng, random_table, banded_table, table1, member_to_bitmap, bitmap_to_member,
                        bulk_removal, fix_one_value_removal)
 from workloads.layout import bits_to_bool, dom_word_offsets
+from workloads.policies import walk_removal
 
 pytestmark = pytest.mark.gpu
 
@@ -805,4 +806,80 @@ def test_nccl_single_rank_path(path):
     nid = C.ct_nccl_unique_id()
     tab = make(p, n_shards=1, shard_rank=0, nccl_unique_id=nid, **PATHS[path])
     run_walk(tab, p, calls=150, seed=4, check_table_every=10)
+    tab.close()
+
+
+# --------------------------------------------------------------------------- ct_propagate_from_async
+FROM_SHAPES = {"fast": dict(_grid_fused=True), "fast_scan": dict(_grid_fused=True, use_gather=False),
+               "fast_noindex": dict(_grid_fused=True, use_index=False), "v1": dict(_grid_fused=True, _fast=False),
+               "small": dict()}
+
+
+@pytest.mark.parametrize("shape", list(FROM_SHAPES))
+def test_propagate_from_walk(shape):
+    """dst := src propagated (one pass on k_fast, copy + call elsewhere): a
+    search-like walk where every call starts from a saved state and the result
+    becomes the next source (so sources carry stale blocks outside their index
+    only if the gap zeroing is wrong); domains, pruned sets and the whole
+    currTable vs the oracle, the source unchanged, a no-op call from a source,
+    and a batch seeded from a propagated state."""
+    import torch
+    p = banded_table(5, 30, 150_001, seed=9, band=6)
+    tab = make(p, **FROM_SHAPES[shape])
+    ok, root_m, _ = oracle_call(p, np.ones(p.R, np.uint8))
+    assert ok
+    wd = tab.Wd
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+    out = torch.zeros(wd, dtype=torch.int64, device="cuda")
+    pr = torch.zeros(wd, dtype=torch.int64, device="cuda")
+    sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+    states = [tab.root.clone(), tab.root.clone()]
+    src, cur = tab.root, root_m.copy()
+    rng = Rng(21, lanes=1)
+    nfrom = 0
+    for k in range(40):
+        r = walk_removal(rng, cur, p.d)
+        if r is None:
+            src, cur = tab.root, root_m.copy()
+            continue
+        dst = states[k % 2] if states[k % 2] is not src else states[(k + 1) % 2]
+        before = src.read_table().copy()
+        din = cur & (1 - r)
+        okk, dout, valid = oracle_call(p, din, want_valid=True)
+        remd = dev(member_to_bitmap(r, p.d))
+        torch.cuda.synchronize()
+        dst.propagate_from_async(src, remd, out, pr, sd)
+        dst.synchronize()
+        src.synchronize()
+        assert int(sd.item()) == (CT_OK if okk else CT_FAIL), k
+        assert np.array_equal(src.read_table(), before), k          # the source is only read
+        if okk:
+            assert np.array_equal(bitmap_to_member(out.cpu().numpy().view(np.uint64), p.d), dout), k
+            assert np.array_equal(bitmap_to_member(pr.cpu().numpy().view(np.uint64), p.d), din & (1 - dout)), k
+            assert np.array_equal(bits_to_bool(dst.read_table(), p.t), valid), k
+            src, cur = dst, dout
+            nfrom += 1
+        else:
+            src, cur = tab.root, root_m.copy()
+    assert nfrom > 10
+    # a no-op call from a propagated source is a copy of it
+    if src is not tab.root:
+        dst = states[0] if states[0] is not src else states[1]
+        torch.cuda.synchronize()
+        dst.propagate_from_async(src, dev(np.zeros(wd, np.uint64)), out, pr, sd)
+        dst.synchronize()
+        assert int(sd.item()) == CT_OK
+        assert np.array_equal(dst.read_table(), src.read_table())
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), src.read_dom())
+        # batches read every block: a batch seeded from a propagated state
+        b = tab.batch(4, init=dst)
+        rems = [walk_removal(rng, cur, p.d) for _ in range(4)]
+        rems = [x if x is not None else np.zeros(p.R, np.uint8) for x in rems]
+        st_b, doms = b.propagate(np.stack([member_to_bitmap(x, p.d) for x in rems]))
+        for s in range(4):
+            okk, dout, _ = oracle_call(p, cur & (1 - rems[s]))
+            assert st_b[s] == (CT_OK if okk else CT_FAIL), s
+            if okk:
+                assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), s
+        b.close()
     tab.close()
