@@ -673,7 +673,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.cuda.current_device()
     wl = WORKLOADS[args.workload]
-    m = measure_c3(args.workload, args, dev, world, rank, full=True)
+    m = measure_c3(args.workload, args, dev, world, rank, full=True, use_gather=not args.no_gather)
     p, root_m, pats = m["p"], m["root_m"], m["pats"]
     latency = filt = shov = None
     cpu = None
@@ -1358,6 +1358,7 @@ def main():
     ap.add_argument("--skip-filter", action="store_true", help="default line: no C3b filter sub-object")
     ap.add_argument("--skip-sharded", action="store_true", help="default line: no sharded-path overhead probe")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-gather", action="store_true", help="c3bulk/c3b: Alg. 3 scans only (ct_config.use_gather = 0)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
