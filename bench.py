@@ -1240,13 +1240,14 @@ def run_f4(args, kind):
     prof = C.ct_table_profile_read(tab.handle, reset=True)
     C.ct_table_profile(tab.handle, False)
     peak, peak_src = peaks()
-    if kind == "short":
+    if kind == "short" or C.KERNEL_PATHS.get(tab.info.kernel_path) == "k_fast":
         kname, slot = "ctk::" + C.KERNEL_PATHS.get(tab.info.kernel_path, "k_fast"), "fused"
         if not prof.get("fused", (0, 0))[0]:
             slot = "small"
         b = [8 * c["upd"] + 16 * c["L_in"] + 16 * c["writes"] + 8 * c["filt"] + 32 * c["gathered"] +
              4 * (c["L_in"] + c["L_out"]) for c in per_pat]
-        model = ("counted: 8 x support words loaded (update + filter) + 16 B per index entry read / block "
+        model = ("counted: 8 x support words loaded (update + filter: residue scans / gathered cells for short "
+                 "tables, the counting filter's rows for negative ones) + 16 B per index entry read / block "
                  "rewritten + 4 B index entries + 32 B per gathered tuple")
     else:
         kname, slot = "ctk::k_neg_count", "scan"

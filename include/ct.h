@@ -105,7 +105,19 @@ typedef struct ct_config {
                               /*    the tuples as 8/16-bit value offsets, t x n cells)   */
                               /*    instead of scanning supports rows (Alg. 3), when that */
                               /*    reads fewer bytes; 0: always scan.  Same results.    */
+  /* Launch-shape controls (tests and ablations; results never change):        */
+  int32_t launch_shape;       /* CT_SHAPE_*: force the single-state launch shape; a    */
+                              /*    table that does not fit it gets the automatic one   */
+                              /*    (ct_table_info.kernel_path tells which runs)         */
+  int32_t grid_override;      /* > 0: CTAs of the cooperative single-state kernels and  */
+                              /*    of the model kernels (fewer CTAs than tiles/tables) */
+  int32_t batch_per_state;    /* 1: ct_propagate_many runs the per-state phase kernels  */
+                              /*    instead of the tile-major batch update              */
+  int32_t search_levels;      /* > 0: trail depth of the device-resident DFS (models);  */
+                              /*    a deeper search falls back to the host driver       */
 } ct_config;
+enum { CT_SHAPE_AUTO = 0, CT_SHAPE_PHASES = 1, CT_SHAPE_FUSED = 2, CT_SHAPE_FAST = 3, CT_SHAPE_SMALL = 4,
+       CT_SHAPE_WIDE = 5 };
 
 /* Fill *cfg with defaults: device 0, NULL stream, default allocator, 1 shard,
  * CT_POLICY_AUTO, residues, index, graphs and the fused kernel on. */
@@ -351,7 +363,7 @@ ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, i
  * fixpoints and backtracking stay on the GPU; falls back to the host driver if
  * the trail would exceed 512 levels or the model has a push pending), 1 =
  * host-driven (one fixpoint launch per node).  Identical results and node
- * traces; ct_model_search uses driver 0 (environment CT_HOST_DFS=1: 1).
+ * traces; ct_model_search uses driver 0.
  * device_ms is then the whole kernel's time. */
 ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
                              int32_t driver, int32_t *out_solution, ct_search_stats *out_stats);

@@ -84,6 +84,7 @@ struct FastShT {
   const StateDev *in;            // the call's INPUT state (the state itself, or the source of ct_propagate_from)
   int from;                      // 1: input and output states differ
   long long calls;               // the input state's call count
+  unsigned long long nbound;     // negative tables: the input's valid forbidden tuples (bounds this call's)
   int red[NW];                   // block-reduction scratch
   uint32_t woff[NW];
   uint64_t scan[NW];
@@ -275,6 +276,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     fs.in = &in;
     fs.from = src != nullptr;
     fs.calls = ci->calls;
+    fs.nbound = ci->nvalid;
     fs.cnt[0] = fs.cnt[1] = fs.cnt[2] = 0;
   }
   for (int i = tid; i <= n; i += NT) {
@@ -312,8 +314,13 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
   }
   // Δ_x = removed ∧ dom, D_x = dom ∧ ¬removed, sizes (Alg. 1 L1-2)
   for (int k = tid; k < Wd; k += NT) {
-    const uint64_t dm = k == tid ? dm0 : in.dom[k];
-    const uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
+    uint64_t dm = k == tid ? dm0 : in.dom[k];
+    uint64_t rm = k == tid ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
+    if (tb.negative) {   // values the last filter pruned leave currTable now (ct_neg.cuh's pend)
+      const uint64_t pd = in.pend[k];
+      dm |= pd;
+      rm |= pd;
+    }
     const int x = k == tid ? x0 : tb.wordVar[k];
     const uint64_t delta = rm & dm, di = dm & ~rm;
     p.din[k] = di;
@@ -337,6 +344,31 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
     }
   }
   __syncthreads();
+  if (tb.negative) {
+    // count rows (ct_neg.cuh): the values of x are counted iff P_x = prod_{y != x}
+    // |D_y| <= the input's |V| (which bounds this call's); vfl bit 2
+    const unsigned long long B = fs.nbound;
+    for (int x = tid; x < n; x += NT) {
+      unsigned long long P = 1;   // saturates at B + 1
+      for (int y = 0; y < n; ++y) {
+        if (y == x) continue;
+        const unsigned long long cy = (unsigned long long)p.cs[y];
+        if (cy == 0) {
+          P = 0;
+          break;
+        }
+        if (P > B / cy) {
+          P = B + 1;
+          break;
+        }
+        P *= cy;
+      }
+      if (P <= B) p.vfl[x] |= 4;
+    }
+    if (writer)
+      for (int r = tid; r < R; r += NT) st.cnt[r] = 0;   // read after the first grid barrier
+    __syncthreads();
+  }
   const bool fail = fs.fail != 0;
   const bool noop = (fs.ngroups == 0) && !root_mode;
   int nrows = 0, nitems = 0;
@@ -350,7 +382,7 @@ __device__ void cta_ingest(const TableDev &tb, const StateDev &st, const uint64_
       if (k < Wd) {
         const int x = p.wvar[k], fl = p.vfl[x];
         const uint64_t b = (fl & 2) ? ((fl & 1) ? p.dl[k] : p.din[k]) : 0ull;
-        const uint64_t it = p.cs[x] > 1 ? p.din[k] : 0ull;
+        const uint64_t it = (tb.negative ? (fl & 4) != 0 : p.cs[x] > 1) ? p.din[k] : 0ull;
         p.bw[k] = b;
         p.iw[k] = it;
         cu = __popcll(b);
@@ -774,6 +806,95 @@ __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPt
 }
 
 
+// The finalize of a negative table on the k_fast path (ct_neg.cuh's
+// k_neg_finalize from this CTA's shared memory): (x, a) leaves the domain iff
+// its count of valid forbidden tuples reached P_x = prod_{y != x} |D_y|; FAIL
+// iff a domain empties; the pruned values are kept in `pend` so the next call
+// removes their tuples; |V| = the CTAs' popcounts (tcnt[G + j]).
+__device__ int cta_finalize_neg(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
+                                uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
+                                int32_t *__restrict__ out_status, bool sys_fence, int G) {
+  constexpr int NT = kFastTPB;
+  Ctl *c = st.ctl;
+  const int tid = threadIdx.x, Wd = tb.Wd, n = tb.n;
+  __shared__ int s_empty;
+  int status = fs.dead ? -5 : (fs.fail ? 1 : 0);
+  uint64_t *s_nd = p.dl;
+  unsigned long long *s_P = reinterpret_cast<unsigned long long *>(p.iw);   // [n] (n <= Wd; free after the ingest)
+  for (int k = tid; k < Wd; k += NT) s_nd[k] = p.din[k];
+  if (tid == 0) s_empty = 0;
+  __syncthreads();
+  if (status == 0 && !fs.noop) {
+    for (int x = tid; x < n; x += NT) {   // exact for the counted variables (P_x <= |V| < 2^63)
+      unsigned long long P = 1;
+      for (int y = 0; y < n; ++y)
+        if (y != x) P = (P > (1ull << 62) / max(1, p.cs[y])) ? (1ull << 62) : P * (unsigned long long)p.cs[y];
+      s_P[x] = P;
+    }
+    __syncthreads();
+    for (int i = tid; i < fs.nitems; i += NT) {
+      const int r = p.items[i];
+      const int x = row_var(p.rb, n, r);
+      if (__ldcg(st.cnt + r) >= s_P[x]) {   // every assignment of D with x = a is forbidden
+        const int a = r - p.rb[x];
+        smem_clear_bit(s_nd + p.dof[x] + (a >> 6), a & 63);
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < n; x += NT) {
+      uint64_t any = 0;
+      for (int w = p.dof[x]; w < p.dof[x + 1]; ++w) any |= s_nd[w];
+      if (!any) s_empty = 1;
+    }
+    __syncthreads();
+    if (s_empty) status = 1;
+  }
+  if (status != 0) {
+    if (tid == 0) {
+      if (status == 1 || fs.from) {
+        c->dead = 1;
+        c->calls = fs.calls + (status == 1 ? 1 : 0);
+      }
+      c->last_status = status;
+      if (out_status) *out_status = status;
+    }
+    return status;
+  }
+  for (int k = tid; k < Wd; k += NT) {
+    const uint64_t nd = s_nd[k], di = p.din[k];
+    st.dom[k] = nd;
+    st.pend[k] = di & ~nd;
+    if (out_dom) out_dom[k] = nd;
+    if (out_pruned) out_pruned[k] = di & ~nd;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (!fs.noop) {
+      const uint32_t *tcnt = reinterpret_cast<const uint32_t *>(st.tilestat);
+      unsigned long long nv = 0;
+      for (int j = 0; j < G; ++j) nv += __ldcg(tcnt + G + j);
+      c->nvalid = nv;
+    } else if (fs.from) {
+      c->nvalid = fs.nbound;
+    }
+    if (sys_fence) __threadfence_system();
+    if (!fs.noop && tb.use_index) {
+      c->parity = fs.par ^ 1;
+      c->L = fs.Lout;
+      c->identity = 0;
+    } else if (fs.from) {
+      c->parity = fs.par;
+      c->L = fs.L;
+      c->identity = fs.ident;
+    }
+    if (fs.from) c->dead = 0;
+    c->calls = fs.calls + 1;
+    c->last_status = 0;
+    if (out_status) *out_status = 0;
+  }
+  return 0;
+}
+
 // ------------------------------------------------------------------ k_fast
 // Cooperative launch (all CTAs co-resident), kFastTPB threads, dynamic smem
 // fast_smem_bytes(n, Wd, R).  with_finalize = 0 for sharded tables (the flags are
@@ -824,7 +945,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
         kept += __syncthreads_count(cnt != 0);
       }
       if (tid == 0) tcnt[rank] = (uint32_t)kept;
-      if (tb.cells) {
+      if (tb.cells || tb.negative) {
         nv = warp_sum_u32(nv);
         if (lane == 0) atomicAdd(&fs.nvalid, nv);
       }
@@ -873,10 +994,50 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
         if (rank == 0) c->L_out = tot;
       }
     }
-    if (tb.cells && tid == 0) {   // this CTA's valid tuples -> the grid's (read after the probe barrier)
+    if ((tb.cells || tb.negative) && tid == 0) {   // this CTA's valid tuples -> the grid's (read later)
       tcnt[G + rank] = (uint32_t)fs.nvalid;
     }
     __syncthreads();
+    if (tb.negative) {
+      // ---- counting filter of a negative table (ct_neg.cuh): cnt[row] += popc(T & S[row])
+      // over this CTA's own update range (blocks its own threads just wrote),
+      // per-row partial sums in shared memory, one global atomic per row
+      uint32_t *s_cnt = p.ulist;   // [nitems] (free after the update)
+      for (int i = tid; i < fs.nitems; i += kFastTPB) s_cnt[i] = 0;
+      __syncthreads();
+      const int32_t *__restrict__ idx_in = fs.par ? fs.in->idx1 : fs.in->idx0;
+      const int nit = fs.nitems;
+      for (int base = k_lo; base < k_hi; base += kFastTPB) {
+        const int k = base + tid;
+        int pid = 0;
+        ulonglong2 t = make_ulonglong2(0ull, 0ull);
+        if (k < k_hi) {
+          pid = fs.ident ? k : idx_in[k];
+          t = T2[pid];
+        }
+        const bool any = (t.x | t.y) != 0;
+        for (int i = 0; i < nit; i += 4) {
+          ulonglong2 a[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            a[q] = (any && i + q < nit) ? ld_sup2(tb.S + (int64_t)p.items[i + q] * tb.Wp + 2 * (int64_t)pid)
+                                        : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t cq = __reduce_add_sync(0xffffffffu, (uint32_t)(__popcll(t.x & a[q].x) + __popcll(t.y & a[q].y)));
+            if (lane == 0 && cq) atomicAdd(&s_cnt[i + q], cq);
+          }
+        }
+        if (any) f_loads += 2 * nit;
+      }
+      __syncthreads();
+      for (int i = tid; i < nit; i += kFastTPB)
+        if (s_cnt[i]) atomicAdd(st.cnt + p.items[i], (unsigned long long)s_cnt[i]);
+      if (tb.use_index) fast_compact_range(tb, st, fs, k_lo, k_hi);
+      if (t0) c->tph[3] = c->tph[4] = c->tph[5] = globaltimer();
+      cta_count(f_loads, &c->scan_loads, fs);
+      goto completion;
+    }
 
     // ---- probe (a6a): residue + up to kSelfRounds rounds over the pre-update index.
     // Item i goes to CTA i % G; when there are few items per CTA, wpi warps of
@@ -1103,7 +1264,8 @@ finalize:
       out_pruned = st.out + 1 + tb.Wd;
       out_status = reinterpret_cast<int32_t *>(st.out);
     }
-    fstatus = cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
+    fstatus = tb.negative ? cta_finalize_neg(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0, G)
+                          : cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
   }
   if (tid == 0) c->tph[7] = globaltimer();
   if (compact_after) {   // the leader's own index entries, after the outputs

@@ -81,6 +81,7 @@ struct TableDev {
                             // each, packed LSB-first (the gather filter of k_fast, ct_fast.cuh)
   int32_t cell_bits;        // 8 or 16
   int32_t cell_words;       // uint32 words per tuple
+  int32_t negative;         // 1: a negative table (f4) on the k_fast path: counting filter (ct_fast.cuh)
   const int32_t *domOnly;   // [n] or nullptr: 1 if x's column has a star cell (short tables, f4), so the
                             // Δ-branch (which drops every tuple whose row has a removed value) is unsound
                             // for x: a star tuple is in every row of x and must survive
@@ -1358,7 +1359,10 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
 // kSmallTPB threads, separated by __syncthreads instead of grid barriers, and
 // the compaction is a plain block scan (no look-back).  Same phase semantics
 // as k_fused; with_finalize = 0 for sharded tables.
-constexpr int kSmallTPB = 1024;
+#ifndef CT_SMALL_TPB
+#define CT_SMALL_TPB 1024
+#endif
+constexpr int kSmallTPB = CT_SMALL_TPB;   // experiment builds: -DCT_SMALL_TPB=256|512
 constexpr int kWarpIngestMaxRows = 1024;   // k_small ingests with one warp up to this many support rows
 constexpr int kSmallMaxPairs = 8192;
 

@@ -392,7 +392,7 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     CT_TRY(launch_state_copy(tb, s->mem, src->mem, st));
     src = nullptr;
   }
-  if (tb->kind == CT_TABLE_NEGATIVE) {   // ct_neg.cuh: shared ingest + update, counting filter
+  if (tb->kind == CT_TABLE_NEGATIVE && !tb->use_fast) {   // ct_neg.cuh: shared ingest + update, counting filter
     CT_TRY(enqueue_neg(tb, s, removed, root_mode, out_dom, out_pruned, out_status, use_state_out));
     return CT_OK;
   }
@@ -742,9 +742,10 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
   tb->use_res = cfg.use_residues ? 1 : 0;
   tb->use_index = cfg.use_index ? 1 : 0;
   tb->use_graph = cfg.use_graph ? 1 : 0;
-  tb->use_fused = (cfg.use_fused && kind != CT_TABLE_NEGATIVE) ? 1 : 0;   // negative: ct_neg.cuh's kernels
-  if (const char *ev = getenv("CT_FUSED_COOP")) tb->coop = atoi(ev) ? 1 : 0;   // experiment knob
-  if (const char *ev = getenv("CT_FUSED_GRID")) tb->fused_grid_override = atoi(ev);
+  tb->use_fused = cfg.use_fused ? 1 : 0;   // negative tables: k_fast's counting mode, else ct_neg.cuh's kernels
+  if (cfg.launch_shape < 0 || cfg.launch_shape > CT_SHAPE_WIDE) return fail(CT_EINVAL, "bad launch_shape");
+  if (cfg.launch_shape == CT_SHAPE_PHASES) tb->use_fused = 0;
+  tb->fused_grid_override = std::max(0, cfg.grid_override);
   tb->n_shards = cfg.n_shards;
   tb->rank = cfg.shard_rank;
   if (cfg.alloc) {
@@ -870,7 +871,7 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
   // k_fast: per-CTA ingest lists in shared memory (tables with few support rows)
   {
     int fast_ok = (tb->use_fused && tb->R <= kLocalRowsMax) ? 1 : 0;
-    if (const char *ev = getenv("CT_NO_FAST")) fast_ok = fast_ok && !atoi(ev);
+    if (cfg.launch_shape == CT_SHAPE_FUSED) fast_ok = 0;
     if (fast_ok) {
       tb->fast_smem = fast_smem_bytes(n, tb->Wd, tb->R);
       CUDA_TRY(cudaFuncSetAttribute(k_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->fast_smem));
@@ -890,7 +891,7 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
   // R rows of a tile of >= 8 blocks fit (ct_batch.cuh)
   {
     int legacy = 0;
-    if (const char *ev = getenv("CT_BATCH_LEGACY")) legacy = atoi(ev);
+    legacy = cfg.batch_per_state ? 1 : 0;
     const size_t cap = 200 * 1024;
     int tw = 0;
     if (!legacy && tb->R >= 1) {
@@ -924,14 +925,14 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
   // latency-bound tables: the whole call in one CTA (k_small)
   {
     int small_max = kSmallMaxPairs;
-    if (const char *ev = getenv("CT_SMALL_MAX_PAIRS")) small_max = atoi(ev);
+    if (cfg.launch_shape == CT_SHAPE_FUSED || cfg.launch_shape == CT_SHAPE_FAST) small_max = 0;
     tb->use_small = (tb->use_fused && dv.W2 <= small_max) ? 1 : 0;
   }
   // ... unless the filter dominates: many support rows over few words (k_wide)
   {
     int wide_ok = (tb->use_small && tb->R >= kWideMinRows) ? 1 : 0;
-    if (const char *ev = getenv("CT_NO_WIDE")) wide_ok = wide_ok && !atoi(ev);
-    if (const char *ev = getenv("CT_WIDE")) wide_ok = (tb->use_fused && dv.W2 <= kSmallMaxPairs && atoi(ev)) ? 1 : wide_ok;
+    if (cfg.launch_shape == CT_SHAPE_SMALL) wide_ok = 0;
+    if (cfg.launch_shape == CT_SHAPE_WIDE) wide_ok = (tb->use_fused && dv.W2 <= kSmallMaxPairs) ? 1 : wide_ok;
     tb->wide_smem = wide_smem_bytes(n, tb->Wd);
     if (wide_ok && tb->wide_smem <= 200 * 1024) {
       CUDA_TRY(cudaFuncSetAttribute(k_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->wide_smem));
@@ -940,6 +941,11 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     }
   }
   if (tb->use_small && tb->small_smem > 200 * 1024) tb->use_small = 0;   // k_small's on-chip lists do not fit
+  if (kind == CT_TABLE_NEGATIVE) {   // only k_fast has the counting filter; otherwise k_ingest .. k_neg_finalize
+    tb->use_small = tb->use_wide = 0;
+    if (!tb->use_fast) tb->use_fused = 0;
+    dv.negative = tb->use_fast;
+  }
 
   // gather filter (k_fast, ct_fast.cuh): the local tuples' value offsets, 8 or
   // 16 bits per cell, for tables whose filter may scan many support rows
@@ -1058,9 +1064,9 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->row_stride_words = t->Wp;
   o->device_bytes = (int64_t)(t->S_bytes + t->meta_bytes);
   o->state_bytes = (int64_t)t->lay.total;
-  o->kernel_path = t->kind == CT_TABLE_NEGATIVE ? 5 : t->use_wide ? 4 : t->use_small ? 3 : t->use_fast ? 2
-                  : t->use_fused ? 1 : 0;
-  o->grid = t->kind == CT_TABLE_NEGATIVE ? t->sm_count * t->neg_occ : t->use_wide ? 1 : t->use_small ? 1
+  const bool neg_kernels = t->kind == CT_TABLE_NEGATIVE && !t->use_fast;
+  o->kernel_path = neg_kernels ? 5 : t->use_wide ? 4 : t->use_small ? 3 : t->use_fast ? 2 : t->use_fused ? 1 : 0;
+  o->grid = neg_kernels ? t->sm_count * t->neg_occ : t->use_wide ? 1 : t->use_small ? 1
           : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   o->batch_tile = t->bt_tw;
   o->gather_cell_bits = t->cells ? t->dev.cell_bits : 0;
@@ -1134,9 +1140,8 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
       a.type = cudaMemoryTypeUnregistered;
     }
     // (pinned removals read in place by every CTA instead: C3 bulk e2e 8.7k vs
-    // 9.8k with the DMA; CT_HOST_ZERO_COPY=1 selects it for experiments)
-    static const bool zero_copy = getenv("CT_HOST_ZERO_COPY") != nullptr;
-    if (a.type == cudaMemoryTypeUnregistered || (a.type == cudaMemoryTypeHost && !zero_copy)) {
+    // 9.8k with the DMA)
+    if (a.type == cudaMemoryTypeUnregistered || a.type == cudaMemoryTypeHost) {
       CUDA_TRY(cudaMemcpyAsync(s->h.slot, removed, (size_t)tb->Wd * 8, cudaMemcpyHostToDevice, s->stream));
       removed = s->h.slot;
     }
@@ -1611,6 +1616,7 @@ ct_status ct_table_profile_read(ct_table *t, ct_kernel_times *out, int32_t reset
 // ================================================================== models (f1)
 struct ct_model {
   int device = 0;
+  int search_levels = 0;   // ct_config.search_levels
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int nv = 0, ntab = 0, Wg = 0;
@@ -1716,6 +1722,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
     return s;
   };
   m->device = cfg.device;
+  m->search_levels = cfg.search_levels;
   m->nv = n_vars;
   m->ntab = n_tables;
   m->vlo.assign(var_lo, var_lo + n_vars);
@@ -1737,6 +1744,8 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   cfg.stream = m->stream;
   cfg.use_graph = 0;
   cfg.alloc = nullptr;   // the model owns its memory (plain cudaMalloc)
+  const int model_grid = cfg.grid_override;
+  cfg.grid_override = 0;   // the model's grid, not the tables'
   // ---- tables (each built and propagated at its own root)
   std::vector<uint64_t> gdom(m->Wg, 0ull);
   for (int v = 0; v < n_vars; ++v)
@@ -1869,7 +1878,7 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   // over 148 arrivals is ~2 us cheaper than over 444 (C5: 82 -> 72 us/node)
   (void)tiles;
   m->grid = sms;
-  if (const char *e = getenv("CT_MODEL_GRID")) m->grid = std::max(1, std::min(sms * occ, atoi(e)));
+  if (model_grid > 0) m->grid = std::max(1, std::min(sms * occ, model_grid));
   if (cudaHostAlloc((void **)&m->h_in, (size_t)std::max(m->Wg, 1) * 8, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostAlloc((void **)&m->h_out, (size_t)(4 + m->Wg) * 8, cudaHostAllocMapped) != cudaSuccess ||
       cudaHostGetDevicePointer((void **)&m->d_in, m->h_in, 0) != cudaSuccess ||
@@ -2041,7 +2050,7 @@ static ct_status model_search_device(ct_model *m, int32_t value_order, int64_t m
     int64_t vals = 1;
     for (int v = 0; v < m->nv; ++v) vals += m->vd[v];
     m->levels = (int)std::min<int64_t>(kSearchMaxLevels, vals);
-    if (const char *ev = getenv("CT_SEARCH_LEVELS")) m->levels = std::max(2, std::min(m->levels, atoi(ev)));   // tests
+    if (m->search_levels > 0) m->levels = std::max(2, std::min(m->levels, m->search_levels));
     if (cudaMalloc(&m->snap_dev, (size_t)m->levels * pool16 * 16) != cudaSuccess) {
       cudaGetLastError();
       m->snap_dev = nullptr;
@@ -2121,9 +2130,7 @@ ct_status ct_model_search_phases(const ct_model *m, int64_t *out6) {
 
 ct_status ct_model_search(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,
                           int32_t *out_solution, ct_search_stats *out_stats) {
-  int driver = 0;
-  if (const char *ev = getenv("CT_HOST_DFS")) driver = atoi(ev) ? 1 : 0;
-  return ct_model_search_ex(m, value_order, max_nodes, max_solutions, driver, out_solution, out_stats);
+  return ct_model_search_ex(m, value_order, max_nodes, max_solutions, 0, out_solution, out_stats);
 }
 
 ct_status ct_model_search_ex(ct_model *m, int32_t value_order, int64_t max_nodes, int64_t max_solutions,

@@ -51,7 +51,12 @@ class ct_config(ctypes.Structure):
                 ("nccl_unique_id", ctypes.c_void_p),
                 ("update_policy", ctypes.c_int32), ("use_residues", ctypes.c_int32),
                 ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32),
-                ("use_fused", ctypes.c_int32), ("use_gather", ctypes.c_int32)]
+                ("use_fused", ctypes.c_int32), ("use_gather", ctypes.c_int32),
+                ("launch_shape", ctypes.c_int32), ("grid_override", ctypes.c_int32),
+                ("batch_per_state", ctypes.c_int32), ("search_levels", ctypes.c_int32)]
+
+CT_SHAPE_AUTO, CT_SHAPE_PHASES, CT_SHAPE_FUSED, CT_SHAPE_FAST, CT_SHAPE_SMALL, CT_SHAPE_WIDE = 0, 1, 2, 3, 4, 5
+SHAPES = {"auto": 0, "phases": 1, "fused": 2, "fast": 3, "small": 4, "wide": 5}
 
 
 class ct_table_info(ctypes.Structure):
@@ -247,7 +252,8 @@ class TorchAllocator:
 def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1, shard_rank: int = 0,
                 nccl_unique_id: bytes | None = None, update_policy: int = CT_POLICY_AUTO,
                 use_residues: bool = True, use_index: bool = True, use_graph: bool = True,
-                use_fused: bool = True, use_gather: bool = True):
+                use_fused: bool = True, use_gather: bool = True, launch_shape: int | str = 0,
+                grid_override: int = 0, batch_per_state: bool = False, search_levels: int = 0):
     cfg = ct_config()
     lib().ct_config_init(ctypes.byref(cfg))
     cfg.device = device
@@ -265,6 +271,10 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
     cfg.use_graph = int(bool(use_graph))
     cfg.use_fused = int(bool(use_fused))
     cfg.use_gather = int(bool(use_gather))
+    cfg.launch_shape = SHAPES[launch_shape] if isinstance(launch_shape, str) else int(launch_shape)
+    cfg.grid_override = int(grid_override)
+    cfg.batch_per_state = int(bool(batch_per_state))
+    cfg.search_levels = int(search_levels)
     return cfg, keep
 
 

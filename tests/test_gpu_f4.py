@@ -18,13 +18,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _make(p, kind, _grid_fused=False, **kw):
-    import os
     if _grid_fused:
-        os.environ["CT_SMALL_MAX_PAIRS"] = "0"
-    try:
-        return Table(p.lo, p.d, p.tuples, kind=kind, **kw)
-    finally:
-        os.environ.pop("CT_SMALL_MAX_PAIRS", None)
+        kw["launch_shape"] = "fast"
+    return Table(p.lo, p.d, p.tuples, kind=kind, **kw)
 
 
 def _oracle(kind, p, member):
@@ -136,8 +132,9 @@ def test_short_bulk_and_batch():
 
 
 NEG_KNOBS = [dict(), dict(update_policy=CT_POLICY_DOM), dict(update_policy=CT_POLICY_DELTA),
-             dict(use_index=False), dict(use_graph=False)]
-NEG_IDS = ["auto", "dom", "delta", "noindex", "nograph"]
+             dict(use_index=False), dict(use_graph=False), dict(launch_shape="phases"),
+             dict(launch_shape="phases", use_index=False), dict(launch_shape="fast", grid_override=3)]
+NEG_IDS = ["auto", "dom", "delta", "noindex", "nograph", "kernels", "kernels_noindex", "fast_grid3"]
 
 
 @pytest.mark.parametrize("knobs", NEG_KNOBS, ids=NEG_IDS)
@@ -148,6 +145,8 @@ def test_negative_walk_vs_oracle(shape, knobs):
     n, d, t = shape
     p = negative_table(n, d, t, seed=31 + t, lo=1)
     tab = _make(p, "negative", **knobs)
+    expect = "negative" if knobs.get("launch_shape") == "phases" else "k_fast"
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == expect
     fails, prunes = _walk(tab, p, "negative", 150, seed=8, m=1, q=0.3)
     assert prunes > 0
     tab.close()

@@ -13,8 +13,8 @@ from workloads.csp import csp_model
 pytestmark = pytest.mark.gpu
 
 
-def _model(m):
-    return Model(m["vlo"], m["vd"], m["scopes"], m["tables"])
+def _model(m, **cfg):
+    return Model(m["vlo"], m["vd"], m["scopes"], m["tables"], **cfg)
 
 
 def test_table1_model_first_solution():
@@ -114,17 +114,12 @@ def test_device_and_host_drivers_agree(seed):
 
 
 def test_device_search_falls_back_when_the_trail_is_short():
-    """A trail shorter than the search depth (CT_SEARCH_LEVELS, read when the
-    device search is first set up) makes the device driver stop and the host
-    driver rerun the search: same results as a plain host-driven search."""
-    import os
+    """A trail shorter than the search depth (ct_config.search_levels) makes
+    the device driver stop and the host driver rerun the search: same results
+    as a plain host-driven search."""
     m = csp_model(6, 5, 4, 40, seed=51, arities=[3, 3, 2, 4])
-    os.environ["CT_SEARCH_LEVELS"] = "3"
-    try:
-        M = _model(m)
-        a = M.search(value_order=0, max_solutions=0, driver="device")
-    finally:
-        os.environ.pop("CT_SEARCH_LEVELS", None)
+    M = _model(m, search_levels=3)
+    a = M.search(value_order=0, max_solutions=0, driver="device")
     b = M.search(value_order=0, max_solutions=0, driver="host")
     ref = oracle_dfs(m["vlo"], m["vd"], m["scopes"], m["tables"], value_order=0, max_solutions=0)
     assert b[2].max_depth > 2                      # the trail was too short for this tree
@@ -136,17 +131,11 @@ def test_device_search_falls_back_when_the_trail_is_short():
 
 @pytest.mark.parametrize("grid", [1, 3])
 def test_model_grid_smaller_than_table_count(grid):
-    """Model kernels on fewer CTAs than tables (CT_MODEL_GRID, read at model
-    creation): one CTA ingests / finalizes several tables, so its barrier
-    arrival carries several tables' verdicts.  Fixpoints and the DFS trace vs
-    the oracle."""
-    import os
+    """Model kernels on fewer CTAs than tables (ct_config.grid_override): one
+    CTA ingests / finalizes several tables, so its barrier arrival carries
+    several tables' verdicts.  Fixpoints and the DFS trace vs the oracle."""
     m = csp_model(10, 8, 6, 400, seed=91, arities=[3, 4, 2, 5, 3, 4])
-    os.environ["CT_MODEL_GRID"] = str(grid)
-    try:
-        M = _model(m)
-    finally:
-        os.environ.pop("CT_MODEL_GRID", None)
+    M = _model(m, grid_override=grid)
     ok, root = oracle.fixpoint(m["vlo"], m["vd"], m["scopes"], m["tables"], np.ones(int(m["vd"].sum()), np.uint8))
     assert (M.root_status == CT_OK) == ok
     if ok:

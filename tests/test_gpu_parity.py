@@ -47,25 +47,20 @@ def _built():
 
 def make(p, _grid_fused=False, _fast=True, _grid=0, _wide=None, **kw):
     """_grid_fused: force a cooperative multi-CTA kernel even for tables small
-    enough for the single-CTA one; _fast=False: the barrier-per-phase k_fused
-    instead of k_fast; _wide=True/False: force / forbid the k_wide shape (all
-    environment knobs are read at create time)."""
-    import os
+    enough for the single-CTA one (ct_config.launch_shape); _fast=False: the
+    barrier-per-phase k_fused instead of k_fast; _grid: fewer CTAs than tiles
+    (grid_override); _wide=True/False: force / forbid the k_wide shape."""
     if _grid_fused:
-        os.environ["CT_SMALL_MAX_PAIRS"] = "0"
-    if not _fast:
-        os.environ["CT_NO_FAST"] = "1"
-    if _grid:
-        os.environ["CT_FUSED_GRID"] = str(_grid)   # fewer CTAs than tiles: several tiles per CTA
+        kw.setdefault("launch_shape", "fast" if _fast else "fused")
+    elif not _fast:
+        kw.setdefault("launch_shape", "fused")
     if _wide is True:
-        os.environ["CT_WIDE"] = "1"
+        kw.setdefault("launch_shape", "wide")
     elif _wide is False:
-        os.environ["CT_NO_WIDE"] = "1"
-    try:
-        return Table(p.lo, p.d, p.tuples, **kw)
-    finally:
-        for k in ("CT_SMALL_MAX_PAIRS", "CT_NO_FAST", "CT_FUSED_GRID", "CT_WIDE", "CT_NO_WIDE"):
-            os.environ.pop(k, None)
+        kw.setdefault("launch_shape", "small")
+    if _grid:
+        kw["grid_override"] = _grid   # several tiles per CTA
+    return Table(p.lo, p.d, p.tuples, **kw)
 
 
 # --------------------------------------------------------------------------- a1 supports builder
@@ -540,21 +535,11 @@ BATCH_SHAPES = {
     "tinyR": (3, 7, 5_000 + 13, 1),
     "oneblock": (4, 6, 100, 0),
 }
-BATCH_PATHS = {"tiled": {}, "legacy": {"CT_BATCH_LEGACY": "1"}}
+BATCH_PATHS = {"tiled": {}, "legacy": {"batch_per_state": True}}
 
 
-def make_env(p, env, **kw):
-    import os
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        return make(p, **kw)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+def make_env(p, cfg, **kw):
+    return make(p, **cfg, **kw)
 
 
 def batch_walk(tab, p, S, steps, seed, check_table=False, from_states=None):
@@ -606,9 +591,7 @@ def test_batch_matches_oracle(shape, path):
     p = random_table(n, d, t, seed=5, lo=lo)
     tab = make_env(p, BATCH_PATHS[path])
     tw = {"c4like": 32, "tw16": 16, "tw8": 8, "perstate": 0, "tinyR": 32, "oneblock": 32}[shape]
-    import os
-    if not os.environ.get("CT_BATCH_LEGACY"):
-        assert tab.info.batch_tile == (tw if path == "tiled" else 0)
+    assert tab.info.batch_tile == (tw if path == "tiled" else 0)
     batch_walk(tab, p, S=67, steps=10, seed=1000, check_table=(shape in ("c4like", "tinyR", "oneblock")))
     tab.close()
 

@@ -61,9 +61,7 @@ def main():
     if "fast" in which:
         p = banded_table(6, 60, 300_000, seed=4)
         for g in (True, False):
-            os.environ["CT_SMALL_MAX_PAIRS"] = "0"
-            t = Table(p.lo, p.d, p.tuples, use_gather=g)
-            os.environ.pop("CT_SMALL_MAX_PAIRS")
+            t = Table(p.lo, p.d, p.tuples, use_gather=g, launch_shape="fast")
             root = bitmap_to_member(t.root_dom, p.d)
             st = t.root.clone()
             rng = Rng(3)
@@ -81,11 +79,7 @@ def main():
         print("fast ok", flush=True)
     if "fused" in which:
         p = random_table(4, 30, 200_000, seed=6)
-        os.environ["CT_SMALL_MAX_PAIRS"] = "0"
-        os.environ["CT_NO_FAST"] = "1"
-        t = Table(p.lo, p.d, p.tuples)
-        os.environ.pop("CT_SMALL_MAX_PAIRS")
-        os.environ.pop("CT_NO_FAST")
+        t = Table(p.lo, p.d, p.tuples, launch_shape="fused")
         walk(t, p, 10, 7)
         t.close()
         print("fused ok", flush=True)
