@@ -1195,8 +1195,7 @@ def run_f4(args, kind):
     torch.cuda.synchronize()   # the tensors above were filled on torch's stream
 
     def step(k):
-        work.copy_from(tab.root)
-        work.propagate_async(rem_dev[k % P], out_dom, out_pr, status)
+        work.propagate_from_async(tab.root, rem_dev[k % P], out_dom, out_pr, status)
 
     # parity of the first pattern (untimed)
     step(0)
@@ -1268,7 +1267,7 @@ def run_f4(args, kind):
                 "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded, workloads.%s_table)" % kind,
                 "config": {"workload": kind if kind == "short" else "neg", "table": desc,
-                           "step": "state restore (D2D) + ct_propagate_async of a bulk removal (50 % of every var)",
+                           "step": "ct_propagate_from_async(work, root) of a bulk removal (50 % of every var)",
                            "patterns": P, "parallelism": "1 GPU" if world == 1 else f"{world} replicas",
                            "kernel_path": C.KERNEL_PATHS.get(tab.info.kernel_path), "build_s": round(build_s, 3),
                            "l2": "inputs larger than L2"},

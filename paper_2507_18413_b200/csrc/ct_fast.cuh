@@ -1007,28 +1007,45 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
       __syncthreads();
       const int32_t *__restrict__ idx_in = fs.par ? fs.in->idx1 : fs.in->idx0;
       const int nit = fs.nitems;
-      for (int base = k_lo; base < k_hi; base += kFastTPB) {
-        const int k = base + tid;
-        int pid = 0;
-        ulonglong2 t = make_ulonglong2(0ull, 0ull);
-        if (k < k_hi) {
-          pid = fs.ident ? k : idx_in[k];
-          t = T2[pid];
+      // a warp holds 32 x kNegE of the range's blocks in registers (lane l:
+      // entries l, l + 32, ...) and streams the rows i = warp, warp + 8, ...
+      // over them, two rows' loads in flight; row i belongs to one warp, so
+      // its partial sum is a plain shared-memory update
+      constexpr int kNegE = 8;
+      for (int base = k_lo; base < k_hi; base += 32 * kNegE) {
+        int pid[kNegE];
+        ulonglong2 t[kNegE];
+#pragma unroll
+        for (int j = 0; j < kNegE; ++j) {
+          const int k = base + 32 * j + lane;
+          pid[j] = k < k_hi ? (fs.ident ? k : idx_in[k]) : -1;
+          t[j] = pid[j] >= 0 ? T2[pid[j]] : make_ulonglong2(0ull, 0ull);
+          if (pid[j] >= 0 && (t[j].x | t[j].y) == 0) pid[j] = -1;   // a dead block loads no row
         }
-        const bool any = (t.x | t.y) != 0;
-        for (int i = 0; i < nit; i += 4) {
-          ulonglong2 a[4];
+        for (int i = warp; i < nit; i += 2 * kFastWarps) {
+          const int i2 = i + kFastWarps;
+          const uint64_t *__restrict__ r0 = tb.S + (int64_t)p.items[i] * tb.Wp;
+          const uint64_t *__restrict__ r1 = tb.S + (int64_t)p.items[i2 < nit ? i2 : i] * tb.Wp;
+          ulonglong2 a[kNegE], b[kNegE];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            a[q] = (any && i + q < nit) ? ld_sup2(tb.S + (int64_t)p.items[i + q] * tb.Wp + 2 * (int64_t)pid)
-                                        : make_ulonglong2(0ull, 0ull);
+          for (int j = 0; j < kNegE; ++j) {
+            a[j] = pid[j] >= 0 ? ld_sup2(r0 + 2 * (int64_t)pid[j]) : make_ulonglong2(0ull, 0ull);
+            b[j] = (pid[j] >= 0 && i2 < nit) ? ld_sup2(r1 + 2 * (int64_t)pid[j]) : make_ulonglong2(0ull, 0ull);
+          }
+          uint32_t ca = 0, cb = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t cq = __reduce_add_sync(0xffffffffu, (uint32_t)(__popcll(t.x & a[q].x) + __popcll(t.y & a[q].y)));
-            if (lane == 0 && cq) atomicAdd(&s_cnt[i + q], cq);
+          for (int j = 0; j < kNegE; ++j) {
+            ca += __popcll(t[j].x & a[j].x) + __popcll(t[j].y & a[j].y);
+            cb += __popcll(t[j].x & b[j].x) + __popcll(t[j].y & b[j].y);
+            if (pid[j] >= 0) f_loads += i2 < nit ? 4 : 2;
+          }
+          ca = __reduce_add_sync(0xffffffffu, ca);
+          cb = __reduce_add_sync(0xffffffffu, cb);
+          if (lane == 0) {
+            s_cnt[i] += ca;
+            if (i2 < nit) s_cnt[i2] += cb;
           }
         }
-        if (any) f_loads += 2 * nit;
       }
       __syncthreads();
       for (int i = tid; i < nit; i += kFastTPB)

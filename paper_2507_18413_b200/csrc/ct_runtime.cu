@@ -388,7 +388,7 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
                                 bool local_only, const ct_state *src = nullptr) {
   cudaStream_t st = s->stream;
-  if (src && !(tb->use_fast && !tb->use_wide && !tb->use_small && tb->kind != CT_TABLE_NEGATIVE)) {
+  if (src && !(tb->use_fast && !tb->use_wide && !tb->use_small)) {
     CT_TRY(launch_state_copy(tb, s->mem, src->mem, st));
     src = nullptr;
   }

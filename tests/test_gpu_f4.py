@@ -203,3 +203,47 @@ def test_negative_bulk_large():
             assert np.array_equal(bitmap_to_member(dom, p.d), dout), k
             assert int(np.unpackbits(st.read_table().view(np.uint8)).sum()) == nv, k
     tab.close()
+
+
+@pytest.mark.parametrize("kind", ["short", "negative"])
+def test_propagate_from_f4(kind):
+    """ct_propagate_from_async on short and negative tables (k_fast reads the
+    source, writes the output; the negative table's pending prunes travel with
+    the source): a chain of calls, each from the previous output, vs the oracle."""
+    import torch
+    if kind == "short":
+        p = short_table(4, 30, 70_001, seed=11, p_star=0.01)
+    else:
+        p = negative_table(3, 60, 170_000, seed=12, lo=1)
+    tab = _make(p, kind, _grid_fused=True)
+    assert C.KERNEL_PATHS[tab.info.kernel_path] == "k_fast"
+    ok, root_m, _ = _oracle(kind, p, np.ones(p.R, np.uint8))
+    assert ok
+    wd = tab.Wd
+    out = torch.zeros(wd, dtype=torch.int64, device="cuda")
+    sd = torch.zeros(1, dtype=torch.int32, device="cuda")
+    a, b = tab.root.clone(), tab.root.clone()
+    src, cur = tab.root, root_m.copy()
+    rng = Rng(31, lanes=1)
+    done = 0
+    for k in range(40):
+        rem = walk_removal(rng, cur, p.d, m=1, q=0.3)
+        if rem is None:
+            src, cur = tab.root, root_m.copy()
+            continue
+        dst = a if src is not a else b
+        din = cur & (1 - rem)
+        okk, dout, _ = _oracle(kind, p, din)
+        remd = torch.from_numpy(member_to_bitmap(rem, p.d).view(np.int64)).cuda()
+        torch.cuda.synchronize()
+        dst.propagate_from_async(src, remd, out, None, sd)
+        dst.synchronize()
+        assert int(sd.item()) == (CT_OK if okk else CT_FAIL), k
+        if okk:
+            assert np.array_equal(bitmap_to_member(out.cpu().numpy().view(np.uint64), p.d), dout), k
+            src, cur = dst, dout
+            done += 1
+        else:
+            src, cur = tab.root, root_m.copy()
+    assert done > 10
+    tab.close()
