@@ -890,7 +890,8 @@ def run_c4(args):
     upd_n, upd_ms = prof["update"]
     launches = sum(v[0] for v in prof.values())
     if tab.info.batch_tile:
-        launches += upd_n + prof["scan"][0]    # k_bcompact shares the update slot, k_bscan runs 2 passes per slot
+        # k_bcompact (and k_bsparse) share the update slot, k_bscan runs 2 passes per slot
+        launches += upd_n * (2 if tab.info.batch_cells else 1) + prof["scan"][0]
     roofline = None
     if tab.info.batch_tile and upd_n:
         # dominant kernel: the tile-major update (k_bupdate + k_bcompact, one event pair).

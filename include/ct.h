@@ -115,6 +115,11 @@ typedef struct ct_config {
                               /*    instead of the tile-major batch update              */
   int32_t search_levels;      /* > 0: trail depth of the device-resident DFS (models);  */
                               /*    a deeper search falls back to the host driver       */
+  int32_t batch_cells;        /* 1 (default): the tile-major batch update may check the  */
+                              /*    few valid tuples of a sparse (state, tile) against  */
+                              /*    the new domains instead of OR-ing*/
+                              /*    support rows (needs the t x n cells of use_gather); */
+                              /*    0: rows only.  Same results.                         */
 } ct_config;
 enum { CT_SHAPE_AUTO = 0, CT_SHAPE_PHASES = 1, CT_SHAPE_FUSED = 2, CT_SHAPE_FAST = 3, CT_SHAPE_SMALL = 4,
        CT_SHAPE_WIDE = 5 };
@@ -213,6 +218,8 @@ typedef struct ct_table_info {
                                 /* 0 = one pass per state (R too large for the tile)      */
   int32_t gather_cell_bits;     /* bits per cell of the gather filter's tuple copy, 0 = off */
   int32_t kind;                 /* CT_TABLE_*                                             */
+  int32_t batch_cells;          /* 1: the batch update's cell route and sparse-state route */
+                                /* are on (ct_config.batch_cells and 8-bit tuple cells)   */
 } ct_table_info;
 
 ct_status ct_table_info_get(const ct_table *t, ct_table_info *out);
@@ -412,14 +419,16 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *out);
  * tile-major update (ct_table_info.batch_tile > 0) update_support_words and
  * update_table_writes are per batch only, see ct_batch_work. */
 ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
-/* Work counters of the tile-major batch path (measurement only).  out6 = host
- * int64[6]: [0] 64-bit support words the update OR-ed (from shared memory),
+/* Work counters of the tile-major batch path (measurement only).  out8 = host
+ * int64[8]: [0] 64-bit support words the update OR-ed (from shared memory),
  * [1] 16-byte currTable blocks it read, [2] blocks it rewrote, [3] support
- * bytes staged from global into shared memory -- [0..3] summed over all calls
- * since the last reset (reset != 0 zeroes them after the read); [4] support
- * words the filter scans loaded and [5] residue-probe misses, both of the last
- * call.  All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
-ct_status ct_batch_work(ct_batch *b, int64_t *out6, int32_t reset);
+ * (and tuple-cell) bytes staged from global into shared memory, [6] valid
+ * tuples the update's cell routes checked, [7] state updates that took the
+ * sparse-state route -- [0..3], [6] and [7] summed over all calls since the
+ * last reset (reset != 0 zeroes them after the read); [4] support words the
+ * filter scans loaded and [5] residue-probe misses, both of the last call.
+ * All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
+ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset);
 
 /* Per-kernel device timing (measurement only).  While enabled, every
  * *_async / ct_propagate_many call on this table's states and batches records a

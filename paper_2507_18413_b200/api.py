@@ -26,7 +26,7 @@ class Table:
                  update_policy: int = C.CT_POLICY_AUTO, use_residues: bool = True, use_index: bool = True,
                  use_graph: bool = True, use_fused: bool = True, kind: str | int = "positive",
                  use_gather: bool = True, launch_shape: int | str = 0, grid_override: int = 0,
-                 batch_per_state: bool = False):
+                 batch_per_state: bool = False, batch_cells: bool = True):
         """kind: "positive" (ct_create), "short" (cells == CT_STAR match any value)
         or "negative" (the tuples are the forbidden assignments) -- include/ct.h f4."""
         import torch
@@ -40,7 +40,8 @@ class Table:
         self.allocator = C.TorchAllocator(self.device) if torch_alloc else None
         cfg, self._keep = C.make_config(self.device, stream_ptr, self.allocator, n_shards, shard_rank,
                                         nccl_unique_id, update_policy, use_residues, use_index, use_graph,
-                                        use_fused, use_gather, launch_shape, grid_override, batch_per_state)
+                                        use_fused, use_gather, launch_shape, grid_override, batch_per_state,
+                                        batch_cells=batch_cells)
         self.lo = np.ascontiguousarray(lo, np.int32)
         self.d = np.ascontiguousarray(d, np.int32)
         self.kind = C.TABLE_KINDS[kind] if isinstance(kind, str) else int(kind)

@@ -37,6 +37,17 @@ constexpr int kBTPB = 1024;        // k_bupdate threads per CTA
 constexpr int kBSmallTPB = 128;    // k_bingest / k_bfinalize threads per CTA (one state each)
 constexpr int kBProbeTPB = 256;
 constexpr int kBScanTPB = 256;
+constexpr int kCellVars = 2;       // cell route: at most this many changed variables per state
+#ifndef CT_SPARSE_DIV
+#define CT_SPARSE_DIV 4
+#endif
+#ifndef CT_CELL_K
+#define CT_CELL_K 4
+#endif
+constexpr int kSparseDiv = CT_SPARSE_DIV;   // sparse route iff active blocks L <= W2 / kSparseDiv
+constexpr int kCellK = CT_CELL_K;           // cell route iff kCellK x (largest block popcount) <= P
+constexpr int kBSparseTPB = 256;   // k_bsparse threads per CTA (one state each)
+constexpr int kSpB = 4;            // k_bsparse: valid tuples whose cells one thread loads together
 
 // Device view of a batch: S state blocks of `pitch` bytes in one pool, field
 // offsets from ct_runtime.cu's StateLayout.
@@ -45,14 +56,19 @@ struct BatchDev {
   int64_t pitch;
   int64_t o_ctl, o_T, o_ulist, o_items, o_res, o_sup, o_scan, o_idx0, o_idx1, o_bmask;
   int64_t o_plist;           // padded update list (kTW = 32 path), see k_bingest
+  int64_t t_local;           // tuples of the table (shard): the cell tile's bound
   int32_t plist_po;          // its first padded entry (uint32 index)
+  int32_t cell_route;        // 1: k_bupdate<32> stages the tile's tuple cells and may check valid tuples directly
   int32_t *bgo;              // [S] per call: (groups << 20) | update-list length, or -1 if the state does not update
   int2 *miss, *miss2;        // [S·R] global lists of (state, row) probe misses (pass 0 / pass 1 of k_bscan)
   int32_t *nmiss, *nmiss2;   // their lengths (zeroed by k_bingest)
+  int32_t *dense, *ndense;   // [S] states k_bupdate updates (in k_bingest's arrival order) and their
+                             // number; k_bfinalize zeroes the count for the next call
   int2 *sinfo;               // [S] per call: (index buffer parity, L_out) of each state, from k_bcompact
-  unsigned long long *work;  // [4] whole batch, summed over calls until ct_batch_work resets them:
+  unsigned long long *work;  // [6] whole batch, summed over calls until ct_batch_work resets them:
                              // update support words, currTable blocks read, blocks rewritten,
-                             // support bytes staged into shared memory
+                             // support (and cell) bytes staged into shared memory, valid tuples
+                             // checked by the cell routes, states updated by k_bsparse
 };
 
 __device__ __forceinline__ Ctl *bctl(const BatchDev &b, int s) {
@@ -65,11 +81,16 @@ __device__ __forceinline__ T *bfield(const BatchDev &b, int s, int64_t off) {
 
 // ------------------------------------------------------------------ a2: ingest, one CTA per state
 // dev_ingest (Alg. 1 L1-3, Alg. 2), then, for the kTW = 32 update, the
-// update list re-laid out for it: each variable group padded to a multiple of
-// 4 entries with the all-zero row R, entries stored as shared-memory byte
-// offsets (row · 512), and a group table
-//   plist[0] = G, plist[4 + g] = padded start | real size << 16 | Δ-branch << 31,
-//   plist[4 + G] = padded total,  plist[po + k] = padded entry k.
+// update list re-laid out as ONE flat list of shared-memory byte offsets
+// (row · 512) in groups padded to a multiple of 4 entries with the all-zero
+// row R.  The Δ-branch variables share a single group: T & ¬OR(Δ_x1 rows) &
+// ¬OR(Δ_x2 rows) = T & ¬OR(Δ_x1 rows ∪ Δ_x2 rows) (De Morgan), so however many
+// variables take the Δ-branch they cost one group end; every dom-branch
+// variable is a group of its own.  The last entry of a group carries kEndBit
+// (and kInvBit for the Δ group), so k_bupdate walks the list without a group
+// table:  plist[0] = padded total P,  plist[po + k] = padded entry k;
+// bgo[s] = sparse route << 30 | P << 12 | update-list length (< 4096), or -1
+// if the state does not update.
 // The per-state work of the layout is paid once per call, not once per tile.
 __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const StateDev *__restrict__ states,
                                                        const uint64_t *__restrict__ removed,
@@ -90,7 +111,7 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
   }
   __syncthreads();
   const int n = tb.n, Wd = tb.Wd;
-  int G = 0;
+  int P = 0;
   if (s_go && build_plist) {
     // dev_ingest's shared arrays: |Δ_x|, |D_x| and the group starts of the update list
     const int32_t *s_cd = reinterpret_cast<const int32_t *>(smem + 2 * Wd);
@@ -98,33 +119,91 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
     const int32_t *s_ust = s_cs + n;
     __shared__ uint64_t s_warp[kBSmallTPB / 32];
     uint32_t *pl = bfield<uint32_t>(bd, blockIdx.x, bd.o_plist);
+    uint32_t *pe = pl + bd.plist_po;
     const uint32_t zrow = (uint32_t)tb.R * 512u;
+    const uint32_t *ul = reinterpret_cast<const uint32_t *>(st.ulist);
+    // per variable: (dom-branch padded size << 32) | Δ-branch size
+    auto sizes = [&](int x) -> uint64_t {
+      if (x >= n) return 0ull;
+      const int sz = s_ust[x + 1] - s_ust[x];
+      if (!sz) return 0ull;
+      return use_delta(tb, x, s_cd[x], s_cs[x]) ? (uint64_t)sz : ((uint64_t)((sz + 3) & ~3) << 32);
+    };
+    // pass 1: the Δ group's size (it goes first, the dom groups after it)
+    uint64_t tot = 0;
+    for (int base = 0; base < n; base += kBSmallTPB) {
+      uint64_t t;
+      block_excl_scan<kBSmallTPB>(sizes(base + threadIdx.x), s_warp, t);
+      tot += t;
+    }
+    const int nd = (int)(tot & 0xffffffffu), pd = (nd + 3) & ~3;
+    P = pd + (int)(tot >> 32);
+    // pass 2: every variable writes its entries at its offset
     uint64_t carry = 0;
     for (int base = 0; base < n; base += kBSmallTPB) {
       const int x = base + threadIdx.x;
-      int sz = 0;
-      if (x < n) sz = s_ust[x + 1] - s_ust[x];
-      const uint64_t v = sz ? ((uint64_t)((sz + 3) & ~3) << 32) | 1ull : 0ull;
-      uint64_t total;
-      const uint64_t ex = block_excl_scan<kBSmallTPB>(v, s_warp, total) + carry;
-      if (sz) {
-        const int g = (int)(ex & 0xffffffffu);
-        const int pst = (int)(ex >> 32);
-        const bool useDelta = use_delta(tb, x, s_cd[x], s_cs[x]);
-        pl[4 + g] = (uint32_t)pst | ((uint32_t)sz << 16) | (useDelta ? 0x80000000u : 0u);
-        const uint32_t *ul = reinterpret_cast<const uint32_t *>(st.ulist);
-        const int psz = (sz + 3) & ~3;
-        for (int j = 0; j < psz; ++j) pl[bd.plist_po + pst + j] = j < sz ? (ul[s_ust[x] + j] & kRowMask) * 512u : zrow;
+      const uint64_t v = sizes(x);
+      uint64_t t;
+      const uint64_t ex = block_excl_scan<kBSmallTPB>(v, s_warp, t) + carry;
+      carry += t;
+      if (v) {
+        const bool dl = (v >> 32) == 0;
+        const int sz = s_ust[x + 1] - s_ust[x];
+        const int off = dl ? (int)(ex & 0xffffffffu) : pd + (int)(ex >> 32);
+        for (int j = 0; j < sz; ++j) pe[off + j] = (ul[s_ust[x] + j] & kRowMask) * 512u;
+        if (!dl) {
+          const int psz = (sz + 3) & ~3;
+          for (int j = sz; j < psz; ++j) pe[off + j] = zrow;
+          pe[off + psz - 1] |= kEndBit;
+        }
       }
-      carry += total;
     }
-    G = (int)(carry & 0xffffffffu);
+    if (threadIdx.x < pd - nd) pe[nd + threadIdx.x] = zrow;
+    // cell-route descriptor (tile32_cells): the changed variables' cell
+    // positions and new domains D'_x (dev_ingest's s_din), when there are at
+    // most kCellVars of them and each domain is one 64-bit word:
+    //   plist[1] = their number (0: rows only), plist[4 + k] = cell word << 8 |
+    //   bit shift, plist[8 + 2k .. 9 + 2k] = D'_x lo/hi
+    __shared__ int s_nchg, s_cok;
     if (threadIdx.x == 0) {
-      pl[0] = (uint32_t)G;
-      pl[4 + G] = (uint32_t)(carry >> 32);
+      s_nchg = 0;
+      s_cok = bd.cell_route;
+    }
+    __syncthreads();   // also orders the Δ group's entries before its flags below
+    for (int x = threadIdx.x; x < n; x += kBSmallTPB) {
+      if (s_ust[x + 1] > s_ust[x]) {
+        const int k = atomicAdd(&s_nchg, 1);
+        const int w0 = tb.domOff[x];
+        if (k >= kCellVars || tb.domOff[x + 1] - w0 != 1) {
+          s_cok = 0;
+        } else {
+          const int bit = x * tb.cell_bits;
+          pl[4 + k] = (uint32_t)((bit >> 5) << 8) | (uint32_t)(bit & 31);
+          pl[8 + 2 * k] = (uint32_t)smem[w0];
+          pl[9 + 2 * k] = (uint32_t)(smem[w0] >> 32);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (pd) pe[pd - 1] |= kEndBit | kInvBit;
+      pl[0] = (uint32_t)P;
+      pl[1] = s_cok ? (uint32_t)s_nchg : 0u;
     }
   }
-  if (threadIdx.x == 0) bd.bgo[blockIdx.x] = s_go ? (G << 20) | s_nrows : -1;
+  if (threadIdx.x == 0) {
+    int sparse = 0;
+    if (s_go && build_plist && bd.cell_route && tb.use_index) {
+      // the sparse route (k_bsparse) for a state with few active blocks whose
+      // changed variables the cell route can check (plist[1] > 0)
+      const uint32_t *pl = bfield<const uint32_t>(bd, blockIdx.x, bd.o_plist);
+      const Ctl *c = st.ctl;
+      const int L = c->identity ? tb.W2 : c->L;
+      sparse = (__ldcg(pl + 1) > 0u && (int64_t)L * kSparseDiv <= tb.W2) ? 1 : 0;
+    }
+    bd.bgo[blockIdx.x] = s_go ? (sparse << 30) | (P << 12) | s_nrows : -1;
+    if (s_go && !sparse) bd.dense[atomicAdd(bd.ndense, 1)] = blockIdx.x;
+  }
 }
 
 // ------------------------------------------------------------------ a3-a5: tile-major update
@@ -134,122 +213,130 @@ __device__ __forceinline__ ulonglong2 lds128(uint32_t addr) {
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];\n" : "=l"(v.x), "=l"(v.y) : "r"(addr));
   return v;
 }
-
-// One state's tile when the tile is a full warp (kTW = 32): every lane works on
-// the same state, so the walk over the update list is warp-uniform and split
-// at the variable-group ends (one ballot per 32 entries).  Per row: a shuffle
-// of the row's byte offset, a 16-byte shared load and 3-input ORs, four rows
-// per step.  Lanes whose block is already dead keep loading (no predicate, no
-// branch): their mask only shrinks, so their result stays 0.  `s_lane` =
-// shared address of this lane's column of row 0, `zrow` = byte offset of the
-// all-zero row R.  Returns the new block value; adds to `nl` (on every lane)
-// the rows the warp's live blocks needed.
-__device__ __forceinline__ ulonglong2 tile32_state(uint32_t s_lane, uint32_t zrow, const uint32_t *ul, int nr,
-                                                   uint32_t ev, ulonglong2 tw, bool live, uint32_t &nl) {
-  const int lane = threadIdx.x & 31;
-  uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-  if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
-  for (int p0 = 0; p0 < nr; p0 += 32) {
-    if (p0 > 0) ev = p0 + lane < nr ? __ldcg(ul + p0 + lane) : 0u;
-    const int cnt = min(32, nr - p0);
-    const uint32_t rbyte = (ev & kRowMask) * 512u;          // entry `lane`: its row's byte offset in s_sup
-    unsigned ends = __ballot_sync(0xffffffffu, (ev & kEndBit) != 0u);
-    if (cnt < 32) ends &= (1u << cnt) - 1u;
-    int q = 0;
-    while (q < cnt) {
-      const int qe = ends ? __ffs(ends) - 1 : cnt - 1;     // last entry of this group in the chunk
-      // four rows per step; entries past the group's end read the zero row
-      for (int k = q; k <= qe; k += 4) {
-        uint32_t r0 = __shfl_sync(0xffffffffu, rbyte, k), r1 = __shfl_sync(0xffffffffu, rbyte, (k + 1) & 31);
-        uint32_t r2 = __shfl_sync(0xffffffffu, rbyte, (k + 2) & 31), r3 = __shfl_sync(0xffffffffu, rbyte, (k + 3) & 31);
-        if (k + 1 > qe) r1 = zrow;
-        if (k + 2 > qe) r2 = zrow;
-        if (k + 3 > qe) r3 = zrow;
-        const ulonglong2 v0 = lds128(s_lane + r0), v1 = lds128(s_lane + r1);
-        const ulonglong2 v2 = lds128(s_lane + r2), v3 = lds128(s_lane + r3);
-        ax |= v0.x | v1.x;
-        ay |= v0.y | v1.y;
-        ax |= v2.x | v3.x;
-        ay |= v2.y | v3.y;
-      }
-      nl += (uint32_t)(qe - q + 1) * (uint32_t)__popc(__ballot_sync(0xffffffffu, live));   // warp total
-      if (ends) {                                           // the group ends here: AND its mask in
-        const bool inv = (__shfl_sync(0xffffffffu, ev, qe) & kInvBit) != 0u;
-        if (inv) {
-          mx &= ~ax;
-          my &= ~ay;
-        } else {
-          mx &= ax;
-          my &= ay;
-        }
-        ax = ay = 0;
-        live = live && ((tw.x & mx) | (tw.y & my)) != 0;   // Alg. 2, per block
-        ends &= ends - 1u;
-        if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
-      }
-      q = qe + 1;
-    }
-  }
-  return make_ulonglong2(tw.x & mx, tw.y & my);
+// The same, predicated on p != 0 (v keeps its value otherwise).
+__device__ __forceinline__ void lds128p(uint32_t addr, uint32_t p, ulonglong2 &v) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n @q ld.shared.v2.u64 {%0, %1}, [%2];\n}\n"
+               : "+l"(v.x), "+l"(v.y) : "r"(addr), "r"(p));
 }
 
-// The same from the padded list (k_bingest): `gt` = lane g holds group g's
-// table entry (lane G: the padded total), `pe` = lane k holds padded entry k
-// of the chunk starting at entry 0; later chunks are loaded from `pl`.  Every
-// group is a multiple of 4 entries, so a step of 4 rows never needs a bound.
-__device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s_pl, const uint32_t *pl, int G,
-                                                    uint32_t gt, uint32_t pe, ulonglong2 tw, bool live,
-                                                    uint32_t &nl) {
+// One state's tile when the tile is a full warp (kTW = 32): every lane works on
+// the same state, so the walk over the flat padded list (k_bingest) is
+// warp-uniform.  `pe` = lane k holds entry k of the first 32 (prefetched);
+// later chunks of 32 are loaded from `pl`; the current chunk sits in this
+// warp's shared slot `s_pl`, so one broadcast 16-byte load yields four row
+// offsets.  Per step of four rows: four conflict-free 16-byte shared loads
+// (predicated off for lanes whose block is dead: they cost no wavefront) and
+// 3-input ORs; a group end (kEndBit on the step's 4th entry) ANDs the group's
+// OR, complemented for the Δ group, into the mask and applies Alg. 2's early
+// break per block.  `s_lane` = shared address of this lane's
+// column of row 0.  Returns the new block value; adds to `nsteps` the steps
+// this lane took while live (4 support rows each).
+__device__ __forceinline__ ulonglong2 tile32_flat(uint32_t s_lane, uint32_t *s_pl, const uint32_t *pl, int P,
+                                                  uint32_t pe, ulonglong2 tw, bool live, uint32_t &nsteps) {
   const int lane = threadIdx.x & 31;
   uint64_t mx = ~0ull, my = ~0ull, ax = 0, ay = 0;
-  if (!__any_sync(0xffffffffu, live)) return make_ulonglong2(0ull, 0ull);
-  // the current 32 entries live in this warp's shared slot: four row offsets
-  // per broadcast 16-byte load instead of four shuffles
-  int chunk = 0;
-  s_pl[lane] = pe;
-  __syncwarp();
-  uint32_t ge = __shfl_sync(0xffffffffu, gt, 0);
-  for (int g = 0; g < G; ++g) {
-    const uint32_t gn = __shfl_sync(0xffffffffu, gt, g + 1);
-    const int en = (int)(gn & 0xffffu);
-    for (int k = (int)(ge & 0xffffu); k < en;) {
-      if ((k >> 5) != chunk) {                                 // warp-uniform, once per 32 entries
-        chunk = k >> 5;
-        const uint32_t v = __ldcg(pl + chunk * 32 + lane);
-        __syncwarp();
-        s_pl[lane] = v;
-        __syncwarp();
+  uint32_t lv = live ? 1u : 0u;
+  ulonglong2 v0 = make_ulonglong2(0ull, 0ull), v1 = v0, v2 = v0, v3 = v0;
+  for (int c = 0; c < P; c += 32) {
+    if (c > 0) pe = __ldcg(pl + c + lane);
+    __syncwarp();
+    s_pl[lane] = pe;
+    __syncwarp();
+    const uint4 *rp = reinterpret_cast<const uint4 *>(s_pl);
+    const int n4 = min(32, P - c) >> 2;
+    for (int i = 0; i < n4; ++i) {
+      const uint4 r = rp[i];
+      // predicated (not branched) loads: a dead lane issues no shared-memory
+      // access and ORs stale values, which is harmless: its mask only shrinks
+      // (a Δ group ANDs a complement, a dom group an OR), and its block is 0
+      lds128p(s_lane + r.x, lv, v0);
+      lds128p(s_lane + r.y, lv, v1);
+      lds128p(s_lane + r.z, lv, v2);
+      lds128p(s_lane + (r.w & (kEndBit - 1u)), lv, v3);
+      ax |= v0.x | v1.x;
+      ay |= v0.y | v1.y;
+      ax |= v2.x | v3.x;
+      ay |= v2.y | v3.y;
+      nsteps += lv;
+      if (r.w & kEndBit) {                                  // warp-uniform: a group ends here
+        const uint64_t inv = (r.w & kInvBit) ? ~0ull : 0ull; // Δ group: AND the complement
+        mx &= ax ^ inv;
+        my &= ay ^ inv;
+        ax = ay = 0;
+        live = live && ((tw.x & mx) | (tw.y & my)) != 0;    // Alg. 2, per block
+        lv = live ? 1u : 0u;
+        if (!__any_sync(0xffffffffu, live)) {
+          __syncwarp();
+          return make_ulonglong2(0ull, 0ull);
+        }
       }
-      const int kend = min(en, (chunk + 1) * 32);
-      const uint4 *rp = reinterpret_cast<const uint4 *>(s_pl + (k & 31));
-      // dead lanes drop out: a quarter-warp with no live block costs no
-      // shared-memory wavefront
-      const int nsteps = live ? (kend - k) >> 2 : 0;
-      for (int i = 0; i < nsteps; ++i) {
-        const uint4 r = rp[i];
-        const ulonglong2 v0 = lds128(s_lane + r.x), v1 = lds128(s_lane + r.y);
-        const ulonglong2 v2 = lds128(s_lane + r.z), v3 = lds128(s_lane + r.w);
-        ax |= v0.x | v1.x;
-        ay |= v0.y | v1.y;
-        ax |= v2.x | v3.x;
-        ay |= v2.y | v3.y;
-      }
-      k = kend;
     }
-    nl += ((ge >> 16) & 0x7fffu) * (uint32_t)__popc(__ballot_sync(0xffffffffu, live));   // warp total
-    const uint64_t inv = (ge & 0x80000000u) ? ~0ull : 0ull;   // Δ-branch: AND the complement
-    mx &= ax ^ inv;
-    my &= ay ^ inv;
-    ax = ay = 0;
-    live = live && ((tw.x & mx) | (tw.y & my)) != 0;          // Alg. 2, per block
-    if (!__any_sync(0xffffffffu, live)) {
-      __syncwarp();
-      return make_ulonglong2(0ull, 0ull);
-    }
-    ge = gn;
   }
   __syncwarp();   // the slot is rewritten for the next state
   return make_ulonglong2(tw.x & mx, tw.y & my);
+}
+
+// The cell route: the same new block computed from the definition of a valid
+// tuple instead of the support rows -- a tuple that was
+// valid before the call stays valid iff its value of every CHANGED variable is
+// still in D'_x (the unchanged variables' values were, and still are, in
+// their domains).  Alg. 2's mask ANDed into T keeps exactly these tuples, so
+// the result is the same block; k_bupdate takes this route for a (state, tile)
+// when the warp's blocks hold so few valid tuples that checking each one is
+// cheaper than OR-ing the update list's rows.  `s_cells` = the tile's cells in
+// shared memory, [cell word][bit position 0..127][block 0..31] (a lane reads
+// its own block's column: conflict-free); `dsc` = lane k holds plist[k]
+// (k_bingest's descriptor); `maxc` = the warp's largest per-block popcount.
+// Adds the tuples this lane checked to `nchk`.
+__device__ __forceinline__ ulonglong2 tile32_cells(const uint32_t *s_cells, int nchg, uint32_t dsc, ulonglong2 tw,
+                                                   bool live, int maxc, uint32_t &nchk) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t ws0 = __shfl_sync(0xffffffffu, dsc, 4), ws1 = __shfl_sync(0xffffffffu, dsc, 5);
+  const uint32_t d0l = __shfl_sync(0xffffffffu, dsc, 8), d0h = __shfl_sync(0xffffffffu, dsc, 9);
+  const uint32_t d1l = __shfl_sync(0xffffffffu, dsc, 10), d1h = __shfl_sync(0xffffffffu, dsc, 11);
+  const uint64_t dm0 = ((uint64_t)d0h << 32) | d0l;
+  const uint64_t dm1 = nchg > 1 ? (((uint64_t)d1h << 32) | d1l) : ~0ull;   // one variable: accept all
+  const uint32_t *c0 = s_cells + (ws0 >> 8) * 4096 + lane, *c1 = s_cells + (ws1 >> 8) * 4096 + lane;
+  const uint32_t sh0 = ws0 & 31u, sh1 = nchg > 1 ? (ws1 & 31u) : 0u;
+  // the block as four 32-bit words: the remaining bits (a, b, c, d) are
+  // visited lowest first, one per iteration, and a failed tuple's bit is
+  // cleared from the result words (ra .. rd)
+  uint32_t a = 0, b = 0, c = 0, d = 0;
+  if (live) {
+    a = (uint32_t)tw.x;
+    b = (uint32_t)(tw.x >> 32);
+    c = (uint32_t)tw.y;
+    d = (uint32_t)(tw.y >> 32);
+  }
+  uint32_t ra = a, rb = b, rc = c, rd = d;
+  for (int it = 0; it < maxc; ++it) {
+    const uint32_t w = a ? a : b ? b : c ? c : d;
+    if (w) {
+      const int q = a ? 0 : b ? 32 : c ? 64 : 96;
+      const uint32_t bit = w & (0u - w);
+      const int pos = q + __ffs(w) - 1;
+      const uint32_t v0 = (c0[pos * 32] >> sh0) & 0xffu;
+      const uint32_t v1 = (c1[pos * 32] >> sh1) & 0xffu;
+      const uint32_t ok = (uint32_t)((dm0 >> v0) & (dm1 >> v1)) & 1u;
+      const uint32_t kill = ok ? 0u : bit;
+      if (q == 0) {
+        a ^= bit;
+        ra ^= kill;
+      } else if (q == 32) {
+        b ^= bit;
+        rb ^= kill;
+      } else if (q == 64) {
+        c ^= bit;
+        rc ^= kill;
+      } else {
+        d ^= bit;
+        rd ^= kill;
+      }
+      ++nchk;
+    }
+  }
+  if (!live) return make_ulonglong2(0ull, 0ull);
+  return make_ulonglong2(((uint64_t)rb << 32) | ra, ((uint64_t)rd << 32) | rc);
 }
 
 // Persistent: CTA c processes the contiguous unit range [U·c/G, U·(c+1)/G) of
@@ -260,7 +347,7 @@ __device__ __forceinline__ ulonglong2 tile32_padded(uint32_t s_lane, uint32_t *s
 template <int kTW>
 __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, int S, int ntiles, int nchunk,
                                                      int chunk_states) {
-  extern __shared__ __align__(16) ulonglong2 s_sup[];   // [R + 1][kTW], row R = 0
+  extern __shared__ __align__(16) ulonglong2 s_sup[];   // [R + 1][kTW], row R = 0; then the cell tile (kTW = 32)
   __shared__ __align__(16) uint32_t s_plw[kBTPB];        // per warp: 32 update-list entries (kTW = 32 path)
   constexpr int SPW = 32 / kTW;                         // states per warp
   const int R = tb.R, W2 = tb.W2;
@@ -271,7 +358,8 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
   const int64_t units = (int64_t)ntiles * nchunk;
   const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
   int cur_tile = -1;
-  uint32_t w_loads = 0, w_writes = 0, w_reads = 0;   // this lane's share of the batch work counters
+  const int nd = __ldcg(bd.ndense);   // states on the list (k_bingest)
+  uint32_t w_loads = 0, w_writes = 0, w_reads = 0, w_cells = 0;   // this lane's share of the batch work counters
   unsigned long long w_staged = 0;
   for (int64_t u = u0; u < u1; ++u) {
     const int tile = (int)(u / nchunk), chunk = (int)(u - (int64_t)tile * nchunk);
@@ -283,59 +371,90 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
         s_sup[i] = (row < R && blk < Wp2) ? ld_sup2(tb.S + (int64_t)row * Wp + 2 * blk)
                                           : make_ulonglong2(0ull, 0ull);
       }
+      if (kTW == 32 && bd.cell_route) {
+        // the tile's 4096 tuples' cells, [cell word][bit position][block]:
+        // thread q reads 4 consecutive tuples of block q % 32 (whole sectors)
+        uint32_t *s_cells = reinterpret_cast<uint32_t *>(s_sup + (R + 1) * kTW);
+        const int cw = tb.cell_words;
+        for (int q = threadIdx.x; q < 1024; q += blockDim.x) {
+          const int b = q & 31, p4 = (q >> 5) * 4;
+          const int64_t j0 = (int64_t)tile * 4096 + b * 128 + p4;
+          const uint32_t *src = tb.cells + j0 * cw;
+          for (int t = 0; t < 4; ++t) {
+            const bool ok = j0 + t < bd.t_local;
+            for (int w = 0; w < cw; ++w) s_cells[w * 4096 + (p4 + t) * 32 + b] = ok ? __ldg(src + t * cw + w) : 0u;
+          }
+        }
+        w_staged += (unsigned long long)4096 * cw * 4;
+      }
       __syncthreads();
       cur_tile = tile;
       w_staged += (unsigned long long)(R + 1) * kTW * 16;
     }
-    const int s0 = chunk * chunk_states, s1 = min(S, s0 + chunk_states);
+    // this unit's slice of the dense-state list (k_bingest: the updating
+    // states that k_bsparse does not take)
+    const int cs = (nd + nchunk - 1) / nchunk;
+    const int s0 = chunk * cs, s1 = min(nd, s0 + cs);
     const int blk = tile * kTW + bl;
     const bool inblk = blk < W2;
     // software pipeline: the next state's go word, currTable block and first
-    // update-list entries are in flight while the current state is processed
-    int s = s0 + warp * SPW + sub;
+    // update-list entries are in flight while the current state is processed,
+    // and the state id after it (the list entry they depend on)
     const int step = nwarps * SPW;
+    int i = s0 + warp * SPW + sub;
     int go_n = -1;
     ulonglong2 tw_n = make_ulonglong2(0ull, 0ull);
-    uint32_t ev_n = 0, gt_n = 0;
+    uint32_t ev_n = 0, dsc_n = 0;
     auto fetch = [&](int ss) {
       go_n = -1;
       tw_n = make_ulonglong2(0ull, 0ull);
-      ev_n = gt_n = 0;
-      if (ss < s1) {
+      ev_n = dsc_n = 0;
+      if (ss >= 0) {
         const char *sb = bd.pool + (int64_t)ss * bd.pitch;
         go_n = __ldcg(bd.bgo + ss);
         if (inblk) tw_n = __ldcg(reinterpret_cast<const ulonglong2 *>(sb + bd.o_T) + blk);
         if constexpr (kTW == 32) {
           const uint32_t *pl = reinterpret_cast<const uint32_t *>(sb + bd.o_plist);
-          gt_n = __ldcg(pl + 4 + lane);
           ev_n = __ldcg(pl + bd.plist_po + lane);
+          if (lane < 12) dsc_n = __ldcg(pl + lane);
         } else {
           if (bl < R) ev_n = __ldcg(reinterpret_cast<const uint32_t *>(sb + bd.o_ulist) + bl);
         }
       }
     };
-    fetch(s);
-    for (int base = s0 + warp * SPW; base < s1; base += step, s += step) {
+    int id_c = i < s1 ? __ldcg(bd.dense + i) : -1;
+    fetch(id_c);
+    int id_n = i + step < s1 ? __ldcg(bd.dense + i + step) : -1;
+    for (int base = s0 + warp * SPW; base < s1; base += step, i += step) {
+      const int s = max(id_c, 0);
       const int go = go_n;
-      const int nr = go < 0 ? -1 : (go & 0xfffff);
+      const int nr = go < 0 ? -1 : (go & 0xfff);
       const ulonglong2 tw = tw_n;
       uint32_t ev = ev_n;
-      const uint32_t gt = gt_n;
-      fetch(s + step);
+      const uint32_t dsc = dsc_n;
+      fetch(id_n);
+      id_c = id_n;
+      id_n = i + 2 * step < s1 ? __ldcg(bd.dense + i + 2 * step) : -1;
       const bool upd = nr >= 0 && inblk;         // this lane's block takes part in the update
       const bool had = upd && (tw.x | tw.y) != 0;
       uint32_t nl = 0;
-      char *sb = bd.pool + (int64_t)min(s, S - 1) * bd.pitch;
+      char *sb = bd.pool + (int64_t)s * bd.pitch;
       const uint32_t *ul = reinterpret_cast<const uint32_t *>(sb + bd.o_ulist);
       ulonglong2 nt;
       if constexpr (kTW == 32) {
         if (nr < 0) continue;                    // warp-uniform: one state per warp
-        const int G = go >> 20;
-        if (G < 32) {
-          nt = tile32_padded(s_lane, s_plw + 32 * warp, reinterpret_cast<const uint32_t *>(sb + bd.o_plist) + bd.plist_po,
-                             G, gt, ev, tw, had, nl);
-        } else {                                 // > 31 changed variables: the plain list
-          nt = tile32_state(s_lane, (uint32_t)R * 512u, ul, nr, __ldcg(ul + lane), tw, had, nl);
+        const int P = (go >> 12) & 0x3ffff;
+        const int nchg = __shfl_sync(0xffffffffu, dsc, 1);
+        const int cnt = had ? __popcll(tw.x) + __popcll(tw.y) : 0;
+        const int maxc = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+        if (maxc == 0) {
+          nt = make_ulonglong2(0ull, 0ull);
+        } else if (nchg > 0 && kCellK * maxc <= P) {   // few valid tuples: check them (cost model: DESIGN §7)
+          nt = tile32_cells(reinterpret_cast<const uint32_t *>(s_sup + (R + 1) * kTW), nchg, dsc, tw, had, maxc,
+                            w_cells);
+        } else {
+          nt = tile32_flat(s_lane, s_plw + 32 * warp, reinterpret_cast<const uint32_t *>(sb + bd.o_plist) + bd.plist_po,
+                           P, ev, tw, had, nl);
         }
       } else {
         bool live = had;
@@ -378,7 +497,7 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
       w_writes += wr ? 1u : 0u;
       w_reads += upd ? 1u : 0u;
       if constexpr (kTW == 32) {
-        if (lane == 0) w_loads += nl;     // nl is the warp total here
+        w_loads += 4u * nl;               // steps of 4 rows (padding rows included) while live
       } else {
         w_loads += nl;                    // per lane
       }
@@ -398,11 +517,13 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
     w_loads += __shfl_xor_sync(0xffffffffu, w_loads, o);
     w_writes += __shfl_xor_sync(0xffffffffu, w_writes, o);
     w_reads += __shfl_xor_sync(0xffffffffu, w_reads, o);
+    w_cells += __shfl_xor_sync(0xffffffffu, w_cells, o);
   }
   if (lane == 0) {
     if (w_loads) atomicAdd(bd.work + 0, 2ull * w_loads);
     if (w_reads) atomicAdd(bd.work + 1, (unsigned long long)w_reads);
     if (w_writes) atomicAdd(bd.work + 2, (unsigned long long)w_writes);
+    if (w_cells) atomicAdd(bd.work + 4, (unsigned long long)w_cells);
   }
   if (threadIdx.x == 0 && w_staged) atomicAdd(bd.work + 3, w_staged);
 }
@@ -416,7 +537,8 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
 // single-state path would write (a batch state continues like a single state).
 __global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev bd) {
   const int s = blockIdx.x;
-  if (__ldcg(bd.bgo + s) < 0) return;
+  const int go = __ldcg(bd.bgo + s);
+  if (go < 0 || (go >> 30)) return;   // no update, or k_bsparse compacted it
   __shared__ uint64_t s_warp[kBSmallTPB / 32];
   __shared__ uint32_t s_word[kBSmallTPB], s_pre[kBSmallTPB];
   Ctl *c = bctl(bd, s);
@@ -447,6 +569,112 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bcompact(TableDev tb, BatchDev b
   if (threadIdx.x == 0) {
     c->L_out = (int32_t)carry;
     bd.sinfo[s] = make_int2(__ldcg(&c->parity), (int)carry);
+  }
+}
+
+// ------------------------------------------------------------------ a3-a5, sparse states: one CTA per state
+// A state whose active index holds few blocks (bgo bit 30, k_bingest) is
+// updated through its index instead of densely: each active block's valid
+// tuples are checked against the changed variables' new domains (the cell
+// route's test, tile32_cells: a tuple valid before the call stays valid iff
+// tau[x] in D'_x for every changed x, PAPER.md L189-193 -- the tuples Alg. 2's
+// mask keeps), the block is rewritten if it changed, and the surviving blocks
+// form the new order-preserving index at once (a4, chunks of 128 entries,
+// block scan), so k_bcompact skips the state.  Reads L_in 16-byte blocks and
+// one cell word per changed variable per valid tuple (the cells are
+// L2-resident), instead of all W2 blocks.
+__global__ void __launch_bounds__(kBSparseTPB) k_bsparse(TableDev tb, BatchDev bd) {
+  const int s = blockIdx.x;
+  const int go = __ldcg(bd.bgo + s);
+  if (go < 0 || !(go >> 30)) return;
+  __shared__ uint64_t s_warp[kBSparseTPB / 32];
+  Ctl *c = bctl(bd, s);
+  const uint32_t *pl = bfield<const uint32_t>(bd, s, bd.o_plist);
+  const int nchg = (int)__ldcg(pl + 1);
+  const uint32_t ws0 = __ldcg(pl + 4), ws1 = __ldcg(pl + 5);
+  const uint64_t dm0 = ((uint64_t)__ldcg(pl + 9) << 32) | __ldcg(pl + 8);
+  const uint64_t dm1 = nchg > 1 ? (((uint64_t)__ldcg(pl + 11) << 32) | __ldcg(pl + 10)) : ~0ull;
+  const uint32_t sh0 = ws0 & 31u, sh1 = nchg > 1 ? (ws1 & 31u) : 0u;
+  const int64_t cw = tb.cell_words;
+  const uint32_t *cl0 = tb.cells + (ws0 >> 8), *cl1 = tb.cells + (nchg > 1 ? (ws1 >> 8) : (ws0 >> 8));
+  const int ident = __ldcg(&c->identity), par = __ldcg(&c->parity);
+  const int L = ident ? tb.W2 : __ldcg(&c->L);
+  const int32_t *idx_in = ident ? nullptr : bfield<const int32_t>(bd, s, par ? bd.o_idx1 : bd.o_idx0);
+  int32_t *idx_out = bfield<int32_t>(bd, s, par ? bd.o_idx0 : bd.o_idx1);
+  ulonglong2 *T = bfield<ulonglong2>(bd, s, bd.o_T);
+  uint32_t n_writes = 0, n_cells = 0;
+  int carry = 0;
+  for (int base = 0; base < L; base += kBSparseTPB) {
+    const int i = base + threadIdx.x;
+    bool keep = false;
+    int b = 0;
+    if (i < L) {
+      b = idx_in ? __ldcg(idx_in + i) : i;
+      const ulonglong2 t = __ldcg(T + b);
+      uint64_t kx = 0, ky = 0;
+      const int64_t j0 = (int64_t)b * 128;
+      // the block's valid tuples in batches of kSpB: their cell loads are
+      // independent, so a batch costs one round trip to L2
+      uint64_t rx = t.x, ry = t.y;
+      while (rx | ry) {
+        int pos[kSpB];
+        uint32_t c0[kSpB], c1[kSpB];
+#pragma unroll
+        for (int k = 0; k < kSpB; ++k) {
+          pos[k] = -1;
+          if (rx) {
+            pos[k] = __ffsll((long long)rx) - 1;
+            rx &= rx - 1;
+          } else if (ry) {
+            pos[k] = 64 + __ffsll((long long)ry) - 1;
+            ry &= ry - 1;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kSpB; ++k) {
+          c0[k] = c1[k] = 0u;
+          if (pos[k] >= 0) {
+            c0[k] = __ldg(cl0 + (j0 + pos[k]) * cw);
+            c1[k] = __ldg(cl1 + (j0 + pos[k]) * cw);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kSpB; ++k) {
+          if (pos[k] < 0) continue;
+          const uint32_t v0 = (c0[k] >> sh0) & 0xffu, v1 = (c1[k] >> sh1) & 0xffu;
+          if (!((dm0 >> v0) & (dm1 >> v1) & 1ull)) {
+            if (pos[k] >= 64) ky |= 1ull << (pos[k] - 64);
+            else kx |= 1ull << pos[k];
+          }
+          ++n_cells;
+        }
+      }
+      const ulonglong2 nt = make_ulonglong2(t.x & ~kx, t.y & ~ky);
+      if (kx | ky) {
+        T[b] = nt;
+        ++n_writes;
+      }
+      keep = (nt.x | nt.y) != 0ull;
+    }
+    uint64_t total;
+    const uint64_t ex = block_excl_scan<kBSparseTPB>(keep ? 1ull : 0ull, s_warp, total);
+    if (keep) idx_out[carry + (int)ex] = b;
+    carry += (int)total;
+  }
+  if (threadIdx.x == 0) {
+    c->L_out = carry;
+    bd.sinfo[s] = make_int2(par, carry);
+    atomicAdd(bd.work + 1, (unsigned long long)L);
+    atomicAdd(bd.work + 5, 1ull);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    n_writes += __shfl_xor_sync(0xffffffffu, n_writes, o);
+    n_cells += __shfl_xor_sync(0xffffffffu, n_cells, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (n_writes) atomicAdd(bd.work + 2, (unsigned long long)n_writes);
+    if (n_cells) atomicAdd(bd.work + 4, (unsigned long long)n_cells);
   }
 }
 
@@ -652,11 +880,12 @@ __global__ void __launch_bounds__(kBScanTPB) k_bscan(TableDev tb, BatchDev bd, i
 // ------------------------------------------------------------------ a6c-a8: finalize, one CTA per state
 __global__ void __launch_bounds__(kBSmallTPB) k_bfinalize(TableDev tb, const StateDev *__restrict__ states,
                                                          uint64_t *__restrict__ out_dom, int64_t dom_stride,
-                                                         int32_t *__restrict__ out_status) {
+                                                         int32_t *__restrict__ out_status, BatchDev bd) {
   extern __shared__ __align__(16) uint64_t smem[];
   const StateDev &st = states[blockIdx.x];
   if (out_dom) out_dom += (int64_t)blockIdx.x * dom_stride;
   if (out_status) out_status += blockIdx.x;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *bd.ndense = 0;   // k_bupdate is done with the list
   dev_finalize<kBSmallTPB>(tb, st, out_dom, nullptr, out_status, smem);
 }
 

@@ -945,7 +945,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
         kept += __syncthreads_count(cnt != 0);
       }
       if (tid == 0) tcnt[rank] = (uint32_t)kept;
-      if (tb.cells || tb.negative) {
+      if (tb.gather || tb.negative) {
         nv = warp_sum_u32(nv);
         if (lane == 0) atomicAdd(&fs.nvalid, nv);
       }
@@ -994,7 +994,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
         if (rank == 0) c->L_out = tot;
       }
     }
-    if ((tb.cells || tb.negative) && tid == 0) {   // this CTA's valid tuples -> the grid's (read later)
+    if ((tb.gather || tb.negative) && tid == 0) {   // this CTA's valid tuples -> the grid's (read later)
       tcnt[G + rank] = (uint32_t)fs.nvalid;
     }
     __syncthreads();
@@ -1137,7 +1137,7 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
       // misses: scan them (Alg. 3 over the new index) or gather the valid
       // tuples' values (fast_gather_range) -- whichever reads fewer bytes.  Both
       // inputs are final after the probe barrier, so every CTA decides alike.
-      if (tb.cells) {
+      if (tb.gather) {
         __syncthreads();   // every thread has read the barrier's mode from fs.nscan
         if (tid == 0) fs.nscan = __ldcg(&c->nscan);
         unsigned long long v = 0;

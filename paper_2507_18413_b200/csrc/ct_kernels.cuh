@@ -81,6 +81,8 @@ struct TableDev {
                             // each, packed LSB-first (the gather filter of k_fast, ct_fast.cuh)
   int32_t cell_bits;        // 8 or 16
   int32_t cell_words;       // uint32 words per tuple
+  int32_t gather;           // 1: k_fast's filter may use the cells (use_gather); they may also exist for
+                            // the batch update's cell route only (ct_batch.cuh)
   int32_t negative;         // 1: a negative table (f4) on the k_fast path: counting filter (ct_fast.cuh)
   const int32_t *domOnly;   // [n] or nullptr: 1 if x's column has a star cell (short tables, f4), so the
                             // Δ-branch (which drops every tuple whose row has a removed value) is unsound

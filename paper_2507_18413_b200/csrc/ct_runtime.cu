@@ -74,7 +74,7 @@ struct DeviceGuard {
 
 inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-inline int plist_po(int n) { return 4 + (int)round_up(n + 1, 4); }
+inline int plist_po(int) { return 16; }   // header: P, the cell-route descriptor (ct_batch.cuh k_bingest)
 
 // Byte layout of one state's device block.  The persistent prefix [0, persist)
 // is what ct_state_copy moves; the rest is per-call scratch.
@@ -122,6 +122,7 @@ struct ct_table {
   int use_wide = 0;                  // k_wide + k_wide_filter (ct_wide.cuh): many rows, few words
   size_t wide_smem = 0;
   int bt_tw = 0, bt_grid = 0;        // tile-major batch update (ct_batch.cuh): tile width, 0 = per-state kernels
+  int bt_cells = 0;                  // 1: its cell route is on (tuple cells staged next to the support tile)
   size_t bt_smem = 0;
   int neg_occ = 1;                   // k_neg_count CTAs per SM (negative tables)
   int live = 0;   // states + batches alive
@@ -584,6 +585,7 @@ void ct_config_init(ct_config *cfg) {
   cfg->use_graph = 1;
   cfg->use_fused = 1;
   cfg->use_gather = 1;
+  cfg->batch_cells = 1;
 }
 
 ct_status ct_shard_range(int64_t n_tuples, int32_t n_shards, int32_t rank, int64_t *word_begin, int64_t *words) {
@@ -887,6 +889,28 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
       }
     }
   }
+  // gather filter (k_fast, ct_fast.cuh): the local tuples' value offsets, 8 or
+  // 16 bits per cell, for tables whose filter may scan many support rows
+  {
+    int maxd = 1;
+    for (int i = 0; i < n; ++i) maxd = std::max(maxd, dom_size[i]);
+    const bool star_free = kind == CT_TABLE_POSITIVE || (kind == CT_TABLE_SHORT && !any_star);
+    // ... and for the batch update's cell route (8-bit cells, ct_batch.cuh)
+    const bool batch_cells = cfg.batch_cells && !cfg.batch_per_state && kind == CT_TABLE_POSITIVE && maxd <= 256 &&
+                             tb->R >= 1 && bupdate_smem_bytes(tb->R, 32) <= 200 * 1024;
+    if (((cfg.use_gather && tb->use_fast) || batch_cells) && star_free && maxd <= 65536 && tb->t_local > 0) {
+      const int bits = maxd <= 256 ? 8 : 16;
+      const int words = (n * bits + 31) / 32;
+      tb->cells_bytes = (size_t)tb->t_local * words * 4;
+      tb->cells = (uint32_t *)tb->dalloc(tb->cells_bytes);
+      if (!tb->cells) return fail(CT_ENOMEM, "device allocation of %zu bytes of gather cells failed", tb->cells_bytes);
+      tb->dev.cells = tb->cells;
+      tb->dev.cell_bits = bits;
+      tb->dev.cell_words = words;
+      tb->dev.gather = (cfg.use_gather && tb->use_fast) ? 1 : 0;
+    }
+  }
+
   // batches: tile-major update with the support tile in shared memory when all
   // R rows of a tile of >= 8 blocks fit (ct_batch.cuh)
   {
@@ -901,6 +925,16 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     }
     if (tw) {
       tb->bt_smem = bupdate_smem_bytes(tb->R, tw);
+      // cell route (ct_batch.cuh tile32_cells): the tile's tuple cells next to
+      // the support tile, when the table has 8-bit cells and both fit
+      tb->bt_cells = 0;
+      if (tw == 32 && tb->cells && tb->dev.cell_bits == 8 && kind == CT_TABLE_POSITIVE && cfg.batch_cells) {
+        const size_t cb = (size_t)4096 * tb->dev.cell_words * 4;
+        if (tb->bt_smem + cb <= 216 * 1024) {
+          tb->bt_smem += cb;
+          tb->bt_cells = 1;
+        }
+      }
       int occ = 0;
       if (tw == 32) {
         CUDA_TRY(cudaFuncSetAttribute(k_bupdate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->bt_smem));
@@ -945,24 +979,6 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     tb->use_small = tb->use_wide = 0;
     if (!tb->use_fast) tb->use_fused = 0;
     dv.negative = tb->use_fast;
-  }
-
-  // gather filter (k_fast, ct_fast.cuh): the local tuples' value offsets, 8 or
-  // 16 bits per cell, for tables whose filter may scan many support rows
-  {
-    int maxd = 1;
-    for (int i = 0; i < n; ++i) maxd = std::max(maxd, dom_size[i]);
-    const bool star_free = kind == CT_TABLE_POSITIVE || (kind == CT_TABLE_SHORT && !any_star);
-    if (cfg.use_gather && tb->use_fast && star_free && maxd <= 65536 && tb->t_local > 0) {
-      const int bits = maxd <= 256 ? 8 : 16;
-      const int words = (n * bits + 31) / 32;
-      tb->cells_bytes = (size_t)tb->t_local * words * 4;
-      tb->cells = (uint32_t *)tb->dalloc(tb->cells_bytes);
-      if (!tb->cells) return fail(CT_ENOMEM, "device allocation of %zu bytes of gather cells failed", tb->cells_bytes);
-      tb->dev.cells = tb->cells;
-      tb->dev.cell_bits = bits;
-      tb->dev.cell_words = words;
-    }
   }
 
   // ---------------- root state + supports (a1)
@@ -1069,8 +1085,9 @@ ct_status ct_table_info_get(const ct_table *t, ct_table_info *o) {
   o->grid = neg_kernels ? t->sm_count * t->neg_occ : t->use_wide ? 1 : t->use_small ? 1
           : t->use_fast ? t->fast_grid : t->use_fused ? t->fused_grid : 0;
   o->batch_tile = t->bt_tw;
-  o->gather_cell_bits = t->cells ? t->dev.cell_bits : 0;
+  o->gather_cell_bits = t->dev.gather ? t->dev.cell_bits : 0;
   o->kind = t->kind;
+  o->batch_cells = t->bt_cells;
   return CT_OK;
 }
 
@@ -1297,7 +1314,8 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_dom = (uint64_t *)tb->dalloc(io);
   b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
-  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64 + (size_t)n_states * sizeof(int2);
+  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64 + (size_t)n_states * sizeof(int2) +
+                  (size_t)n_states * sizeof(int32_t);   // + the dense-state list
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
   if (b->d_miss && cudaMemsetAsync(b->d_miss, 0, b->miss_bytes, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "batch counter initialisation failed"));
@@ -1334,8 +1352,12 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
     bd.miss2 = b->d_miss + nm;
     bd.nmiss = reinterpret_cast<int32_t *>(b->d_miss + 2 * nm);
     bd.nmiss2 = bd.nmiss + 1;
+    bd.ndense = bd.nmiss + 2;                                                     // zeroed with the region
     bd.work = reinterpret_cast<unsigned long long *>(b->d_miss + 2 * nm + 2);   // 16-byte aligned
-    bd.sinfo = b->d_miss + 2 * nm + 8;                                            // after work[4]
+    bd.sinfo = b->d_miss + 2 * nm + 8;                                            // after work[6]
+    bd.dense = reinterpret_cast<int32_t *>(bd.sinfo + n_states);
+    bd.t_local = tb->t_local;
+    bd.cell_route = tb->bt_cells;
   }
   if (cudaMemcpyAsync(b->d_desc, b->h.data(), b->desc_bytes, cudaMemcpyHostToDevice, tb->stream) != cudaSuccess)
     return cleanup(fail(CT_ECUDA, "descriptor upload failed"));
@@ -1420,6 +1442,7 @@ static ct_status enqueue_batch_tiled(ct_batch *b, const uint64_t *removed, uint6
       k_bupdate<8><<<G, kBTPB, tb->bt_smem, st>>>(tb->dev, b->bd, S, ntiles, nchunk, chunk_states);
   }
   k_bcompact<<<S, kBSmallTPB, 0, st>>>(tb->dev, b->bd);
+  if (tb->bt_cells) k_bsparse<<<S, kBSparseTPB, 0, st>>>(tb->dev, b->bd);
   prof_mark(tb, 1, e, st);
   e = prof_event(tb, st);
   const int64_t pth = (int64_t)S * std::max(tb->R, 1);
@@ -1431,7 +1454,7 @@ static ct_status enqueue_batch_tiled(ct_batch *b, const uint64_t *removed, uint6
   prof_mark(tb, 3, e, st);
   e = prof_event(tb, st);
   k_bfinalize<<<S, kBSmallTPB, finalize_smem_bytes(tb->n, tb->Wd), st>>>(tb->dev, b->d_desc, out_dom, tb->Wd,
-                                                                         out_status);
+                                                                         out_status, b->bd);
   prof_mark(tb, 5, e, st);
   CUDA_TRY(cudaGetLastError());
   return CT_OK;
@@ -1499,14 +1522,19 @@ ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
   return CT_OK;
 }
 
-ct_status ct_batch_work(ct_batch *b, int64_t *out6, int32_t reset) {
-  if (!b || !out6) return fail(CT_EINVAL, "NULL argument");
+ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset) {
+  if (!b || !out8) return fail(CT_EINVAL, "NULL argument");
   DeviceGuard g(b->tb->device);
   CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
-  for (int i = 0; i < 6; ++i) out6[i] = -1;
+  int64_t *out6 = out8;
+  for (int i = 0; i < 8; ++i) out8[i] = -1;
   if (!b->tb->bt_tw) return CT_OK;
-  CUDA_TRY(cudaMemcpy(out6, b->bd.work, 4 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 4 * sizeof(int64_t)));
+  int64_t w6[6];
+  CUDA_TRY(cudaMemcpy(w6, b->bd.work, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 4; ++i) out8[i] = w6[i];
+  out8[6] = w6[4];
+  out8[7] = w6[5];
+  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 6 * sizeof(int64_t)));
   // filter side of the last call: summed over the states' own counters
   std::vector<Ctl> c((size_t)b->S);
   CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,

@@ -53,7 +53,8 @@ class ct_config(ctypes.Structure):
                 ("use_index", ctypes.c_int32), ("use_graph", ctypes.c_int32),
                 ("use_fused", ctypes.c_int32), ("use_gather", ctypes.c_int32),
                 ("launch_shape", ctypes.c_int32), ("grid_override", ctypes.c_int32),
-                ("batch_per_state", ctypes.c_int32), ("search_levels", ctypes.c_int32)]
+                ("batch_per_state", ctypes.c_int32), ("search_levels", ctypes.c_int32),
+                ("batch_cells", ctypes.c_int32)]
 
 CT_SHAPE_AUTO, CT_SHAPE_PHASES, CT_SHAPE_FUSED, CT_SHAPE_FAST, CT_SHAPE_SMALL, CT_SHAPE_WIDE = 0, 1, 2, 3, 4, 5
 SHAPES = {"auto": 0, "phases": 1, "fused": 2, "fast": 3, "small": 4, "wide": 5}
@@ -66,7 +67,8 @@ class ct_table_info(ctypes.Structure):
                 ("word_begin", ctypes.c_int64), ("words", ctypes.c_int64),
                 ("row_stride_words", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
                 ("state_bytes", ctypes.c_int64), ("kernel_path", ctypes.c_int32), ("grid", ctypes.c_int32),
-                ("batch_tile", ctypes.c_int32), ("gather_cell_bits", ctypes.c_int32), ("kind", ctypes.c_int32)]
+                ("batch_tile", ctypes.c_int32), ("gather_cell_bits", ctypes.c_int32), ("kind", ctypes.c_int32),
+                ("batch_cells", ctypes.c_int32)]
 
 KERNEL_PATHS = {0: "per-phase", 1: "k_fused", 2: "k_fast", 3: "k_small", 4: "k_wide", 5: "negative"}
 
@@ -253,7 +255,8 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
                 nccl_unique_id: bytes | None = None, update_policy: int = CT_POLICY_AUTO,
                 use_residues: bool = True, use_index: bool = True, use_graph: bool = True,
                 use_fused: bool = True, use_gather: bool = True, launch_shape: int | str = 0,
-                grid_override: int = 0, batch_per_state: bool = False, search_levels: int = 0):
+                grid_override: int = 0, batch_per_state: bool = False, search_levels: int = 0,
+                batch_cells: bool = True):
     cfg = ct_config()
     lib().ct_config_init(ctypes.byref(cfg))
     cfg.device = device
@@ -275,6 +278,7 @@ def make_config(device: int = 0, stream=None, allocator=None, n_shards: int = 1,
     cfg.grid_override = int(grid_override)
     cfg.batch_per_state = int(bool(batch_per_state))
     cfg.search_levels = int(search_levels)
+    cfg.batch_cells = int(bool(batch_cells))
     return cfg, keep
 
 
@@ -451,10 +455,10 @@ def ct_state_read_table(state, n_words: int) -> np.ndarray:
 
 def ct_batch_work(batch, reset: bool = False) -> dict:
     """Work counters of the tile-major batch path (include/ct.h)."""
-    out = np.zeros(6, dtype=np.int64)
+    out = np.zeros(8, dtype=np.int64)
     _check(lib().ct_batch_work(batch, _np_ptr(out), int(bool(reset))), allow_fail=False)
     keys = ("update_support_words", "table_blocks_read", "table_blocks_written", "support_bytes_staged",
-            "filter_support_words", "probe_misses")
+            "filter_support_words", "probe_misses", "update_cells_checked", "update_sparse_states")
     return {k: int(v) for k, v in zip(keys, out)}
 
 

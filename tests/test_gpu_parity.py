@@ -542,7 +542,7 @@ def make_env(p, cfg, **kw):
     return make(p, **cfg, **kw)
 
 
-def batch_walk(tab, p, S, steps, seed, check_table=False, from_states=None):
+def batch_walk(tab, p, S, steps, seed, check_table=False, from_states=None, work_out=None):
     """S independent policy-P(2, 0.5) walks through ct_propagate_many, each state
     checked against the oracle (status, domains; currTable if asked); FAILed
     slots are restored by ct_batch_copy (odd steps) or ct_batch_restore_dead."""
@@ -580,6 +580,8 @@ def batch_walk(tab, p, S, steps, seed, check_table=False, from_states=None):
                     b.copy(s, tab.root)             # host-driven restore of one slot
                 cur[s] = root_m.copy()              # (even steps: restored by the device kernel)
         b.restore_dead(tab.root)
+    if work_out is not None:
+        work_out.update(b.work())
     b.close()
     return nfail
 
@@ -593,6 +595,23 @@ def test_batch_matches_oracle(shape, path):
     tw = {"c4like": 32, "tw16": 16, "tw8": 8, "perstate": 0, "tinyR": 32, "oneblock": 32}[shape]
     assert tab.info.batch_tile == (tw if path == "tiled" else 0)
     batch_walk(tab, p, S=67, steps=10, seed=1000, check_table=(shape in ("c4like", "tinyR", "oneblock")))
+    tab.close()
+
+
+@pytest.mark.parametrize("cells", [True, False])
+def test_batch_cell_and_sparse_routes(cells):
+    """The tile-major update's cell route (few valid tuples in a (state, tile):
+    each is checked against the new domains instead of OR-ing support rows) and
+    the sparse-state route (k_bsparse: states with few active blocks updated
+    through their index) reach the oracle's results; batch_cells = 0 turns
+    both off.  Long walks so that states become sparse."""
+    p = random_table(6, 50, 200_000, seed=15)
+    tab = make(p, batch_cells=cells)
+    assert tab.info.batch_tile == 32 and tab.info.batch_cells == int(cells)
+    work = {}
+    batch_walk(tab, p, S=48, steps=14, seed=4000, check_table=True, work_out=work)
+    assert (work["update_cells_checked"] > 0) == cells
+    assert (work["update_sparse_states"] > 0) == cells
     tab.close()
 
 
