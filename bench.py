@@ -615,53 +615,72 @@ def measure_c3_e2e(tab, work, rem_host, P, wd, args, world):
 
 
 def sharded_overhead(m, args, dev):
-    """N = 1: the same C3 bulk steps through the SHARDED code path (a 1-rank NCCL
-    communicator: k_fast without finalize, ncclAllReduce of the R+1 flags,
-    k_finalize) vs the unsharded single launch, and the Amdahl projection to 8
-    GPUs (the update streams 1/G of the table, the rest is fixed)."""
+    """N = 1: the same C3 bulk steps through the SHARDED code paths vs the
+    unsharded single launch, and the Amdahl projection to 8 GPUs (SURVEY §8(e):
+    the update streams 1/G of the table, the rest is taken as fixed).
+      nccl: a 1-rank NCCL communicator -- k_fast without finalize,
+            ncclAllReduce of the R+1 flags, k_finalize (three stream operations);
+      peer: the in-kernel NVLink combine (ct_peer_attach) with one rank: the
+            k_fast finalizer stores its flags into the inbox, releases, acquires
+            and ORs them (one kernel; with G ranks the same code stores to G
+            inboxes over NVLink)."""
     import torch
     from paper_2507_18413_b200 import Table
     from paper_2507_18413_b200 import ct as C
     p, wd = m["p"], m["tab"].Wd
-    tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=1, shard_rank=0, nccl_unique_id=C.ct_nccl_unique_id())
     rem_dev = torch.from_numpy(m["rem_host"].view(np.int64)).to(f"cuda:{dev}")
     od = torch.zeros(wd, dtype=torch.int64, device=f"cuda:{dev}")
     sd = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
-    w = tab.root.clone()
-    stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
     P = len(m["rem_host"])
 
-    def run(n):
-        for k in range(n):
-            w.propagate_from_async(tab.root, rem_dev[k % P], od, None, sd)
+    def measure(peer):
+        tab = Table(p.lo, p.d, p.tuples, device=dev, n_shards=1, shard_rank=0,
+                    nccl_unique_id=None if peer else C.ct_nccl_unique_id())
+        if peer:
+            C.ct_peer_attach(tab.handle, [C.ct_peer_export(tab.handle)])
+        w = tab.root.clone()
+        stream = torch.cuda.ExternalStream(tab.stream_ptr, device=f"cuda:{dev}")
 
-    run(args.warmup)
-    w.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    run(args.steps)
-    ev1.record(stream)
-    ev1.synchronize()
-    t_sh = ev0.elapsed_time(ev1) / args.steps * 1e3               # us per step
-    C.ct_table_profile(tab.handle, True)
-    C.ct_table_profile_read(tab.handle, reset=True)
-    run(args.steps)
-    prof = C.ct_table_profile_read(tab.handle, reset=True)
-    tab.close()
+        def run(n):
+            for k in range(n):
+                w.propagate_from_async(tab.root, rem_dev[k % P], od, None, sd)
+
+        run(args.warmup)
+        w.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        run(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        t_sh = ev0.elapsed_time(ev1) / args.steps * 1e3               # us per step
+        C.ct_table_profile(tab.handle, True)
+        C.ct_table_profile_read(tab.handle, reset=True)
+        run(args.steps)
+        prof = C.ct_table_profile_read(tab.handle, reset=True)
+        tab.close()
+        return t_sh, {k: (v[1] / v[0] * 1e3 if v[0] else None) for k, v in prof.items() if v[0]}
+
+    t_nccl, k_nccl = measure(False)
+    t_peer, k_peer = measure(True)
     t1 = m["ms_per_step"] * 1e3
     ph = m["phase_ns"]                                             # k_fast: ingest, update(+barrier), ...
     t_upd = ph[1] / 1e3 if ph and ph[1] > 0 else None
-    proj = {}
-    if t_upd:
+
+    def proj(t_sh):
+        if not t_upd:
+            return {}
         fixed = t1 - t_upd
-        for g in (2, 4, 8):
-            proj[str(g)] = t1 / (t_upd / g + fixed + max(0.0, t_sh - t1))
-    return {"unsharded_us_per_step": t1, "sharded_path_us_per_step": t_sh, "overhead_us": t_sh - t1,
-            "kernels_us_per_launch": {k: (v[1] / v[0] * 1e3 if v[0] else None) for k, v in prof.items() if v[0]},
-            "update_phase_us": t_upd,
-            "amdahl_projected_speedup": proj,
-            "note": "1-rank NCCL communicator on one GPU: the launch/collective cost a sharded call adds; "
-                    "projection = T1 / (T_update/G + (T1 - T_update) + overhead), not a measurement"}
+        return {str(g): t1 / (t_upd / g + fixed + max(0.0, t_sh - t1)) for g in (2, 4, 8)}
+
+    return {"unsharded_us_per_step": t1, "sharded_path_us_per_step": t_nccl, "overhead_us": t_nccl - t1,
+            "kernels_us_per_launch": k_nccl, "update_phase_us": t_upd,
+            "amdahl_projected_speedup": proj(t_nccl),
+            "peer": {"sharded_path_us_per_step": t_peer, "overhead_us": t_peer - t1,
+                     "kernels_us_per_launch": k_peer, "amdahl_projected_speedup": proj(t_peer),
+                     "api": "ct_peer_export / ct_peer_attach (1 rank: the table's own inbox)"},
+            "note": "1 GPU: the cost a sharded call adds (nccl: 1-rank communicator; peer: in-kernel NVLink "
+                    "combine with one rank); projection = T1 / (T_update/G + (T1 - T_update) + overhead), "
+                    "not a measurement"}
 
 
 def run_ours(args):

@@ -430,6 +430,31 @@ ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
  * All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
 ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset);
 
+/* ---- a10 over NVLink peer memory.
+ * Instead of an NCCL all-reduce between two kernels, the k_fast finalizer of a
+ * tuple-range shard stores its R+1 flag bytes into every rank's inbox over
+ * NVLink (CUDA IPC peer pointers), publishes them with a system-scope release,
+ * waits for every rank's flags of the same call and ORs them itself: one
+ * kernel per sharded call.  Collective protocol, every rank in the same order:
+ *   ct_peer_export(table, handle)        -> this rank's inbox as a
+ *                                           CT_PEER_HANDLE_BYTES-byte IPC handle
+ *   (exchange the handles, e.g. torch.distributed.all_gather_object)
+ *   ct_peer_attach(table, n_shards, all) -> handles[n_shards][CT_PEER_HANDLE_BYTES],
+ *                                           rank order; opens the others' inboxes
+ * After attach every sharded call on the table combines in-kernel (the NCCL
+ * communicator, if any, is no longer used by k_fast).  Requirements: the
+ * table runs the k_fast launch shape (ct_table_info.kernel_path 2; CT_EINVAL
+ * otherwise), all ranks on one node with peer access, and a table's sharded
+ * calls issued in the same order on every rank and one at a time (its states
+ * on one stream): the calls are matched by a per-table epoch counter.  With
+ * n_shards = 1 the table exchanges with itself (tests the protocol on one GPU).
+ * Errors: CT_EINVAL (NULL, wrong count, not exported, already attached,
+ * launch shape), CT_ENOMEM, CT_ECUDA (IPC).  A rank that never arrives makes
+ * the others' kernels trap after ct_debug_spin_limit (CT_ECUDA). */
+#define CT_PEER_HANDLE_BYTES 64
+ct_status ct_peer_export(ct_table *t, void *out_handle);
+ct_status ct_peer_attach(ct_table *t, int32_t n_shards, const void *handles);
+
 /* Per-kernel device timing (measurement only).  While enabled, every
  * *_async / ct_propagate_many call on this table's states and batches records a
  * CUDA event pair around each of its kernels on the launching stream (not inside

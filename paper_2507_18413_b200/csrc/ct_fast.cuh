@@ -733,13 +733,56 @@ __device__ __forceinline__ int probe_row(const int32_t *__restrict__ idx_old, in
   return -1;
 }
 
+// ------------------------------------------------------------------ a10 over NVLink: in-kernel flag exchange
+// Tuple-range shards combine their R+1 flag bytes ("row r
+// supported by a valid tuple of my slice", "my slice is non-empty") by OR.
+// With peer inboxes attached (ct_peer_attach) the finalizer CTA of k_fast does
+// it itself instead of a separate all-reduce + finalize launch: it stores its
+// flags into slot (epoch & 1, rank) of every rank's inbox over NVLink (peer
+// pointers from CUDA IPC), publishes them with one system-scope release per
+// rank, waits (acquire) for every rank's flags of the same epoch in its own
+// inbox, and ORs them into st.sup.  Every rank makes the same sequence of
+// sharded calls (SPMD), so the epochs agree; two slots suffice because a rank
+// can write epoch e + 2 only after every rank published e + 1, i.e. finished
+// reading e.  Returns the combined non-empty flag.  All threads of the CTA.
+__device__ int peer_combine(const TableDev &tb, const StateDev &st) {
+  const int tid = threadIdx.x, G = tb.peer_n, me = tb.peer_rank, pw = tb.peer_pw;
+  const int nw = (tb.R + 1 + 3) >> 2;   // the flag bytes as 32-bit words (st.sup is padded to 256 bytes)
+  // drawn by CTA 0 at kernel entry (k_fast), visible here after the completion counter
+  const uint32_t ep = __ldcg(&st.ctl->peer_ep), slot = ep & 1u;
+  const uint32_t *sw = reinterpret_cast<const uint32_t *>(st.sup);
+  for (int g = 0; g < G; ++g) {
+    uint32_t *dst = tb.peers[g] + ((size_t)slot * G + me) * pw;
+    for (int w = tid; w < nw; w += blockDim.x) dst[w] = __ldcg(sw + w);
+  }
+  __syncthreads();
+  const size_t fbase = (size_t)2 * G * pw;
+  if (tid < G) {
+    // the block barrier orders every thread's payload stores before this
+    // thread's system-scope release (cumulative), which publishes them
+    st_release_sys_u32(tb.peers[tid] + fbase + ((size_t)slot * G + me) * 32, ep);
+    const uint32_t *f = tb.inbox + fbase + ((size_t)slot * G + tid) * 32;   // sender tid's flag here
+    SpinGuard sg;
+    while (ld_acquire_sys_u32(f) != ep) spin_check(sg, 5, ep, (unsigned long long)tid, 0);
+  }
+  __syncthreads();
+  uint32_t *out = reinterpret_cast<uint32_t *>(st.sup);
+  for (int w = tid; w < nw; w += blockDim.x) {
+    uint32_t acc = 0;
+    for (int g = 0; g < G; ++g) acc |= __ldcv(tb.inbox + ((size_t)slot * G + g) * pw + w);
+    out[w] = acc;
+  }
+  __syncthreads();
+  return *reinterpret_cast<volatile const uint8_t *>(st.sup + tb.R) != 0;
+}
+
 // ------------------------------------------------------------------ a6c-a8: finalize from shared memory
 // Alg. 3 L3-4 over the filter items this CTA listed in its ingest: a value of
 // x in s_sup leaves the domain iff its row is unsupported; lastDom <- dom.
 // Returns the status; on CT_OK the new domains are left in p.dl (s_nd).
 __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPtrs &p, const FastSh &fs,
                             uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
-                            int32_t *__restrict__ out_status, bool sys_fence) {
+                            int32_t *__restrict__ out_status, bool sys_fence, int nonempty = -1) {
   // ct_propagate_from: the output state's persistent fields are the input's,
   // advanced by this call (in place this is the same as updating them)
   constexpr int NT = kFastTPB;
@@ -749,6 +792,7 @@ __device__ int cta_finalize(const TableDev &tb, const StateDev &st, const FastPt
   if (fs.dead) status = -5;              // CT_ESTATE
   else if (fs.fail) status = 1;          // CT_FAIL: some D_x empty
   else if (fs.noop) status = 0;
+  else if (nonempty >= 0) status = nonempty ? 0 : 1;   // shards: the combined flag (peer_combine)
   else status = fs.Lout > 0 ? 0 : 1;     // currTable empty <=> FAIL (Alg. 1 L5)
   if (status != 0) {
     if (tid == 0) {
@@ -1281,8 +1325,12 @@ finalize:
       out_pruned = st.out + 1 + tb.Wd;
       out_status = reinterpret_cast<int32_t *>(st.out);
     }
+    // with_finalize == 2: tuple-range shards with peer inboxes -- combine the
+    // flags over NVLink first (every rank agrees on dead / fail / noop, so
+    // they all skip the exchange alike)
+    const int ne = (with_finalize == 2 && !(fs.dead || fs.fail || fs.noop)) ? peer_combine(tb, st) : -1;
     fstatus = tb.negative ? cta_finalize_neg(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0, G)
-                          : cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0);
+                          : cta_finalize(tb, st, p, fs, out_dom, out_pruned, out_status, use_state_out != 0, ne);
   }
   if (tid == 0) c->tph[7] = globaltimer();
   if (compact_after) {   // the leader's own index entries, after the outputs
@@ -1306,6 +1354,9 @@ __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, co
   if (threadIdx.x == 0) {
     s_st = states[0];
     if (src_state) s_src = src_state[0];
+    // tuple-range shards combining over NVLink: every call draws the next
+    // epoch (dead / no-op calls too, alike on every rank); the finalizer reads it
+    if (with_finalize == 2 && blockIdx.x == 0) s_st.ctl->peer_ep = atomicAdd(tb.peer_epoch, 1u) + 1u;
   }
   __syncthreads();
   fast_call(tb, s_st, fs, fast_ptrs(smem, tb), removed, nullptr, root_mode, with_finalize, out_dom, out_pruned,

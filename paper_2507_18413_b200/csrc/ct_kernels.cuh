@@ -83,6 +83,12 @@ struct TableDev {
   int32_t cell_words;       // uint32 words per tuple
   int32_t gather;           // 1: k_fast's filter may use the cells (use_gather); they may also exist for
                             // the batch update's cell route only (ct_batch.cuh)
+  // a10 over NVLink peer memory (ct_peer_attach): k_fast's finalizer CTA
+  // exchanges the shard flags with every rank and ORs them itself (peer_combine)
+  uint32_t *const *peers;   // [peer_n] every rank's exchange inbox (this rank's included), or nullptr
+  uint32_t *inbox;          // this rank's inbox: payload [2][peer_n][peer_pw] words, flags [2][peer_n][32]
+  uint32_t *peer_epoch;     // this rank's count of exchanged calls (identical on every rank: SPMD order)
+  int32_t peer_n, peer_rank, peer_pw;
   int32_t negative;         // 1: a negative table (f4) on the k_fast path: counting filter (ct_fast.cuh)
   const int32_t *domOnly;   // [n] or nullptr: 1 if x's column has a star cell (short tables, f4), so the
                             // Δ-branch (which drops every tuple whose row has a removed value) is unsound
@@ -123,7 +129,7 @@ struct Ctl {
   unsigned long long tph[8];   // phase timestamps (%globaltimer, ns); see ct_stats.phase_ns
   int32_t cta_done;    // k_fast: CTAs done with the filter; the last one finalizes
                        // and resets it to 0 (so a copied state always holds 0)
-  int32_t pad[1];
+  uint32_t peer_ep;     // k_fast with peer inboxes: this call's exchange epoch (CTA 0 draws it at entry)
   // negative tables (ct_neg.cuh): valid forbidden tuples after the last call
   // (persists; copied with the state) and this call's running count
   unsigned long long nvalid;
@@ -164,6 +170,14 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");

@@ -97,6 +97,13 @@ struct ct_table {
   int policy = 0, use_res = 1, use_index = 1, use_graph = 1;
   int n_shards = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  // a10 over NVLink peer memory (ct_peer_export / ct_peer_attach)
+  uint32_t *peer_inbox = nullptr;    // this rank's inbox (cudaMalloc: exportable through CUDA IPC)
+  size_t peer_bytes = 0;
+  std::vector<void *> peer_opened;   // other ranks' inboxes opened here
+  uint32_t **d_peers = nullptr;      // device [n] inbox pointers
+  bool peer_on = false;
+  int graph_gen = 0;                 // bumped when the kernels' parameters change (captured graphs go stale)
   std::vector<int32_t> lo, d, rowBase, domOff, scope;
   std::vector<uint64_t> full_dom;    // full-interval domain bitmap
   void *meta = nullptr;
@@ -155,6 +162,7 @@ struct ct_state {
   uint64_t *h_out = nullptr; // pinned [1 + 2 Wd]
   uint64_t *d_in_map = nullptr, *d_out_map = nullptr;   // device aliases of h_in / h_out
   cudaGraphExec_t gexec = nullptr;
+  int gexec_gen = 0;         // tb->graph_gen when gexec was captured
   bool pending = false;      // root of a caller-combined shard before its first apply
 };
 
@@ -427,7 +435,8 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     prof_mark(tb, 7, e, st);
     if (fin_inside || local_only) return CT_OK;
   } else if (tb->use_fast) {
-    const int fin_inside = (!tb->comm && !local_only) ? 1 : 0;
+    // 2: shards combine their flags inside the kernel over NVLink (peer_combine)
+    const int fin_inside = local_only ? 0 : tb->peer_on ? 2 : !tb->comm ? 1 : 0;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)tb->fast_grid);
     lc.blockDim = dim3(kFastTPB);
@@ -563,6 +572,9 @@ static void free_table(ct_table *tb) {
   DeviceGuard g(tb->device);
   if (tb->stream) cudaStreamSynchronize(tb->stream);
   if (tb->comm) ncclCommDestroy(tb->comm);
+  for (void *p : tb->peer_opened) cudaIpcCloseMemHandle(p);
+  if (tb->d_peers) cudaFree(tb->d_peers);
+  if (tb->peer_inbox) cudaFree(tb->peer_inbox);
   for (cudaEvent_t e : tb->ev_pool) cudaEventDestroy(e);
   if (tb->S) tb->dfree(tb->S, tb->S_bytes);
   if (tb->cells) tb->dfree(tb->cells, tb->cells_bytes);
@@ -1101,7 +1113,7 @@ int32_t ct_dom_word_offset(const ct_table *t, int32_t i) {
 ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned) {
   if (!s) return fail(CT_EINVAL, "NULL state");
   ct_table *tb = s->tb;
-  if (tb->n_shards > 1 && !tb->comm)
+  if (tb->n_shards > 1 && !tb->comm && !tb->peer_on)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
   DeviceGuard g(tb->device);
   if (tb->Wd) {
@@ -1110,7 +1122,12 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
   }
   *(volatile int32_t *)s->h_out = kPendingStatus;
   if (tb->use_graph) {
+    if (s->gexec && s->gexec_gen != tb->graph_gen) {   // captured with stale kernel parameters
+      cudaGraphExecDestroy(s->gexec);
+      s->gexec = nullptr;
+    }
     if (!s->gexec) {
+      s->gexec_gen = tb->graph_gen;
       cudaGraph_t graph = nullptr;
       CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
       ct_status st = enqueue_sync_call(s, 0);
@@ -1145,7 +1162,7 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
                              int32_t *out_status) {
   if (!s) return fail(CT_EINVAL, "NULL state");
   ct_table *tb = s->tb;
-  if (tb->n_shards > 1 && !tb->comm)
+  if (tb->n_shards > 1 && !tb->comm && !tb->peer_on)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
   DeviceGuard g(tb->device);
   // removals in host memory: one DMA into the state's device slot (stream
@@ -1172,7 +1189,7 @@ ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint
   if (dst == src) return ct_propagate_async(dst, removed, out_dom, out_pruned, out_status);
   ct_table *tb = dst->tb;
   if (src->tb != tb) return fail(CT_ESTATE, "states belong to different tables");
-  if (tb->n_shards > 1 && !tb->comm)
+  if (tb->n_shards > 1 && !tb->comm && !tb->peer_on)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
   if (src->pending || dst->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine and apply first");
   DeviceGuard g(tb->device);
@@ -1275,6 +1292,71 @@ void ct_state_destroy(ct_state *s) {
     cudaStreamSynchronize(s->stream);
   }
   free_state_mem(s);
+}
+
+// ------------------------------------------------------------------ a10 over NVLink peer memory
+static int peer_pw(const ct_table *tb) { return (int)round_up(((int64_t)tb->R + 1 + 3) / 4, 32); }
+
+ct_status ct_peer_export(ct_table *tb, void *out_handle) {
+  if (!tb || !out_handle) return fail(CT_EINVAL, "NULL argument");
+  DeviceGuard g(tb->device);
+  if (!tb->peer_inbox) {
+    const size_t G = (size_t)std::max(tb->n_shards, 1);
+    tb->peer_bytes = (2 * G * (size_t)peer_pw(tb) + 2 * G * 32 + 32) * 4;
+    if (cudaMalloc(&tb->peer_inbox, tb->peer_bytes) != cudaSuccess) {
+      tb->peer_inbox = nullptr;
+      return fail(CT_ENOMEM, "peer inbox allocation of %zu bytes failed", tb->peer_bytes);
+    }
+    CUDA_TRY(cudaMemset(tb->peer_inbox, 0, tb->peer_bytes));
+  }
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, tb->peer_inbox));
+  static_assert(sizeof h == CT_PEER_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  memcpy(out_handle, &h, sizeof h);
+  return CT_OK;
+}
+
+ct_status ct_peer_attach(ct_table *tb, int32_t n, const void *handles) {
+  if (!tb || !handles) return fail(CT_EINVAL, "NULL argument");
+  const int G = std::max(tb->n_shards, 1);
+  if (n != G) return fail(CT_EINVAL, "ct_peer_attach: %d handles for %d shards", n, G);
+  if (!tb->peer_inbox) return fail(CT_EINVAL, "ct_peer_attach before ct_peer_export");
+  if (tb->peer_on) return fail(CT_EINVAL, "peers already attached");
+  if (!tb->use_fast || tb->use_small || tb->use_wide || tb->kind == CT_TABLE_NEGATIVE)
+    return fail(CT_EINVAL, "the in-kernel peer combine needs the k_fast launch shape (ct_table_info.kernel_path 2)");
+  DeviceGuard dg(tb->device);
+  CUDA_TRY(cudaStreamSynchronize(tb->stream));
+  std::vector<uint32_t *> ptrs((size_t)G, nullptr);
+  const char *hb = static_cast<const char *>(handles);
+  for (int g = 0; g < G; ++g) {
+    if (g == tb->rank) {
+      ptrs[(size_t)g] = tb->peer_inbox;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hb + (size_t)g * CT_PEER_HANDLE_BYTES, sizeof h);
+    void *p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (void *q : tb->peer_opened) cudaIpcCloseMemHandle(q);
+      tb->peer_opened.clear();
+      return fail(CT_ECUDA, "cudaIpcOpenMemHandle of rank %d: %s", g, cudaGetErrorString(e));
+    }
+    tb->peer_opened.push_back(p);
+    ptrs[(size_t)g] = static_cast<uint32_t *>(p);
+  }
+  CUDA_TRY(cudaMalloc(&tb->d_peers, (size_t)G * sizeof(uint32_t *)));
+  CUDA_TRY(cudaMemcpy(tb->d_peers, ptrs.data(), (size_t)G * sizeof(uint32_t *), cudaMemcpyHostToDevice));
+  const int pw = peer_pw(tb);
+  tb->dev.peers = tb->d_peers;
+  tb->dev.inbox = tb->peer_inbox;
+  tb->dev.peer_epoch = tb->peer_inbox + 2 * (size_t)G * pw + 2 * (size_t)G * 32;
+  tb->dev.peer_n = G;
+  tb->dev.peer_rank = tb->rank;
+  tb->dev.peer_pw = pw;
+  tb->peer_on = true;
+  tb->graph_gen += 1;   // every state's captured sync-call graph is re-captured with the new parameters
+  return CT_OK;
 }
 
 void ct_table_destroy(ct_table *t) { free_table(t); }

@@ -148,6 +148,8 @@ SIGNATURES = {
     "ct_batch_read_table": (I32, [P, I32, P]),
     "ct_batch_work": (I32, [P, P, I32]),
     "ct_nccl_unique_id": (I32, [P]),
+    "ct_peer_export": (I32, [P, P]),
+    "ct_peer_attach": (I32, [P, I32, P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
     "ct_table_profile_read": (I32, [P, P, I32]),
@@ -509,6 +511,25 @@ def ct_shard_range(n_tuples: int, n_shards: int, rank: int):
     b, w = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().ct_shard_range(n_tuples, n_shards, rank, ctypes.byref(b), ctypes.byref(w)), allow_fail=False)
     return int(b.value), int(w.value)
+
+
+CT_PEER_HANDLE_BYTES = 64
+
+
+def ct_peer_export(table) -> bytes:
+    """This rank's exchange inbox as a CUDA IPC handle (include/ct.h a10 over NVLink)."""
+    buf = ctypes.create_string_buffer(CT_PEER_HANDLE_BYTES)
+    _check(lib().ct_peer_export(table, buf), allow_fail=False)
+    return buf.raw
+
+
+def ct_peer_attach(table, handles) -> None:
+    """handles: every rank's ct_peer_export bytes, in rank order."""
+    blob = b"".join(bytes(h) for h in handles)
+    if len(blob) != CT_PEER_HANDLE_BYTES * len(handles):
+        raise ValueError("each handle must be CT_PEER_HANDLE_BYTES bytes")
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(lib().ct_peer_attach(table, len(handles), buf), allow_fail=False)
 
 
 def ct_nccl_unique_id() -> bytes:

@@ -9,7 +9,11 @@ slice", plus "my slice is non-empty"); the flags are OR-combined across ranks
 and every rank then applies the same domain update, so the states stay
 bit-identical with no further traffic.  FAIL <=> the combined non-empty byte is 0.
 
-Two combine modes:
+Three combine modes:
+  * "peer": the k_fast finalizer of every rank exchanges the flags with the
+    others through NVLink peer memory and ORs them itself (ct_peer_export /
+    ct_peer_attach; the IPC handles travel through torch.distributed), so a
+    sharded call is ONE kernel; the root propagation (at create) uses NCCL;
   * "nccl" (default): the library owns an NCCL communicator (unique id broadcast
     through torch.distributed) and issues the all-reduce itself, on the table's
     stream, between the filter and finalize kernels -- one graph-capturable call;
@@ -48,6 +52,19 @@ def broadcast_nccl_id(group=None) -> bytes:
     obj = [C.ct_nccl_unique_id() if dist.get_rank(group) == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+def exchange_handles(handle: bytes, group=None) -> list:
+    """Every rank's peer handle, in rank order (all_gather_object: any backend)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(handle), group=group)
+    return out
+
+
+def attach_peers(table_handle, group=None) -> None:
+    """Collective: export this rank's inbox, gather every rank's, attach."""
+    C.ct_peer_attach(table_handle, exchange_handles(C.ct_peer_export(table_handle), group))
 
 
 def combine_flags_(flags, group=None):
@@ -104,11 +121,15 @@ class ShardedTable:
         self.world = dist.get_world_size(group)
         self.mode = mode
         dev = torch.cuda.current_device() if device is None else int(device)
-        nid = broadcast_nccl_id(group) if mode == "nccl" else None
+        if mode not in ("nccl", "torch", "peer"):
+            raise ValueError(f"unknown combine mode {mode!r}")
+        nid = broadcast_nccl_id(group) if mode in ("nccl", "peer") else None
         self.table = Table(lo, d, tuples, device=dev, n_shards=self.world, shard_rank=self.rank,
                            nccl_unique_id=nid, **kw)
-        if mode != "nccl":
+        if mode == "torch":
             finish_pending_root(self.table, lambda f: combine_flags_(f, self.group))
+        if mode == "peer":
+            attach_peers(self.table.handle, self.group)
         self.root = self.table.root
         self.root_status = self.table.root_status
         self.root_dom = self.table.root_dom
@@ -116,7 +137,7 @@ class ShardedTable:
 
     def propagate(self, state, removed=None):
         """Synchronous host call on every rank with identical `removed`."""
-        if self.mode == "nccl":
+        if self.mode in ("nccl", "peer"):
             return state.propagate(removed)
         import torch
         wd = self.Wd

@@ -811,6 +811,43 @@ def test_nccl_single_rank_path(path):
     tab.close()
 
 
+@pytest.mark.parametrize("kind", ["iid", "banded"])
+def test_peer_combine_single_rank(kind):
+    """a10 over NVLink peer memory (ct_peer_attach) with one rank: k_fast's
+    finalizer stores its shard flags into the inbox, releases them at system
+    scope, acquires them back and ORs them before finalizing -- the protocol
+    each of G ranks runs -- and every call of a walk (synchronous calls: the
+    captured graph is re-captured after the attach) matches the oracle.  The
+    banded table drives the filter through misses (gather / scans)."""
+    p = random_table(8, 60, 400_000 + 77, seed=31) if kind == "iid" else banded_table(6, 40, 300_000, seed=8)
+    tab = make(p, _grid_fused=True)
+    assert tab.info.kernel_path == 2
+    st0 = tab.root.clone()
+    st0.propagate(np.zeros(tab.Wd, np.uint64))      # a graph captured before the attach goes stale
+    h = C.ct_peer_export(tab.handle)
+    assert len(h) == C.CT_PEER_HANDLE_BYTES
+    C.ct_peer_attach(tab.handle, [h])
+    with pytest.raises(CTError) as e:                # attach is once per table
+        C.ct_peer_attach(tab.handle, [h])
+    assert e.value.status == C.CT_EINVAL
+    nfail, _ = run_walk(tab, p, calls=150, seed=9, check_table_every=10)
+    st0.close()
+    tab.close()
+
+
+def test_peer_attach_needs_k_fast():
+    p = random_table(5, 20, 30_000, seed=29)          # a k_small table
+    tab = make(p)
+    assert tab.info.kernel_path != 2
+    h = C.ct_peer_export(tab.handle)
+    with pytest.raises(CTError) as e:
+        C.ct_peer_attach(tab.handle, [h])
+    assert e.value.status == C.CT_EINVAL
+    with pytest.raises(CTError):                     # wrong handle count
+        C.ct_peer_attach(tab.handle, [h, h])
+    tab.close()
+
+
 # --------------------------------------------------------------------------- ct_propagate_from_async
 FROM_SHAPES = {"fast": dict(_grid_fused=True), "fast_scan": dict(_grid_fused=True, use_gather=False),
                "fast_noindex": dict(_grid_fused=True, use_index=False), "v1": dict(_grid_fused=True, _fast=False),

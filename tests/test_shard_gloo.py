@@ -15,7 +15,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2507_18413_b200 import ct as C
-from paper_2507_18413_b200.sharded import combine_flags_, shard_ranges, broadcast_nccl_id
+from paper_2507_18413_b200.sharded import combine_flags_, shard_ranges, broadcast_nccl_id, exchange_handles
 
 WORLD = 2
 
@@ -85,6 +85,9 @@ def _worker(rank, world, port, q):
             results["nccl_id_same"] = all(g == got[0] for g in got) and len(got[0]) == 128
         except C.CTError as e:          # no NCCL bootstrap possible on this host
             results["nccl_id_same"] = f"skipped: {e}"
+        # 4) peer-handle exchange (ct_peer_attach's input): rank order, bytes intact
+        fake = bytes([rank + 1]) * C.CT_PEER_HANDLE_BYTES
+        results["handles"] = exchange_handles(fake)
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok", results))
@@ -116,4 +119,5 @@ def test_gloo_world2_shard_protocol():
                 assert got[g + 1][0] % 16 == 0
             assert got == shard_ranges(t, WORLD)
         assert payload["checks"] > 5
+        assert payload["handles"] == [bytes([g + 1]) * C.CT_PEER_HANDLE_BYTES for g in range(WORLD)]
         assert payload["nccl_id_same"] is True or str(payload["nccl_id_same"]).startswith("skipped")
