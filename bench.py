@@ -422,6 +422,22 @@ def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
                 use_gather=use_gather)
     build_s = time.perf_counter() - t0
     assert tab.root_status == CT_OK
+    combine = None
+    if world > 1:
+        # tuple-range shards: the flags are OR-combined inside k_fast over NVLink
+        # peer memory (ct_peer_attach) unless --combine nccl or the attach fails
+        combine = "nccl"
+        if getattr(args, "combine", "peer") == "peer":
+            from paper_2507_18413_b200.sharded import attach_peers
+            try:
+                attach_peers(tab.handle)
+                combine = "peer"
+            except C.CTError as e:
+                print(f"[bench] peer attach failed ({e}); NCCL all-reduce combine", file=sys.stderr)
+        import torch.distributed as dist
+        got = [None] * world
+        dist.all_gather_object(got, combine)
+        assert all(g == got[0] for g in got), got
     root_m = bitmap_to_member(tab.root_dom, p.d)
     P = 16
     pats = bulk_patterns(root_m, p.d, P) if workload == "c3bulk" else fix_patterns(root_m, p.d, P)
@@ -548,7 +564,7 @@ def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
                                 "(L = non-zero currTable words of the call's input / output); sector_floor: the "
                                 "scans at 32-byte-sector granularity (32 x sectors holding a valid tuple x Rm)"),
                 "peak_source": peak_src}
-    out = dict(p=p, tab=tab, work=work, root_m=root_m, pats=pats, rem_host=rem_host, value=value,
+    out = dict(p=p, tab=tab, work=work, root_m=root_m, pats=pats, rem_host=rem_host, value=value, combine=combine,
                ms_per_step=step_ms, build_s=build_s, roofline=roofline, clocks=clk, per_pat=per_pat,
                kernel_ms={k: (v[1] / v[0] if v[0] else None) for k, v in prof.items()},
                kernel_share=k_ms_per_launch / step_ms,
@@ -700,7 +716,8 @@ def run_ours(args):
         cpu = cpu_baseline(p, root_m, pats, budget_s=args.cpu_budget, what=args.workload)
     m["tab"].close()
     if world == 1 and not args.skip_latency and args.workload == "c3bulk":
-        latency = c2_latency(dev)
+        latency = c2_latency(dev, serve=True)
+        latency["launched"] = c2_latency(dev, serve=False)
     if args.workload == "c3bulk" and not args.skip_filter:
         # the filter-heavy C3b line, so the filterDomains roofline is in every default run
         f = measure_c3("c3b", args, dev, world, rank, full=False)
@@ -728,7 +745,7 @@ def run_ours(args):
             "data": "synthetic (seeded " + ("i.i.d." if args.workload == "c3bulk" else "banded") + " table, workloads/)",
             "config": {"workload": args.workload, "table": wl["table"],
                        "step": wl["step"],
-                       "patterns": 16, "parallelism": f"tuple-range shards x{world}" if world > 1 else "1 GPU",
+                       "patterns": 16, "parallelism": f"tuple-range shards x{world}, {m['combine']} flag combine" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (1.0 GB supports streamed each step)",
                        "build_s": round(m["build_s"], 3)},
             "roofline": m["roofline"],
@@ -744,12 +761,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def c2_latency(dev):
-    """p50/p90/p99 of the C call ct_propagate (sync, host buffers, CUDA graph) on
-    config 2: 1000 calls of policy P(2, 0.5) after 100 warm-up calls.  The timer
-    brackets only the foreign call (arguments pre-marshalled), so the number is
-    the library's latency, not Python's.  device_us = the kernel's own duration
-    (%globaltimer phase stamps) for the same calls."""
+def c2_latency(dev, serve=False):
+    """p50/p90/p99 of the C call ct_propagate (sync, host buffers) on config 2:
+    1000 calls of policy P(2, 0.5) after 100 warm-up calls.  The timer brackets
+    only the foreign call (arguments pre-marshalled), so the number is the
+    library's latency, not Python's.  device_us = the kernel's own duration
+    (%globaltimer phase stamps) for the same calls.  serve=False: one CUDA-graph
+    launch per call; serve=True: the state's calls are served by a persistent
+    kernel polling a doorbell in mapped host memory (ct_state_serve; the
+    restores after FAIL / solved stop it, so the next call restarts it)."""
     import ctypes
     from paper_2507_18413_b200 import CT_OK, Table
     from paper_2507_18413_b200 import ct as C
@@ -759,6 +779,8 @@ def c2_latency(dev):
     tab = Table(p.lo, p.d, p.tuples, device=dev)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     st = tab.root.clone()
+    if serve:
+        st.serve(True)
     wd = tab.Wd
     rem = np.zeros(wd, np.uint64)
     out = np.zeros(wd, np.uint64)
@@ -797,7 +819,9 @@ def c2_latency(dev):
     return {"config": "C2 arity 5, domain 20, 1e5 tuples; policy P(2,0.5)", "calls": len(lat),
             "p50_us": q(lat, 0.5), "p90_us": q(lat, 0.9), "p99_us": q(lat, 0.99),
             "device_p50_us": q(dev_us, 0.5), "fails": fails, "restores_solved": solved,
-            "api": "ct_propagate (host buffers; single-CTA kernel in a CUDA graph; zero-copy I/O)"}
+            "api": ("ct_propagate on a served state (ct_state_serve: persistent single-CTA kernel, doorbell and "
+                    "zero-copy I/O in mapped host memory)" if serve else
+                    "ct_propagate (host buffers; single-CTA kernel in a CUDA graph; zero-copy I/O)")}
 
 
 def _time_oracle(p, root_m, pats, budget_s, threads):
@@ -1379,6 +1403,8 @@ def main():
     ap.add_argument("--skip-sharded", action="store_true", help="default line: no sharded-path overhead probe")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-gather", action="store_true", help="c3bulk/c3b: Alg. 3 scans only (ct_config.use_gather = 0)")
+    ap.add_argument("--combine", default="peer", choices=["peer", "nccl"],
+                    help="N > 1 shards: flag combine inside k_fast over NVLink (peer) or an NCCL all-reduce")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -430,6 +430,23 @@ ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
  * All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
 ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset);
 
+/* Served calls (latency-bound tables, BASELINE config 2).  on != 0: the
+ * state's synchronous ct_propagate calls are served by a persistent
+ * single-CTA kernel on the state's own server stream that polls a doorbell in
+ * mapped host memory, instead of one graph launch per call: the call writes
+ * the removal and rings; the kernel (k_small's body) writes domains, pruned
+ * values and the status word straight to mapped host memory.  The server starts
+ * with the first call, stops after ct_debug_serve_idle (default 200 ms)
+ * without a request (the next call restarts it), and is stopped by on = 0,
+ * ct_state_destroy and by every call that writes the state or reads it on a
+ * stream (copies, clones, async / sharded calls, batches from it).  Results
+ * are those of ct_propagate.  Requires the single-CTA launch shape
+ * (ct_table_info.kernel_path 3), one shard and Wd <= 64, else CT_EINVAL; the
+ * state must be used from one host thread.  It occupies one SM while running. */
+ct_status ct_state_serve(ct_state *s, int32_t on);
+/* The served kernel's idle limit (ns, > 0), all states of the process. */
+ct_status ct_debug_serve_idle(int64_t ns);
+
 /* ---- a10 over NVLink peer memory.
  * Instead of an NCCL all-reduce between two kernels, the k_fast finalizer of a
  * tuple-range shard stores its R+1 flag bytes into every rank's inbox over

@@ -90,6 +90,10 @@ class State:
     def copy_from(self, src: "State") -> None:
         C.ct_state_copy(self.handle, src.handle)
 
+    def serve(self, on: bool = True) -> None:
+        """Synchronous calls served by a persistent kernel (ct_state_serve)."""
+        C.ct_state_serve(self.handle, on)
+
     def propagate(self, removed=None, out=None, pruned=None):
         """Synchronous host call.  Returns (status, dom, pruned); dom/pruned are
         None unless status == CT_OK.  out / pruned: optional preallocated

@@ -1393,13 +1393,12 @@ __host__ __device__ inline size_t small_smem_bytes(int n, int Wd, int R) {
   return small_region_bytes(n, Wd) + (size_t)R * 12 + (size_t)R + 32;
 }
 
-__global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const StateDev *__restrict__ states,
-                                                       const uint64_t *__restrict__ removed, int root_mode,
-                                                       int with_finalize, uint64_t *__restrict__ out_dom,
-                                                       uint64_t *__restrict__ out_pruned,
-                                                       int32_t *__restrict__ out_status, int use_state_out) {
-  extern __shared__ __align__(16) uint64_t smem[];
-  const StateDev st = states[0];
+// The whole call (k_small and its served form k_small_serve): `smem` = the
+// dynamic shared memory, small_smem_bytes(n, Wd, R).
+__device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &st, const uint64_t *removed,
+                                           int root_mode, int with_finalize, uint64_t *out_dom,
+                                           uint64_t *out_pruned, int32_t *out_status, int use_state_out,
+                                           uint64_t *smem) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool t0 = tid == 0;
@@ -1547,6 +1546,71 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   small_finalize<kSmallTPB>(tb, st, status, s_pre == 2, s_Lout, out_dom, out_pruned, out_status, smem,
                             onchip ? s_sup : nullptr);
   if (t0) c->tph[5] = c->tph[6] = c->tph[7] = globaltimer();
+}
+
+__global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const StateDev *__restrict__ states,
+                                                       const uint64_t *__restrict__ removed, int root_mode,
+                                                       int with_finalize, uint64_t *__restrict__ out_dom,
+                                                       uint64_t *__restrict__ out_pruned,
+                                                       int32_t *__restrict__ out_status, int use_state_out) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const StateDev st = states[0];
+  small_call(tb, st, removed, root_mode, with_finalize, out_dom, out_pruned, out_status, use_state_out, smem);
+}
+
+// ------------------------------------------------------------------ served calls (ct_state_serve)
+// A persistent k_small for ONE state: thread 0 polls the state's doorbell in
+// mapped host memory (door[0] = the host's request count, door[2] = stop) and
+// each new request runs small_call with the removal copied from the mapped
+// input into shared memory (fresh every request: no cached copy can be stale)
+// and the outputs + status written to the mapped output, exactly as a
+// launched synchronous call -- minus the graph launch.  The server stops on
+// request or after kServeIdleNs without one; either way it first marks
+// door[1] = 2 and never serves again (the host relaunches it for a request it
+// sees unserved), so no request is served twice.
+constexpr int kServeMaxWd = 64;
+__device__ unsigned long long g_serve_idle_ns = 200000000ull;   // 200 ms
+
+__global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const StateDev *__restrict__ states,
+                                                             uint32_t *door, uint32_t last,
+                                                             const uint64_t *h_in) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ uint64_t s_rem[kServeMaxWd];
+  __shared__ uint32_t s_cmd;
+  const StateDev st = states[0];
+  const int tid = threadIdx.x;
+  for (;;) {
+    if (tid == 0) {
+      const unsigned long long t0 = globaltimer();
+      uint32_t cmd = 0;
+      for (;;) {
+        if (*(volatile uint32_t *)(door + 2)) {
+          cmd = 2;
+          break;
+        }
+        const uint32_t q = ld_acquire_sys_u32(door);
+        if (q != last) {
+          last = q;
+          cmd = 1;
+          break;
+        }
+        if (globaltimer() - t0 > g_serve_idle_ns) {
+          cmd = 2;
+          break;
+        }
+      }
+      s_cmd = cmd;
+    }
+    __syncthreads();
+    if (s_cmd == 2) {
+      if (tid == 0) st_release_sys_u32(door + 1, 2u);
+      return;
+    }
+    for (int k = tid; k < tb.Wd; k += kSmallTPB) s_rem[k] = __ldcv(h_in + k);
+    __syncthreads();
+    small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ state copies (backtracking)

@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -163,6 +164,11 @@ struct ct_state {
   uint64_t *d_in_map = nullptr, *d_out_map = nullptr;   // device aliases of h_in / h_out
   cudaGraphExec_t gexec = nullptr;
   int gexec_gen = 0;         // tb->graph_gen when gexec was captured
+  // served calls (ct_state_serve): a persistent k_small_serve polls a doorbell
+  bool serve = false, serving = false;
+  uint32_t *h_door = nullptr, *d_door = nullptr;   // mapped pinned [4]: request count, server state, stop
+  uint32_t srv_seq = 0;      // requests issued
+  cudaStream_t srv_stream = nullptr;
   bool pending = false;      // root of a caller-combined shard before its first apply
 };
 
@@ -503,10 +509,23 @@ static ct_status wait_sync_call(ct_state *s) {
 }
 
 // ------------------------------------------------------------------ state lifetime
+// Stop a state's server (if running) before anything else touches the state.
+static void quiesce(const ct_state *cs) {
+  ct_state *s = const_cast<ct_state *>(cs);
+  if (!s || !s->serving) return;
+  *(volatile uint32_t *)(s->h_door + 2) = 1u;
+  cudaStreamSynchronize(s->srv_stream);
+  *(volatile uint32_t *)(s->h_door + 2) = 0u;
+  s->serving = false;
+}
+
 static void free_state_mem(ct_state *s) {
   if (!s) return;
   ct_table *tb = s->tb;
   DeviceGuard g(tb->device);
+  quiesce(s);
+  if (s->srv_stream) cudaStreamDestroy(s->srv_stream);
+  if (s->h_door) cudaFreeHost(s->h_door);
   // a synchronous call returns once its status word is visible, which the last
   // CTA may write before its final stores: wait for the stream before the
   // memory goes back to the allocator (the torch hook does not synchronize)
@@ -810,8 +829,10 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fused, kFusedTPB, tb->fused_smem));
     if (occ < 1) tb->use_fused = 0;
     tb->small_smem = small_smem_bytes(n, tb->Wd, (int)R);
-    if (tb->small_smem <= 200 * 1024)
+    if (tb->small_smem <= 200 * 1024) {
       CUDA_TRY(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->small_smem));
+      CUDA_TRY(cudaFuncSetAttribute(k_small_serve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->small_smem));
+    }
     tb->fused_occ = std::max(occ, 1);
   }
   tb->scan_occ = std::max(1, tb->scan_occ);
@@ -1109,6 +1130,84 @@ int32_t ct_dom_word_offset(const ct_table *t, int32_t i) {
   return t->domOff[i];
 }
 
+// ------------------------------------------------------------------ served calls (ct_state_serve)
+
+static ct_status launch_server(ct_state *s, uint32_t last) {
+  ct_table *tb = s->tb;
+  CT_TRY(order_after(s->srv_stream, s->stream));   // after the state's earlier work
+  *(volatile uint32_t *)(s->h_door + 1) = 1u;
+  *(volatile uint32_t *)(s->h_door + 2) = 0u;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  k_small_serve<<<1, kSmallTPB, tb->small_smem, s->srv_stream>>>(tb->dev, s->d_desc, s->d_door, last, s->d_in_map);
+  CUDA_TRY(cudaGetLastError());
+  s->serving = true;
+  return CT_OK;
+}
+
+// One ct_propagate on a served state: inputs into the mapped staging, ring
+// the doorbell, wait for the status word (relaunching the server if it had
+// stopped on its idle limit before seeing the request).
+static ct_status served_call(ct_state *s) {
+  if (!s->serving) CT_TRY(launch_server(s, s->srv_seq));
+  const uint32_t req = ++s->srv_seq;
+  std::atomic_thread_fence(std::memory_order_seq_cst);   // the removal and the pending status first
+  *(volatile uint32_t *)s->h_door = req;
+  volatile int32_t *st = (volatile int32_t *)s->h_out;
+  for (uint64_t spin = 1;; ++spin) {
+    if (*st != kPendingStatus) return CT_OK;
+    if (*(volatile uint32_t *)(s->h_door + 1) == 2u) {   // the server stopped without serving this request
+      if (*st != kPendingStatus) return CT_OK;
+      CUDA_TRY(cudaStreamSynchronize(s->srv_stream));
+      if (*st != kPendingStatus) return CT_OK;
+      s->serving = false;
+      CT_TRY(launch_server(s, req - 1));
+    }
+    if ((spin & 4095) == 0) {
+      const cudaError_t e = cudaStreamQuery(s->srv_stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady) {
+        s->serving = false;
+        return fail(CT_ECUDA, "served propagation failed: %s", cudaGetErrorString(e));
+      }
+    }
+  }
+}
+
+ct_status ct_state_serve(ct_state *s, int32_t on) {
+  if (!s) return fail(CT_EINVAL, "NULL state");
+  ct_table *tb = s->tb;
+  DeviceGuard g(tb->device);
+  if (!on) {
+    quiesce(s);
+    s->serve = false;
+    return CT_OK;
+  }
+  if (!tb->use_small || tb->use_wide || tb->n_shards > 1 || tb->kind == CT_TABLE_NEGATIVE || tb->Wd > kServeMaxWd)
+    return fail(CT_EINVAL, "served calls need the single-CTA launch shape (ct_table_info.kernel_path 3), one shard "
+                           "and at most %d domain words", kServeMaxWd);
+  if (s->pending) return fail(CT_ESTATE, "root of a caller-combined shard");
+  if (!s->h_door) {
+    if (cudaHostAlloc((void **)&s->h_door, 64, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer((void **)&s->d_door, s->h_door, 0) != cudaSuccess) {
+      cudaGetLastError();
+      if (s->h_door) cudaFreeHost(s->h_door);
+      s->h_door = nullptr;
+      return fail(CT_ENOMEM, "mapped doorbell allocation failed");
+    }
+    memset(s->h_door, 0, 64);
+    s->srv_seq = 0;
+  }
+  if (!s->srv_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->srv_stream, cudaStreamNonBlocking));
+  s->serve = true;
+  return CT_OK;
+}
+
+ct_status ct_debug_serve_idle(int64_t ns) {
+  if (ns <= 0) return fail(CT_EINVAL, "idle limit must be positive");
+  const unsigned long long v = (unsigned long long)ns;
+  CUDA_TRY(cudaMemcpyToSymbol(g_serve_idle_ns, &v, sizeof v));
+  return CT_OK;
+}
+
 // ------------------------------------------------------------------ propagation
 ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned) {
   if (!s) return fail(CT_EINVAL, "NULL state");
@@ -1121,7 +1220,9 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
     else memset(s->h_in, 0, (size_t)tb->Wd * 8);
   }
   *(volatile int32_t *)s->h_out = kPendingStatus;
-  if (tb->use_graph) {
+  if (s->serve) {
+    CT_TRY(served_call(s));
+  } else if (tb->use_graph) {
     if (s->gexec && s->gexec_gen != tb->graph_gen) {   // captured with stale kernel parameters
       cudaGraphExecDestroy(s->gexec);
       s->gexec = nullptr;
@@ -1148,7 +1249,7 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
   } else {
     CT_TRY(enqueue_sync_call(s, 0));
   }
-  CT_TRY(wait_sync_call(s));
+  if (!s->serve) CT_TRY(wait_sync_call(s));
   const int32_t status = *(volatile const int32_t *)s->h_out;
   if (status == CT_OK) {
     if (out_dom && tb->Wd) memcpy(out_dom, s->h_out + 1, (size_t)tb->Wd * 8);
@@ -1161,6 +1262,7 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
 ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out_dom, uint64_t *out_pruned,
                              int32_t *out_status) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  quiesce(s);
   ct_table *tb = s->tb;
   if (tb->n_shards > 1 && !tb->comm && !tb->peer_on)
     return fail(CT_EINVAL, "sharded table without NCCL: use ct_propagate_local_async/apply_async");
@@ -1186,6 +1288,8 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
 ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint64_t *removed, uint64_t *out_dom,
                                   uint64_t *out_pruned, int32_t *out_status) {
   if (!dst || !src) return fail(CT_EINVAL, "NULL state");
+  quiesce(dst);
+  quiesce(src);
   if (dst == src) return ct_propagate_async(dst, removed, out_dom, out_pruned, out_status);
   ct_table *tb = dst->tb;
   if (src->tb != tb) return fail(CT_ESTATE, "states belong to different tables");
@@ -1211,6 +1315,7 @@ ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint
 
 ct_status ct_propagate_local_async(ct_state *s, const uint64_t *removed) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  quiesce(s);
   if (s->tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "negative tables have no shard-local phase");
   if (s->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   DeviceGuard g(s->tb->device);
@@ -1226,6 +1331,7 @@ ct_status ct_state_flags(ct_state *s, uint8_t **flags_dev, int32_t *n_bytes) {
 
 ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status) {
   if (!s) return fail(CT_EINVAL, "NULL state");
+  quiesce(s);
   if (s->tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "negative tables have no shard-local phase");
   DeviceGuard g(s->tb->device);
   CT_TRY(enqueue_finalize(s->tb, s->d_desc, 1, out_dom, out_pruned, out_status, 0, s->stream));
@@ -1236,6 +1342,7 @@ ct_status ct_propagate_apply_async(ct_state *s, uint64_t *out_dom, uint64_t *out
 // ------------------------------------------------------------------ states
 ct_status ct_state_clone(const ct_state *src, ct_state **out) {
   if (!src || !out) return fail(CT_EINVAL, "NULL argument");
+  quiesce(src);
   if (src->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   ct_table *tb = src->tb;
   DeviceGuard g(tb->device);
@@ -1255,6 +1362,8 @@ ct_status ct_state_copy(ct_state *dst, const ct_state *src) {
   if (!dst || !src) return fail(CT_EINVAL, "NULL argument");
   if (dst->tb != src->tb) return fail(CT_ESTATE, "states belong to different tables");
   if (dst == src) return CT_OK;
+  quiesce(dst);
+  quiesce(src);
   if (src->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
   DeviceGuard g(dst->tb->device);
   CT_TRY(order_after(dst->stream, src->stream));   // the copy reads src after its earlier work
@@ -1266,6 +1375,7 @@ ct_status ct_state_copy(ct_state *dst, const ct_state *src) {
 ct_status ct_state_set_stream(ct_state *s, void *stream) {
   if (!s) return fail(CT_EINVAL, "NULL state");
   if (!stream) return fail(CT_EINVAL, "stream must be a non-legacy cudaStream_t");
+  quiesce(s);
   DeviceGuard g(s->tb->device);
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->stream = (cudaStream_t)stream;
@@ -1365,6 +1475,7 @@ void ct_table_destroy(ct_table *t) { free_table(t); }
 ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, ct_batch **out) {
   if (!tb || !init || !out) return fail(CT_EINVAL, "NULL argument");
   if (init->tb != tb) return fail(CT_ESTATE, "init state belongs to another table");
+  quiesce(init);
   if (n_states < 1 || n_states > 65535) return fail(CT_EINVAL, "n_states must be in [1, 65535]");
   if (tb->n_shards > 1) return fail(CT_EINVAL, "batches of sharded tables are not supported");
   if (tb->kind == CT_TABLE_NEGATIVE) return fail(CT_EINVAL, "batches of negative tables are not supported");
@@ -1461,6 +1572,7 @@ int32_t ct_batch_size(const ct_batch *b) { return b ? b->S : -1; }
 
 ct_status ct_batch_copy(ct_batch *b, int32_t i, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  quiesce(src);
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
   if (i < 0 || i >= b->S) return fail(CT_EINVAL, "batch index %d out of range", i);
   if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
@@ -1473,6 +1585,7 @@ ct_status ct_batch_copy(ct_batch *b, int32_t i, const ct_state *src) {
 
 ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  quiesce(src);
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
   if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
   DeviceGuard g(b->tb->device);
@@ -1485,6 +1598,7 @@ ct_status ct_batch_copy_all(ct_batch *b, const ct_state *src) {
 
 ct_status ct_batch_restore_dead(ct_batch *b, const ct_state *src) {
   if (!b || !src) return fail(CT_EINVAL, "NULL argument");
+  quiesce(src);
   if (src->tb != b->tb) return fail(CT_ESTATE, "state belongs to another table");
   if (src->pending) return fail(CT_ESTATE, "src is a pending shard root");
   DeviceGuard g(b->tb->device);

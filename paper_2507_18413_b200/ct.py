@@ -149,6 +149,8 @@ SIGNATURES = {
     "ct_batch_work": (I32, [P, P, I32]),
     "ct_nccl_unique_id": (I32, [P]),
     "ct_peer_export": (I32, [P, P]),
+    "ct_state_serve": (I32, [P, I32]),
+    "ct_debug_serve_idle": (I32, [I64]),
     "ct_peer_attach": (I32, [P, I32, P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),
@@ -514,6 +516,15 @@ def ct_shard_range(n_tuples: int, n_shards: int, rank: int):
 
 
 CT_PEER_HANDLE_BYTES = 64
+
+
+def ct_state_serve(state, on: bool = True) -> None:
+    """Serve the state's synchronous calls with a persistent kernel (include/ct.h)."""
+    _check(lib().ct_state_serve(state, int(bool(on))), allow_fail=False)
+
+
+def ct_debug_serve_idle(ns: int) -> None:
+    _check(lib().ct_debug_serve_idle(int(ns)), allow_fail=False)
 
 
 def ct_peer_export(table) -> bytes:

@@ -32,13 +32,17 @@ def check_root(tab: Table, p):
     return ok, dout
 
 
-def run_walk(tab: Table, p, calls: int, seed: int, check_table_every: int = 0, m: int = 2, q: float = 0.5):
+def run_walk(tab: Table, p, calls: int, seed: int, check_table_every: int = 0, m: int = 2, q: float = 0.5,
+             serve: bool = False):
     """Policy P(m, q) walk from the root; restore the root after FAIL or when solved.
-    Compares status, domains, pruned set (and currTable every k calls)."""
+    Compares status, domains, pruned set (and currTable every k calls).
+    serve: the walk's state answers through a persistent kernel (ct_state_serve)."""
     ok, root_member = check_root(tab, p)
     assert ok, "walk needs a satisfiable root"
     rng = Rng(seed, lanes=1)
     st = tab.root.clone()
+    if serve:
+        st.serve(True)
     cur = root_member.copy()
     nfail = nsolved = 0
     for k in range(calls):

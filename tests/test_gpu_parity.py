@@ -848,6 +848,60 @@ def test_peer_attach_needs_k_fast():
     tab.close()
 
 
+@pytest.mark.parametrize("shape", ["c2", "tiny"])
+def test_served_walk(shape):
+    """ct_state_serve: a persistent k_small answers the synchronous calls
+    through a doorbell in mapped host memory; every call of a walk (restores
+    after FAIL / solved stop and restart the server) matches the oracle,
+    currTable included."""
+    p = random_table(5, 20, 100_000, seed=1) if shape == "c2" else random_table(3, 5, 300, seed=2)
+    tab = make(p)
+    assert tab.info.kernel_path == 3
+    nfail, nsolved = run_walk(tab, p, calls=300, seed=12, check_table_every=25, serve=True)
+    assert nfail + nsolved > 0
+    tab.close()
+
+
+def test_served_idle_restart():
+    """The server stops on its idle limit; the next call finds it stopped and
+    restarts it (the request is served exactly once)."""
+    import time
+    p = random_table(5, 20, 50_000, seed=3)
+    tab = make(p)
+    root_m = bitmap_to_member(tab.root_dom, p.d)
+    st = tab.root.clone()
+    st.serve(True)
+    C.ct_debug_serve_idle(2_000_000)                  # 2 ms
+    try:
+        rng = Rng(5, lanes=1)
+        cur = root_m.copy()
+        for k in range(12):
+            r = walk_removal(rng, cur, p.d, q=0.2)
+            if r is None:
+                break
+            ok, dout = oracle_call(p, cur & (1 - r))[:2]
+            status, dom, _ = st.propagate(member_to_bitmap(r, p.d))
+            assert status == (CT_OK if ok else CT_FAIL), k
+            if not ok:
+                break
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout), k
+            cur = dout
+            time.sleep(0.01 if k % 2 else 0.0)        # every other call: the server has stopped
+    finally:
+        C.ct_debug_serve_idle(200_000_000)
+    st.close()
+    tab.close()
+
+
+def test_serve_needs_single_cta_shape():
+    p = random_table(5, 20, 30_000, seed=29)
+    tab = make(p, _grid_fused=True)                   # k_fast
+    with pytest.raises(CTError) as e:
+        tab.root.clone().serve(True)
+    assert e.value.status == C.CT_EINVAL
+    tab.close()
+
+
 # --------------------------------------------------------------------------- ct_propagate_from_async
 FROM_SHAPES = {"fast": dict(_grid_fused=True), "fast_scan": dict(_grid_fused=True, use_gather=False),
                "fast_noindex": dict(_grid_fused=True, use_index=False), "v1": dict(_grid_fused=True, _fast=False),
