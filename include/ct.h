@@ -441,11 +441,14 @@ ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset);
  * ct_state_destroy and by every call that writes the state or reads it on a
  * stream (copies, clones, async / sharded calls, batches from it).  Results
  * are those of ct_propagate.  Requires the single-CTA launch shape
- * (ct_table_info.kernel_path 3), one shard and Wd <= 64, else CT_EINVAL; the
+ * (ct_table_info.kernel_path 3), one shard and Wd <= 16, else CT_EINVAL; the
  * state must be used from one host thread.  It occupies one SM while running. */
 ct_status ct_state_serve(ct_state *s, int32_t on);
 /* The served kernel's idle limit (ns, > 0), all states of the process. */
 ct_status ct_debug_serve_idle(int64_t ns);
+/* Experiment builds (-DCT_SERVE_TRACE) only: %globaltimer stamps of the last
+ * served call (out16 = host int64[16]; zeros otherwise). */
+ct_status ct_debug_serve_trace(const ct_state *s, int64_t *out16);
 
 /* ---- a10 over NVLink peer memory.
  * Instead of an NCCL all-reduce between two kernels, the k_fast finalizer of a

@@ -222,6 +222,14 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 // copies every CTA's location and barrier count, and the kernel traps -- a lost
 // arrival then surfaces as CT_ECUDA instead of a GPU spinning forever.
 __device__ unsigned long long g_spin_limit_ns = 4000000000ull;   // 4 s: phases take us to ms
+// experiment builds (-DCT_SERVE_TRACE): k_small_serve stamps points of each
+// served call into its doorbell page (ct_debug_serve_trace)
+#ifdef CT_SERVE_TRACE
+__device__ unsigned long long *g_tr;
+#define SERVE_TRACE(i) do { if (g_tr && threadIdx.x == 0) g_tr[i] = globaltimer(); } while (0)
+#else
+#define SERVE_TRACE(i) do { } while (0)
+#endif
 constexpr int kDiagCtas = 4096;
 __device__ unsigned long long *g_diag;     // host-mapped [kDiagWords] or nullptr
 __device__ uint32_t g_loc[kDiagCtas];      // per-CTA location marker (phase code)
@@ -587,6 +595,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
       rm0 = gdom ? ~__ldcg(gdom + tb.gword[lane]) : (rem ? rem[lane] : 0ull);
     }
     const int dead = __shfl_sync(0xffffffffu, lane == 0 ? c->dead : 0, 0);
+    SERVE_TRACE(2);
     for (int i = lane; i <= n; i += 32) {
       s_rb[i] = tb.rowBase[i];
       s_do[i] = tb.domOff[i];
@@ -621,6 +630,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         if (di) atomicAdd(&s_cs[x], __popcll(di));
       }
       __syncwarp();
+      SERVE_TRACE(3);
       // per variable: s_val, branch (Alg. 2), group sizes -> group starts
       int carry = 0, ngroups = 0, fail = 0;
       for (int base = 0; base < n; base += 32) {
@@ -686,6 +696,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         nrows = ucarry;
         nitems = icarry;
       }
+      SERVE_TRACE(4);
       if (lane == 0) {
         const int L0 = c->L;
         if (sh) {
@@ -714,6 +725,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
       }
     }
   }
+  SERVE_TRACE(5);
   __syncthreads();
 }
 
@@ -1409,6 +1421,7 @@ __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &s
   int32_t *s_res = reinterpret_cast<int32_t *>(ext) + 2 * R;
   uint8_t *s_sup = reinterpret_cast<uint8_t *>(s_res + R);
   if (t0) c->tph[0] = globaltimer();   // phase stamps straight to the state (no registers held)
+  SERVE_TRACE(1);
   // everything the later phases need from the state is requested now, in
   // flight while warp 0 ingests: the residues, and each thread's first entry
   // of both index buffers (the parity is not known yet)
@@ -1430,6 +1443,7 @@ __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &s
   }
   __syncthreads();
   if (t0) c->tph[1] = globaltimer();
+  SERVE_TRACE(6);
   __shared__ int s_go, s_L, s_nrows, s_ident, s_par, s_Lout, s_pre, s_nitems;
   __shared__ uint64_t s_warp[kSmallTPB / 32];
   if (t0) {
@@ -1465,6 +1479,7 @@ __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &s
   }
   __syncthreads();
   if (t0) c->tph[2] = globaltimer();
+  SERVE_TRACE(7);
   // ---- filter (Alg. 3 L3, residues L220): residue probes of every item at
   // once (rows and residues from shared memory: one round trip), then a warp
   // per miss over the new index
@@ -1533,6 +1548,7 @@ __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &s
   }
   __syncthreads();
   if (t0) c->tph[3] = c->tph[4] = globaltimer();
+  SERVE_TRACE(8);
   if (!with_finalize) {
     if (t0) c->tph[5] = c->tph[6] = c->tph[7] = c->tph[4];
     return;
@@ -1559,39 +1575,54 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
 }
 
 // ------------------------------------------------------------------ served calls (ct_state_serve)
-// A persistent k_small for ONE state: thread 0 polls the state's doorbell in
-// mapped host memory (door[0] = the host's request count, door[2] = stop) and
-// each new request runs small_call with the removal copied from the mapped
-// input into shared memory (fresh every request: no cached copy can be stale)
-// and the outputs + status written to the mapped output, exactly as a
-// launched synchronous call -- minus the graph launch.  The server stops on
-// request or after kServeIdleNs without one; either way it first marks
-// door[1] = 2 and never serves again (the host relaunches it for a request it
-// sees unserved), so no request is served twice.
-constexpr int kServeMaxWd = 64;
+// A persistent k_small for ONE state.  The request lives in mapped host memory
+// as tagged 64-bit words, req[k] = seq << 32 | 32-bit half k of the removal
+// bitmap (k < 2 Wd, at least one word): warp 0 polls them in ONE read per
+// lane, and a request is complete when every tag equals the next sequence
+// number (the host writes the words in any order; a partly written request
+// is simply not complete yet), so no second read of the removal is needed.
+// ctl[0] = stop request (host), ctl[1] = 2 once the server has stopped.
+// Each request runs small_call with the removal in shared memory and the
+// outputs + status written to the mapped output, exactly as a launched
+// synchronous call.  The server stops on request or after g_serve_idle_ns
+// without one; either way it first marks ctl[1] = 2 and never serves again
+// (the host relaunches it for a request it sees unserved), so no request is
+// served twice.
+constexpr int kServeMaxWd = 16;   // 2 Wd tagged words <= 32: one per lane of warp 0
 __device__ unsigned long long g_serve_idle_ns = 200000000ull;   // 200 ms
 
 __global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const StateDev *__restrict__ states,
-                                                             uint32_t *door, uint32_t last,
-                                                             const uint64_t *h_in) {
+                                                             const unsigned long long *req, uint32_t *ctl,
+                                                             uint32_t last) {
   extern __shared__ __align__(16) uint64_t smem[];
   __shared__ uint64_t s_rem[kServeMaxWd];
   __shared__ uint32_t s_cmd;
   const StateDev st = states[0];
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nreq = max(2 * tb.Wd, 1);
+#ifdef CT_SERVE_TRACE
+  if (tid == 0) g_tr = reinterpret_cast<unsigned long long *>(ctl + 64);
+#endif
   for (;;) {
-    if (tid == 0) {
+    if (tid < 32) {
       const unsigned long long t0 = globaltimer();
-      uint32_t cmd = 0;
+      const uint32_t want = last + 1u;
+      uint32_t cmd = 0, half = 0;
       for (;;) {
-        if (*(volatile uint32_t *)(door + 2)) {
-          cmd = 2;
+        unsigned long long w = 0;
+        bool ok = true;
+        if (lane < nreq) {
+          w = *(volatile const unsigned long long *)(req + lane);
+          ok = (uint32_t)(w >> 32) == want;
+        }
+        half = (uint32_t)w;
+        if (__all_sync(0xffffffffu, ok)) {
+          cmd = 1;
           break;
         }
-        const uint32_t q = ld_acquire_sys_u32(door);
-        if (q != last) {
-          last = q;
-          cmd = 1;
+        const uint32_t stop = lane == 0 ? *(volatile const uint32_t *)ctl : 0u;
+        if (__shfl_sync(0xffffffffu, stop, 0)) {
+          cmd = 2;
           break;
         }
         if (globaltimer() - t0 > g_serve_idle_ns) {
@@ -1599,16 +1630,18 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const
           break;
         }
       }
-      s_cmd = cmd;
+      if (cmd == 1 && lane < 2 * tb.Wd) reinterpret_cast<uint32_t *>(s_rem)[lane] = half;
+      if (lane == 0) s_cmd = cmd;
+      last = want;
     }
     __syncthreads();
     if (s_cmd == 2) {
-      if (tid == 0) st_release_sys_u32(door + 1, 2u);
+      if (tid == 0) st_release_sys_u32(ctl + 1, 2u);
       return;
     }
-    for (int k = tid; k < tb.Wd; k += kSmallTPB) s_rem[k] = __ldcv(h_in + k);
-    __syncthreads();
+    SERVE_TRACE(0);
     small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem);
+    SERVE_TRACE(15);
     __syncthreads();
   }
 }

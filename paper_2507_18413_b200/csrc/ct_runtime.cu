@@ -166,7 +166,8 @@ struct ct_state {
   int gexec_gen = 0;         // tb->graph_gen when gexec was captured
   // served calls (ct_state_serve): a persistent k_small_serve polls a doorbell
   bool serve = false, serving = false;
-  uint32_t *h_door = nullptr, *d_door = nullptr;   // mapped pinned [4]: request count, server state, stop
+  uint32_t *h_door = nullptr, *d_door = nullptr;   // mapped pinned: [0, 256) tagged request words, then
+                                                   // ctl[0] stop, ctl[1] server state (k_small_serve)
   uint32_t srv_seq = 0;      // requests issued
   cudaStream_t srv_stream = nullptr;
   bool pending = false;      // root of a caller-combined shard before its first apply
@@ -509,13 +510,17 @@ static ct_status wait_sync_call(ct_state *s) {
 }
 
 // ------------------------------------------------------------------ state lifetime
+// served calls (ct_state_serve): the doorbell's layout
+constexpr int kDoorCtl = 64;           // uint32 index of the control words (after 32 tagged request words)
+constexpr size_t kDoorBytes = 512 + 16 * 8;   // + 16 trace stamps at kDoorCtl + 64 (experiment builds)
+
 // Stop a state's server (if running) before anything else touches the state.
 static void quiesce(const ct_state *cs) {
   ct_state *s = const_cast<ct_state *>(cs);
   if (!s || !s->serving) return;
-  *(volatile uint32_t *)(s->h_door + 2) = 1u;
+  *(volatile uint32_t *)(s->h_door + kDoorCtl) = 1u;
   cudaStreamSynchronize(s->srv_stream);
-  *(volatile uint32_t *)(s->h_door + 2) = 0u;
+  *(volatile uint32_t *)(s->h_door + kDoorCtl) = 0u;
   s->serving = false;
 }
 
@@ -831,7 +836,6 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     tb->small_smem = small_smem_bytes(n, tb->Wd, (int)R);
     if (tb->small_smem <= 200 * 1024) {
       CUDA_TRY(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->small_smem));
-      CUDA_TRY(cudaFuncSetAttribute(k_small_serve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tb->small_smem));
     }
     tb->fused_occ = std::max(occ, 1);
   }
@@ -1135,10 +1139,11 @@ int32_t ct_dom_word_offset(const ct_table *t, int32_t i) {
 static ct_status launch_server(ct_state *s, uint32_t last) {
   ct_table *tb = s->tb;
   CT_TRY(order_after(s->srv_stream, s->stream));   // after the state's earlier work
-  *(volatile uint32_t *)(s->h_door + 1) = 1u;
-  *(volatile uint32_t *)(s->h_door + 2) = 0u;
+  *(volatile uint32_t *)(s->h_door + kDoorCtl + 1) = 1u;
+  *(volatile uint32_t *)(s->h_door + kDoorCtl) = 0u;
   std::atomic_thread_fence(std::memory_order_seq_cst);
-  k_small_serve<<<1, kSmallTPB, tb->small_smem, s->srv_stream>>>(tb->dev, s->d_desc, s->d_door, last, s->d_in_map);
+  k_small_serve<<<1, kSmallTPB, tb->small_smem, s->srv_stream>>>(
+      tb->dev, s->d_desc, reinterpret_cast<const unsigned long long *>(s->d_door), s->d_door + kDoorCtl, last);
   CUDA_TRY(cudaGetLastError());
   s->serving = true;
   return CT_OK;
@@ -1150,12 +1155,16 @@ static ct_status launch_server(ct_state *s, uint32_t last) {
 static ct_status served_call(ct_state *s) {
   if (!s->serving) CT_TRY(launch_server(s, s->srv_seq));
   const uint32_t req = ++s->srv_seq;
-  std::atomic_thread_fence(std::memory_order_seq_cst);   // the removal and the pending status first
-  *(volatile uint32_t *)s->h_door = req;
+  std::atomic_thread_fence(std::memory_order_seq_cst);   // the pending status first
+  // the request: the removal's 32-bit halves, each tagged with the sequence number
+  const uint32_t *half = reinterpret_cast<const uint32_t *>(s->h_in);
+  volatile unsigned long long *rq = reinterpret_cast<volatile unsigned long long *>(s->h_door);
+  const int nreq = std::max(2 * s->tb->Wd, 1);
+  for (int k = 0; k < nreq; ++k) rq[k] = ((unsigned long long)req << 32) | (k < 2 * s->tb->Wd ? half[k] : 0u);
   volatile int32_t *st = (volatile int32_t *)s->h_out;
   for (uint64_t spin = 1;; ++spin) {
     if (*st != kPendingStatus) return CT_OK;
-    if (*(volatile uint32_t *)(s->h_door + 1) == 2u) {   // the server stopped without serving this request
+    if (*(volatile uint32_t *)(s->h_door + kDoorCtl + 1) == 2u) {   // the server stopped without serving this request
       if (*st != kPendingStatus) return CT_OK;
       CUDA_TRY(cudaStreamSynchronize(s->srv_stream));
       if (*st != kPendingStatus) return CT_OK;
@@ -1185,19 +1194,29 @@ ct_status ct_state_serve(ct_state *s, int32_t on) {
     return fail(CT_EINVAL, "served calls need the single-CTA launch shape (ct_table_info.kernel_path 3), one shard "
                            "and at most %d domain words", kServeMaxWd);
   if (s->pending) return fail(CT_ESTATE, "root of a caller-combined shard");
+  const size_t ssm = tb->small_smem;
+  if (ssm > 200 * 1024) return fail(CT_EINVAL, "table too large to serve (%zu bytes of shared memory)", ssm);
+  CUDA_TRY(cudaFuncSetAttribute(k_small_serve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm));
   if (!s->h_door) {
-    if (cudaHostAlloc((void **)&s->h_door, 64, cudaHostAllocMapped) != cudaSuccess ||
+    if (cudaHostAlloc((void **)&s->h_door, kDoorBytes, cudaHostAllocMapped) != cudaSuccess ||
         cudaHostGetDevicePointer((void **)&s->d_door, s->h_door, 0) != cudaSuccess) {
       cudaGetLastError();
       if (s->h_door) cudaFreeHost(s->h_door);
       s->h_door = nullptr;
       return fail(CT_ENOMEM, "mapped doorbell allocation failed");
     }
-    memset(s->h_door, 0, 64);
+    memset(s->h_door, 0, kDoorBytes);
     s->srv_seq = 0;
   }
   if (!s->srv_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->srv_stream, cudaStreamNonBlocking));
   s->serve = true;
+  return CT_OK;
+}
+
+ct_status ct_debug_serve_trace(const ct_state *s, int64_t *out16) {
+  if (!s || !out16) return fail(CT_EINVAL, "NULL argument");
+  for (int i = 0; i < 16; ++i)
+    out16[i] = s->h_door ? (int64_t)((volatile unsigned long long *)(s->h_door + kDoorCtl + 64))[i] : 0;
   return CT_OK;
 }
 

@@ -151,6 +151,7 @@ SIGNATURES = {
     "ct_peer_export": (I32, [P, P]),
     "ct_state_serve": (I32, [P, I32]),
     "ct_debug_serve_idle": (I32, [I64]),
+    "ct_debug_serve_trace": (I32, [P, P]),
     "ct_peer_attach": (I32, [P, I32, P]),
     "ct_shard_range": (I32, [I64, I32, I32, P, P]),
     "ct_table_profile": (I32, [P, I32]),

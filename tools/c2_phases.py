@@ -12,6 +12,8 @@ p = random_table(5, 20, 100_000, seed=1)
 tab = Table(p.lo, p.d, p.tuples)
 root_m = bitmap_to_member(tab.root_dom, p.d)
 st = tab.root.clone()
+if "--serve" in sys.argv:
+    st.serve(True)       # ct_state_serve: the persistent kernel answers the calls
 wd = tab.Wd
 rem = np.zeros(wd, np.uint64); out = np.zeros(wd, np.uint64); pr = np.zeros(wd, np.uint64)
 fn = C.lib().ct_propagate
