@@ -696,7 +696,10 @@ __device__ __forceinline__ void bmiss_push(const BatchDev &bd, int2 *list, int *
 // tables with spread-out supports a support is usually a few blocks away), and
 // only then queues the item for k_bscan.  Thread (s, 0) also publishes
 // "currTable non-empty" (sup[R]).
-constexpr int kBProbeNext = 4;
+#ifndef CT_BPROBE_NEXT
+#define CT_BPROBE_NEXT 4
+#endif
+constexpr int kBProbeNext = CT_BPROBE_NEXT;
 __global__ void __launch_bounds__(kBProbeTPB) k_bprobe(TableDev tb, BatchDev bd, int S) {
   const int Rp = max(tb.R, 1), W2 = tb.W2;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -758,7 +761,10 @@ __global__ void __launch_bounds__(kBProbeTPB) k_bprobe(TableDev tb, BatchDev bd,
 // Pass 1: (miss, chunk) units of the second list, chunk-major over the
 // remaining blocks (long scans: values that lost every support, correlated
 // tables), each re-checking the miss's flag between rounds.
-constexpr int kBScanRounds = 4;
+#ifndef CT_BSCAN_ROUNDS
+#define CT_BSCAN_ROUNDS 4
+#endif
+constexpr int kBScanRounds = CT_BSCAN_ROUNDS;
 constexpr int kBScanFirst = kBScanRounds * 32 * kScanUnroll;   // blocks scanned by pass 0
 // Pass 0 with a HALF warp per miss (16 lanes x kScanUnroll entries = 64 index
 // entries per round, the two halves of a warp on two misses), the next miss's
