@@ -944,6 +944,9 @@ def run_c4(args):
         steps = args.steps
         hbm = (16 * (work["table_blocks_read"] + work["table_blocks_written"]) + work["support_bytes_staged"]
                + 2 * work["table_blocks_read"] // 8) / steps
+        # SURVEY §8(d) B_upd's HBM part for a batch step: currTable read + write of
+        # every updating state's ACTIVE input blocks (supports come from L2 / shared memory)
+        alg = 32 * work.get("update_active_blocks_in", 0) / steps
         smem = 8 * work["update_support_words"] / steps
         t = upd_ms / upd_n / 1e3
         peak, peak_src = peaks()
@@ -954,6 +957,10 @@ def run_c4(args):
                     "traffic_kernel": f"ctk::k_bupdate<{tab.info.batch_tile}> only (ncu)",
                     "kernel": f"ctk::k_bupdate<{tab.info.batch_tile}> + ctk::k_bcompact",
                     "bytes_per_launch": hbm, "ms_per_launch": t * 1e3, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": alg, "algorithmic_frac": alg / t / 1e9 / peak,
+                    "bytes_note": "achieved = the bytes the kernels move (every block of a dense state read, "
+                                  "rewritten blocks, support tiles staged); algorithmic = SURVEY B_upd's HBM "
+                                  "part, 32 bytes per active input block of an updating state",
                     "smem": {"achieved": smem / t / 1e9, "peak": smem_peak, "frac": smem / t / 1e9 / smem_peak,
                              "bytes_per_launch": smem,
                              "note": "support words OR-ed by Alg. 2, served from the shared-memory tile "

@@ -419,16 +419,17 @@ ct_status ct_state_stats(const ct_state *s, ct_stats *out);
  * tile-major update (ct_table_info.batch_tile > 0) update_support_words and
  * update_table_writes are per batch only, see ct_batch_work. */
 ct_status ct_batch_stats(const ct_batch *b, ct_stats *out);
-/* Work counters of the tile-major batch path (measurement only).  out8 = host
- * int64[8]: [0] 64-bit support words the update OR-ed (from shared memory),
+/* Work counters of the tile-major batch path (measurement only): [0] 64-bit support words the update OR-ed (from shared memory),
  * [1] 16-byte currTable blocks it read, [2] blocks it rewrote, [3] support
  * (and tuple-cell) bytes staged from global into shared memory, [6] valid
  * tuples the update's cell routes checked, [7] state updates that took the
- * sparse-state route -- [0..3], [6] and [7] summed over all calls since the
- * last reset (reset != 0 zeroes them after the read); [4] support words the
- * filter scans loaded and [5] residue-probe misses, both of the last call.
+ * sparse-state route, [8] the updating states' input active 16-byte blocks
+ * (sum of L_in: the currTable traffic the algorithm needs) -- [0..3] and
+ * [6..8] summed over all calls since the last reset (reset != 0 zeroes them
+ * after the read); [4] support words the filter scans loaded and [5]
+ * residue-probe misses, both of the last call; [9] 0.  out10 = host int64[10].
  * All -1 on the per-state path (batch_tile = 0).  Waits for the stream. */
-ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset);
+ct_status ct_batch_work(ct_batch *b, int64_t *out10, int32_t reset);
 
 /* Served calls (latency-bound tables, BASELINE config 2).  on != 0: the
  * state's synchronous ct_propagate calls are served by a persistent

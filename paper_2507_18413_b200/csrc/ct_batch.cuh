@@ -33,7 +33,10 @@
 
 namespace ctk {
 
-constexpr int kBTPB = 1024;        // k_bupdate threads per CTA
+#ifndef CT_BTPB
+#define CT_BTPB 1024
+#endif
+constexpr int kBTPB = CT_BTPB;     // k_bupdate threads per CTA
 constexpr int kBSmallTPB = 128;    // k_bingest / k_bfinalize threads per CTA (one state each)
 constexpr int kBProbeTPB = 256;
 constexpr int kBScanTPB = 256;
@@ -65,10 +68,11 @@ struct BatchDev {
   int32_t *dense, *ndense;   // [S] states k_bupdate updates (in k_bingest's arrival order) and their
                              // number; k_bfinalize zeroes the count for the next call
   int2 *sinfo;               // [S] per call: (index buffer parity, L_out) of each state, from k_bcompact
-  unsigned long long *work;  // [6] whole batch, summed over calls until ct_batch_work resets them:
+  unsigned long long *work;  // [7] whole batch, summed over calls until ct_batch_work resets them:
                              // update support words, currTable blocks read, blocks rewritten,
                              // support (and cell) bytes staged into shared memory, valid tuples
-                             // checked by the cell routes, states updated by k_bsparse
+                             // checked by the cell routes, states updated by k_bsparse, the updating
+                             // states' input active blocks (sum of L_in: the algorithmic currTable traffic)
 };
 
 __device__ __forceinline__ Ctl *bctl(const BatchDev &b, int s) {
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
       sparse = (__ldcg(pl + 1) > 0u && (int64_t)L * kSparseDiv <= tb.W2) ? 1 : 0;
     }
     bd.bgo[blockIdx.x] = s_go ? (sparse << 30) | (P << 12) | s_nrows : -1;
+    if (s_go) atomicAdd(bd.work + 6, (unsigned long long)(st.ctl->identity ? tb.W2 : st.ctl->L));
     if (s_go && !sparse) bd.dense[atomicAdd(bd.ndense, 1)] = blockIdx.x;
   }
 }

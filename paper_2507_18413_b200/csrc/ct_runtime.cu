@@ -1526,7 +1526,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
   b->d_dom = (uint64_t *)tb->dalloc(io);
   b->d_status = (int32_t *)tb->dalloc((size_t)n_states * 4);
   b->d_bgo = (int32_t *)tb->dalloc((size_t)n_states * 4);
-  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 64 + (size_t)n_states * sizeof(int2) +
+  b->miss_bytes = 2 * (size_t)n_states * std::max(tb->R, 1) * sizeof(int2) + 80 + (size_t)n_states * sizeof(int2) +
                   (size_t)n_states * sizeof(int32_t);   // + the dense-state list
   b->d_miss = (int2 *)tb->dalloc(b->miss_bytes);
   if (b->d_miss && cudaMemsetAsync(b->d_miss, 0, b->miss_bytes, tb->stream) != cudaSuccess)
@@ -1566,7 +1566,7 @@ ct_status ct_batch_create(ct_table *tb, int32_t n_states, const ct_state *init, 
     bd.nmiss2 = bd.nmiss + 1;
     bd.ndense = bd.nmiss + 2;                                                     // zeroed with the region
     bd.work = reinterpret_cast<unsigned long long *>(b->d_miss + 2 * nm + 2);   // 16-byte aligned
-    bd.sinfo = b->d_miss + 2 * nm + 8;                                            // after work[6]
+    bd.sinfo = b->d_miss + 2 * nm + 10;                                           // after work[8]
     bd.dense = reinterpret_cast<int32_t *>(bd.sinfo + n_states);
     bd.t_local = tb->t_local;
     bd.cell_route = tb->bt_cells;
@@ -1737,19 +1737,22 @@ ct_status ct_state_read_table(const ct_state *s, uint64_t *out_bits) {
   return CT_OK;
 }
 
-ct_status ct_batch_work(ct_batch *b, int64_t *out8, int32_t reset) {
-  if (!b || !out8) return fail(CT_EINVAL, "NULL argument");
+ct_status ct_batch_work(ct_batch *b, int64_t *out10, int32_t reset) {
+  int64_t *out8 = out10;
+  if (!b || !out10) return fail(CT_EINVAL, "NULL argument");
   DeviceGuard g(b->tb->device);
   CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
   int64_t *out6 = out8;
-  for (int i = 0; i < 8; ++i) out8[i] = -1;
+  for (int i = 0; i < 10; ++i) out8[i] = -1;
   if (!b->tb->bt_tw) return CT_OK;
-  int64_t w6[6];
-  CUDA_TRY(cudaMemcpy(w6, b->bd.work, 6 * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < 4; ++i) out8[i] = w6[i];
-  out8[6] = w6[4];
-  out8[7] = w6[5];
-  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 6 * sizeof(int64_t)));
+  int64_t w7[7];
+  CUDA_TRY(cudaMemcpy(w7, b->bd.work, 7 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 4; ++i) out8[i] = w7[i];
+  out8[6] = w7[4];
+  out8[7] = w7[5];
+  out8[8] = w7[6];
+  out8[9] = 0;
+  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 7 * sizeof(int64_t)));
   // filter side of the last call: summed over the states' own counters
   std::vector<Ctl> c((size_t)b->S);
   CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,

@@ -460,10 +460,11 @@ def ct_state_read_table(state, n_words: int) -> np.ndarray:
 
 def ct_batch_work(batch, reset: bool = False) -> dict:
     """Work counters of the tile-major batch path (include/ct.h)."""
-    out = np.zeros(8, dtype=np.int64)
+    out = np.zeros(10, dtype=np.int64)
     _check(lib().ct_batch_work(batch, _np_ptr(out), int(bool(reset))), allow_fail=False)
     keys = ("update_support_words", "table_blocks_read", "table_blocks_written", "support_bytes_staged",
-            "filter_support_words", "probe_misses", "update_cells_checked", "update_sparse_states")
+            "filter_support_words", "probe_misses", "update_cells_checked", "update_sparse_states",
+            "update_active_blocks_in")
     return {k: int(v) for k, v in zip(keys, out)}
 
 
