@@ -589,11 +589,19 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     uint64_t dm0 = 0, rm0 = 0;
+    int wv0 = 0;
     if (lane < Wd) {
       dm0 = st.dom[lane];
       // model tables: a value is removed iff the shared (global) domain lost it
       rm0 = gdom ? ~__ldcg(gdom + tb.gword[lane]) : (rem ? rem[lane] : 0ull);
+      wv0 = tb.wordVar[lane];
     }
+    // the row pass's variables, kRowAhead rounds of 32 rows ahead, requested
+    // now with everything else (a latency chain per round otherwise)
+    constexpr int kRowAhead = 4;
+    int rvq[kRowAhead];
+#pragma unroll
+    for (int q = 0; q < kRowAhead; ++q) rvq[q] = q * 32 + lane < R ? tb.rowVar[q * 32 + lane] : 0;
     const int dead = __shfl_sync(0xffffffffu, lane == 0 ? c->dead : 0, 0);
     SERVE_TRACE(2);
     for (int i = lane; i <= n; i += 32) {
@@ -621,7 +629,7 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
       for (int k = lane; k < Wd; k += 32) {
         const uint64_t dm = k == lane ? dm0 : st.dom[k];
         const uint64_t rm = k == lane ? rm0 : (gdom ? ~__ldcg(gdom + tb.gword[k]) : (rem ? rem[k] : 0ull));
-        const int x = tb.wordVar[k];
+        const int x = k == lane ? wv0 : tb.wordVar[k];
         const uint64_t delta = rm & dm, di = dm & ~rm;
         s_din[k] = di;
         s_dl[k] = delta;
@@ -667,9 +675,12 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
         for (int base = 0; base < R; base += 32) {
           const int r = base + lane;
           bool u = false, f = false, useDelta = false;
-          int x = 0;
+          int x = rvq[0];
+#pragma unroll
+          for (int q = 0; q + 1 < kRowAhead; ++q) rvq[q] = rvq[q + 1];
+          const int ra = r + 32 * kRowAhead;
+          rvq[kRowAhead - 1] = ra < R ? tb.rowVar[ra] : 0;
           if (r < R) {
-            x = tb.rowVar[r];
             const int a = r - s_rb[x];
             const int w = s_do[x] + (a >> 6), b = a & 63;
             const int cd = s_cd[x], cs = s_cs[x];
@@ -1330,7 +1341,8 @@ template <int NT>
 __device__ void small_finalize(const TableDev &tb, const StateDev &st, int status, bool noop, int Lout,
                                uint64_t *__restrict__ out_dom, uint64_t *__restrict__ out_pruned,
                                int32_t *__restrict__ out_status, uint64_t *smem,
-                               const uint8_t *s_sup = nullptr) {
+                               const uint8_t *s_sup = nullptr, unsigned long long *tout = nullptr,
+                               uint32_t tag = 0) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, n = tb.n, Wd = tb.Wd;
   const uint64_t *s_din = smem;                                         // dev_ingest: D_x
@@ -1345,7 +1357,8 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
         c->calls += 1;
       }
       c->last_status = status;
-      if (out_status) *out_status = status;
+      if (tout) tout[4 * Wd] = ((unsigned long long)tag << 32) | (uint32_t)status;
+      else if (out_status) *out_status = status;
     }
     return;
   }
@@ -1364,12 +1377,24 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
   for (int k = tid; k < Wd; k += NT) {
     const uint64_t nd = s_nd[k];
     st.dom[k] = nd;
+    if (tout) {
+      // served calls: every output half carries the request's tag, so the host
+      // knows when all have arrived and no system-scope fence is needed
+      const unsigned long long tg = (unsigned long long)tag << 32;
+      const uint64_t pr = s_din[k] & ~nd;
+      tout[2 * k] = tg | (uint32_t)nd;
+      tout[2 * k + 1] = tg | (uint32_t)(nd >> 32);
+      tout[2 * Wd + 2 * k] = tg | (uint32_t)pr;
+      tout[2 * Wd + 2 * k + 1] = tg | (uint32_t)(pr >> 32);
+      continue;
+    }
     if (out_dom) out_dom[k] = nd;
     if (out_pruned) out_pruned[k] = s_din[k] & ~nd;
   }
   __syncthreads();   // then one cumulative system-scope fence by the status writer
   if (tid == 0) {
-    if (out_status) __threadfence_system();
+    if (tout) tout[4 * Wd] = (unsigned long long)tag << 32;   // status CT_OK
+    else if (out_status) __threadfence_system();
     if (!noop && tb.use_index) {
       c->parity ^= 1;
       c->L = Lout;
@@ -1410,7 +1435,8 @@ __host__ __device__ inline size_t small_smem_bytes(int n, int Wd, int R) {
 __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &st, const uint64_t *removed,
                                            int root_mode, int with_finalize, uint64_t *out_dom,
                                            uint64_t *out_pruned, int32_t *out_status, int use_state_out,
-                                           uint64_t *smem) {
+                                           uint64_t *smem, unsigned long long *tout = nullptr,
+                                           uint32_t tag = 0) {
   Ctl *c = st.ctl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool t0 = tid == 0;
@@ -1560,7 +1586,7 @@ __device__ __forceinline__ void small_call(const TableDev &tb, const StateDev &s
   }
   const int status = s_pre == 2 ? 0 : s_pre != 0 ? s_pre : (s_Lout > 0 ? 0 : 1);
   small_finalize<kSmallTPB>(tb, st, status, s_pre == 2, s_Lout, out_dom, out_pruned, out_status, smem,
-                            onchip ? s_sup : nullptr);
+                            onchip ? s_sup : nullptr, tout, tag);
   if (t0) c->tph[5] = c->tph[6] = c->tph[7] = globaltimer();
 }
 
@@ -1589,6 +1615,7 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
 // (the host relaunches it for a request it sees unserved), so no request is
 // served twice.
 constexpr int kServeMaxWd = 16;   // 2 Wd tagged words <= 32: one per lane of warp 0
+constexpr int kServeOutWord = 192;  // uint32 offset from ctl of the tagged outputs: [4 Wd + 1] 64-bit words
 __device__ unsigned long long g_serve_idle_ns = 200000000ull;   // 200 ms
 
 __global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const StateDev *__restrict__ states,
@@ -1596,7 +1623,7 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const
                                                              uint32_t last) {
   extern __shared__ __align__(16) uint64_t smem[];
   __shared__ uint64_t s_rem[kServeMaxWd];
-  __shared__ uint32_t s_cmd;
+  __shared__ uint32_t s_cmd, s_last;
   const StateDev st = states[0];
   const int tid = threadIdx.x, lane = tid & 31;
   const int nreq = max(2 * tb.Wd, 1);
@@ -1631,16 +1658,20 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const
         }
       }
       if (cmd == 1 && lane < 2 * tb.Wd) reinterpret_cast<uint32_t *>(s_rem)[lane] = half;
-      if (lane == 0) s_cmd = cmd;
-      last = want;
+      if (lane == 0) {
+        s_cmd = cmd;
+        s_last = want;
+      }
     }
     __syncthreads();
+    last = s_last;
     if (s_cmd == 2) {
       if (tid == 0) st_release_sys_u32(ctl + 1, 2u);
       return;
     }
     SERVE_TRACE(0);
-    small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem);
+    small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem,
+               reinterpret_cast<unsigned long long *>(ctl + kServeOutWord), last);
     SERVE_TRACE(15);
     __syncthreads();
   }

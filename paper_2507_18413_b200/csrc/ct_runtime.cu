@@ -512,7 +512,8 @@ static ct_status wait_sync_call(ct_state *s) {
 // ------------------------------------------------------------------ state lifetime
 // served calls (ct_state_serve): the doorbell's layout
 constexpr int kDoorCtl = 64;           // uint32 index of the control words (after 32 tagged request words)
-constexpr size_t kDoorBytes = 512 + 16 * 8;   // + 16 trace stamps at kDoorCtl + 64 (experiment builds)
+constexpr size_t kDoorBytes = 2048;   // + 16 trace stamps at kDoorCtl + 64 (experiment builds), the tagged
+                                      // outputs at kDoorCtl + kServeOutWord
 
 // Stop a state's server (if running) before anything else touches the state.
 static void quiesce(const ct_state *cs) {
@@ -1161,13 +1162,30 @@ static ct_status served_call(ct_state *s) {
   volatile unsigned long long *rq = reinterpret_cast<volatile unsigned long long *>(s->h_door);
   const int nreq = std::max(2 * s->tb->Wd, 1);
   for (int k = 0; k < nreq; ++k) rq[k] = ((unsigned long long)req << 32) | (k < 2 * s->tb->Wd ? half[k] : 0u);
-  volatile int32_t *st = (volatile int32_t *)s->h_out;
+  // the outputs come back as tagged 32-bit halves (no fence on the device):
+  // the status word first, then every dom / pruned half of this request
+  const int Wd = s->tb->Wd;
+  volatile const unsigned long long *to =
+      reinterpret_cast<volatile const unsigned long long *>(s->h_door + kDoorCtl + kServeOutWord);
+  auto done = [&]() -> bool {
+    const unsigned long long w = to[4 * Wd];
+    if ((uint32_t)(w >> 32) != req) return false;
+    const int32_t status = (int32_t)(uint32_t)w;
+    if (status == CT_OK) {
+      for (int k = 0; k < 4 * Wd; ++k)
+        if ((uint32_t)(to[k] >> 32) != req) return false;
+      uint32_t *o = reinterpret_cast<uint32_t *>(s->h_out + 1);
+      for (int k = 0; k < 4 * Wd; ++k) o[k] = (uint32_t)to[k];
+    }
+    *(volatile int32_t *)s->h_out = status;
+    return true;
+  };
   for (uint64_t spin = 1;; ++spin) {
-    if (*st != kPendingStatus) return CT_OK;
+    if (done()) return CT_OK;
     if (*(volatile uint32_t *)(s->h_door + kDoorCtl + 1) == 2u) {   // the server stopped without serving this request
-      if (*st != kPendingStatus) return CT_OK;
+      if (done()) return CT_OK;
       CUDA_TRY(cudaStreamSynchronize(s->srv_stream));
-      if (*st != kPendingStatus) return CT_OK;
+      if (done()) return CT_OK;
       s->serving = false;
       CT_TRY(launch_server(s, req - 1));
     }

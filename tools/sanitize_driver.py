@@ -51,7 +51,8 @@ def walk(tab, p, calls, seed, gac=None):
 def main():
     from paper_2507_18413_b200 import ct as C
     C.ct_debug_spin_limit(0, 600.0)   # instrumented CTAs are slow: no watchdog trap
-    which = sys.argv[1:] or ["small", "fast", "fused", "phases", "wide", "batch", "neg", "short", "model"]
+    which = sys.argv[1:] or ["small", "fast", "fused", "phases", "wide", "batch", "batchwalk", "serve", "peer", "neg",
+                             "short", "model"]
     if "small" in which:
         p = random_table(5, 20, 20_000, seed=1)
         t = Table(p.lo, p.d, p.tuples)
@@ -111,6 +112,69 @@ def main():
         b.close()
         t.close()
         print("batch ok", flush=True)
+    if "batchwalk" in which:
+        # several batch steps, so states thin out: the cell route inside
+        # k_bupdate and the sparse-state route (k_bsparse) both run
+        p = random_table(6, 50, 60_000, seed=15)
+        t = Table(p.lo, p.d, p.tuples)
+        ok, root, _ = oracle.gac(p.lo, p.d, p.tuples, np.ones(p.R, np.uint8))
+        S = 32
+        b = t.batch(S)
+        rngs = [Rng(700 + s, lanes=1) for s in range(S)]
+        cur = [root.copy() for _ in range(S)]
+        for step in range(8):
+            rems = []
+            for s in range(S):
+                r = walk_removal(rngs[s], cur[s], p.d)
+                rems.append(r if r is not None else np.zeros(p.R, np.uint8))
+            st, doms = b.propagate(np.stack([member_to_bitmap(r, p.d) for r in rems]))
+            for s in range(S):
+                ok, dout, _ = oracle.gac(p.lo, p.d, p.tuples, cur[s] & (1 - rems[s]))
+                assert st[s] == (CT_OK if ok else CT_FAIL), (step, s)
+                if ok:
+                    assert np.array_equal(bitmap_to_member(doms[s], p.d), dout), (step, s)
+                    cur[s] = dout
+                else:
+                    cur[s] = root.copy()
+            b.restore_dead(t.root)
+        w = b.work()
+        assert w["update_sparse_states"] > 0 and w["update_cells_checked"] > 0, w
+        b.close()
+        t.close()
+        print("batchwalk ok", flush=True)
+    if "serve" in which:
+        p = random_table(5, 20, 20_000, seed=1)
+        t = Table(p.lo, p.d, p.tuples)
+        ok, root, _ = oracle.gac(p.lo, p.d, p.tuples, np.ones(p.R, np.uint8))
+        st = t.root.clone()
+        st.serve(True)
+        rng = Rng(4, lanes=1)
+        cur = root.copy()
+        for _ in range(40):
+            rem = walk_removal(rng, cur, p.d)
+            if rem is None:
+                st.copy_from(t.root)
+                cur = root.copy()
+                continue
+            ok, dout, _ = oracle.gac(p.lo, p.d, p.tuples, cur & (1 - rem))
+            s, dom, _ = st.propagate(member_to_bitmap(rem, p.d))
+            assert s == (CT_OK if ok else CT_FAIL)
+            if ok:
+                assert np.array_equal(bitmap_to_member(dom, p.d), dout)
+                cur = dout
+            else:
+                st.copy_from(t.root)
+                cur = root.copy()
+        st.close()
+        t.close()
+        print("serve ok", flush=True)
+    if "peer" in which:
+        p = random_table(6, 40, 150_000, seed=12)
+        t = Table(p.lo, p.d, p.tuples, launch_shape="fast")
+        C.ct_peer_attach(t.handle, [C.ct_peer_export(t.handle)])
+        walk(t, p, 20, 6)
+        t.close()
+        print("peer ok", flush=True)
     if "neg" in which:
         p = negative_table(3, 12, 1400, seed=31, lo=1)
         t = Table(p.lo, p.d, p.tuples, kind="negative")
