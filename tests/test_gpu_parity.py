@@ -908,6 +908,44 @@ FROM_SHAPES = {"fast": dict(_grid_fused=True), "fast_scan": dict(_grid_fused=Tru
                "small": dict()}
 
 
+def test_pipelined_host_buffer_calls():
+    """Calls kept in flight with pinned host-memory inputs and outputs
+    (bench.py's e2e pattern): every call's removal is DMA'd into one of the
+    state's two device slots on its copy stream while the previous call runs;
+    each call propagates from the root into the work state and writes its
+    outputs to its own host buffers, all checked against the oracle after one
+    sync."""
+    import torch
+    from workloads.policies import bulk_removal
+    p = random_table(6, 30, 300_000 + 5, seed=17)
+    tab = make(p, _grid_fused=True)
+    ok, root_m, _ = oracle_call(p, np.ones(p.R, np.uint8))
+    wd = tab.Wd
+    K = 12
+    rng = Rng(33)
+    rems = [bulk_removal(rng, root_m, p.d, q=0.3 + 0.04 * k) for k in range(K)]
+    pin = lambda n, dt: torch.zeros(n, dtype=dt, pin_memory=True)
+    rbuf = [pin(wd, torch.int64) for _ in range(K)]
+    obuf = [pin(wd, torch.int64) for _ in range(K)]
+    pbuf = [pin(wd, torch.int64) for _ in range(K)]
+    sbuf = [pin(1, torch.int32) for _ in range(K)]
+    for k in range(K):
+        rbuf[k].numpy()[:] = member_to_bitmap(rems[k], p.d).view(np.int64)
+    work = tab.root.clone()
+    for k in range(K):
+        work.propagate_from_async(tab.root, rbuf[k], obuf[k], pbuf[k], sbuf[k])
+    work.synchronize()
+    for k in range(K):
+        din = root_m & (1 - rems[k])
+        okk, dout, _ = oracle_call(p, din)
+        assert int(sbuf[k][0]) == (CT_OK if okk else CT_FAIL), k
+        if okk:
+            assert np.array_equal(bitmap_to_member(obuf[k].numpy().view(np.uint64), p.d), dout), k
+            assert np.array_equal(bitmap_to_member(pbuf[k].numpy().view(np.uint64), p.d), din & (1 - dout)), k
+    work.close()
+    tab.close()
+
+
 @pytest.mark.parametrize("shape", list(FROM_SHAPES))
 def test_propagate_from_walk(shape):
     """dst := src propagated (one pass on k_fast, copy + call elsewhere): a

@@ -22,7 +22,7 @@ timeout 900 ncu $NCUF -k regex:k_fast -s 25 -c 2 -o $O/prof_fast_c3 python bench
 timeout 900 ncu $NCUF -k regex:k_fast -s 25 -c 2 -o $O/prof_fast_c3b python bench.py --workload c3b --steps 5 --warmup 3 --skip-cpu > $O/ncu_full_c3b.log 2>&1
 timeout 900 ncu $NCUF -k regex:k_fast -s 25 -c 2 -o $O/prof_fast_c3b_scan python bench.py --workload c3b --no-gather --steps 5 --warmup 3 --skip-cpu > $O/ncu_full_c3b_scan.log 2>&1
 timeout 600 ncu $NCUL -c 400 --log-file $O/launches_c4.csv python bench.py --workload c4 --steps 5 --warmup 3 --skip-cpu > $O/ncu_launch_c4.log 2>&1
-timeout 900 ncu $NCUF -k regex:k_bupdate -s 8 -c 1 -o $O/prof_bupdate_c4 python bench.py --workload c4 --steps 10 --warmup 3 --skip-cpu > $O/ncu_full_c4.log 2>&1
-timeout 900 ncu $NCUF -k regex:k_neg_count -s 25 -c 2 -o $O/prof_neg python bench.py --workload neg --steps 5 --warmup 3 > $O/ncu_full_neg.log 2>&1
+timeout 900 ncu $NCUF -k regex:k_bupdate -s 13 -c 5 -o $O/prof_bupdate_c4 python bench.py --workload c4 --steps 20 --warmup 3 --skip-cpu > $O/ncu_full_c4.log 2>&1
+timeout 900 ncu $NCUF -k regex:k_fast -s 25 -c 2 -o $O/prof_fast_neg python bench.py --workload neg --steps 5 --warmup 3 > $O/ncu_full_neg.log 2>&1
 timeout 600 ncu $NCUL -c 300 --log-file $O/launches_neg.csv python bench.py --workload neg --steps 20 --warmup 3 > $O/ncu_launch_neg.log 2>&1
 grep -E "rror" $O/ncu_*.log | head
