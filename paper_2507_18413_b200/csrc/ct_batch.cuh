@@ -207,7 +207,10 @@ __global__ void __launch_bounds__(kBSmallTPB) k_bingest(TableDev tb, const State
     }
     bd.bgo[blockIdx.x] = s_go ? (sparse << 30) | (P << 12) | s_nrows : -1;
     if (s_go) atomicAdd(bd.work + 6, (unsigned long long)(st.ctl->identity ? tb.W2 : st.ctl->L));
-    if (s_go && !sparse) bd.dense[atomicAdd(bd.ndense, 1)] = blockIdx.x;
+    if (s_go && !sparse) {
+      const int at = atomicAdd(bd.ndense, 1);
+      if (at < (int)gridDim.x) bd.dense[at] = blockIdx.x;   // (grid = S states)
+    }
   }
 }
 
@@ -301,7 +304,9 @@ __device__ __forceinline__ ulonglong2 tile32_cells(const uint32_t *s_cells, int 
   const uint32_t d1l = __shfl_sync(0xffffffffu, dsc, 10), d1h = __shfl_sync(0xffffffffu, dsc, 11);
   const uint64_t dm0 = ((uint64_t)d0h << 32) | d0l;
   const uint64_t dm1 = nchg > 1 ? (((uint64_t)d1h << 32) | d1l) : ~0ull;   // one variable: accept all
-  const uint32_t *c0 = s_cells + (ws0 >> 8) * 4096 + lane, *c1 = s_cells + (ws1 >> 8) * 4096 + lane;
+  // (one changed variable: the second slot reads the first's word, harmlessly)
+  const uint32_t *c0 = s_cells + (ws0 >> 8) * 4096 + lane;
+  const uint32_t *c1 = s_cells + ((nchg > 1 ? ws1 : ws0) >> 8) * 4096 + lane;
   const uint32_t sh0 = ws0 & 31u, sh1 = nchg > 1 ? (ws1 & 31u) : 0u;
   // the block as four 32-bit words: the remaining bits (a, b, c, d) are
   // visited lowest first, one per iteration, and a failed tuple's bit is
@@ -363,7 +368,7 @@ __global__ void __launch_bounds__(kBTPB, 1) k_bupdate(TableDev tb, BatchDev bd, 
   const int64_t units = (int64_t)ntiles * nchunk;
   const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
   int cur_tile = -1;
-  const int nd = __ldcg(bd.ndense);   // states on the list (k_bingest)
+  const int nd = min(__ldcg(bd.ndense), S);   // states on the list (k_bingest)
   uint32_t w_loads = 0, w_writes = 0, w_reads = 0, w_cells = 0;   // this lane's share of the batch work counters
   unsigned long long w_staged = 0;
   for (int64_t u = u0; u < u1; ++u) {
