@@ -525,6 +525,87 @@ __device__ __forceinline__ uint32_t fast_update_entry(const TableDev &tb, const 
   return (uint32_t)(__popcll(nt.x) + __popcll(nt.y));
 }
 
+// The update of a CTA's index range [k_lo, k_hi) with Q lanes per entry: when
+// the index is short against the grid's threads (a small table with many
+// support rows, or a state deep in a search), one thread per entry would walk
+// all of the entry's update rows alone (t = 1e6, R = 800: 400 dependent-ish
+// loads, the grid mostly idle).  Here the Q lanes of an entry split each
+// variable's rows (lane j: rows j, j + Q, ...; kSplitU in flight), OR-reduce
+// the group with shuffles and AND it in (Alg. 2: the same
+// per-variable OR, complemented for the Δ-branch, ANDed over the changed
+// variables); a block that died skips the rest (L175).  The variables' groups
+// come from the ingest's per-word list positions (upos, dof): no group table.
+#ifndef CT_SPLIT_U
+#define CT_SPLIT_U 8
+#endif
+constexpr int kSplitU = CT_SPLIT_U;   // rows in flight per lane (sweep 4 / 8 / 16)
+template <int Q>
+__device__ __forceinline__ void fast_update_range_split(const TableDev &tb, const StateDev &st, const FastSh &fs,
+                                                        const FastPtrs &p, int k_lo, int k_hi, uint32_t &n_loads,
+                                                        uint32_t &n_writes, uint32_t &nv, int &kept) {
+  const int tid = threadIdx.x, sub = tid & (Q - 1);
+  const StateDev &in = *fs.in;
+  const int32_t *__restrict__ idx_in = fs.par ? in.idx1 : in.idx0;
+  const ulonglong2 *__restrict__ Tin = reinterpret_cast<const ulonglong2 *>(in.T);
+  ulonglong2 *__restrict__ T2 = reinterpret_cast<ulonglong2 *>(st.T);
+  const int64_t Wp = tb.Wp;
+  const int n = tb.n;
+  for (int base = k_lo; base < k_hi; base += kFastTPB / Q) {
+    const int k = base + tid / Q;
+    const bool valid = k < k_hi;
+    int pid = 0;
+    ulonglong2 tw = make_ulonglong2(0ull, 0ull);
+    if (valid) {
+      pid = fs.ident ? k : idx_in[k];
+      tw = Tin[pid];
+    }
+    const uint64_t *__restrict__ col = tb.S + 2 * (int64_t)pid;
+    uint64_t mx = ~0ull, my = ~0ull;
+    bool live = valid && (tw.x | tw.y) != 0ull;
+    for (int x = 0; x < n; ++x) {
+      const int s0 = p.upos[p.dof[x]], s1 = p.upos[p.dof[x + 1]];
+      if (s0 == s1) continue;   // x not in s_val (shared-memory values: uniform)
+      uint64_t ax = 0, ay = 0;
+      if (live) {
+        for (int r0 = s0 + sub; r0 < s1; r0 += Q * kSplitU) {
+          ulonglong2 v[kSplitU];
+#pragma unroll
+          for (int u = 0; u < kSplitU; ++u) {
+            const int r = r0 + u * Q;
+            v[u] = r < s1 ? ld_sup2(col + (int64_t)(p.ulist[r] & kRowMask) * Wp) : make_ulonglong2(0ull, 0ull);
+            n_loads += r < s1 ? 2u : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < kSplitU; ++u) {
+            ax |= v[u].x;
+            ay |= v[u].y;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = Q / 2; o > 0; o >>= 1) {
+        ax |= __shfl_xor_sync(0xffffffffu, ax, o);
+        ay |= __shfl_xor_sync(0xffffffffu, ay, o);
+      }
+      const uint64_t inv = (p.vfl[x] & 1) ? ~0ull : 0ull;   // Δ-branch: AND the complement
+      mx &= ax ^ inv;
+      my &= ay ^ inv;
+      live = live && ((tw.x & mx) | (tw.y & my)) != 0ull;
+    }
+    uint32_t cnt = 0;
+    if (valid && sub == 0) {
+      const ulonglong2 nt = make_ulonglong2(tw.x & mx, tw.y & my);
+      if (nt.x != tw.x || nt.y != tw.y || fs.from) {
+        T2[pid] = nt;
+        ++n_writes;
+      }
+      cnt = (uint32_t)(__popcll(nt.x) + __popcll(nt.y));
+    }
+    nv += cnt;
+    kept += __syncthreads_count(cnt != 0);
+  }
+}
+
 // ct_propagate_from: blocks outside the source's index are zero in the source
 // but stale in the output, so each CTA zeroes the gaps between its own index
 // entries (the last CTA with entries also after the last one; rank 0 all of
@@ -982,11 +1063,23 @@ __device__ __forceinline__ int fast_call(const TableDev &tb, const StateDev &st,
     {
       int kept = 0;
       uint32_t nv = 0;   // valid tuples of this thread's blocks (the gather filter's cost model)
-      for (int base = k_lo; base < k_hi; base += kFastTPB) {
-        const int k = base + tid;
-        const uint32_t cnt = k < k_hi ? fast_update_entry(tb, st, fs, p.ulist, k, n_loads, n_writes) : 0u;
-        nv += cnt;
-        kept += __syncthreads_count(cnt != 0);
+      // lanes per index entry: 1, or more when the index is short against the grid
+      int q = 1;
+      while (q < 32 && (int64_t)(2 * q) * fs.L <= (int64_t)G * kFastTPB) q *= 2;
+      switch (q) {
+        case 1:
+          for (int base = k_lo; base < k_hi; base += kFastTPB) {
+            const int k = base + tid;
+            const uint32_t cnt = k < k_hi ? fast_update_entry(tb, st, fs, p.ulist, k, n_loads, n_writes) : 0u;
+            nv += cnt;
+            kept += __syncthreads_count(cnt != 0);
+          }
+          break;
+        case 2: fast_update_range_split<2>(tb, st, fs, p, k_lo, k_hi, n_loads, n_writes, nv, kept); break;
+        case 4: fast_update_range_split<4>(tb, st, fs, p, k_lo, k_hi, n_loads, n_writes, nv, kept); break;
+        case 8: fast_update_range_split<8>(tb, st, fs, p, k_lo, k_hi, n_loads, n_writes, nv, kept); break;
+        case 16: fast_update_range_split<16>(tb, st, fs, p, k_lo, k_hi, n_loads, n_writes, nv, kept); break;
+        default: fast_update_range_split<32>(tb, st, fs, p, k_lo, k_hi, n_loads, n_writes, nv, kept); break;
       }
       if (tid == 0) tcnt[rank] = (uint32_t)kept;
       if (tb.gather || tb.negative) {

@@ -1418,6 +1418,7 @@ __device__ void small_finalize(const TableDev &tb, const StateDev &st, int statu
 constexpr int kSmallTPB = CT_SMALL_TPB;   // experiment builds: -DCT_SMALL_TPB=256|512
 constexpr int kWarpIngestMaxRows = 1024;   // k_small ingests with one warp up to this many support rows
 constexpr int kSmallMaxPairs = 8192;
+constexpr int64_t kSmallMaxWork = 1 << 20;   // W2 x R block-rows above which a table leaves k_small (16 MB)
 
 // Dynamic shared memory of k_small: the ingest / finalize region, then (warp
 // ingest only) the update list, the filter items, the residues and the

@@ -934,6 +934,10 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
         // largest index (W2 entries) is at most kFastTPB entries
         const int per_sm = (int)((dv.W2 + (int64_t)tb->sm_count * kFastTPB - 1) / ((int64_t)tb->sm_count * kFastTPB));
         tb->fast_grid = tb->sm_count * std::max(1, std::min(occ, per_sm));
+        // heavy calls on a short index (W2 x R >= 4M block-rows, e.g. t = 1e6 with
+        // R = 800): the whole resident grid, its update splitting each entry's
+        // rows over several lanes (fast_update_range_split)
+        if ((int64_t)dv.W2 * tb->R >= (int64_t)1 << 22) tb->fast_grid = tb->sm_count * occ;
         if (tb->fused_grid_override > 0) tb->fast_grid = std::min(tb->sm_count * occ, tb->fused_grid_override);
       }
     }
@@ -1010,6 +1014,14 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
     int small_max = kSmallMaxPairs;
     if (cfg.launch_shape == CT_SHAPE_FUSED || cfg.launch_shape == CT_SHAPE_FAST) small_max = 0;
     tb->use_small = (tb->use_fused && dv.W2 <= small_max) ? 1 : 0;
+    // ... but not when one call may stream more support rows than one CTA
+    // should (W2 x R block-rows: a call removing from every variable reads up
+    // to ~W2 x R / 2 of them; t = 1e6, R = 800: 100 MB in one CTA = 0.6 ms),
+    // unless the table is a k_wide candidate (many rows over few words: the
+    // filter dominates there and k_wide spreads it over a grid)
+    if (tb->use_small && (int64_t)dv.W2 * tb->R > kSmallMaxWork && tb->R < kWideMinRows &&
+        cfg.launch_shape != CT_SHAPE_SMALL)
+      tb->use_small = 0;
   }
   // ... unless the filter dominates: many support rows over few words (k_wide)
   {

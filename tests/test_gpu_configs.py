@@ -7,6 +7,8 @@ bench.py times (SURVEY §8(d) "Oracle timing" / parity rows):
   C4        4096 states x 100 batch steps of the 1e6-tuple table: all 4096
             states for the first 3 steps, then 128 seeded states for all 100
   C5        12 tables x 1e6 tuples: the first 1000 DFS nodes' trace vs oracle.dfs
+  C3 / C3b at t = 1e6 (the HBM target's second size): a 300-call
+            walk, and 3 calls fixing x0 (gather filter and Alg. 3 scans)
 
 The oracle runs its tuple scan over every host core (oracle_gac_split, pinned
 to the single-thread oracle in tests/test_oracle.py); every oracle input comes
@@ -110,3 +112,35 @@ def test_c5_first_1000_nodes_full_size():
     assert (stats.failures, stats.solutions) == (ref["failures"], len(ref["solutions"]))
     assert stats.trace_hash == ref["trace_hash"]
     M.close()
+
+
+@pytest.mark.timeout(900)
+def test_c3_walk_1e6():
+    p = random_table(8, 100, 1_000_000, seed=3)
+    tab = Table(p.lo, p.d, p.tuples)
+    nfail, nsolved = run_walk(tab, p, calls=300, seed=11, check_table_every=50)
+    tab.close()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("gather", [True, False])
+def test_c3b_banded_1e6(gather):
+    p = banded_table(8, 100, 1_000_000, seed=4)
+    tab = Table(p.lo, p.d, p.tuples, use_gather=gather)
+    ok, root_m = check_root(tab, p)
+    assert ok
+    rng = Rng(12)
+    st = tab.root.clone()
+    for k in range(3):
+        rem = fix_one_value_removal(rng, root_m, p.d, var=0)
+        din = root_m & (1 - rem)
+        ok, dout, valid = oracle_call(p, din, want_valid=True)
+        st.copy_from(tab.root)
+        status, dom, pr = st.propagate(member_to_bitmap(rem, p.d))
+        assert status == (CT_OK if ok else CT_FAIL), k
+        if ok:
+            assert np.array_equal(bitmap_to_member(dom, p.d), dout), k
+            assert np.array_equal(bitmap_to_member(pr, p.d), din & (1 - dout)), k
+            assert np.array_equal(bits_to_bool(st.read_table(), p.t), valid), k
+    st.close()
+    tab.close()

@@ -407,7 +407,7 @@ def test_boundary_fast_rows(d, expect):
 @pytest.mark.parametrize("d,expect", [(1023, "k_small"), (1024, "k_wide")])
 def test_boundary_wide_rows(d, expect):
     """k_wide takes over from k_small at R = 2048 support rows."""
-    p = random_table(2, d, 300_000 + 9, seed=65)
+    p = random_table(2, d, 30_000 + 9, seed=65)   # W2 x R under k_small's work limit
     tab = make(p)
     assert C.KERNEL_PATHS[tab.info.kernel_path] == expect
     run_walk(tab, p, calls=40, seed=66, check_table_every=8)
