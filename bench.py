@@ -442,18 +442,22 @@ def measure_c3(workload, args, dev, world, rank, full=True, use_gather=True):
     if world > 1:
         # tuple-range shards: the flags are OR-combined inside k_fast over NVLink
         # peer memory (ct_peer_attach) unless --combine nccl or the attach fails
+        import torch.distributed as dist
         combine = "nccl"
         if getattr(args, "combine", "peer") == "peer":
-            from paper_2507_18413_b200.sharded import attach_peers
-            try:
+            # every rank must reach every other rank's memory (peer access over
+            # NVLink) before any rank attaches: decided together, attached together
+            devs = [None] * world
+            dist.all_gather_object(devs, dev)
+            ok = all(torch.cuda.can_device_access_peer(dev, o) for o in devs if o != dev)
+            oks = [None] * world
+            dist.all_gather_object(oks, ok)
+            if all(oks):
+                from paper_2507_18413_b200.sharded import attach_peers
                 attach_peers(tab.handle)
                 combine = "peer"
-            except C.CTError as e:
-                print(f"[bench] peer attach failed ({e}); NCCL all-reduce combine", file=sys.stderr)
-        import torch.distributed as dist
-        got = [None] * world
-        dist.all_gather_object(got, combine)
-        assert all(g == got[0] for g in got), got
+            else:
+                print("[bench] no peer access between all ranks' GPUs: NCCL all-reduce combine", file=sys.stderr)
     root_m = bitmap_to_member(tab.root_dom, p.d)
     P = 16
     pats = bulk_patterns(root_m, p.d, P) if iid else fix_patterns(root_m, p.d, P)
