@@ -440,9 +440,10 @@ ct_status ct_batch_work(ct_batch *b, int64_t *out10, int32_t reset);
  * with the first call, stops after ct_debug_serve_idle (default 200 ms)
  * without a request (the next call restarts it), and is stopped by on = 0,
  * ct_state_destroy and by every call that writes the state or reads it on a
- * stream (copies, clones, async / sharded calls, batches from it).  Results
- * are those of ct_propagate.  Requires the single-CTA launch shape
- * (ct_table_info.kernel_path 3), one shard and Wd <= 16, else CT_EINVAL; the
+ * stream (clones, async / sharded calls, batches from it); ct_state_copy
+ * INTO a running served state (a search's restore) is served in place.
+ * Results are those of ct_propagate.  Requires the single-CTA launch shape
+ * (ct_table_info.kernel_path 3), one shard and Wd <= 14, else CT_EINVAL; the
  * state must be used from one host thread.  It occupies one SM while running. */
 ct_status ct_state_serve(ct_state *s, int32_t on);
 /* The served kernel's idle limit (ns, > 0), all states of the process. */

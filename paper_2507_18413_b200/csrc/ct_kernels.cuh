@@ -1601,83 +1601,6 @@ __global__ void __launch_bounds__(kSmallTPB, 1) k_small(TableDev tb, const State
   small_call(tb, st, removed, root_mode, with_finalize, out_dom, out_pruned, out_status, use_state_out, smem);
 }
 
-// ------------------------------------------------------------------ served calls (ct_state_serve)
-// A persistent k_small for ONE state.  The request lives in mapped host memory
-// as tagged 64-bit words, req[k] = seq << 32 | 32-bit half k of the removal
-// bitmap (k < 2 Wd, at least one word): warp 0 polls them in ONE read per
-// lane, and a request is complete when every tag equals the next sequence
-// number (the host writes the words in any order; a partly written request
-// is simply not complete yet), so no second read of the removal is needed.
-// ctl[0] = stop request (host), ctl[1] = 2 once the server has stopped.
-// Each request runs small_call with the removal in shared memory and the
-// outputs + status written to the mapped output, exactly as a launched
-// synchronous call.  The server stops on request or after g_serve_idle_ns
-// without one; either way it first marks ctl[1] = 2 and never serves again
-// (the host relaunches it for a request it sees unserved), so no request is
-// served twice.
-constexpr int kServeMaxWd = 16;   // 2 Wd tagged words <= 32: one per lane of warp 0
-constexpr int kServeOutWord = 192;  // uint32 offset from ctl of the tagged outputs: [4 Wd + 1] 64-bit words
-__device__ unsigned long long g_serve_idle_ns = 200000000ull;   // 200 ms
-
-__global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const StateDev *__restrict__ states,
-                                                             const unsigned long long *req, uint32_t *ctl,
-                                                             uint32_t last) {
-  extern __shared__ __align__(16) uint64_t smem[];
-  __shared__ uint64_t s_rem[kServeMaxWd];
-  __shared__ uint32_t s_cmd, s_last;
-  const StateDev st = states[0];
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int nreq = max(2 * tb.Wd, 1);
-#ifdef CT_SERVE_TRACE
-  if (tid == 0) g_tr = reinterpret_cast<unsigned long long *>(ctl + 64);
-#endif
-  for (;;) {
-    if (tid < 32) {
-      const unsigned long long t0 = globaltimer();
-      const uint32_t want = last + 1u;
-      uint32_t cmd = 0, half = 0;
-      for (;;) {
-        unsigned long long w = 0;
-        bool ok = true;
-        if (lane < nreq) {
-          w = *(volatile const unsigned long long *)(req + lane);
-          ok = (uint32_t)(w >> 32) == want;
-        }
-        half = (uint32_t)w;
-        if (__all_sync(0xffffffffu, ok)) {
-          cmd = 1;
-          break;
-        }
-        const uint32_t stop = lane == 0 ? *(volatile const uint32_t *)ctl : 0u;
-        if (__shfl_sync(0xffffffffu, stop, 0)) {
-          cmd = 2;
-          break;
-        }
-        if (globaltimer() - t0 > g_serve_idle_ns) {
-          cmd = 2;
-          break;
-        }
-      }
-      if (cmd == 1 && lane < 2 * tb.Wd) reinterpret_cast<uint32_t *>(s_rem)[lane] = half;
-      if (lane == 0) {
-        s_cmd = cmd;
-        s_last = want;
-      }
-    }
-    __syncthreads();
-    last = s_last;
-    if (s_cmd == 2) {
-      if (tid == 0) st_release_sys_u32(ctl + 1, 2u);
-      return;
-    }
-    SERVE_TRACE(0);
-    small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem,
-               reinterpret_cast<unsigned long long *>(ctl + kServeOutWord), last);
-    SERVE_TRACE(15);
-    __syncthreads();
-  }
-}
-
 // ------------------------------------------------------------------ state copies (backtracking)
 // Byte offsets / sizes of the persistent fields of a state block.
 struct CopyLayout {
@@ -1725,6 +1648,94 @@ __global__ void __launch_bounds__(256) k_restore_dead(char *__restrict__ pool, s
   __syncthreads();
   if (!s_dead) return;
   copy_state_fields(dst, src, cl, threadIdx.x, blockDim.x);
+}
+
+// ------------------------------------------------------------------ served calls (ct_state_serve)
+// A persistent k_small for ONE state.  The request lives in mapped host memory
+// as tagged 64-bit words, req[k] = seq << 32 | payload: k < 2 Wd the 32-bit
+// halves of the removal bitmap, then the operation (0 propagate, 1 copy from
+// another state of the table: the restore of a search, served in place so the
+// server keeps running) and the source state's address (two halves).  Warp 0
+// polls them in ONE read per lane, and a request is complete when every tag
+// equals the next sequence number (the host writes the words in any order; a
+// partly written request is simply not complete yet).
+// ctl[0] = stop request (host), ctl[1] = 2 once the server has stopped.
+// Each request runs small_call with the removal in shared memory and the
+// outputs + status written to the mapped output, exactly as a launched
+// synchronous call.  The server stops on request or after g_serve_idle_ns
+// without one; either way it first marks ctl[1] = 2 and never serves again
+// (the host relaunches it for a request it sees unserved), so no request is
+// served twice.
+constexpr int kServeMaxWd = 14;   // 2 Wd + 3 tagged words <= 32: one per lane of warp 0
+constexpr int kServeOutWord = 192;  // uint32 offset from ctl of the tagged outputs: [4 Wd + 1] 64-bit words
+__device__ unsigned long long g_serve_idle_ns = 200000000ull;   // 200 ms
+
+__global__ void __launch_bounds__(kSmallTPB, 1) k_small_serve(TableDev tb, const StateDev *__restrict__ states,
+                                                             const unsigned long long *req, uint32_t *ctl,
+                                                             uint32_t last, CopyLayout cl) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  __shared__ uint64_t s_rem[kServeMaxWd];
+  __shared__ uint32_t s_cmd, s_last, s_op, s_src[2];
+  const StateDev st = states[0];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int nreq = 2 * tb.Wd + 3;
+#ifdef CT_SERVE_TRACE
+  if (tid == 0) g_tr = reinterpret_cast<unsigned long long *>(ctl + 64);
+#endif
+  for (;;) {
+    if (tid < 32) {
+      const unsigned long long t0 = globaltimer();
+      const uint32_t want = last + 1u;
+      uint32_t cmd = 0, half = 0;
+      for (;;) {
+        unsigned long long w = 0;
+        bool ok = true;
+        if (lane < nreq) {
+          w = *(volatile const unsigned long long *)(req + lane);
+          ok = (uint32_t)(w >> 32) == want;
+        }
+        half = (uint32_t)w;
+        if (__all_sync(0xffffffffu, ok)) {
+          cmd = 1;
+          break;
+        }
+        const uint32_t stop = lane == 0 ? *(volatile const uint32_t *)ctl : 0u;
+        if (__shfl_sync(0xffffffffu, stop, 0)) {
+          cmd = 2;
+          break;
+        }
+        if (globaltimer() - t0 > g_serve_idle_ns) {
+          cmd = 2;
+          break;
+        }
+      }
+      if (cmd == 1 && lane < 2 * tb.Wd) reinterpret_cast<uint32_t *>(s_rem)[lane] = half;
+      if (cmd == 1 && lane == 2 * tb.Wd) s_op = half;
+      if (cmd == 1 && lane > 2 * tb.Wd && lane < nreq) s_src[lane - 2 * tb.Wd - 1] = half;
+      if (lane == 0) {
+        s_cmd = cmd;
+        s_last = want;
+      }
+    }
+    __syncthreads();
+    last = s_last;
+    if (s_cmd == 2) {
+      if (tid == 0) st_release_sys_u32(ctl + 1, 2u);
+      return;
+    }
+    unsigned long long *tout = reinterpret_cast<unsigned long long *>(ctl + kServeOutWord);
+    if (s_op == 1) {   // restore: this state := the source state (copy_state_fields), then the tagged OK
+      const char *src = reinterpret_cast<const char *>(((unsigned long long)s_src[1] << 32) | s_src[0]);
+      copy_state_fields(reinterpret_cast<char *>(st.ctl), src, cl, threadIdx.x, blockDim.x);
+      __syncthreads();
+      if (tid == 0) tout[4 * tb.Wd] = (unsigned long long)last << 32;
+      continue;
+    }
+    SERVE_TRACE(0);
+    small_call(tb, st, s_rem, 0, 1, nullptr, nullptr, nullptr, 1, smem, tout, last);
+    SERVE_TRACE(15);
+    __syncthreads();
+  }
 }
 
 }  // namespace ctk

@@ -1177,7 +1177,8 @@ static ct_status launch_server(ct_state *s, uint32_t last) {
   *(volatile uint32_t *)(s->h_door + kDoorCtl) = 0u;
   std::atomic_thread_fence(std::memory_order_seq_cst);
   k_small_serve<<<1, kSmallTPB, tb->small_smem, s->srv_stream>>>(
-      tb->dev, s->d_desc, reinterpret_cast<const unsigned long long *>(s->d_door), s->d_door + kDoorCtl, last);
+      tb->dev, s->d_desc, reinterpret_cast<const unsigned long long *>(s->d_door), s->d_door + kDoorCtl, last,
+      copy_layout(tb));
   CUDA_TRY(cudaGetLastError());
   s->serving = true;
   return CT_OK;
@@ -1186,15 +1187,22 @@ static ct_status launch_server(ct_state *s, uint32_t last) {
 // One ct_propagate on a served state: inputs into the mapped staging, ring
 // the doorbell, wait for the status word (relaunching the server if it had
 // stopped on its idle limit before seeing the request).
-static ct_status served_call(ct_state *s) {
+// src != nullptr: a restore request (this state := src, served in place).
+static ct_status served_call(ct_state *s, const ct_state *src = nullptr) {
   if (!s->serving) CT_TRY(launch_server(s, s->srv_seq));
   const uint32_t req = ++s->srv_seq;
   std::atomic_thread_fence(std::memory_order_seq_cst);   // the pending status first
-  // the request: the removal's 32-bit halves, each tagged with the sequence number
+  // the request: the removal's 32-bit halves, the operation and the source
+  // state's address, each tagged with the sequence number
   const uint32_t *half = reinterpret_cast<const uint32_t *>(s->h_in);
   volatile unsigned long long *rq = reinterpret_cast<volatile unsigned long long *>(s->h_door);
-  const int nreq = std::max(2 * s->tb->Wd, 1);
-  for (int k = 0; k < nreq; ++k) rq[k] = ((unsigned long long)req << 32) | (k < 2 * s->tb->Wd ? half[k] : 0u);
+  const int w2 = 2 * s->tb->Wd;
+  const unsigned long long tg = (unsigned long long)req << 32;
+  const unsigned long long sa = src ? (unsigned long long)(uintptr_t)src->mem : 0ull;
+  for (int k = 0; k < w2; ++k) rq[k] = tg | (src ? 0u : half[k]);
+  rq[w2] = tg | (src ? 1u : 0u);
+  rq[w2 + 1] = tg | (uint32_t)sa;
+  rq[w2 + 2] = tg | (uint32_t)(sa >> 32);
   // the outputs come back as tagged 32-bit halves (no fence on the device):
   // the status word first, then every dom / pruned half of this request
   const int Wd = s->tb->Wd;
@@ -1203,6 +1211,7 @@ static ct_status served_call(ct_state *s) {
   auto done = [&]() -> bool {
     const unsigned long long w = to[4 * Wd];
     if ((uint32_t)(w >> 32) != req) return false;
+    if (src) return true;   // a restore answers with its tagged status only
     const int32_t status = (int32_t)(uint32_t)w;
     if (status == CT_OK) {
       for (int k = 0; k < 4 * Wd; ++k)
@@ -1451,6 +1460,15 @@ ct_status ct_state_copy(ct_state *dst, const ct_state *src) {
   if (!dst || !src) return fail(CT_EINVAL, "NULL argument");
   if (dst->tb != src->tb) return fail(CT_ESTATE, "states belong to different tables");
   if (dst == src) return CT_OK;
+  if (dst->serving && !src->pending) {
+    // a served state restores in place (its server copies src and keeps
+    // running); src's queued work first (a served src is idle between calls)
+    DeviceGuard g(dst->tb->device);
+    if (cudaStreamQuery(src->stream) != cudaSuccess) CUDA_TRY(cudaStreamSynchronize(src->stream));
+    CT_TRY(served_call(dst, src));
+    dst->pending = false;
+    return CT_OK;
+  }
   quiesce(dst);
   quiesce(src);
   if (src->pending) return fail(CT_ESTATE, "root of a caller-combined shard: combine its flags and apply first");
