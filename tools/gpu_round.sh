@@ -29,3 +29,18 @@ timeout 900 ncu $NCUF -k regex:k_bupdate -s 13 -c 5 -o $O/prof_bupdate_c4 python
 timeout 900 ncu $NCUF -k regex:k_fast -s 25 -c 2 -o $O/prof_fast_neg python bench.py --workload neg --steps 5 --warmup 3 > $O/ncu_full_neg.log 2>&1
 timeout 600 ncu $NCUL -c 300 --log-file $O/launches_neg.csv python bench.py --workload neg --steps 20 --warmup 3 > $O/ncu_launch_neg.log 2>&1
 grep -E "rror" $O/ncu_*.log | head
+# summaries on the box (the .ncu-rep files are large: gpurun brings back <= 64 MiB)
+P=$O/profiles; mkdir -p $P; cp profiles/ncu_traffic.json $P/ 2>/dev/null
+S="env CT_PROFILES_DIR=$P python tools/ncu_summarize.py --round 2"
+$S --launches $O/launches_c3.csv --full $O/prof_fast_c3.ncu-rep --kernel k_fast --workload c3bulk > /dev/null 2>&1
+$S --full $O/prof_fast_c3b.ncu-rep --kernel k_fast --workload c3b > /dev/null 2>&1
+$S --full $O/prof_fast_c3b_scan.ncu-rep --kernel k_fast --workload c3b_scan > /dev/null 2>&1
+$S --full $O/prof_fast_c3bulk6.ncu-rep --kernel k_fast --workload c3bulk6 > /dev/null 2>&1
+$S --full $O/prof_fast_c3b6.ncu-rep --kernel k_fast --workload c3b6 > /dev/null 2>&1
+$S --full $O/prof_fast_c3b6_scan.ncu-rep --kernel k_fast --workload c3b6_scan > /dev/null 2>&1
+$S --launches $O/launches_c4.csv --full $O/prof_bupdate_c4.ncu-rep --kernel k_bupdate --workload c4 > /dev/null 2>&1
+$S --launches $O/launches_neg.csv --full $O/prof_fast_neg.ncu-rep --kernel k_fast --workload negative > /dev/null 2>&1
+ls $P
+# keep the headline kernel's full capture only
+find $O -name "*.ncu-rep" ! -name "prof_fast_c3.ncu-rep" -delete
+du -sh $O

@@ -64,7 +64,8 @@ def main():
     ap.add_argument("--workload", default="c3bulk")
     ap.add_argument("--note", default="")
     a = ap.parse_args()
-    prof = os.path.join(ROOT, "profiles")
+    prof = os.environ.get("CT_PROFILES_DIR") or os.path.join(ROOT, "profiles")
+    os.makedirs(prof, exist_ok=True)
     os.makedirs(prof, exist_ok=True)
     tag = f"r{a.round:02d}_{a.workload}"
     md = [f"# ncu summary, round {a.round}, workload {a.workload}", ""]
