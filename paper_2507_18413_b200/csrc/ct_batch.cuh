@@ -779,10 +779,16 @@ constexpr int kBScanFirst = kBScanRounds * 32 * kScanUnroll;   // blocks scanned
 // Pass 0 with a HALF warp per miss (16 lanes x kScanUnroll entries = 64 index
 // entries per round, the two halves of a warp on two misses), the next miss's
 // list entry and index parameters loaded while the current one is scanned.
+#ifndef CT_BSCAN_QW
+#define CT_BSCAN_QW 8
+#endif
+constexpr int kBScanQW = CT_BSCAN_QW;   // lanes per miss in pass 0 (32 / kBScanQW misses per warp)
 __device__ void bscan_pass0(const TableDev &tb, const BatchDev &bd, int gw, int nw) {
-  const int lane = threadIdx.x & 31, hl = lane & 15, half = lane >> 4;
+  constexpr int QW = kBScanQW, GW = 32 / QW;
+  const int lane = threadIdx.x & 31, hl = lane % QW, grp = lane / QW;
   const int nm = __ldcg(bd.nmiss);
-  constexpr int kR = 16 * kScanUnroll;   // entries per round
+  constexpr int kR = QW * kScanUnroll;   // entries per round
+  constexpr unsigned kGM = QW == 32 ? 0xffffffffu : ((1u << QW) - 1u);
   auto fetch = [&](int m, int2 &e, int2 &inf) {
     e = make_int2(0, 0);
     inf = make_int2(0, 0);
@@ -792,10 +798,10 @@ __device__ void bscan_pass0(const TableDev &tb, const BatchDev &bd, int gw, int 
     }
   };
   int2 e, inf, e_n, inf_n;
-  int m = 2 * gw + half;
+  int m = GW * gw + grp;
   fetch(m, e, inf);
-  for (int mb = 2 * gw; mb < nm; mb += 2 * nw, m += 2 * nw) {
-    fetch(m + 2 * nw, e_n, inf_n);
+  for (int mb = GW * gw; mb < nm; mb += GW * nw, m += GW * nw) {
+    fetch(m + GW * nw, e_n, inf_n);
     const bool valid = m < nm;
     const int s = e.x, row = e.y;
     const int L = valid ? (tb.use_index ? inf.y : tb.W2) : 0;
@@ -811,7 +817,7 @@ __device__ void bscan_pass0(const TableDev &tb, const BatchDev &bd, int gw, int 
       bool in[kScanUnroll];
 #pragma unroll
       for (int q = 0; q < kScanUnroll; ++q) {
-        const int k = k0 + q * 16 + hl;
+        const int k = k0 + q * QW + hl;
         in[q] = active && k < Lf;
         pid[q] = in[q] ? (idx ? __ldcg(idx + k) : k) : 0;
       }
@@ -825,8 +831,8 @@ __device__ void bscan_pass0(const TableDev &tb, const BatchDev &bd, int gw, int 
 #pragma unroll
       for (int q = kScanUnroll - 1; q >= 0; --q) {
         const unsigned b = __ballot_sync(0xffffffffu, ((t[q].x & v[q].x) | (t[q].y & v[q].y)) != 0);
-        const unsigned hb = (b >> (16 * half)) & 0xffffu;
-        const int src = hb ? (16 * half + __ffs(hb) - 1) : lane;
+        const unsigned hb = (b >> (QW * grp)) & kGM;
+        const int src = hb ? (QW * grp + __ffs(hb) - 1) : lane;
         const int p = __shfl_sync(0xffffffffu, pid[q], src);
         if (hb && active) hit = p;
       }
