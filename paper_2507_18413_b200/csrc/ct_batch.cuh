@@ -16,16 +16,20 @@
 //              global load.  Alg. 2 per block as in
 //              update_tile: the per-variable OR of the listed rows, complemented
 //              for the Δ-branch, ANDed over the changed variables, the block
-//              dies early (L175) once nothing valid is left in it.
-//              Batch states are DENSE: the update visits every block of the
-//              state (a zero block costs one 16-byte read and no support load),
-//              so there is no per-state index to compact; after the call the
-//              state's index is the identity over its W2 blocks.
+//              dies early (L175) once nothing valid is left in it.  It visits
+//              every block of the DENSE states (a zero block costs one 16-byte
+//              read and no support load); a (state, tile) with few valid
+//              tuples checks them against the new domains instead (the cell
+//              route, tile32_cells).  The survivor bits go to a per-state
+//              bitmap and k_bcompact builds the order-preserving index.
+//   k_bsparse  (a3-a5) states whose input index is short are updated through
+//              it, one CTA per state, their valid tuples checked against the
+//              new domains, and compacted in the same pass.
 //   k_bprobe   (a6a) one THREAD per (state, filter item): residue probe
 //              (PAPER.md L220): T[res] & S[x,a][res] != 0 settles the value,
 //              else the next few blocks; a miss goes to a global miss list.
-//   k_bscan    (a6b) a warp per miss over the first blocks, then (miss, chunk)
-//              units over the rest for the misses still open.
+//   k_bscan    (a6b) a quarter warp per miss over the first index entries,
+//              then (miss, chunk) units over the rest for the misses still open.
 //   k_bingest / k_bfinalize: dev_ingest / dev_finalize (ct_kernels.cuh) with
 //              128-thread CTAs, one per state.
 #pragma once
