@@ -586,8 +586,13 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
   int32_t *s_ust = s_cs + n;
   int32_t *s_rb = s_ust + n + 1;
   int32_t *s_do = s_rb + n + 1;
+  constexpr int kRowWarps = 4;   // warps of the per-row pass
+  __shared__ int s_wi[4];        // warp 0's verdicts: dead, fail, noop, groups
+  __shared__ int s_wc[2 * kRowWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int rv0 = 0;   // this thread's row of the first round: its variable, requested at once
+  if (warp < kRowWarps && warp * 32 + lane < R) rv0 = tb.rowVar[warp * 32 + lane];
   if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
     uint64_t dm0 = 0, rm0 = 0;
     int wv0 = 0;
     if (lane < Wd) {
@@ -596,12 +601,6 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
       rm0 = gdom ? ~__ldcg(gdom + tb.gword[lane]) : (rem ? rem[lane] : 0ull);
       wv0 = tb.wordVar[lane];
     }
-    // the row pass's variables, kRowAhead rounds of 32 rows ahead, requested
-    // now with everything else (a latency chain per round otherwise)
-    constexpr int kRowAhead = 4;
-    int rvq[kRowAhead];
-#pragma unroll
-    for (int q = 0; q < kRowAhead; ++q) rvq[q] = q * 32 + lane < R ? tb.rowVar[q * 32 + lane] : 0;
     const int dead = __shfl_sync(0xffffffffu, lane == 0 ? c->dead : 0, 0);
     SERVE_TRACE(2);
     for (int i = lane; i <= n; i += 32) {
@@ -667,74 +666,98 @@ __device__ void warp_ingest(const TableDev &tb, const StateDev &st, const uint64
       fail = __reduce_or_sync(0xffffffffu, fail);
       __syncwarp();
       const bool noop = ngroups == 0 && !root_mode;
-      int nrows = 0, nitems = 0;
-      if (!(fail || noop)) {
-        // per support row: update list (grouped by var, group end marked) and
-        // filter items (Alg. 1 L3: s_sup), both in row order
-        int ucarry = 0, icarry = 0;
-        for (int base = 0; base < R; base += 32) {
-          const int r = base + lane;
-          bool u = false, f = false, useDelta = false;
-          int x = rvq[0];
-#pragma unroll
-          for (int q = 0; q + 1 < kRowAhead; ++q) rvq[q] = rvq[q + 1];
-          const int ra = r + 32 * kRowAhead;
-          rvq[kRowAhead - 1] = ra < R ? tb.rowVar[ra] : 0;
-          if (r < R) {
-            const int a = r - s_rb[x];
-            const int w = s_do[x] + (a >> 6), b = a & 63;
-            const int cd = s_cd[x], cs = s_cs[x];
-            useDelta = use_delta(tb, x, cd, cs);
-            const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
-            u = cd > 0 && (useDelta ? inDl : inD);
-            f = cs > 1 && inD;
-          }
-          const unsigned bu = __ballot_sync(0xffffffffu, u), bf = __ballot_sync(0xffffffffu, f);
-          if (u) {
-            const int up = ucarry + __popc(bu & lanemask_lt());
-            uint32_t e = (uint32_t)r | (useDelta ? kInvBit : 0u);
-            if (up == s_ust[x + 1] - 1) e |= kEndBit;
-            if (sh) sh->ulist[up] = (int32_t)e;
-            else st.ulist[up] = (int32_t)e;
-          }
-          if (f) {
-            if (sh) sh->items[icarry + __popc(bf & lanemask_lt())] = r;
-            else st.items[icarry + __popc(bf & lanemask_lt())] = r;
-          }
-          ucarry += __popc(bu);
-          icarry += __popc(bf);
-        }
-        nrows = ucarry;
-        nitems = icarry;
-      }
-      SERVE_TRACE(4);
       if (lane == 0) {
-        const int L0 = c->L;
-        if (sh) {
-          sh->skip = 0;
-          sh->noop = noop && !fail;
-          sh->fail = fail;
-          sh->nrows = nrows;
-          sh->nitems = nitems;
-          sh->L = L0;
-          sh->ident = c->identity;
-          sh->par = c->parity;
-        }
-        c->skip = 0;
-        c->noop = noop && !fail;
-        c->fail_fast = fail;
-        c->ngroups = ngroups;
-        c->nrows = nrows;
-        c->nitems = nitems;
-        c->L_in = L0;
-        c->L_out = 0;
-        c->tile_ctr = 0;
-        c->nscan = 0;
-        c->upd_loads = 0;
-        c->upd_writes = 0;
-        c->scan_loads = 0;
+        s_wi[1] = fail;
+        s_wi[2] = noop;
+        s_wi[3] = ngroups;
       }
     }
+    if (lane == 0) s_wi[0] = dead;
+  }
+  SERVE_TRACE(4);
+  __syncthreads();
+  // per support row: update list (grouped by var, group end marked) and filter
+  // items (Alg. 1 L3: s_sup), both in row order -- kRowWarps warps, 32 x
+  // kRowWarps rows per round, the warps' offsets from their ballot counts
+  const int dead = s_wi[0], fail = s_wi[1], noop = s_wi[2];
+  int nrows = 0, nitems = 0;
+  if (!dead && !(fail || noop)) {
+    int ucarry = 0, icarry = 0;
+    for (int base = 0; base < R; base += 32 * kRowWarps) {   // uniform over the block (barriers inside)
+      const int r = base + warp * 32 + lane;
+      bool u = false, f = false, useDelta = false;
+      int x = 0;
+      if (warp < kRowWarps && r < R) {
+        x = base == 0 ? rv0 : tb.rowVar[r];
+        const int a = r - s_rb[x];
+        const int w = s_do[x] + (a >> 6), b = a & 63;
+        const int cd = s_cd[x], cs = s_cs[x];
+        useDelta = use_delta(tb, x, cd, cs);
+        const bool inD = (s_din[w] >> b) & 1, inDl = (s_dl[w] >> b) & 1;
+        u = cd > 0 && (useDelta ? inDl : inD);
+        f = cs > 1 && inD;
+      }
+      const unsigned bu = __ballot_sync(0xffffffffu, u), bf = __ballot_sync(0xffffffffu, f);
+      if (lane == 0 && warp < kRowWarps) {
+        s_wc[warp] = __popc(bu);
+        s_wc[kRowWarps + warp] = __popc(bf);
+      }
+      __syncthreads();
+      int uo = ucarry, io = icarry, ut = 0, it = 0;
+#pragma unroll
+      for (int q = 0; q < kRowWarps; ++q) {
+        if (q < warp) {
+          uo += s_wc[q];
+          io += s_wc[kRowWarps + q];
+        }
+        ut += s_wc[q];
+        it += s_wc[kRowWarps + q];
+      }
+      if (u) {
+        const int up = uo + __popc(bu & lanemask_lt());
+        uint32_t e = (uint32_t)r | (useDelta ? kInvBit : 0u);
+        if (up == s_ust[x + 1] - 1) e |= kEndBit;
+        if (sh) sh->ulist[up] = (int32_t)e;
+        else st.ulist[up] = (int32_t)e;
+      }
+      if (f) {
+        const int ip = io + __popc(bf & lanemask_lt());
+        if (sh) sh->items[ip] = r;
+        else st.items[ip] = r;
+      }
+      ucarry += ut;
+      icarry += it;
+      __syncthreads();   // s_wc is rewritten next round
+    }
+    nrows = ucarry;
+    nitems = icarry;
+  }
+  if (threadIdx.x == 0 && !dead) {
+    const int ngroups = s_wi[3];
+    const int L0 = c->L;
+    if (sh) {
+      sh->skip = 0;
+      sh->noop = noop && !fail;
+      sh->fail = fail;
+      sh->nrows = nrows;
+      sh->nitems = nitems;
+      sh->L = L0;
+      sh->ident = c->identity;
+      sh->par = c->parity;
+    }
+    c->skip = 0;
+    c->noop = noop && !fail;
+    c->fail_fast = fail;
+    c->ngroups = ngroups;
+    c->nrows = nrows;
+    c->nitems = nitems;
+    c->L_in = L0;
+    c->L_out = 0;
+    c->tile_ctr = 0;
+    c->nscan = 0;
+    c->upd_loads = 0;
+    c->upd_writes = 0;
+    c->scan_loads = 0;
   }
   SERVE_TRACE(5);
   __syncthreads();
