@@ -471,8 +471,8 @@ ct_status ct_debug_serve_trace(const ct_state *s, int64_t *out16);
  * on one stream): the calls are matched by a per-table epoch counter.  With
  * n_shards = 1 the table exchanges with itself (tests the protocol on one GPU).
  * Errors: CT_EINVAL (NULL, wrong count, not exported, already attached,
- * launch shape), CT_ENOMEM, CT_ECUDA (IPC).  A rank that never arrives makes
- * the others' kernels trap after ct_debug_spin_limit (CT_ECUDA). */
+ * launch shape), CT_ENOMEM, CT_ECUDA (IPC).  A rank that does not arrive
+ * within 120 s makes the others' kernels trap (CT_ECUDA). */
 #define CT_PEER_HANDLE_BYTES 64
 ct_status ct_peer_export(ct_table *t, void *out_handle);
 ct_status ct_peer_attach(ct_table *t, int32_t n_shards, const void *handles);

@@ -843,8 +843,16 @@ __device__ int peer_combine(const TableDev &tb, const StateDev &st) {
     // thread's system-scope release (cumulative), which publishes them
     st_release_sys_u32(tb.peers[tid] + fbase + ((size_t)slot * G + me) * 32, ep);
     const uint32_t *f = tb.inbox + fbase + ((size_t)slot * G + tid) * 32;   // sender tid's flag here
-    SpinGuard sg;
-    while (ld_acquire_sys_u32(f) != ep) spin_check(sg, 5, ep, (unsigned long long)tid, 0);
+    // the other ranks may reach this call a while later (their host work
+    // between calls): a much longer limit than the grid barriers' watchdog
+    const unsigned long long t0 = globaltimer();
+    uint32_t n = 0;
+    while (ld_acquire_sys_u32(f) != ep) {
+      if ((++n & 1023u) == 0 && globaltimer() - t0 > 120000000000ull) {   // 120 s
+        spin_report(5, ep, (unsigned long long)tid, 0);
+        __trap();
+      }
+    }
   }
   __syncthreads();
   uint32_t *out = reinterpret_cast<uint32_t *>(st.sup);
