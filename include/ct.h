@@ -241,10 +241,15 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom,
 
 /* Asynchronous, device-accessible buffers, enqueued on the state's stream; the
  * call does not wait.  The buffers may be device memory or pinned host memory
- * (cudaHostAlloc / cudaMallocHost).  A host `removed` is copied into the
- * state's device slot by one stream-ordered DMA (pageable memory is accepted
- * but the copy then blocks); host outputs are written in place by the kernel
- * (zero-copy).  So a caller can keep many host-buffer calls in flight.
+ * (cudaHostAlloc / cudaMallocHost).  A host `removed` is read at enqueue and
+ * passed with the launch on the k_fast shape (ct_table_info.kernel_path 2,
+ * Wd <= 16); otherwise it is DMA'd into one of the state's two device slots on
+ * the state's copy stream, overlapping the previous call (pageable memory is
+ * accepted but the copy then blocks).  On the k_fast shape the host buffer
+ * may be reused as soon as the call returns; otherwise only after the call
+ * has run (the DMA is asynchronous).  Host outputs are written in place
+ * by the kernel (zero-copy).  So a caller can keep many host-buffer calls in
+ * flight.
  *   removed     device uint64[Wd] (NULL = nothing removed)
  *   out_dom     device uint64[Wd] or NULL
  *   out_pruned  device uint64[Wd] or NULL

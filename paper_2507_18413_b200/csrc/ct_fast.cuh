@@ -1443,13 +1443,23 @@ finalize:
 
 // grid = co-resident CTAs (cooperative launch), kFastTPB threads, dynamic smem
 // fast_smem_bytes(n, Wd, R).
+// A small removal bitmap passed by value with the launch (async calls whose
+// removal sits in host memory): no copy node, no cross-stream event.
+constexpr int kRemArgWords = 16;
+struct RemArg {
+  uint64_t w[kRemArgWords];
+  int32_t n;   // words in use; 0: take `removed`
+};
+
 __global__ void __launch_bounds__(kFastTPB, CT_FAST_MINB) k_fast(TableDev tb, const StateDev *__restrict__ states,
                                                    const uint64_t *__restrict__ removed, int root_mode,
                                                    int with_finalize, uint64_t *__restrict__ out_dom,
                                                    uint64_t *__restrict__ out_pruned,
                                                    int32_t *__restrict__ out_status, int use_state_out,
-                                                   const StateDev *__restrict__ src_state) {
+                                                   const StateDev *__restrict__ src_state,
+                                                   const __grid_constant__ RemArg ra) {
   extern __shared__ __align__(16) uint64_t smem[];
+  if (ra.n) removed = ra.w;
   __shared__ FastSh fs;
   __shared__ StateDev s_st, s_src;   // the states' pointers live in shared memory, not in registers
   if (threadIdx.x == 0) {

@@ -409,7 +409,7 @@ static ct_status enqueue_neg(ct_table *tb, ct_state *s, const uint64_t *removed,
 // reads src and writes s directly; every other launch shape copies first.
 static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *removed, int root_mode,
                                 uint64_t *out_dom, uint64_t *out_pruned, int32_t *out_status, int use_state_out,
-                                bool local_only, const ct_state *src = nullptr) {
+                                bool local_only, const ct_state *src = nullptr, const RemArg *ra = nullptr) {
   cudaStream_t st = s->stream;
   if (src && !(tb->use_fast && !tb->use_wide && !tb->use_small)) {
     CT_TRY(launch_state_copy(tb, s->mem, src->mem, st));
@@ -462,9 +462,12 @@ static ct_status enqueue_single(ct_table *tb, ct_state *s, const uint64_t *remov
     lc.attrs = attr;
     lc.numAttrs = 1;
     const int e = prof_event(tb, st);
+    RemArg rarg;
+    rarg.n = 0;
+    if (ra) rarg = *ra;
     CUDA_TRY(cudaLaunchKernelEx(&lc, k_fast, tb->dev, (const StateDev *)s->d_desc, removed, root_mode, fin_inside,
                                 out_dom, out_pruned, out_status, use_state_out,
-                                src ? (const StateDev *)src->d_desc : (const StateDev *)nullptr));
+                                src ? (const StateDev *)src->d_desc : (const StateDev *)nullptr, rarg));
     prof_mark(tb, 6, e, st);
     if (fin_inside || local_only) return CT_OK;
   } else if (tb->use_fused) {
@@ -1343,9 +1346,10 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
 // the state's stream waits for the copy -- so the copy for call i + 1 runs
 // while call i propagates (one copy stream per state, two slots).  Returns the
 // device slot; *slot_b = the slot to mark free after the call (-1: none).
-static ct_status stage_removed(ct_state *s, const uint64_t *&removed, int &slot_b) {
+static ct_status stage_removed(ct_state *s, const uint64_t *&removed, int &slot_b, RemArg *ra = nullptr) {
   ct_table *tb = s->tb;
   slot_b = -1;
+  if (ra) ra->n = 0;
   if (!removed || !tb->Wd) return CT_OK;
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, removed) != cudaSuccess) {
@@ -1353,6 +1357,14 @@ static ct_status stage_removed(ct_state *s, const uint64_t *&removed, int &slot_
     a.type = cudaMemoryTypeUnregistered;
   }
   if (a.type != cudaMemoryTypeUnregistered && a.type != cudaMemoryTypeHost) return CT_OK;   // device memory
+  // k_fast: a small removal travels by value with the launch (read here, at enqueue)
+  if (ra && tb->use_fast && !tb->use_small && !tb->use_wide && tb->Wd <= kRemArgWords &&
+      tb->kind != CT_TABLE_NEGATIVE) {
+    memcpy(ra->w, removed, (size_t)tb->Wd * 8);
+    ra->n = tb->Wd;
+    removed = nullptr;
+    return CT_OK;
+  }
   if (!s->cp_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(&s->cp_stream, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
@@ -1385,8 +1397,9 @@ ct_status ct_propagate_async(ct_state *s, const uint64_t *removed, uint64_t *out
   // host link (pinned removals read in place by every CTA: C3 bulk e2e 8.7k
   // vs 9.8k with a DMA)
   int slot_b;
-  CT_TRY(stage_removed(s, removed, slot_b));
-  CT_TRY(enqueue_single(tb, s, removed, 0, out_dom, out_pruned, out_status, 0, false));
+  RemArg ra;
+  CT_TRY(stage_removed(s, removed, slot_b, &ra));
+  CT_TRY(enqueue_single(tb, s, removed, 0, out_dom, out_pruned, out_status, 0, false, nullptr, ra.n ? &ra : nullptr));
   if (slot_b >= 0) CUDA_TRY(cudaEventRecord(s->slot_free[slot_b], s->stream));
   return CT_OK;
 }
@@ -1405,8 +1418,9 @@ ct_status ct_propagate_from_async(ct_state *dst, const ct_state *src, const uint
   DeviceGuard g(tb->device);
   CT_TRY(order_after(dst->stream, src->stream));   // src's earlier work first
   int slot_b;
-  CT_TRY(stage_removed(dst, removed, slot_b));
-  CT_TRY(enqueue_single(tb, dst, removed, 0, out_dom, out_pruned, out_status, 0, false, src));
+  RemArg ra;
+  CT_TRY(stage_removed(dst, removed, slot_b, &ra));
+  CT_TRY(enqueue_single(tb, dst, removed, 0, out_dom, out_pruned, out_status, 0, false, src, ra.n ? &ra : nullptr));
   if (slot_b >= 0) CUDA_TRY(cudaEventRecord(dst->slot_free[slot_b], dst->stream));
   return order_after(const_cast<ct_state *>(src)->stream, dst->stream);   // src's next writes wait for the call
 }
