@@ -1341,11 +1341,14 @@ ct_status ct_propagate(ct_state *s, const uint64_t *removed, uint64_t *out_dom, 
   return (ct_status)status;
 }
 
-// A host-memory removal for an async call on s: DMA'd into slot (cp_i & 1) on
+// A host-memory removal for an async call on s.  On the k_fast shape (and
+// ra != nullptr) it is read now into *ra and travels with the launch by value
+// (removed becomes nullptr).  Otherwise it is DMA'd into slot (cp_i & 1) on
 // the state's copy stream once the call that last read that slot is done, and
 // the state's stream waits for the copy -- so the copy for call i + 1 runs
-// while call i propagates (one copy stream per state, two slots).  Returns the
-// device slot; *slot_b = the slot to mark free after the call (-1: none).
+// while call i propagates (one copy stream per state, two slots); removed
+// becomes the device slot and slot_b the slot to mark free after the call
+// (-1: none).
 static ct_status stage_removed(ct_state *s, const uint64_t *&removed, int &slot_b, RemArg *ra = nullptr) {
   ct_table *tb = s->tb;
   slot_b = -1;
