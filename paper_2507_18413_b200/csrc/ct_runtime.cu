@@ -1541,7 +1541,8 @@ ct_status ct_peer_export(ct_table *tb, void *out_handle) {
       tb->peer_inbox = nullptr;
       return fail(CT_ENOMEM, "peer inbox allocation of %zu bytes failed", tb->peer_bytes);
     }
-    CUDA_TRY(cudaMemset(tb->peer_inbox, 0, tb->peer_bytes));
+    CUDA_TRY(cudaMemsetAsync(tb->peer_inbox, 0, tb->peer_bytes, tb->stream));   // on the table's (non-blocking) stream
+    CUDA_TRY(cudaStreamSynchronize(tb->stream));   // zeroed before a peer attaches
   }
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, tb->peer_inbox));
@@ -1857,7 +1858,10 @@ ct_status ct_batch_work(ct_batch *b, int64_t *out10, int32_t reset) {
   out8[7] = w7[5];
   out8[8] = w7[6];
   out8[9] = 0;
-  if (reset) CUDA_TRY(cudaMemset(b->bd.work, 0, 7 * sizeof(int64_t)));
+  if (reset) {   // ordered before the next batch call's kernels on the table's stream
+    CUDA_TRY(cudaMemsetAsync(b->bd.work, 0, 7 * sizeof(int64_t), b->tb->stream));
+    CUDA_TRY(cudaStreamSynchronize(b->tb->stream));
+  }
   // filter side of the last call: summed over the states' own counters
   std::vector<Ctl> c((size_t)b->S);
   CUDA_TRY(cudaMemcpy2D(c.data(), sizeof(Ctl), b->mem + b->tb->lay.ctl, b->tb->lay.total, sizeof(Ctl), (size_t)b->S,
@@ -2166,7 +2170,11 @@ ct_status ct_model_create(int32_t n_vars, const int32_t *var_lo, const int32_t *
   m->meta_bytes = (size_t)round_up((int64_t)(tdev + sdev), 256) + 256 + 2 * round_up((int64_t)gw_total * 4, 256) +
                   (size_t)kBarWords * 4;
   if (cudaMalloc(&m->meta, m->meta_bytes) != cudaSuccess) return bail(fail(CT_ENOMEM, "model metadata allocation failed"));
-  cudaMemset(m->meta, 0, m->meta_bytes);
+  if (cudaMemsetAsync(m->meta, 0, m->meta_bytes, m->stream) != cudaSuccess)
+    return bail(fail(CT_ECUDA, "model metadata memset failed"));
+  // the pool and metadata memsets (m->stream, non-blocking) finish before the
+  // synchronous uploads below write into them
+  if (cudaStreamSynchronize(m->stream) != cudaSuccess) return bail(fail(CT_ECUDA, "model stream sync failed"));
   TableDev *d_tabs = (TableDev *)m->meta;
   StateDev *d_sts = (StateDev *)(m->meta + tdev);
   ModelCtl *d_mc = (ModelCtl *)(m->meta + round_up((int64_t)(tdev + sdev), 256));
