@@ -23,6 +23,12 @@
 #include "ct_wide.cuh"
 #include "ct_neg.cuh"
 
+// Support-row pitch padding in 64-bit words (a multiple of 16; experiment builds
+// only, tools/gpu_pitch.sh: does the row pitch alias HBM channels in the scans?)
+#ifndef CT_SUP_PITCH_PAD
+#define CT_SUP_PITCH_PAD 0
+#endif
+
 using namespace ctk;
 
 constexpr int32_t kPendingStatus = 0x7FFFFFFF;   // mapped status word before the kernel writes it
@@ -828,7 +834,7 @@ static ct_status create_impl(int32_t kind, int32_t n, const int32_t *scope, cons
   tb->Wtot = (n_tuples + 63) / 64;
   CT_TRY(ct_shard_range(n_tuples, tb->n_shards, tb->rank, &tb->wbeg, &tb->W));
   if (tb->W > INT32_MAX - 1024) return fail(CT_EINVAL, "table shard too large (%lld words)", (long long)tb->W);
-  tb->Wp = round_up(std::max<int64_t>(tb->W, 1), 16);
+  tb->Wp = round_up(std::max<int64_t>(tb->W, 1), 16) + CT_SUP_PITCH_PAD;
   const int64_t j0 = std::min(tb->wbeg * 64, n_tuples), j1 = std::min((tb->wbeg + tb->W) * 64, n_tuples);
   tb->t_local = j1 - j0;
   tb->full_dom.assign(tb->Wd, 0ull);
