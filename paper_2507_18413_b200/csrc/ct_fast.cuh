@@ -49,7 +49,7 @@ constexpr int kLocalRowsMax = 4096;                    // R limit of the per-CTA
 #define CT_FAST_TPB 256
 #endif
 #ifndef CT_FAST_UNROLL
-#define CT_FAST_UNROLL 16
+#define CT_FAST_UNROLL 12   // support rows in flight per lane (sweep 8/12/16/24: profiles/r02_fast_unroll.md)
 #endif
 #ifndef CT_FAST_MINB
 #define CT_FAST_MINB 3
